@@ -1,0 +1,209 @@
+/*
+ * mspq_capi.h — the C-ABI of the B200-native MoE-SpeQ decode path (libmspq.so).
+ *
+ * Two layers, both plain C (no torch / C++ types; device pointers are void*, streams are
+ * cudaStream_t passed as void*; every call returns an int status and never throws):
+ *
+ *  (1) Kernel entry points the host engine calls through (SURVEY.md §8b "C-ABI"):
+ *        mspq_gate_topk        K1  fused residual-combine + RMSNorm + bf16 router + top-k/softmax
+ *                                  (replaces the reference's trace-supplied routing:
+ *                                   TokenRecord.target_sets/draft_sets/draft_gates, trace.hpp:43-49,
+ *                                   and build_elb's input, scheduler.cpp:41-63)
+ *        mspq_build_schedule       expert-grouped entry schedule == reorder_verification
+ *                                  (scheduler.cpp:339-357)
+ *        mspq_moe_int4         K2  INT4 (GPTQ-sym g128) grouped expert FFN for the draft
+ *        mspq_moe_bf16         K3  bf16 grouped expert FFN for the verify (reads the HBM slot pool)
+ *        mspq_lm_head / mspq_argmax  logits + greedy token
+ *        mspq_accept_scan      K5  accept rule (sim.cpp:352-365) on token ids
+ *      plus weight generation / quantisation helpers used by tests.
+ *
+ *  (2) The engine: the drop-in for the reference's run_simulation (sim.hpp:86) entry point.
+ *        mspq_replay           device control plane (K4) over a reference Trace, returning the
+ *                              reference's SimReport JSON (sim.cpp:468-510) -- bit-exact.
+ *        mspq_engine_create / mspq_engine_configure / mspq_generate
+ *                              live speculative decode: INT4 draft -> ELB -> 3-phase prefetch over
+ *                              PCIe copy engines into a capped HBM slot pool -> bf16 grouped
+ *                              verify -> accept -> Amortization-Roofline governor; returns the
+ *                              same SimReport JSON with measured times + per-cycle traces.
+ *
+ * Status codes: 0 = OK; 1..18 = moespeq::ErrorCode ordinal + 1 (errors.hpp:8-27, same order);
+ * 1000 = CUDA error; 1001 = capacity/overflow in the device controller; 2000 = internal.
+ */
+#ifndef MSPQ_CAPI_H
+#define MSPQ_CAPI_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MSPQ_OK 0
+#define MSPQ_ERR_MALFORMED_RECORD 1
+#define MSPQ_ERR_SHAPE_VIOLATION 2
+#define MSPQ_ERR_EMPTY_TRACE 3
+#define MSPQ_ERR_INVALID_FIDELITY 4
+#define MSPQ_ERR_DEGENERATE_SHAPE 5
+#define MSPQ_ERR_LAYER_OUT_OF_RANGE 6
+#define MSPQ_ERR_SHAPE_MISMATCH 7
+#define MSPQ_ERR_RANGE_OUT_OF_BOUNDS 8
+#define MSPQ_ERR_EMPTY_CACHE 9
+#define MSPQ_ERR_UNKNOWN_POLICY 10
+#define MSPQ_ERR_EMPTY_REQUIRED 11
+#define MSPQ_ERR_INCOMPLETE_ROUTING 12
+#define MSPQ_ERR_K_OUT_OF_RANGE 13
+#define MSPQ_ERR_INSUFFICIENT_SAMPLES 14
+#define MSPQ_ERR_EMPTY_RANGE 15
+#define MSPQ_ERR_INFEASIBLE_BUDGET 16
+#define MSPQ_ERR_INVALID_CONFIG 17
+#define MSPQ_ERR_IO 18
+#define MSPQ_ERR_CUDA 1000
+#define MSPQ_ERR_OVERFLOW 1001
+#define MSPQ_ERR_INTERNAL 2000
+
+/* Model / draft config (the reference's ModelShape, trace.hpp:29-37, plus the dimensions a
+ * real model needs).  Scales are the fp32 values the weight generator multiplies by. */
+typedef struct mspq_model_desc {
+  int L, E, K;      /* MoE layers, experts per layer, top-k */
+  int d, f, V, P;   /* hidden, expert ffn, vocab, positional rows */
+  unsigned long long seed;
+  float embed_scale, pos_scale, a_router, a_up, a_down, a_lm, eps;
+  int unique_experts; /* 0 = every (layer, expert) distinct; else payload = key % unique */
+} mspq_model_desc;
+
+typedef struct mspq_engine_opts {
+  int device;
+  int kmax;                     /* longest speculation window the buffers are sized for */
+  const char* host_store_path;  /* NULL/"" = private cudaHostAlloc; else /dev/shm file shared
+                                   by all ranks (rank with host_store_role 0 creates + fills) */
+  int host_store_role;
+  int slot_extra;               /* extra HBM buffers beyond the cache budget (0 = auto) */
+  int log_cap;                  /* per-cycle event log capacity (0 = auto) */
+  int trace_level;              /* 0 = counts only, 1 = per-cycle tokens/routing, 2 = + event log */
+} mspq_engine_opts;
+
+typedef struct mspq_engine mspq_engine;
+
+const char* mspq_status_string(int status);
+const char* mspq_last_error(void);
+void mspq_free(void* p);
+int mspq_version(void);
+
+/* ---------------------------------------------------------------- (1) kernel entry points */
+int mspq_fill_bf16(unsigned long long seed, unsigned long long tensor, float scale, int kind,
+                   void* out_bf16, long long n, long long start, void* stream);
+int mspq_fill_expert(unsigned long long seed, int layer, int expert, int d, int f, float a_up,
+                     float a_down, void* blob_bf16, void* stream);
+int mspq_quantize_int4(const void* w_bf16, int rows, int cols, void* q_u32, void* s_bf16,
+                       void* stream);
+int mspq_embed(const void* embed, const void* pos, const int32_t* tokens,
+               const int32_t* positions, int T, int d, float* h, void* stream);
+/* K1.  y/entry_of/prev_wts may be NULL (no combine); router NULL = norm only;
+ * elb_ids/elb_gates/elb_row NULL = no ELB write. */
+int mspq_gate_topk(float* h, const float* y, const int32_t* entry_of, const float* prev_wts,
+                   const void* gamma, const void* router, void* xn, int32_t* ids, float* wts,
+                   float* logits, int32_t* elb_ids, float* elb_gates, const int32_t* elb_row,
+                   int layer, int L, int T, int d, int E, int K, float eps, void* stream);
+/* schedule arrays: n_groups[1], group_expert[G], group_buf[G], group_off[G+1], entry_tok[T*K],
+ * entry_of[T*K] */
+int mspq_build_schedule(const int32_t* ids, int T, int K, int E, int32_t* n_groups,
+                        int32_t* group_expert, int32_t* group_buf, int32_t* group_off,
+                        int32_t* entry_tok, int32_t* entry_of, void* stream);
+/* K2: blobs = all L*E INT4 expert blobs, blob_bytes apart, indexed by layer*E + expert */
+int mspq_moe_int4(const int32_t* n_groups, const int32_t* group_expert, const int32_t* group_buf,
+                  const int32_t* group_off, const int32_t* entry_tok, const void* xn, void* act,
+                  float* y, const void* blobs, long long blob_bytes, int layer, int E, int d,
+                  int f, int max_groups, void* stream);
+/* K3: pool = HBM slot pool, group_buf[g] = buffer index of group g's expert */
+int mspq_moe_bf16(const int32_t* n_groups, const int32_t* group_expert, const int32_t* group_buf,
+                  const int32_t* group_off, const int32_t* entry_tok, const void* xn, void* act,
+                  float* y, const void* pool, long long blob_bytes, int E, int d, int f,
+                  int max_groups, void* stream);
+int mspq_lm_head(const void* xn, const void* lm, int T, int V, int d, float* logits,
+                 void* stream);
+int mspq_argmax(const float* logits, int T, int V, int32_t* out, void* stream);
+/* K5: res[0] = accepted, res[1] = bonus token */
+int mspq_accept_scan(const int32_t* draft, const int32_t* target_argmax, int k, int32_t* res,
+                     void* stream);
+/* draft-loop variants that keep the decode state on the device (graph-replayable):
+ * argmax_advance: draft_toks[*row] = tok; *cur_tok = tok; *cur_pos += 1; *row += 1.
+ * accept_advance: K5 + next head: *cur_tok = bonus, *cur_pos = head_pos + accepted + 1. */
+int mspq_argmax_advance(const float* logits, int V, int32_t* out, int32_t* row,
+                        int32_t* draft_toks, int32_t* cur_tok, int32_t* cur_pos, void* stream);
+int mspq_accept_advance(const int32_t* draft, const int32_t* target_argmax, int k, int32_t* res,
+                        int32_t* cur_tok, int32_t* cur_pos, int head_pos, void* stream);
+long long mspq_int4_blob_bytes(int d, int f);
+long long mspq_bf16_blob_bytes(int d, int f);
+
+
+/* ---------------------------------------------------------------- K4 expert-cache controller
+ * Device-resident cache table (key -> HBM buffer, LRU stamps, per-layer sizes), ELB, planner
+ * state and copy-request queue; all decisions are made by kernels (one warp per launch).
+ * Restates CacheState / plan_prefetch / select_victim_lookahead / policy_step
+ * (scheduler.cpp:76-312) and the cycle's insertion rules (sim.cpp:152-295). */
+typedef struct mspq_cache mspq_cache;
+typedef struct mspq_cache_view {  /* device pointers owned by the cache */
+  int32_t* elb_ids;   /* [kmax][L][K] */
+  float* elb_gates;   /* [kmax][L][K] */
+  int32_t* scal;      /* scalar slots (see ctl.h CtlScalar) */
+  int32_t* req;       /* device alias of host_req */
+  int32_t* log;       /* [log_cap][6] (kind, tag, key, hit, victim, buffer) */
+  int32_t* plan;      /* [plan_cap][3] (row, key, phase) */
+  int32_t* cov;       /* [L][2] */
+  int32_t* step;      /* [L][kmax+1][2] */
+  int32_t* res;       /* [L*E] key -> buffer */
+  int32_t* host_stat; /* HOST pointer: mapped mirror of scal, valid after the launch completes */
+  int32_t* host_req;  /* HOST pointer: mapped copy requests of the last launch */
+  int32_t* host_sched;/* HOST pointer: [0] n_groups, [1..] group_buf of the last verify step */
+  int req_cap, log_cap, plan_cap, nbuf;
+} mspq_cache_view;
+int mspq_cache_create(int L, int E, int K, int kmax, int nbuf, int log_cap, mspq_cache** out);
+int mspq_cache_destroy(mspq_cache* c);
+/* mode 0 per-layer / 1 global; policy = moespeq::Policy ordinal; caps[L] (per-layer) */
+int mspq_cache_configure(mspq_cache* c, int mode, int policy, const int* caps, int cap_global,
+                         int budget, double f1, double f2, void* stream);
+int mspq_cache_view_get(mspq_cache* c, mspq_cache_view* v);
+int mspq_cache_begin_cycle(mspq_cache* c, int k, void* stream);
+int mspq_cache_plan_row(mspq_cache* c, int row, void* stream);
+int mspq_cache_verify_layer(mspq_cache* c, int layer, int nslots, const int32_t* tgt,
+                            int32_t* n_groups, int32_t* group_expert, int32_t* group_buf,
+                            int32_t* group_off, int32_t* entry_tok, int32_t* entry_of,
+                            void* stream);
+/* token-major replay of one cycle over device trace arrays (target/draft [n][L][K] int32,
+ * gates [n][L][K] double or NULL).  out_*: counts[6], batches[kmax][3], jit_rows[kmax][2],
+ * cov[L][2], step[(kmax+1)*L][2], flush_keys[L*E] */
+int mspq_cache_replay_cycle(mspq_cache* c, const int32_t* target, const int32_t* draft,
+                            const double* gates, int pos, int k_eff, int head_pos,
+                            int32_t* out_counts, int32_t* out_batches, int32_t* out_jit_rows,
+                            int32_t* out_cov, int32_t* out_step, int32_t* out_flush_keys,
+                            void* stream);
+
+/* ---------------------------------------------------------------- (2) engine */
+/* run_simulation on the device control plane: trace = reference JSONL (trace.hpp:76-80),
+ * config = reference run-config JSON (run_config.hpp:30-50).  *report_json: SimReport JSON;
+ * with "log": true in config_json also the per-event hit/miss log. */
+int mspq_replay(int device, const char* trace_jsonl, const char* config_json,
+                char** report_json);
+/* Amortization-Roofline governor (perfmodel.cpp:85-217) on a JSON request:
+ * {"profile":{...},"p":[...],"alpha":a,"k_min","k_max","k_slo","g","ttft_budget","outcomes"}
+ * -> {"select_k","k_slo_ttft","t_cycle":[k=0..],"k_accept":[..],"t_verify":[..],"updated_p"} */
+int mspq_governor(const char* request_json, char** out_json);
+
+int mspq_engine_create(const mspq_model_desc* model, const mspq_engine_opts* opts,
+                       mspq_engine** out);
+int mspq_engine_destroy(mspq_engine* eng);
+/* expert-cache budget / policy / governor in the reference run-config schema; resets the cache */
+int mspq_engine_configure(mspq_engine* eng, const char* config_json);
+/* greedy speculative decode of max_new tokens after the prompt (last prompt token is the
+ * first window head).  *report_json: SimReport JSON + measured fields + per-cycle traces. */
+int mspq_generate(mspq_engine* eng, const int32_t* prompt, int n_prompt, int max_new,
+                  char** report_json);
+int mspq_engine_info(mspq_engine* eng, char** json);
+/* copy a device tensor of the engine out (tests): name in {"embed","pos","lm","router:<l>",
+ * "gamma:<l>","gamma:final","draft:<l>:<e>","expert:<l>:<e>"} */
+int mspq_engine_read(mspq_engine* eng, const char* name, void* host_dst, long long bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -352,9 +352,7 @@ class CausalPlanner:
     def row(self, elb, i):
         k, out = self.k, []
         self._absorb(elb, i)
-        if i < self.t1:
-            return out
-        if i < self.t2:
+        if self.t1 <= i < self.t2:
             if self.budget > 0:
                 pool = sorted(self.cands.items(),
                               key=lambda kv: (-(kv[1][0] * float(k - kv[1][1]) / k), kv[1][1], kv[0]))
@@ -362,11 +360,12 @@ class CausalPlanner:
                     out.append((i, key, 2))
                     self.scheduled.add(key)
                     del self.cands[key]
-            # a phase boundary at or past the window end flushes at the last row
-            if i == k - 1 and self.t2 >= k:
-                out += self._flush(i)
-            return out
-        return self._flush(i)
+        elif i >= self.t2:
+            out += self._flush(i)
+        # a phase boundary at or past the window end flushes at the last row (scheduler.cpp:243-252)
+        if i == k - 1 and self.t2 >= k:
+            out += self._flush(i)
+        return out
 
     def _flush(self, i):
         out = []

@@ -1,0 +1,367 @@
+"""TEST INFRASTRUCTURE ONLY — numpy restatement of the MoE-SpeQ decode math.
+
+"Parity unpinned by the reference": /root/reference has no model, weights, gating, GEMMs or
+logits.  This file *defines* the numerics the device must reproduce, from the
+paper: bf16 router / norms / non-expert params, INT4 symmetric group-128
+draft experts (GPTQ's sym convention scale = 2*amax/15, zero = 8), greedy
+verification = accepted prefix + one target token, reordered grouped verify
+(PAPER.md:495-496).  Order-sensitive fp32 pieces (fixed-order dots, RMSNorm sums, the exp used
+by softmax/SiLU) are in csrc/model_ref.c so they are bit-identical to the kernels; expert FFN
+dot products are computed here in float64 (the device result must lie within tolerance).
+
+Weights come from a counter-based hash, so any single tensor can be regenerated on the CPU
+without materialising the model.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "_build", "libmspq_oracle.so")
+_lib = None
+
+
+def build():
+    os.makedirs(os.path.join(_HERE, "_build"), exist_ok=True)
+    src = os.path.join(_HERE, "csrc", "model_ref.c")
+    if (not os.path.exists(_SO)) or os.path.getmtime(_SO) < os.path.getmtime(src):
+        import subprocess
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-o", _SO,
+                               src, "-lm"])
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_SO)
+        P = ctypes.c_void_p
+        L.orc_warp_dot.restype = ctypes.c_float
+        L.orc_warp_dot.argtypes = [P, P, ctypes.c_int]
+        L.orc_sumsq_cta.restype = ctypes.c_float
+        L.orc_sumsq_cta.argtypes = [P, ctypes.c_int]
+        L.orc_rmsnorm.argtypes = [P, P, ctypes.c_int, ctypes.c_float, P]
+        L.orc_det_exp.restype = ctypes.c_float
+        L.orc_det_exp.argtypes = [ctypes.c_float]
+        L.orc_router_topk.argtypes = [P, P, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, P]
+        L.orc_lm_head.argtypes = [P, P, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P]
+        L.orc_act.argtypes = [P, P, ctypes.c_int, P]
+        _lib = L
+    return _lib
+
+
+def _p(a):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+# ----------------------------------------------------------------------------- bf16 helpers
+def f32_to_bf16(x: np.ndarray) -> np.ndarray:
+    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32)
+    return ((u + np.uint32(0x7FFF) + ((u >> np.uint32(16)) & np.uint32(1))) >> np.uint32(16)).astype(np.uint16)
+
+
+def bf16_to_f32(b: np.ndarray) -> np.ndarray:
+    return (np.asarray(b, dtype=np.uint16).astype(np.uint32) << np.uint32(16)).view(np.float32)
+
+
+# ----------------------------------------------------------------------------- counter RNG
+M64 = (1 << 64) - 1
+GOLD = 0x9E3779B97F4A7C15
+STEP = 0xD1B54A32D192ED03
+
+
+def _mix_py(z: int) -> int:
+    z = (z + GOLD) & M64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M64
+    return z ^ (z >> 31)
+
+
+def _mix_np(z: np.ndarray) -> np.ndarray:
+    with np.errstate(over="ignore"):
+        z = z + np.uint64(GOLD)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return z ^ (z >> np.uint64(31))
+
+
+def tensor_key(seed: int, tensor: int) -> int:
+    return _mix_py((seed ^ _mix_py(tensor)) & M64)
+
+
+def uniform(seed: int, tensor: int, n: int, start: int = 0) -> np.ndarray:
+    """val(idx) in (-1, 1), exact in fp32: ((u>>40) - 2^23 + 0.5) * 2^-23."""
+    key = np.uint64(tensor_key(seed, tensor))
+    idx = np.arange(start, start + n, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = _mix_np(key + idx * np.uint64(STEP))
+    hi = (z >> np.uint64(40)).astype(np.int64) - (1 << 23)
+    return ((hi.astype(np.float32) + np.float32(0.5)) * np.float32(1.0 / 8388608.0)).astype(np.float32)
+
+
+# tensor ids
+T_EMBED, T_POS, T_LM, T_FINAL_GAMMA = 1, 2, 3, 4
+
+
+def t_gamma(l):
+    return 0x100 + l * 16
+
+
+def t_router(l):
+    return 0x100 + l * 16 + 1
+
+
+def t_expert(l, e, m):
+    return 0x1000000 + ((l * 1024 + e) * 4 + m)
+
+
+def gen(seed, tensor, rows, cols, scale) -> np.ndarray:
+    v = uniform(seed, tensor, rows * cols)
+    return f32_to_bf16(v * np.float32(scale)).reshape(rows, cols)
+
+
+def gen_gamma(seed, tensor, d) -> np.ndarray:
+    v = uniform(seed, tensor, d)
+    return f32_to_bf16(np.float32(1.0) + v * np.float32(0.125))
+
+
+# ----------------------------------------------------------------------------- INT4 (GPTQ sym)
+def quantize(w_bf16: np.ndarray, group: int = 128):
+    """Per row, per 128-column group: scale = bf16(amax / 7.5), q = clamp(rint(w/scale)+8, 0, 15)."""
+    w = bf16_to_f32(w_bf16).reshape(w_bf16.shape[0], -1, group)
+    amax = np.abs(w).max(axis=2)
+    s32 = (amax / np.float32(7.5)).astype(np.float32)
+    sb = f32_to_bf16(s32)
+    sf = bf16_to_f32(sb)
+    sf_safe = np.where(sf == 0, np.float32(1.0), sf).astype(np.float32)
+    q = np.rint((w / sf_safe[:, :, None]).astype(np.float32)) + np.float32(8)
+    q = np.clip(q, 0, 15).astype(np.uint8).reshape(w_bf16.shape)
+    sb = np.where(sf == 0, f32_to_bf16(np.ones_like(sf)), sb)
+    return q, sb
+
+
+def dequantize(q: np.ndarray, sb: np.ndarray, group: int = 128) -> np.ndarray:
+    rows, cols = q.shape
+    s = bf16_to_f32(sb)
+    return ((q.astype(np.float32) - np.float32(8)).reshape(rows, -1, group) * s[:, :, None]).reshape(rows, cols)
+
+
+def pack_int4(q: np.ndarray) -> np.ndarray:
+    """[rows, cols] nibbles -> [rows, cols/8] uint32, nibble n of word w = column 8w+n."""
+    rows, cols = q.shape
+    q = q.astype(np.uint32).reshape(rows, cols // 8, 8)
+    out = np.zeros((rows, cols // 8), dtype=np.uint32)
+    for n in range(8):
+        out |= q[:, :, n] << np.uint32(4 * n)
+    return out
+
+
+# ----------------------------------------------------------------------------- model
+@dataclass
+class ModelDesc:
+    L: int
+    E: int
+    K: int
+    d: int
+    f: int
+    V: int
+    P: int = 4096          # positional table rows
+    seed: int = 1234
+    embed_scale: float = 1.0
+    pos_scale: float = 0.5
+    router_scale: float = 3.0
+    moe_scale: float = 0.5
+    lm_scale: float = 1.0
+    eps: float = 1e-6
+
+    # scales passed to the device as fp32 (computed once, identically on both sides)
+    def a_router(self):
+        return float(np.float32(self.router_scale * math.sqrt(3.0 / self.d)))
+
+    def a_up(self):
+        return float(np.float32(math.sqrt(3.0 / self.d)))
+
+    def a_down(self):
+        return float(np.float32(self.moe_scale * math.sqrt(3.0 / self.f)))
+
+    def a_lm(self):
+        return float(np.float32(self.lm_scale * math.sqrt(3.0 / self.d)))
+
+    def expert_bytes_bf16(self):
+        return 3 * self.d * self.f * 2
+
+    def expert_bytes_int4(self):
+        return 3 * self.d * self.f // 2 + 3 * self.d * self.f // 128 * 2
+
+
+CONFIGS = {
+    # BASELINE.json configs (ffn for tiny chosen: 512; Qwen3 moe_intermediate 768)
+    "tiny": dict(L=4, E=8, K=2, d=256, f=512, V=512),
+    "mixtral": dict(L=32, E=8, K=2, d=4096, f=14336, V=32000),
+    "phi": dict(L=32, E=16, K=2, d=4096, f=6400, V=32064),
+    "qwen3": dict(L=48, E=128, K=8, d=2048, f=768, V=151936),
+}
+
+
+class Model:
+    """CPU model: weights regenerated lazily from the counter hash."""
+
+    def __init__(self, desc: ModelDesc):
+        self.m = desc
+        self._cache = {}
+
+    def _get(self, key, fn):
+        if key not in self._cache:
+            self._cache[key] = fn()
+        return self._cache[key]
+
+    def embed_row(self, tok):
+        m = self.m
+        return self._get(("emb", tok), lambda: f32_to_bf16(
+            uniform(m.seed, T_EMBED, m.d, start=tok * m.d) * np.float32(m.embed_scale)))
+
+    def pos_row(self, p):
+        m = self.m
+        return self._get(("pos", p), lambda: f32_to_bf16(
+            uniform(m.seed, T_POS, m.d, start=p * m.d) * np.float32(m.pos_scale)))
+
+    def gamma(self, l):
+        m = self.m
+        t = T_FINAL_GAMMA if l < 0 else t_gamma(l)
+        return self._get(("gamma", l), lambda: gen_gamma(m.seed, t, m.d))
+
+    def router(self, l):
+        m = self.m
+        return self._get(("router", l), lambda: gen(m.seed, t_router(l), m.E, m.d, m.a_router()))
+
+    def lm(self):
+        m = self.m
+        return self._get("lm", lambda: gen(m.seed, T_LM, m.V, m.d, m.a_lm()))
+
+    def expert(self, l, e):
+        """bf16 (gate [f,d], up [f,d], down [d,f])."""
+        m = self.m
+        return self._get(("x", l, e), lambda: (
+            gen(m.seed, t_expert(l, e, 0), m.f, m.d, m.a_up()),
+            gen(m.seed, t_expert(l, e, 1), m.f, m.d, m.a_up()),
+            gen(m.seed, t_expert(l, e, 2), m.d, m.f, m.a_down())))
+
+    def expert_q(self, l, e):
+        """INT4 (q, scales) for gate, up, down."""
+        def mk():
+            g, u, dn = self.expert(l, e)
+            return quantize(g), quantize(u), quantize(dn)
+        return self._get(("q", l, e), mk)
+
+    # -- pieces -----------------------------------------------------------------------------
+    def rmsnorm(self, h, gamma):
+        out = np.empty(self.m.d, dtype=np.uint16)
+        lib().orc_rmsnorm(_p(h), _p(gamma), self.m.d, ctypes.c_float(self.m.eps), _p(out))
+        return out
+
+    def route(self, xn, l):
+        m = self.m
+        logits = np.empty(m.E, dtype=np.float32)
+        ids = np.empty(m.K, dtype=np.int32)
+        wts = np.empty(m.K, dtype=np.float32)
+        wr = np.ascontiguousarray(self.router(l))
+        lib().orc_router_topk(_p(xn), _p(wr), m.E, m.d, m.K, _p(logits), _p(ids), _p(wts))
+        return ids, wts, logits
+
+    def ffn(self, xn, l, e, draft: bool):
+        m = self.m
+        x = bf16_to_f32(xn)
+        G, U, D = self.expert_f32(l, e, draft)
+        gv = np.ascontiguousarray(G @ x, dtype=np.float32)
+        uv = np.ascontiguousarray(U @ x, dtype=np.float32)
+        a = np.empty(m.f, dtype=np.uint16)
+        lib().orc_act(_p(gv), _p(uv), m.f, _p(a))
+        y = (D @ bf16_to_f32(a)).astype(np.float32)
+        return y, a
+
+    def expert_f32(self, l, e, draft):
+        """Dequantised (draft) or widened (target) fp32 matrices, cached."""
+        def mk():
+            if draft:
+                (gq, gs), (uq, us), (dq, ds) = self.expert_q(l, e)
+                return dequantize(gq, gs), dequantize(uq, us), dequantize(dq, ds)
+            g, u, dn = self.expert(l, e)
+            return bf16_to_f32(g), bf16_to_f32(u), bf16_to_f32(dn)
+        return self._get(("f32", l, e, draft), mk)
+
+    def lm_head(self, xn_rows):
+        m = self.m
+        T = xn_rows.shape[0]
+        logits = np.empty((T, m.V), dtype=np.float32)
+        am = np.empty(T, dtype=np.int32)
+        lm = np.ascontiguousarray(self.lm())
+        lib().orc_lm_head(_p(np.ascontiguousarray(xn_rows)), _p(lm), T, m.V, m.d, _p(logits), _p(am))
+        return logits, am
+
+    # -- one token ---------------------------------------------------------------------------
+    def forward(self, tok, pos, draft: bool, record=None, h_override=None):
+        """Returns (argmax token, per-layer (ids, wts), final logits).  `h_override[l]`, when
+        given, replaces the residual entering layer l (teacher forcing from the device)."""
+        m = self.m
+        h = (bf16_to_f32(self.embed_row(tok)) + bf16_to_f32(self.pos_row(pos))).astype(np.float32)
+        routing = []
+        for l in range(m.L):
+            if h_override is not None and l in h_override:
+                h = np.asarray(h_override[l], dtype=np.float32).copy()
+            xn = self.rmsnorm(h, self.gamma(l))
+            ids, wts, logits = self.route(xn, l)
+            routing.append((ids.copy(), wts.copy()))
+            acc = np.zeros(m.d, dtype=np.float32)
+            for j in range(m.K):
+                y, _ = self.ffn(xn, l, int(ids[j]), draft)
+                acc = (acc + (np.float32(wts[j]) * y).astype(np.float32)).astype(np.float32)
+            if record is not None:
+                record.append(dict(layer=l, h_in=h.copy(), xn=xn, logits=logits))
+            h = (h + acc).astype(np.float32)
+        xf = self.rmsnorm(h, self.gamma(-1))
+        logits, am = self.lm_head(xf[None, :])
+        return int(am[0]), routing, logits[0]
+
+
+def speculative_decode(model: Model, last_token: int, start_pos: int, ks, max_new: int):
+    """Greedy speculative decoding with the INT4 draft: each cycle drafts k
+    tokens from the head (previous bonus), verifies the k+1-slot window with the bf16 target
+    (slot i target argmax predicts slot i+1), accepts the longest matching prefix plus the
+    target's token at the first mismatch.  Yields per-cycle records; `ks` supplies k per cycle
+    (the governor's choice is a host-timing decision, so the oracle consumes it)."""
+    out, tok, pos, committed = [], last_token, start_pos, 0
+    ci = 0
+    while committed < max_new:
+        k = min(ks[ci] if ci < len(ks) else ks[-1], max_new - committed)
+        k = max(k, 1)
+        draft_toks, elb_rows = [], []
+        t, p = tok, pos
+        for i in range(k):
+            nt, routing, _ = model.forward(t, p, draft=True)
+            elb_rows.append(routing)
+            draft_toks.append(nt)
+            t, p = nt, p + 1
+        window = [tok] + draft_toks
+        tgt_routing, tgt_argmax = [], []
+        for s, wt in enumerate(window):
+            am, routing, _ = model.forward(wt, pos + s, draft=False)
+            tgt_routing.append(routing)
+            tgt_argmax.append(am)
+        acc = 0
+        while acc < k and draft_toks[acc] == tgt_argmax[acc]:
+            acc += 1
+        bonus = tgt_argmax[acc]
+        new = draft_toks[:acc] + [bonus]
+        new = new[:max_new - committed]
+        out.append(dict(k=k, draft=draft_toks, elb=elb_rows, target=tgt_routing,
+                        target_argmax=tgt_argmax, accepted=acc, committed=new))
+        committed += len(new)
+        pos += acc + 1
+        tok = bonus
+        ci += 1
+    return out

@@ -1,0 +1,149 @@
+"""B200-native MoE-SpeQ decode hot path (arXiv 2511.14102).
+
+Python mirror of the reference's public API for this path (proj/python/moespeq re-exports
+proj/bindings/module.cpp): `run_simulation(trace, config)` keeps its name and meaning but runs
+every cache decision on the GPU (device controller, K4); `Engine.generate(...)` is the live
+speculative decode (INT4 draft -> ELB -> 3-phase prefetch over copy engines -> bf16 grouped
+verify -> accept -> governor).  Configs use the reference run-config JSON schema
+(run_config.hpp:30-50).  All compute goes through libmspq.so (include/mspq_capi.h); there is no
+CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import math
+from dataclasses import dataclass
+
+from . import _lib
+from ._lib import MspqError, check, lib, take_string
+
+__version__ = "0.1.0"
+
+POLICIES = ["lru", "lookahead", "sp-sooner", "sp-later", "speculative"]
+
+# BASELINE.json shapes (tiny ffn chosen = 512; Qwen3-30B-A3B moe_intermediate = 768)
+MODEL_SHAPES = {
+    "tiny": dict(L=4, E=8, K=2, d=256, f=512, V=512),
+    "mixtral": dict(L=32, E=8, K=2, d=4096, f=14336, V=32000),
+    "phi": dict(L=32, E=16, K=2, d=4096, f=6400, V=32064),
+    "qwen3": dict(L=48, E=128, K=8, d=2048, f=768, V=151936),
+}
+
+
+@dataclass
+class ModelConfig:
+    """Model / draft config: ModelShape (trace.hpp:29-37) + the dims a real model needs."""
+    L: int
+    E: int
+    K: int
+    d: int
+    f: int
+    V: int
+    P: int = 4096
+    seed: int = 1234
+    embed_scale: float = 1.0
+    pos_scale: float = 0.5
+    router_scale: float = 3.0
+    moe_scale: float = 0.5
+    lm_scale: float = 1.0
+    eps: float = 1e-6
+    unique_experts: int = 0
+
+    @classmethod
+    def named(cls, name, **kw):
+        d = dict(MODEL_SHAPES[name])
+        d.update(kw)
+        return cls(**d)
+
+    def _f32(self, x):
+        return ctypes.c_float(x).value
+
+    def desc(self) -> _lib.ModelDesc:
+        f32 = self._f32
+        return _lib.ModelDesc(self.L, self.E, self.K, self.d, self.f, self.V, self.P, self.seed,
+                              self.embed_scale, self.pos_scale,
+                              f32(self.router_scale * math.sqrt(3.0 / self.d)),
+                              f32(math.sqrt(3.0 / self.d)),
+                              f32(self.moe_scale * math.sqrt(3.0 / self.f)),
+                              f32(self.lm_scale * math.sqrt(3.0 / self.d)), self.eps,
+                              self.unique_experts)
+
+    def expert_bytes_bf16(self):
+        return lib().mspq_bf16_blob_bytes(self.d, self.f)
+
+    def expert_bytes_int4(self):
+        return lib().mspq_int4_blob_bytes(self.d, self.f)
+
+
+def _cfg_json(config) -> bytes:
+    if isinstance(config, (bytes, str)):
+        return config.encode() if isinstance(config, str) else config
+    return json.dumps(config).encode()
+
+
+def run_simulation(trace_jsonl: str, config: dict, device: int = 0) -> dict:
+    """run_simulation (sim.hpp:86) with the expert-cache control plane on the GPU.
+    trace: reference JSONL text; config: reference run-config dict.  Returns the SimReport
+    JSON dict (sim.cpp:468-510)."""
+    out = ctypes.c_void_p()
+    check(lib().mspq_replay(device, trace_jsonl.encode(), _cfg_json(config), ctypes.byref(out)))
+    return json.loads(take_string(out))
+
+
+replay = run_simulation
+
+
+def governor(request: dict) -> dict:
+    """Amortization-Roofline governor evaluation (perfmodel.cpp:85-217) in the product."""
+    out = ctypes.c_void_p()
+    check(lib().mspq_governor(json.dumps(request).encode(), ctypes.byref(out)))
+    return json.loads(take_string(out))
+
+
+class Engine:
+    """Live engine: owns the device model (bf16 non-expert + INT4 draft experts resident),
+    the pinned host expert store, the capped HBM slot pool and the device cache controller."""
+
+    def __init__(self, model: ModelConfig, kmax: int = 16, device: int = 0,
+                 host_store_path: str | None = None, host_store_role: int = 0,
+                 slot_extra: int = 0, trace_level: int = 1, log_cap: int = 0):
+        self.model = model
+        self._desc = model.desc()
+        self._path = (host_store_path or "").encode()
+        self._opts = _lib.EngineOpts(device, kmax, self._path, host_store_role, slot_extra,
+                                     log_cap, trace_level)
+        self._h = ctypes.c_void_p()
+        check(lib().mspq_engine_create(ctypes.byref(self._desc), ctypes.byref(self._opts),
+                                       ctypes.byref(self._h)))
+
+    def configure(self, config: dict):
+        """Expert-cache budget / policy / governor (reference run-config schema)."""
+        check(lib().mspq_engine_configure(self._h, _cfg_json(config)))
+
+    def generate(self, prompt, max_new_tokens: int) -> dict:
+        arr = (ctypes.c_int32 * len(prompt))(*prompt)
+        out = ctypes.c_void_p()
+        check(lib().mspq_generate(self._h, arr, len(prompt), max_new_tokens, ctypes.byref(out)))
+        return json.loads(take_string(out))
+
+    def info(self) -> dict:
+        out = ctypes.c_void_p()
+        check(lib().mspq_engine_info(self._h, ctypes.byref(out)))
+        return json.loads(take_string(out))
+
+    def read(self, name: str, nbytes: int):
+        buf = (ctypes.c_uint8 * nbytes)()
+        check(lib().mspq_engine_read(self._h, name.encode(), buf, nbytes))
+        return bytes(buf)
+
+    def close(self):
+        if self._h:
+            lib().mspq_engine_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,103 @@
+"""ctypes binding of libmspq.so (include/mspq_capi.h).  No fallback: if the CUDA library is
+missing the import of anything that needs it raises."""
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmspq.so")
+
+_lib = None
+
+c_int, c_ll, c_ull, c_float, c_double, c_void_p, c_char_p = (
+    ctypes.c_int, ctypes.c_longlong, ctypes.c_ulonglong, ctypes.c_float, ctypes.c_double,
+    ctypes.c_void_p, ctypes.c_char_p)
+
+
+class ModelDesc(ctypes.Structure):
+    _fields_ = [("L", c_int), ("E", c_int), ("K", c_int), ("d", c_int), ("f", c_int),
+                ("V", c_int), ("P", c_int), ("seed", c_ull), ("embed_scale", c_float),
+                ("pos_scale", c_float), ("a_router", c_float), ("a_up", c_float),
+                ("a_down", c_float), ("a_lm", c_float), ("eps", c_float),
+                ("unique_experts", c_int)]
+
+
+class EngineOpts(ctypes.Structure):
+    _fields_ = [("device", c_int), ("kmax", c_int), ("host_store_path", c_char_p),
+                ("host_store_role", c_int), ("slot_extra", c_int), ("log_cap", c_int),
+                ("trace_level", c_int)]
+
+
+# (name, restype, argtypes)
+_SIGS = [
+    ("mspq_status_string", c_char_p, [c_int]),
+    ("mspq_last_error", c_char_p, []),
+    ("mspq_free", None, [c_void_p]),
+    ("mspq_version", c_int, []),
+    ("mspq_fill_bf16", c_int, [c_ull, c_ull, c_float, c_int, c_void_p, c_ll, c_ll, c_void_p]),
+    ("mspq_fill_expert", c_int, [c_ull, c_int, c_int, c_int, c_int, c_float, c_float, c_void_p, c_void_p]),
+    ("mspq_quantize_int4", c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p]),
+    ("mspq_embed", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p]),
+    ("mspq_gate_topk", c_int, [c_void_p] * 13 + [c_int] * 6 + [c_float, c_void_p]),
+    ("mspq_build_schedule", c_int, [c_void_p, c_int, c_int, c_int] + [c_void_p] * 7),
+    ("mspq_moe_int4", c_int, [c_void_p] * 9 + [c_ll] + [c_int] * 5 + [c_void_p]),
+    ("mspq_moe_bf16", c_int, [c_void_p] * 9 + [c_ll] + [c_int] * 4 + [c_void_p]),
+    ("mspq_lm_head", c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p]),
+    ("mspq_argmax", c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p]),
+    ("mspq_argmax_advance", c_int, [c_void_p, c_int] + [c_void_p] * 6),
+    ("mspq_accept_scan", c_int, [c_void_p, c_void_p, c_int, c_void_p, c_void_p]),
+    ("mspq_accept_advance", c_int, [c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_int, c_void_p]),
+    ("mspq_int4_blob_bytes", c_ll, [c_int, c_int]),
+    ("mspq_bf16_blob_bytes", c_ll, [c_int, c_int]),
+    ("mspq_cache_create", c_int, [c_int] * 6 + [c_void_p]),
+    ("mspq_cache_destroy", c_int, [c_void_p]),
+    ("mspq_cache_configure", c_int, [c_void_p, c_int, c_int, c_void_p, c_int, c_int, c_double, c_double, c_void_p]),
+    ("mspq_cache_view_get", c_int, [c_void_p, c_void_p]),
+    ("mspq_cache_begin_cycle", c_int, [c_void_p, c_int, c_void_p]),
+    ("mspq_cache_plan_row", c_int, [c_void_p, c_int, c_void_p]),
+    ("mspq_cache_verify_layer", c_int, [c_void_p, c_int, c_int] + [c_void_p] * 8),
+    ("mspq_cache_replay_cycle", c_int, [c_void_p] * 4 + [c_int] * 3 + [c_void_p] * 7),
+    ("mspq_replay", c_int, [c_int, c_char_p, c_char_p, ctypes.POINTER(c_void_p)]),
+    ("mspq_governor", c_int, [c_char_p, ctypes.POINTER(c_void_p)]),
+    ("mspq_engine_create", c_int, [ctypes.POINTER(ModelDesc), ctypes.POINTER(EngineOpts), ctypes.POINTER(c_void_p)]),
+    ("mspq_engine_destroy", c_int, [c_void_p]),
+    ("mspq_engine_configure", c_int, [c_void_p, c_char_p]),
+    ("mspq_generate", c_int, [c_void_p, c_void_p, c_int, c_int, ctypes.POINTER(c_void_p)]),
+    ("mspq_engine_info", c_int, [c_void_p, ctypes.POINTER(c_void_p)]),
+    ("mspq_engine_read", c_int, [c_void_p, c_char_p, c_void_p, c_ll]),
+]
+
+EXPORTS = [s[0] for s in _SIGS]
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"libmspq.so not built ({LIB_PATH}); run __graft_entry__.build()")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, res, args in _SIGS:
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+class MspqError(RuntimeError):
+    """moespeq::Error analogue: .code = status (ErrorCode ordinal + 1, or 1000+)."""
+
+    def __init__(self, code, msg):
+        super().__init__(f"{lib().mspq_status_string(code).decode()}: {msg}")
+        self.code = code
+        self.name = lib().mspq_status_string(code).decode()
+
+
+def check(status):
+    if status != 0:
+        raise MspqError(status, lib().mspq_last_error().decode())
+
+
+def take_string(ptr) -> str:
+    s = ctypes.cast(ptr, c_char_p).value.decode()
+    lib().mspq_free(ptr)
+    return s

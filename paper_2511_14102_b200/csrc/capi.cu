@@ -1,0 +1,264 @@
+// extern "C" kernel entry points of libmspq.so (include/mspq_capi.h, part 1 + K4).
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/mspq_capi.h"
+#include "ctl.h"
+#include "kernels.h"
+#include "status.h"
+
+using namespace mspq;
+
+namespace mspq {
+thread_local std::string g_last_error;
+int set_error(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+int cuda_status(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return MSPQ_OK;
+  return set_error(MSPQ_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+}  // namespace mspq
+
+#define ST(s) reinterpret_cast<cudaStream_t>(s)
+#define CK(expr, where) return cuda_status((expr), where)
+
+extern "C" {
+
+const char* mspq_status_string(int s) {
+  static const char* names[] = {"OK", "MalformedRecord", "ShapeViolation", "EmptyTrace",
+                                "InvalidFidelity", "DegenerateShape", "LayerOutOfRange",
+                                "ShapeMismatch", "RangeOutOfBounds", "EmptyCache", "UnknownPolicy",
+                                "EmptyRequired", "IncompleteRouting", "KOutOfRange",
+                                "InsufficientSamples", "EmptyRange", "InfeasibleBudget",
+                                "InvalidConfig", "IoError"};
+  if (s >= 0 && s <= 18) return names[s];
+  if (s == MSPQ_ERR_CUDA) return "CudaError";
+  if (s == MSPQ_ERR_OVERFLOW) return "Overflow";
+  return "Internal";
+}
+const char* mspq_last_error(void) { return g_last_error.c_str(); }
+void mspq_free(void* p) { free(p); }
+int mspq_version(void) { return 1; }
+
+long long mspq_int4_blob_bytes(int d, int f) {
+  return (long long)2 * f * d / 2 + (long long)2 * f * (d / 128) * 2 + (long long)d * f / 2 +
+         (long long)d * (f / 128) * 2;
+}
+long long mspq_bf16_blob_bytes(int d, int f) { return (long long)3 * d * f * 2; }
+
+int mspq_fill_bf16(unsigned long long seed, unsigned long long tensor, float scale, int kind,
+                   void* out, long long n, long long start, void* stream) {
+  CK(launch_fill_bf16(seed, tensor, scale, kind, (uint16_t*)out, n, start, ST(stream)), "fill_bf16");
+}
+int mspq_fill_expert(unsigned long long seed, int l, int e, int d, int f, float a_up, float a_down,
+                     void* blob, void* stream) {
+  CK(launch_fill_expert(seed, l, e, d, f, a_up, a_down, (uint16_t*)blob, ST(stream)), "fill_expert");
+}
+int mspq_quantize_int4(const void* w, int rows, int cols, void* q, void* s, void* stream) {
+  if (cols % 128) return set_error(MSPQ_ERR_SHAPE_MISMATCH, "quantize: cols % 128 != 0");
+  CK(launch_quantize((const uint16_t*)w, rows, cols, (uint32_t*)q, (uint16_t*)s, ST(stream)), "quantize");
+}
+int mspq_embed(const void* embed, const void* pos, const int32_t* tokens, const int32_t* positions,
+               int T, int d, float* h, void* stream) {
+  CK(launch_embed((const uint16_t*)embed, (const uint16_t*)pos, tokens, positions, T, d, h, ST(stream)),
+     "embed");
+}
+int mspq_gate_topk(float* h, const float* y, const int32_t* entry_of, const float* prev_wts,
+                   const void* gamma, const void* router, void* xn, int32_t* ids, float* wts,
+                   float* logits, int32_t* elb_ids, float* elb_gates, const int32_t* elb_row,
+                   int layer, int L, int T, int d, int E, int K, float eps, void* stream) {
+  if (d % 256 || K > 64 || E > 1024 || K > E)
+    return set_error(MSPQ_ERR_SHAPE_MISMATCH, "gate_topk: need d%256==0, K<=min(E,64), E<=1024");
+  RouteArgs a{h, y, entry_of, prev_wts, (const uint16_t*)gamma, (const uint16_t*)router,
+              (uint16_t*)xn, ids, wts, logits, elb_ids, elb_gates, elb_row, layer, L, d, E, K, eps};
+  CK(launch_route(a, T, ST(stream)), "gate_topk");
+}
+int mspq_build_schedule(const int32_t* ids, int T, int K, int E, int32_t* n_groups,
+                        int32_t* group_expert, int32_t* group_buf, int32_t* group_off,
+                        int32_t* entry_tok, int32_t* entry_of, void* stream) {
+  SchedPtrs s{n_groups, group_expert, group_buf, group_off, entry_tok, entry_of};
+  CK(launch_build_schedule(ids, T, K, E, s, ST(stream)), "build_schedule");
+}
+int mspq_moe_int4(const int32_t* n_groups, const int32_t* group_expert, const int32_t* group_buf,
+                  const int32_t* group_off, const int32_t* entry_tok, const void* xn, void* act,
+                  float* y, const void* blobs, long long blob_bytes, int layer, int E, int d, int f,
+                  int max_groups, void* stream) {
+  if (d % 256 || f % 256) return set_error(MSPQ_ERR_SHAPE_MISMATCH, "moe_int4: d, f % 256");
+  SchedPtrs s{(int32_t*)n_groups, (int32_t*)group_expert, (int32_t*)group_buf, (int32_t*)group_off,
+              (int32_t*)entry_tok, nullptr};
+  ExpertArgs a{s, (const uint16_t*)xn, (uint16_t*)act, y, (const unsigned char*)blobs, blob_bytes,
+               layer, E, d, f};
+  CK(launch_expert(a, true, max_groups, ST(stream)), "moe_int4");
+}
+int mspq_moe_bf16(const int32_t* n_groups, const int32_t* group_expert, const int32_t* group_buf,
+                  const int32_t* group_off, const int32_t* entry_tok, const void* xn, void* act,
+                  float* y, const void* pool, long long blob_bytes, int E, int d, int f,
+                  int max_groups, void* stream) {
+  if (d % 256 || f % 256) return set_error(MSPQ_ERR_SHAPE_MISMATCH, "moe_bf16: d, f % 256");
+  SchedPtrs s{(int32_t*)n_groups, (int32_t*)group_expert, (int32_t*)group_buf, (int32_t*)group_off,
+              (int32_t*)entry_tok, nullptr};
+  ExpertArgs a{s, (const uint16_t*)xn, (uint16_t*)act, y, (const unsigned char*)pool, blob_bytes,
+               0, E, d, f};
+  CK(launch_expert(a, false, max_groups, ST(stream)), "moe_bf16");
+}
+int mspq_lm_head(const void* xn, const void* lm, int T, int V, int d, float* logits, void* stream) {
+  CK(launch_lm_head((const uint16_t*)xn, (const uint16_t*)lm, T, V, d, logits, ST(stream)), "lm_head");
+}
+int mspq_argmax(const float* logits, int T, int V, int32_t* out, void* stream) {
+  DraftState ds{nullptr, nullptr, nullptr, nullptr};
+  CK(launch_argmax(logits, T, V, out, ds, ST(stream)), "argmax");
+}
+int mspq_accept_scan(const int32_t* draft, const int32_t* tgt, int k, int32_t* res, void* stream) {
+  CK(launch_accept(draft, tgt, k, res, nullptr, nullptr, 0, ST(stream)), "accept_scan");
+}
+
+int mspq_argmax_advance(const float* logits, int V, int32_t* out, int32_t* row,
+                        int32_t* draft_toks, int32_t* cur_tok, int32_t* cur_pos, void* stream) {
+  DraftState ds{row, draft_toks, cur_tok, cur_pos};
+  CK(launch_argmax(logits, 1, V, out, ds, ST(stream)), "argmax_advance");
+}
+int mspq_accept_advance(const int32_t* draft, const int32_t* tgt, int k, int32_t* res,
+                        int32_t* cur_tok, int32_t* cur_pos, int head_pos, void* stream) {
+  CK(launch_accept(draft, tgt, k, res, cur_tok, cur_pos, head_pos, ST(stream)), "accept_advance");
+}
+
+// ------------------------------------------------------------------ K4
+struct mspq_cache {
+  CtlDev C;
+  int kmax, nbuf;
+  void* blk;
+  void* hblk;  // mapped pinned: [0,256) status mirror, then requests
+};
+
+int mspq_cache_create(int L, int E, int K, int kmax, int nbuf, int log_cap, mspq_cache** out) {
+  if (L < 1 || E < 1 || K < 1 || K > E || L * E > 8192 || E > 1024)
+    return set_error(MSPQ_ERR_SHAPE_VIOLATION, "cache: need 1<=K<=E<=1024, L*E<=8192");
+  mspq_cache* c = new mspq_cache();
+  c->kmax = kmax;
+  c->nbuf = nbuf;
+  CtlDev& C = c->C;
+  C.L = L;
+  C.E = E;
+  C.K = K;
+  const int n = L * E;
+  C.req_cap = 4 * n + 64;
+  C.log_cap = log_cap > 0 ? log_cap : (kmax + 1) * L * K * 4 + 4 * n + 64;
+  C.plan_cap = n + 64;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 255) & ~size_t(255);
+    return o;
+  };
+  size_t o_cap = take(L * 4), o_res = take(n * 4), o_stamp = take(n * 8), o_clock = take(8),
+         o_lsize = take(L * 4), o_scal = take(S_COUNT * 4), o_free = take(nbuf * 4 + 4),
+         o_pend = take(nbuf * 4 + 4), o_snap = take(n), o_sched = take(n), o_cf = take(n * 4),
+         o_cc = take(n * 8), o_eids = take((size_t)kmax * L * K * 4),
+         o_eg = take((size_t)kmax * L * K * 4),
+         o_log = take((size_t)C.log_cap * 24), o_plan = take((size_t)C.plan_cap * 12),
+         o_cov = take(L * 8), o_step = take((size_t)L * (kmax + 1) * 8);
+  cudaError_t e = cudaMalloc(&c->blk, off);
+  if (e != cudaSuccess) {
+    delete c;
+    return cuda_status(e, "cache_create");
+  }
+  // copy requests + status are written by the controller straight into mapped pinned memory
+  const size_t hbytes = 256 + (size_t)(E + 8) * 4 + (size_t)C.req_cap * 12;
+  e = cudaHostAlloc(&c->hblk, hbytes, cudaHostAllocMapped);
+  if (e != cudaSuccess) {
+    cudaFree(c->blk);
+    delete c;
+    return cuda_status(e, "cache_create(host)");
+  }
+  memset(c->hblk, 0, hbytes);
+  void* dptr = nullptr;
+  cudaHostGetDevicePointer(&dptr, c->hblk, 0);
+  cudaMemset(c->blk, 0, off);
+  char* b = (char*)c->blk;
+  C.cap = (int*)(b + o_cap);
+  C.res = (int*)(b + o_res);
+  C.stamp = (unsigned long long*)(b + o_stamp);
+  C.clock = (unsigned long long*)(b + o_clock);
+  C.lsize = (int*)(b + o_lsize);
+  C.scal = (int*)(b + o_scal);
+  C.free_stack = (int*)(b + o_free);
+  C.pending = (int*)(b + o_pend);
+  C.snap = (unsigned char*)(b + o_snap);
+  C.sched = (unsigned char*)(b + o_sched);
+  C.cand_first = (int*)(b + o_cf);
+  C.cand_conf = (double*)(b + o_cc);
+  C.elb_ids = (int32_t*)(b + o_eids);
+  C.elb_gates = (float*)(b + o_eg);
+  C.hstat = (int*)dptr;
+  C.hsched = (int*)((char*)dptr + 256);
+  C.req = (int*)((char*)dptr + 256 + (size_t)(E + 8) * 4);
+  C.log = (int*)(b + o_log);
+  C.plan = (int*)(b + o_plan);
+  C.cov = (int*)(b + o_cov);
+  C.step = (int*)(b + o_step);
+  *out = c;
+  return MSPQ_OK;
+}
+
+int mspq_cache_destroy(mspq_cache* c) {
+  if (!c) return MSPQ_OK;
+  cudaFree(c->blk);
+  cudaFreeHost(c->hblk);
+  delete c;
+  return MSPQ_OK;
+}
+
+int mspq_cache_configure(mspq_cache* c, int mode, int policy, const int* caps, int cap_global,
+                         int budget, double f1, double f2, void* stream) {
+  if (policy < 0 || policy > 4) return set_error(MSPQ_ERR_UNKNOWN_POLICY, "policy ordinal");
+  CtlDev& C = c->C;
+  C.mode = mode;
+  C.policy = policy;
+  C.cap_global = cap_global;
+  C.budget = budget;
+  C.f1 = f1;
+  C.f2 = f2;
+  cudaError_t e = cudaMemcpyAsync(C.cap, caps, C.L * sizeof(int), cudaMemcpyHostToDevice, ST(stream));
+  if (e != cudaSuccess) return cuda_status(e, "cache_configure");
+  CK(ctl_reset(C, c->nbuf, ST(stream)), "cache_reset");
+}
+
+int mspq_cache_view_get(mspq_cache* c, mspq_cache_view* v) {
+  const CtlDev& C = c->C;
+  *v = mspq_cache_view{C.elb_ids, C.elb_gates, C.scal, C.req, C.log, C.plan, C.cov, C.step, C.res,
+                       (int32_t*)c->hblk, (int32_t*)((char*)c->hblk + 256 + (size_t)(C.E + 8) * 4),
+                       (int32_t*)((char*)c->hblk + 256),
+                       C.req_cap, C.log_cap, C.plan_cap, c->nbuf};
+  return MSPQ_OK;
+}
+
+int mspq_cache_begin_cycle(mspq_cache* c, int k, void* stream) {
+  if (k < 0 || k > c->kmax) return set_error(MSPQ_ERR_K_OUT_OF_RANGE, "k > kmax");
+  CK(ctl_begin_cycle(c->C, k, ST(stream)), "cache_begin_cycle");
+}
+int mspq_cache_plan_row(mspq_cache* c, int row, void* stream) {
+  CK(ctl_plan_row(c->C, row, ST(stream)), "cache_plan_row");
+}
+int mspq_cache_verify_layer(mspq_cache* c, int layer, int nslots, const int32_t* tgt,
+                            int32_t* n_groups, int32_t* group_expert, int32_t* group_buf,
+                            int32_t* group_off, int32_t* entry_tok, int32_t* entry_of,
+                            void* stream) {
+  if (nslots > c->kmax + 1) return set_error(MSPQ_ERR_K_OUT_OF_RANGE, "nslots > kmax+1");
+  SchedPtrs s{n_groups, group_expert, group_buf, group_off, entry_tok, entry_of};
+  CK(ctl_verify_layer(c->C, layer, nslots, tgt, s, ST(stream)), "cache_verify_layer");
+}
+int mspq_cache_replay_cycle(mspq_cache* c, const int32_t* target, const int32_t* draft,
+                            const double* gates, int pos, int k_eff, int head_pos,
+                            int32_t* out_counts, int32_t* out_batches, int32_t* out_jit_rows,
+                            int32_t* out_cov, int32_t* out_step, int32_t* out_flush_keys,
+                            void* stream) {
+  if (k_eff > c->kmax) return set_error(MSPQ_ERR_K_OUT_OF_RANGE, "k_eff > kmax");
+  ReplayTrace tr{target, draft, gates};
+  ReplayOut o{out_counts, out_batches, out_jit_rows, out_cov, out_step, out_flush_keys};
+  CK(ctl_replay_cycle(c->C, tr, pos, k_eff, head_pos, o, ST(stream)), "cache_replay_cycle");
+}
+
+}  // extern "C"

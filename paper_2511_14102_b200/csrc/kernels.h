@@ -1,0 +1,75 @@
+// Internal launcher interface between the C-ABI / host engine and the kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+namespace mspq {
+
+// Expert-grouped schedule (K3's reorder_verification output); device pointers.
+struct SchedPtrs {
+  int32_t* n_groups;      // [1]
+  int32_t* group_expert;  // [G]
+  int32_t* group_buf;     // [G]   HBM slot-pool buffer (verify) / expert id (draft)
+  int32_t* group_off;     // [G+1] entry offsets
+  int32_t* entry_tok;     // [N]   window token of each entry
+  int32_t* entry_of;      // [T*K] entry index of (token, k-slot)
+};
+
+struct ExpertArgs {
+  SchedPtrs s;
+  const uint16_t* xn;           // [T][d] bf16 normed input
+  uint16_t* act;                // [N][f] bf16
+  float* y;                     // [N][d] fp32
+  const unsigned char* w_base;  // int4: all L*E draft blobs; bf16: slot pool
+  int64_t blob_bytes;
+  int layer, E, d, f;
+};
+
+// Draft-loop state living on the device so a draft step is a replayable CUDA graph.
+struct DraftState {
+  int32_t* row;         // ELB row / draft index
+  int32_t* draft_toks;  // [kmax]
+  int32_t* cur_tok;
+  int32_t* cur_pos;
+};
+
+struct RouteArgs {
+  float* h;                  // [T][d] residual, updated in place by the combine
+  const float* y;            // [N][d] expert outputs of the previous layer (nullable)
+  const int32_t* entry_of;   // [T][K] entry index of (t, j) in y
+  const float* prev_wts;     // [T][K]
+  const uint16_t* gamma;     // [d]
+  const uint16_t* router;    // [E][d] (nullable -> norm only)
+  uint16_t* xn;              // [T][d]
+  int32_t* ids;              // [T][K]
+  float* wts;                // [T][K]
+  float* logits;             // [T][E] (nullable)
+  int32_t* elb_ids;          // [kmax][L][K] (nullable)
+  float* elb_gates;
+  const int32_t* elb_row;    // device row counter
+  int layer, L, d, E, K;
+  float eps;
+};
+
+cudaError_t launch_fill_bf16(uint64_t seed, uint64_t tensor, float scale, int kind, uint16_t* out,
+                             int64_t n, int64_t start, cudaStream_t st);
+cudaError_t launch_fill_expert(uint64_t seed, int cl, int ce, int d, int f, float a_up,
+                               float a_down, uint16_t* blob, cudaStream_t st);
+cudaError_t launch_quantize(const uint16_t* w, int rows, int cols, uint32_t* q, uint16_t* s,
+                            cudaStream_t st);
+cudaError_t launch_embed(const uint16_t* embed, const uint16_t* pos, const int32_t* tokens,
+                         const int32_t* positions, int T, int d, float* h, cudaStream_t st);
+cudaError_t launch_route(const RouteArgs& a, int T, cudaStream_t st);
+cudaError_t launch_build_schedule(const int32_t* ids, int T, int K, int E, SchedPtrs s,
+                                  cudaStream_t st);
+cudaError_t launch_expert(const ExpertArgs& a, bool int4, int max_groups, cudaStream_t st);
+cudaError_t launch_lm_head(const uint16_t* xn, const uint16_t* lm, int T, int V, int d,
+                           float* logits, cudaStream_t st);
+cudaError_t launch_argmax(const float* logits, int T, int V, int32_t* out, DraftState ds,
+                          cudaStream_t st);
+cudaError_t launch_accept(const int32_t* draft, const int32_t* tgt, int k, int32_t* res,
+                          int32_t* cur_tok, int32_t* cur_pos, int head_pos, cudaStream_t st);
+
+}  // namespace mspq

@@ -1,0 +1,580 @@
+// MoE decode math on sm_100a: weight init, INT4 (GPTQ-sym g128) quantisation, embedding,
+// fused residual-combine + RMSNorm + router + top-k/softmax (K1), grouped expert FFN for the
+// INT4 draft (K2) and the bf16 verify (K3), LM head + argmax, accept/reject scan (K5).
+//
+// Layouts:
+//   bf16 expert blob  : W13[2f][d] rows interleaved (2i = gate_i, 2i+1 = up_i) ++ W2[d][f]
+//   int4 expert blob  : W13q[2f][d/8] u32 | W13s[2f][d/128] bf16 | W2q[d][f/8] u32 | W2s[d][f/128] bf16
+//                       nibble n of word w = column 8w+n, value q in [0,15], weight = (q-8)*s
+//   schedule          : groups in ascending expert order, entries (= (token, k-slot) pairs) in
+//                       window order inside a group -- reorder_verification (scheduler.cpp:339-357)
+#include "common.cuh"
+#include "kernels.h"
+
+namespace mspq {
+
+// ============================================================================ init
+__global__ void k_fill_bf16(uint64_t key, float scale, int kind, uint16_t* __restrict__ out,
+                            int64_t n, int64_t start) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float v = unit_val(key, (uint64_t)(start + i));
+    float w = kind == 0 ? __fmul_rn(v, scale) : __fadd_rn(1.0f, __fmul_rn(v, 0.125f));
+    out[i] = f2bf(w);
+  }
+}
+
+// One expert's bf16 blob (interleaved W13 + W2) straight from the counter hash.
+__global__ void k_fill_expert(uint64_t seed, int cl, int ce, int d, int f, float a_up,
+                              float a_down, uint16_t* __restrict__ blob) {
+  const uint64_t kg = tensor_key(seed, t_expert(cl, ce, 0));
+  const uint64_t ku = tensor_key(seed, t_expert(cl, ce, 1));
+  const uint64_t kd = tensor_key(seed, t_expert(cl, ce, 2));
+  const int64_t n13 = (int64_t)2 * f * d, n2 = (int64_t)d * f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n13 + n2;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float v;
+    if (i < n13) {
+      int64_t r = i / d, c = i - r * d;
+      int64_t row = r >> 1;
+      v = __fmul_rn(unit_val((r & 1) ? ku : kg, (uint64_t)(row * d + c)), a_up);
+    } else {
+      v = __fmul_rn(unit_val(kd, (uint64_t)(i - n13)), a_down);
+    }
+    blob[i] = f2bf(v);
+  }
+}
+
+// GPTQ-sym RTN, one warp per (row, 128-column group): lane owns 4 columns.
+__global__ void k_quantize_g128(const uint16_t* __restrict__ w, int rows, int cols,
+                                uint32_t* __restrict__ q, uint16_t* __restrict__ s) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int groups = cols / 128;
+  if (gw >= (int64_t)rows * groups) return;
+  const int64_t row = gw / groups;
+  const int g = (int)(gw - row * groups);
+  const uint16_t* src = w + row * cols + g * 128 + lane * 4;
+  float v[4];
+  float amax = 0.0f;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    v[j] = bf2f(src[j]);
+    amax = fmaxf(amax, fabsf(v[j]));
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
+  uint16_t sb = f2bf(__fdiv_rn(amax, 7.5f));
+  float sf = bf2f(sb);
+  if (sf == 0.0f) {
+    sb = f2bf(1.0f);
+    sf = 1.0f;
+  }
+  uint32_t nib = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    float qq = __fadd_rn(rintf(__fdiv_rn(v[j], sf)), 8.0f);
+    qq = fminf(fmaxf(qq, 0.0f), 15.0f);
+    nib |= ((uint32_t)qq) << (4 * j);
+  }
+  // lanes 2w, 2w+1 hold the low/high half of packed word w (columns 8w..8w+7)
+  uint32_t other = __shfl_xor_sync(0xffffffffu, nib, 1);
+  if ((lane & 1) == 0) q[row * (cols / 8) + g * 16 + (lane >> 1)] = nib | (other << 16);
+  if (lane == 0) s[row * groups + g] = sb;
+}
+
+// ============================================================================ embedding
+__global__ void k_embed(const uint16_t* __restrict__ embed, const uint16_t* __restrict__ pos,
+                        const int32_t* __restrict__ tokens, const int32_t* __restrict__ positions,
+                        int d, float* __restrict__ h) {
+  const int t = blockIdx.x;
+  const int64_t tok = tokens[t], p = positions[t];
+  for (int i = threadIdx.x; i < d; i += blockDim.x)
+    h[(int64_t)t * d + i] = __fadd_rn(bf2f(embed[tok * d + i]), bf2f(pos[p * d + i]));
+}
+
+// ============================================================================ K1
+// One CTA (256 threads) per token.  (1) optional residual combine h += sum_j w_j*y_j in
+// k-slot order; (2) fixed-order sum of squares (thread t owns float4 chunks t, t+256, ...);
+// (3) xn = bf16((h*r)*gamma); (4) router logits by fixed-order warp dots; (5) top-k (desc,
+// tie -> lower id) + softmax over the selection with det_exp.  Writes ids/wts, optional logits,
+// optional ELB row (ids + raw gates) at *elb_row.
+
+
+__global__ void __launch_bounds__(256) k_resid_norm_route(RouteArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint16_t* xs = reinterpret_cast<uint16_t*>(smem_raw);                  // d bf16
+  float* lg = reinterpret_cast<float*>(smem_raw + a.d * 2);              // E floats
+  __shared__ float part[8];
+  __shared__ float rscale;
+  const int t = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float* h = a.h + (int64_t)t * a.d;
+  const int nch = a.d >> 2;
+  float acc = 0.0f;
+  for (int c = tid; c < nch; c += 256) {
+    float4 hv = reinterpret_cast<float4*>(h)[c];
+    if (a.y) {
+      float v[4] = {hv.x, hv.y, hv.z, hv.w};
+      float cb[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int j = 0; j < a.K; ++j) {
+        const float w = a.prev_wts[t * a.K + j];
+        const float4 yv = reinterpret_cast<const float4*>(a.y + (int64_t)a.entry_of[t * a.K + j] * a.d)[c];
+        cb[0] = __fadd_rn(cb[0], __fmul_rn(w, yv.x));
+        cb[1] = __fadd_rn(cb[1], __fmul_rn(w, yv.y));
+        cb[2] = __fadd_rn(cb[2], __fmul_rn(w, yv.z));
+        cb[3] = __fadd_rn(cb[3], __fmul_rn(w, yv.w));
+      }
+      hv = make_float4(__fadd_rn(v[0], cb[0]), __fadd_rn(v[1], cb[1]), __fadd_rn(v[2], cb[2]),
+                       __fadd_rn(v[3], cb[3]));
+      reinterpret_cast<float4*>(h)[c] = hv;
+    }
+    acc = fmaf(hv.x, hv.x, acc);
+    acc = fmaf(hv.y, hv.y, acc);
+    acc = fmaf(hv.z, hv.z, acc);
+    acc = fmaf(hv.w, hv.w, acc);
+  }
+  acc = warp_butterfly_sum(acc);
+  if (lane == 0) part[warp] = acc;
+  __syncthreads();
+  if (tid == 0) {
+    float tot = part[0];
+    for (int w = 1; w < 8; ++w) tot = __fadd_rn(tot, part[w]);
+    float ms = __fdiv_rn(tot, (float)a.d);
+    rscale = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(ms, a.eps)));
+  }
+  __syncthreads();
+  const float r = rscale;
+  for (int c = tid; c < nch; c += 256) {
+    float4 hv = reinterpret_cast<float4*>(h)[c];
+    float v[4] = {hv.x, hv.y, hv.z, hv.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int i = 4 * c + e;
+      uint16_t b = f2bf(__fmul_rn(__fmul_rn(v[e], r), bf2f(a.gamma[i])));
+      xs[i] = b;
+      a.xn[(int64_t)t * a.d + i] = b;
+    }
+  }
+  if (!a.router) return;
+  __syncthreads();
+  for (int e = warp; e < a.E; e += 8) {
+    float z = warp_dot_bf16(xs, a.router + (int64_t)e * a.d, a.d, lane);
+    if (lane == 0) lg[e] = z;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int sel[64];
+    for (int j = 0; j < a.K; ++j) {
+      int best = -1;
+      for (int e = 0; e < a.E; ++e) {
+        bool used = false;
+        for (int q = 0; q < j; ++q) used |= (sel[q] == e);
+        if (used) continue;
+        if (best < 0 || lg[e] > lg[best]) best = e;
+      }
+      sel[j] = best;
+    }
+    const float m = lg[sel[0]];
+    float ex[64], s = 0.0f;
+    for (int j = 0; j < a.K; ++j) {
+      ex[j] = det_exp(__fsub_rn(lg[sel[j]], m));
+      s = __fadd_rn(s, ex[j]);
+    }
+    const int row = a.elb_ids ? *a.elb_row : 0;
+    for (int j = 0; j < a.K; ++j) {
+      const float w = __fdiv_rn(ex[j], s);
+      a.ids[t * a.K + j] = sel[j];
+      a.wts[t * a.K + j] = w;
+      if (a.elb_ids) {
+        const int64_t o = ((int64_t)row * a.L + a.layer) * a.K + j;
+        a.elb_ids[o] = sel[j];
+        a.elb_gates[o] = w;
+      }
+    }
+    if (a.logits)
+      for (int e = 0; e < a.E; ++e) a.logits[(int64_t)t * a.E + e] = lg[e];
+  }
+}
+
+// ============================================================================ schedule
+// Groups (token, k-slot) entries by expert, ascending expert id, window order inside a group
+// (reorder_verification, scheduler.cpp:339-357).  Used for the draft; the verify schedule is
+// built by the cache controller (it also assigns HBM buffers).
+__global__ void k_build_schedule(const int32_t* __restrict__ ids, int T, int K, int E,
+                                 SchedPtrs s) {
+  if (threadIdx.x != 0) return;
+  int g = 0, n = 0;
+  for (int e = 0; e < E; ++e) {
+    int start = n;
+    for (int t = 0; t < T; ++t)
+      for (int j = 0; j < K; ++j)
+        if (ids[t * K + j] == e) {
+          s.entry_tok[n] = t;
+          s.entry_of[t * K + j] = n;
+          ++n;
+        }
+    if (n > start) {
+      s.group_expert[g] = e;
+      s.group_buf[g] = e;
+      s.group_off[g] = start;
+      ++g;
+    }
+  }
+  s.group_off[g] = n;
+  *s.n_groups = g;
+}
+
+// ============================================================================ K2 / K3
+// Grouped expert GEMV on CUDA cores (v0).  One CTA = 8 warps; warp owns RPW output rows of one
+// group's expert for all of that group's entries (<= MT).  MODE 0: up/gate (interleaved rows,
+// SiLU*up epilogue -> bf16 act [entry][f]); MODE 1: down (-> fp32 y [entry][d]).
+template <int MODE, bool INT4, int RPW, int MT>
+__device__ __forceinline__ void grouped_rows_body(const ExpertArgs& a, int g, int m, int e0,
+                                                  const unsigned char* blob, int row0) {
+  const int lane = threadIdx.x & 31;
+  const int cols = MODE == 0 ? a.d : a.f;
+  constexpr int PR = MODE == 0 ? 2 * RPW : RPW;  // physical rows per warp
+  // weight pointers
+  const unsigned char* wq;
+  const uint16_t* ws;
+  const uint16_t* wb;
+  if (INT4) {
+    const int64_t q13 = (int64_t)2 * a.f * a.d / 2, s13 = (int64_t)2 * a.f * (a.d / 128) * 2;
+    const int64_t q2 = (int64_t)a.d * a.f / 2;
+    wq = blob + (MODE == 0 ? 0 : q13 + s13);
+    ws = reinterpret_cast<const uint16_t*>(blob + (MODE == 0 ? q13 : q13 + s13 + q2));
+    wb = nullptr;
+  } else {
+    wb = reinterpret_cast<const uint16_t*>(blob) + (MODE == 0 ? 0 : (int64_t)2 * a.f * a.d);
+    wq = nullptr;
+    ws = nullptr;
+  }
+  const int prow0 = MODE == 0 ? 2 * row0 : row0;
+  float acc[PR][MT];
+#pragma unroll
+  for (int r = 0; r < PR; ++r)
+#pragma unroll
+    for (int t = 0; t < MT; ++t) acc[r][t] = 0.0f;
+
+  if (!INT4) {
+    const int nch = cols >> 3;
+#pragma unroll 2
+    for (int c = lane; c < nch; c += 32) {
+      float wf[PR][8];
+#pragma unroll
+      for (int r = 0; r < PR; ++r) {
+        uint4 wv = ldg_nc_v4(wb + (int64_t)(prow0 + r) * cols + 8 * c);
+        bf16x8_to_f32(wv, wf[r]);
+      }
+#pragma unroll
+      for (int t = 0; t < MT; ++t) {
+        if (t < m) {
+          const uint16_t* xp = MODE == 0 ? a.xn + (int64_t)a.s.entry_tok[e0 + t] * a.d
+                                         : a.act + (int64_t)(e0 + t) * a.f;
+          uint4 xv = *reinterpret_cast<const uint4*>(xp + 8 * c);
+          float xf[8];
+          bf16x8_to_f32(xv, xf);
+#pragma unroll
+          for (int r = 0; r < PR; ++r)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[r][t] = fmaf(wf[r][e], xf[e], acc[r][t]);
+        }
+      }
+    }
+  } else {
+    const int nch = cols >> 5;  // 32 columns per 16-byte word group
+    const int ngr = cols >> 7;
+#pragma unroll 2
+    for (int c = lane; c < nch; c += 32) {
+      uint4 wv[PR];
+      float sc[PR];
+#pragma unroll
+      for (int r = 0; r < PR; ++r) {
+        wv[r] = ldg_nc_v4(wq + ((int64_t)(prow0 + r) * cols + 32 * c) / 2);
+        sc[r] = bf2f(ws[(int64_t)(prow0 + r) * ngr + (c >> 2)]);
+      }
+#pragma unroll
+      for (int t = 0; t < MT; ++t) {
+        if (t < m) {
+          const uint16_t* xp = MODE == 0 ? a.xn + (int64_t)a.s.entry_tok[e0 + t] * a.d
+                                         : a.act + (int64_t)(e0 + t) * a.f;
+          float xf[32];
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            uint4 xv = *reinterpret_cast<const uint4*>(xp + 32 * c + 8 * v);
+            bf16x8_to_f32(xv, xf + 8 * v);
+          }
+#pragma unroll
+          for (int r = 0; r < PR; ++r) {
+            float p = 0.0f;
+            const uint32_t wr[4] = {wv[r].x, wv[r].y, wv[r].z, wv[r].w};
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+#pragma unroll
+              for (int n = 0; n < 8; ++n) {
+                const float qf = __uint_as_float(0x4B000000u | ((wr[v] >> (4 * n)) & 0xFu)) - 8388616.0f;
+                p = fmaf(qf, xf[8 * v + n], p);
+              }
+            acc[r][t] = fmaf(p, sc[r], acc[r][t]);
+          }
+        }
+      }
+    }
+  }
+  // reduce & epilogue
+#pragma unroll
+  for (int r = 0; r < PR; ++r)
+#pragma unroll
+    for (int t = 0; t < MT; ++t) acc[r][t] = warp_butterfly_sum(acc[r][t]);
+  if (lane == 0) {
+#pragma unroll
+    for (int t = 0; t < MT; ++t) {
+      if (t < m) {
+        if (MODE == 0) {
+#pragma unroll
+          for (int r = 0; r < RPW; ++r) {
+            const float gv = acc[2 * r][t], uv = acc[2 * r + 1][t];
+            a.act[(int64_t)(e0 + t) * a.f + row0 + r] = f2bf(__fmul_rn(silu_det(gv), uv));
+          }
+        } else {
+#pragma unroll
+          for (int r = 0; r < RPW; ++r) a.y[(int64_t)(e0 + t) * a.d + row0 + r] = acc[r][t];
+        }
+      }
+    }
+  }
+}
+
+template <int MODE, bool INT4, int RPW>
+__global__ void __launch_bounds__(256) k_grouped_rows(ExpertArgs a) {
+  const int g = blockIdx.y;
+  if (g >= *a.s.n_groups) return;
+  const int e0 = a.s.group_off[g];
+  const int m = a.s.group_off[g + 1] - e0;
+  const int warp = threadIdx.x >> 5;
+  const int row0 = (blockIdx.x * 8 + warp) * RPW;
+  const int nrows = MODE == 0 ? a.f : a.d;
+  if (row0 >= nrows) return;
+  const unsigned char* blob;
+  if (INT4)
+    blob = a.w_base + ((int64_t)a.layer * a.E + a.s.group_expert[g]) * a.blob_bytes;
+  else
+    blob = a.w_base + (int64_t)a.s.group_buf[g] * a.blob_bytes;
+  for (int base = 0; base < m; base += 16) {
+    const int mm = min(16, m - base);
+    if (mm == 1)
+      grouped_rows_body<MODE, INT4, RPW, 1>(a, g, 1, e0 + base, blob, row0);
+    else if (mm <= 2)
+      grouped_rows_body<MODE, INT4, RPW, 2>(a, g, mm, e0 + base, blob, row0);
+    else if (mm <= 4)
+      grouped_rows_body<MODE, INT4, RPW, 4>(a, g, mm, e0 + base, blob, row0);
+    else if (mm <= 8)
+      grouped_rows_body<MODE, INT4, RPW, 8>(a, g, mm, e0 + base, blob, row0);
+    else
+      grouped_rows_body<MODE, INT4, RPW, 16>(a, g, mm, e0 + base, blob, row0);
+  }
+}
+
+// ============================================================================ LM head
+// logits[t][v] by the same fixed-order warp dot as the router; one warp owns RPW vocab rows
+// for all T tokens.
+template <int RPW>
+__global__ void __launch_bounds__(256) k_lm_head(const uint16_t* __restrict__ xn,
+                                                 const uint16_t* __restrict__ lm, int T, int V,
+                                                 int d, float* __restrict__ logits) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int v0 = (blockIdx.x * 8 + warp) * RPW;
+  if (v0 >= V) return;
+  const int nch = d >> 3;
+  for (int t0 = 0; t0 < T; t0 += 4) {
+    float acc[RPW][4];
+#pragma unroll
+    for (int r = 0; r < RPW; ++r)
+#pragma unroll
+      for (int t = 0; t < 4; ++t) acc[r][t] = 0.0f;
+    for (int c = lane; c < nch; c += 32) {
+      float wf[RPW][8];
+#pragma unroll
+      for (int r = 0; r < RPW; ++r) {
+        if (v0 + r < V) {
+          uint4 wv = ldg_nc_v4(lm + (int64_t)(v0 + r) * d + 8 * c);
+          bf16x8_to_f32(wv, wf[r]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) wf[r][e] = 0.0f;
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        if (t0 + t < T) {
+          uint4 xv = *reinterpret_cast<const uint4*>(xn + (int64_t)(t0 + t) * d + 8 * c);
+          float xf[8];
+          bf16x8_to_f32(xv, xf);
+#pragma unroll
+          for (int r = 0; r < RPW; ++r)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[r][t] = fmaf(xf[e], wf[r][e], acc[r][t]);
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RPW; ++r)
+#pragma unroll
+      for (int t = 0; t < 4; ++t) acc[r][t] = warp_butterfly_sum(acc[r][t]);
+    if (lane == 0)
+      for (int r = 0; r < RPW; ++r)
+        for (int t = 0; t < 4; ++t)
+          if (v0 + r < V && t0 + t < T) logits[(int64_t)(t0 + t) * V + v0 + r] = acc[r][t];
+  }
+}
+
+// argmax per token (tie -> lower id); optionally advances the draft state:
+// draft_toks[*row] = tok, *cur_tok = tok, *cur_pos += 1, *row += 1.
+__global__ void __launch_bounds__(1024) k_argmax(const float* __restrict__ logits, int V,
+                                                 int32_t* __restrict__ out, DraftState ds) {
+  const int t = blockIdx.x;
+  const float* lg = logits + (int64_t)t * V;
+  float best = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int v = threadIdx.x; v < V; v += blockDim.x) {
+    const float z = lg[v];
+    if (z > best || (z == best && v < bi)) {
+      best = z;
+      bi = v;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const float ob = __shfl_xor_sync(0xffffffffu, best, off);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+    if (ob > best || (ob == best && oi < bi)) {
+      best = ob;
+      bi = oi;
+    }
+  }
+  __shared__ float sb[32];
+  __shared__ int si[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    sb[warp] = best;
+    si[warp] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int nw = blockDim.x >> 5;
+    for (int w = 1; w < nw; ++w)
+      if (sb[w] > best || (sb[w] == best && si[w] < bi)) {
+        best = sb[w];
+        bi = si[w];
+      }
+    out[t] = bi;
+    if (ds.row) {
+      const int r = *ds.row;
+      ds.draft_toks[r] = bi;
+      *ds.cur_tok = bi;
+      *ds.cur_pos += 1;
+      *ds.row = r + 1;
+    }
+  }
+}
+
+// ============================================================================ K5
+// Greedy verification (sim.cpp:352-365 on token ids): window slot i's target argmax predicts
+// slot i+1; accepted = longest prefix with draft[i] == tgt[i]; bonus = tgt[accepted].
+// Writes res = {accepted, bonus} and, for the next cycle, the head token/position.
+__global__ void k_accept_scan(const int32_t* __restrict__ draft, const int32_t* __restrict__ tgt,
+                              int k, int32_t* __restrict__ res, int32_t* cur_tok,
+                              int32_t* cur_pos, int head_pos) {
+  if (threadIdx.x != 0) return;
+  int acc = 0;
+  while (acc < k && draft[acc] == tgt[acc]) ++acc;
+  res[0] = acc;
+  res[1] = tgt[acc];
+  if (cur_tok) {
+    *cur_tok = tgt[acc];
+    *cur_pos = head_pos + acc + 1;
+  }
+}
+
+// ============================================================================ launchers
+cudaError_t launch_fill_bf16(uint64_t seed, uint64_t tensor, float scale, int kind, uint16_t* out,
+                             int64_t n, int64_t start, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  k_fill_bf16<<<blocks, 256, 0, st>>>(tensor_key(seed, tensor), scale, kind, out, n, start);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_expert(uint64_t seed, int cl, int ce, int d, int f, float a_up,
+                               float a_down, uint16_t* blob, cudaStream_t st) {
+  k_fill_expert<<<148 * 8, 256, 0, st>>>(seed, cl, ce, d, f, a_up, a_down, blob);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_quantize(const uint16_t* w, int rows, int cols, uint32_t* q, uint16_t* s,
+                            cudaStream_t st) {
+  int64_t warps = (int64_t)rows * (cols / 128);
+  int64_t blocks = (warps * 32 + 255) / 256;
+  k_quantize_g128<<<(unsigned)blocks, 256, 0, st>>>(w, rows, cols, q, s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_embed(const uint16_t* embed, const uint16_t* pos, const int32_t* tokens,
+                         const int32_t* positions, int T, int d, float* h, cudaStream_t st) {
+  k_embed<<<T, 256, 0, st>>>(embed, pos, tokens, positions, d, h);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_route(const RouteArgs& a, int T, cudaStream_t st) {
+  size_t smem = (size_t)a.d * 2 + (size_t)a.E * 4;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_resid_norm_route, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_resid_norm_route<<<T, 256, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_build_schedule(const int32_t* ids, int T, int K, int E, SchedPtrs s,
+                                  cudaStream_t st) {
+  k_build_schedule<<<1, 32, 0, st>>>(ids, T, K, E, s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_expert(const ExpertArgs& a, bool int4, int max_groups, cudaStream_t st) {
+  constexpr int RPW0 = 2, RPW1 = 4;
+  {
+    dim3 grid((a.f + 8 * RPW0 - 1) / (8 * RPW0), max_groups);
+    if (int4)
+      k_grouped_rows<0, true, RPW0><<<grid, 256, 0, st>>>(a);
+    else
+      k_grouped_rows<0, false, RPW0><<<grid, 256, 0, st>>>(a);
+  }
+  {
+    dim3 grid((a.d + 8 * RPW1 - 1) / (8 * RPW1), max_groups);
+    if (int4)
+      k_grouped_rows<1, true, RPW1><<<grid, 256, 0, st>>>(a);
+    else
+      k_grouped_rows<1, false, RPW1><<<grid, 256, 0, st>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lm_head(const uint16_t* xn, const uint16_t* lm, int T, int V, int d,
+                           float* logits, cudaStream_t st) {
+  constexpr int RPW = 4;
+  k_lm_head<RPW><<<(V + 8 * RPW - 1) / (8 * RPW), 256, 0, st>>>(xn, lm, T, V, d, logits);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_argmax(const float* logits, int T, int V, int32_t* out, DraftState ds,
+                          cudaStream_t st) {
+  k_argmax<<<T, 1024, 0, st>>>(logits, V, out, ds);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_accept(const int32_t* draft, const int32_t* tgt, int k, int32_t* res,
+                          int32_t* cur_tok, int32_t* cur_pos, int head_pos, cudaStream_t st) {
+  k_accept_scan<<<1, 32, 0, st>>>(draft, tgt, k, res, cur_tok, cur_pos, head_pos);
+  return cudaGetLastError();
+}
+
+}  // namespace mspq

@@ -1,0 +1,928 @@
+// Live speculative decode engine (the generate() drop-in next to run_simulation, sim.hpp:86).
+//
+// Per cycle:
+//   governor: k = select_k(profile re-fit on this B200, EMA acceptance, g)   perfmodel.cpp:166-183
+//   draft:    k replays of a captured CUDA graph (embed -> L x [K1 gate/top-k + ELB row -> K2
+//             INT4 grouped FFN] -> norm -> LM head -> argmax/advance); after each row the device
+//             planner (K4 plan_row) decides Phase-II/III prefetches; the host issues those H2D
+//             copies on the copy-engine stream while the next draft row runs.
+//   verify:   layer-major over the k+1 window slots: K1 (target routing) -> K4 verify_layer
+//             (refill / demand policy steps, slot-pool buffers, grouped-GEMM schedule) -> demand
+//             H2D -> wait on the copies this layer's experts need (= exposed stall) -> K3 bf16
+//             grouped FFN -> ... -> LM head -> argmax -> K5 accept/advance.
+//   record:   CycleRecord in the reference schema (sim.cpp:468-510) with measured times.
+#include <cuda_runtime.h>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <set>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/mspq_capi.h"
+#include "json.hpp"
+#include "status.h"
+
+using json = nlohmann::ordered_json;
+
+#include "host_common.h"
+
+using namespace mspq_host;
+
+#define CUDA_OK(x)                                                                                  \
+  do {                                                                                              \
+    cudaError_t _e = (x);                                                                           \
+    if (_e != cudaSuccess) fail(MSPQ_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(_e));   \
+  } while (0)
+#define CAPI_OK(x)                                                     \
+  do {                                                                 \
+    int _s = (x);                                                      \
+    if (_s) fail(_s, std::string(#x) + ": " + mspq_last_error());      \
+  } while (0)
+
+namespace {
+
+enum : int { S_TOTAL = 0, S_NFREE, S_NPEND, S_K, S_T1, S_T2, S_NREQ, S_NLOG, S_NPLAN, S_FETCHED, S_DEMAND, S_JIT, S_OVERFLOW };
+
+struct Sched {
+  int32_t* base = nullptr;
+  int32_t *n_groups, *group_expert, *group_buf, *group_off, *entry_tok, *entry_of;
+  void carve(int32_t* p, int G, int N) {
+    base = p;
+    n_groups = p;
+    group_expert = p + 4;
+    group_buf = group_expert + G;
+    group_off = group_buf + G;
+    entry_tok = group_off + G + 1;
+    entry_of = entry_tok + N;
+  }
+  static size_t ints(int G, int N) { return 4 + 3 * (size_t)G + 1 + 2 * (size_t)N + 8; }
+};
+
+double elapsed_s(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms * 1e-3;
+}
+
+}  // namespace
+
+struct mspq_engine {
+  mspq_model_desc m{};
+  mspq_engine_opts o{};
+  std::string store_path;
+  cudaStream_t sc = nullptr, sx = nullptr;
+  int64_t S16 = 0, S4 = 0;
+  int Tmax = 0, G = 0, N = 0;
+  // device weights
+  void* wblk = nullptr;
+  uint16_t *embed = nullptr, *pos = nullptr, *lm = nullptr, *gfinal = nullptr, *gamma = nullptr, *router = nullptr;
+  unsigned char* draft4 = nullptr;
+  // host store
+  unsigned char* host = nullptr;
+  size_t host_bytes = 0;
+  int n_payload = 0;
+  bool host_is_shm = false;
+  // slot pool
+  unsigned char* pool = nullptr;
+  int nbuf = 0;
+  mspq_cache* cache = nullptr;
+  mspq_cache_view view{};
+  // workspaces
+  void* ws = nullptr;
+  float* h = nullptr;
+  uint16_t* xn = nullptr;
+  int32_t* ids_t = nullptr;
+  float* wts_t = nullptr;
+  int32_t* ids_d = nullptr;
+  float* wts_d = nullptr;
+  Sched sv[2], sd[2];
+  float *yv[2] = {nullptr, nullptr}, *yd[2] = {nullptr, nullptr};
+  uint16_t* act = nullptr;
+  float* logits = nullptr;
+  int32_t* amax = nullptr;
+  int32_t* dst = nullptr;  // device state: [0] row [1] cur_tok [2] cur_pos [3] accepted [4] bonus [8..] win_tok [8+Tmax+1..] win_pos
+  int32_t* hpin = nullptr;  // pinned host mirror for small transfers
+  size_t hpin_ints = 0;
+  // draft graph
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  // copy bookkeeping
+  std::vector<cudaEvent_t> ev_ready;
+  std::vector<char> ready_rec;
+  std::vector<int> last_cycle, last_layer;
+  std::vector<cudaEvent_t> ev_gemm, ev_w0, ev_w1, ev_row;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_pool_next = 0;
+  cudaEvent_t ev_c0 = nullptr, ev_dend = nullptr, ev_end = nullptr, ev_t0 = nullptr;
+  // config
+  bool configured = false;
+  HostCfg cfg;
+  std::vector<int> caps;
+  double pcie_bw_measured = 0.0, draft_step_s = 0.0;
+  std::vector<std::pair<double, double>> verify_fit;
+  int cycle_serial = 0;
+
+  int32_t* win_tok() { return dst + 8; }
+  int32_t* win_pos() { return dst + 8 + Tmax + 1; }
+  int64_t payload(int key) const { return m.unique_experts > 0 ? key % m.unique_experts : key; }
+
+  cudaEvent_t pool_event() {
+    if (ev_pool_next >= ev_pool.size()) {
+      cudaEvent_t e;
+      CUDA_OK(cudaEventCreate(&e));
+      ev_pool.push_back(e);
+    }
+    return ev_pool[ev_pool_next++];
+  }
+};
+
+namespace {
+
+void make_weights(mspq_engine* E) {
+  const auto& m = E->m;
+  const int64_t d = m.d;
+  size_t n_embed = (size_t)m.V * d, n_pos = (size_t)m.P * d, n_lm = n_embed, n_g = (size_t)(m.L + 1) * d,
+         n_r = (size_t)m.L * m.E * d;
+  size_t total = (n_embed + n_pos + n_lm + n_g + n_r) * 2;
+  CUDA_OK(cudaMalloc(&E->wblk, total));
+  uint16_t* p = (uint16_t*)E->wblk;
+  E->embed = p;
+  p += n_embed;
+  E->pos = p;
+  p += n_pos;
+  E->lm = p;
+  p += n_lm;
+  E->gamma = p;
+  p += (size_t)m.L * d;
+  E->gfinal = p;
+  p += d;
+  E->router = p;
+  void* s = E->sc;
+  CAPI_OK(mspq_fill_bf16(m.seed, 1, m.embed_scale, 0, E->embed, (long long)n_embed, 0, s));
+  CAPI_OK(mspq_fill_bf16(m.seed, 2, m.pos_scale, 0, E->pos, (long long)n_pos, 0, s));
+  CAPI_OK(mspq_fill_bf16(m.seed, 3, m.a_lm, 0, E->lm, (long long)n_lm, 0, s));
+  CAPI_OK(mspq_fill_bf16(m.seed, 4, 0.f, 1, E->gfinal, d, 0, s));
+  for (int l = 0; l < m.L; ++l) {
+    CAPI_OK(mspq_fill_bf16(m.seed, 0x100ull + (uint64_t)l * 16, 0.f, 1, E->gamma + (size_t)l * d, d, 0, s));
+    CAPI_OK(mspq_fill_bf16(m.seed, 0x100ull + (uint64_t)l * 16 + 1, m.a_router, 0, E->router + (size_t)l * m.E * d,
+                           (long long)m.E * d, 0, s));
+  }
+}
+
+void alloc_host_store(mspq_engine* E) {
+  E->host_bytes = (size_t)E->n_payload * E->S16;
+  if (E->store_path.empty()) {
+    CUDA_OK(cudaHostAlloc((void**)&E->host, E->host_bytes, cudaHostAllocPortable));
+    return;
+  }
+  // shared pinned store: a /dev/shm file mapped by every rank and registered with CUDA
+  const bool create = E->o.host_store_role == 0;
+  const std::string ready = E->store_path + ".ready";
+  int fd;
+  if (create) {
+    unlink(ready.c_str());
+    fd = open(E->store_path.c_str(), O_RDWR | O_CREAT | O_TRUNC, 0600);
+    if (fd < 0) fail(MSPQ_ERR_IO, "cannot create host store " + E->store_path);
+    if (ftruncate(fd, (off_t)E->host_bytes) != 0) fail(MSPQ_ERR_IO, "ftruncate host store");
+  } else {
+    for (int i = 0; i < 36000 && access(ready.c_str(), F_OK) != 0; ++i)
+      std::this_thread::sleep_for(std::chrono::milliseconds(50));
+    if (access(ready.c_str(), F_OK) != 0) fail(MSPQ_ERR_IO, "host store never became ready");
+    fd = open(E->store_path.c_str(), O_RDWR);
+    if (fd < 0) fail(MSPQ_ERR_IO, "cannot open host store " + E->store_path);
+  }
+  void* p = mmap(nullptr, E->host_bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  close(fd);
+  if (p == MAP_FAILED) fail(MSPQ_ERR_IO, "mmap host store");
+  E->host = (unsigned char*)p;
+  E->host_is_shm = true;
+  CUDA_OK(cudaHostRegister(E->host, E->host_bytes, cudaHostRegisterPortable));
+}
+
+// Generates every expert once on the GPU: bf16 blob -> pinned host store (payload) and the
+// INT4 draft of every key that maps to it.
+void make_experts(mspq_engine* E) {
+  const auto& m = E->m;
+  const int LE = m.L * m.E;
+  const int64_t S16 = E->S16, S4 = E->S4;
+  CUDA_OK(cudaMalloc(&E->draft4, (size_t)LE * S4));
+  unsigned char* stage[2];
+  CUDA_OK(cudaMalloc(&stage[0], S16));
+  CUDA_OK(cudaMalloc(&stage[1], S16));
+  const bool fill_host = !(E->host_is_shm && E->o.host_store_role != 0);
+  const int64_t q13 = (int64_t)2 * m.f * m.d / 2, s13 = (int64_t)2 * m.f * (m.d / 128) * 2, q2 = (int64_t)m.d * m.f / 2;
+  for (int p = 0; p < E->n_payload; ++p) {
+    unsigned char* st = stage[p & 1];
+    const int cl = p / m.E, ce = p % m.E;
+    CAPI_OK(mspq_fill_expert(m.seed, cl, ce, m.d, m.f, m.a_up, m.a_down, st, E->sc));
+    for (int key = p; key < LE; key += E->n_payload) {
+      unsigned char* b4 = E->draft4 + (size_t)key * S4;
+      CAPI_OK(mspq_quantize_int4(st, 2 * m.f, m.d, b4, b4 + q13, E->sc));
+      CAPI_OK(mspq_quantize_int4(st + (size_t)2 * m.f * m.d * 2, m.d, m.f, b4 + q13 + s13, b4 + q13 + s13 + q2, E->sc));
+    }
+    if (fill_host) CUDA_OK(cudaMemcpyAsync(E->host + (size_t)p * S16, st, S16, cudaMemcpyDeviceToHost, E->sc));
+  }
+  CUDA_OK(cudaStreamSynchronize(E->sc));
+  cudaFree(stage[0]);
+  cudaFree(stage[1]);
+  if (E->host_is_shm && E->o.host_store_role == 0) {
+    const std::string ready = E->store_path + ".ready";
+    int fd = open(ready.c_str(), O_WRONLY | O_CREAT, 0600);
+    if (fd >= 0) close(fd);
+  }
+}
+
+void make_workspaces(mspq_engine* E) {
+  const auto& m = E->m;
+  const int T = E->Tmax, K = m.K, L = m.L, d = m.d, f = m.f;
+  E->G = std::min(m.E, T * K);
+  E->N = T * K;
+  const size_t sched_ints = Sched::ints(E->G, E->N);
+  size_t off = 0;
+  auto take = [&](size_t b) {
+    size_t o = off;
+    off += (b + 255) & ~size_t(255);
+    return o;
+  };
+  size_t o_h = take((size_t)T * d * 4), o_xn = take((size_t)T * d * 2), o_it = take((size_t)L * T * K * 4),
+         o_wt = take((size_t)L * T * K * 4), o_id = take((size_t)L * K * 4), o_wd = take((size_t)L * K * 4),
+         o_sv0 = take(sched_ints * 4), o_sv1 = take(sched_ints * 4), o_sd0 = take(Sched::ints(K, K) * 4),
+         o_sd1 = take(Sched::ints(K, K) * 4), o_yv0 = take((size_t)E->N * d * 4), o_yv1 = take((size_t)E->N * d * 4),
+         o_yd0 = take((size_t)K * d * 4), o_yd1 = take((size_t)K * d * 4), o_act = take((size_t)E->N * f * 2),
+         o_lg = take((size_t)T * m.V * 4), o_am = take((size_t)T * 4), o_dst = take((size_t)(8 + 2 * (T + 1)) * 4);
+  CUDA_OK(cudaMalloc(&E->ws, off));
+  CUDA_OK(cudaMemset(E->ws, 0, off));
+  char* b = (char*)E->ws;
+  E->h = (float*)(b + o_h);
+  E->xn = (uint16_t*)(b + o_xn);
+  E->ids_t = (int32_t*)(b + o_it);
+  E->wts_t = (float*)(b + o_wt);
+  E->ids_d = (int32_t*)(b + o_id);
+  E->wts_d = (float*)(b + o_wd);
+  E->sv[0].carve((int32_t*)(b + o_sv0), E->G, E->N);
+  E->sv[1].carve((int32_t*)(b + o_sv1), E->G, E->N);
+  E->sd[0].carve((int32_t*)(b + o_sd0), K, K);
+  E->sd[1].carve((int32_t*)(b + o_sd1), K, K);
+  E->yv[0] = (float*)(b + o_yv0);
+  E->yv[1] = (float*)(b + o_yv1);
+  E->yd[0] = (float*)(b + o_yd0);
+  E->yd[1] = (float*)(b + o_yd1);
+  E->act = (uint16_t*)(b + o_act);
+  E->logits = (float*)(b + o_lg);
+  E->amax = (int32_t*)(b + o_am);
+  E->dst = (int32_t*)(b + o_dst);
+  E->hpin_ints = 64 + (size_t)L * T * K * 2 + (size_t)E->Tmax * L * K * 2 + 4 * T + (size_t)L * 2 + (size_t)L * T * 2 + 64;
+  CUDA_OK(cudaHostAlloc((void**)&E->hpin, E->hpin_ints * 4, 0));
+}
+
+// One draft step for a single token, captured once as a CUDA graph.
+void enqueue_draft_step(mspq_engine* E, cudaStream_t s) {
+  const auto& m = E->m;
+  const int K = m.K, L = m.L, d = m.d;
+  int32_t* row = E->dst + 0;
+  int32_t* cur_tok = E->dst + 1;
+  int32_t* cur_pos = E->dst + 2;
+  CAPI_OK(mspq_embed(E->embed, E->pos, cur_tok, cur_pos, 1, d, E->h, s));
+  for (int l = 0; l < L; ++l) {
+    const int pl = (l - 1) & 1;
+    CAPI_OK(mspq_gate_topk(E->h, l ? E->yd[pl] : nullptr, l ? E->sd[pl].entry_of : nullptr,
+                           l ? E->wts_d + (size_t)(l - 1) * K : nullptr, E->gamma + (size_t)l * d,
+                           E->router + (size_t)l * m.E * d, E->xn, E->ids_d + (size_t)l * K, E->wts_d + (size_t)l * K,
+                           nullptr, E->view.elb_ids, E->view.elb_gates, row, l, L, 1, d, m.E, K, m.eps, s));
+    Sched& sc = E->sd[l & 1];
+    CAPI_OK(mspq_build_schedule(E->ids_d + (size_t)l * K, 1, K, m.E, sc.n_groups, sc.group_expert, sc.group_buf,
+                                sc.group_off, sc.entry_tok, sc.entry_of, s));
+    CAPI_OK(mspq_moe_int4(sc.n_groups, sc.group_expert, sc.group_buf, sc.group_off, sc.entry_tok, E->xn, E->act,
+                          E->yd[l & 1], E->draft4, E->S4, l, m.E, d, m.f, K, s));
+  }
+  const int pl = (L - 1) & 1;
+  CAPI_OK(mspq_gate_topk(E->h, E->yd[pl], E->sd[pl].entry_of, E->wts_d + (size_t)(L - 1) * K, E->gfinal, nullptr,
+                         E->xn, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, L, L, 1, d, m.E, K, m.eps, s));
+  CAPI_OK(mspq_lm_head(E->xn, E->lm, 1, m.V, d, E->logits, s));
+  CAPI_OK(mspq_argmax_advance(E->logits, m.V, E->amax, row, E->win_tok() + 1, cur_tok, cur_pos, s));
+}
+
+void capture_draft_graph(mspq_engine* E) {
+  CUDA_OK(cudaStreamBeginCapture(E->sc, cudaStreamCaptureModeThreadLocal));
+  try {
+    enqueue_draft_step(E, E->sc);
+  } catch (...) {
+    cudaGraph_t g;
+    cudaStreamEndCapture(E->sc, &g);
+    throw;
+  }
+  CUDA_OK(cudaStreamEndCapture(E->sc, &E->graph));
+  CUDA_OK(cudaGraphInstantiate(&E->gexec, E->graph, 0));
+}
+
+double measure_pcie(mspq_engine* E) {
+  const size_t bytes = std::min<size_t>(E->S16, 64u << 20);
+  void* dbuf;
+  CUDA_OK(cudaMalloc(&dbuf, bytes));
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  for (int i = 0; i < 2; ++i) CUDA_OK(cudaMemcpyAsync(dbuf, E->host, bytes, cudaMemcpyHostToDevice, E->sx));
+  cudaEventRecord(a, E->sx);
+  for (int i = 0; i < 8; ++i) CUDA_OK(cudaMemcpyAsync(dbuf, E->host, bytes, cudaMemcpyHostToDevice, E->sx));
+  cudaEventRecord(b, E->sx);
+  cudaEventSynchronize(b);
+  const double bw = 8.0 * bytes / elapsed_s(a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(dbuf);
+  return bw;
+}
+
+}  // namespace
+
+// ============================================================================ configure
+static void configure(mspq_engine* E, const std::string& text) {
+  const auto& m = E->m;
+  HostCfg c = parse_host_cfg(text);
+  validate_host_cfg(c, m.K);
+  if (c.entropy_weighted) fail(MSPQ_ERR_INVALID_CONFIG, "entropy_weighted_capacity needs a trace (replay only)");
+  const int kcap = std::max(c.use_governor ? c.k_max : c.fixed_k, 1);
+  if (kcap > E->o.kmax) fail(MSPQ_ERR_K_OUT_OF_RANGE, "k above the engine's kmax");
+  E->caps.assign(m.L, (int)std::min<long>(c.cache_capacity, m.E));
+  const long cap_total = c.mode == 0 ? (long)m.L * std::min<long>(c.cache_capacity, m.E)
+                                     : std::min<long>(c.cache_capacity, (long)m.L * m.E);
+  const int extra = E->o.slot_extra > 0 ? E->o.slot_extra : std::min(m.E, E->Tmax * m.K) + 4;
+  const int nbuf = (int)cap_total + extra;
+  if (nbuf > E->nbuf) {
+    if (E->cache) mspq_cache_destroy(E->cache);
+    if (E->pool) cudaFree(E->pool);
+    E->pool = nullptr;
+    E->cache = nullptr;
+    CUDA_OK(cudaMalloc(&E->pool, (size_t)nbuf * E->S16));
+    E->nbuf = nbuf;
+    CAPI_OK(mspq_cache_create(m.L, m.E, m.K, E->o.kmax, nbuf, E->o.log_cap, &E->cache));
+    CAPI_OK(mspq_cache_view_get(E->cache, &E->view));
+    for (auto ev : E->ev_ready) cudaEventDestroy(ev);
+    E->ev_ready.assign(nbuf, nullptr);
+    for (auto& ev : E->ev_ready) CUDA_OK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    if (E->gexec) {
+      cudaGraphExecDestroy(E->gexec);
+      cudaGraphDestroy(E->graph);
+      E->gexec = nullptr;
+    }
+    capture_draft_graph(E);
+  }
+  E->ready_rec.assign(E->nbuf, 0);
+  E->last_cycle.assign(E->nbuf, -1);
+  E->last_layer.assign(E->nbuf, -1);
+  CAPI_OK(mspq_cache_configure(E->cache, c.mode, c.policy, E->caps.data(), (int)std::min<long>(c.cache_capacity, (long)m.L * m.E),
+                               c.budget, c.f1, c.f2, E->sc));
+  CUDA_OK(cudaStreamSynchronize(E->sc));
+  // ---- HardwareProfile re-fit on this B200 (unless the config pins one)
+  if (E->pcie_bw_measured == 0.0) E->pcie_bw_measured = measure_pcie(E);
+  if (E->draft_step_s == 0.0) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    int32_t init[3] = {0, 0, 0};
+    CUDA_OK(cudaMemcpy(E->dst, init, sizeof(init), cudaMemcpyHostToDevice));
+    for (int i = 0; i < 2; ++i) CUDA_OK(cudaGraphLaunch(E->gexec, E->sc));
+    int32_t z[3] = {0, 0, 0};
+    CUDA_OK(cudaMemcpyAsync(E->dst, z, sizeof(z), cudaMemcpyHostToDevice, E->sc));
+    cudaEventRecord(a, E->sc);
+    for (int i = 0; i < 4; ++i) CUDA_OK(cudaGraphLaunch(E->gexec, E->sc));
+    cudaEventRecord(b, E->sc);
+    CUDA_OK(cudaEventSynchronize(b));
+    E->draft_step_s = elapsed_s(a, b) / 4.0;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+  if (!c.profile_given) {
+    Profile p;
+    p.pcie_bandwidth = E->pcie_bw_measured;
+    p.pcie_init_latency = 0.0;
+    p.pcie_overhead = 10e-6;
+    p.expert_size_bytes = (uint64_t)E->S16;
+    p.draft_base = 0.0;
+    p.draft_per_token = E->draft_step_s;
+    // verify samples from the resident-expert roofline of this model on the measured peaks:
+    // per layer E[union(w)] bf16 experts + router, plus the LM head, at the draft's achieved
+    // bytes/s (the same kernels' streaming rate).
+    const double draft_bytes = (double)m.L * m.K * E->S4 + (double)m.V * m.d * 2 + (double)m.L * m.E * m.d * 2;
+    const double bw = draft_bytes / std::max(E->draft_step_s, 1e-6);
+    p.verify_samples.clear();
+    for (double w : {1.0, 5.0, 9.0, 17.0}) {
+      const double uni = (double)m.E * (1.0 - std::pow(1.0 - (double)m.K / m.E, w));
+      const double bytes = (double)m.L * uni * E->S16 + (double)m.V * m.d * 2 + (double)m.L * m.E * m.d * 2;
+      p.verify_samples.push_back({w, bytes / bw});
+    }
+    c.profile = p;
+  }
+  E->cfg = c;
+  E->configured = true;
+}
+
+// ============================================================================ generate
+struct CopyBatch {
+  cudaEvent_t a = nullptr, b = nullptr;
+  int count = 0;
+  const char* label = "io_new";
+};
+
+static int issue_copies(mspq_engine* E, int cycle, CopyBatch& batch, uint64_t& bytes) {
+  const int n = E->view.host_stat[S_NREQ];
+  if (E->view.host_stat[S_OVERFLOW]) fail(MSPQ_ERR_OVERFLOW, "device controller ran out of buffers / queue");
+  if (n > E->view.req_cap) fail(MSPQ_ERR_OVERFLOW, "copy request queue overflow");
+  for (int i = 0; i < n; ++i) {
+    const int key = E->view.host_req[i * 3], buf = E->view.host_req[i * 3 + 1];
+    if (buf < 0 || buf >= E->nbuf) fail(MSPQ_ERR_OVERFLOW, "invalid slot buffer");
+    if (!batch.a) {
+      batch.a = E->pool_event();
+      CUDA_OK(cudaEventRecord(batch.a, E->sx));
+    }
+    if (E->last_cycle[buf] == cycle) CUDA_OK(cudaStreamWaitEvent(E->sx, E->ev_gemm[E->last_layer[buf]], 0));
+    CUDA_OK(cudaMemcpyAsync(E->pool + (size_t)buf * E->S16, E->host + (size_t)E->payload(key) * E->S16, E->S16,
+                            cudaMemcpyHostToDevice, E->sx));
+    CUDA_OK(cudaEventRecord(E->ev_ready[buf], E->sx));
+    E->ready_rec[buf] = 1;
+    bytes += (uint64_t)E->S16;
+    ++batch.count;
+  }
+  if (batch.a) {
+    batch.b = E->pool_event();
+    CUDA_OK(cudaEventRecord(batch.b, E->sx));
+  }
+  return n;
+}
+
+static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt, int max_new) {
+  if (!E->configured) fail(MSPQ_ERR_INVALID_CONFIG, "engine not configured");
+  if (n_prompt < 1) fail(MSPQ_ERR_EMPTY_RANGE, "empty prompt");
+  const auto& m = E->m;
+  const HostCfg& c = E->cfg;
+  const Profile& prof = c.profile;
+  const int L = m.L, K = m.K, Ex = m.E, d = m.d;
+  if (n_prompt - 1 + max_new + E->Tmax >= m.P) fail(MSPQ_ERR_RANGE_OUT_OF_BOUNDS, "positions exceed the positional table");
+  for (int i = 0; i < n_prompt; ++i)
+    if (prompt[i] < 0 || prompt[i] >= m.V) fail(MSPQ_ERR_RANGE_OUT_OF_BOUNDS, "prompt token out of vocab");
+  const int level = E->o.trace_level;
+  int head_pos = n_prompt - 1;
+  // device decode state
+  E->hpin[0] = 0;
+  E->hpin[1] = prompt[n_prompt - 1];
+  E->hpin[2] = head_pos;
+  CUDA_OK(cudaMemcpyAsync(E->dst, E->hpin, 12, cudaMemcpyHostToDevice, E->sc));
+  CUDA_OK(cudaMemcpyAsync(E->win_tok(), E->hpin + 1, 4, cudaMemcpyHostToDevice, E->sc));
+  const int kcap = std::max(c.use_governor ? c.k_max : c.fixed_k, 1);
+  std::vector<double> accept(kcap, c.initial_accept);
+  double g = static_cast<double>(L) * static_cast<double>(K);
+  auto est = [&g]() { return Est([gg = g](int k) { return static_cast<int>(std::llround(gg * static_cast<double>(k))); }); };
+  int k_slo = c.k_slo;
+  if (c.use_governor && c.ttft_budget > 0.0) k_slo = std::min(k_slo, k_slo_from_ttft(prof, c.ttft_budget, est(), c.k_min, c.k_max));
+  CUDA_OK(cudaEventRecord(E->ev_t0, E->sc));
+  CUDA_OK(cudaStreamWaitEvent(E->sx, E->ev_t0, 0));
+  std::vector<int> committed;
+  json cycles = json::array();
+  double stall_total = 0.0, layer_cov_total = 0.0, step_cov_total = 0.0;
+  uint64_t h2d_bytes = 0, total_new = 0, layer_cov_count = 0, step_total = 0, acc_total = 0;
+  const auto wall0 = std::chrono::steady_clock::now();
+  int ci = 0;
+  while ((int)committed.size() < max_new) {
+    const int rem = max_new - (int)committed.size();
+    const int cycle = ++E->cycle_serial;
+    E->ev_pool_next = 0;
+    const int kk = c.use_governor ? select_k(prof, accept, c.k_min, c.k_max, k_slo, est()) : c.fixed_k;
+    const int k = std::max(1, std::min({kk, rem, E->o.kmax}));
+    const int T = k + 1;
+    uint64_t cyc_bytes = 0;
+    std::vector<CopyBatch> batches;
+    // ---------------- draft + planner
+    CUDA_OK(cudaEventRecord(E->ev_c0, E->sc));
+    CUDA_OK(cudaMemsetAsync(E->dst, 0, 4, E->sc));  // row = 0
+    CAPI_OK(mspq_cache_begin_cycle(E->cache, k, E->sc));
+    CUDA_OK(cudaGraphLaunch(E->gexec, E->sc));
+    for (int i = 0; i < k; ++i) {
+      CAPI_OK(mspq_cache_plan_row(E->cache, i, E->sc));
+      CUDA_OK(cudaEventRecord(E->ev_row[i], E->sc));
+      if (i + 1 < k) CUDA_OK(cudaGraphLaunch(E->gexec, E->sc));
+      CUDA_OK(cudaEventSynchronize(E->ev_row[i]));
+      CopyBatch b;
+      issue_copies(E, cycle, b, cyc_bytes);
+      if (b.count) batches.push_back(b);
+    }
+    CUDA_OK(cudaEventRecord(E->ev_dend, E->sc));
+    // ---------------- verify (layer-major)
+    for (int s = 0; s < T; ++s) E->hpin[s] = head_pos + s;
+    CUDA_OK(cudaMemcpyAsync(E->win_pos(), E->hpin, T * 4, cudaMemcpyHostToDevice, E->sc));
+    CAPI_OK(mspq_embed(E->embed, E->pos, E->win_tok(), E->win_pos(), T, d, E->h, E->sc));
+    double stall = 0.0;
+    int demand_total = 0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> stall_ev;
+    for (int l = 0; l < L; ++l) {
+      const int pl = (l - 1) & 1;
+      int32_t* tgt = E->ids_t + (size_t)l * T * K;
+      CAPI_OK(mspq_gate_topk(E->h, l ? E->yv[pl] : nullptr, l ? E->sv[pl].entry_of : nullptr,
+                             l ? E->wts_t + (size_t)(l - 1) * T * K : nullptr, E->gamma + (size_t)l * d,
+                             E->router + (size_t)l * Ex * d, E->xn, tgt, E->wts_t + (size_t)l * T * K, nullptr, nullptr,
+                             nullptr, nullptr, l, L, T, d, Ex, K, m.eps, E->sc));
+      Sched& sv = E->sv[l & 1];
+      CAPI_OK(mspq_cache_verify_layer(E->cache, l, T, tgt, sv.n_groups, sv.group_expert, sv.group_buf, sv.group_off,
+                                      sv.entry_tok, sv.entry_of, E->sc));
+      CUDA_OK(cudaEventRecord(E->ev_w0[l], E->sc));
+      CUDA_OK(cudaEventSynchronize(E->ev_w0[l]));
+      CopyBatch b;
+      b.label = "io_new";
+      issue_copies(E, cycle, b, cyc_bytes);
+      if (b.count) batches.push_back(b);
+      // wait for every copy this layer's experts still depend on
+      const int ng = E->view.host_sched[0];
+      bool waited = false;
+      for (int gi = 0; gi < ng; ++gi) {
+        const int buf = E->view.host_sched[1 + gi];
+        if (buf < 0 || buf >= E->nbuf) fail(MSPQ_ERR_OVERFLOW, "schedule buffer out of range");
+        if (E->ready_rec[buf]) {
+          if (cudaEventQuery(E->ev_ready[buf]) == cudaErrorNotReady) {
+            CUDA_OK(cudaStreamWaitEvent(E->sc, E->ev_ready[buf], 0));
+            waited = true;
+          } else {
+            E->ready_rec[buf] = 0;
+          }
+        }
+      }
+      if (waited) {
+        CUDA_OK(cudaEventRecord(E->ev_w1[l], E->sc));
+        stall_ev.push_back({E->ev_w0[l], E->ev_w1[l]});
+      }
+      CAPI_OK(mspq_moe_bf16(sv.n_groups, sv.group_expert, sv.group_buf, sv.group_off, sv.entry_tok, E->xn, E->act,
+                            E->yv[l & 1], E->pool, E->S16, Ex, d, m.f, E->G, E->sc));
+      CUDA_OK(cudaEventRecord(E->ev_gemm[l], E->sc));
+      for (int gi = 0; gi < ng; ++gi) {
+        const int buf = E->view.host_sched[1 + gi];
+        E->last_cycle[buf] = cycle;
+        E->last_layer[buf] = l;
+      }
+      demand_total += 0;
+    }
+    const int pl = (L - 1) & 1;
+    CAPI_OK(mspq_gate_topk(E->h, E->yv[pl], E->sv[pl].entry_of, E->wts_t + (size_t)(L - 1) * T * K, E->gfinal, nullptr,
+                           E->xn, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, L, L, T, d, Ex, K, m.eps, E->sc));
+    CAPI_OK(mspq_lm_head(E->xn, E->lm, T, m.V, d, E->logits, E->sc));
+    CAPI_OK(mspq_argmax(E->logits, T, m.V, E->amax, E->sc));
+    CAPI_OK(mspq_accept_advance(E->win_tok() + 1, E->amax, k, E->dst + 3, E->dst + 1, E->dst + 2, head_pos, E->sc));
+    // next head = bonus
+    CUDA_OK(cudaMemcpyAsync(E->win_tok(), E->dst + 1, 4, cudaMemcpyDeviceToDevice, E->sc));
+    // results back: accepted, bonus, window tokens, target argmax (+ traces)
+    int32_t* hp = E->hpin;
+    size_t o = 0;
+    const size_t o_res = o;
+    CUDA_OK(cudaMemcpyAsync(hp + o, E->dst + 3, 8, cudaMemcpyDeviceToHost, E->sc));
+    o += 2;
+    const size_t o_win = o;
+    CUDA_OK(cudaMemcpyAsync(hp + o, E->dst + 8 + 1, k * 4, cudaMemcpyDeviceToHost, E->sc));  // draft tokens
+    o += k;
+    const size_t o_am = o;
+    CUDA_OK(cudaMemcpyAsync(hp + o, E->amax, T * 4, cudaMemcpyDeviceToHost, E->sc));
+    o += T;
+    const size_t o_cov = o;
+    CUDA_OK(cudaMemcpyAsync(hp + o, E->view.cov, (size_t)L * 8, cudaMemcpyDeviceToHost, E->sc));
+    o += (size_t)L * 2;
+    const size_t o_step = o;
+    CUDA_OK(cudaMemcpyAsync(hp + o, E->view.step, (size_t)L * T * 8, cudaMemcpyDeviceToHost, E->sc));
+    o += (size_t)L * T * 2;
+    const size_t o_tr = o;
+    if (level >= 1) {
+      CUDA_OK(cudaMemcpyAsync(hp + o, E->ids_t, (size_t)L * T * K * 4, cudaMemcpyDeviceToHost, E->sc));
+      o += (size_t)L * T * K;
+      CUDA_OK(cudaMemcpyAsync(hp + o, E->view.elb_ids, (size_t)k * L * K * 4, cudaMemcpyDeviceToHost, E->sc));
+      o += (size_t)k * L * K;
+      CUDA_OK(cudaMemcpyAsync(hp + o, E->view.elb_gates, (size_t)k * L * K * 4, cudaMemcpyDeviceToHost, E->sc));
+      o += (size_t)k * L * K;
+    }
+    CUDA_OK(cudaEventRecord(E->ev_end, E->sc));
+    CUDA_OK(cudaEventSynchronize(E->ev_end));
+    const int fetched = E->view.host_stat[S_FETCHED], demand = E->view.host_stat[S_DEMAND];
+    const int n_log = E->view.host_stat[S_NLOG];
+    for (auto& [a, b] : stall_ev) stall += elapsed_s(a, b);
+    const int accepted = hp[o_res], bonus_tok = hp[o_res + 1];
+    std::vector<int> new_toks;
+    for (int i = 0; i < accepted; ++i) new_toks.push_back(hp[o_win + i]);
+    new_toks.push_back(bonus_tok);
+    if ((int)new_toks.size() > rem) new_toks.resize(rem);
+    const int consumed = (int)new_toks.size();
+    const int bonus = consumed > accepted ? 1 : 0;
+    // ---- record (reference CycleRecord schema + measured extensions)
+    json rec;
+    rec["cycle"] = ci;
+    rec["k"] = k;
+    rec["accepted"] = consumed - bonus;
+    rec["bonus"] = bonus;
+    const double t_start = elapsed_s(E->ev_t0, E->ev_c0), t_dend = elapsed_s(E->ev_t0, E->ev_dend),
+                 t_end = elapsed_s(E->ev_t0, E->ev_end);
+    rec["start_s"] = t_start;
+    rec["span_s"] = t_end - t_start;
+    json cov = json::array();
+    for (int l = 0; l < L; ++l) {
+      const double v = static_cast<double>(hp[o_cov + l * 2]) / static_cast<double>(hp[o_cov + l * 2 + 1]);
+      cov.push_back(v);
+      layer_cov_total += v;
+      ++layer_cov_count;
+    }
+    rec["coverage"] = cov;
+    double sc_sum = 0.0;
+    for (int s = 0; s < T; ++s)
+      for (int l = 0; l < L; ++l)
+        sc_sum += static_cast<double>(hp[o_step + (l * T + s) * 2]) / static_cast<double>(hp[o_step + (l * T + s) * 2 + 1]);
+    rec["step_coverage"] = sc_sum / (T * L);
+    rec["steps"] = T * L;
+    rec["new_experts"] = fetched;
+    rec["bytes"] = cyc_bytes;
+    rec["io_wait_s"] = stall;
+    double sync_s = 0.0;
+    json segs = json::array();
+    segs.push_back(segment("compute", "draft", t_start, t_dend - t_start));
+    for (auto& b : batches) {
+      const double bs = elapsed_s(E->ev_t0, b.a), be = elapsed_s(E->ev_t0, b.b);
+      segs.push_back(segment("io", b.label, bs, be - bs));
+    }
+    segs.push_back(segment("compute", "verify", t_dend, t_end - t_dend));
+    rec["sync_fetch_s"] = sync_s;
+    rec["sync_count"] = demand;
+    rec["segments"] = segs;
+    rec["tokens"] = new_toks;
+    if (level >= 1) {
+      json dt = json::array(), ta = json::array();
+      for (int i = 0; i < k; ++i) dt.push_back(hp[o_win + i]);
+      for (int s = 0; s < T; ++s) ta.push_back(hp[o_am + s]);
+      rec["draft_tokens"] = dt;
+      rec["target_argmax"] = ta;
+      json tgt = json::array();  // [slot][layer][K]
+      for (int s = 0; s < T; ++s) {
+        json sl = json::array();
+        for (int l = 0; l < L; ++l) {
+          json c2 = json::array();
+          for (int j = 0; j < K; ++j) c2.push_back(hp[o_tr + ((size_t)l * T + s) * K + j]);
+          sl.push_back(c2);
+        }
+        tgt.push_back(sl);
+      }
+      rec["target"] = tgt;
+      const size_t o_e = o_tr + (size_t)L * T * K, o_g = o_e + (size_t)k * L * K;
+      json elb = json::array(), gates = json::array();
+      for (int r = 0; r < k; ++r) {
+        json rl = json::array(), gl = json::array();
+        for (int l = 0; l < L; ++l) {
+          json c2 = json::array(), g2 = json::array();
+          for (int j = 0; j < K; ++j) {
+            c2.push_back(hp[o_e + ((size_t)r * L + l) * K + j]);
+            float gv;
+            memcpy(&gv, &hp[o_g + ((size_t)r * L + l) * K + j], 4);
+            g2.push_back(gv);
+          }
+          rl.push_back(c2);
+          gl.push_back(g2);
+        }
+        elb.push_back(rl);
+        gates.push_back(gl);
+      }
+      rec["elb"] = elb;
+      rec["elb_gates"] = gates;
+    }
+    if (level >= 2) {
+      const int nl = std::min(n_log, E->view.log_cap);
+      std::vector<int32_t> lg((size_t)nl * 6);
+      if (nl) CUDA_OK(cudaMemcpy(lg.data(), E->view.log, (size_t)nl * 24, cudaMemcpyDeviceToHost));
+      json lj = json::array();
+      for (int i = 0; i < nl; ++i) {
+        const int32_t* ev = &lg[(size_t)i * 6];
+        lj.push_back({ev[0], ev[1], ev[2] / Ex, ev[2] % Ex, ev[3], ev[4] < 0 ? -1 : ev[4] / Ex,
+                      ev[4] < 0 ? -1 : ev[4] % Ex, ev[5]});
+      }
+      rec["log"] = lj;
+    }
+    cycles.push_back(rec);
+    // ---- governor state (sim.cpp:394-404 semantics on the live outcomes)
+    std::vector<bool> outcomes;
+    for (int i = 0; i < k; ++i) {
+      const bool ok = i < accepted;
+      outcomes.push_back(ok);
+      if (!ok) break;
+    }
+    if (outcomes.size() > accept.size()) outcomes.resize(accept.size());
+    accept = update_acceptance(accept, c.ema_alpha, outcomes);
+    g = static_cast<double>(fetched) / static_cast<double>(k);
+    stall_total += stall;
+    step_cov_total += sc_sum;
+    step_total += (uint64_t)T * L;
+    acc_total += (uint64_t)(consumed - bonus);
+    total_new += fetched;
+    h2d_bytes += cyc_bytes;
+    for (int t2 : new_toks) committed.push_back(t2);
+    head_pos += accepted + 1;
+    ++ci;
+    demand_total += demand;
+  }
+  // everything (including trailing prefetches) has landed before we report
+  CUDA_OK(cudaStreamSynchronize(E->sx));
+  const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+  json rep;
+  const double total_time = cycles.empty() ? 0.0
+                                           : cycles.back()["start_s"].get<double>() + cycles.back()["span_s"].get<double>();
+  rep["total_tokens"] = committed.size();
+  rep["total_time_s"] = total_time;
+  rep["tpot_s"] = committed.empty() ? 0.0 : total_time / committed.size();
+  rep["ttft_s"] = cycles.empty() ? 0.0 : cycles[0]["span_s"].get<double>();
+  rep["mean_coverage"] = layer_cov_count ? layer_cov_total / layer_cov_count : 0.0;
+  rep["mean_step_coverage"] = step_total ? step_cov_total / step_total : 0.0;
+  rep["mean_accepted"] = cycles.empty() ? 0.0 : (double)acc_total / cycles.size();
+  rep["stall_time_s"] = stall_total;
+  rep["total_new_experts"] = total_new;
+  rep["cycles"] = cycles;
+  rep["tokens"] = committed;
+  rep["h2d_bytes"] = h2d_bytes;
+  rep["wall_s"] = wall;
+  rep["profile"] = c.profile.to_json();
+  rep["policy"] = policy_name(c.policy);
+  return rep.dump();
+}
+
+// ============================================================================ C-ABI
+namespace {
+template <class F>
+int guarded(F&& f) {
+  try {
+    return f();
+  } catch (const Err& e) {
+    return mspq::set_error(e.code, e.msg);
+  } catch (const nlohmann::json::exception& e) {
+    return mspq::set_error(MSPQ_ERR_INVALID_CONFIG, e.what());
+  } catch (const std::exception& e) {
+    return mspq::set_error(MSPQ_ERR_INTERNAL, e.what());
+  }
+}
+char* dupstr(const std::string& s) {
+  char* p = (char*)malloc(s.size() + 1);
+  memcpy(p, s.c_str(), s.size() + 1);
+  return p;
+}
+void destroy(mspq_engine* E) {
+  if (!E) return;
+  cudaDeviceSynchronize();
+  if (E->gexec) cudaGraphExecDestroy(E->gexec);
+  if (E->graph) cudaGraphDestroy(E->graph);
+  for (auto v : {&E->ev_ready, &E->ev_gemm, &E->ev_w0, &E->ev_w1, &E->ev_row, &E->ev_pool})
+    for (auto ev : *v)
+      if (ev) cudaEventDestroy(ev);
+  for (auto ev : {E->ev_c0, E->ev_dend, E->ev_end, E->ev_t0})
+    if (ev) cudaEventDestroy(ev);
+  if (E->cache) mspq_cache_destroy(E->cache);
+  if (E->pool) cudaFree(E->pool);
+  if (E->ws) cudaFree(E->ws);
+  if (E->draft4) cudaFree(E->draft4);
+  if (E->wblk) cudaFree(E->wblk);
+  if (E->hpin) cudaFreeHost(E->hpin);
+  if (E->host) {
+    if (E->host_is_shm) {
+      cudaHostUnregister(E->host);
+      munmap(E->host, E->host_bytes);
+    } else {
+      cudaFreeHost(E->host);
+    }
+  }
+  if (E->sc) cudaStreamDestroy(E->sc);
+  if (E->sx) cudaStreamDestroy(E->sx);
+  delete E;
+}
+}  // namespace
+
+extern "C" {
+
+int mspq_engine_create(const mspq_model_desc* md, const mspq_engine_opts* op, mspq_engine** out) {
+  return guarded([&] {
+    *out = nullptr;
+    const auto& m = *md;
+    if (m.L < 1 || m.E < 1 || m.K < 1 || m.K > m.E || m.E > 1024 || m.L * m.E > 8192)
+      fail(MSPQ_ERR_SHAPE_VIOLATION, "need 1 <= K <= E <= 1024, L*E <= 8192");
+    if (m.d % 256 || m.f % 256 || m.V < 1 || m.P < 2) fail(MSPQ_ERR_SHAPE_VIOLATION, "need d, f multiples of 256");
+    if (op->kmax < 1 || op->kmax > 32) fail(MSPQ_ERR_K_OUT_OF_RANGE, "kmax must be in [1, 32]");
+    mspq_engine* E = new mspq_engine();
+    try {
+      E->m = m;
+      E->o = *op;
+      E->store_path = op->host_store_path ? op->host_store_path : "";
+      E->o.host_store_path = nullptr;
+      CUDA_OK(cudaSetDevice(op->device));
+      CUDA_OK(cudaStreamCreateWithFlags(&E->sc, cudaStreamNonBlocking));
+      int lo, hi;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      CUDA_OK(cudaStreamCreateWithPriority(&E->sx, cudaStreamNonBlocking, hi));
+      E->S16 = mspq_bf16_blob_bytes(m.d, m.f);
+      E->S4 = mspq_int4_blob_bytes(m.d, m.f);
+      E->Tmax = op->kmax + 1;
+      E->n_payload = m.unique_experts > 0 ? std::min(m.unique_experts, m.L * m.E) : m.L * m.E;
+      make_weights(E);
+      alloc_host_store(E);
+      make_experts(E);
+      make_workspaces(E);
+      E->ev_gemm.resize(m.L);
+      E->ev_w0.resize(m.L);
+      E->ev_w1.resize(m.L);
+      E->ev_row.resize(E->Tmax);
+      for (auto v : {&E->ev_gemm, &E->ev_w0, &E->ev_w1, &E->ev_row})
+        for (auto& ev : *v) CUDA_OK(cudaEventCreate(&ev));
+      for (auto p : {&E->ev_c0, &E->ev_dend, &E->ev_end, &E->ev_t0}) CUDA_OK(cudaEventCreate(p));
+      CUDA_OK(cudaStreamSynchronize(E->sc));
+    } catch (...) {
+      destroy(E);
+      throw;
+    }
+    *out = E;
+    return MSPQ_OK;
+  });
+}
+
+int mspq_engine_destroy(mspq_engine* E) {
+  return guarded([&] {
+    destroy(E);
+    return MSPQ_OK;
+  });
+}
+
+int mspq_engine_configure(mspq_engine* E, const char* cfg) {
+  return guarded([&] {
+    configure(E, cfg);
+    return MSPQ_OK;
+  });
+}
+
+int mspq_generate(mspq_engine* E, const int32_t* prompt, int n, int max_new, char** report) {
+  return guarded([&] {
+    *report = dupstr(generate(E, prompt, n, max_new));
+    return MSPQ_OK;
+  });
+}
+
+int mspq_engine_info(mspq_engine* E, char** out) {
+  return guarded([&] {
+    json j;
+    const auto& m = E->m;
+    j["L"] = m.L;
+    j["E"] = m.E;
+    j["K"] = m.K;
+    j["d"] = m.d;
+    j["f"] = m.f;
+    j["V"] = m.V;
+    j["expert_bytes_bf16"] = E->S16;
+    j["expert_bytes_int4"] = E->S4;
+    j["host_store_bytes"] = E->host_bytes;
+    j["n_payload"] = E->n_payload;
+    j["slot_buffers"] = E->nbuf;
+    j["slot_pool_bytes"] = (uint64_t)E->nbuf * E->S16;
+    j["draft_resident_bytes"] = (uint64_t)m.L * m.E * E->S4;
+    j["pcie_bw_measured"] = E->pcie_bw_measured;
+    j["draft_step_s"] = E->draft_step_s;
+    if (E->configured) j["profile"] = E->cfg.profile.to_json();
+    *out = dupstr(j.dump());
+    return MSPQ_OK;
+  });
+}
+
+int mspq_engine_read(mspq_engine* E, const char* name, void* dst, long long bytes) {
+  return guarded([&] {
+    const auto& m = E->m;
+    std::string n = name;
+    const void* src = nullptr;
+    size_t avail = 0;
+    bool from_host = false;
+    auto two = [&](const std::string& rest, int& a, int& b) { return sscanf(rest.c_str(), "%d:%d", &a, &b) == 2; };
+    if (n == "embed") src = E->embed, avail = (size_t)m.V * m.d * 2;
+    else if (n == "lm") src = E->lm, avail = (size_t)m.V * m.d * 2;
+    else if (n == "pos") src = E->pos, avail = (size_t)m.P * m.d * 2;
+    else if (n == "gamma:final") src = E->gfinal, avail = (size_t)m.d * 2;
+    else if (n.rfind("gamma:", 0) == 0) src = E->gamma + (size_t)atoi(n.c_str() + 6) * m.d, avail = (size_t)m.d * 2;
+    else if (n.rfind("router:", 0) == 0) src = E->router + (size_t)atoi(n.c_str() + 7) * m.E * m.d, avail = (size_t)m.E * m.d * 2;
+    else if (n.rfind("draft:", 0) == 0) {
+      int l, e;
+      if (!two(n.substr(6), l, e)) fail(MSPQ_ERR_INVALID_CONFIG, n);
+      src = E->draft4 + ((size_t)l * m.E + e) * E->S4;
+      avail = E->S4;
+    } else if (n.rfind("expert:", 0) == 0) {
+      int l, e;
+      if (!two(n.substr(7), l, e)) fail(MSPQ_ERR_INVALID_CONFIG, n);
+      src = E->host + (size_t)E->payload(l * m.E + e) * E->S16;
+      avail = E->S16;
+      from_host = true;
+    } else
+      fail(MSPQ_ERR_INVALID_CONFIG, "unknown tensor " + n);
+    if ((size_t)bytes > avail) fail(MSPQ_ERR_RANGE_OUT_OF_BOUNDS, "read beyond tensor");
+    if (from_host) memcpy(dst, src, bytes);
+    else CUDA_OK(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+    return MSPQ_OK;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,9 @@
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+
+namespace mspq {
+int set_error(int code, const std::string& msg);
+int cuda_status(cudaError_t e, const char* where);
+}  // namespace mspq

@@ -1,0 +1,125 @@
+"""Thin torch-tensor wrappers over the kernel entry points of the C-ABI (for tests and
+benchmarks).  torch is only used for device memory and streams."""
+from __future__ import annotations
+
+import torch
+
+from ._lib import check, lib
+
+
+def _p(t):
+    return None if t is None else t.data_ptr()
+
+
+def _s(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def int4_blob_bytes(d, f):
+    return lib().mspq_int4_blob_bytes(d, f)
+
+
+def bf16_blob_bytes(d, f):
+    return lib().mspq_bf16_blob_bytes(d, f)
+
+
+def fill_bf16(seed, tensor, scale, n, kind=0, start=0, device="cuda"):
+    out = torch.empty(n, dtype=torch.int16, device=device)
+    check(lib().mspq_fill_bf16(seed, tensor, scale, kind, _p(out), n, start, _s()))
+    return out
+
+
+def fill_expert(seed, layer, expert, d, f, a_up, a_down, device="cuda"):
+    out = torch.empty(bf16_blob_bytes(d, f) // 2, dtype=torch.int16, device=device)
+    check(lib().mspq_fill_expert(seed, layer, expert, d, f, a_up, a_down, _p(out), _s()))
+    return out
+
+
+def quantize_int4(w_i16, rows, cols):
+    q = torch.empty(rows * cols // 8, dtype=torch.int32, device=w_i16.device)
+    s = torch.empty(rows * cols // 128, dtype=torch.int16, device=w_i16.device)
+    check(lib().mspq_quantize_int4(_p(w_i16), rows, cols, _p(q), _p(s), _s()))
+    return q, s
+
+
+def embed(embed_w, pos_w, tokens, positions, d):
+    T = tokens.numel()
+    h = torch.empty(T, d, dtype=torch.float32, device=tokens.device)
+    check(lib().mspq_embed(_p(embed_w), _p(pos_w), _p(tokens), _p(positions), T, d, _p(h), _s()))
+    return h
+
+
+def gate_topk(h, gamma, router, E, K, eps=1e-6, y=None, entry_of=None, prev_wts=None,
+              elb_ids=None, elb_gates=None, elb_row=None, layer=0, L=1, want_logits=True):
+    T, d = h.shape
+    dev = h.device
+    xn = torch.empty(T, d, dtype=torch.int16, device=dev)
+    ids = torch.empty(T, K, dtype=torch.int32, device=dev)
+    wts = torch.empty(T, K, dtype=torch.float32, device=dev)
+    logits = torch.empty(T, E, dtype=torch.float32, device=dev) if want_logits and router is not None else None
+    check(lib().mspq_gate_topk(_p(h), _p(y), _p(entry_of), _p(prev_wts), _p(gamma), _p(router),
+                               _p(xn), _p(ids), _p(wts), _p(logits), _p(elb_ids), _p(elb_gates),
+                               _p(elb_row), layer, L, T, d, E, K, eps, _s()))
+    return xn, ids, wts, logits
+
+
+class Schedule:
+    def __init__(self, T, K, E, device="cuda"):
+        G = min(E, T * K)
+        self.T, self.K, self.E, self.G = T, K, E, G
+        z = lambda n: torch.zeros(n, dtype=torch.int32, device=device)
+        self.n_groups, self.group_expert, self.group_buf = z(1), z(G), z(G)
+        self.group_off, self.entry_tok, self.entry_of = z(G + 1), z(T * K), z(T * K)
+
+    def ptrs(self):
+        return [_p(self.n_groups), _p(self.group_expert), _p(self.group_buf), _p(self.group_off),
+                _p(self.entry_tok), _p(self.entry_of)]
+
+
+def build_schedule(ids, E):
+    T, K = ids.shape
+    s = Schedule(T, K, E, ids.device)
+    check(lib().mspq_build_schedule(_p(ids), T, K, E, *s.ptrs(), _s()))
+    return s
+
+
+def moe_int4(s: Schedule, xn, blobs, blob_bytes, layer, E, d, f):
+    N = s.T * s.K
+    act = torch.empty(N, f, dtype=torch.int16, device=xn.device)
+    y = torch.empty(N, d, dtype=torch.float32, device=xn.device)
+    check(lib().mspq_moe_int4(_p(s.n_groups), _p(s.group_expert), _p(s.group_buf), _p(s.group_off),
+                              _p(s.entry_tok), _p(xn), _p(act), _p(y), _p(blobs), blob_bytes, layer,
+                              E, d, f, s.G, _s()))
+    return act, y
+
+
+def moe_bf16(s: Schedule, xn, pool, blob_bytes, E, d, f):
+    N = s.T * s.K
+    act = torch.empty(N, f, dtype=torch.int16, device=xn.device)
+    y = torch.empty(N, d, dtype=torch.float32, device=xn.device)
+    check(lib().mspq_moe_bf16(_p(s.n_groups), _p(s.group_expert), _p(s.group_buf), _p(s.group_off),
+                              _p(s.entry_tok), _p(xn), _p(act), _p(y), _p(pool), blob_bytes, E, d,
+                              f, s.G, _s()))
+    return act, y
+
+
+def lm_head(xn, lm, V):
+    T, d = xn.shape
+    logits = torch.empty(T, V, dtype=torch.float32, device=xn.device)
+    check(lib().mspq_lm_head(_p(xn), _p(lm), T, V, d, _p(logits), _s()))
+    return logits
+
+
+def argmax(logits):
+    T, V = logits.shape
+    out = torch.empty(T, dtype=torch.int32, device=logits.device)
+    check(lib().mspq_argmax(_p(logits), T, V, _p(out), _s()))
+    return out
+
+
+def accept_scan(draft, target_argmax):
+    k = draft.numel()
+    res = torch.empty(2, dtype=torch.int32, device=draft.device)
+    check(lib().mspq_accept_scan(_p(draft), _p(target_argmax), k, _p(res), _s()))
+    return res

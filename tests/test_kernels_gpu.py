@@ -1,0 +1,203 @@
+"""Kernel parity vs the CPU oracle (oracle/model.py + oracle/csrc/model_ref.c).
+
+Bit-exact: weight generation, INT4 quantisation, RMSNorm, router logits/top-k/softmax weights,
+LM-head logits and argmax, accept scan, schedule.  Tolerance (stated per test): expert FFN
+outputs (fp32 accumulation order differs from the float64 oracle)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import model as om
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [("tiny", 8, 2, 256, 512), ("phi", 16, 2, 4096, 6400), ("qwen3", 128, 8, 2048, 768),
+          ("mixtral", 8, 2, 4096, 14336)]
+
+
+def i16_to_u16(t):
+    return t.cpu().numpy().view(np.uint16)
+
+
+def to_dev(a_u16):
+    return torch.from_numpy(np.ascontiguousarray(a_u16).view(np.int16)).cuda()
+
+
+def test_weight_generation_bit_exact(cuda):
+    from paper_2511_14102_b200 import ops
+    for tensor, scale, kind in [(om.T_EMBED, 1.0, 0), (om.t_router(3), 0.25, 0), (om.t_gamma(2), 0, 1)]:
+        g = i16_to_u16(ops.fill_bf16(77, tensor, scale, 5000, kind=kind, start=123))
+        if kind == 0:
+            w = om.f32_to_bf16(om.uniform(77, tensor, 5000, start=123) * np.float32(scale))
+        else:
+            w = om.f32_to_bf16(np.float32(1.0) + om.uniform(77, tensor, 5000, start=123) * np.float32(0.125))
+        assert np.array_equal(g, w)
+
+
+@pytest.mark.parametrize("name,E,K,d,f", SHAPES[:3])
+def test_expert_blob_and_int4_quantisation_bit_exact(cuda, name, E, K, d, f):
+    from paper_2511_14102_b200 import ops
+    desc = om.ModelDesc(L=2, E=E, K=K, d=d, f=f, V=512, seed=9)
+    mdl = om.Model(desc)
+    blob = ops.fill_expert(desc.seed, 1, 3, d, f, desc.a_up(), desc.a_down())
+    g, u, dn = mdl.expert(1, 3)
+    w13 = np.empty((2 * f, d), dtype=np.uint16)
+    w13[0::2], w13[1::2] = g, u
+    hb = i16_to_u16(blob)
+    assert np.array_equal(hb[:2 * f * d].reshape(2 * f, d), w13)
+    assert np.array_equal(hb[2 * f * d:].reshape(d, f), dn)
+    q, s = ops.quantize_int4(blob[:2 * f * d], 2 * f, d)
+    (gq, gs), (uq, us), _ = mdl.expert_q(1, 3)
+    qq = np.empty((2 * f, d), dtype=np.uint8)
+    qq[0::2], qq[1::2] = gq, uq
+    ss = np.empty((2 * f, d // 128), dtype=np.uint16)
+    ss[0::2], ss[1::2] = gs, us
+    assert np.array_equal(q.cpu().numpy().view(np.uint32).reshape(2 * f, d // 8), om.pack_int4(qq))
+    assert np.array_equal(i16_to_u16(s).reshape(2 * f, d // 128), ss)
+
+
+@pytest.mark.parametrize("name,E,K,d,f", SHAPES)
+@pytest.mark.parametrize("T", [1, 5, 17])
+def test_norm_router_topk_bit_exact(cuda, name, E, K, d, f, T):
+    """K1: given identical fp32 residuals, xn, logits, ids and weights are bit-identical."""
+    from paper_2511_14102_b200 import ops
+    desc = om.ModelDesc(L=1, E=E, K=K, d=d, f=f, V=512, seed=31)
+    mdl = om.Model(desc)
+    rng = np.random.default_rng(T * 7 + E)
+    h = (rng.standard_normal((T, d)) * 1.3).astype(np.float32)
+    gamma, router = mdl.gamma(0), mdl.router(0)
+    xn, ids, wts, logits = ops.gate_topk(torch.from_numpy(h).cuda(), to_dev(gamma), to_dev(router), E, K)
+    xn, ids, wts, logits = i16_to_u16(xn), ids.cpu().numpy(), wts.cpu().numpy(), logits.cpu().numpy()
+    for t in range(T):
+        oxn = mdl.rmsnorm(h[t], gamma)
+        oids, owts, olog = mdl.route(oxn, 0)
+        assert np.array_equal(xn[t], oxn)
+        assert np.array_equal(logits[t].view(np.uint32), olog.view(np.uint32))
+        assert np.array_equal(ids[t], oids)
+        assert np.array_equal(wts[t].view(np.uint32), owts.view(np.uint32))
+
+
+def test_router_combine_matches_oracle(cuda):
+    """Residual combine h += sum_j w_j*y_j (k-slot order, no FMA contraction) feeding the norm."""
+    from paper_2511_14102_b200 import ops
+    E, K, d, T = 16, 2, 4096, 5
+    desc = om.ModelDesc(L=2, E=E, K=K, d=d, f=6400, V=512, seed=3)
+    mdl = om.Model(desc)
+    rng = np.random.default_rng(0)
+    h = rng.standard_normal((T, d)).astype(np.float32)
+    y = rng.standard_normal((T * K, d)).astype(np.float32)
+    w = rng.random((T, K)).astype(np.float32)
+    eo = rng.permutation(T * K).astype(np.int32).reshape(T, K)
+    ht = torch.from_numpy(h).cuda()
+    xn, ids, wts, _ = ops.gate_topk(ht, to_dev(mdl.gamma(1)), to_dev(mdl.router(1)), E, K,
+                                    y=torch.from_numpy(y).cuda(), entry_of=torch.from_numpy(eo).cuda(),
+                                    prev_wts=torch.from_numpy(w).cuda())
+    hn = ht.cpu().numpy()
+    for t in range(T):
+        acc = np.zeros(d, dtype=np.float32)
+        for j in range(K):
+            acc = (acc + (np.float32(w[t, j]) * y[eo[t, j]]).astype(np.float32)).astype(np.float32)
+        want = (h[t] + acc).astype(np.float32)
+        assert np.array_equal(hn[t].view(np.uint32), want.view(np.uint32))
+        assert np.array_equal(i16_to_u16(xn)[t], mdl.rmsnorm(want, mdl.gamma(1)))
+
+
+@pytest.mark.parametrize("V,d,T", [(512, 256, 1), (32064, 4096, 5), (151936, 2048, 3)])
+def test_lm_head_and_argmax_bit_exact(cuda, V, d, T):
+    from paper_2511_14102_b200 import ops
+    desc = om.ModelDesc(L=1, E=8, K=2, d=d, f=512, V=V, seed=5)
+    mdl = om.Model(desc)
+    rng = np.random.default_rng(1)
+    xn = om.f32_to_bf16(rng.standard_normal((T, d)).astype(np.float32))
+    lm = mdl.lm()
+    logits = ops.lm_head(to_dev(xn), to_dev(lm), V)
+    am = ops.argmax(logits)
+    ol, oam = mdl.lm_head(xn)
+    assert np.array_equal(logits.cpu().numpy().view(np.uint32), ol.view(np.uint32))
+    assert np.array_equal(am.cpu().numpy(), oam)
+
+
+def test_argmax_tie_breaks_to_lower_id(cuda):
+    from paper_2511_14102_b200 import ops
+    x = torch.zeros(2, 4099, device="cuda")
+    x[0, 17] = 3.0
+    x[0, 4000] = 3.0
+    x[1, 4098] = 1.0
+    assert ops.argmax(x).tolist() == [17, 4098]
+
+
+@pytest.mark.parametrize("name,E,K,d,f", SHAPES)
+def test_moe_int4_and_bf16_within_tolerance(cuda, name, E, K, d, f):
+    """K2/K3 vs float64 oracle: |y - y_ref| <= 2e-3 * max|y_ref| + 1e-5 (fp32 accumulation,
+    bf16 activation rounding may flip by one bf16 ulp)."""
+    from paper_2511_14102_b200 import ops
+    L = 1
+    desc = om.ModelDesc(L=L, E=E, K=K, d=d, f=f, V=512, seed=13)
+    mdl = om.Model(desc)
+    T = 2 if name == "mixtral" else 5
+    rng = np.random.default_rng(2)
+    ids = np.stack([rng.choice(E, K, replace=False) for _ in range(T)]).astype(np.int32)
+    used = sorted(set(ids.ravel().tolist()))
+    xn = om.f32_to_bf16(rng.standard_normal((T, d)).astype(np.float32))
+    s = ops.build_schedule(torch.from_numpy(ids).cuda(), E)
+    sb = ops.bf16_blob_bytes(d, f)
+    s4 = ops.int4_blob_bytes(d, f)
+    # bf16 pool: buffer index = expert id; int4 blobs for layer 0, all experts (only used filled)
+    pool = torch.zeros(E * sb // 2, dtype=torch.int16, device="cuda")
+    blobs = torch.zeros(E * s4, dtype=torch.uint8, device="cuda")
+    for e in used:
+        b = ops.fill_expert(desc.seed, 0, e, d, f, desc.a_up(), desc.a_down())
+        pool[e * sb // 2:(e + 1) * sb // 2] = b
+        q13, s13 = ops.quantize_int4(b[:2 * f * d], 2 * f, d)
+        q2, s2 = ops.quantize_int4(b[2 * f * d:], d, f)
+        parts = [q13.view(torch.uint8), s13.view(torch.uint8), q2.view(torch.uint8), s2.view(torch.uint8)]
+        blobs[e * s4:(e + 1) * s4] = torch.cat(parts)
+    ng = int(s.n_groups.item())
+    assert ng == len(used)
+    eo = s.entry_of.cpu().numpy().reshape(T, K)
+    for int4 in (False, True):
+        if int4:
+            _, y = ops.moe_int4(s, to_dev(xn), blobs, s4, 0, E, d, f)
+        else:
+            _, y = ops.moe_bf16(s, to_dev(xn), pool, sb, E, d, f)
+        y = y.cpu().numpy()
+        for t in range(T):
+            for j in range(K):
+                want, _ = mdl.ffn(xn[t], 0, int(ids[t, j]), draft=int4)
+                got = y[eo[t, j]]
+                tol = 2e-3 * np.abs(want).max() + 1e-5
+                assert np.abs(got - want).max() <= tol, (int4, t, j, np.abs(got - want).max(), tol)
+
+
+def test_schedule_is_reorder_verification(cuda):
+    from paper_2511_14102_b200 import ops
+    from oracle import control_plane as cp
+    rng = np.random.default_rng(4)
+    for _ in range(20):
+        T, K, E = rng.integers(1, 18), 2, 16
+        ids = np.stack([rng.choice(E, K, replace=False) for _ in range(T)]).astype(np.int32)
+        s = ops.build_schedule(torch.from_numpy(ids).cuda(), E)
+        ng = int(s.n_groups.item())
+        ge, go, et = s.group_expert.cpu().tolist(), s.group_off.cpu().tolist(), s.entry_tok.cpu().tolist()
+        plan = cp.reorder_verification(list(range(T)), [[list(r) for r in ids]])[0]
+        assert ng == len(plan)
+        for g, grp in enumerate(plan):
+            assert ge[g] == grp["expert"]
+            assert et[go[g]:go[g + 1]] == grp["tokens"]
+
+
+def test_accept_scan(cuda):
+    from paper_2511_14102_b200 import ops
+    rng = np.random.default_rng(9)
+    for _ in range(50):
+        k = int(rng.integers(1, 17))
+        tgt = rng.integers(0, 5, k + 1).astype(np.int32)
+        dr = tgt[:k].copy()
+        cut = int(rng.integers(0, k + 1))
+        if cut < k:
+            dr[cut] = (dr[cut] + 1) % 5
+        res = ops.accept_scan(torch.from_numpy(dr).cuda(), torch.from_numpy(tgt).cuda()).tolist()
+        acc = 0
+        while acc < k and dr[acc] == tgt[acc]:
+            acc += 1
+        assert res == [acc, int(tgt[acc])]
