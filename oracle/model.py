@@ -175,7 +175,7 @@ class ModelDesc:
     embed_scale: float = 1.0
     pos_scale: float = 0.5
     router_scale: float = 3.0
-    moe_scale: float = 0.5
+    moe_scale: float = 0.06
     lm_scale: float = 1.0
     eps: float = 1e-6
 

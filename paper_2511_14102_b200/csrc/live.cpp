@@ -119,7 +119,8 @@ struct mspq_engine {
   std::vector<cudaEvent_t> ev_ready;
   std::vector<char> ready_rec;
   std::vector<int> last_cycle, last_layer;
-  std::vector<cudaEvent_t> ev_gemm, ev_w0, ev_w1, ev_row;
+  std::vector<cudaEvent_t> ev_gemm, ev_w0, ev_w1, ev_row, ev_k0, ev_g0, ev_g1;
+  int graph_nodes = 0;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_pool_next = 0;
   cudaEvent_t ev_c0 = nullptr, ev_dend = nullptr, ev_end = nullptr, ev_t0 = nullptr;
@@ -322,6 +323,9 @@ void capture_draft_graph(mspq_engine* E) {
   }
   CUDA_OK(cudaStreamEndCapture(E->sc, &E->graph));
   CUDA_OK(cudaGraphInstantiate(&E->gexec, E->graph, 0));
+  size_t nn = 0;
+  CUDA_OK(cudaGraphGetNodes(E->graph, nullptr, &nn));
+  E->graph_nodes = (int)nn;
 }
 
 double measure_pcie(mspq_engine* E) {
@@ -492,6 +496,9 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
   uint64_t h2d_bytes = 0, total_new = 0, layer_cov_count = 0, step_total = 0, acc_total = 0;
   const auto wall0 = std::chrono::steady_clock::now();
   int ci = 0;
+  long launches = 0, k3_groups = 0, draft_steps = 0;
+  double k3_time = 0.0, k3_bytes = 0.0, draft_time = 0.0;
+  std::vector<int> layer_groups(L, 0);
   while ((int)committed.size() < max_new) {
     const int rem = max_new - (int)committed.size();
     const int cycle = ++E->cycle_serial;
@@ -505,11 +512,20 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
     CUDA_OK(cudaEventRecord(E->ev_c0, E->sc));
     CUDA_OK(cudaMemsetAsync(E->dst, 0, 4, E->sc));  // row = 0
     CAPI_OK(mspq_cache_begin_cycle(E->cache, k, E->sc));
+    CUDA_OK(cudaEventRecord(E->ev_g0[0], E->sc));
     CUDA_OK(cudaGraphLaunch(E->gexec, E->sc));
+    CUDA_OK(cudaEventRecord(E->ev_g1[0], E->sc));
+    launches += 1 + E->graph_nodes;
     for (int i = 0; i < k; ++i) {
       CAPI_OK(mspq_cache_plan_row(E->cache, i, E->sc));
       CUDA_OK(cudaEventRecord(E->ev_row[i], E->sc));
-      if (i + 1 < k) CUDA_OK(cudaGraphLaunch(E->gexec, E->sc));
+      ++launches;
+      if (i + 1 < k) {
+        CUDA_OK(cudaEventRecord(E->ev_g0[i + 1], E->sc));
+        CUDA_OK(cudaGraphLaunch(E->gexec, E->sc));
+        CUDA_OK(cudaEventRecord(E->ev_g1[i + 1], E->sc));
+        launches += E->graph_nodes;
+      }
       CUDA_OK(cudaEventSynchronize(E->ev_row[i]));
       CopyBatch b;
       issue_copies(E, cycle, b, cyc_bytes);
@@ -558,9 +574,13 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
         CUDA_OK(cudaEventRecord(E->ev_w1[l], E->sc));
         stall_ev.push_back({E->ev_w0[l], E->ev_w1[l]});
       }
+      CUDA_OK(cudaEventRecord(E->ev_k0[l], E->sc));
       CAPI_OK(mspq_moe_bf16(sv.n_groups, sv.group_expert, sv.group_buf, sv.group_off, sv.entry_tok, E->xn, E->act,
                             E->yv[l & 1], E->pool, E->S16, Ex, d, m.f, E->G, E->sc));
       CUDA_OK(cudaEventRecord(E->ev_gemm[l], E->sc));
+      launches += 4;  // gate_topk, verify_layer, 2 x grouped FFN
+      k3_groups += ng;
+      layer_groups[l] = ng;
       for (int gi = 0; gi < ng; ++gi) {
         const int buf = E->view.host_sched[1 + gi];
         E->last_cycle[buf] = cycle;
@@ -569,6 +589,7 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
       demand_total += 0;
     }
     const int pl = (L - 1) & 1;
+    launches += 6;  // embed, final norm, lm head, argmax, accept, begin_cycle
     CAPI_OK(mspq_gate_topk(E->h, E->yv[pl], E->sv[pl].entry_of, E->wts_t + (size_t)(L - 1) * T * K, E->gfinal, nullptr,
                            E->xn, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, L, L, T, d, Ex, K, m.eps, E->sc));
     CAPI_OK(mspq_lm_head(E->xn, E->lm, T, m.V, d, E->logits, E->sc));
@@ -608,6 +629,13 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
     const int fetched = E->view.host_stat[S_FETCHED], demand = E->view.host_stat[S_DEMAND];
     const int n_log = E->view.host_stat[S_NLOG];
     for (auto& [a, b] : stall_ev) stall += elapsed_s(a, b);
+    for (int l = 0; l < L; ++l) {
+      const double t = elapsed_s(E->ev_k0[l], E->ev_gemm[l]);
+      k3_time += t;
+      k3_bytes += (double)layer_groups[l] * E->S16;
+    }
+    for (int i = 0; i < k; ++i) draft_time += elapsed_s(E->ev_g0[i], E->ev_g1[i]);
+    draft_steps += k;
     const int accepted = hp[o_res], bonus_tok = hp[o_res + 1];
     std::vector<int> new_toks;
     for (int i = 0; i < accepted; ++i) new_toks.push_back(hp[o_win + i]);
@@ -747,6 +775,19 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
   rep["wall_s"] = wall;
   rep["profile"] = c.profile.to_json();
   rep["policy"] = policy_name(c.policy);
+  // kernel evidence: K3 (bf16 grouped verify FFN) per-launch device time (CUDA events on the
+  // launching stream) and algorithmic bytes (expert weights streamed); draft step = one graph
+  // replay (L x (K1 + K2) + LM head).
+  json ks;
+  ks["kernel_launches"] = launches;
+  ks["k3_launches"] = (long)L * (long)cycles.size();
+  ks["k3_time_s"] = k3_time;
+  ks["k3_weight_bytes"] = k3_bytes;
+  ks["k3_groups"] = k3_groups;
+  ks["draft_steps"] = draft_steps;
+  ks["draft_time_s"] = draft_time;
+  ks["draft_step_bytes"] = (double)m.L * m.K * E->S4 + (double)m.V * m.d * 2 + (double)m.L * m.E * m.d * 2;
+  rep["kernels"] = ks;
   return rep.dump();
 }
 
@@ -774,7 +815,7 @@ void destroy(mspq_engine* E) {
   cudaDeviceSynchronize();
   if (E->gexec) cudaGraphExecDestroy(E->gexec);
   if (E->graph) cudaGraphDestroy(E->graph);
-  for (auto v : {&E->ev_ready, &E->ev_gemm, &E->ev_w0, &E->ev_w1, &E->ev_row, &E->ev_pool})
+  for (auto v : {&E->ev_ready, &E->ev_gemm, &E->ev_w0, &E->ev_w1, &E->ev_row, &E->ev_pool, &E->ev_k0, &E->ev_g0, &E->ev_g1})
     for (auto ev : *v)
       if (ev) cudaEventDestroy(ev);
   for (auto ev : {E->ev_c0, E->ev_dend, E->ev_end, E->ev_t0})
@@ -832,7 +873,10 @@ int mspq_engine_create(const mspq_model_desc* md, const mspq_engine_opts* op, ms
       E->ev_w0.resize(m.L);
       E->ev_w1.resize(m.L);
       E->ev_row.resize(E->Tmax);
-      for (auto v : {&E->ev_gemm, &E->ev_w0, &E->ev_w1, &E->ev_row})
+      E->ev_g0.resize(E->Tmax);
+      E->ev_g1.resize(E->Tmax);
+      E->ev_k0.resize(m.L);
+      for (auto v : {&E->ev_gemm, &E->ev_w0, &E->ev_w1, &E->ev_row, &E->ev_k0, &E->ev_g0, &E->ev_g1})
         for (auto& ev : *v) CUDA_OK(cudaEventCreate(&ev));
       for (auto p : {&E->ev_c0, &E->ev_dend, &E->ev_end, &E->ev_t0}) CUDA_OK(cudaEventCreate(p));
       CUDA_OK(cudaStreamSynchronize(E->sc));
