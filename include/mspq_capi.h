@@ -98,27 +98,41 @@ int mspq_quantize_int4(const void* w_bf16, int rows, int cols, void* q_u32, void
                        void* stream);
 int mspq_embed(const void* embed, const void* pos, const int32_t* tokens,
                const int32_t* positions, int T, int d, float* h, void* stream);
-/* K1.  y/entry_of/prev_wts may be NULL (no combine); router NULL = norm only;
+/* K1.  y/entry_of/prev_wts may be NULL (no combine); y may hold y_splits partial planes
+ * y_split_stride floats apart (summed in order); router NULL = norm only;
  * elb_ids/elb_gates/elb_row NULL = no ELB write. */
 int mspq_gate_topk(float* h, const float* y, const int32_t* entry_of, const float* prev_wts,
-                   const void* gamma, const void* router, void* xn, int32_t* ids, float* wts,
+                   int y_splits, long long y_split_stride, const void* gamma, const void* router, void* xn, int32_t* ids, float* wts,
                    float* logits, int32_t* elb_ids, float* elb_gates, const int32_t* elb_row,
                    int layer, int L, int T, int d, int E, int K, float eps, void* stream);
 /* schedule arrays: n_groups[1], group_expert[G], group_buf[G], group_off[G+1], entry_tok[T*K],
- * entry_of[T*K] */
-int mspq_build_schedule(const int32_t* ids, int T, int K, int E, int32_t* n_groups,
+ * entry_of[T*K]; gbuf[E] (nullable) gives group_buf per expert (else group_buf = expert id) */
+int mspq_build_schedule(const int32_t* ids, int T, int K, int E, const int32_t* gbuf, int32_t* n_groups,
                         int32_t* group_expert, int32_t* group_buf, int32_t* group_off,
-                        int32_t* entry_tok, int32_t* entry_of, void* stream);
-/* K2: blobs = all L*E INT4 expert blobs, blob_bytes apart, indexed by layer*E + expert */
+                        int32_t* entry_tok, int32_t* entry_of, int32_t* entry_group, void* stream);
+/* K2: blobs = all L*E INT4 expert blobs, blob_bytes apart, indexed by layer*E + expert.
+ * max_group_size = most entries any group can have (= window tokens T; 1 selects the M=1 path) */
 int mspq_moe_int4(const int32_t* n_groups, const int32_t* group_expert, const int32_t* group_buf,
                   const int32_t* group_off, const int32_t* entry_tok, const void* xn, void* act,
                   float* y, const void* blobs, long long blob_bytes, int layer, int E, int d,
-                  int f, int max_groups, void* stream);
+                  int f, int max_groups, int max_group_size, void* stream);
 /* K3: pool = HBM slot pool, group_buf[g] = buffer index of group g's expert */
 int mspq_moe_bf16(const int32_t* n_groups, const int32_t* group_expert, const int32_t* group_buf,
                   const int32_t* group_off, const int32_t* entry_tok, const void* xn, void* act,
                   float* y, const void* pool, long long blob_bytes, int E, int d, int f,
-                  int max_groups, void* stream);
+                  int max_groups, int max_group_size, void* stream);
+/* K3 on tcgen05 (umma.cu): the same grouped FFN over TILE-MAJOR bf16 experts (each 128x64
+ * block a contiguous SW128 K-major image, see mspq_tile_bf16).  Runs gather -> W13 GEMM ->
+ * SiLU*up -> W2 GEMM.  split1/split2 = K splits of the two GEMMs; y = [split2][T*K][d] fp32
+ * partial planes (feed mspq_gate_topk with y_splits = split2, stride = T*K*d). */
+long long mspq_moe_bf16_tc_ws_bytes(int d, int f, int T, int K, int max_groups, int max_split1);
+int mspq_moe_bf16_tc(const int32_t* n_groups, const int32_t* group_expert, const int32_t* group_buf,
+                     const int32_t* group_off, const int32_t* entry_tok, const int32_t* entry_group,
+                     const void* xn, const void* pool, long long blob_bytes, int d, int f, int T,
+                     int K, int max_groups, int split1, int split2, void* ws, float* y,
+                     void* stream);
+/* row-major [rows][cols] bf16 -> tile-major [rows/128][cols/64] SW128 images (16 KB each) */
+int mspq_tile_bf16(const void* src, int rows, int cols, void* dst, void* stream);
 int mspq_lm_head(const void* xn, const void* lm, int T, int V, int d, float* logits,
                  void* stream);
 int mspq_argmax(const float* logits, int T, int V, int32_t* out, void* stream);
@@ -165,10 +179,10 @@ int mspq_cache_configure(mspq_cache* c, int mode, int policy, const int* caps, i
 int mspq_cache_view_get(mspq_cache* c, mspq_cache_view* v);
 int mspq_cache_begin_cycle(mspq_cache* c, int k, void* stream);
 int mspq_cache_plan_row(mspq_cache* c, int row, void* stream);
+/* verify step of one layer: policy steps for every (slot, expert) of tgt[nslots][K]; writes
+ * gbuf[E] = HBM buffer each required expert is read from (-2 = not required) */
 int mspq_cache_verify_layer(mspq_cache* c, int layer, int nslots, const int32_t* tgt,
-                            int32_t* n_groups, int32_t* group_expert, int32_t* group_buf,
-                            int32_t* group_off, int32_t* entry_tok, int32_t* entry_of,
-                            void* stream);
+                            int32_t* gbuf, void* stream);
 /* token-major replay of one cycle over device trace arrays (target/draft [n][L][K] int32,
  * gates [n][L][K] double or NULL).  out_*: counts[6], batches[kmax][3], jit_rows[kmax][2],
  * cov[L][2], step[(kmax+1)*L][2], flush_keys[L*E] */

@@ -37,10 +37,13 @@ _SIGS = [
     ("mspq_fill_expert", c_int, [c_ull, c_int, c_int, c_int, c_int, c_float, c_float, c_void_p, c_void_p]),
     ("mspq_quantize_int4", c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p]),
     ("mspq_embed", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p]),
-    ("mspq_gate_topk", c_int, [c_void_p] * 13 + [c_int] * 6 + [c_float, c_void_p]),
-    ("mspq_build_schedule", c_int, [c_void_p, c_int, c_int, c_int] + [c_void_p] * 7),
-    ("mspq_moe_int4", c_int, [c_void_p] * 9 + [c_ll] + [c_int] * 5 + [c_void_p]),
-    ("mspq_moe_bf16", c_int, [c_void_p] * 9 + [c_ll] + [c_int] * 4 + [c_void_p]),
+    ("mspq_gate_topk", c_int, [c_void_p] * 4 + [c_int, c_ll] + [c_void_p] * 9 + [c_int] * 6 + [c_float, c_void_p]),
+    ("mspq_build_schedule", c_int, [c_void_p, c_int, c_int, c_int] + [c_void_p] * 9),
+    ("mspq_moe_int4", c_int, [c_void_p] * 9 + [c_ll] + [c_int] * 6 + [c_void_p]),
+    ("mspq_moe_bf16", c_int, [c_void_p] * 9 + [c_ll] + [c_int] * 5 + [c_void_p]),
+    ("mspq_moe_bf16_tc_ws_bytes", c_ll, [c_int] * 6),
+    ("mspq_moe_bf16_tc", c_int, [c_void_p] * 8 + [c_ll] + [c_int] * 7 + [c_void_p] * 3),
+    ("mspq_tile_bf16", c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p]),
     ("mspq_lm_head", c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p]),
     ("mspq_argmax", c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p]),
     ("mspq_argmax_advance", c_int, [c_void_p, c_int] + [c_void_p] * 6),
@@ -54,7 +57,7 @@ _SIGS = [
     ("mspq_cache_view_get", c_int, [c_void_p, c_void_p]),
     ("mspq_cache_begin_cycle", c_int, [c_void_p, c_int, c_void_p]),
     ("mspq_cache_plan_row", c_int, [c_void_p, c_int, c_void_p]),
-    ("mspq_cache_verify_layer", c_int, [c_void_p, c_int, c_int] + [c_void_p] * 8),
+    ("mspq_cache_verify_layer", c_int, [c_void_p, c_int, c_int] + [c_void_p] * 3),
     ("mspq_cache_replay_cycle", c_int, [c_void_p] * 4 + [c_int] * 3 + [c_void_p] * 7),
     ("mspq_replay", c_int, [c_int, c_char_p, c_char_p, ctypes.POINTER(c_void_p)]),
     ("mspq_governor", c_int, [c_char_p, ctypes.POINTER(c_void_p)]),

@@ -15,7 +15,7 @@ JSON_DIR = "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_front
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I" + CSRC,
           "-I" + os.path.join(ROOT, "include"), "-I" + JSON_DIR]
-SOURCES = ["kernels_model.cu", "ctl.cu", "capi.cu", "engine.cpp", "live.cpp"]
+SOURCES = ["kernels_model.cu", "umma.cu", "ctl.cu", "capi.cu", "engine.cpp", "live.cpp"]
 
 
 def _needs(src, obj, deps):
@@ -35,8 +35,9 @@ def build(verbose=False, force=False):
         obj = os.path.join(OBJ, s + ".o")
         if force or _needs(src, obj, headers):
             cmd = [NVCC] + ARCH + COMMON + ["-x", "cu" if s.endswith(".cu") else "c++", "-c", src, "-o", obj]
-            if s.endswith(".cpp"):
-                cmd = [NVCC] + COMMON + ["-std=c++17", "-c", src, "-o", obj]
+            if s.endswith(".cpp"):  # host-only C++: g++ against the CUDA runtime headers
+                cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-I" + CSRC, "-I" + os.path.join(ROOT, "include"),
+                       "-I" + JSON_DIR, "-I/usr/local/cuda/include", "-c", src, "-o", obj]
             jobs.append(cmd)
 
     def run(cmd):

@@ -67,42 +67,82 @@ int mspq_embed(const void* embed, const void* pos, const int32_t* tokens, const 
      "embed");
 }
 int mspq_gate_topk(float* h, const float* y, const int32_t* entry_of, const float* prev_wts,
-                   const void* gamma, const void* router, void* xn, int32_t* ids, float* wts,
+                   int y_splits, long long y_split_stride, const void* gamma, const void* router, void* xn, int32_t* ids, float* wts,
                    float* logits, int32_t* elb_ids, float* elb_gates, const int32_t* elb_row,
                    int layer, int L, int T, int d, int E, int K, float eps, void* stream) {
   if (d % 256 || K > 64 || E > 1024 || K > E)
     return set_error(MSPQ_ERR_SHAPE_MISMATCH, "gate_topk: need d%256==0, K<=min(E,64), E<=1024");
   RouteArgs a{h, y, entry_of, prev_wts, (const uint16_t*)gamma, (const uint16_t*)router,
-              (uint16_t*)xn, ids, wts, logits, elb_ids, elb_gates, elb_row, layer, L, d, E, K, eps};
+              (uint16_t*)xn, ids, wts, logits, y_splits < 1 ? 1 : y_splits, y_split_stride,
+              elb_ids, elb_gates, elb_row, layer, L, d, E, K, eps};
   CK(launch_route(a, T, ST(stream)), "gate_topk");
 }
-int mspq_build_schedule(const int32_t* ids, int T, int K, int E, int32_t* n_groups,
+int mspq_build_schedule(const int32_t* ids, int T, int K, int E, const int32_t* gbuf, int32_t* n_groups,
                         int32_t* group_expert, int32_t* group_buf, int32_t* group_off,
-                        int32_t* entry_tok, int32_t* entry_of, void* stream) {
-  SchedPtrs s{n_groups, group_expert, group_buf, group_off, entry_tok, entry_of};
-  CK(launch_build_schedule(ids, T, K, E, s, ST(stream)), "build_schedule");
+                        int32_t* entry_tok, int32_t* entry_of, int32_t* entry_group, void* stream) {
+  if (E > 1024 || T * K > 4096) return set_error(MSPQ_ERR_SHAPE_MISMATCH, "build_schedule: E<=1024, T*K<=4096");
+  SchedPtrs s{n_groups, group_expert, group_buf, group_off, entry_tok, entry_of, entry_group};
+  CK(launch_build_schedule(ids, T, K, E, gbuf, s, ST(stream)), "build_schedule");
 }
 int mspq_moe_int4(const int32_t* n_groups, const int32_t* group_expert, const int32_t* group_buf,
                   const int32_t* group_off, const int32_t* entry_tok, const void* xn, void* act,
                   float* y, const void* blobs, long long blob_bytes, int layer, int E, int d, int f,
-                  int max_groups, void* stream) {
+                  int max_groups, int max_group_size, void* stream) {
   if (d % 256 || f % 256) return set_error(MSPQ_ERR_SHAPE_MISMATCH, "moe_int4: d, f % 256");
   SchedPtrs s{(int32_t*)n_groups, (int32_t*)group_expert, (int32_t*)group_buf, (int32_t*)group_off,
-              (int32_t*)entry_tok, nullptr};
+              (int32_t*)entry_tok, nullptr, nullptr};
   ExpertArgs a{s, (const uint16_t*)xn, (uint16_t*)act, y, (const unsigned char*)blobs, blob_bytes,
                layer, E, d, f};
-  CK(launch_expert(a, true, max_groups, ST(stream)), "moe_int4");
+  CK(launch_expert(a, true, max_groups, max_group_size, ST(stream)), "moe_int4");
 }
 int mspq_moe_bf16(const int32_t* n_groups, const int32_t* group_expert, const int32_t* group_buf,
                   const int32_t* group_off, const int32_t* entry_tok, const void* xn, void* act,
                   float* y, const void* pool, long long blob_bytes, int E, int d, int f,
-                  int max_groups, void* stream) {
+                  int max_groups, int max_group_size, void* stream) {
   if (d % 256 || f % 256) return set_error(MSPQ_ERR_SHAPE_MISMATCH, "moe_bf16: d, f % 256");
   SchedPtrs s{(int32_t*)n_groups, (int32_t*)group_expert, (int32_t*)group_buf, (int32_t*)group_off,
-              (int32_t*)entry_tok, nullptr};
+              (int32_t*)entry_tok, nullptr, nullptr};
   ExpertArgs a{s, (const uint16_t*)xn, (uint16_t*)act, y, (const unsigned char*)pool, blob_bytes,
                0, E, d, f};
-  CK(launch_expert(a, false, max_groups, ST(stream)), "moe_bf16");
+  CK(launch_expert(a, false, max_groups, max_group_size, ST(stream)), "moe_bf16");
+}
+static int tc_bn(int T) { return T <= 16 ? 16 : 32; }
+long long mspq_moe_bf16_tc_ws_bytes(int d, int f, int T, int K, int max_groups, int max_split1) {
+  const long long BN = tc_bn(T), N = (long long)T * K;
+  auto al = [](long long b) { return (b + 1023) / 1024 * 1024; };
+  return al(max_groups * (d / 64) * BN * 128) + al((long long)max_split1 * N * 2 * f * 4) +
+         al(max_groups * (f / 64) * BN * 128);
+}
+int mspq_moe_bf16_tc(const int32_t* n_groups, const int32_t* group_expert, const int32_t* group_buf,
+                     const int32_t* group_off, const int32_t* entry_tok, const int32_t* entry_group,
+                     const void* xn, const void* pool, long long blob_bytes, int d, int f, int T, int K,
+                     int max_groups, int split1, int split2, void* ws, float* y, void* stream) {
+  if (d % 128 || f % 128 || T > 32 || split1 < 1 || split2 < 1)
+    return set_error(MSPQ_ERR_SHAPE_MISMATCH, "moe_bf16_tc: d, f % 128, T <= 32, splits >= 1");
+  const int BN = tc_bn(T);
+  const long long N = (long long)T * K;
+  auto al = [](long long b) { return (b + 1023) / 1024 * 1024; };
+  unsigned char* b1 = (unsigned char*)ws;
+  float* p1 = (float*)(b1 + al(max_groups * (d / 64) * BN * 128));
+  unsigned char* b2 = (unsigned char*)p1 + al((long long)split1 * N * 2 * f * 4);
+  SchedPtrs s{(int32_t*)n_groups, (int32_t*)group_expert, (int32_t*)group_buf, (int32_t*)group_off,
+              (int32_t*)entry_tok, nullptr, (int32_t*)entry_group};
+  cudaStream_t st = ST(stream);
+  cudaError_t e = launch_gather_b((const uint16_t*)xn, d, s, max_groups, d, BN, b1, st);
+  if (e != cudaSuccess) return cuda_status(e, "gather_b");
+  UmmaArgs u1{(const unsigned char*)pool, blob_bytes, 0, 2 * f, d, n_groups, group_buf, group_off, b1, p1,
+              N * 2 * f, split1};
+  e = launch_umma_grouped(u1, max_groups, BN, st);
+  if (e != cudaSuccess) return cuda_status(e, "umma W13");
+  e = launch_finalize_act(p1, split1, N * 2 * f, s, entry_group, (int)N, f, BN, b2, st);
+  if (e != cudaSuccess) return cuda_status(e, "finalize_act");
+  UmmaArgs u2{(const unsigned char*)pool, blob_bytes, (long long)2 * f * d * 2, d, f, n_groups, group_buf,
+              group_off, b2, y, N * d, split2};
+  CK(launch_umma_grouped(u2, max_groups, BN, st), "umma W2");
+}
+int mspq_tile_bf16(const void* src, int rows, int cols, void* dst, void* stream) {
+  if (rows % 128 || cols % 64) return set_error(MSPQ_ERR_SHAPE_MISMATCH, "tile_bf16: rows%128, cols%64");
+  CK(launch_tile_bf16((const uint16_t*)src, rows, cols, (unsigned char*)dst, ST(stream)), "tile_bf16");
 }
 int mspq_lm_head(const void* xn, const void* lm, int T, int V, int d, float* logits, void* stream) {
   CK(launch_lm_head((const uint16_t*)xn, (const uint16_t*)lm, T, V, d, logits, ST(stream)), "lm_head");
@@ -243,12 +283,9 @@ int mspq_cache_plan_row(mspq_cache* c, int row, void* stream) {
   CK(ctl_plan_row(c->C, row, ST(stream)), "cache_plan_row");
 }
 int mspq_cache_verify_layer(mspq_cache* c, int layer, int nslots, const int32_t* tgt,
-                            int32_t* n_groups, int32_t* group_expert, int32_t* group_buf,
-                            int32_t* group_off, int32_t* entry_tok, int32_t* entry_of,
-                            void* stream) {
+                            int32_t* gbuf, void* stream) {
   if (nslots > c->kmax + 1) return set_error(MSPQ_ERR_K_OUT_OF_RANGE, "nslots > kmax+1");
-  SchedPtrs s{n_groups, group_expert, group_buf, group_off, entry_tok, entry_of};
-  CK(ctl_verify_layer(c->C, layer, nslots, tgt, s, ST(stream)), "cache_verify_layer");
+  CK(ctl_verify_layer(c->C, layer, nslots, tgt, gbuf, ST(stream)), "cache_verify_layer");
 }
 int mspq_cache_replay_cycle(mspq_cache* c, const int32_t* target, const int32_t* draft,
                             const double* gates, int pos, int k_eff, int head_pos,

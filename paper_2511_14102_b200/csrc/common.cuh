@@ -112,11 +112,30 @@ MSPQ_D uint4 ldg_nc_v4(const void* p) {
 
 // Fixed-order warp dot over n bf16 (n % 256 == 0): lane owns 8-element chunks lane, lane+32,
 // ... accumulated with fmaf in order, then an xor butterfly.  == orc_warp_dot.
+// Loads are issued 4 chunks ahead of the (unchanged) accumulation order for memory-level
+// parallelism.
 MSPQ_D float warp_dot_bf16(const uint16_t* __restrict__ x, const uint16_t* __restrict__ w, int n,
                            int lane) {
   float acc = 0.0f;
   const int nchunks = n >> 3;
-  for (int c = lane; c < nchunks; c += 32) {
+  int c = lane;
+  for (; c + 96 < nchunks; c += 128) {
+    uint4 wv[4], xv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      wv[u] = ldg_nc_v4(w + 8 * (c + 32 * u));
+      xv[u] = *reinterpret_cast<const uint4*>(x + 8 * (c + 32 * u));
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      float xf[8], wf[8];
+      bf16x8_to_f32(xv[u], xf);
+      bf16x8_to_f32(wv[u], wf);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc = fmaf(xf[e], wf[e], acc);
+    }
+  }
+  for (; c < nchunks; c += 32) {
     uint4 xv = *reinterpret_cast<const uint4*>(x + 8 * c);
     uint4 wv = ldg_nc_v4(w + 8 * c);
     float xf[8], wf[8];

@@ -43,7 +43,7 @@ struct Ctx {
   bool emit = true;     // copy requests (live engine); replay runs the control plane only
 };
 
-MSPQ_D volatile int* V(int* p) { return (volatile int*)p; }
+MSPQ_D int* V(int* p) { return p; }
 
 MSPQ_D int get(const Ctx& x, int slot) { return V(x.C.scal)[slot]; }
 MSPQ_D void put(const Ctx& x, int slot, int v) {
@@ -59,10 +59,10 @@ MSPQ_D bool contains(const Ctx& x, int key) { return V(x.C.res)[key] >= 0; }
 
 MSPQ_D void touch(const Ctx& x, int key) {
   if (lane_id() == 0) {
-    volatile unsigned long long* clk = (volatile unsigned long long*)x.C.clock;
+    unsigned long long* clk = (unsigned long long*)x.C.clock;
     unsigned long long c = *clk + 1;
     *clk = c;
-    ((volatile unsigned long long*)x.C.stamp)[key] = c;
+    ((unsigned long long*)x.C.stamp)[key] = c;
   }
   __syncwarp();
 }
@@ -81,7 +81,7 @@ MSPQ_D int lru_victim(const Ctx& x, int layer) {
   int bk = -1;
   for (int key = key_lo(x, layer) + lane_id(); key < key_hi(x, layer); key += 32)
     if (contains(x, key)) {
-      unsigned long long s = ((volatile unsigned long long*)x.C.stamp)[key];
+      unsigned long long s = ((unsigned long long*)x.C.stamp)[key];
       if (s < best) {
         best = s;
         bk = key;
@@ -135,12 +135,12 @@ MSPQ_D int belady_victim(const Ctx& x, int now, int visible, int layer) {
 // step's GEMM reads (first-request buffer of this layer), which is parked until the step ends.
 MSPQ_D void erase(const Ctx& x, int key) {
   if (lane_id() == 0) {
-    volatile int* res = V(x.C.res);
+    int* res = V(x.C.res);
     int buf = res[key];
     res[key] = -1;
     V(x.C.lsize)[key / x.C.E] -= 1;
     V(x.C.scal)[S_TOTAL] -= 1;
-    const bool defer = x.gb && key / x.C.E == x.step_layer && ((volatile int*)x.gb)[key % x.C.E] == buf;
+    const bool defer = x.gb && key / x.C.E == x.step_layer && ((int*)x.gb)[key % x.C.E] == buf;
     if (buf >= 0) {
       if (defer) {
         int np = V(x.C.scal)[S_NPEND];
@@ -158,7 +158,7 @@ MSPQ_D void erase(const Ctx& x, int key) {
 
 MSPQ_D void insert_key(const Ctx& x, int key) {
   if (lane_id() == 0) {
-    volatile int* scal = V(x.C.scal);
+    int* scal = V(x.C.scal);
     int nf = scal[S_NFREE];
     int buf = -1;
     if (nf > 0) {
@@ -168,10 +168,10 @@ MSPQ_D void insert_key(const Ctx& x, int key) {
       scal[S_OVERFLOW] = 1;
     }
     V(x.C.res)[key] = buf;
-    volatile unsigned long long* clk = (volatile unsigned long long*)x.C.clock;
+    unsigned long long* clk = (unsigned long long*)x.C.clock;
     unsigned long long c = *clk + 1;
     *clk = c;
-    ((volatile unsigned long long*)x.C.stamp)[key] = c;
+    ((unsigned long long*)x.C.stamp)[key] = c;
     V(x.C.lsize)[key / x.C.E] += 1;
     scal[S_TOTAL] += 1;
   }
@@ -180,10 +180,10 @@ MSPQ_D void insert_key(const Ctx& x, int key) {
 
 MSPQ_D void log_event(const Ctx& x, int kind, int tag, int key, int hit, int victim) {
   if (lane_id() == 0) {
-    volatile int* scal = V(x.C.scal);
+    int* scal = V(x.C.scal);
     int n = scal[S_NLOG];
     if (x.C.log && n < x.C.log_cap) {
-      volatile int* ev = V(x.C.log) + (int64_t)n * 6;
+      int* ev = V(x.C.log) + (int64_t)n * 6;
       ev[0] = kind;
       ev[1] = tag;
       ev[2] = key;
@@ -199,10 +199,10 @@ MSPQ_D void log_event(const Ctx& x, int kind, int tag, int key, int hit, int vic
 MSPQ_D void copy_request(const Ctx& x, int key, int kind) {
   if (!x.emit) return;
   if (lane_id() == 0) {
-    volatile int* scal = V(x.C.scal);
+    int* scal = V(x.C.scal);
     int n = scal[S_NREQ];
     if (n < x.C.req_cap) {
-      volatile int* rq = V(x.C.req) + (int64_t)n * 3;
+      volatile int* rq = (volatile int*)x.C.req + (int64_t)n * 3;
       rq[0] = key;
       rq[1] = V(x.C.res)[key];
       rq[2] = kind;
@@ -281,7 +281,7 @@ MSPQ_D void publish(const Ctx& x) {
 
 MSPQ_D void release_pending(const Ctx& x) {
   if (lane_id() == 0) {
-    volatile int* scal = V(x.C.scal);
+    int* scal = V(x.C.scal);
     int np = scal[S_NPEND], nf = scal[S_NFREE];
     for (int i = 0; i < np; ++i) V(x.C.free_stack)[nf + i] = V(x.C.pending)[i];
     scal[S_NFREE] = nf + np;
@@ -312,11 +312,11 @@ MSPQ_D void absorb_row(const Ctx& x, int r, const unsigned char* snap_or_null) {
       const int e = x.elb.ids[((int64_t)r * L + l) * K + j];
       const int key = l * E + e;
       const bool res = snap_or_null ? snap_or_null[key] != 0 : contains(x, key);
-      if (res || ((volatile unsigned char*)x.C.sched)[key]) continue;
+      if (res || ((unsigned char*)x.C.sched)[key]) continue;
       const double c = conf_of(x, r, l, j);
       if (lane_id() == 0) {
-        volatile int* cf = V(x.C.cand_first);
-        volatile double* cc = (volatile double*)x.C.cand_conf;
+        int* cf = V(x.C.cand_first);
+        double* cc = x.C.cand_conf;
         if (cf[key] < 0) {
           cf[key] = r;
           cc[key] = c;
@@ -334,9 +334,9 @@ MSPQ_D int best_candidate(const Ctx& x, int k) {
   int bf = INT_MAX, bk = -1;
   const int n = x.C.L * x.C.E;
   for (int key = lane_id(); key < n; key += 32) {
-    const int f = ((volatile int*)x.C.cand_first)[key];
+    const int f = (x.C.cand_first)[key];
     if (f < 0) continue;
-    const double p = ((volatile double*)x.C.cand_conf)[key] * (double)(k - f) / (double)k;
+    const double p = (x.C.cand_conf)[key] * (double)(k - f) / (double)k;
     if (bk < 0 || p > bp || (p == bp && (f < bf || (f == bf && key < bk)))) {
       bp = p;
       bf = f;
@@ -358,7 +358,7 @@ MSPQ_D int best_candidate(const Ctx& x, int k) {
 
 MSPQ_D void mark_scheduled(const Ctx& x, int key) {
   if (lane_id() == 0) {
-    ((volatile unsigned char*)x.C.sched)[key] = 1;
+    ((unsigned char*)x.C.sched)[key] = 1;
     V(x.C.cand_first)[key] = -1;
   }
   __syncwarp();
@@ -366,7 +366,7 @@ MSPQ_D void mark_scheduled(const Ctx& x, int key) {
 
 MSPQ_D void plan_item(const Ctx& x, int row, int key, int phase) {
   if (lane_id() == 0) {
-    volatile int* scal = V(x.C.scal);
+    int* scal = V(x.C.scal);
     int n = scal[S_NPLAN];
     if (n < x.C.plan_cap) {
       V(x.C.plan)[n * 3 + 0] = row;
@@ -397,7 +397,7 @@ MSPQ_D void phase3_flush(const Ctx& x, int i, int k, F&& on_item) {
   for (int f = 0; f < k; ++f)
     for (int base = 0; base < n; base += 32) {
       const int key = base + lane_id();
-      const bool m = key < n && ((volatile int*)x.C.cand_first)[key] == f;
+      const bool m = key < n && (x.C.cand_first)[key] == f;
       unsigned bal = __ballot_sync(0xffffffffu, m);
       while (bal) {
         const int b = __ffs(bal) - 1;
@@ -414,8 +414,8 @@ MSPQ_D void clear_planner(const Ctx& x) {
   const int n = x.C.L * x.C.E;
   for (int key = lane_id(); key < n; key += 32) {
     V(x.C.cand_first)[key] = -1;
-    ((volatile unsigned char*)x.C.sched)[key] = 0;
-    ((volatile unsigned char*)x.C.snap)[key] = contains(x, key) ? 1 : 0;
+    ((unsigned char*)x.C.sched)[key] = 0;
+    ((unsigned char*)x.C.snap)[key] = contains(x, key) ? 1 : 0;
   }
   __syncwarp();
 }
@@ -486,9 +486,9 @@ __global__ void k_ctl_plan_row(CtlDev C, int i) {
 }
 
 // Verify layer l over nslots window slots (slot s < k has ELB row s; slot k is unpredicted).
-// tgt[s*K + j] = target expert ids.  Emits the grouped-GEMM schedule for the layer.
+// tgt[s*K + j] = target expert ids.  Emits the per-expert first-request buffer table.
 __global__ void k_ctl_verify_layer(CtlDev C, int l, int nslots, const int32_t* __restrict__ tgt,
-                                   SchedPtrs sched) {
+                                   int32_t* __restrict__ gbuf_out) {
   const int k = V(C.scal)[S_K];
   Ctx x{C, {C.elb_ids, C.elb_gates, nullptr, k}};
   const int E = C.E, K = C.K, L = C.L;
@@ -554,32 +554,13 @@ __global__ void k_ctl_verify_layer(CtlDev C, int l, int nslots, const int32_t* _
       __syncwarp();
     }
   }
-  // grouped-GEMM schedule: experts ascending, entries in window order (scheduler.cpp:339-357)
-  if (lane_id() == 0) {
-    int g = 0, nent = 0;
-    for (int e = 0; e < E; ++e) {
-      if (gbuf[e] == -2) continue;
-      const int start = nent;
-      for (int s = 0; s < nslots; ++s)
-        for (int j = 0; j < K; ++j)
-          if (tgt[s * K + j] == e) {
-            sched.entry_tok[nent] = s;
-            sched.entry_of[s * K + j] = nent;
-            ++nent;
-          }
-      sched.group_expert[g] = e;
-      sched.group_buf[g] = gbuf[e];
-      sched.group_off[g] = start;
-      ++g;
-    }
-    sched.group_off[g] = nent;
-    *sched.n_groups = g;
-    if (C.hsched) {
-      volatile int* hs = (volatile int*)C.hsched;
-      hs[0] = g;
-      for (int q = 0; q < g; ++q) hs[1 + q] = sched.group_buf[q];
-    }
+  // first-request buffer of every expert of this layer (-2 = not required): the grouped-GEMM
+  // schedule (k_build_schedule) reads it; the host waits on exactly these buffers' copies.
+  for (int e = lane_id(); e < E; e += 32) {
+    gbuf_out[e] = gbuf[e];
+    if (C.hsched) ((volatile int*)C.hsched)[1 + e] = gbuf[e];
   }
+  if (lane_id() == 0 && C.hsched) ((volatile int*)C.hsched)[0] = E;
   __syncwarp();
   release_pending(x);
   publish(x);
@@ -786,9 +767,9 @@ cudaError_t ctl_plan_row(const CtlDev& C, int i, cudaStream_t st) {
   k_ctl_plan_row<<<1, 32, 0, st>>>(C, i);
   return cudaGetLastError();
 }
-cudaError_t ctl_verify_layer(const CtlDev& C, int l, int nslots, const int32_t* tgt, SchedPtrs s,
+cudaError_t ctl_verify_layer(const CtlDev& C, int l, int nslots, const int32_t* tgt, int32_t* gbuf,
                              cudaStream_t st) {
-  k_ctl_verify_layer<<<1, 32, 0, st>>>(C, l, nslots, tgt, s);
+  k_ctl_verify_layer<<<1, 32, 0, st>>>(C, l, nslots, tgt, gbuf);
   return cudaGetLastError();
 }
 cudaError_t ctl_replay_cycle(const CtlDev& C, const ReplayTrace& tr, int pos, int k_eff,

@@ -46,7 +46,7 @@ struct CtlDev {
   int* cov;                    // [L][2] live: (hits, size) of each layer's required union
   int* step;                   // [L][nslots][2] live: per (layer, slot) step coverage counts
   int* hstat;                  // [S_COUNT] mapped pinned host mirror of scal (written at exit)
-  int* hsched;                 // [1+E] mapped: n_groups, group_buf[] of the last verify step
+  int* hsched;                 // [1+E] mapped: E, then first-request buffer per expert (-2 unused)
 };
 
 struct ReplayTrace {
@@ -67,7 +67,7 @@ struct ReplayOut {
 cudaError_t ctl_reset(const CtlDev& C, int nbuf, cudaStream_t st);
 cudaError_t ctl_begin_cycle(const CtlDev& C, int k, cudaStream_t st);
 cudaError_t ctl_plan_row(const CtlDev& C, int i, cudaStream_t st);
-cudaError_t ctl_verify_layer(const CtlDev& C, int l, int nslots, const int32_t* tgt, SchedPtrs s,
+cudaError_t ctl_verify_layer(const CtlDev& C, int l, int nslots, const int32_t* tgt, int32_t* gbuf,
                              cudaStream_t st);
 cudaError_t ctl_replay_cycle(const CtlDev& C, const ReplayTrace& tr, int pos, int k_eff,
                              int head_pos, const ReplayOut& o, cudaStream_t st);

@@ -15,6 +15,22 @@ struct SchedPtrs {
   int32_t* group_off;     // [G+1] entry offsets
   int32_t* entry_tok;     // [N]   window token of each entry
   int32_t* entry_of;      // [T*K] entry index of (token, k-slot)
+  int32_t* entry_group;   // [N]   group of each entry (nullable)
+};
+
+// tcgen05 grouped GEMM (umma.cu): one matrix (W13 or W2) of every group's expert
+struct UmmaArgs {
+  const unsigned char* w_base;  // slot pool of tile-major bf16 expert blobs
+  int64_t blob_bytes;
+  int64_t w_off;                // byte offset of the matrix inside a blob
+  int rows, kdim;               // rows (2f | d), K (d | f)
+  const int32_t* n_groups;
+  const int32_t* group_buf;
+  const int32_t* group_off;
+  const unsigned char* bimg;    // [G][kdim/64][BN*128] swizzled B images
+  float* out;                   // [splits][N][rows] fp32 partial planes
+  int64_t out_split_stride;
+  int splits;
 };
 
 struct ExpertArgs {
@@ -46,6 +62,8 @@ struct RouteArgs {
   int32_t* ids;              // [T][K]
   float* wts;                // [T][K]
   float* logits;             // [T][E] (nullable)
+  int y_splits;              // K-split partial planes of y, summed in order by the combine
+  int64_t y_split_stride;
   int32_t* elb_ids;          // [kmax][L][K] (nullable)
   float* elb_gates;
   const int32_t* elb_row;    // device row counter
@@ -53,6 +71,13 @@ struct RouteArgs {
   float eps;
 };
 
+cudaError_t launch_umma_grouped(const UmmaArgs& a, int max_groups, int BN, cudaStream_t st);
+cudaError_t launch_gather_b(const uint16_t* x, int ld, SchedPtrs s, int max_groups, int kdim, int BN,
+                            unsigned char* img, cudaStream_t st);
+cudaError_t launch_finalize_act(const float* p1, int splits, int64_t split_stride, SchedPtrs s,
+                                const int32_t* entry_group, int n_entries, int f, int BN, unsigned char* img,
+                                cudaStream_t st);
+cudaError_t launch_tile_bf16(const uint16_t* src, int rows, int cols, unsigned char* dst, cudaStream_t st);
 cudaError_t launch_fill_bf16(uint64_t seed, uint64_t tensor, float scale, int kind, uint16_t* out,
                              int64_t n, int64_t start, cudaStream_t st);
 cudaError_t launch_fill_expert(uint64_t seed, int cl, int ce, int d, int f, float a_up,
@@ -62,9 +87,10 @@ cudaError_t launch_quantize(const uint16_t* w, int rows, int cols, uint32_t* q, 
 cudaError_t launch_embed(const uint16_t* embed, const uint16_t* pos, const int32_t* tokens,
                          const int32_t* positions, int T, int d, float* h, cudaStream_t st);
 cudaError_t launch_route(const RouteArgs& a, int T, cudaStream_t st);
-cudaError_t launch_build_schedule(const int32_t* ids, int T, int K, int E, SchedPtrs s,
-                                  cudaStream_t st);
-cudaError_t launch_expert(const ExpertArgs& a, bool int4, int max_groups, cudaStream_t st);
+cudaError_t launch_build_schedule(const int32_t* ids, int T, int K, int E, const int32_t* gbuf,
+                                  SchedPtrs s, cudaStream_t st);
+cudaError_t launch_expert(const ExpertArgs& a, bool int4, int max_groups, int max_group_size,
+                          cudaStream_t st);
 cudaError_t launch_lm_head(const uint16_t* xn, const uint16_t* lm, int T, int V, int d,
                            float* logits, cudaStream_t st);
 cudaError_t launch_argmax(const float* logits, int T, int V, int32_t* out, DraftState ds,

@@ -118,7 +118,12 @@ __global__ void __launch_bounds__(256) k_resid_norm_route(RouteArgs a) {
       float cb[4] = {0.f, 0.f, 0.f, 0.f};
       for (int j = 0; j < a.K; ++j) {
         const float w = a.prev_wts[t * a.K + j];
-        const float4 yv = reinterpret_cast<const float4*>(a.y + (int64_t)a.entry_of[t * a.K + j] * a.d)[c];
+        const float* yb = a.y + (int64_t)a.entry_of[t * a.K + j] * a.d;
+        float4 yv = reinterpret_cast<const float4*>(yb)[c];
+        for (int sp = 1; sp < a.y_splits; ++sp) {  // K-split partial planes, fixed order
+          const float4 p = reinterpret_cast<const float4*>(yb + sp * a.y_split_stride)[c];
+          yv = make_float4(__fadd_rn(yv.x, p.x), __fadd_rn(yv.y, p.y), __fadd_rn(yv.z, p.z), __fadd_rn(yv.w, p.w));
+        }
         cb[0] = __fadd_rn(cb[0], __fmul_rn(w, yv.x));
         cb[1] = __fadd_rn(cb[1], __fmul_rn(w, yv.y));
         cb[2] = __fadd_rn(cb[2], __fmul_rn(w, yv.z));
@@ -198,30 +203,62 @@ __global__ void __launch_bounds__(256) k_resid_norm_route(RouteArgs a) {
 
 // ============================================================================ schedule
 // Groups (token, k-slot) entries by expert, ascending expert id, window order inside a group
-// (reorder_verification, scheduler.cpp:339-357).  Used for the draft; the verify schedule is
-// built by the cache controller (it also assigns HBM buffers).
-__global__ void k_build_schedule(const int32_t* __restrict__ ids, int T, int K, int E,
-                                 SchedPtrs s) {
-  if (threadIdx.x != 0) return;
-  int g = 0, n = 0;
-  for (int e = 0; e < E; ++e) {
-    int start = n;
-    for (int t = 0; t < T; ++t)
-      for (int j = 0; j < K; ++j)
-        if (ids[t * K + j] == e) {
-          s.entry_tok[n] = t;
-          s.entry_of[t * K + j] = n;
-          ++n;
-        }
-    if (n > start) {
-      s.group_expert[g] = e;
-      s.group_buf[g] = e;
-      s.group_off[g] = start;
-      ++g;
+// (reorder_verification, scheduler.cpp:339-357).  One CTA: thread e owns expert e; block scans
+// give group and entry offsets.  gbuf (verify) supplies each group's HBM slot-pool buffer.
+__global__ void __launch_bounds__(1024) k_build_schedule(const int32_t* __restrict__ ids, int T, int K, int E,
+                                                         const int32_t* __restrict__ gbuf, SchedPtrs s) {
+  __shared__ int sid[4096];
+  __shared__ int wsum[2][32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int n = T * K;
+  for (int i = tid; i < n; i += blockDim.x) sid[i] = ids[i];
+  __syncthreads();
+  int cnt = 0;
+  if (tid < E)
+    for (int i = 0; i < n; ++i) cnt += sid[i] == tid;
+  const int flag = cnt > 0;
+  // inclusive warp scans of (cnt, flag)
+  int c = cnt, f = flag;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int oc = __shfl_up_sync(0xffffffffu, c, off), of = __shfl_up_sync(0xffffffffu, f, off);
+    if (lane >= off) {
+      c += oc;
+      f += of;
     }
   }
-  s.group_off[g] = n;
-  *s.n_groups = g;
+  if (lane == 31) {
+    wsum[0][warp] = c;
+    wsum[1][warp] = f;
+  }
+  __syncthreads();
+  int bc = 0, bf = 0, tc = 0, tf = 0;
+  for (int w = 0; w < nw; ++w) {
+    if (w < warp) {
+      bc += wsum[0][w];
+      bf += wsum[1][w];
+    }
+    tc += wsum[0][w];
+    tf += wsum[1][w];
+  }
+  const int eoff = bc + c - cnt, gidx = bf + f - flag;
+  if (flag) {
+    s.group_expert[gidx] = tid;
+    s.group_buf[gidx] = gbuf ? gbuf[tid] : tid;
+    s.group_off[gidx] = eoff;
+    int m = eoff;
+    for (int i = 0; i < n; ++i)
+      if (sid[i] == tid) {
+        s.entry_tok[m] = i / K;
+        s.entry_of[i] = m;
+        if (s.entry_group) s.entry_group[m] = gidx;
+        ++m;
+      }
+  }
+  if (tid == 0) {
+    s.group_off[tf] = tc;
+    *s.n_groups = tf;
+  }
 }
 
 // ============================================================================ K2 / K3
@@ -345,6 +382,81 @@ __device__ __forceinline__ void grouped_rows_body(const ExpertArgs& a, int g, in
   }
 }
 
+// K2 fast path for one-entry groups (the draft decodes one token): x staged once in smem as fp32,
+// warp owns RPW output rows, lane owns 32-column chunks (one 16-byte word group of nibbles per
+// row), two chunks in flight per lane.  Per element: nibble->float (LOP3 + FADD via the 2^23
+// magic) and one FFMA; the group-128 scale is applied once per 32-column partial.
+template <int MODE, int RPW>
+__global__ void __launch_bounds__(256) k_int4_m1(ExpertArgs a) {
+  extern __shared__ __align__(16) float xs[];
+  const int g = blockIdx.y;
+  if (g >= *a.s.n_groups) return;
+  const int e0 = a.s.group_off[g];
+  const int cols = MODE == 0 ? a.d : a.f;
+  const uint16_t* xp = MODE == 0 ? a.xn + (int64_t)a.s.entry_tok[e0] * a.d : a.act + (int64_t)e0 * a.f;
+  for (int i = threadIdx.x; i < cols; i += 256) xs[i] = bf2f(xp[i]);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row0 = (blockIdx.x * 8 + warp) * RPW;
+  const int nrows = MODE == 0 ? a.f : a.d;
+  if (row0 >= nrows) return;
+  const unsigned char* blob = a.w_base + ((int64_t)a.layer * a.E + a.s.group_expert[g]) * a.blob_bytes;
+  const int64_t q13 = (int64_t)2 * a.f * a.d / 2, s13 = (int64_t)2 * a.f * (a.d / 128) * 2;
+  const int64_t q2 = (int64_t)a.d * a.f / 2;
+  const unsigned char* wq = blob + (MODE == 0 ? 0 : q13 + s13);
+  const uint16_t* ws = reinterpret_cast<const uint16_t*>(blob + (MODE == 0 ? q13 : q13 + s13 + q2));
+  constexpr int PR = MODE == 0 ? 2 * RPW : RPW;
+  const int prow0 = MODE == 0 ? 2 * row0 : row0;
+  const int nch = cols >> 5, ngr = cols >> 7;
+  float acc[PR];
+#pragma unroll
+  for (int r = 0; r < PR; ++r) acc[r] = 0.0f;
+#pragma unroll 2
+  for (int c = lane; c < nch; c += 32) {
+    uint4 wv[PR];
+    float sc[PR];
+#pragma unroll
+    for (int r = 0; r < PR; ++r) {
+      wv[r] = ldg_nc_v4(wq + ((int64_t)(prow0 + r) * cols + 32 * c) / 2);
+      sc[r] = bf2f(ws[(int64_t)(prow0 + r) * ngr + (c >> 2)]);
+    }
+    float xf[32];
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const float4 t = reinterpret_cast<const float4*>(xs + 32 * c)[v];
+      xf[4 * v] = t.x;
+      xf[4 * v + 1] = t.y;
+      xf[4 * v + 2] = t.z;
+      xf[4 * v + 3] = t.w;
+    }
+#pragma unroll
+    for (int r = 0; r < PR; ++r) {
+      const uint32_t wr[4] = {wv[r].x, wv[r].y, wv[r].z, wv[r].w};
+      float p = 0.0f;
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+#pragma unroll
+        for (int n = 0; n < 8; ++n) {
+          const float qf = __uint_as_float(0x4B000000u | ((wr[v] >> (4 * n)) & 0xFu)) - 8388616.0f;
+          p = fmaf(qf, xf[8 * v + n], p);
+        }
+      acc[r] = fmaf(p, sc[r], acc[r]);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < PR; ++r) acc[r] = warp_butterfly_sum(acc[r]);
+  if (lane == 0) {
+    if (MODE == 0) {
+#pragma unroll
+      for (int r = 0; r < RPW; ++r)
+        a.act[(int64_t)e0 * a.f + row0 + r] = f2bf(__fmul_rn(silu_det(acc[2 * r]), acc[2 * r + 1]));
+    } else {
+#pragma unroll
+      for (int r = 0; r < RPW; ++r) a.y[(int64_t)e0 * a.d + row0 + r] = acc[r];
+    }
+  }
+}
+
 template <int MODE, bool INT4, int RPW>
 __global__ void __launch_bounds__(256) k_grouped_rows(ExpertArgs a) {
   const int g = blockIdx.y;
@@ -360,6 +472,16 @@ __global__ void __launch_bounds__(256) k_grouped_rows(ExpertArgs a) {
     blob = a.w_base + ((int64_t)a.layer * a.E + a.s.group_expert[g]) * a.blob_bytes;
   else
     blob = a.w_base + (int64_t)a.s.group_buf[g] * a.blob_bytes;
+  if (INT4) {
+    for (int base = 0; base < m; base += 4) {
+      const int mm = min(4, m - base);
+      if (mm == 1)
+        grouped_rows_body<MODE, INT4, RPW, 1>(a, g, 1, e0 + base, blob, row0);
+      else
+        grouped_rows_body<MODE, INT4, RPW, 4>(a, g, mm, e0 + base, blob, row0);
+    }
+    return;
+  }
   for (int base = 0; base < m; base += 16) {
     const int mm = min(16, m - base);
     if (mm == 1)
@@ -533,13 +655,28 @@ cudaError_t launch_route(const RouteArgs& a, int T, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_build_schedule(const int32_t* ids, int T, int K, int E, SchedPtrs s,
-                                  cudaStream_t st) {
-  k_build_schedule<<<1, 32, 0, st>>>(ids, T, K, E, s);
+cudaError_t launch_build_schedule(const int32_t* ids, int T, int K, int E, const int32_t* gbuf,
+                                  SchedPtrs s, cudaStream_t st) {
+  const int threads = std::max(32, (E + 31) / 32 * 32);
+  k_build_schedule<<<1, threads, 0, st>>>(ids, T, K, E, gbuf, s);
   return cudaGetLastError();
 }
 
-cudaError_t launch_expert(const ExpertArgs& a, bool int4, int max_groups, cudaStream_t st) {
+cudaError_t launch_expert(const ExpertArgs& a, bool int4, int max_groups, int max_group_size,
+                          cudaStream_t st) {
+  if (int4 && max_group_size == 1) {
+    constexpr int R0 = 2, R1 = 4;
+    const size_t sm0 = (size_t)a.d * 4, sm1 = (size_t)a.f * 4;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_int4_m1<0, R0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_int4_m1<1, R1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    k_int4_m1<0, R0><<<dim3((a.f + 8 * R0 - 1) / (8 * R0), max_groups), 256, sm0, st>>>(a);
+    k_int4_m1<1, R1><<<dim3((a.d + 8 * R1 - 1) / (8 * R1), max_groups), 256, sm1, st>>>(a);
+    return cudaGetLastError();
+  }
   constexpr int RPW0 = 2, RPW1 = 4;
   {
     dim3 grid((a.f + 8 * RPW0 - 1) / (8 * RPW0), max_groups);

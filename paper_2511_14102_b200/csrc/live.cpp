@@ -54,7 +54,7 @@ enum : int { S_TOTAL = 0, S_NFREE, S_NPEND, S_K, S_T1, S_T2, S_NREQ, S_NLOG, S_N
 
 struct Sched {
   int32_t* base = nullptr;
-  int32_t *n_groups, *group_expert, *group_buf, *group_off, *entry_tok, *entry_of;
+  int32_t *n_groups, *group_expert, *group_buf, *group_off, *entry_tok, *entry_of, *entry_group;
   void carve(int32_t* p, int G, int N) {
     base = p;
     n_groups = p;
@@ -63,8 +63,9 @@ struct Sched {
     group_off = group_buf + G;
     entry_tok = group_off + G + 1;
     entry_of = entry_tok + N;
+    entry_group = entry_of + N;
   }
-  static size_t ints(int G, int N) { return 4 + 3 * (size_t)G + 1 + 2 * (size_t)N + 8; }
+  static size_t ints(int G, int N) { return 4 + 3 * (size_t)G + 1 + 3 * (size_t)N + 8; }
 };
 
 double elapsed_s(cudaEvent_t a, cudaEvent_t b) {
@@ -106,9 +107,14 @@ struct mspq_engine {
   float* wts_d = nullptr;
   Sched sv[2], sd[2];
   float *yv[2] = {nullptr, nullptr}, *yd[2] = {nullptr, nullptr};
+  int yv_splits[2] = {1, 1};
+  void* tcws = nullptr;
+  static constexpr int kMaxSplit = 8;
   uint16_t* act = nullptr;
   float* logits = nullptr;
   int32_t* amax = nullptr;
+  int32_t* gbuf = nullptr;  // [E] first-request buffer per expert of the current verify layer
+  std::vector<int> layer_bufs;
   int32_t* dst = nullptr;  // device state: [0] row [1] cur_tok [2] cur_pos [3] accepted [4] bonus [8..] win_tok [8+Tmax+1..] win_pos
   int32_t* hpin = nullptr;  // pinned host mirror for small transfers
   size_t hpin_ints = 0;
@@ -217,8 +223,11 @@ void make_experts(mspq_engine* E) {
   const int64_t S16 = E->S16, S4 = E->S4;
   CUDA_OK(cudaMalloc(&E->draft4, (size_t)LE * S4));
   unsigned char* stage[2];
+  unsigned char* tiled[2];
   CUDA_OK(cudaMalloc(&stage[0], S16));
   CUDA_OK(cudaMalloc(&stage[1], S16));
+  CUDA_OK(cudaMalloc(&tiled[0], S16));
+  CUDA_OK(cudaMalloc(&tiled[1], S16));
   const bool fill_host = !(E->host_is_shm && E->o.host_store_role != 0);
   const int64_t q13 = (int64_t)2 * m.f * m.d / 2, s13 = (int64_t)2 * m.f * (m.d / 128) * 2, q2 = (int64_t)m.d * m.f / 2;
   for (int p = 0; p < E->n_payload; ++p) {
@@ -230,11 +239,19 @@ void make_experts(mspq_engine* E) {
       CAPI_OK(mspq_quantize_int4(st, 2 * m.f, m.d, b4, b4 + q13, E->sc));
       CAPI_OK(mspq_quantize_int4(st + (size_t)2 * m.f * m.d * 2, m.d, m.f, b4 + q13 + s13, b4 + q13 + s13 + q2, E->sc));
     }
-    if (fill_host) CUDA_OK(cudaMemcpyAsync(E->host + (size_t)p * S16, st, S16, cudaMemcpyDeviceToHost, E->sc));
+    if (fill_host) {
+      // host store keeps the tile-major SW128 images K3 streams with one bulk copy per tile
+      unsigned char* tl = tiled[p & 1];
+      CAPI_OK(mspq_tile_bf16(st, 2 * m.f, m.d, tl, E->sc));
+      CAPI_OK(mspq_tile_bf16(st + (size_t)2 * m.f * m.d * 2, m.d, m.f, tl + (size_t)2 * m.f * m.d * 2, E->sc));
+      CUDA_OK(cudaMemcpyAsync(E->host + (size_t)p * S16, tl, S16, cudaMemcpyDeviceToHost, E->sc));
+    }
   }
   CUDA_OK(cudaStreamSynchronize(E->sc));
   cudaFree(stage[0]);
   cudaFree(stage[1]);
+  cudaFree(tiled[0]);
+  cudaFree(tiled[1]);
   if (E->host_is_shm && E->o.host_store_role == 0) {
     const std::string ready = E->store_path + ".ready";
     int fd = open(ready.c_str(), O_WRONLY | O_CREAT, 0600);
@@ -257,9 +274,12 @@ void make_workspaces(mspq_engine* E) {
   size_t o_h = take((size_t)T * d * 4), o_xn = take((size_t)T * d * 2), o_it = take((size_t)L * T * K * 4),
          o_wt = take((size_t)L * T * K * 4), o_id = take((size_t)L * K * 4), o_wd = take((size_t)L * K * 4),
          o_sv0 = take(sched_ints * 4), o_sv1 = take(sched_ints * 4), o_sd0 = take(Sched::ints(K, K) * 4),
-         o_sd1 = take(Sched::ints(K, K) * 4), o_yv0 = take((size_t)E->N * d * 4), o_yv1 = take((size_t)E->N * d * 4),
+         o_sd1 = take(Sched::ints(K, K) * 4), o_yv0 = take((size_t)mspq_engine::kMaxSplit * E->N * d * 4),
+         o_yv1 = take((size_t)mspq_engine::kMaxSplit * E->N * d * 4),
          o_yd0 = take((size_t)K * d * 4), o_yd1 = take((size_t)K * d * 4), o_act = take((size_t)E->N * f * 2),
-         o_lg = take((size_t)T * m.V * 4), o_am = take((size_t)T * 4), o_dst = take((size_t)(8 + 2 * (T + 1)) * 4);
+         o_lg = take((size_t)T * m.V * 4), o_am = take((size_t)T * 4), o_dst = take((size_t)(8 + 2 * (T + 1)) * 4),
+         o_gb = take((size_t)m.E * 4),
+         o_tc = take((size_t)mspq_moe_bf16_tc_ws_bytes(d, f, T, K, E->G, mspq_engine::kMaxSplit));
   CUDA_OK(cudaMalloc(&E->ws, off));
   CUDA_OK(cudaMemset(E->ws, 0, off));
   char* b = (char*)E->ws;
@@ -281,6 +301,8 @@ void make_workspaces(mspq_engine* E) {
   E->logits = (float*)(b + o_lg);
   E->amax = (int32_t*)(b + o_am);
   E->dst = (int32_t*)(b + o_dst);
+  E->gbuf = (int32_t*)(b + o_gb);
+  E->tcws = (void*)(b + o_tc);
   E->hpin_ints = 64 + (size_t)L * T * K * 2 + (size_t)E->Tmax * L * K * 2 + 4 * T + (size_t)L * 2 + (size_t)L * T * 2 + 64;
   CUDA_OK(cudaHostAlloc((void**)&E->hpin, E->hpin_ints * 4, 0));
 }
@@ -296,17 +318,17 @@ void enqueue_draft_step(mspq_engine* E, cudaStream_t s) {
   for (int l = 0; l < L; ++l) {
     const int pl = (l - 1) & 1;
     CAPI_OK(mspq_gate_topk(E->h, l ? E->yd[pl] : nullptr, l ? E->sd[pl].entry_of : nullptr,
-                           l ? E->wts_d + (size_t)(l - 1) * K : nullptr, E->gamma + (size_t)l * d,
+                           l ? E->wts_d + (size_t)(l - 1) * K : nullptr, 1, 0, E->gamma + (size_t)l * d,
                            E->router + (size_t)l * m.E * d, E->xn, E->ids_d + (size_t)l * K, E->wts_d + (size_t)l * K,
                            nullptr, E->view.elb_ids, E->view.elb_gates, row, l, L, 1, d, m.E, K, m.eps, s));
     Sched& sc = E->sd[l & 1];
-    CAPI_OK(mspq_build_schedule(E->ids_d + (size_t)l * K, 1, K, m.E, sc.n_groups, sc.group_expert, sc.group_buf,
-                                sc.group_off, sc.entry_tok, sc.entry_of, s));
+    CAPI_OK(mspq_build_schedule(E->ids_d + (size_t)l * K, 1, K, m.E, nullptr, sc.n_groups, sc.group_expert, sc.group_buf,
+                                sc.group_off, sc.entry_tok, sc.entry_of, nullptr, s));
     CAPI_OK(mspq_moe_int4(sc.n_groups, sc.group_expert, sc.group_buf, sc.group_off, sc.entry_tok, E->xn, E->act,
-                          E->yd[l & 1], E->draft4, E->S4, l, m.E, d, m.f, K, s));
+                          E->yd[l & 1], E->draft4, E->S4, l, m.E, d, m.f, K, 1, s));
   }
   const int pl = (L - 1) & 1;
-  CAPI_OK(mspq_gate_topk(E->h, E->yd[pl], E->sd[pl].entry_of, E->wts_d + (size_t)(L - 1) * K, E->gfinal, nullptr,
+  CAPI_OK(mspq_gate_topk(E->h, E->yd[pl], E->sd[pl].entry_of, E->wts_d + (size_t)(L - 1) * K, 1, 0, E->gfinal, nullptr,
                          E->xn, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, L, L, 1, d, m.E, K, m.eps, s));
   CAPI_OK(mspq_lm_head(E->xn, E->lm, 1, m.V, d, E->logits, s));
   CAPI_OK(mspq_argmax_advance(E->logits, m.V, E->amax, row, E->win_tok() + 1, cur_tok, cur_pos, s));
@@ -543,23 +565,29 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
       const int pl = (l - 1) & 1;
       int32_t* tgt = E->ids_t + (size_t)l * T * K;
       CAPI_OK(mspq_gate_topk(E->h, l ? E->yv[pl] : nullptr, l ? E->sv[pl].entry_of : nullptr,
-                             l ? E->wts_t + (size_t)(l - 1) * T * K : nullptr, E->gamma + (size_t)l * d,
+                             l ? E->wts_t + (size_t)(l - 1) * T * K : nullptr, E->yv_splits[pl],
+                             (long long)T * K * d, E->gamma + (size_t)l * d,
                              E->router + (size_t)l * Ex * d, E->xn, tgt, E->wts_t + (size_t)l * T * K, nullptr, nullptr,
                              nullptr, nullptr, l, L, T, d, Ex, K, m.eps, E->sc));
       Sched& sv = E->sv[l & 1];
-      CAPI_OK(mspq_cache_verify_layer(E->cache, l, T, tgt, sv.n_groups, sv.group_expert, sv.group_buf, sv.group_off,
-                                      sv.entry_tok, sv.entry_of, E->sc));
+      CAPI_OK(mspq_cache_verify_layer(E->cache, l, T, tgt, E->gbuf, E->sc));
       CUDA_OK(cudaEventRecord(E->ev_w0[l], E->sc));
+      CAPI_OK(mspq_build_schedule(tgt, T, K, Ex, E->gbuf, sv.n_groups, sv.group_expert, sv.group_buf, sv.group_off,
+                                  sv.entry_tok, sv.entry_of, sv.entry_group, E->sc));
       CUDA_OK(cudaEventSynchronize(E->ev_w0[l]));
       CopyBatch b;
       b.label = "io_new";
       issue_copies(E, cycle, b, cyc_bytes);
       if (b.count) batches.push_back(b);
       // wait for every copy this layer's experts still depend on
-      const int ng = E->view.host_sched[0];
+      std::vector<int>& gb = E->layer_bufs;
+      gb.clear();
+      for (int e = 0; e < Ex; ++e)
+        if (E->view.host_sched[1 + e] >= 0) gb.push_back(E->view.host_sched[1 + e]);
+      const int ng = (int)gb.size();
       bool waited = false;
       for (int gi = 0; gi < ng; ++gi) {
-        const int buf = E->view.host_sched[1 + gi];
+        const int buf = gb[gi];
         if (buf < 0 || buf >= E->nbuf) fail(MSPQ_ERR_OVERFLOW, "schedule buffer out of range");
         if (E->ready_rec[buf]) {
           if (cudaEventQuery(E->ev_ready[buf]) == cudaErrorNotReady) {
@@ -574,15 +602,23 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
         CUDA_OK(cudaEventRecord(E->ev_w1[l], E->sc));
         stall_ev.push_back({E->ev_w0[l], E->ev_w1[l]});
       }
+      // K splits so each tcgen05 GEMM has >= ~2 CTAs per SM
+      auto pick_split = [&](int rows, int kdim) {
+        const int units = std::max(1, ng * (rows / 128));
+        int sp = (296 + units - 1) / units;
+        return std::max(1, std::min({sp, mspq_engine::kMaxSplit, kdim / 64}));
+      };
+      const int sp1 = pick_split(2 * m.f, d), sp2 = pick_split(d, m.f);
+      E->yv_splits[l & 1] = sp2;
       CUDA_OK(cudaEventRecord(E->ev_k0[l], E->sc));
-      CAPI_OK(mspq_moe_bf16(sv.n_groups, sv.group_expert, sv.group_buf, sv.group_off, sv.entry_tok, E->xn, E->act,
-                            E->yv[l & 1], E->pool, E->S16, Ex, d, m.f, E->G, E->sc));
+      CAPI_OK(mspq_moe_bf16_tc(sv.n_groups, sv.group_expert, sv.group_buf, sv.group_off, sv.entry_tok, sv.entry_group,
+                               E->xn, E->pool, E->S16, d, m.f, T, K, E->G, sp1, sp2, E->tcws, E->yv[l & 1], E->sc));
       CUDA_OK(cudaEventRecord(E->ev_gemm[l], E->sc));
-      launches += 4;  // gate_topk, verify_layer, 2 x grouped FFN
+      launches += 7;  // gate_topk, verify_layer, schedule, gather, 2 x tcgen05 GEMM, finalize
       k3_groups += ng;
       layer_groups[l] = ng;
       for (int gi = 0; gi < ng; ++gi) {
-        const int buf = E->view.host_sched[1 + gi];
+        const int buf = gb[gi];
         E->last_cycle[buf] = cycle;
         E->last_layer[buf] = l;
       }
@@ -590,7 +626,8 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
     }
     const int pl = (L - 1) & 1;
     launches += 6;  // embed, final norm, lm head, argmax, accept, begin_cycle
-    CAPI_OK(mspq_gate_topk(E->h, E->yv[pl], E->sv[pl].entry_of, E->wts_t + (size_t)(L - 1) * T * K, E->gfinal, nullptr,
+    CAPI_OK(mspq_gate_topk(E->h, E->yv[pl], E->sv[pl].entry_of, E->wts_t + (size_t)(L - 1) * T * K, E->yv_splits[pl],
+                           (long long)T * K * d, E->gfinal, nullptr,
                            E->xn, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, L, L, T, d, Ex, K, m.eps, E->sc));
     CAPI_OK(mspq_lm_head(E->xn, E->lm, T, m.V, d, E->logits, E->sc));
     CAPI_OK(mspq_argmax(E->logits, T, m.V, E->amax, E->sc));

@@ -51,14 +51,16 @@ def embed(embed_w, pos_w, tokens, positions, d):
 
 
 def gate_topk(h, gamma, router, E, K, eps=1e-6, y=None, entry_of=None, prev_wts=None,
-              elb_ids=None, elb_gates=None, elb_row=None, layer=0, L=1, want_logits=True):
+              elb_ids=None, elb_gates=None, elb_row=None, layer=0, L=1, want_logits=True,
+              y_splits=1, y_split_stride=0):
     T, d = h.shape
     dev = h.device
     xn = torch.empty(T, d, dtype=torch.int16, device=dev)
     ids = torch.empty(T, K, dtype=torch.int32, device=dev)
     wts = torch.empty(T, K, dtype=torch.float32, device=dev)
     logits = torch.empty(T, E, dtype=torch.float32, device=dev) if want_logits and router is not None else None
-    check(lib().mspq_gate_topk(_p(h), _p(y), _p(entry_of), _p(prev_wts), _p(gamma), _p(router),
+    check(lib().mspq_gate_topk(_p(h), _p(y), _p(entry_of), _p(prev_wts), y_splits, y_split_stride,
+                               _p(gamma), _p(router),
                                _p(xn), _p(ids), _p(wts), _p(logits), _p(elb_ids), _p(elb_gates),
                                _p(elb_row), layer, L, T, d, E, K, eps, _s()))
     return xn, ids, wts, logits
@@ -71,26 +73,27 @@ class Schedule:
         z = lambda n: torch.zeros(n, dtype=torch.int32, device=device)
         self.n_groups, self.group_expert, self.group_buf = z(1), z(G), z(G)
         self.group_off, self.entry_tok, self.entry_of = z(G + 1), z(T * K), z(T * K)
+        self.entry_group = z(T * K)
 
     def ptrs(self):
         return [_p(self.n_groups), _p(self.group_expert), _p(self.group_buf), _p(self.group_off),
-                _p(self.entry_tok), _p(self.entry_of)]
+                _p(self.entry_tok), _p(self.entry_of), _p(self.entry_group)]
 
 
 def build_schedule(ids, E):
     T, K = ids.shape
     s = Schedule(T, K, E, ids.device)
-    check(lib().mspq_build_schedule(_p(ids), T, K, E, *s.ptrs(), _s()))
+    check(lib().mspq_build_schedule(_p(ids), T, K, E, None, *s.ptrs(), _s()))
     return s
 
 
-def moe_int4(s: Schedule, xn, blobs, blob_bytes, layer, E, d, f):
+def moe_int4(s: Schedule, xn, blobs, blob_bytes, layer, E, d, f, max_group_size=None):
     N = s.T * s.K
     act = torch.empty(N, f, dtype=torch.int16, device=xn.device)
     y = torch.empty(N, d, dtype=torch.float32, device=xn.device)
     check(lib().mspq_moe_int4(_p(s.n_groups), _p(s.group_expert), _p(s.group_buf), _p(s.group_off),
                               _p(s.entry_tok), _p(xn), _p(act), _p(y), _p(blobs), blob_bytes, layer,
-                              E, d, f, s.G, _s()))
+                              E, d, f, s.G, max_group_size or s.T, _s()))
     return act, y
 
 
@@ -100,8 +103,27 @@ def moe_bf16(s: Schedule, xn, pool, blob_bytes, E, d, f):
     y = torch.empty(N, d, dtype=torch.float32, device=xn.device)
     check(lib().mspq_moe_bf16(_p(s.n_groups), _p(s.group_expert), _p(s.group_buf), _p(s.group_off),
                               _p(s.entry_tok), _p(xn), _p(act), _p(y), _p(pool), blob_bytes, E, d,
-                              f, s.G, _s()))
+                              f, s.G, s.T, _s()))
     return act, y
+
+
+def tile_bf16(src_i16, rows, cols):
+    dst = torch.empty(rows * cols, dtype=torch.int16, device=src_i16.device)
+    check(lib().mspq_tile_bf16(_p(src_i16), rows, cols, _p(dst), _s()))
+    return dst
+
+
+def moe_bf16_tc(s: Schedule, xn, pool_tiled, blob_bytes, d, f, split1=1, split2=1):
+    """K3 on tcgen05; returns y summed over the split planes [T*K][d]."""
+    T, K, G = s.T, s.K, s.G
+    N = T * K
+    ws = torch.empty(lib().mspq_moe_bf16_tc_ws_bytes(d, f, T, K, G, split1), dtype=torch.uint8,
+                     device=xn.device)
+    y = torch.empty(split2, N, d, dtype=torch.float32, device=xn.device)
+    check(lib().mspq_moe_bf16_tc(_p(s.n_groups), _p(s.group_expert), _p(s.group_buf), _p(s.group_off),
+                                 _p(s.entry_tok), _p(s.entry_group), _p(xn), _p(pool_tiled), blob_bytes,
+                                 d, f, T, K, G, split1, split2, _p(ws), _p(y), _s()))
+    return y.sum(0) if split2 > 1 else y[0], y
 
 
 def lm_head(xn, lm, V):

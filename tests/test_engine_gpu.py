@@ -121,10 +121,12 @@ def test_engine_weights_match_oracle_generator(cuda):
     eng, cfg = _engine()
     model = om.Model(_oracle_desc(cfg))
     d, f = cfg.d, cfg.f
+    from test_kernels_gpu import untile
     raw = np.frombuffer(eng.read("expert:2:5", cfg.expert_bytes_bf16()), dtype=np.uint16)
     g, u, dn = model.expert(2, 5)
-    assert np.array_equal(raw[:2 * f * d].reshape(2 * f, d)[0::2], g)
-    assert np.array_equal(raw[2 * f * d:].reshape(d, f), dn)
+    w13 = untile(raw[:2 * f * d], 2 * f, d)  # host store keeps tile-major SW128 images
+    assert np.array_equal(w13[0::2], g) and np.array_equal(w13[1::2], u)
+    assert np.array_equal(untile(raw[2 * f * d:], d, f), dn)
     r = np.frombuffer(eng.read("router:1", cfg.E * d * 2), dtype=np.uint16).reshape(cfg.E, d)
     assert np.array_equal(r, model.router(1))
     eng.close()
