@@ -102,6 +102,20 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def aggregate(dev_t, wall, tok, world):
+    """Replica aggregation: times are the MAX over ranks, tokens the SUM (whole-job throughput
+    = all ranks' tokens / slowest rank).  Timing only -- no data-path collective."""
+    import torch
+    if world <= 1:
+        return dev_t, wall, float(tok)
+    import torch.distributed as dist
+    t = torch.tensor([dev_t, wall], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    n = torch.tensor([float(tok)], dtype=torch.float64)
+    dist.all_reduce(n, op=dist.ReduceOp.SUM)
+    return t[0].item(), t[1].item(), n[0].item()
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -236,15 +250,7 @@ def main():
     ks = [c for r in reps for c in r.get("cycles", [])]
     mean_k = statistics.mean([c["k"] for c in ks]) if ks else None
     acc = sum(c["accepted"] for c in ks) / max(1, sum(c["k"] for c in ks))
-    vals = torch.tensor([dev_t, wall, float(tok)], dtype=torch.float64)
-    if world > 1:
-        mx = vals.clone()
-        torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
-        sm = vals.clone()
-        torch.distributed.all_reduce(sm, op=torch.distributed.ReduceOp.SUM)
-        dev_max, wall_max, tok_all = mx[0].item(), mx[1].item(), sm[2].item()
-    else:
-        dev_max, wall_max, tok_all = dev_t, wall, float(tok)
+    dev_max, wall_max, tok_all = aggregate(dev_t, wall, tok, world)
     if rank != 0:
         eng.close()
         return

@@ -100,11 +100,14 @@ int mspq_embed(const void* embed, const void* pos, const int32_t* tokens,
                const int32_t* positions, int T, int d, float* h, void* stream);
 /* K1.  y/entry_of/prev_wts may be NULL (no combine); y may hold y_splits partial planes
  * y_split_stride floats apart (summed in order); router NULL = norm only;
- * elb_ids/elb_gates/elb_row NULL = no ELB write. */
+ * elb_ids/elb_gates/elb_row NULL = no ELB write.  sched_block (T == 1 only, nullable): also
+ * write the token's expert-grouped schedule, packed [n_groups, pad x3, group_expert[K],
+ * group_buf[K], group_off[K+1], entry_tok[K], entry_of[K], entry_group[K]]. */
 int mspq_gate_topk(float* h, const float* y, const int32_t* entry_of, const float* prev_wts,
                    int y_splits, long long y_split_stride, const void* gamma, const void* router, void* xn, int32_t* ids, float* wts,
                    float* logits, int32_t* elb_ids, float* elb_gates, const int32_t* elb_row,
-                   int layer, int L, int T, int d, int E, int K, float eps, void* stream);
+                   int32_t* sched_block, int layer, int L, int T, int d, int E, int K, float eps,
+                   void* stream);
 /* schedule arrays: n_groups[1], group_expert[G], group_buf[G], group_off[G+1], entry_tok[T*K],
  * entry_of[T*K]; gbuf[E] (nullable) gives group_buf per expert (else group_buf = expert id) */
 int mspq_build_schedule(const int32_t* ids, int T, int K, int E, const int32_t* gbuf, int32_t* n_groups,
@@ -177,6 +180,9 @@ int mspq_cache_destroy(mspq_cache* c);
 int mspq_cache_configure(mspq_cache* c, int mode, int policy, const int* caps, int cap_global,
                          int budget, double f1, double f2, void* stream);
 int mspq_cache_view_get(mspq_cache* c, mspq_cache_view* v);
+/* 1 (default when the state fits) = each launch runs on a shared-memory copy of the table;
+ * 0 = operate on global memory directly.  Decisions are identical (tested). */
+int mspq_cache_set_staging(mspq_cache* c, int on);
 int mspq_cache_begin_cycle(mspq_cache* c, int k, void* stream);
 int mspq_cache_plan_row(mspq_cache* c, int row, void* stream);
 /* verify step of one layer: policy steps for every (slot, expert) of tgt[nslots][K]; writes

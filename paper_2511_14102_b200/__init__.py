@@ -147,3 +147,54 @@ class Engine:
             self.close()
         except Exception:
             pass
+
+
+def to_reference_trace(report: dict, model: ModelConfig, meta: dict | None = None) -> str:
+    """Per-committed-position reference trace (trace.hpp:43-49, JSONL trace.cpp:286-311) from a
+    live generate() report recorded with trace_level >= 1.
+
+    Position p's target_sets = the target model's routing when the verify processed token p
+    (window slot s of the cycle that committed it, or slot 0 = head of the next cycle for a
+    bonus token); draft_sets/gates = the draft's routing of the same token (ELB row s) when the
+    draft processed it; acc = the draft's token at p was accepted (bonus tokens: false).
+    An accepted token in the unpredicted last window slot was never routed by the draft; its
+    draft_sets are taken from its target routing and its position listed in
+    meta["draft_from_target"].  The last committed token (never verified) ends the trace.
+    Feeding the result to
+    run_simulation / classify_fidelity / layer_entropy analyses a live run with the
+    reference's own tools."""
+    L, K = model.L, model.K
+    recs = []  # (target_sets, draft_sets, gates, acc)
+    synth = []
+    cyc = report["cycles"]
+    for ci, c in enumerate(cyc):
+        if "target" not in c:
+            raise ValueError("report needs trace_level >= 1")
+        k = c["k"]
+        # slot 0 = head: the previous cycle's bonus token (or the last prompt token)
+        if ci > 0:
+            recs.append((c["target"][0], c["elb"][0], c["elb_gates"][0], False))
+        for s in range(1, c["accepted"] + 1):
+            if s >= k:  # accepted token in the unpredicted last slot: no draft routing
+                synth.append(len(recs))
+                recs.append((c["target"][s], c["target"][s], None, True))
+            else:
+                recs.append((c["target"][s], c["elb"][s], c["elb_gates"][s], True))
+    meta = dict(meta or {})
+    meta["draft_from_target"] = ",".join(map(str, synth))
+    return _emit_trace(recs, model, meta)
+
+
+def _emit_trace(recs, model, meta):
+    head = {"shape": {"L": model.L, "N": model.E, "top_k": model.K, "shared": 0,
+                      "expert_bytes": model.expert_bytes_bf16()},
+            "meta": dict({"source": "mspq-live"}, **(meta or {}))}
+    out = [json.dumps(head, separators=(",", ":"))]
+    # gates must be on every record or none (trace.cpp parse): fall back to 1.0 for synthesized
+    for p, (tg, dr, gt, acc) in enumerate(recs):
+        gates = gt if gt is not None else [[1.0] * model.K for _ in range(model.L)]
+        out.append(json.dumps({"pos": p, "target": [[l, tg[l]] for l in range(model.L)],
+                               "draft": [[l, dr[l]] for l in range(model.L)],
+                               "gates": [[l, gates[l]] for l in range(model.L)], "acc": acc},
+                              separators=(",", ":")))
+    return "\n".join(out) + "\n"

@@ -37,7 +37,7 @@ _SIGS = [
     ("mspq_fill_expert", c_int, [c_ull, c_int, c_int, c_int, c_int, c_float, c_float, c_void_p, c_void_p]),
     ("mspq_quantize_int4", c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p]),
     ("mspq_embed", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p]),
-    ("mspq_gate_topk", c_int, [c_void_p] * 4 + [c_int, c_ll] + [c_void_p] * 9 + [c_int] * 6 + [c_float, c_void_p]),
+    ("mspq_gate_topk", c_int, [c_void_p] * 4 + [c_int, c_ll] + [c_void_p] * 10 + [c_int] * 6 + [c_float, c_void_p]),
     ("mspq_build_schedule", c_int, [c_void_p, c_int, c_int, c_int] + [c_void_p] * 9),
     ("mspq_moe_int4", c_int, [c_void_p] * 9 + [c_ll] + [c_int] * 6 + [c_void_p]),
     ("mspq_moe_bf16", c_int, [c_void_p] * 9 + [c_ll] + [c_int] * 5 + [c_void_p]),
@@ -55,6 +55,7 @@ _SIGS = [
     ("mspq_cache_destroy", c_int, [c_void_p]),
     ("mspq_cache_configure", c_int, [c_void_p, c_int, c_int, c_void_p, c_int, c_int, c_double, c_double, c_void_p]),
     ("mspq_cache_view_get", c_int, [c_void_p, c_void_p]),
+    ("mspq_cache_set_staging", c_int, [c_void_p, c_int]),
     ("mspq_cache_begin_cycle", c_int, [c_void_p, c_int, c_void_p]),
     ("mspq_cache_plan_row", c_int, [c_void_p, c_int, c_void_p]),
     ("mspq_cache_verify_layer", c_int, [c_void_p, c_int, c_int] + [c_void_p] * 3),
@@ -84,6 +85,14 @@ def lib():
             fn.argtypes = args
         _lib = L
     return _lib
+
+
+class CacheView(ctypes.Structure):
+    _fields_ = [("elb_ids", c_void_p), ("elb_gates", c_void_p), ("scal", c_void_p), ("req", c_void_p),
+                ("log", c_void_p), ("plan", c_void_p), ("cov", c_void_p), ("step", c_void_p),
+                ("res", c_void_p), ("host_stat", ctypes.POINTER(ctypes.c_int32)),
+                ("host_req", ctypes.POINTER(ctypes.c_int32)), ("host_sched", ctypes.POINTER(ctypes.c_int32)),
+                ("req_cap", c_int), ("log_cap", c_int), ("plan_cap", c_int), ("nbuf", c_int)]
 
 
 class MspqError(RuntimeError):

@@ -69,12 +69,13 @@ int mspq_embed(const void* embed, const void* pos, const int32_t* tokens, const 
 int mspq_gate_topk(float* h, const float* y, const int32_t* entry_of, const float* prev_wts,
                    int y_splits, long long y_split_stride, const void* gamma, const void* router, void* xn, int32_t* ids, float* wts,
                    float* logits, int32_t* elb_ids, float* elb_gates, const int32_t* elb_row,
-                   int layer, int L, int T, int d, int E, int K, float eps, void* stream) {
+                   int32_t* sched_block, int layer, int L, int T, int d, int E, int K, float eps,
+                   void* stream) {
   if (d % 256 || K > 64 || E > 1024 || K > E)
     return set_error(MSPQ_ERR_SHAPE_MISMATCH, "gate_topk: need d%256==0, K<=min(E,64), E<=1024");
   RouteArgs a{h, y, entry_of, prev_wts, (const uint16_t*)gamma, (const uint16_t*)router,
               (uint16_t*)xn, ids, wts, logits, y_splits < 1 ? 1 : y_splits, y_split_stride,
-              elb_ids, elb_gates, elb_row, layer, L, d, E, K, eps};
+              elb_ids, elb_gates, elb_row, T == 1 ? sched_block : nullptr, layer, L, d, E, K, eps};
   CK(launch_route(a, T, ST(stream)), "gate_topk");
 }
 int mspq_build_schedule(const int32_t* ids, int T, int K, int E, const int32_t* gbuf, int32_t* n_groups,
@@ -183,6 +184,8 @@ int mspq_cache_create(int L, int E, int K, int kmax, int nbuf, int log_cap, mspq
   C.L = L;
   C.E = E;
   C.K = K;
+  C.nbuf = nbuf;
+  C.kmax = kmax;
   const int n = L * E;
   C.req_cap = 4 * n + 64;
   C.log_cap = log_cap > 0 ? log_cap : (kmax + 1) * L * K * 4 + 4 * n + 64;
@@ -239,6 +242,7 @@ int mspq_cache_create(int L, int E, int K, int kmax, int nbuf, int log_cap, mspq
   C.plan = (int*)(b + o_plan);
   C.cov = (int*)(b + o_cov);
   C.step = (int*)(b + o_step);
+  C.stage = ctl_stage_bytes(C, true) > 0 ? 1 : 0;
   *out = c;
   return MSPQ_OK;
 }
@@ -275,6 +279,10 @@ int mspq_cache_view_get(mspq_cache* c, mspq_cache_view* v) {
   return MSPQ_OK;
 }
 
+int mspq_cache_set_staging(mspq_cache* c, int on) {
+  c->C.stage = on && ctl_stage_bytes(c->C, true) > 0 ? 1 : 0;
+  return MSPQ_OK;
+}
 int mspq_cache_begin_cycle(mspq_cache* c, int k, void* stream) {
   if (k < 0 || k > c->kmax) return set_error(MSPQ_ERR_K_OUT_OF_RANGE, "k > kmax");
   CK(ctl_begin_cycle(c->C, k, ST(stream)), "cache_begin_cycle");

@@ -43,7 +43,7 @@ struct Ctx {
   bool emit = true;     // copy requests (live engine); replay runs the control plane only
 };
 
-MSPQ_D int* V(int* p) { return p; }
+MSPQ_D volatile int* V(int* p) { return (volatile int*)p; }
 
 MSPQ_D int get(const Ctx& x, int slot) { return V(x.C.scal)[slot]; }
 MSPQ_D void put(const Ctx& x, int slot, int v) {
@@ -59,10 +59,10 @@ MSPQ_D bool contains(const Ctx& x, int key) { return V(x.C.res)[key] >= 0; }
 
 MSPQ_D void touch(const Ctx& x, int key) {
   if (lane_id() == 0) {
-    unsigned long long* clk = (unsigned long long*)x.C.clock;
+    volatile unsigned long long* clk = (volatile unsigned long long*)x.C.clock;
     unsigned long long c = *clk + 1;
     *clk = c;
-    ((unsigned long long*)x.C.stamp)[key] = c;
+    ((volatile unsigned long long*)x.C.stamp)[key] = c;
   }
   __syncwarp();
 }
@@ -81,7 +81,7 @@ MSPQ_D int lru_victim(const Ctx& x, int layer) {
   int bk = -1;
   for (int key = key_lo(x, layer) + lane_id(); key < key_hi(x, layer); key += 32)
     if (contains(x, key)) {
-      unsigned long long s = ((unsigned long long*)x.C.stamp)[key];
+      unsigned long long s = ((volatile unsigned long long*)x.C.stamp)[key];
       if (s < best) {
         best = s;
         bk = key;
@@ -135,12 +135,12 @@ MSPQ_D int belady_victim(const Ctx& x, int now, int visible, int layer) {
 // step's GEMM reads (first-request buffer of this layer), which is parked until the step ends.
 MSPQ_D void erase(const Ctx& x, int key) {
   if (lane_id() == 0) {
-    int* res = V(x.C.res);
+    volatile int* res = V(x.C.res);
     int buf = res[key];
     res[key] = -1;
     V(x.C.lsize)[key / x.C.E] -= 1;
     V(x.C.scal)[S_TOTAL] -= 1;
-    const bool defer = x.gb && key / x.C.E == x.step_layer && ((int*)x.gb)[key % x.C.E] == buf;
+    const bool defer = x.gb && key / x.C.E == x.step_layer && ((volatile int*)x.gb)[key % x.C.E] == buf;
     if (buf >= 0) {
       if (defer) {
         int np = V(x.C.scal)[S_NPEND];
@@ -158,7 +158,7 @@ MSPQ_D void erase(const Ctx& x, int key) {
 
 MSPQ_D void insert_key(const Ctx& x, int key) {
   if (lane_id() == 0) {
-    int* scal = V(x.C.scal);
+    volatile int* scal = V(x.C.scal);
     int nf = scal[S_NFREE];
     int buf = -1;
     if (nf > 0) {
@@ -168,10 +168,10 @@ MSPQ_D void insert_key(const Ctx& x, int key) {
       scal[S_OVERFLOW] = 1;
     }
     V(x.C.res)[key] = buf;
-    unsigned long long* clk = (unsigned long long*)x.C.clock;
+    volatile unsigned long long* clk = (volatile unsigned long long*)x.C.clock;
     unsigned long long c = *clk + 1;
     *clk = c;
-    ((unsigned long long*)x.C.stamp)[key] = c;
+    ((volatile unsigned long long*)x.C.stamp)[key] = c;
     V(x.C.lsize)[key / x.C.E] += 1;
     scal[S_TOTAL] += 1;
   }
@@ -180,10 +180,10 @@ MSPQ_D void insert_key(const Ctx& x, int key) {
 
 MSPQ_D void log_event(const Ctx& x, int kind, int tag, int key, int hit, int victim) {
   if (lane_id() == 0) {
-    int* scal = V(x.C.scal);
+    volatile int* scal = V(x.C.scal);
     int n = scal[S_NLOG];
     if (x.C.log && n < x.C.log_cap) {
-      int* ev = V(x.C.log) + (int64_t)n * 6;
+      volatile int* ev = V(x.C.log) + (int64_t)n * 6;
       ev[0] = kind;
       ev[1] = tag;
       ev[2] = key;
@@ -199,7 +199,7 @@ MSPQ_D void log_event(const Ctx& x, int kind, int tag, int key, int hit, int vic
 MSPQ_D void copy_request(const Ctx& x, int key, int kind) {
   if (!x.emit) return;
   if (lane_id() == 0) {
-    int* scal = V(x.C.scal);
+    volatile int* scal = V(x.C.scal);
     int n = scal[S_NREQ];
     if (n < x.C.req_cap) {
       volatile int* rq = (volatile int*)x.C.req + (int64_t)n * 3;
@@ -281,7 +281,7 @@ MSPQ_D void publish(const Ctx& x) {
 
 MSPQ_D void release_pending(const Ctx& x) {
   if (lane_id() == 0) {
-    int* scal = V(x.C.scal);
+    volatile int* scal = V(x.C.scal);
     int np = scal[S_NPEND], nf = scal[S_NFREE];
     for (int i = 0; i < np; ++i) V(x.C.free_stack)[nf + i] = V(x.C.pending)[i];
     scal[S_NFREE] = nf + np;
@@ -312,11 +312,11 @@ MSPQ_D void absorb_row(const Ctx& x, int r, const unsigned char* snap_or_null) {
       const int e = x.elb.ids[((int64_t)r * L + l) * K + j];
       const int key = l * E + e;
       const bool res = snap_or_null ? snap_or_null[key] != 0 : contains(x, key);
-      if (res || ((unsigned char*)x.C.sched)[key]) continue;
+      if (res || ((volatile unsigned char*)x.C.sched)[key]) continue;
       const double c = conf_of(x, r, l, j);
       if (lane_id() == 0) {
-        int* cf = V(x.C.cand_first);
-        double* cc = x.C.cand_conf;
+        volatile int* cf = V(x.C.cand_first);
+        volatile double* cc = (volatile double*)x.C.cand_conf;
         if (cf[key] < 0) {
           cf[key] = r;
           cc[key] = c;
@@ -334,9 +334,9 @@ MSPQ_D int best_candidate(const Ctx& x, int k) {
   int bf = INT_MAX, bk = -1;
   const int n = x.C.L * x.C.E;
   for (int key = lane_id(); key < n; key += 32) {
-    const int f = (x.C.cand_first)[key];
+    const int f = ((volatile int*)x.C.cand_first)[key];
     if (f < 0) continue;
-    const double p = (x.C.cand_conf)[key] * (double)(k - f) / (double)k;
+    const double p = ((volatile double*)x.C.cand_conf)[key] * (double)(k - f) / (double)k;
     if (bk < 0 || p > bp || (p == bp && (f < bf || (f == bf && key < bk)))) {
       bp = p;
       bf = f;
@@ -358,7 +358,7 @@ MSPQ_D int best_candidate(const Ctx& x, int k) {
 
 MSPQ_D void mark_scheduled(const Ctx& x, int key) {
   if (lane_id() == 0) {
-    ((unsigned char*)x.C.sched)[key] = 1;
+    ((volatile unsigned char*)x.C.sched)[key] = 1;
     V(x.C.cand_first)[key] = -1;
   }
   __syncwarp();
@@ -366,7 +366,7 @@ MSPQ_D void mark_scheduled(const Ctx& x, int key) {
 
 MSPQ_D void plan_item(const Ctx& x, int row, int key, int phase) {
   if (lane_id() == 0) {
-    int* scal = V(x.C.scal);
+    volatile int* scal = V(x.C.scal);
     int n = scal[S_NPLAN];
     if (n < x.C.plan_cap) {
       V(x.C.plan)[n * 3 + 0] = row;
@@ -397,7 +397,7 @@ MSPQ_D void phase3_flush(const Ctx& x, int i, int k, F&& on_item) {
   for (int f = 0; f < k; ++f)
     for (int base = 0; base < n; base += 32) {
       const int key = base + lane_id();
-      const bool m = key < n && (x.C.cand_first)[key] == f;
+      const bool m = key < n && ((volatile int*)x.C.cand_first)[key] == f;
       unsigned bal = __ballot_sync(0xffffffffu, m);
       while (bal) {
         const int b = __ffs(bal) - 1;
@@ -414,8 +414,8 @@ MSPQ_D void clear_planner(const Ctx& x) {
   const int n = x.C.L * x.C.E;
   for (int key = lane_id(); key < n; key += 32) {
     V(x.C.cand_first)[key] = -1;
-    ((unsigned char*)x.C.sched)[key] = 0;
-    ((unsigned char*)x.C.snap)[key] = contains(x, key) ? 1 : 0;
+    ((volatile unsigned char*)x.C.sched)[key] = 0;
+    ((volatile unsigned char*)x.C.snap)[key] = contains(x, key) ? 1 : 0;
   }
   __syncwarp();
 }
@@ -446,7 +446,7 @@ MSPQ_D int sorted_keys(const int32_t* ids, int K, int l, int E, int* out) {
 }  // namespace
 
 // =============================================================== live engine
-__global__ void k_ctl_begin_cycle(CtlDev C, int k) {
+MSPQ_D void body_begin_cycle(CtlDev C, int k) {
   Ctx x{C, {C.elb_ids, C.elb_gates, nullptr, k}};
   int t1, t2;
   t12(k, C.f1, C.f2, t1, t2);
@@ -459,7 +459,7 @@ __global__ void k_ctl_begin_cycle(CtlDev C, int k) {
 }
 
 // After draft row i: Phase II selection / Phase III flush with immediate (causal) inserts.
-__global__ void k_ctl_plan_row(CtlDev C, int i) {
+MSPQ_D void body_plan_row(CtlDev C, int i) {
   const int k = V(C.scal)[S_K];
   Ctx x{C, {C.elb_ids, C.elb_gates, nullptr, k}};
   put(x, S_NREQ, 0);
@@ -487,7 +487,7 @@ __global__ void k_ctl_plan_row(CtlDev C, int i) {
 
 // Verify layer l over nslots window slots (slot s < k has ELB row s; slot k is unpredicted).
 // tgt[s*K + j] = target expert ids.  Emits the per-expert first-request buffer table.
-__global__ void k_ctl_verify_layer(CtlDev C, int l, int nslots, const int32_t* __restrict__ tgt,
+MSPQ_D void body_verify_layer(CtlDev C, int l, int nslots, const int32_t* __restrict__ tgt,
                                    int32_t* __restrict__ gbuf_out) {
   const int k = V(C.scal)[S_K];
   Ctx x{C, {C.elb_ids, C.elb_gates, nullptr, k}};
@@ -570,7 +570,7 @@ __global__ void k_ctl_verify_layer(CtlDev C, int l, int nslots, const int32_t* _
 // One speculative cycle of Engine::run (sim.cpp:118-295) over trace positions [pos, pos+k):
 // plan + phase-2 inserts, coverage, the token-major slot loop.  Modeled times are NOT
 // computed here; the host restates the lane arithmetic from the emitted counts.
-__global__ void k_ctl_replay_cycle(CtlDev C, ReplayTrace tr, int pos, int k_eff, int head_pos,
+MSPQ_D void body_replay_cycle(CtlDev C, ReplayTrace tr, int pos, int k_eff, int head_pos,
                                    ReplayOut out) {
   const int L = C.L, K = C.K, E = C.E;
   const int64_t rs = (int64_t)L * K;
@@ -736,6 +736,102 @@ __global__ void k_ctl_replay_cycle(CtlDev C, ReplayTrace tr, int pos, int k_eff,
   publish(x);
 }
 
+// ---------------------------------------------------------------- shared-memory staging
+// The whole cache/planner state (and the live ELB ids) is copied into shared memory by the
+// CTA's 256 threads, warp 0 runs the control logic at smem latency, and the mutable state is
+// written back.  Falls back to global memory when the state does not fit (stage_bytes == 0).
+MSPQ_HD size_t al16(size_t b) { return (b + 15) & ~(size_t)15; }
+MSPQ_HD size_t stage_bytes_of(int L, int E, int K, int nbuf, int kmax, bool elb) {
+  const size_t n = (size_t)L * E;
+  return al16(n * 4) + al16(n * 8) + 16 + al16(L * 4) + al16(S_COUNT * 4) + 2 * al16((size_t)(nbuf + 1) * 4) +
+         2 * al16(n) + al16(n * 4) + al16(n * 8) + al16(L * 4) + (elb ? al16((size_t)kmax * L * K * 4) : 0);
+}
+
+template <class T>
+MSPQ_D void cp(T* dst, const T* src, size_t cnt) {
+  for (size_t i = threadIdx.x; i < cnt; i += blockDim.x) dst[i] = src[i];
+}
+
+MSPQ_D void stage(const CtlDev& G, CtlDev& S, unsigned char* sm, bool in, bool elb) {
+  const size_t n = (size_t)G.L * G.E;
+  unsigned char* p = sm;
+  auto take = [&](size_t b) {
+    unsigned char* q = p;
+    p += al16(b);
+    return q;
+  };
+  S.res = (int*)take(n * 4);
+  S.stamp = (unsigned long long*)take(n * 8);
+  S.clock = (unsigned long long*)take(16);
+  S.lsize = (int*)take(G.L * 4);
+  S.scal = (int*)take(S_COUNT * 4);
+  S.free_stack = (int*)take((size_t)(G.nbuf + 1) * 4);
+  S.pending = (int*)take((size_t)(G.nbuf + 1) * 4);
+  S.snap = (unsigned char*)take(n);
+  S.sched = (unsigned char*)take(n);
+  S.cand_first = (int*)take(n * 4);
+  S.cand_conf = (double*)take(n * 8);
+  S.cap = (int*)take(G.L * 4);
+  if (elb) S.elb_ids = (int32_t*)take((size_t)G.kmax * G.L * G.K * 4);
+  if (in) {
+    cp(S.res, G.res, n);
+    cp(S.stamp, G.stamp, n);
+    cp(S.clock, G.clock, 1);
+    cp(S.lsize, G.lsize, G.L);
+    cp(S.scal, G.scal, S_COUNT);
+    cp(S.free_stack, G.free_stack, G.nbuf);
+    cp(S.pending, G.pending, G.nbuf);
+    cp(S.snap, G.snap, n);
+    cp(S.sched, G.sched, n);
+    cp(S.cand_first, G.cand_first, n);
+    cp(S.cand_conf, G.cand_conf, n);
+    cp(S.cap, G.cap, G.L);
+    if (elb) cp(S.elb_ids, G.elb_ids, (size_t)G.kmax * G.L * G.K);
+  } else {
+    cp(G.res, S.res, n);
+    cp(G.stamp, S.stamp, n);
+    cp(G.clock, S.clock, 1);
+    cp(G.lsize, S.lsize, G.L);
+    cp(G.scal, S.scal, S_COUNT);
+    cp(G.free_stack, S.free_stack, G.nbuf);
+    cp(G.pending, S.pending, G.nbuf);
+    cp(G.snap, S.snap, n);
+    cp(G.sched, S.sched, n);
+    cp(G.cand_first, S.cand_first, n);
+    cp(G.cand_conf, S.cand_conf, n);
+  }
+}
+
+// STAGED is a template parameter so the state pointers' address space (shared vs global) is
+// known at compile time inside the control logic.
+#define CTL_KERNEL(NAME, BODY, ELB, PARAMS, ARGS)                   \
+  template <bool STAGED>                                            \
+  __global__ void __launch_bounds__(256) NAME PARAMS {              \
+    extern __shared__ __align__(16) unsigned char ctl_sm[];         \
+    CtlDev S = C;                                                   \
+    if constexpr (STAGED) {                                         \
+      stage(C, S, ctl_sm, true, ELB);                               \
+      __syncthreads();                                              \
+    }                                                               \
+    if (threadIdx.x < 32) BODY ARGS;                                \
+    if constexpr (STAGED) {                                         \
+      __syncthreads();                                              \
+      stage(C, S, ctl_sm, false, ELB);                              \
+    }                                                               \
+  }
+
+CTL_KERNEL(k_ctl_begin_cycle, body_begin_cycle, true, (CtlDev C, int k), (S, k))
+CTL_KERNEL(k_ctl_plan_row, body_plan_row, true, (CtlDev C, int i), (S, i))
+CTL_KERNEL(k_ctl_verify_layer, body_verify_layer, true,
+           (CtlDev C, int l, int nslots, const int32_t* tgt, int32_t* gbuf), (S, l, nslots, tgt, gbuf))
+CTL_KERNEL(k_ctl_replay_cycle, body_replay_cycle, false,
+           (CtlDev C, ReplayTrace tr, int pos, int k_eff, int head_pos, ReplayOut o), (S, tr, pos, k_eff, head_pos, o))
+
+size_t ctl_stage_bytes(const CtlDev& C, bool elb) {
+  const size_t b = stage_bytes_of(C.L, C.E, C.K, C.nbuf, C.kmax, elb);
+  return b + 16 * 1024 <= 227 * 1024 ? b : 0;  // leave room for the kernels' static smem
+}
+
 __global__ void k_ctl_reset(CtlDev C, int nbuf) {
   const int n = C.L * C.E;
   for (int key = lane_id(); key < n; key += 32) {
@@ -759,22 +855,35 @@ cudaError_t ctl_reset(const CtlDev& C, int nbuf, cudaStream_t st) {
   k_ctl_reset<<<1, 32, 0, st>>>(C, nbuf);
   return cudaGetLastError();
 }
+template <class K>
+static size_t prep(K kern, const CtlDev& C, bool elb) {
+  const size_t b = ctl_stage_bytes(C, elb);
+  if (b > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b);
+  return b;
+}
+#define CTL_LAUNCH(KERN, ELB, ...)                                              \
+  do {                                                                          \
+    if (C.stage)                                                                \
+      KERN<true><<<1, 256, prep(KERN<true>, C, ELB), st>>>(__VA_ARGS__);        \
+    else                                                                        \
+      KERN<false><<<1, 32, 0, st>>>(__VA_ARGS__);                               \
+  } while (0)
 cudaError_t ctl_begin_cycle(const CtlDev& C, int k, cudaStream_t st) {
-  k_ctl_begin_cycle<<<1, 32, 0, st>>>(C, k);
+  CTL_LAUNCH(k_ctl_begin_cycle, true, C, k);
   return cudaGetLastError();
 }
 cudaError_t ctl_plan_row(const CtlDev& C, int i, cudaStream_t st) {
-  k_ctl_plan_row<<<1, 32, 0, st>>>(C, i);
+  CTL_LAUNCH(k_ctl_plan_row, true, C, i);
   return cudaGetLastError();
 }
 cudaError_t ctl_verify_layer(const CtlDev& C, int l, int nslots, const int32_t* tgt, int32_t* gbuf,
                              cudaStream_t st) {
-  k_ctl_verify_layer<<<1, 32, 0, st>>>(C, l, nslots, tgt, gbuf);
+  CTL_LAUNCH(k_ctl_verify_layer, true, C, l, nslots, tgt, gbuf);
   return cudaGetLastError();
 }
 cudaError_t ctl_replay_cycle(const CtlDev& C, const ReplayTrace& tr, int pos, int k_eff,
                              int head_pos, const ReplayOut& o, cudaStream_t st) {
-  k_ctl_replay_cycle<<<1, 32, 0, st>>>(C, tr, pos, k_eff, head_pos, o);
+  CTL_LAUNCH(k_ctl_replay_cycle, false, C, tr, pos, k_eff, head_pos, o);
   return cudaGetLastError();
 }
 

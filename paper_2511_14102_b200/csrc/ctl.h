@@ -22,6 +22,7 @@ enum ReplayCount : int { R_NBATCH = 0, R_FETCHED, R_DEMAND, R_NPLAN, R_NLOG, R_O
 
 struct CtlDev {
   int L, E, K, mode, policy, cap_global, budget;
+  int nbuf, kmax, stage;       // stage = run launches on a shared-memory copy of the state
   double f1, f2;
   int* cap;                    // [L] per-layer capacities (entropy-weighted override allowed)
   int* res;                    // [L*E] buffer id or -1
@@ -64,6 +65,7 @@ struct ReplayOut {
   int* flush_keys;  // [L*E]
 };
 
+size_t ctl_stage_bytes(const CtlDev& C, bool elb);
 cudaError_t ctl_reset(const CtlDev& C, int nbuf, cudaStream_t st);
 cudaError_t ctl_begin_cycle(const CtlDev& C, int k, cudaStream_t st);
 cudaError_t ctl_plan_row(const CtlDev& C, int i, cudaStream_t st);

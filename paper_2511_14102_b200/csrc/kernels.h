@@ -67,6 +67,7 @@ struct RouteArgs {
   int32_t* elb_ids;          // [kmax][L][K] (nullable)
   float* elb_gates;
   const int32_t* elb_row;    // device row counter
+  int32_t* sched;            // T == 1: packed draft schedule (nullable), see mspq_gate_topk
   int layer, L, d, E, K;
   float eps;
 };

@@ -198,6 +198,36 @@ __global__ void __launch_bounds__(256) k_resid_norm_route(RouteArgs a) {
     }
     if (a.logits)
       for (int e = 0; e < a.E; ++e) a.logits[(int64_t)t * a.E + e] = lg[e];
+    if (a.sched && gridDim.x == 1) {
+      // one token: K single-entry groups in ascending expert order (reorder_verification)
+      int ord[64];
+      for (int j = 0; j < a.K; ++j) {
+        int p = j;
+        while (p > 0 && sel[ord[p - 1]] > sel[j]) {
+          ord[p] = ord[p - 1];
+          --p;
+        }
+        ord[p] = j;
+      }
+      int32_t* sb = a.sched;
+      int32_t* ge = sb + 4;
+      int32_t* gb = ge + a.K;
+      int32_t* go = gb + a.K;
+      int32_t* et = go + a.K + 1;
+      int32_t* eo = et + a.K;
+      int32_t* eg = eo + a.K;
+      sb[0] = a.K;
+      for (int g2 = 0; g2 < a.K; ++g2) {
+        const int j = ord[g2];
+        ge[g2] = sel[j];
+        gb[g2] = sel[j];
+        go[g2] = g2;
+        et[g2] = 0;
+        eo[j] = g2;
+        eg[g2] = g2;
+      }
+      go[a.K] = a.K;
+    }
   }
 }
 
@@ -394,20 +424,25 @@ __global__ void __launch_bounds__(256) k_int4_m1(ExpertArgs a) {
   const int e0 = a.s.group_off[g];
   const int cols = MODE == 0 ? a.d : a.f;
   const uint16_t* xp = MODE == 0 ? a.xn + (int64_t)a.s.entry_tok[e0] * a.d : a.act + (int64_t)e0 * a.f;
-  for (int i = threadIdx.x; i < cols; i += 256) xs[i] = bf2f(xp[i]);
+  for (int i = threadIdx.x; i < cols / 8; i += 256) {  // 16-byte loads, 8 bf16 -> 8 fp32
+    float f8[8];
+    bf16x8_to_f32(reinterpret_cast<const uint4*>(xp)[i], f8);
+    reinterpret_cast<float4*>(xs)[2 * i] = make_float4(f8[0], f8[1], f8[2], f8[3]);
+    reinterpret_cast<float4*>(xs)[2 * i + 1] = make_float4(f8[4], f8[5], f8[6], f8[7]);
+  }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int row0 = (blockIdx.x * 8 + warp) * RPW;
   const int nrows = MODE == 0 ? a.f : a.d;
-  if (row0 >= nrows) return;
   const unsigned char* blob = a.w_base + ((int64_t)a.layer * a.E + a.s.group_expert[g]) * a.blob_bytes;
   const int64_t q13 = (int64_t)2 * a.f * a.d / 2, s13 = (int64_t)2 * a.f * (a.d / 128) * 2;
   const int64_t q2 = (int64_t)a.d * a.f / 2;
   const unsigned char* wq = blob + (MODE == 0 ? 0 : q13 + s13);
   const uint16_t* ws = reinterpret_cast<const uint16_t*>(blob + (MODE == 0 ? q13 : q13 + s13 + q2));
   constexpr int PR = MODE == 0 ? 2 * RPW : RPW;
-  const int prow0 = MODE == 0 ? 2 * row0 : row0;
   const int nch = cols >> 5, ngr = cols >> 7;
+  // persistent over row blocks: the x staging above is paid once per CTA
+  for (int row0 = (blockIdx.x * 8 + warp) * RPW; row0 < nrows; row0 += gridDim.x * 8 * RPW) {
+  const int prow0 = MODE == 0 ? 2 * row0 : row0;
   float acc[PR];
 #pragma unroll
   for (int r = 0; r < PR; ++r) acc[r] = 0.0f;
@@ -454,6 +489,7 @@ __global__ void __launch_bounds__(256) k_int4_m1(ExpertArgs a) {
 #pragma unroll
       for (int r = 0; r < RPW; ++r) a.y[(int64_t)e0 * a.d + row0 + r] = acc[r];
     }
+  }
   }
 }
 
@@ -673,8 +709,12 @@ cudaError_t launch_expert(const ExpertArgs& a, bool int4, int max_groups, int ma
       cudaFuncSetAttribute(k_int4_m1<1, R1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       attr = true;
     }
-    k_int4_m1<0, R0><<<dim3((a.f + 8 * R0 - 1) / (8 * R0), max_groups), 256, sm0, st>>>(a);
-    k_int4_m1<1, R1><<<dim3((a.d + 8 * R1 - 1) / (8 * R1), max_groups), 256, sm1, st>>>(a);
+    // ~4 CTAs per SM in total across the groups, each looping over row blocks
+    const int per_group = std::max(1, (148 * 4) / std::max(1, max_groups));
+    const int nb0 = std::min((a.f + 8 * R0 - 1) / (8 * R0), per_group);
+    const int nb1 = std::min((a.d + 8 * R1 - 1) / (8 * R1), per_group);
+    k_int4_m1<0, R0><<<dim3(nb0, max_groups), 256, sm0, st>>>(a);
+    k_int4_m1<1, R1><<<dim3(nb1, max_groups), 256, sm1, st>>>(a);
     return cudaGetLastError();
   }
   constexpr int RPW0 = 2, RPW1 = 4;

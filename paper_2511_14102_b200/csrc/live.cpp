@@ -320,18 +320,46 @@ void enqueue_draft_step(mspq_engine* E, cudaStream_t s) {
     CAPI_OK(mspq_gate_topk(E->h, l ? E->yd[pl] : nullptr, l ? E->sd[pl].entry_of : nullptr,
                            l ? E->wts_d + (size_t)(l - 1) * K : nullptr, 1, 0, E->gamma + (size_t)l * d,
                            E->router + (size_t)l * m.E * d, E->xn, E->ids_d + (size_t)l * K, E->wts_d + (size_t)l * K,
-                           nullptr, E->view.elb_ids, E->view.elb_gates, row, l, L, 1, d, m.E, K, m.eps, s));
+                           nullptr, E->view.elb_ids, E->view.elb_gates, row, E->sd[l & 1].base, l, L, 1, d, m.E, K,
+                           m.eps, s));
     Sched& sc = E->sd[l & 1];
-    CAPI_OK(mspq_build_schedule(E->ids_d + (size_t)l * K, 1, K, m.E, nullptr, sc.n_groups, sc.group_expert, sc.group_buf,
-                                sc.group_off, sc.entry_tok, sc.entry_of, nullptr, s));
     CAPI_OK(mspq_moe_int4(sc.n_groups, sc.group_expert, sc.group_buf, sc.group_off, sc.entry_tok, E->xn, E->act,
                           E->yd[l & 1], E->draft4, E->S4, l, m.E, d, m.f, K, 1, s));
   }
   const int pl = (L - 1) & 1;
   CAPI_OK(mspq_gate_topk(E->h, E->yd[pl], E->sd[pl].entry_of, E->wts_d + (size_t)(L - 1) * K, 1, 0, E->gfinal, nullptr,
-                         E->xn, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, L, L, 1, d, m.E, K, m.eps, s));
+                         E->xn, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, L, L, 1, d, m.E, K, m.eps,
+                         s));
   CAPI_OK(mspq_lm_head(E->xn, E->lm, 1, m.V, d, E->logits, s));
   CAPI_OK(mspq_argmax_advance(E->logits, m.V, E->amax, row, E->win_tok() + 1, cur_tok, cur_pos, s));
+}
+
+// Norm gammas + routers (contiguous, ~4 MB for Phi) are re-read every draft step while 2.6 GB
+// of expert/LM weights stream past; mark them L2-persisting for the captured graph's kernels.
+void l2_persist(mspq_engine* E, cudaGraph_t g) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess || prop.persistingL2CacheMaxSize <= 0) return;
+  const size_t want = ((size_t)(E->m.L + 1) * E->m.d + (size_t)E->m.L * E->m.E * E->m.d) * 2;
+  const size_t win = std::min<size_t>(want, prop.accessPolicyMaxWindowSize);
+  cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(win, prop.persistingL2CacheMaxSize));
+  cudaKernelNodeAttrValue v{};
+  v.accessPolicyWindow.base_ptr = E->gamma;
+  v.accessPolicyWindow.num_bytes = win;
+  v.accessPolicyWindow.hitRatio = 1.0f;
+  v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  size_t n = 0;
+  cudaGraphGetNodes(g, nullptr, &n);
+  std::vector<cudaGraphNode_t> nodes(n);
+  cudaGraphGetNodes(g, nodes.data(), &n);
+  for (auto nd : nodes) {
+    cudaGraphNodeType t;
+    cudaGraphNodeGetType(nd, &t);
+    if (t == cudaGraphNodeTypeKernel) cudaGraphKernelNodeSetAttribute(nd, cudaKernelNodeAttributeAccessPolicyWindow, &v);
+  }
+  cudaGetLastError();  // the window is a hint: never fail the engine over it
 }
 
 void capture_draft_graph(mspq_engine* E) {
@@ -344,6 +372,7 @@ void capture_draft_graph(mspq_engine* E) {
     throw;
   }
   CUDA_OK(cudaStreamEndCapture(E->sc, &E->graph));
+  l2_persist(E, E->graph);
   CUDA_OK(cudaGraphInstantiate(&E->gexec, E->graph, 0));
   size_t nn = 0;
   CUDA_OK(cudaGraphGetNodes(E->graph, nullptr, &nn));
@@ -568,7 +597,7 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
                              l ? E->wts_t + (size_t)(l - 1) * T * K : nullptr, E->yv_splits[pl],
                              (long long)T * K * d, E->gamma + (size_t)l * d,
                              E->router + (size_t)l * Ex * d, E->xn, tgt, E->wts_t + (size_t)l * T * K, nullptr, nullptr,
-                             nullptr, nullptr, l, L, T, d, Ex, K, m.eps, E->sc));
+                             nullptr, nullptr, nullptr, l, L, T, d, Ex, K, m.eps, E->sc));
       Sched& sv = E->sv[l & 1];
       CAPI_OK(mspq_cache_verify_layer(E->cache, l, T, tgt, E->gbuf, E->sc));
       CUDA_OK(cudaEventRecord(E->ev_w0[l], E->sc));
@@ -628,7 +657,8 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
     launches += 6;  // embed, final norm, lm head, argmax, accept, begin_cycle
     CAPI_OK(mspq_gate_topk(E->h, E->yv[pl], E->sv[pl].entry_of, E->wts_t + (size_t)(L - 1) * T * K, E->yv_splits[pl],
                            (long long)T * K * d, E->gfinal, nullptr,
-                           E->xn, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, L, L, T, d, Ex, K, m.eps, E->sc));
+                           E->xn, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, L, L, T, d, Ex, K, m.eps,
+                           E->sc));
     CAPI_OK(mspq_lm_head(E->xn, E->lm, T, m.V, d, E->logits, E->sc));
     CAPI_OK(mspq_argmax(E->logits, T, m.V, E->amax, E->sc));
     CAPI_OK(mspq_accept_advance(E->win_tok() + 1, E->amax, k, E->dst + 3, E->dst + 1, E->dst + 2, head_pos, E->sc));

@@ -62,7 +62,7 @@ def gate_topk(h, gamma, router, E, K, eps=1e-6, y=None, entry_of=None, prev_wts=
     check(lib().mspq_gate_topk(_p(h), _p(y), _p(entry_of), _p(prev_wts), y_splits, y_split_stride,
                                _p(gamma), _p(router),
                                _p(xn), _p(ids), _p(wts), _p(logits), _p(elb_ids), _p(elb_gates),
-                               _p(elb_row), layer, L, T, d, E, K, eps, _s()))
+                               _p(elb_row), None, layer, L, T, d, E, K, eps, _s()))
     return xn, ids, wts, logits
 
 

@@ -145,3 +145,21 @@ def test_engine_rejects_bad_configs(cuda):
         eng.configure({"k": 32})
     assert e.value.name == "KOutOfRange"
     eng.close()
+
+
+def test_live_trace_replays_through_reference_tools(cuda, ref):
+    """A live run exported as a reference JSONL trace parses and replays in the reference's own
+    run_simulation, and the device replay of it is bit-exact with that."""
+    import paper_2511_14102_b200 as m
+    eng, cfg = _engine()
+    eng.configure({"policy": "speculative", "cache_capacity": 3, "k": 4})
+    rep = eng.generate([3, 1, 4, 1, 5], 48)
+    eng.close()
+    text = m.to_reference_trace(rep, cfg)
+    lines = text.strip().splitlines()
+    assert len(lines) > 10
+    conf = {"policy": "speculative", "cache_capacity": 3, "k": 4, "collect_plans": True}
+    want = ref.run_simulation(text, conf)
+    got = m.run_simulation(text, conf)
+    from helpers import diff
+    assert diff(got, want) is None
