@@ -134,6 +134,18 @@ int mspq_moe_bf16_tc(const int32_t* n_groups, const int32_t* group_expert, const
                      const void* xn, const void* pool, long long blob_bytes, int d, int f, int T,
                      int K, int max_groups, int split1, int split2, void* ws, float* y,
                      void* stream);
+/* K2 on tcgen05 (umma.cu k_umma_int4): the INT4 draft FFN over TILE-MAJOR INT4 blobs
+ * (mspq_tile_int4), blobs indexed by layer*E + group_buf[g] (= expert id for the draft
+ * schedule).  Exact GPTQ-sym dequant: bf16 (q-8) tiles into smem, per-128-column scales in the
+ * fp32 epilogue.  Same workspace size / outputs as mspq_moe_bf16_tc. */
+int mspq_moe_int4_tc(const int32_t* n_groups, const int32_t* group_expert, const int32_t* group_buf,
+                     const int32_t* group_off, const int32_t* entry_tok, const int32_t* entry_group,
+                     const void* xn, const void* blobs, long long blob_bytes, int layer, int E, int d,
+                     int f, int T, int K, int max_groups, int split1, int split2, void* ws, float* y,
+                     void* stream);
+/* row-major quantised INT4 (q[rows][cols/8] u32, standard nibble order; s[rows][cols/128] bf16)
+ * -> tile-major [rows/128][cols/64][128][8] u32 + [rows/128][cols/128][128] bf16 */
+int mspq_tile_int4(const void* q, const void* s, int rows, int cols, void* tq, void* ts, void* stream);
 /* row-major [rows][cols] bf16 -> tile-major [rows/128][cols/64] SW128 images (16 KB each) */
 int mspq_tile_bf16(const void* src, int rows, int cols, void* dst, void* stream);
 int mspq_lm_head(const void* xn, const void* lm, int T, int V, int d, float* logits,

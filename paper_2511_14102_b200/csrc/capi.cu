@@ -141,6 +141,39 @@ int mspq_moe_bf16_tc(const int32_t* n_groups, const int32_t* group_expert, const
               group_off, b2, y, N * d, split2};
   CK(launch_umma_grouped(u2, max_groups, BN, st), "umma W2");
 }
+int mspq_moe_int4_tc(const int32_t* n_groups, const int32_t* group_expert, const int32_t* group_buf,
+                     const int32_t* group_off, const int32_t* entry_tok, const int32_t* entry_group,
+                     const void* xn, const void* blobs, long long blob_bytes, int layer, int E, int d, int f, int T,
+                     int K, int max_groups, int split1, int split2, void* ws, float* y, void* stream) {
+  if (d % 128 || f % 128 || T > 32 || split1 < 1 || split2 < 1)
+    return set_error(MSPQ_ERR_SHAPE_MISMATCH, "moe_int4_tc: d, f % 128, T <= 32, splits >= 1");
+  const int BN = tc_bn(T);
+  const long long N = (long long)T * K;
+  auto al = [](long long b) { return (b + 1023) / 1024 * 1024; };
+  unsigned char* b1 = (unsigned char*)ws;
+  float* p1 = (float*)(b1 + al(max_groups * (d / 64) * BN * 128));
+  unsigned char* b2 = (unsigned char*)p1 + al((long long)split1 * N * 2 * f * 4);
+  SchedPtrs s{(int32_t*)n_groups, (int32_t*)group_expert, (int32_t*)group_buf, (int32_t*)group_off,
+              (int32_t*)entry_tok, nullptr, (int32_t*)entry_group};
+  cudaStream_t st = ST(stream);
+  const long long q13 = (long long)2 * f * d / 2, s13 = (long long)2 * f * (d / 128) * 2, q2 = (long long)d * f / 2;
+  cudaError_t e = launch_gather_b((const uint16_t*)xn, d, s, max_groups, d, BN, b1, st);
+  if (e != cudaSuccess) return cuda_status(e, "gather_b");
+  UmmaArgs u1{(const unsigned char*)blobs, blob_bytes, 0, 2 * f, d, n_groups, group_buf, group_off, b1, p1,
+              N * 2 * f, split1, q13, layer * E};
+  e = launch_umma_int4(u1, max_groups, BN, st);
+  if (e != cudaSuccess) return cuda_status(e, "umma_int4 W13");
+  e = launch_finalize_act(p1, split1, N * 2 * f, s, entry_group, (int)N, f, BN, b2, st);
+  if (e != cudaSuccess) return cuda_status(e, "finalize_act");
+  UmmaArgs u2{(const unsigned char*)blobs, blob_bytes, q13 + s13, d, f, n_groups, group_buf, group_off, b2, y,
+              N * d, split2, q13 + s13 + q2, layer * E};
+  CK(launch_umma_int4(u2, max_groups, BN, st), "umma_int4 W2");
+}
+int mspq_tile_int4(const void* q, const void* s, int rows, int cols, void* tq, void* ts, void* stream) {
+  if (rows % 128 || cols % 128) return set_error(MSPQ_ERR_SHAPE_MISMATCH, "tile_int4: rows%128, cols%128");
+  CK(launch_tile_int4((const uint32_t*)q, (const uint16_t*)s, rows, cols, (uint32_t*)tq, (uint16_t*)ts, ST(stream)),
+     "tile_int4");
+}
 int mspq_tile_bf16(const void* src, int rows, int cols, void* dst, void* stream) {
   if (rows % 128 || cols % 64) return set_error(MSPQ_ERR_SHAPE_MISMATCH, "tile_bf16: rows%128, cols%64");
   CK(launch_tile_bf16((const uint16_t*)src, rows, cols, (unsigned char*)dst, ST(stream)), "tile_bf16");

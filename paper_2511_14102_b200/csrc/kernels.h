@@ -31,6 +31,8 @@ struct UmmaArgs {
   float* out;                   // [splits][N][rows] fp32 partial planes
   int64_t out_split_stride;
   int splits;
+  int64_t s_off;                // INT4: byte offset of the matrix's scales inside a blob
+  int expert_base;              // INT4: blob index = expert_base + group_buf[g]
 };
 
 struct ExpertArgs {
@@ -73,6 +75,9 @@ struct RouteArgs {
 };
 
 cudaError_t launch_umma_grouped(const UmmaArgs& a, int max_groups, int BN, cudaStream_t st);
+cudaError_t launch_umma_int4(const UmmaArgs& a, int max_groups, int BN, cudaStream_t st);
+cudaError_t launch_tile_int4(const uint32_t* q, const uint16_t* s, int rows, int cols, uint32_t* tq, uint16_t* ts,
+                             cudaStream_t st);
 cudaError_t launch_gather_b(const uint16_t* x, int ld, SchedPtrs s, int max_groups, int kdim, int BN,
                             unsigned char* img, cudaStream_t st);
 cudaError_t launch_finalize_act(const float* p1, int splits, int64_t split_stride, SchedPtrs s,

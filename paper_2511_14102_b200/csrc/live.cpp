@@ -108,7 +108,9 @@ struct mspq_engine {
   Sched sv[2], sd[2];
   float *yv[2] = {nullptr, nullptr}, *yd[2] = {nullptr, nullptr};
   int yv_splits[2] = {1, 1};
+  int yd_split1 = 1, yd_split2 = 1;
   void* tcws = nullptr;
+  void* tcws_d = nullptr;
   static constexpr int kMaxSplit = 8;
   uint16_t* act = nullptr;
   float* logits = nullptr;
@@ -230,14 +232,18 @@ void make_experts(mspq_engine* E) {
   CUDA_OK(cudaMalloc(&tiled[1], S16));
   const bool fill_host = !(E->host_is_shm && E->o.host_store_role != 0);
   const int64_t q13 = (int64_t)2 * m.f * m.d / 2, s13 = (int64_t)2 * m.f * (m.d / 128) * 2, q2 = (int64_t)m.d * m.f / 2;
+  unsigned char* rq;  // row-major quantised staging, tiled into the draft blob below
+  CUDA_OK(cudaMalloc(&rq, S4));
   for (int p = 0; p < E->n_payload; ++p) {
     unsigned char* st = stage[p & 1];
     const int cl = p / m.E, ce = p % m.E;
     CAPI_OK(mspq_fill_expert(m.seed, cl, ce, m.d, m.f, m.a_up, m.a_down, st, E->sc));
+    CAPI_OK(mspq_quantize_int4(st, 2 * m.f, m.d, rq, rq + q13, E->sc));
+    CAPI_OK(mspq_quantize_int4(st + (size_t)2 * m.f * m.d * 2, m.d, m.f, rq + q13 + s13, rq + q13 + s13 + q2, E->sc));
     for (int key = p; key < LE; key += E->n_payload) {
       unsigned char* b4 = E->draft4 + (size_t)key * S4;
-      CAPI_OK(mspq_quantize_int4(st, 2 * m.f, m.d, b4, b4 + q13, E->sc));
-      CAPI_OK(mspq_quantize_int4(st + (size_t)2 * m.f * m.d * 2, m.d, m.f, b4 + q13 + s13, b4 + q13 + s13 + q2, E->sc));
+      CAPI_OK(mspq_tile_int4(rq, rq + q13, 2 * m.f, m.d, b4, b4 + q13, E->sc));
+      CAPI_OK(mspq_tile_int4(rq + q13 + s13, rq + q13 + s13 + q2, m.d, m.f, b4 + q13 + s13, b4 + q13 + s13 + q2, E->sc));
     }
     if (fill_host) {
       // host store keeps the tile-major SW128 images K3 streams with one bulk copy per tile
@@ -248,6 +254,7 @@ void make_experts(mspq_engine* E) {
     }
   }
   CUDA_OK(cudaStreamSynchronize(E->sc));
+  cudaFree(rq);
   cudaFree(stage[0]);
   cudaFree(stage[1]);
   cudaFree(tiled[0]);
@@ -276,10 +283,12 @@ void make_workspaces(mspq_engine* E) {
          o_sv0 = take(sched_ints * 4), o_sv1 = take(sched_ints * 4), o_sd0 = take(Sched::ints(K, K) * 4),
          o_sd1 = take(Sched::ints(K, K) * 4), o_yv0 = take((size_t)mspq_engine::kMaxSplit * E->N * d * 4),
          o_yv1 = take((size_t)mspq_engine::kMaxSplit * E->N * d * 4),
-         o_yd0 = take((size_t)K * d * 4), o_yd1 = take((size_t)K * d * 4), o_act = take((size_t)E->N * f * 2),
+         o_yd0 = take((size_t)mspq_engine::kMaxSplit * K * d * 4), o_yd1 = take((size_t)mspq_engine::kMaxSplit * K * d * 4),
+         o_act = take((size_t)E->N * f * 2),
          o_lg = take((size_t)T * m.V * 4), o_am = take((size_t)T * 4), o_dst = take((size_t)(8 + 2 * (T + 1)) * 4),
          o_gb = take((size_t)m.E * 4),
-         o_tc = take((size_t)mspq_moe_bf16_tc_ws_bytes(d, f, T, K, E->G, mspq_engine::kMaxSplit));
+         o_tc = take((size_t)mspq_moe_bf16_tc_ws_bytes(d, f, T, K, E->G, mspq_engine::kMaxSplit)),
+         o_tcd = take((size_t)mspq_moe_bf16_tc_ws_bytes(d, f, 1, K, K, mspq_engine::kMaxSplit));
   CUDA_OK(cudaMalloc(&E->ws, off));
   CUDA_OK(cudaMemset(E->ws, 0, off));
   char* b = (char*)E->ws;
@@ -303,14 +312,23 @@ void make_workspaces(mspq_engine* E) {
   E->dst = (int32_t*)(b + o_dst);
   E->gbuf = (int32_t*)(b + o_gb);
   E->tcws = (void*)(b + o_tc);
+  E->tcws_d = (void*)(b + o_tcd);
   E->hpin_ints = 64 + (size_t)L * T * K * 2 + (size_t)E->Tmax * L * K * 2 + 4 * T + (size_t)L * 2 + (size_t)L * T * 2 + 64;
   CUDA_OK(cudaHostAlloc((void**)&E->hpin, E->hpin_ints * 4, 0));
 }
 
 // One draft step for a single token, captured once as a CUDA graph.
+int split_for(int units_per_split1, int kblocks) {
+  const int units = std::max(1, units_per_split1);
+  const int sp = (296 + units - 1) / units;
+  return std::max(1, std::min({sp, mspq_engine::kMaxSplit, kblocks}));
+}
+
 void enqueue_draft_step(mspq_engine* E, cudaStream_t s) {
   const auto& m = E->m;
   const int K = m.K, L = m.L, d = m.d;
+  E->yd_split1 = split_for(K * (2 * m.f / 128), d / 64);
+  E->yd_split2 = split_for(K * (d / 128), m.f / 64);
   int32_t* row = E->dst + 0;
   int32_t* cur_tok = E->dst + 1;
   int32_t* cur_pos = E->dst + 2;
@@ -318,16 +336,19 @@ void enqueue_draft_step(mspq_engine* E, cudaStream_t s) {
   for (int l = 0; l < L; ++l) {
     const int pl = (l - 1) & 1;
     CAPI_OK(mspq_gate_topk(E->h, l ? E->yd[pl] : nullptr, l ? E->sd[pl].entry_of : nullptr,
-                           l ? E->wts_d + (size_t)(l - 1) * K : nullptr, 1, 0, E->gamma + (size_t)l * d,
+                           l ? E->wts_d + (size_t)(l - 1) * K : nullptr, E->yd_split2, (long long)K * d,
+                           E->gamma + (size_t)l * d,
                            E->router + (size_t)l * m.E * d, E->xn, E->ids_d + (size_t)l * K, E->wts_d + (size_t)l * K,
                            nullptr, E->view.elb_ids, E->view.elb_gates, row, E->sd[l & 1].base, l, L, 1, d, m.E, K,
                            m.eps, s));
     Sched& sc = E->sd[l & 1];
-    CAPI_OK(mspq_moe_int4(sc.n_groups, sc.group_expert, sc.group_buf, sc.group_off, sc.entry_tok, E->xn, E->act,
-                          E->yd[l & 1], E->draft4, E->S4, l, m.E, d, m.f, K, 1, s));
+    CAPI_OK(mspq_moe_int4_tc(sc.n_groups, sc.group_expert, sc.group_buf, sc.group_off, sc.entry_tok, sc.entry_group,
+                             E->xn, E->draft4, E->S4, l, m.E, d, m.f, 1, K, K, E->yd_split1, E->yd_split2, E->tcws_d,
+                             E->yd[l & 1], s));
   }
   const int pl = (L - 1) & 1;
-  CAPI_OK(mspq_gate_topk(E->h, E->yd[pl], E->sd[pl].entry_of, E->wts_d + (size_t)(L - 1) * K, 1, 0, E->gfinal, nullptr,
+  CAPI_OK(mspq_gate_topk(E->h, E->yd[pl], E->sd[pl].entry_of, E->wts_d + (size_t)(L - 1) * K, E->yd_split2,
+                         (long long)K * d, E->gfinal, nullptr,
                          E->xn, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, L, L, 1, d, m.E, K, m.eps,
                          s));
   CAPI_OK(mspq_lm_head(E->xn, E->lm, 1, m.V, d, E->logits, s));
@@ -566,7 +587,7 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
     CUDA_OK(cudaEventRecord(E->ev_g0[0], E->sc));
     CUDA_OK(cudaGraphLaunch(E->gexec, E->sc));
     CUDA_OK(cudaEventRecord(E->ev_g1[0], E->sc));
-    launches += 1 + E->graph_nodes;
+    launches += E->graph_nodes;
     for (int i = 0; i < k; ++i) {
       CAPI_OK(mspq_cache_plan_row(E->cache, i, E->sc));
       CUDA_OK(cudaEventRecord(E->ev_row[i], E->sc));
@@ -842,9 +863,9 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
   rep["wall_s"] = wall;
   rep["profile"] = c.profile.to_json();
   rep["policy"] = policy_name(c.policy);
-  // kernel evidence: K3 (bf16 grouped verify FFN) per-launch device time (CUDA events on the
-  // launching stream) and algorithmic bytes (expert weights streamed); draft step = one graph
-  // replay (L x (K1 + K2) + LM head).
+  // kernel evidence: K3 (bf16 grouped verify FFN, tcgen05) per-launch device time (CUDA events
+  // on the launching stream) and algorithmic bytes (expert weights streamed); draft step = one
+  // graph replay (L x (K1 + K2 tcgen05 INT4) + LM head).
   json ks;
   ks["kernel_launches"] = launches;
   ks["k3_launches"] = (long)L * (long)cycles.size();

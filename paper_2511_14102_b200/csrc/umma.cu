@@ -235,6 +235,204 @@ __global__ void k_tile_bf16(const uint16_t* __restrict__ src, int rows, int cols
   }
 }
 
+// ============================================================================ K2 v2 (INT4)
+// The draft's GPTQ-sym INT4 expert GEMM on tcgen05.  Per 128x64 tile the producer bulk-copies
+// the 4 KB packed tile (+ the token tile); four dequant warps expand it to the exact bf16
+// (q - 8) values of the SW128 image (one LOP3 + one HSUB2 per two weights via the 128.0 bf16
+// magic), the MMA warp accumulates each 128-column scale group into one of two TMEM buffers, and
+// four epilogue warps apply that group's per-row scale in fp32 while the next group runs:
+//   y[row] = sum_g s[row][g] * sum_{k in g} (q[row][k] - 8) * x[k]      (exact GPTQ-sym dequant)
+// Tile-major INT4 layout: packed [rows/128][cols/64][128 rows x 8 words]; word w of a row holds
+// columns 8w..8w+7 with column 8w+2i at bits 4i and 8w+2i+1 at bits 16+4i.  Scales
+// [rows/128][cols/128][128] bf16.
+MSPQ_D void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(bar)) : "memory");
+}
+MSPQ_D void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+MSPQ_D uint4 dequant8(uint32_t w) {
+  // (w >> 4i) & 0x000F000F | 0x43004300 = bf16x2(128 + q_lo, 128 + q_hi); minus 136 -> exact q - 8
+  const __nv_bfloat162 off = __floats2bfloat162_rn(136.0f, 136.0f);
+  uint32_t o[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint32_t t = ((w >> (4 * i)) & 0x000F000Fu) | 0x43004300u;
+    __nv_bfloat162 v = *reinterpret_cast<__nv_bfloat162*>(&t);
+    v = __hsub2(v, off);
+    o[i] = *reinterpret_cast<uint32_t*>(&v);
+  }
+  return make_uint4(o[0], o[1], o[2], o[3]);
+}
+
+template <int BN, int PS, int DS>
+__global__ void __launch_bounds__(320, 1) k_umma_int4(UmmaArgs a) {
+  constexpr int TILE_Q = BM * BK / 2;  // 4 KB packed
+  constexpr int TB = BN * 128;         // token tile bytes
+  const int S = a.splits, RT = a.rows / BM;
+  const int unit = blockIdx.x;
+  const int s = unit % S, rt = (unit / S) % RT, g = unit / (S * RT);
+  if (g >= *a.n_groups) return;
+  const int kb_total = a.kdim / BK;
+  int per = (kb_total + S - 1) / S;
+  per = (per + 1) & ~1;  // splits align to 128-column scale groups
+  const int kb0 = s * per, nk = max(0, min(kb_total, kb0 + per) - kb0);
+  const int e0 = a.group_off[g], m = a.group_off[g + 1] - e0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* outp = a.out + (int64_t)s * a.out_split_stride;
+  if (nk == 0) {
+    for (int i = threadIdx.x; i < m * BM; i += blockDim.x)
+      outp[(int64_t)(e0 + i / BM) * a.rows + rt * BM + (i % BM)] = 0.0f;
+    return;
+  }
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  unsigned char* sD = base;                        // DS x (16 KB A + TB)   dequantized stages
+  unsigned char* sP = sD + DS * (TILE_A + TB);     // PS x (4 KB packed + TB)
+  uint64_t* full_p = reinterpret_cast<uint64_t*>(sP + PS * (TILE_Q + TB));
+  uint64_t* empty_p = full_p + PS;
+  uint64_t* full_d = empty_p + PS;
+  uint64_t* empty_d = full_d + DS;
+  uint64_t* accf = empty_d + DS;  // [2]
+  uint64_t* acce = accf + 2;      // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 2);
+
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < PS; ++i) {
+      mbar_init(&full_p[i], 1);
+      mbar_init(&empty_p[i], 128);
+    }
+    for (int i = 0; i < DS; ++i) {
+      mbar_init(&full_d[i], 128);
+      mbar_init(&empty_d[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&accf[i], 1);
+      mbar_init(&acce[i], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                 "r"(BN * 2 <= 32 ? 32 : 64));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int ngr = nk / 2;
+
+  if (warp == 0) {
+    if (lane == 0) {  // producer: packed weight tile + token tile per k-block
+      const unsigned char* wsrc = a.w_base + ((int64_t)a.expert_base + a.group_buf[g]) * a.blob_bytes + a.w_off +
+                                  ((int64_t)rt * kb_total + kb0) * TILE_Q;
+      const unsigned char* bsrc = a.bimg + ((int64_t)g * kb_total + kb0) * TB;
+      for (int i = 0; i < nk; ++i) {
+        const int st = i % PS, r = i / PS;
+        if (r > 0) mbar_wait(&empty_p[st], (r - 1) & 1);
+        mbar_expect_tx(&full_p[st], TILE_Q + TB);
+        unsigned char* dst = sP + st * (TILE_Q + TB);
+        bulk_g2s(dst, wsrc + (int64_t)i * TILE_Q, TILE_Q, &full_p[st]);
+        bulk_g2s(dst + TILE_Q, bsrc + (int64_t)i * TB, TB, &full_p[st]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer: one TMEM accumulator per 128-column scale group (2 buffers)
+      constexpr uint32_t idesc = idesc_bf16(BN);
+      for (int i = 0; i < nk; ++i) {
+        const int st = i % DS, r = i / DS;
+        const int gi = i >> 1, b = gi & 1;
+        const bool first = (i & 1) == 0;
+        if (first && gi >= 2) mbar_wait(&acce[b], ((gi >> 1) - 1) & 1);
+        mbar_wait(&full_d[st], r & 1);
+        tc_fence_after();
+        const uint64_t da = sw128_desc(su32(sD + st * (TILE_A + TB)));
+        const uint64_t db = sw128_desc(su32(sD + st * (TILE_A + TB) + TILE_A));
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k)
+          umma_bf16(tmem + b * BN, da + 2 * k, db + 2 * k, idesc, !(first && k == 0));
+        umma_commit(&empty_d[st]);
+        if (!first) umma_commit(&accf[b]);
+      }
+    }
+  } else if (warp < 6) {  // dequant warps: thread t owns tile row t
+    const int t = threadIdx.x - 64;
+    for (int i = 0; i < nk; ++i) {
+      const int ps = i % PS, pr = i / PS, ds = i % DS, dr = i / DS;
+      mbar_wait(&full_p[ps], pr & 1);
+      if (dr > 0) mbar_wait(&empty_d[ds], (dr - 1) & 1);
+      const unsigned char* src = sP + ps * (TILE_Q + TB);
+      unsigned char* dst = sD + ds * (TILE_A + TB);
+      const uint4 w0 = *reinterpret_cast<const uint4*>(src + t * 32);
+      const uint4 w1 = *reinterpret_cast<const uint4*>(src + t * 32 + 16);
+      const uint32_t ws[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+      for (int wi = 0; wi < 8; ++wi) *reinterpret_cast<uint4*>(dst + sw128_off(t, 8 * wi)) = dequant8(ws[wi]);
+      for (int c = t; c < TB / 16; c += 128)
+        reinterpret_cast<uint4*>(dst + TILE_A)[c] = reinterpret_cast<const uint4*>(src + TILE_Q)[c];
+      fence_proxy_async_smem();
+      mbar_arrive(&full_d[ds]);
+      mbar_arrive(&empty_p[ps]);
+    }
+  } else {  // epilogue warps 6..9: per-group scale, fp32 accumulation in registers
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const uint16_t* sc = reinterpret_cast<const uint16_t*>(a.w_base + ((int64_t)a.expert_base + a.group_buf[g]) * a.blob_bytes +
+                                                           a.s_off) +
+                         ((int64_t)rt * (a.kdim / 128) + kb0 / 2) * BM + row;
+    float acc[BN];
+#pragma unroll
+    for (int j = 0; j < BN; ++j) acc[j] = 0.0f;
+    for (int gi = 0; gi < ngr; ++gi) {
+      const int b = gi & 1;
+      const float scale = bf2f(sc[(int64_t)gi * BM]);
+      mbar_wait(&accf[b], (gi >> 1) & 1);
+      tc_fence_after();
+      float v[BN];
+      tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + b * BN, v);
+      if (BN == 32) tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + b * BN + 16, v + 16);
+      tc_fence_before();
+      mbar_arrive(&acce[b]);
+#pragma unroll
+      for (int j = 0; j < BN; ++j) acc[j] = fmaf(scale, v[j], acc[j]);
+    }
+    for (int j = 0; j < m && j < BN; ++j) outp[(int64_t)(e0 + j) * a.rows + rt * BM + row] = acc[j];
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN * 2 <= 32 ? 32 : 64));
+  }
+}
+
+// row-major quantised (standard nibble order, scales [rows][cols/128]) -> tile-major INT4 layout
+__global__ void k_tile_int4(const uint32_t* __restrict__ q, const uint16_t* __restrict__ sc, int rows, int cols,
+                            uint32_t* __restrict__ tq, uint16_t* __restrict__ ts) {
+  const int wpr = cols / 8;  // words per row
+  const int kbt = cols / BK, ngr = cols / 128;
+  const int64_t nw = (int64_t)rows * wpr;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nw; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / wpr;
+    const int w = (int)(i - r * wpr);
+    const uint32_t v = q[i];
+    uint32_t o = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t nib = (v >> (4 * j)) & 0xFu;
+      o |= nib << ((j & 1) ? 16 + 4 * (j >> 1) : 4 * (j >> 1));
+    }
+    const int rt = (int)(r / BM), rr = (int)(r % BM), kb = w / 8, ww = w % 8;
+    tq[(((int64_t)rt * kbt + kb) * BM + rr) * 8 + ww] = o;
+  }
+  const int64_t ns = (int64_t)rows * ngr;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ns; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / ngr;
+    const int gg = (int)(i - r * ngr);
+    ts[(((int64_t)(r / BM) * ngr) + gg) * BM + (r % BM)] = sc[i];
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_umma_grouped(const UmmaArgs& a, int max_groups, int BN, cudaStream_t st) {
@@ -250,6 +448,29 @@ cudaError_t launch_umma_grouped(const UmmaArgs& a, int max_groups, int BN, cudaS
     cudaFuncSetAttribute(k_umma_grouped<32, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_umma_grouped<32, STAGES><<<units, 192, smem, st>>>(a);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_umma_int4(const UmmaArgs& a, int max_groups, int BN, cudaStream_t st) {
+  constexpr int PS = 6, DS = 3;
+  const int units = max_groups * (a.rows / BM) * a.splits;
+  if (units == 0) return cudaSuccess;
+  auto smem = [&](int bn) {
+    return (size_t)1024 + DS * (TILE_A + bn * 128) + PS * (BM * BK / 2 + bn * 128) + (2 * PS + 2 * DS + 4) * 8 + 16;
+  };
+  if (BN == 16) {
+    cudaFuncSetAttribute(k_umma_int4<16, PS, DS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(16));
+    k_umma_int4<16, PS, DS><<<units, 320, smem(16), st>>>(a);
+  } else {
+    cudaFuncSetAttribute(k_umma_int4<32, PS, DS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(32));
+    k_umma_int4<32, PS, DS><<<units, 320, smem(32), st>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tile_int4(const uint32_t* q, const uint16_t* s, int rows, int cols, uint32_t* tq, uint16_t* ts,
+                             cudaStream_t st) {
+  k_tile_int4<<<148 * 4, 256, 0, st>>>(q, s, rows, cols, tq, ts);
   return cudaGetLastError();
 }
 

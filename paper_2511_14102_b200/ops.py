@@ -126,6 +126,26 @@ def moe_bf16_tc(s: Schedule, xn, pool_tiled, blob_bytes, d, f, split1=1, split2=
     return y.sum(0) if split2 > 1 else y[0], y
 
 
+def tile_int4(q_i32, s_i16, rows, cols):
+    tq = torch.empty_like(q_i32)
+    ts = torch.empty_like(s_i16)
+    check(lib().mspq_tile_int4(_p(q_i32), _p(s_i16), rows, cols, _p(tq), _p(ts), _s()))
+    return tq, ts
+
+
+def moe_int4_tc(s: Schedule, xn, blobs_tiled, blob_bytes, layer, E, d, f, split1=1, split2=1):
+    """K2 on tcgen05 over tile-major INT4 blobs; returns y summed over split planes."""
+    T, K, G = s.T, s.K, s.G
+    N = T * K
+    ws = torch.empty(lib().mspq_moe_bf16_tc_ws_bytes(d, f, T, K, G, split1), dtype=torch.uint8,
+                     device=xn.device)
+    y = torch.empty(split2, N, d, dtype=torch.float32, device=xn.device)
+    check(lib().mspq_moe_int4_tc(_p(s.n_groups), _p(s.group_expert), _p(s.group_buf), _p(s.group_off),
+                                 _p(s.entry_tok), _p(s.entry_group), _p(xn), _p(blobs_tiled), blob_bytes,
+                                 layer, E, d, f, T, K, G, split1, split2, _p(ws), _p(y), _s()))
+    return y.sum(0) if split2 > 1 else y[0], y
+
+
 def lm_head(xn, lm, V):
     T, d = xn.shape
     logits = torch.empty(T, V, dtype=torch.float32, device=xn.device)

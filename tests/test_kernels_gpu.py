@@ -262,3 +262,41 @@ def test_moe_bf16_tcgen05_within_tolerance(cuda, name, E, K, d, f, T, split1, sp
             got = y[eo[t, j]]
             tol = 2e-3 * np.abs(want).max() + 1e-5
             assert np.abs(got - want).max() <= tol, (t, j, np.abs(got - want).max(), tol)
+
+
+@pytest.mark.parametrize("name,E,K,d,f", SHAPES)
+@pytest.mark.parametrize("T,split1,split2", [(1, 1, 1), (1, 2, 5), (5, 3, 2)])
+def test_moe_int4_tcgen05_within_tolerance(cuda, name, E, K, d, f, T, split1, split2):
+    """K2 v2 (tcgen05, bf16 (q-8) tiles + per-group fp32 scale epilogue) vs the oracle's
+    dequantised INT4 FFN."""
+    from paper_2511_14102_b200 import ops
+    if name == "mixtral":
+        T = min(T, 2)
+    desc = om.ModelDesc(L=2, E=E, K=K, d=d, f=f, V=512, seed=23)
+    mdl = om.Model(desc)
+    layer = 1
+    rng = np.random.default_rng(T + split2)
+    ids = np.stack([rng.choice(E, K, replace=False) for _ in range(T)]).astype(np.int32)
+    used = sorted(set(ids.ravel().tolist()))
+    xn = om.f32_to_bf16(rng.standard_normal((T, d)).astype(np.float32))
+    s = ops.build_schedule(torch.from_numpy(ids).cuda(), E)
+    s4 = ops.int4_blob_bytes(d, f)
+    blobs = torch.zeros(2 * E * s4, dtype=torch.uint8, device="cuda")
+    for e in used:
+        b = ops.fill_expert(desc.seed, layer, e, d, f, desc.a_up(), desc.a_down())
+        q13, s13 = ops.quantize_int4(b[:2 * f * d], 2 * f, d)
+        q2, s2 = ops.quantize_int4(b[2 * f * d:], d, f)
+        tq13, ts13 = ops.tile_int4(q13, s13, 2 * f, d)
+        tq2, ts2 = ops.tile_int4(q2, s2, d, f)
+        parts = [tq13.view(torch.uint8), ts13.view(torch.uint8), tq2.view(torch.uint8), ts2.view(torch.uint8)]
+        o = (layer * E + e) * s4
+        blobs[o:o + s4] = torch.cat(parts)
+    y, _ = ops.moe_int4_tc(s, to_dev(xn), blobs, s4, layer, E, d, f, split1=split1, split2=split2)
+    y = y.cpu().numpy()
+    eo = s.entry_of.cpu().numpy().reshape(T, K)
+    for t in range(T):
+        for j in range(K):
+            want, _ = mdl.ffn(xn[t], layer, int(ids[t, j]), draft=True)
+            got = y[eo[t, j]]
+            tol = 2e-3 * np.abs(want).max() + 1e-5
+            assert np.abs(got - want).max() <= tol, (t, j, np.abs(got - want).max(), tol)
