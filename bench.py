@@ -124,6 +124,25 @@ def peaks():
     return 6650.0, 1590.0, "fallback"
 
 
+def ncu_traffic():
+    """dram read+write bytes per launch of k_umma_grouped from the committed ncu --set full
+    capture (profiles/), with that launch's algorithmic bytes for comparison."""
+    p = os.path.join(ROOT, "profiles", "r01", "ncu_raw_k_umma_grouped.txt")
+    if not os.path.exists(p):
+        return None
+    v = {}
+    for ln in open(p):
+        k, _, val = ln.partition(" = ")
+        v[k.strip()] = val.strip()
+    try:
+        rd = float(v["dram__bytes_read.sum"]) * 1e6  # MB in the capture
+        wr = float(v["dram__bytes_write.sum"]) * 1e6
+    except (KeyError, ValueError):
+        return None
+    return {"bytes_per_launch": rd + wr, "algorithmic_bytes_per_launch": 7 * 12800 * 4096 * 2,
+            "source": "profiles/r01/ncu_raw_k_umma_grouped.txt (W13 GEMM of one verify layer, 7 experts)"}
+
+
 def prompts(n, V, seed):
     import random
     rng = random.Random(seed)
@@ -280,9 +299,10 @@ def main():
         "e2e": {"value": tok_all / wall_max, "unit": "tokens/s", "h2d_bytes_per_step": 128 * 4,
                 "d2h_bytes_per_step": a.tokens * 4,
                 "expert_h2d_bytes_per_step": h2d / a.steps},
-        "roofline": {"bound": "hbm", "kernel": "K3 bf16 grouped verify FFN (k_grouped_rows<bf16>)",
+        "roofline": {"bound": "hbm",
+                     "kernel": "K3 bf16 grouped verify FFN on tcgen05 (gather + k_umma_grouped W13 + SiLU + W2), per layer",
                      "achieved": k3_ach, "peak": hbm, "unit": "GB/s", "frac": k3_ach / hbm if hbm else None,
-                     "traffic": None, "peak_kind": pk_kind,
+                     "traffic": ncu_traffic(), "peak_kind": pk_kind,
                      "bytes_per_launch": k3_b / max(k3_n, 1), "launch_ms": k3_t / max(k3_n, 1) * 1e3},
         "path_roofline": {"bound": "pcie" if t_pcie >= t_hbm else "hbm", "t_roof_s": t_roof,
                           "t_measured_s": dev_t, "frac": t_roof / dev_t if dev_t else None,

@@ -235,6 +235,7 @@ int mspq_cache_create(int L, int E, int K, int kmax, int nbuf, int log_cap, mspq
          o_cc = take(n * 8), o_eids = take((size_t)kmax * L * K * 4),
          o_eg = take((size_t)kmax * L * K * 4),
          o_log = take((size_t)C.log_cap * 24), o_plan = take((size_t)C.plan_cap * 12),
+         o_reqd = take((size_t)C.req_cap * 12),
          o_cov = take(L * 8), o_step = take((size_t)L * (kmax + 1) * 8);
   cudaError_t e = cudaMalloc(&c->blk, off);
   if (e != cudaSuccess) {
@@ -272,6 +273,7 @@ int mspq_cache_create(int L, int E, int K, int kmax, int nbuf, int log_cap, mspq
   C.hsched = (int*)((char*)dptr + 256);
   C.req = (int*)((char*)dptr + 256 + (size_t)(E + 8) * 4);
   C.log = (int*)(b + o_log);
+  C.req_dev = (int*)(b + o_reqd);
   C.plan = (int*)(b + o_plan);
   C.cov = (int*)(b + o_cov);
   C.step = (int*)(b + o_step);

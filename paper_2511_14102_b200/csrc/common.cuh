@@ -147,4 +147,48 @@ MSPQ_D float warp_dot_bf16(const uint16_t* __restrict__ x, const uint16_t* __res
   return warp_butterfly_sum(acc);
 }
 
+// Two fixed-order warp dots sharing x (each identical to warp_dot_bf16), loads interleaved.
+MSPQ_D void warp_dot2_bf16(const uint16_t* __restrict__ x, const uint16_t* __restrict__ w0,
+                           const uint16_t* __restrict__ w1, int n, int lane, float& z0, float& z1) {
+  float a0 = 0.0f, a1 = 0.0f;
+  const int nchunks = n >> 3;
+  int c = lane;
+  for (; c + 96 < nchunks; c += 128) {
+    uint4 v0[4], v1[4], xv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      v0[u] = ldg_nc_v4(w0 + 8 * (c + 32 * u));
+      v1[u] = ldg_nc_v4(w1 + 8 * (c + 32 * u));
+      xv[u] = *reinterpret_cast<const uint4*>(x + 8 * (c + 32 * u));
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      float xf[8], f0[8], f1[8];
+      bf16x8_to_f32(xv[u], xf);
+      bf16x8_to_f32(v0[u], f0);
+      bf16x8_to_f32(v1[u], f1);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        a0 = fmaf(xf[e], f0[e], a0);
+        a1 = fmaf(xf[e], f1[e], a1);
+      }
+    }
+  }
+  for (; c < nchunks; c += 32) {
+    const uint4 xv = *reinterpret_cast<const uint4*>(x + 8 * c);
+    const uint4 v0 = ldg_nc_v4(w0 + 8 * c), v1 = ldg_nc_v4(w1 + 8 * c);
+    float xf[8], f0[8], f1[8];
+    bf16x8_to_f32(xv, xf);
+    bf16x8_to_f32(v0, f0);
+    bf16x8_to_f32(v1, f1);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      a0 = fmaf(xf[e], f0[e], a0);
+      a1 = fmaf(xf[e], f1[e], a1);
+    }
+  }
+  z0 = warp_butterfly_sum(a0);
+  z1 = warp_butterfly_sum(a1);
+}
+
 }  // namespace mspq

@@ -202,7 +202,7 @@ MSPQ_D void copy_request(const Ctx& x, int key, int kind) {
     volatile int* scal = V(x.C.scal);
     int n = scal[S_NREQ];
     if (n < x.C.req_cap) {
-      volatile int* rq = (volatile int*)x.C.req + (int64_t)n * 3;
+      int* rq = x.C.req_dev + (int64_t)n * 3;  // device staging; copied to mapped memory at exit
       rq[0] = key;
       rq[1] = V(x.C.res)[key];
       rq[2] = kind;
@@ -802,6 +802,16 @@ MSPQ_D void stage(const CtlDev& G, CtlDev& S, unsigned char* sm, bool in, bool e
   }
 }
 
+// copy requests are accumulated in device memory and written to the host-mapped queue in one
+// coalesced pass at kernel exit (the host reads them after the launch's event)
+MSPQ_D void flush_requests(const CtlDev& G, const CtlDev& S) {
+  const int n = min(((volatile int*)S.scal)[S_NREQ], G.req_cap);
+  const int4* src = reinterpret_cast<const int4*>(G.req_dev);
+  volatile int* dst = (volatile int*)G.req;
+  for (int i = threadIdx.x; i < n * 3; i += blockDim.x) dst[i] = G.req_dev[i];
+  (void)src;
+}
+
 // STAGED is a template parameter so the state pointers' address space (shared vs global) is
 // known at compile time inside the control logic.
 #define CTL_KERNEL(NAME, BODY, ELB, PARAMS, ARGS)                   \
@@ -814,10 +824,9 @@ MSPQ_D void stage(const CtlDev& G, CtlDev& S, unsigned char* sm, bool in, bool e
       __syncthreads();                                              \
     }                                                               \
     if (threadIdx.x < 32) BODY ARGS;                                \
-    if constexpr (STAGED) {                                         \
-      __syncthreads();                                              \
-      stage(C, S, ctl_sm, false, ELB);                              \
-    }                                                               \
+    __syncthreads();                                                \
+    flush_requests(C, S);                                           \
+    if constexpr (STAGED) stage(C, S, ctl_sm, false, ELB);          \
   }
 
 CTL_KERNEL(k_ctl_begin_cycle, body_begin_cycle, true, (CtlDev C, int k), (S, k))

@@ -38,7 +38,8 @@ struct CtlDev {
   double* cand_conf;           // [L*E] best confidence seen
   int32_t* elb_ids;            // [kmax][L][K] live ELB (written by the draft router)
   float* elb_gates;            // [kmax][L][K]
-  int* req;                    // [req_cap][3] copy requests (key, buffer, kind)
+  int* req;                    // [req_cap][3] copy requests (key, buffer, kind), host-mapped
+  int* req_dev;                // [req_cap][3] device-side accumulation of the same
   int req_cap;
   int* log;                    // [log_cap][6] (kind, tag, key, hit, victim, buffer)
   int log_cap;

@@ -110,34 +110,59 @@ __global__ void __launch_bounds__(256) k_resid_norm_route(RouteArgs a) {
   const int t = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   float* h = a.h + (int64_t)t * a.d;
   const int nch = a.d >> 2;
-  float acc = 0.0f;
-  for (int c = tid; c < nch; c += 256) {
-    float4 hv = reinterpret_cast<float4*>(h)[c];
-    if (a.y) {
-      float v[4] = {hv.x, hv.y, hv.z, hv.w};
-      float cb[4] = {0.f, 0.f, 0.f, 0.f};
-      for (int j = 0; j < a.K; ++j) {
-        const float w = a.prev_wts[t * a.K + j];
-        const float* yb = a.y + (int64_t)a.entry_of[t * a.K + j] * a.d;
-        float4 yv = reinterpret_cast<const float4*>(yb)[c];
-        for (int sp = 1; sp < a.y_splits; ++sp) {  // K-split partial planes, fixed order
-          const float4 p = reinterpret_cast<const float4*>(yb + sp * a.y_split_stride)[c];
-          yv = make_float4(__fadd_rn(yv.x, p.x), __fadd_rn(yv.y, p.y), __fadd_rn(yv.z, p.z), __fadd_rn(yv.w, p.w));
-        }
-        cb[0] = __fadd_rn(cb[0], __fmul_rn(w, yv.x));
-        cb[1] = __fadd_rn(cb[1], __fmul_rn(w, yv.y));
-        cb[2] = __fadd_rn(cb[2], __fmul_rn(w, yv.z));
-        cb[3] = __fadd_rn(cb[3], __fmul_rn(w, yv.w));
+  // Latency-bound single CTA per token: every thread owns <= 8 float4 chunks (c = tid + 256 i,
+  // d <= 8192); all loads of a phase are issued before use.  Summation orders are unchanged
+  // (k-slot order for the combine, chunk order for the sum of squares).
+  constexpr int MAXC = 8;
+  float4 hv[MAXC];
+#pragma unroll
+  for (int i = 0; i < MAXC; ++i)
+    if (tid + 256 * i < nch) hv[i] = reinterpret_cast<float4*>(h)[tid + 256 * i];
+  if (a.y) {
+    float4 cb[MAXC];
+#pragma unroll
+    for (int i = 0; i < MAXC; ++i) cb[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j = 0; j < a.K; ++j) {
+      const float w = a.prev_wts[t * a.K + j];
+      const float* yb = a.y + (int64_t)a.entry_of[t * a.K + j] * a.d;
+      float4 yv[MAXC];
+#pragma unroll
+      for (int i = 0; i < MAXC; ++i)
+        if (tid + 256 * i < nch) yv[i] = reinterpret_cast<const float4*>(yb)[tid + 256 * i];
+      for (int sp = 1; sp < a.y_splits; ++sp) {  // K-split partial planes, fixed order
+#pragma unroll
+        for (int i = 0; i < MAXC; ++i)
+          if (tid + 256 * i < nch) {
+            const float4 p = reinterpret_cast<const float4*>(yb + sp * a.y_split_stride)[tid + 256 * i];
+            yv[i] = make_float4(__fadd_rn(yv[i].x, p.x), __fadd_rn(yv[i].y, p.y), __fadd_rn(yv[i].z, p.z),
+                                __fadd_rn(yv[i].w, p.w));
+          }
       }
-      hv = make_float4(__fadd_rn(v[0], cb[0]), __fadd_rn(v[1], cb[1]), __fadd_rn(v[2], cb[2]),
-                       __fadd_rn(v[3], cb[3]));
-      reinterpret_cast<float4*>(h)[c] = hv;
+#pragma unroll
+      for (int i = 0; i < MAXC; ++i) {
+        cb[i].x = __fadd_rn(cb[i].x, __fmul_rn(w, yv[i].x));
+        cb[i].y = __fadd_rn(cb[i].y, __fmul_rn(w, yv[i].y));
+        cb[i].z = __fadd_rn(cb[i].z, __fmul_rn(w, yv[i].z));
+        cb[i].w = __fadd_rn(cb[i].w, __fmul_rn(w, yv[i].w));
+      }
     }
-    acc = fmaf(hv.x, hv.x, acc);
-    acc = fmaf(hv.y, hv.y, acc);
-    acc = fmaf(hv.z, hv.z, acc);
-    acc = fmaf(hv.w, hv.w, acc);
+#pragma unroll
+    for (int i = 0; i < MAXC; ++i)
+      if (tid + 256 * i < nch) {
+        hv[i] = make_float4(__fadd_rn(hv[i].x, cb[i].x), __fadd_rn(hv[i].y, cb[i].y), __fadd_rn(hv[i].z, cb[i].z),
+                            __fadd_rn(hv[i].w, cb[i].w));
+        reinterpret_cast<float4*>(h)[tid + 256 * i] = hv[i];
+      }
   }
+  float acc = 0.0f;
+#pragma unroll
+  for (int i = 0; i < MAXC; ++i)
+    if (tid + 256 * i < nch) {
+      acc = fmaf(hv[i].x, hv[i].x, acc);
+      acc = fmaf(hv[i].y, hv[i].y, acc);
+      acc = fmaf(hv[i].z, hv[i].z, acc);
+      acc = fmaf(hv[i].w, hv[i].w, acc);
+    }
   acc = warp_butterfly_sum(acc);
   if (lane == 0) part[warp] = acc;
   __syncthreads();
@@ -149,22 +174,36 @@ __global__ void __launch_bounds__(256) k_resid_norm_route(RouteArgs a) {
   }
   __syncthreads();
   const float r = rscale;
-  for (int c = tid; c < nch; c += 256) {
-    float4 hv = reinterpret_cast<float4*>(h)[c];
-    float v[4] = {hv.x, hv.y, hv.z, hv.w};
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int i = 4 * c + e;
-      uint16_t b = f2bf(__fmul_rn(__fmul_rn(v[e], r), bf2f(a.gamma[i])));
-      xs[i] = b;
-      a.xn[(int64_t)t * a.d + i] = b;
+  for (int i = 0; i < MAXC; ++i) {
+    const int c = tid + 256 * i;
+    if (c < nch) {
+      const uint2 gq = reinterpret_cast<const uint2*>(a.gamma)[c];
+      const float v[4] = {hv[i].x, hv[i].y, hv[i].z, hv[i].w};
+      const float gm[4] = {__uint_as_float(gq.x << 16), __uint_as_float(gq.x & 0xffff0000u),
+                           __uint_as_float(gq.y << 16), __uint_as_float(gq.y & 0xffff0000u)};
+      uint16_t b[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) b[e] = f2bf(__fmul_rn(__fmul_rn(v[e], r), gm[e]));
+      const uint2 packed = make_uint2((uint32_t)b[0] | ((uint32_t)b[1] << 16), (uint32_t)b[2] | ((uint32_t)b[3] << 16));
+      reinterpret_cast<uint2*>(xs)[c] = packed;
+      reinterpret_cast<uint2*>(a.xn + (int64_t)t * a.d)[c] = packed;
     }
   }
   if (!a.router) return;
   __syncthreads();
-  for (int e = warp; e < a.E; e += 8) {
-    float z = warp_dot_bf16(xs, a.router + (int64_t)e * a.d, a.d, lane);
-    if (lane == 0) lg[e] = z;
+  for (int e = warp; e < a.E; e += 16) {
+    if (e + 8 < a.E) {
+      float z0, z1;
+      warp_dot2_bf16(xs, a.router + (int64_t)e * a.d, a.router + (int64_t)(e + 8) * a.d, a.d, lane, z0, z1);
+      if (lane == 0) {
+        lg[e] = z0;
+        lg[e + 8] = z1;
+      }
+    } else {
+      const float z = warp_dot_bf16(xs, a.router + (int64_t)e * a.d, a.d, lane);
+      if (lane == 0) lg[e] = z;
+    }
   }
   __syncthreads();
   if (tid == 0) {

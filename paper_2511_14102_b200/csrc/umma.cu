@@ -264,10 +264,22 @@ MSPQ_D uint4 dequant8(uint32_t w) {
   return make_uint4(o[0], o[1], o[2], o[3]);
 }
 
-template <int BN, int PS, int DS>
-__global__ void __launch_bounds__(320, 1) k_umma_int4(UmmaArgs a) {
-  constexpr int TILE_Q = BM * BK / 2;  // 4 KB packed
-  constexpr int TB = BN * 128;         // token tile bytes
+MSPQ_D void sts128(uint32_t addr, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+MSPQ_D uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+
+// warps: 0 producer, 1 MMA, 2..9 dequant (256 threads, two per tile row), 10..13 epilogue
+template <int BN, int KBS, int PS, int DS, int NACC>
+__global__ void __launch_bounds__(448, 2) k_umma_int4(UmmaArgs a) {
+  constexpr int TILE_Q = BM * BK / 2;  // 4 KB packed per 128x64 tile
+  constexpr int TB = BN * 128;         // token tile bytes per k-block
+  constexpr int STAGE = KBS * (TILE_Q + TB);  // one bulk-copy stage = KBS consecutive k-blocks
   const int S = a.splits, RT = a.rows / BM;
   const int unit = blockIdx.x;
   const int s = unit % S, rt = (unit / S) % RT, g = unit / (S * RT);
@@ -286,26 +298,27 @@ __global__ void __launch_bounds__(320, 1) k_umma_int4(UmmaArgs a) {
   }
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  unsigned char* sD = base;                        // DS x (16 KB A + TB)   dequantized stages
-  unsigned char* sP = sD + DS * (TILE_A + TB);     // PS x (4 KB packed + TB)
-  uint64_t* full_p = reinterpret_cast<uint64_t*>(sP + PS * (TILE_Q + TB));
+  unsigned char* sD = base;                   // DS x (16 KB A + TB)    dequantised k-blocks
+  unsigned char* sP = sD + DS * (TILE_A + TB);  // PS x STAGE             packed stages
+  uint64_t* full_p = reinterpret_cast<uint64_t*>(sP + PS * STAGE);
   uint64_t* empty_p = full_p + PS;
   uint64_t* full_d = empty_p + PS;
   uint64_t* empty_d = full_d + DS;
-  uint64_t* accf = empty_d + DS;  // [2]
-  uint64_t* acce = accf + 2;      // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 2);
+  uint64_t* accf = empty_d + DS;  // [NACC]
+  uint64_t* acce = accf + NACC;   // [NACC]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + NACC);
+  constexpr uint32_t TCOLS = BN * NACC <= 32 ? 32 : (BN * NACC <= 64 ? 64 : (BN * NACC <= 128 ? 128 : 256));
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < PS; ++i) {
       mbar_init(&full_p[i], 1);
-      mbar_init(&empty_p[i], 128);
+      mbar_init(&empty_p[i], 256);
     }
     for (int i = 0; i < DS; ++i) {
-      mbar_init(&full_d[i], 128);
+      mbar_init(&full_d[i], 256);
       mbar_init(&empty_d[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NACC; ++i) {
       mbar_init(&accf[i], 1);
       mbar_init(&acce[i], 128);
     }
@@ -313,7 +326,7 @@ __global__ void __launch_bounds__(320, 1) k_umma_int4(UmmaArgs a) {
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
-                 "r"(BN * 2 <= 32 ? 32 : 64));
+                 "r"(TCOLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -321,29 +334,31 @@ __global__ void __launch_bounds__(320, 1) k_umma_int4(UmmaArgs a) {
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int ngr = nk / 2;
+  const int nst = (nk + KBS - 1) / KBS;
 
   if (warp == 0) {
-    if (lane == 0) {  // producer: packed weight tile + token tile per k-block
+    if (lane == 0) {  // producer: KBS packed weight tiles + KBS token tiles per bulk stage
       const unsigned char* wsrc = a.w_base + ((int64_t)a.expert_base + a.group_buf[g]) * a.blob_bytes + a.w_off +
                                   ((int64_t)rt * kb_total + kb0) * TILE_Q;
       const unsigned char* bsrc = a.bimg + ((int64_t)g * kb_total + kb0) * TB;
-      for (int i = 0; i < nk; ++i) {
-        const int st = i % PS, r = i / PS;
+      for (int j = 0; j < nst; ++j) {
+        const int st = j % PS, r = j / PS;
+        const int cnt = min(KBS, nk - j * KBS);
         if (r > 0) mbar_wait(&empty_p[st], (r - 1) & 1);
-        mbar_expect_tx(&full_p[st], TILE_Q + TB);
-        unsigned char* dst = sP + st * (TILE_Q + TB);
-        bulk_g2s(dst, wsrc + (int64_t)i * TILE_Q, TILE_Q, &full_p[st]);
-        bulk_g2s(dst + TILE_Q, bsrc + (int64_t)i * TB, TB, &full_p[st]);
+        mbar_expect_tx(&full_p[st], cnt * (TILE_Q + TB));
+        unsigned char* dst = sP + st * STAGE;
+        bulk_g2s(dst, wsrc + (int64_t)j * KBS * TILE_Q, cnt * TILE_Q, &full_p[st]);
+        bulk_g2s(dst + KBS * TILE_Q, bsrc + (int64_t)j * KBS * TB, cnt * TB, &full_p[st]);
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // MMA issuer: one TMEM accumulator per 128-column scale group (2 buffers)
+    if (lane == 0) {  // MMA issuer: one TMEM accumulator per 128-column scale group (NACC buffers)
       constexpr uint32_t idesc = idesc_bf16(BN);
       for (int i = 0; i < nk; ++i) {
         const int st = i % DS, r = i / DS;
-        const int gi = i >> 1, b = gi & 1;
+        const int gi = i >> 1, b = gi % NACC;
         const bool first = (i & 1) == 0;
-        if (first && gi >= 2) mbar_wait(&acce[b], ((gi >> 1) - 1) & 1);
+        if (first && gi >= NACC) mbar_wait(&acce[b], ((gi / NACC) - 1) & 1);
         mbar_wait(&full_d[st], r & 1);
         tc_fence_after();
         const uint64_t da = sw128_desc(su32(sD + st * (TILE_A + TB)));
@@ -355,26 +370,27 @@ __global__ void __launch_bounds__(320, 1) k_umma_int4(UmmaArgs a) {
         if (!first) umma_commit(&accf[b]);
       }
     }
-  } else if (warp < 6) {  // dequant warps: thread t owns tile row t
+  } else if (warp < 10) {  // dequant warps: threads 2r, 2r+1 own the two halves of tile row r
     const int t = threadIdx.x - 64;
+    const int r = t >> 1, hf = t & 1;
     for (int i = 0; i < nk; ++i) {
-      const int ps = i % PS, pr = i / PS, ds = i % DS, dr = i / DS;
+      const int j = i / KBS, w = i - j * KBS;
+      const int ps = j % PS, pr = j / PS, ds = i % DS, dr = i / DS;
+      const int cnt = min(KBS, nk - j * KBS);
       mbar_wait(&full_p[ps], pr & 1);
       if (dr > 0) mbar_wait(&empty_d[ds], (dr - 1) & 1);
-      const unsigned char* src = sP + ps * (TILE_Q + TB);
-      unsigned char* dst = sD + ds * (TILE_A + TB);
-      const uint4 w0 = *reinterpret_cast<const uint4*>(src + t * 32);
-      const uint4 w1 = *reinterpret_cast<const uint4*>(src + t * 32 + 16);
-      const uint32_t ws[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+      const uint32_t src = su32(sP + ps * STAGE);
+      const uint32_t dst = su32(sD + ds * (TILE_A + TB));
+      const uint4 w0 = lds128(src + w * TILE_Q + r * 32 + hf * 16);
+      const uint32_t ws[4] = {w0.x, w0.y, w0.z, w0.w};
 #pragma unroll
-      for (int wi = 0; wi < 8; ++wi) *reinterpret_cast<uint4*>(dst + sw128_off(t, 8 * wi)) = dequant8(ws[wi]);
-      for (int c = t; c < TB / 16; c += 128)
-        reinterpret_cast<uint4*>(dst + TILE_A)[c] = reinterpret_cast<const uint4*>(src + TILE_Q)[c];
+      for (int wi = 0; wi < 4; ++wi) sts128(dst + sw128_off(r, 8 * (4 * hf + wi)), dequant8(ws[wi]));
+      for (int c = t; c < TB / 16; c += 256) sts128(dst + TILE_A + 16 * c, lds128(src + KBS * TILE_Q + w * TB + 16 * c));
       fence_proxy_async_smem();
       mbar_arrive(&full_d[ds]);
-      mbar_arrive(&empty_p[ps]);
+      if (w == cnt - 1) mbar_arrive(&empty_p[ps]);
     }
-  } else {  // epilogue warps 6..9: per-group scale, fp32 accumulation in registers
+  } else {  // epilogue warps 10..13: per-group scale, fp32 accumulation in registers
     const int q = warp & 3;
     const int row = q * 32 + lane;
     const uint16_t* sc = reinterpret_cast<const uint16_t*>(a.w_base + ((int64_t)a.expert_base + a.group_buf[g]) * a.blob_bytes +
@@ -383,10 +399,18 @@ __global__ void __launch_bounds__(320, 1) k_umma_int4(UmmaArgs a) {
     float acc[BN];
 #pragma unroll
     for (int j = 0; j < BN; ++j) acc[j] = 0.0f;
+    // the per-row scales of 8 groups are fetched together, ahead of their accumulators, so the
+    // drain of one group never waits on a global-memory round trip
+    constexpr int SW = 8;
+    float scw[SW];
     for (int gi = 0; gi < ngr; ++gi) {
-      const int b = gi & 1;
-      const float scale = bf2f(sc[(int64_t)gi * BM]);
-      mbar_wait(&accf[b], (gi >> 1) & 1);
+      if (gi % SW == 0) {
+#pragma unroll
+        for (int u = 0; u < SW; ++u) scw[u] = gi + u < ngr ? bf2f(sc[(int64_t)(gi + u) * BM]) : 0.0f;
+      }
+      const int b = gi % NACC;
+      const float scale = scw[gi % SW];
+      mbar_wait(&accf[b], (gi / NACC) & 1);
       tc_fence_after();
       float v[BN];
       tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + b * BN, v);
@@ -402,7 +426,7 @@ __global__ void __launch_bounds__(320, 1) k_umma_int4(UmmaArgs a) {
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN * 2 <= 32 ? 32 : 64));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
   }
 }
 
@@ -452,18 +476,22 @@ cudaError_t launch_umma_grouped(const UmmaArgs& a, int max_groups, int BN, cudaS
 }
 
 cudaError_t launch_umma_int4(const UmmaArgs& a, int max_groups, int BN, cudaStream_t st) {
-  constexpr int PS = 6, DS = 3;
+  // 2 k-blocks per bulk stage x 6 stages (72 KB of packed weights in flight per CTA), 2
+  // dequantised slots, 4 TMEM accumulators (one per in-flight 128-column scale group), 8
+  // dequant warps: ~108 KB smem and <= 72 registers -> 2 CTAs/SM
+  constexpr int KBS = 2, PS = 6, DS = 2, NACC = 4;
   const int units = max_groups * (a.rows / BM) * a.splits;
   if (units == 0) return cudaSuccess;
   auto smem = [&](int bn) {
-    return (size_t)1024 + DS * (TILE_A + bn * 128) + PS * (BM * BK / 2 + bn * 128) + (2 * PS + 2 * DS + 4) * 8 + 16;
+    return (size_t)1024 + DS * (TILE_A + bn * 128) + PS * KBS * (BM * BK / 2 + bn * 128) +
+           (2 * PS + 2 * DS + 2 * NACC) * 8 + 16;
   };
   if (BN == 16) {
-    cudaFuncSetAttribute(k_umma_int4<16, PS, DS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(16));
-    k_umma_int4<16, PS, DS><<<units, 320, smem(16), st>>>(a);
+    cudaFuncSetAttribute(k_umma_int4<16, KBS, PS, DS, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(16));
+    k_umma_int4<16, KBS, PS, DS, NACC><<<units, 448, smem(16), st>>>(a);
   } else {
-    cudaFuncSetAttribute(k_umma_int4<32, PS, DS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(32));
-    k_umma_int4<32, PS, DS><<<units, 320, smem(32), st>>>(a);
+    cudaFuncSetAttribute(k_umma_int4<32, KBS, PS, DS, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(32));
+    k_umma_int4<32, KBS, PS, DS, NACC><<<units, 448, smem(32), st>>>(a);
   }
   return cudaGetLastError();
 }
