@@ -287,11 +287,11 @@ def main():
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": dev_max / a.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (random-init weights from a counter hash, random prompts)",
-        "config": {"workload": f"{a.model}-shaped decode, {a.tokens} tokens/step, per-layer cap {cap}/{E}, "
-                               f"policy {a.policy}, k={a.k}, INT4 draft",
-                   "model": a.model, "L": L, "E": E, "top_k": K, "d": cfgm.d, "ffn": cfgm.f, "vocab": cfgm.V,
+        "config": {"workload": f"{a.model}-shaped speculative decode (BASELINE config 3), {a.tokens} tokens/step, "
+                               f"per-layer expert cache {cap}/{E}, policy {a.policy}, k={a.k}, INT4 draft, bf16 verify",
+                   "shape": {"name": a.model, "L": L, "E": E, "top_k": K, "d": cfgm.d, "ffn": cfgm.f, "vocab": cfgm.V},
                    "cache_capacity_per_layer": cap, "host_store_GB": info["host_store_bytes"] / 1e9,
-                   "l2_note": "inputs larger than L2: every verify streams >=157 MB experts per layer"},
+                   "l2": "inputs larger than L2: each verify layer streams >= 157 MB of experts; no flush needed"},
         "exposed_h2d_ms_per_token": stall / max(tok, 1) * 1e3,
         "exposed_h2d_frac": stall / dev_t if dev_t else None,
         "mean_k": mean_k, "accept_rate": acc,

@@ -46,6 +46,7 @@ _SIGS = [
     ("mspq_tile_bf16", c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p]),
     ("mspq_moe_int4_tc", c_int, [c_void_p] * 8 + [c_ll] + [c_int] * 9 + [c_void_p] * 3),
     ("mspq_tile_int4", c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p]),
+    ("mspq_debug_timeline", c_int, [c_void_p, c_int]),
     ("mspq_lm_head", c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p]),
     ("mspq_argmax", c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p]),
     ("mspq_argmax_advance", c_int, [c_void_p, c_int] + [c_void_p] * 6),

@@ -1,4 +1,5 @@
 // extern "C" kernel entry points of libmspq.so (include/mspq_capi.h, part 1 + K4).
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -174,6 +175,7 @@ int mspq_tile_int4(const void* q, const void* s, int rows, int cols, void* tq, v
   CK(launch_tile_int4((const uint32_t*)q, (const uint16_t*)s, rows, cols, (uint32_t*)tq, (uint16_t*)ts, ST(stream)),
      "tile_int4");
 }
+int mspq_debug_timeline(long long* dst, int n) { CK(debug_int4_timeline(dst, n), "debug_timeline"); }
 int mspq_tile_bf16(const void* src, int rows, int cols, void* dst, void* stream) {
   if (rows % 128 || cols % 64) return set_error(MSPQ_ERR_SHAPE_MISMATCH, "tile_bf16: rows%128, cols%64");
   CK(launch_tile_bf16((const uint16_t*)src, rows, cols, (unsigned char*)dst, ST(stream)), "tile_bf16");
@@ -253,7 +255,16 @@ int mspq_cache_create(int L, int E, int K, int kmax, int nbuf, int log_cap, mspq
   memset(c->hblk, 0, hbytes);
   void* dptr = nullptr;
   cudaHostGetDevicePointer(&dptr, c->hblk, 0);
-  cudaMemset(c->blk, 0, off);
+  // the block is zeroed synchronously: callers drive the cache on their own (possibly
+  // non-blocking) streams, which do not order against the legacy stream
+  e = cudaMemset(c->blk, 0, off);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    cudaFree(c->blk);
+    cudaFreeHost(c->hblk);
+    delete c;
+    return cuda_status(e, "cache_create(zero)");
+  }
   char* b = (char*)c->blk;
   C.cap = (int*)(b + o_cap);
   C.res = (int*)(b + o_res);
@@ -277,7 +288,7 @@ int mspq_cache_create(int L, int E, int K, int kmax, int nbuf, int log_cap, mspq
   C.plan = (int*)(b + o_plan);
   C.cov = (int*)(b + o_cov);
   C.step = (int*)(b + o_step);
-  C.stage = ctl_stage_bytes(C, true) > 0 ? 1 : 0;
+  C.stage = ctl_stage_bytes(C, true) > 0 && !getenv("MSPQ_CTL_NO_STAGING") ? 1 : 0;
   *out = c;
   return MSPQ_OK;
 }

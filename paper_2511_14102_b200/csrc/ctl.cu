@@ -134,6 +134,7 @@ MSPQ_D int belady_victim(const Ctx& x, int now, int visible, int layer) {
 // Evicted buffers return to the free stack at once, except a buffer the current verify
 // step's GEMM reads (first-request buffer of this layer), which is parked until the step ends.
 MSPQ_D void erase(const Ctx& x, int key) {
+  if (key < 0) return;  // nothing resident in the scope (capacity 0): nothing to evict
   if (lane_id() == 0) {
     volatile int* res = V(x.C.res);
     int buf = res[key];

@@ -291,6 +291,7 @@ void make_workspaces(mspq_engine* E) {
          o_tcd = take((size_t)mspq_moe_bf16_tc_ws_bytes(d, f, 1, K, K, mspq_engine::kMaxSplit));
   CUDA_OK(cudaMalloc(&E->ws, off));
   CUDA_OK(cudaMemset(E->ws, 0, off));
+  CUDA_OK(cudaDeviceSynchronize());  // the engine's streams are non-blocking w.r.t. the legacy stream
   char* b = (char*)E->ws;
   E->h = (float*)(b + o_h);
   E->xn = (uint16_t*)(b + o_xn);
@@ -466,7 +467,7 @@ static void configure(mspq_engine* E, const std::string& text) {
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     int32_t init[3] = {0, 0, 0};
-    CUDA_OK(cudaMemcpy(E->dst, init, sizeof(init), cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpyAsync(E->dst, init, sizeof(init), cudaMemcpyHostToDevice, E->sc));
     for (int i = 0; i < 2; ++i) CUDA_OK(cudaGraphLaunch(E->gexec, E->sc));
     int32_t z[3] = {0, 0, 0};
     CUDA_OK(cudaMemcpyAsync(E->dst, z, sizeof(z), cudaMemcpyHostToDevice, E->sc));

@@ -39,6 +39,25 @@ MSPQ_D bool mbar_try(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// try_wait with a suspend-time hint: the waiting warp sleeps until the phase completes (or
+// ~1 ms passes) instead of spinning and stealing issue slots from the working warps
+MSPQ_D bool mbar_try_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(su32(bar)), "r"(parity), "r"(1000000u)
+      : "memory");
+  return ok != 0;
+}
+MSPQ_D void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  if (mbar_try_sleep(bar, parity)) return;
+  const long long t0 = clock64();
+  while (!mbar_try_sleep(bar, parity))
+    if (clock64() - t0 > 4000000000LL) __trap();
+}
 // bounded wait: a lost arrival traps (error) instead of hanging the GPU
 MSPQ_D void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try(bar, parity)) return;
@@ -274,6 +293,12 @@ MSPQ_D uint4 lds128(uint32_t addr) {
   return v;
 }
 
+// Per-role cycle stamps of the first CTA (diagnostics, read with mspq_debug_timeline).
+__device__ long long g_int4_tl[2048];
+MSPQ_D void tl_mark(int slot) {
+  if (blockIdx.x == 0 && slot < 2048) g_int4_tl[slot] = clock64();
+}
+
 // warps: 0 producer, 1 MMA, 2..9 dequant (256 threads, two per tile row), 10..13 epilogue
 template <int BN, int KBS, int PS, int DS, int NACC>
 __global__ void __launch_bounds__(448, 2) k_umma_int4(UmmaArgs a) {
@@ -341,10 +366,12 @@ __global__ void __launch_bounds__(448, 2) k_umma_int4(UmmaArgs a) {
       const unsigned char* wsrc = a.w_base + ((int64_t)a.expert_base + a.group_buf[g]) * a.blob_bytes + a.w_off +
                                   ((int64_t)rt * kb_total + kb0) * TILE_Q;
       const unsigned char* bsrc = a.bimg + ((int64_t)g * kb_total + kb0) * TB;
+      tl_mark(0);
       for (int j = 0; j < nst; ++j) {
         const int st = j % PS, r = j / PS;
         const int cnt = min(KBS, nk - j * KBS);
         if (r > 0) mbar_wait(&empty_p[st], (r - 1) & 1);
+        tl_mark(1 + j);
         mbar_expect_tx(&full_p[st], cnt * (TILE_Q + TB));
         unsigned char* dst = sP + st * STAGE;
         bulk_g2s(dst, wsrc + (int64_t)j * KBS * TILE_Q, cnt * TILE_Q, &full_p[st]);
@@ -360,6 +387,7 @@ __global__ void __launch_bounds__(448, 2) k_umma_int4(UmmaArgs a) {
         const bool first = (i & 1) == 0;
         if (first && gi >= NACC) mbar_wait(&acce[b], ((gi / NACC) - 1) & 1);
         mbar_wait(&full_d[st], r & 1);
+        tl_mark(768 + i);
         tc_fence_after();
         const uint64_t da = sw128_desc(su32(sD + st * (TILE_A + TB)));
         const uint64_t db = sw128_desc(su32(sD + st * (TILE_A + TB) + TILE_A));
@@ -377,8 +405,10 @@ __global__ void __launch_bounds__(448, 2) k_umma_int4(UmmaArgs a) {
       const int j = i / KBS, w = i - j * KBS;
       const int ps = j % PS, pr = j / PS, ds = i % DS, dr = i / DS;
       const int cnt = min(KBS, nk - j * KBS);
-      mbar_wait(&full_p[ps], pr & 1);
-      if (dr > 0) mbar_wait(&empty_d[ds], (dr - 1) & 1);
+      mbar_wait_sleep(&full_p[ps], pr & 1);
+      if (t == 0) tl_mark(256 + i);
+      if (dr > 0) mbar_wait_sleep(&empty_d[ds], (dr - 1) & 1);
+      if (t == 0) tl_mark(1024 + i);
       const uint32_t src = su32(sP + ps * STAGE);
       const uint32_t dst = su32(sD + ds * (TILE_A + TB));
       const uint4 w0 = lds128(src + w * TILE_Q + r * 32 + hf * 16);
@@ -388,6 +418,7 @@ __global__ void __launch_bounds__(448, 2) k_umma_int4(UmmaArgs a) {
       for (int c = t; c < TB / 16; c += 256) sts128(dst + TILE_A + 16 * c, lds128(src + KBS * TILE_Q + w * TB + 16 * c));
       fence_proxy_async_smem();
       mbar_arrive(&full_d[ds]);
+      if (t == 0) tl_mark(512 + i);
       if (w == cnt - 1) mbar_arrive(&empty_p[ps]);
     }
   } else {  // epilogue warps 10..13: per-group scale, fp32 accumulation in registers
@@ -410,7 +441,8 @@ __global__ void __launch_bounds__(448, 2) k_umma_int4(UmmaArgs a) {
       }
       const int b = gi % NACC;
       const float scale = scw[gi % SW];
-      mbar_wait(&accf[b], (gi / NACC) & 1);
+      mbar_wait_sleep(&accf[b], (gi / NACC) & 1);
+      if (threadIdx.x == 320) tl_mark(1280 + gi);
       tc_fence_after();
       float v[BN];
       tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + b * BN, v);
@@ -494,6 +526,10 @@ cudaError_t launch_umma_int4(const UmmaArgs& a, int max_groups, int BN, cudaStre
     k_umma_int4<32, KBS, PS, DS, NACC><<<units, 448, smem(32), st>>>(a);
   }
   return cudaGetLastError();
+}
+
+cudaError_t debug_int4_timeline(long long* dst, int n) {
+  return cudaMemcpyFromSymbol(dst, g_int4_tl, sizeof(long long) * std::min(n, 2048));
 }
 
 cudaError_t launch_tile_int4(const uint32_t* q, const uint16_t* s, int rows, int cols, uint32_t* tq, uint16_t* ts,
