@@ -80,6 +80,8 @@ typedef struct mspq_engine_opts {
   int slot_extra;               /* extra HBM buffers beyond the cache budget (0 = auto) */
   int log_cap;                  /* per-cycle event log capacity (0 = auto) */
   int trace_level;              /* 0 = counts only, 1 = per-cycle tokens/routing, 2 = + event log */
+  int expert_codec;             /* host-store format of the bf16 experts: 0 = raw tile images,
+                                   1 = XC lossless blobs (mspq_xc_encode), decoded on the GPU */
 } mspq_engine_opts;
 
 typedef struct mspq_engine mspq_engine;
@@ -163,6 +165,18 @@ int mspq_argmax_advance(const float* logits, int V, int32_t* out, int32_t* row,
                         int32_t* draft_toks, int32_t* cur_tok, int32_t* cur_pos, void* stream);
 int mspq_accept_advance(const int32_t* draft, const int32_t* target_argmax, int k, int32_t* res,
                         int32_t* cur_tok, int32_t* cur_pos, int head_pos, void* stream);
+/* Lossless expert codec (csrc/xcodec.cu): bf16 16 KB tile images <-> one blob of
+ * raw sign/mantissa bytes + per-tile Huffman-coded exponents.  The host store keeps experts in
+ * this form so the PCIe copy engines move ~2/3 of the bf16 bytes; decode restores the exact
+ * images in the HBM slot.  encode blocks on the stream (it builds the code on the host);
+ * tiles/scratch/out must be 256-byte aligned device buffers. */
+long long mspq_xc_max_blob_bytes(long long n_tiles);
+long long mspq_xc_scratch_bytes(long long n_tiles);
+int mspq_xc_encode(const void* tiles, long long n_tiles, void* scratch, void* out, long long out_cap,
+                   long long* out_bytes, void* stream);
+/* decode tiles [tile0, tile1) of a device blob into dst (tile t -> dst + 16 KB * t); n_ctas <= 0
+ * picks the default grid (32 CTAs of 8 warps) */
+int mspq_xc_decode(const void* blob, int tile0, int tile1, void* dst, int n_ctas, void* stream);
 long long mspq_int4_blob_bytes(int d, int f);
 long long mspq_bf16_blob_bytes(int d, int f);
 
@@ -234,7 +248,8 @@ int mspq_generate(mspq_engine* eng, const int32_t* prompt, int n_prompt, int max
                   char** report_json);
 int mspq_engine_info(mspq_engine* eng, char** json);
 /* copy a device tensor of the engine out (tests): name in {"embed","pos","lm","router:<l>",
- * "gamma:<l>","gamma:final","draft:<l>:<e>","expert:<l>:<e>"} */
+ * "gamma:<l>","gamma:final","draft:<l>:<e>","expert:<l>:<e>" (bf16 tile images, decoded if the
+ * store is coded), "expert_blob:<l>:<e>" (the stored bytes as they cross PCIe)} */
 int mspq_engine_read(mspq_engine* eng, const char* name, void* host_dst, long long bytes);
 
 #ifdef __cplusplus

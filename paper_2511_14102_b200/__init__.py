@@ -107,12 +107,15 @@ class Engine:
 
     def __init__(self, model: ModelConfig, kmax: int = 16, device: int = 0,
                  host_store_path: str | None = None, host_store_role: int = 0,
-                 slot_extra: int = 0, trace_level: int = 1, log_cap: int = 0):
+                 slot_extra: int = 0, trace_level: int = 1, log_cap: int = 0,
+                 expert_codec: str = "xc"):
         self.model = model
         self._desc = model.desc()
         self._path = (host_store_path or "").encode()
+        if expert_codec not in ("none", "xc"):
+            raise ValueError("expert_codec must be 'none' or 'xc'")
         self._opts = _lib.EngineOpts(device, kmax, self._path, host_store_role, slot_extra,
-                                     log_cap, trace_level)
+                                     log_cap, trace_level, 1 if expert_codec == "xc" else 0)
         self._h = ctypes.c_void_p()
         check(lib().mspq_engine_create(ctypes.byref(self._desc), ctypes.byref(self._opts),
                                        ctypes.byref(self._h)))

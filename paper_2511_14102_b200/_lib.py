@@ -24,7 +24,7 @@ class ModelDesc(ctypes.Structure):
 class EngineOpts(ctypes.Structure):
     _fields_ = [("device", c_int), ("kmax", c_int), ("host_store_path", c_char_p),
                 ("host_store_role", c_int), ("slot_extra", c_int), ("log_cap", c_int),
-                ("trace_level", c_int)]
+                ("trace_level", c_int), ("expert_codec", c_int)]
 
 
 # (name, restype, argtypes)
@@ -52,6 +52,10 @@ _SIGS = [
     ("mspq_argmax_advance", c_int, [c_void_p, c_int] + [c_void_p] * 6),
     ("mspq_accept_scan", c_int, [c_void_p, c_void_p, c_int, c_void_p, c_void_p]),
     ("mspq_accept_advance", c_int, [c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_int, c_void_p]),
+    ("mspq_xc_max_blob_bytes", c_ll, [c_ll]),
+    ("mspq_xc_scratch_bytes", c_ll, [c_ll]),
+    ("mspq_xc_encode", c_int, [c_void_p, c_ll, c_void_p, c_void_p, c_ll, ctypes.POINTER(c_ll), c_void_p]),
+    ("mspq_xc_decode", c_int, [c_void_p, c_int, c_int, c_void_p, c_int, c_void_p]),
     ("mspq_int4_blob_bytes", c_ll, [c_int, c_int]),
     ("mspq_bf16_blob_bytes", c_ll, [c_int, c_int]),
     ("mspq_cache_create", c_int, [c_int] * 6 + [c_void_p]),

@@ -87,9 +87,18 @@ struct mspq_engine {
   void* wblk = nullptr;
   uint16_t *embed = nullptr, *pos = nullptr, *lm = nullptr, *gfinal = nullptr, *gamma = nullptr, *router = nullptr;
   unsigned char* draft4 = nullptr;
-  // host store
+  // host store (expert_codec 1: one XC blob per payload in a region of Sreg bytes)
   unsigned char* host = nullptr;
   size_t host_bytes = 0;
+  int codec = 0;
+  int64_t Sreg = 0;        // host bytes reserved per payload (S16 raw; worst-case blob with the codec)
+  int n_tiles = 0;         // 16 KB tile images per bf16 expert
+  uint64_t xc_bytes_total = 0;
+  cudaStream_t sdec = nullptr;        // codec: decode stream (copy chunks land on sx, decode here)
+  unsigned char* stage[2] = {nullptr, nullptr};
+  cudaEvent_t ev_stage[2] = {nullptr, nullptr};
+  char stage_rec[2] = {0, 0};
+  int stage_next = 0;
   int n_payload = 0;
   bool host_is_shm = false;
   // slot pool
@@ -143,6 +152,11 @@ struct mspq_engine {
   int32_t* win_tok() { return dst + 8; }
   int32_t* win_pos() { return dst + 8 + Tmax + 1; }
   int64_t payload(int key) const { return m.unique_experts > 0 ? key % m.unique_experts : key; }
+  const unsigned char* host_blob(int64_t p) const { return host + (size_t)p * Sreg; }
+  // bytes the copy engine moves for payload p (the blob size with the codec)
+  uint64_t wire_bytes(int64_t p) const {
+    return codec ? reinterpret_cast<const uint32_t*>(host_blob(p) + 64)[n_tiles] : (uint64_t)S16;
+  }
 
   cudaEvent_t pool_event() {
     if (ev_pool_next >= ev_pool.size()) {
@@ -188,7 +202,7 @@ void make_weights(mspq_engine* E) {
 }
 
 void alloc_host_store(mspq_engine* E) {
-  E->host_bytes = (size_t)E->n_payload * E->S16;
+  E->host_bytes = (size_t)E->n_payload * E->Sreg;
   if (E->store_path.empty()) {
     CUDA_OK(cudaHostAlloc((void**)&E->host, E->host_bytes, cudaHostAllocPortable));
     return;
@@ -234,6 +248,11 @@ void make_experts(mspq_engine* E) {
   const int64_t q13 = (int64_t)2 * m.f * m.d / 2, s13 = (int64_t)2 * m.f * (m.d / 128) * 2, q2 = (int64_t)m.d * m.f / 2;
   unsigned char* rq;  // row-major quantised staging, tiled into the draft blob below
   CUDA_OK(cudaMalloc(&rq, S4));
+  unsigned char *xscr = nullptr, *xout = nullptr;
+  if (E->codec && fill_host) {
+    CUDA_OK(cudaMalloc(&xscr, (size_t)mspq_xc_scratch_bytes(E->n_tiles)));
+    CUDA_OK(cudaMalloc(&xout, (size_t)E->Sreg));
+  }
   for (int p = 0; p < E->n_payload; ++p) {
     unsigned char* st = stage[p & 1];
     const int cl = p / m.E, ce = p % m.E;
@@ -250,15 +269,26 @@ void make_experts(mspq_engine* E) {
       unsigned char* tl = tiled[p & 1];
       CAPI_OK(mspq_tile_bf16(st, 2 * m.f, m.d, tl, E->sc));
       CAPI_OK(mspq_tile_bf16(st + (size_t)2 * m.f * m.d * 2, m.d, m.f, tl + (size_t)2 * m.f * m.d * 2, E->sc));
-      CUDA_OK(cudaMemcpyAsync(E->host + (size_t)p * S16, tl, S16, cudaMemcpyDeviceToHost, E->sc));
+      if (E->codec) {
+        long long nb = 0;
+        CAPI_OK(mspq_xc_encode(tl, E->n_tiles, xscr, xout, E->Sreg, &nb, E->sc));
+        CUDA_OK(cudaMemcpyAsync(E->host + (size_t)p * E->Sreg, xout, (size_t)nb, cudaMemcpyDeviceToHost, E->sc));
+        CUDA_OK(cudaStreamSynchronize(E->sc));  // xout is reused by the next payload
+      } else {
+        CUDA_OK(cudaMemcpyAsync(E->host + (size_t)p * S16, tl, S16, cudaMemcpyDeviceToHost, E->sc));
+      }
     }
   }
+  if (xscr) cudaFree(xscr);
+  if (xout) cudaFree(xout);
   CUDA_OK(cudaStreamSynchronize(E->sc));
   cudaFree(rq);
   cudaFree(stage[0]);
   cudaFree(stage[1]);
   cudaFree(tiled[0]);
   cudaFree(tiled[1]);
+  if (E->codec)
+    for (int p = 0; p < E->n_payload; ++p) E->xc_bytes_total += E->wire_bytes(p);
   if (E->host_is_shm && E->o.host_store_role == 0) {
     const std::string ready = E->store_path + ".ready";
     int fd = open(ready.c_str(), O_WRONLY | O_CREAT, 0600);
@@ -484,7 +514,8 @@ static void configure(mspq_engine* E, const std::string& text) {
     p.pcie_bandwidth = E->pcie_bw_measured;
     p.pcie_init_latency = 0.0;
     p.pcie_overhead = 10e-6;
-    p.expert_size_bytes = (uint64_t)E->S16;
+    // bytes one fetch puts on the link: the mean XC blob with the codec
+    p.expert_size_bytes = E->codec ? (uint64_t)(E->xc_bytes_total / E->n_payload) : (uint64_t)E->S16;
     p.draft_base = 0.0;
     p.draft_per_token = E->draft_step_s;
     // verify samples from the resident-expert roofline of this model on the measured peaks:
@@ -522,17 +553,45 @@ static int issue_copies(mspq_engine* E, int cycle, CopyBatch& batch, uint64_t& b
       batch.a = E->pool_event();
       CUDA_OK(cudaEventRecord(batch.a, E->sx));
     }
-    if (E->last_cycle[buf] == cycle) CUDA_OK(cudaStreamWaitEvent(E->sx, E->ev_gemm[E->last_layer[buf]], 0));
-    CUDA_OK(cudaMemcpyAsync(E->pool + (size_t)buf * E->S16, E->host + (size_t)E->payload(key) * E->S16, E->S16,
-                            cudaMemcpyHostToDevice, E->sx));
-    CUDA_OK(cudaEventRecord(E->ev_ready[buf], E->sx));
+    const bool reused = E->last_cycle[buf] == cycle;  // the slot's last reader is this cycle's GEMM
+    unsigned char* slot = E->pool + (size_t)buf * E->S16;
+    if (!E->codec) {
+      if (reused) CUDA_OK(cudaStreamWaitEvent(E->sx, E->ev_gemm[E->last_layer[buf]], 0));
+      CUDA_OK(cudaMemcpyAsync(slot, E->host_blob(E->payload(key)), E->S16, cudaMemcpyHostToDevice, E->sx));
+      CUDA_OK(cudaEventRecord(E->ev_ready[buf], E->sx));
+      bytes += (uint64_t)E->S16;
+    } else {
+      // compressed blob -> staging (copy engine, chunked) -> decode kernel -> slot.  Chunk c's
+      // decode starts as soon as its bytes land, so only the last chunk's decode is exposed.
+      const unsigned char* hb = E->host_blob(E->payload(key));
+      const uint32_t* toff = reinterpret_cast<const uint32_t*>(hb + 64);
+      const int sb = E->stage_next;
+      E->stage_next ^= 1;
+      unsigned char* stg = E->stage[sb];
+      if (E->stage_rec[sb]) CUDA_OK(cudaStreamWaitEvent(E->sx, E->ev_stage[sb], 0));
+      if (reused) CUDA_OK(cudaStreamWaitEvent(E->sdec, E->ev_gemm[E->last_layer[buf]], 0));
+      const int nt = E->n_tiles;
+      const int nc = std::max(1, std::min(8, (int)(toff[nt] / (8u << 20))));
+      for (int c = 0; c < nc; ++c) {
+        const int t0 = (int)((int64_t)nt * c / nc), t1 = (int)((int64_t)nt * (c + 1) / nc);
+        const uint32_t b0 = c ? toff[t0] : 0u, b1 = toff[t1];
+        CUDA_OK(cudaMemcpyAsync(stg + b0, hb + b0, b1 - b0, cudaMemcpyHostToDevice, E->sx));
+        cudaEvent_t ev = E->pool_event();
+        CUDA_OK(cudaEventRecord(ev, E->sx));
+        CUDA_OK(cudaStreamWaitEvent(E->sdec, ev, 0));
+        CAPI_OK(mspq_xc_decode(stg, t0, t1, slot, 128, E->sdec));
+      }
+      CUDA_OK(cudaEventRecord(E->ev_stage[sb], E->sdec));
+      E->stage_rec[sb] = 1;
+      CUDA_OK(cudaEventRecord(E->ev_ready[buf], E->sdec));
+      bytes += toff[nt];
+    }
     E->ready_rec[buf] = 1;
-    bytes += (uint64_t)E->S16;
     ++batch.count;
   }
   if (batch.a) {
     batch.b = E->pool_event();
-    CUDA_OK(cudaEventRecord(batch.b, E->sx));
+    CUDA_OK(cudaEventRecord(batch.b, E->codec ? E->sdec : E->sx));
   }
   return n;
 }
@@ -845,6 +904,7 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
   }
   // everything (including trailing prefetches) has landed before we report
   CUDA_OK(cudaStreamSynchronize(E->sx));
+  if (E->sdec) CUDA_OK(cudaStreamSynchronize(E->sdec));
   const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
   json rep;
   const double total_time = cycles.empty() ? 0.0
@@ -861,6 +921,8 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
   rep["cycles"] = cycles;
   rep["tokens"] = committed;
   rep["h2d_bytes"] = h2d_bytes;
+  rep["h2d_bytes_bf16"] = (uint64_t)total_new * (uint64_t)E->S16;
+  rep["expert_codec"] = E->codec ? "xc" : "none";
   rep["wall_s"] = wall;
   rep["profile"] = c.profile.to_json();
   rep["policy"] = policy_name(c.policy);
@@ -923,8 +985,13 @@ void destroy(mspq_engine* E) {
       cudaFreeHost(E->host);
     }
   }
+  for (int i = 0; i < 2; ++i) {
+    if (E->stage[i]) cudaFree(E->stage[i]);
+    if (E->ev_stage[i]) cudaEventDestroy(E->ev_stage[i]);
+  }
   if (E->sc) cudaStreamDestroy(E->sc);
   if (E->sx) cudaStreamDestroy(E->sx);
+  if (E->sdec) cudaStreamDestroy(E->sdec);
   delete E;
 }
 }  // namespace
@@ -951,6 +1018,17 @@ int mspq_engine_create(const mspq_model_desc* md, const mspq_engine_opts* op, ms
       cudaDeviceGetStreamPriorityRange(&lo, &hi);
       CUDA_OK(cudaStreamCreateWithPriority(&E->sx, cudaStreamNonBlocking, hi));
       E->S16 = mspq_bf16_blob_bytes(m.d, m.f);
+      E->codec = op->expert_codec;
+      if (E->codec < 0 || E->codec > 1) fail(MSPQ_ERR_INVALID_CONFIG, "expert_codec must be 0 (none) or 1 (xc)");
+      E->n_tiles = (int)(E->S16 / 16384);
+      E->Sreg = E->codec ? ((mspq_xc_max_blob_bytes(E->n_tiles) + 4095) / 4096) * 4096 : E->S16;
+      if (E->codec) {
+        CUDA_OK(cudaStreamCreateWithPriority(&E->sdec, cudaStreamNonBlocking, hi));
+        for (int i = 0; i < 2; ++i) {
+          CUDA_OK(cudaMalloc(&E->stage[i], (size_t)E->Sreg));
+          CUDA_OK(cudaEventCreateWithFlags(&E->ev_stage[i], cudaEventDisableTiming));
+        }
+      }
       E->S4 = mspq_int4_blob_bytes(m.d, m.f);
       E->Tmax = op->kmax + 1;
       E->n_payload = m.unique_experts > 0 ? std::min(m.unique_experts, m.L * m.E) : m.L * m.E;
@@ -1012,6 +1090,8 @@ int mspq_engine_info(mspq_engine* E, char** out) {
     j["expert_bytes_bf16"] = E->S16;
     j["expert_bytes_int4"] = E->S4;
     j["host_store_bytes"] = E->host_bytes;
+    j["expert_codec"] = E->codec ? "xc" : "none";
+    j["expert_wire_bytes_mean"] = E->codec ? (double)E->xc_bytes_total / E->n_payload : (double)E->S16;
     j["n_payload"] = E->n_payload;
     j["slot_buffers"] = E->nbuf;
     j["slot_pool_bytes"] = (uint64_t)E->nbuf * E->S16;
@@ -1046,8 +1126,31 @@ int mspq_engine_read(mspq_engine* E, const char* name, void* dst, long long byte
     } else if (n.rfind("expert:", 0) == 0) {
       int l, e;
       if (!two(n.substr(7), l, e)) fail(MSPQ_ERR_INVALID_CONFIG, n);
-      src = E->host + (size_t)E->payload(l * m.E + e) * E->S16;
+      const unsigned char* hb = E->host_blob(E->payload(l * m.E + e));
+      if (E->codec) {  // decode the stored blob back into the bf16 tile images
+        if ((size_t)bytes > (size_t)E->S16) fail(MSPQ_ERR_RANGE_OUT_OF_BOUNDS, "read beyond tensor");
+        void *dblob, *dimg;
+        const uint64_t wb = E->wire_bytes(E->payload(l * m.E + e));
+        CUDA_OK(cudaMalloc(&dblob, wb));
+        CUDA_OK(cudaMalloc(&dimg, E->S16));
+        CUDA_OK(cudaMemcpy(dblob, hb, wb, cudaMemcpyHostToDevice));
+        const int st = mspq_xc_decode(dblob, 0, E->n_tiles, dimg, 0, nullptr);
+        cudaError_t ce = cudaDeviceSynchronize();
+        if (ce == cudaSuccess && st == 0) ce = cudaMemcpy(dst, dimg, bytes, cudaMemcpyDeviceToHost);
+        cudaFree(dblob);
+        cudaFree(dimg);
+        if (st) fail(st, mspq_last_error());
+        if (ce != cudaSuccess) fail(MSPQ_ERR_CUDA, cudaGetErrorString(ce));
+        return MSPQ_OK;
+      }
+      src = hb;
       avail = E->S16;
+      from_host = true;
+    } else if (n.rfind("expert_blob:", 0) == 0) {
+      int l, e;
+      if (!two(n.substr(12), l, e)) fail(MSPQ_ERR_INVALID_CONFIG, n);
+      src = E->host_blob(E->payload(l * m.E + e));
+      avail = E->codec ? E->wire_bytes(E->payload(l * m.E + e)) : E->S16;
       from_host = true;
     } else
       fail(MSPQ_ERR_INVALID_CONFIG, "unknown tensor " + n);

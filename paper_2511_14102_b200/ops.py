@@ -165,3 +165,23 @@ def accept_scan(draft, target_argmax):
     res = torch.empty(2, dtype=torch.int32, device=draft.device)
     check(lib().mspq_accept_scan(_p(draft), _p(target_argmax), k, _p(res), _s()))
     return res
+
+
+# ---------------------------------------------------------------- lossless expert codec
+def xc_encode(tiles_i16):
+    """bf16 tile images (int16 view, n_tiles * 8192 values, device) -> uint8 blob (device)."""
+    import ctypes
+    n = tiles_i16.numel() // 8192
+    scratch = torch.empty(lib().mspq_xc_scratch_bytes(n), dtype=torch.uint8, device=tiles_i16.device)
+    out = torch.empty(lib().mspq_xc_max_blob_bytes(n), dtype=torch.uint8, device=tiles_i16.device)
+    nb = ctypes.c_longlong(0)
+    check(lib().mspq_xc_encode(_p(tiles_i16), n, _p(scratch), _p(out), out.numel(), ctypes.byref(nb), _s()))
+    return out[: nb.value].clone()
+
+
+def xc_decode(blob_u8, n_tiles, tile0=0, tile1=None, dst=None, n_ctas=0):
+    tile1 = n_tiles if tile1 is None else tile1
+    if dst is None:
+        dst = torch.zeros(n_tiles * 8192, dtype=torch.int16, device=blob_u8.device)
+    check(lib().mspq_xc_decode(_p(blob_u8), tile0, tile1, _p(dst), n_ctas, _s()))
+    return dst

@@ -95,7 +95,8 @@ def test_live_hit_miss_sequence_all_policies(cuda, policy, mode):
         assert got == w, (policy, mode, c["cycle"])
         tot_fetched += c["new_experts"]
     # every fetched expert moved real bytes over PCIe
-    assert rep["h2d_bytes"] == tot_fetched * cfg.expert_bytes_bf16()
+    assert rep["h2d_bytes_bf16"] == tot_fetched * cfg.expert_bytes_bf16()
+    assert 0 < rep["h2d_bytes"] <= rep["h2d_bytes_bf16"] or tot_fetched == 0
     eng.close()
 
 
@@ -163,3 +164,27 @@ def test_live_trace_replays_through_reference_tools(cuda, ref):
     got = m.run_simulation(text, conf)
     from helpers import diff
     assert diff(got, want) is None
+
+
+def test_expert_codec_is_lossless_end_to_end(cuda):
+    """The XC host store (compressed experts, GPU decode into the slot) changes only the bytes on
+    the link: tokens, routing traces and the hit/miss log equal the raw-store engine's."""
+    import paper_2511_14102_b200 as m
+    cfg = m.ModelConfig.named("tiny")
+    conf = {"policy": "speculative", "cache_capacity": 3, "k": 4}
+    prompt = [7, 100, 3, 250, 11]
+    reps = {}
+    for codec in ["none", "xc"]:
+        eng = m.Engine(cfg, kmax=8, trace_level=2, expert_codec=codec)
+        eng.configure(conf)
+        reps[codec] = eng.generate(prompt, 32)
+        if codec == "xc":
+            assert eng.read("expert_blob:1:2", 64)[:4] == b"XCB1"
+        eng.close()
+    a, b = reps["none"], reps["xc"]
+    assert a["tokens"] == b["tokens"]
+    for ca, cb in zip(a["cycles"], b["cycles"]):
+        for key in ["k", "draft_tokens", "target_argmax", "target", "elb", "log", "new_experts"]:
+            assert ca[key] == cb[key], key
+    assert b["h2d_bytes_bf16"] == a["h2d_bytes"]
+    assert b["total_new_experts"] > 0 and b["h2d_bytes"] < 0.72 * a["h2d_bytes"]
