@@ -148,7 +148,8 @@ int mspq_moe_int4_tc(const int32_t* n_groups, const int32_t* group_expert, const
 /* row-major quantised INT4 (q[rows][cols/8] u32, standard nibble order; s[rows][cols/128] bf16)
  * -> tile-major [rows/128][cols/64][128][8] u32 + [rows/128][cols/128][128] bf16 */
 int mspq_tile_int4(const void* q, const void* s, int rows, int cols, void* tq, void* ts, void* stream);
-/* diagnostics: per-role clock64 stamps of the first CTA of the last K2 launch (2048 slots) */
+/* diagnostics: per-role clock64 stamps (2048 slots) of the first CTA of the first K2 launch after
+ * a call with n < 0 (arms the recorder); n > 0 copies the stamps out */
 int mspq_debug_timeline(long long* dst, int n);
 /* row-major [rows][cols] bf16 -> tile-major [rows/128][cols/64] SW128 images (16 KB each) */
 int mspq_tile_bf16(const void* src, int rows, int cols, void* dst, void* stream);

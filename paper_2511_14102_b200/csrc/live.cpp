@@ -349,10 +349,12 @@ void make_workspaces(mspq_engine* E) {
 }
 
 // One draft step for a single token, captured once as a CUDA graph.
+// K splits for a draft GEMM: the most that still fit ONE wave of K2 CTAs (2 per SM), so no
+// CTA streams its weights in a second, mostly idle wave
 int split_for(int units_per_split1, int kblocks) {
   const int units = std::max(1, units_per_split1);
-  const int sp = (296 + units - 1) / units;
-  return std::max(1, std::min({sp, mspq_engine::kMaxSplit, kblocks}));
+  const int sp = std::max(1, 296 / units);
+  return std::max(1, std::min({sp, mspq_engine::kMaxSplit, std::max(1, kblocks / 2)}));
 }
 
 void enqueue_draft_step(mspq_engine* E, cudaStream_t s) {

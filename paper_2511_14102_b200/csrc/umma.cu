@@ -194,7 +194,9 @@ __global__ void __launch_bounds__(192, 1) k_umma_grouped(UmmaArgs a) {
     float v[BN];
     tmem_ld16(tmem + ((uint32_t)(q * 32) << 16), v);
     if (BN == 32) tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + 16, v + 16);
-    for (int t = 0; t < m && t < BN; ++t) outp[(int64_t)(e0 + t) * a.rows + row] = v[t];
+#pragma unroll
+    for (int t = 0; t < BN; ++t)
+      if (t < m) outp[(int64_t)(e0 + t) * a.rows + row] = v[t];
   }
   tc_fence_before();
   __syncthreads();
@@ -254,12 +256,17 @@ __global__ void k_tile_bf16(const uint16_t* __restrict__ src, int rows, int cols
   }
 }
 
-// ============================================================================ K2 v2 (INT4)
-// The draft's GPTQ-sym INT4 expert GEMM on tcgen05.  Per 128x64 tile the producer bulk-copies
-// the 4 KB packed tile (+ the token tile); four dequant warps expand it to the exact bf16
-// (q - 8) values of the SW128 image (one LOP3 + one HSUB2 per two weights via the 128.0 bf16
-// magic), the MMA warp accumulates each 128-column scale group into one of two TMEM buffers, and
-// four epilogue warps apply that group's per-row scale in fp32 while the next group runs:
+// ============================================================================ K2 v3 (INT4)
+// The draft's GPTQ-sym INT4 expert GEMM on tcgen05 with the DEQUANTISED WEIGHTS IN TMEM.
+// Per 128-column scale group the producer bulk-copies the two 4 KB packed tiles (weight ring)
+// and the two token tiles (token ring); eight dequant warps expand the packed tiles to the exact
+// bf16 (q - 8) values (one LOP3 + one HSUB2 per two weights via the 128.0 bf16 magic) and
+// tcgen05.st them straight into a TMEM A-slot (lane = weight row, column c = K elements 2c,
+// 2c+1) -- no shared-memory round trip for the 16-bit weights, and the weight stage recycles as
+// soon as it has been read.  The MMA warp runs kind::f16 with A from TMEM and the token tile
+// (B) from smem (an A-from-TMEM N=16 MMA costs ~28 SM cycles against ~39 with A from smem,
+// measured: tools/micro/mma_rate.cu), one accumulator per group; four epilogue warps apply the
+// group's per-row scale in fp32 while the next groups run:
 //   y[row] = sum_g s[row][g] * sum_{k in g} (q[row][k] - 8) * x[k]      (exact GPTQ-sym dequant)
 // Tile-major INT4 layout: packed [rows/128][cols/64][128 rows x 8 words]; word w of a row holds
 // columns 8w..8w+7 with column 8w+2i at bits 4i and 8w+2i+1 at bits 16+4i.  Scales
@@ -267,44 +274,75 @@ __global__ void k_tile_bf16(const uint16_t* __restrict__ src, int rows, int cols
 MSPQ_D void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(bar)) : "memory");
 }
-MSPQ_D void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// non-blocking probe of a phase
+MSPQ_D bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(su32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 
-MSPQ_D uint4 dequant8(uint32_t w) {
+MSPQ_D uint32_t dq2(uint32_t w, int i) {
   // (w >> 4i) & 0x000F000F | 0x43004300 = bf16x2(128 + q_lo, 128 + q_hi); minus 136 -> exact q - 8
-  const __nv_bfloat162 off = __floats2bfloat162_rn(136.0f, 136.0f);
-  uint32_t o[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    uint32_t t = ((w >> (4 * i)) & 0x000F000Fu) | 0x43004300u;
-    __nv_bfloat162 v = *reinterpret_cast<__nv_bfloat162*>(&t);
-    v = __hsub2(v, off);
-    o[i] = *reinterpret_cast<uint32_t*>(&v);
-  }
-  return make_uint4(o[0], o[1], o[2], o[3]);
+  uint32_t t = ((w >> (4 * i)) & 0x000F000Fu) | 0x43004300u;
+  __nv_bfloat162 v = *reinterpret_cast<__nv_bfloat162*>(&t);
+  v = __hsub2(v, __floats2bfloat162_rn(136.0f, 136.0f));
+  return *reinterpret_cast<uint32_t*>(&v);
 }
 
-MSPQ_D void sts128(uint32_t addr, uint4 v) {
-  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
-               : "memory");
-}
 MSPQ_D uint4 lds128(uint32_t addr) {
   uint4 v;
   asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
   return v;
 }
 
-// Per-role cycle stamps of the first CTA (diagnostics, read with mspq_debug_timeline).
-__device__ long long g_int4_tl[2048];
-MSPQ_D void tl_mark(int slot) {
-  if (blockIdx.x == 0 && slot < 2048) g_int4_tl[slot] = clock64();
+// 32 consecutive TMEM columns of this warp's 32 lanes <- 32 registers per thread
+MSPQ_D void tmem_st32(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
-// warps: 0 producer, 1 MMA, 2..9 dequant (256 threads, two per tile row), 10..13 epilogue
-template <int BN, int KBS, int PS, int DS, int NACC>
+// kind::f16, A from TMEM: D[128 x N] (+)= A_tmem[128 x 16] . B_smem[N x 16]^T
+MSPQ_D void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(accum)
+      : "memory");
+}
+
+// Per-role cycle stamps of the first CTA of the first K2 launch after mspq_debug_timeline(_, -1)
+// armed it (diagnostics).
+__device__ long long g_int4_tl[2048];
+__device__ int g_int4_tl_arm;
+MSPQ_D void tl_mark(bool on, int slot) {
+  if (on && slot < 2048) g_int4_tl[slot] = clock64();
+}
+
+// warps: 0 producer, 1 TMEM alloc + MMA, 2..9 dequant (lane quarter warp & 3, k-block half
+// (warp - 2) >> 2 of the group), 10..13 epilogue.  PW weight stages (2 packed tiles) recycle
+// when the dequant warps have read them; PT token stages (2 token tiles) when the group's MMA
+// completes.  NA TMEM A-slots (64 columns = one 128-column group each), NACC accumulators.
+template <int BN, int PW, int PT, int NA, int NACC>
 __global__ void __launch_bounds__(448, 2) k_umma_int4(UmmaArgs a) {
-  constexpr int TILE_Q = BM * BK / 2;  // 4 KB packed per 128x64 tile
-  constexpr int TB = BN * 128;         // token tile bytes per k-block
-  constexpr int STAGE = KBS * (TILE_Q + TB);  // one bulk-copy stage = KBS consecutive k-blocks
+  constexpr int TILE_Q = BM * BK / 2;             // 4 KB packed per 128x64 tile
+  constexpr int TB = BN * 128;                    // token tile bytes per k-block
+  constexpr int WST = 2 * TILE_Q, TST = 2 * TB;   // one 128-column scale group
+  constexpr uint32_t ACOL = NACC * BN;            // first A-slot column
+  constexpr uint32_t TCOLS = (ACOL + NA * 64) <= 128 ? 128 : ((ACOL + NA * 64) <= 256 ? 256 : 512);
   const int S = a.splits, RT = a.rows / BM;
   const int unit = blockIdx.x;
   const int s = unit % S, rt = (unit / S) % RT, g = unit / (S * RT);
@@ -321,32 +359,32 @@ __global__ void __launch_bounds__(448, 2) k_umma_int4(UmmaArgs a) {
       outp[(int64_t)(e0 + i / BM) * a.rows + rt * BM + (i % BM)] = 0.0f;
     return;
   }
+  const bool tl = blockIdx.x == 0 && g_int4_tl_arm != 0;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  unsigned char* sD = base;                   // DS x (16 KB A + TB)    dequantised k-blocks
-  unsigned char* sP = sD + DS * (TILE_A + TB);  // PS x STAGE             packed stages
-  uint64_t* full_p = reinterpret_cast<uint64_t*>(sP + PS * STAGE);
-  uint64_t* empty_p = full_p + PS;
-  uint64_t* full_d = empty_p + PS;
-  uint64_t* empty_d = full_d + DS;
-  uint64_t* accf = empty_d + DS;  // [NACC]
-  uint64_t* acce = accf + NACC;   // [NACC]
+  unsigned char* sT = base;             // PT x TST (SW128 token tiles: 1024-aligned)
+  unsigned char* sW = sT + PT * TST;    // PW x WST
+  // ONE tcgen05.commit per group (a commit costs ~190 cycles of the issuing thread, 4x an
+  // N=16 MMA): done[gi % ND] frees the token stage (producer), the A-slot (dequant) and
+  // publishes the accumulator (epilogue).  ND >= PT, NA, NACC keeps every waiter in one phase.
+  constexpr int ND = PT > NA ? (PT > NACC ? PT : NACC) : (NA > NACC ? NA : NACC);
+  uint64_t* full_w = reinterpret_cast<uint64_t*>(sW + PW * WST);
+  uint64_t* empty_w = full_w + PW;
+  uint64_t* full_t = empty_w + PW;
+  uint64_t* full_a = full_t + PT;
+  uint64_t* done = full_a + NA;   // [ND]
+  uint64_t* acce = done + ND;     // [NACC]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + NACC);
-  constexpr uint32_t TCOLS = BN * NACC <= 32 ? 32 : (BN * NACC <= 64 ? 64 : (BN * NACC <= 128 ? 128 : 256));
 
   if (warp == 0 && lane == 0) {
-    for (int i = 0; i < PS; ++i) {
-      mbar_init(&full_p[i], 1);
-      mbar_init(&empty_p[i], 256);
+    for (int i = 0; i < PW; ++i) {
+      mbar_init(&full_w[i], 1);
+      mbar_init(&empty_w[i], 256);
     }
-    for (int i = 0; i < DS; ++i) {
-      mbar_init(&full_d[i], 256);
-      mbar_init(&empty_d[i], 1);
-    }
-    for (int i = 0; i < NACC; ++i) {
-      mbar_init(&accf[i], 1);
-      mbar_init(&acce[i], 128);
-    }
+    for (int i = 0; i < PT; ++i) mbar_init(&full_t[i], 1);
+    for (int i = 0; i < NA; ++i) mbar_init(&full_a[i], 256);
+    for (int i = 0; i < ND; ++i) mbar_init(&done[i], 1);
+    for (int i = 0; i < NACC; ++i) mbar_init(&acce[i], 128);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -359,67 +397,71 @@ __global__ void __launch_bounds__(448, 2) k_umma_int4(UmmaArgs a) {
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int ngr = nk / 2;
-  const int nst = (nk + KBS - 1) / KBS;
 
   if (warp == 0) {
-    if (lane == 0) {  // producer: KBS packed weight tiles + KBS token tiles per bulk stage
+    if (lane == 0) {  // producer: the weight ring runs ahead of the token ring
       const unsigned char* wsrc = a.w_base + ((int64_t)a.expert_base + a.group_buf[g]) * a.blob_bytes + a.w_off +
                                   ((int64_t)rt * kb_total + kb0) * TILE_Q;
       const unsigned char* bsrc = a.bimg + ((int64_t)g * kb_total + kb0) * TB;
-      tl_mark(0);
-      for (int j = 0; j < nst; ++j) {
-        const int st = j % PS, r = j / PS;
-        const int cnt = min(KBS, nk - j * KBS);
-        if (r > 0) mbar_wait(&empty_p[st], (r - 1) & 1);
-        tl_mark(1 + j);
-        mbar_expect_tx(&full_p[st], cnt * (TILE_Q + TB));
-        unsigned char* dst = sP + st * STAGE;
-        bulk_g2s(dst, wsrc + (int64_t)j * KBS * TILE_Q, cnt * TILE_Q, &full_p[st]);
-        bulk_g2s(dst + KBS * TILE_Q, bsrc + (int64_t)j * KBS * TB, cnt * TB, &full_p[st]);
+      tl_mark(tl, 0);
+      int jw = 0, jt = 0;
+      const long long c0 = clock64();
+      while (jw < ngr || jt < ngr) {
+        if (jw < ngr && (jw < PW || mbar_test(&empty_w[jw % PW], ((jw / PW) - 1) & 1))) {
+          tl_mark(tl, 1 + jw);
+          mbar_expect_tx(&full_w[jw % PW], WST);
+          bulk_g2s(sW + (jw % PW) * WST, wsrc + (int64_t)jw * WST, WST, &full_w[jw % PW]);
+          ++jw;
+        }
+        if (jt < ngr && jt < jw && (jt < PT || mbar_test(&done[(jt - PT) % ND], ((jt - PT) / ND) & 1))) {
+          mbar_expect_tx(&full_t[jt % PT], TST);
+          bulk_g2s(sT + (jt % PT) * TST, bsrc + (int64_t)jt * TST, TST, &full_t[jt % PT]);
+          ++jt;
+        }
+        if (clock64() - c0 > 4000000000LL) __trap();
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // MMA issuer: one TMEM accumulator per 128-column scale group (NACC buffers)
+    if (lane == 0) {  // MMA issuer: A from the TMEM slot, B from the token stage
       constexpr uint32_t idesc = idesc_bf16(BN);
-      for (int i = 0; i < nk; ++i) {
-        const int st = i % DS, r = i / DS;
-        const int gi = i >> 1, b = gi % NACC;
-        const bool first = (i & 1) == 0;
-        if (first && gi >= NACC) mbar_wait(&acce[b], ((gi / NACC) - 1) & 1);
-        mbar_wait(&full_d[st], r & 1);
-        tl_mark(768 + i);
+      for (int gi = 0; gi < ngr; ++gi) {
+        const int st = gi % PT, sl = gi % NA, b = gi % NACC;
+        if (gi >= NACC) mbar_wait(&acce[b], ((gi / NACC) - 1) & 1);
+        mbar_wait(&full_t[st], (gi / PT) & 1);
+        mbar_wait(&full_a[sl], (gi / NA) & 1);
+        tl_mark(tl, 768 + gi);
         tc_fence_after();
-        const uint64_t da = sw128_desc(su32(sD + st * (TILE_A + TB)));
-        const uint64_t db = sw128_desc(su32(sD + st * (TILE_A + TB) + TILE_A));
+        const uint32_t sb = su32(sT + st * TST);
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k)
-          umma_bf16(tmem + b * BN, da + 2 * k, db + 2 * k, idesc, !(first && k == 0));
-        umma_commit(&empty_d[st]);
-        if (!first) umma_commit(&accf[b]);
+        for (int kk = 0; kk < 8; ++kk)
+          umma_ts(tmem + b * BN, tmem + ACOL + sl * 64 + kk * 8, sw128_desc(sb + (kk >> 2) * TB) + 2 * (kk & 3),
+                  idesc, kk != 0);
+        umma_commit(&done[gi % ND]);
       }
     }
-  } else if (warp < 10) {  // dequant warps: threads 2r, 2r+1 own the two halves of tile row r
-    const int t = threadIdx.x - 64;
-    const int r = t >> 1, hf = t & 1;
-    for (int i = 0; i < nk; ++i) {
-      const int j = i / KBS, w = i - j * KBS;
-      const int ps = j % PS, pr = j / PS, ds = i % DS, dr = i / DS;
-      const int cnt = min(KBS, nk - j * KBS);
-      mbar_wait_sleep(&full_p[ps], pr & 1);
-      if (t == 0) tl_mark(256 + i);
-      if (dr > 0) mbar_wait_sleep(&empty_d[ds], (dr - 1) & 1);
-      if (t == 0) tl_mark(1024 + i);
-      const uint32_t src = su32(sP + ps * STAGE);
-      const uint32_t dst = su32(sD + ds * (TILE_A + TB));
-      const uint4 w0 = lds128(src + w * TILE_Q + r * 32 + hf * 16);
-      const uint32_t ws[4] = {w0.x, w0.y, w0.z, w0.w};
+  } else if (warp < 10) {  // dequant warps: row q*32 + lane, k-block half h of each group
+    const int q = warp & 3, h = (warp - 2) >> 2;
+    const int r = q * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    for (int gi = 0; gi < ngr; ++gi) {
+      const int st = gi % PW, sl = gi % NA;
+      mbar_wait_sleep(&full_w[st], (gi / PW) & 1);
+      if (threadIdx.x == 64) tl_mark(tl, 256 + gi);
+      const uint32_t src = su32(sW + st * WST + h * TILE_Q + r * 32);
+      const uint4 w0 = lds128(src), w1 = lds128(src + 16);
+      const uint32_t ws[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+      uint32_t v[32];
 #pragma unroll
-      for (int wi = 0; wi < 4; ++wi) sts128(dst + sw128_off(r, 8 * (4 * hf + wi)), dequant8(ws[wi]));
-      for (int c = t; c < TB / 16; c += 256) sts128(dst + TILE_A + 16 * c, lds128(src + KBS * TILE_Q + w * TB + 16 * c));
-      fence_proxy_async_smem();
-      mbar_arrive(&full_d[ds]);
-      if (t == 0) tl_mark(512 + i);
-      if (w == cnt - 1) mbar_arrive(&empty_p[ps]);
+      for (int wi = 0; wi < 8; ++wi)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[wi * 4 + i] = dq2(ws[wi], i);
+      mbar_arrive(&empty_w[st]);  // the packed stage is consumed: the producer may refill it
+      if (gi >= NA) mbar_wait_sleep(&done[(gi - NA) % ND], ((gi - NA) / ND) & 1);
+      tc_fence_after();
+      tmem_st32(tmem + lane_base + ACOL + sl * 64 + h * 32, v);
+      tc_fence_before();
+      mbar_arrive(&full_a[sl]);
+      if (threadIdx.x == 64) tl_mark(tl, 512 + gi);
     }
   } else {  // epilogue warps 10..13: per-group scale, fp32 accumulation in registers
     const int q = warp & 3;
@@ -440,9 +482,12 @@ __global__ void __launch_bounds__(448, 2) k_umma_int4(UmmaArgs a) {
         for (int u = 0; u < SW; ++u) scw[u] = gi + u < ngr ? bf2f(sc[(int64_t)(gi + u) * BM]) : 0.0f;
       }
       const int b = gi % NACC;
-      const float scale = scw[gi % SW];
-      mbar_wait_sleep(&accf[b], (gi / NACC) & 1);
-      if (threadIdx.x == 320) tl_mark(1280 + gi);
+      float scale = scw[0];
+#pragma unroll
+      for (int u = 1; u < SW; ++u)
+        if (gi % SW == u) scale = scw[u];
+      mbar_wait(&done[gi % ND], (gi / ND) & 1);
+      if (threadIdx.x == 320) tl_mark(tl, 1280 + gi);
       tc_fence_after();
       float v[BN];
       tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + b * BN, v);
@@ -452,7 +497,10 @@ __global__ void __launch_bounds__(448, 2) k_umma_int4(UmmaArgs a) {
 #pragma unroll
       for (int j = 0; j < BN; ++j) acc[j] = fmaf(scale, v[j], acc[j]);
     }
-    for (int j = 0; j < m && j < BN; ++j) outp[(int64_t)(e0 + j) * a.rows + rt * BM + row] = acc[j];
+#pragma unroll
+    for (int j = 0; j < BN; ++j)
+      if (j < m) outp[(int64_t)(e0 + j) * a.rows + rt * BM + row] = acc[j];
+    if (tl && threadIdx.x == 320) g_int4_tl_arm = 0;
   }
   tc_fence_before();
   __syncthreads();
@@ -508,27 +556,28 @@ cudaError_t launch_umma_grouped(const UmmaArgs& a, int max_groups, int BN, cudaS
 }
 
 cudaError_t launch_umma_int4(const UmmaArgs& a, int max_groups, int BN, cudaStream_t st) {
-  // 2 k-blocks per bulk stage x 6 stages (72 KB of packed weights in flight per CTA), 2
-  // dequantised slots, 4 TMEM accumulators (one per in-flight 128-column scale group), 8
-  // dequant warps: ~108 KB smem and <= 72 registers -> 2 CTAs/SM
-  constexpr int KBS = 2, PS = 6, DS = 2, NACC = 4;
+  // weight ring 10 x 8 KB (BN=16) / 8 x 8 KB (BN=32), token ring 4 stages, 3 TMEM A-slots and
+  // 4 / 2 accumulators in 256 TMEM columns: <= 113 KB smem -> 2 CTAs/SM
+  constexpr int PT = 4, NA = 3;
   const int units = max_groups * (a.rows / BM) * a.splits;
   if (units == 0) return cudaSuccess;
-  auto smem = [&](int bn) {
-    return (size_t)1024 + DS * (TILE_A + bn * 128) + PS * KBS * (BM * BK / 2 + bn * 128) +
-           (2 * PS + 2 * DS + 2 * NACC) * 8 + 16;
-  };
+  auto smem = [&](int bn, int pw) { return (size_t)1024 + PT * 2 * bn * 128 + pw * 2 * (BM * BK / 2) + 48 * 8 + 16; };
   if (BN == 16) {
-    cudaFuncSetAttribute(k_umma_int4<16, KBS, PS, DS, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(16));
-    k_umma_int4<16, KBS, PS, DS, NACC><<<units, 448, smem(16), st>>>(a);
+    cudaFuncSetAttribute(k_umma_int4<16, 10, PT, NA, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(16, 10));
+    k_umma_int4<16, 10, PT, NA, 4><<<units, 448, smem(16, 10), st>>>(a);
   } else {
-    cudaFuncSetAttribute(k_umma_int4<32, KBS, PS, DS, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(32));
-    k_umma_int4<32, KBS, PS, DS, NACC><<<units, 448, smem(32), st>>>(a);
+    cudaFuncSetAttribute(k_umma_int4<32, 8, PT, NA, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(32, 8));
+    k_umma_int4<32, 8, PT, NA, 2><<<units, 448, smem(32, 8), st>>>(a);
   }
   return cudaGetLastError();
 }
 
+// n < 0 arms the recorder for the next K2 launch; n > 0 copies the stamps out
 cudaError_t debug_int4_timeline(long long* dst, int n) {
+  if (n < 0) {
+    const int one = 1;
+    return cudaMemcpyToSymbol(g_int4_tl_arm, &one, sizeof(int));
+  }
   return cudaMemcpyFromSymbol(dst, g_int4_tl, sizeof(long long) * std::min(n, 2048));
 }
 

@@ -1,4 +1,5 @@
-"""Run one Phi-shaped K2 (INT4 tcgen05) W13 launch and print the first CTA's per-role timeline."""
+"""Per-role timeline of the first CTA of one Phi-shaped K2 (INT4 tcgen05) W13 launch (engine split
+choice: W13 S=SP1 (default 1), W2 S=SP2 (default 4)), plus the per-call time of the draft FFN."""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -9,17 +10,20 @@ blobs = torch.randint(0, 255, (E * s4,), dtype=torch.uint8, device="cuda")
 ids = torch.tensor([[3, 7]], dtype=torch.int32, device="cuda")
 s = ops.build_schedule(ids, E)
 xn = torch.randint(-3000, 3000, (1, d), dtype=torch.int16, device="cuda")
-for split1 in (1, 2):
-    for _ in range(3):
-        ops.moe_int4_tc(s, xn, blobs, s4, 0, E, d, f, split1=split1, split2=1)
-    torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record()
-    for _ in range(10):
-        ops.moe_int4_tc(s, xn, blobs, s4, 0, E, d, f, split1=split1, split2=1)
-    ev1.record(); torch.cuda.synchronize()
-    print("split1", split1, "total per call (gather+W13+finalize+W2) us", ev0.elapsed_time(ev1) * 100)
+sp1, sp2 = int(os.environ.get("SP1", 1)), int(os.environ.get("SP2", 4))
+for _ in range(3):
+    ops.moe_int4_tc(s, xn, blobs, s4, 0, E, d, f, split1=sp1, split2=sp2)
+torch.cuda.synchronize()
+ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+ev0.record()
+for _ in range(10):
+    ops.moe_int4_tc(s, xn, blobs, s4, 0, E, d, f, split1=sp1, split2=sp2)
+ev1.record(); torch.cuda.synchronize()
+print(f"split {sp1}/{sp2}: gather+W13+finalize+W2 {ev0.elapsed_time(ev1) * 100:.1f} us per call")
 tl = (ctypes.c_longlong * 2048)()
+_lib.check(_lib.lib().mspq_debug_timeline(tl, -1))
+ops.moe_int4_tc(s, xn, blobs, s4, 0, E, d, f, split1=sp1, split2=sp2)
+torch.cuda.synchronize()
 _lib.check(_lib.lib().mspq_debug_timeline(tl, 2048))
 t = np.array(tl[:2048], dtype=np.int64)
 t0 = t[0]
@@ -27,9 +31,8 @@ def show(name, lo, n):
     v = t[lo:lo + n]
     v = v[v > 0]
     print(name, ((v - t0) / 1965).round(2).tolist()[:40])
-show("producer stage issue (us)", 1, 40)
-show("dequant got data kb", 256, 40)
-show("dequant got slot kb", 1024, 40)
-show("dequant done kb", 512, 40)
-show("mma got kb", 768, 40)
+show("producer weight issue (us)", 1, 40)
+show("dequant got data group", 256, 40)
+show("dequant done group", 512, 40)
+show("mma got group", 768, 40)
 show("epilogue got group", 1280, 40)

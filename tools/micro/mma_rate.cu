@@ -1,0 +1,94 @@
+// Microbenchmark: tcgen05.mma issue rate for small N (swap-AB GEMV shapes), A from smem vs
+// TMEM, one accumulator vs alternating accumulators.  One CTA, one elected thread issues
+// `iters` MMAs then commits; cycles measured with clock64 around issue+wait.
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint64_t desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)64 << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__host__ __device__ constexpr uint32_t idesc(int n) { return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24); }
+template <int N, int MODE>  // MODE 0: SS one acc, 1: SS two accs alternating, 2: TS one acc, 3: TS 4 accs, 4: SS + commit per 8
+__global__ void k(long long* out, int iters) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  __shared__ uint64_t bar, bar2;
+  __shared__ uint32_t slot;
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&slot)), "r"(128));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar2)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) ((uint32_t*)sm)[i] = 0;
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  uint32_t tm = slot;
+  if (threadIdx.x == 0) {
+    const uint64_t da = desc(su32(sm)), db = desc(su32(sm + 16384));
+    long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+      uint32_t d = tm + ((MODE == 1) ? (i & 1) * N : (MODE == 3 ? (i & 3) * N : 0));
+      uint32_t acc = i >= 4;
+      if (MODE == 4 && (i & 7) == 7)
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar2)));
+      if (MODE <= 1 || MODE == 4)
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d), "l"(da + 2 * (i & 3)), "l"(db + 2 * (i & 3)), "r"(idesc(N)), "r"(acc));
+      else
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d), "r"(tm + 64 + 8 * (i & 7)), "l"(db + 2 * (i & 3)), "r"(idesc(N)), "r"(acc));
+    }
+    long long t1 = clock64();
+    if (MODE == 4) t1 = 0;
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar)));
+    uint32_t ok = 0;
+    while (!ok) asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(su32(&bar)));
+    long long t2 = clock64();
+    out[2 * blockIdx.x] = t1 - t0;
+    out[2 * blockIdx.x + 1] = t2 - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "r"(128));
+}
+template <int N, int MODE>
+void run(const char* name) {
+  long long* d;
+  cudaMalloc(&d, 16);
+  cudaFuncSetAttribute(k<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 1024);
+  for (int iters : {64, 256, 1024}) {
+    k<N, MODE><<<1, 128, 65536 + 1024>>>(d, iters);
+    long long h[2];
+    cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+    printf("%-10s N=%3d iters=%5d issue %7lld cyc  done %7lld cyc  -> %.1f cyc/mma  (%s)\n", name, N, iters, h[0], h[1],
+           (double)h[1] / iters, cudaGetErrorString(cudaGetLastError()));
+  }
+  cudaFree(d);
+}
+template <int N, int MODE>
+void run_grid(const char* name, int grid) {
+  long long* d;
+  cudaMalloc(&d, 16 * grid);
+  cudaFuncSetAttribute(k<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 1024);
+  k<N, MODE><<<grid, 128, 65536 + 1024>>>(d, 1024);
+  long long* h = new long long[2 * grid];
+  cudaMemcpy(h, d, 16 * grid, cudaMemcpyDeviceToHost);
+  double mx = 0, mn = 1e18;
+  for (int i = 0; i < grid; ++i) { mx = h[2 * i + 1] > mx ? h[2 * i + 1] : mx; mn = h[2 * i + 1] < mn ? h[2 * i + 1] : mn; }
+  printf("%-10s N=%3d grid=%4d per-CTA cyc/mma min %.1f max %.1f (%s)\n", name, N, grid, mn / 1024, mx / 1024, cudaGetErrorString(cudaGetLastError()));
+  delete[] h;
+  cudaFree(d);
+}
+int main() {
+  run<16, 0>("SS 1acc");
+  run<16, 4>("SS commit8");
+  run_grid<16, 0>("SS 1acc", 148);
+  run_grid<16, 0>("SS 1acc", 296);
+  run_grid<16, 0>("SS 1acc", 444);
+  run_grid<16, 2>("TS 1acc", 296);
+  return 0;
+}
