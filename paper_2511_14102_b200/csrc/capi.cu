@@ -149,6 +149,7 @@ int mspq_moe_int4_tc(const int32_t* n_groups, const int32_t* group_expert, const
   if (d % 128 || f % 128 || T > 32 || split1 < 1 || split2 < 1)
     return set_error(MSPQ_ERR_SHAPE_MISMATCH, "moe_int4_tc: d, f % 128, T <= 32, splits >= 1");
   const int BN = tc_bn(T);
+  const int IR = (BN == 16 && T <= 8) ? 8 : BN;  // B image rows (8: aliased 8-row token tiles)
   const long long N = (long long)T * K;
   auto al = [](long long b) { return (b + 1023) / 1024 * 1024; };
   unsigned char* b1 = (unsigned char*)ws;
@@ -158,16 +159,16 @@ int mspq_moe_int4_tc(const int32_t* n_groups, const int32_t* group_expert, const
               (int32_t*)entry_tok, nullptr, (int32_t*)entry_group};
   cudaStream_t st = ST(stream);
   const long long q13 = (long long)2 * f * d / 2, s13 = (long long)2 * f * (d / 128) * 2, q2 = (long long)d * f / 2;
-  cudaError_t e = launch_gather_b((const uint16_t*)xn, d, s, max_groups, d, BN, b1, st);
+  cudaError_t e = launch_gather_b((const uint16_t*)xn, d, s, max_groups, d, IR, b1, st);
   if (e != cudaSuccess) return cuda_status(e, "gather_b");
   UmmaArgs u1{(const unsigned char*)blobs, blob_bytes, 0, 2 * f, d, n_groups, group_buf, group_off, b1, p1,
-              N * 2 * f, split1, q13, layer * E};
+              N * 2 * f, split1, q13, layer * E, IR};
   e = launch_umma_int4(u1, max_groups, BN, st);
   if (e != cudaSuccess) return cuda_status(e, "umma_int4 W13");
-  e = launch_finalize_act(p1, split1, N * 2 * f, s, entry_group, (int)N, f, BN, b2, st);
+  e = launch_finalize_act(p1, split1, N * 2 * f, s, entry_group, (int)N, f, IR, b2, st);
   if (e != cudaSuccess) return cuda_status(e, "finalize_act");
   UmmaArgs u2{(const unsigned char*)blobs, blob_bytes, q13 + s13, d, f, n_groups, group_buf, group_off, b2, y,
-              N * d, split2, q13 + s13 + q2, layer * E};
+              N * d, split2, q13 + s13 + q2, layer * E, IR};
   CK(launch_umma_int4(u2, max_groups, BN, st), "umma_int4 W2");
 }
 int mspq_tile_int4(const void* q, const void* s, int rows, int cols, void* tq, void* ts, void* stream) {

@@ -33,6 +33,7 @@ struct UmmaArgs {
   int splits;
   int64_t s_off;                // INT4: byte offset of the matrix's scales inside a blob
   int expert_base;              // INT4: blob index = expert_base + group_buf[g]
+  int brows = 0;                // rows per B image (8 = aliased 8-row tiles, else BN)
 };
 
 struct ExpertArgs {

@@ -333,14 +333,20 @@ MSPQ_D void tl_mark(bool on, int slot) {
 }
 
 // warps: 0 producer, 1 TMEM alloc + MMA, 2..9 dequant (lane quarter warp & 3, k-block half
-// (warp - 2) >> 2 of the group), 10..13 epilogue.  PW weight stages (2 packed tiles) recycle
-// when the dequant warps have read them; PT token stages (2 token tiles) when the group's MMA
-// completes.  NA TMEM A-slots (64 columns = one 128-column group each), NACC accumulators.
-template <int BN, int PW, int PT, int NA, int NACC>
+// (warp - 2) >> 2 of the group), 10..13 epilogue.
+// A bulk copy costs its issuing thread ~0.3 us however small it is (tools/micro/bulk_rate.cu:
+// 14 / 29 / 48 GB/s per thread at 4 / 8 / 16 KB), so every copy moves TWO 128-column groups:
+// PW weight stages of 16 KB (4 packed tiles) recycle when the dequant warps have read them, PT
+// token stages (4 token tiles) when the stage's last MMA completes.  With BROWS = 8 (<= 8
+// tokens, N = 16) a token tile holds 8 rows (1 KB) and the descriptor's 8-row-group stride is 0:
+// the MMA's rows 8..15 alias rows 0..7, whose results the epilogue never stores.  NA TMEM
+// A-slots (64 columns = one group each), NACC TMEM accumulators.
+template <int BN, int BROWS, int PW, int PT, int NA, int NACC>
 __global__ void __launch_bounds__(448, 2) k_umma_int4(UmmaArgs a) {
   constexpr int TILE_Q = BM * BK / 2;             // 4 KB packed per 128x64 tile
-  constexpr int TB = BN * 128;                    // token tile bytes per k-block
-  constexpr int WST = 2 * TILE_Q, TST = 2 * TB;   // one 128-column scale group
+  constexpr int TB = BROWS * 128;                 // token tile bytes per k-block
+  constexpr int GS = 2;                           // groups per stage
+  constexpr int WST = GS * 2 * TILE_Q, TST = GS * 2 * TB;
   constexpr uint32_t ACOL = NACC * BN;            // first A-slot column
   constexpr uint32_t TCOLS = (ACOL + NA * 64) <= 128 ? 128 : ((ACOL + NA * 64) <= 256 ? 256 : 512);
   const int S = a.splits, RT = a.rows / BM;
@@ -366,8 +372,9 @@ __global__ void __launch_bounds__(448, 2) k_umma_int4(UmmaArgs a) {
   unsigned char* sW = sT + PT * TST;    // PW x WST
   // ONE tcgen05.commit per group (a commit costs ~190 cycles of the issuing thread, 4x an
   // N=16 MMA): done[gi % ND] frees the token stage (producer), the A-slot (dequant) and
-  // publishes the accumulator (epilogue).  ND >= PT, NA, NACC keeps every waiter in one phase.
-  constexpr int ND = PT > NA ? (PT > NACC ? PT : NACC) : (NA > NACC ? NA : NACC);
+  // publishes the accumulator (epilogue).  ND >= GS*PT, NA, NACC keeps every waiter in one phase.
+  constexpr int ND0 = GS * PT > NA ? GS * PT : NA;
+  constexpr int ND = ND0 > NACC ? ND0 : NACC;
   uint64_t* full_w = reinterpret_cast<uint64_t*>(sW + PW * WST);
   uint64_t* empty_w = full_w + PW;
   uint64_t* full_t = empty_w + PW;
@@ -397,6 +404,7 @@ __global__ void __launch_bounds__(448, 2) k_umma_int4(UmmaArgs a) {
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int ngr = nk / 2;
+  const int nst = (ngr + GS - 1) / GS;
 
   if (warp == 0) {
     if (lane == 0) {  // producer: the weight ring runs ahead of the token ring
@@ -406,17 +414,22 @@ __global__ void __launch_bounds__(448, 2) k_umma_int4(UmmaArgs a) {
       tl_mark(tl, 0);
       int jw = 0, jt = 0;
       const long long c0 = clock64();
-      while (jw < ngr || jt < ngr) {
-        if (jw < ngr && (jw < PW || mbar_test(&empty_w[jw % PW], ((jw / PW) - 1) & 1))) {
+      while (jw < nst || jt < nst) {
+        if (jw < nst && (jw < PW || mbar_test(&empty_w[jw % PW], ((jw / PW) - 1) & 1))) {
           tl_mark(tl, 1 + jw);
-          mbar_expect_tx(&full_w[jw % PW], WST);
-          bulk_g2s(sW + (jw % PW) * WST, wsrc + (int64_t)jw * WST, WST, &full_w[jw % PW]);
+          const int cnt = min(GS, ngr - jw * GS);
+          mbar_expect_tx(&full_w[jw % PW], cnt * 2 * TILE_Q);
+          bulk_g2s(sW + (jw % PW) * WST, wsrc + (int64_t)jw * WST, cnt * 2 * TILE_Q, &full_w[jw % PW]);
           ++jw;
         }
-        if (jt < ngr && jt < jw && (jt < PT || mbar_test(&done[(jt - PT) % ND], ((jt - PT) / ND) & 1))) {
-          mbar_expect_tx(&full_t[jt % PT], TST);
-          bulk_g2s(sT + (jt % PT) * TST, bsrc + (int64_t)jt * TST, TST, &full_t[jt % PT]);
-          ++jt;
+        if (jt < nst && jt < jw) {
+          const int gl = min(GS * (jt - PT) + GS - 1, ngr - 1);  // last group of stage jt - PT
+          if (jt < PT || mbar_test(&done[gl % ND], (gl / ND) & 1)) {
+            const int cnt = min(GS, ngr - jt * GS);
+            mbar_expect_tx(&full_t[jt % PT], cnt * 2 * TB);
+            bulk_g2s(sT + (jt % PT) * TST, bsrc + (int64_t)jt * TST, cnt * 2 * TB, &full_t[jt % PT]);
+            ++jt;
+          }
         }
         if (clock64() - c0 > 4000000000LL) __trap();
       }
@@ -424,18 +437,20 @@ __global__ void __launch_bounds__(448, 2) k_umma_int4(UmmaArgs a) {
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer: A from the TMEM slot, B from the token stage
       constexpr uint32_t idesc = idesc_bf16(BN);
+      // SW128 K-major B descriptor; 8-row-group stride 0 in BROWS = 8 mode (rows 8..15 alias 0..7)
+      constexpr uint64_t sbo_fix = BROWS == 8 ? ~((uint64_t)0x3FFF << 32) : ~(uint64_t)0;
       for (int gi = 0; gi < ngr; ++gi) {
-        const int st = gi % PT, sl = gi % NA, b = gi % NACC;
+        const int js = gi / GS, st = js % PT, sl = gi % NA, b = gi % NACC;
         if (gi >= NACC) mbar_wait(&acce[b], ((gi / NACC) - 1) & 1);
-        mbar_wait(&full_t[st], (gi / PT) & 1);
+        mbar_wait(&full_t[st], (js / PT) & 1);
         mbar_wait(&full_a[sl], (gi / NA) & 1);
         tl_mark(tl, 768 + gi);
         tc_fence_after();
-        const uint32_t sb = su32(sT + st * TST);
+        const uint32_t sb = su32(sT + st * TST + (gi % GS) * 2 * TB);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
-          umma_ts(tmem + b * BN, tmem + ACOL + sl * 64 + kk * 8, sw128_desc(sb + (kk >> 2) * TB) + 2 * (kk & 3),
-                  idesc, kk != 0);
+          umma_ts(tmem + b * BN, tmem + ACOL + sl * 64 + kk * 8,
+                  (sw128_desc(sb + (kk >> 2) * TB) & sbo_fix) + 2 * (kk & 3), idesc, kk != 0);
         umma_commit(&done[gi % ND]);
       }
     }
@@ -444,10 +459,10 @@ __global__ void __launch_bounds__(448, 2) k_umma_int4(UmmaArgs a) {
     const int r = q * 32 + lane;
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     for (int gi = 0; gi < ngr; ++gi) {
-      const int st = gi % PW, sl = gi % NA;
-      mbar_wait_sleep(&full_w[st], (gi / PW) & 1);
+      const int js = gi / GS, st = js % PW, sl = gi % NA;
+      mbar_wait_sleep(&full_w[st], (js / PW) & 1);
       if (threadIdx.x == 64) tl_mark(tl, 256 + gi);
-      const uint32_t src = su32(sW + st * WST + h * TILE_Q + r * 32);
+      const uint32_t src = su32(sW + st * WST + ((gi % GS) * 2 + h) * TILE_Q + r * 32);
       const uint4 w0 = lds128(src), w1 = lds128(src + 16);
       const uint32_t ws[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
       uint32_t v[32];
@@ -455,7 +470,7 @@ __global__ void __launch_bounds__(448, 2) k_umma_int4(UmmaArgs a) {
       for (int wi = 0; wi < 8; ++wi)
 #pragma unroll
         for (int i = 0; i < 4; ++i) v[wi * 4 + i] = dq2(ws[wi], i);
-      mbar_arrive(&empty_w[st]);  // the packed stage is consumed: the producer may refill it
+      if (gi % GS == GS - 1 || gi == ngr - 1) mbar_arrive(&empty_w[st]);  // stage consumed: refill it
       if (gi >= NA) mbar_wait_sleep(&done[(gi - NA) % ND], ((gi - NA) / ND) & 1);
       tc_fence_after();
       tmem_st32(tmem + lane_base + ACOL + sl * 64 + h * 32, v);
@@ -556,18 +571,26 @@ cudaError_t launch_umma_grouped(const UmmaArgs& a, int max_groups, int BN, cudaS
 }
 
 cudaError_t launch_umma_int4(const UmmaArgs& a, int max_groups, int BN, cudaStream_t st) {
-  // weight ring 10 x 8 KB (BN=16) / 8 x 8 KB (BN=32), token ring 4 stages, 3 TMEM A-slots and
-  // 4 / 2 accumulators in 256 TMEM columns: <= 113 KB smem -> 2 CTAs/SM
-  constexpr int PT = 4, NA = 3;
+  // 16 KB weight stages (two groups), token stages of two groups, 3 TMEM A-slots and 4 / 2
+  // accumulators in 256 TMEM columns: ~98 KB smem -> 2 CTAs/SM
+  constexpr int NA = 3;
   const int units = max_groups * (a.rows / BM) * a.splits;
   if (units == 0) return cudaSuccess;
-  auto smem = [&](int bn, int pw) { return (size_t)1024 + PT * 2 * bn * 128 + pw * 2 * (BM * BK / 2) + 48 * 8 + 16; };
-  if (BN == 16) {
-    cudaFuncSetAttribute(k_umma_int4<16, 10, PT, NA, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(16, 10));
-    k_umma_int4<16, 10, PT, NA, 4><<<units, 448, smem(16, 10), st>>>(a);
+  auto smem = [&](int brows, int pw, int pt) {
+    return (size_t)1024 + pt * 4 * brows * 128 + pw * 4 * (BM * BK / 2) + 64 * 8 + 16;
+  };
+  if (BN == 16 && a.brows == 8) {
+    auto k = k_umma_int4<16, 8, 5, 4, NA, 4>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(8, 5, 4));
+    k<<<units, 448, smem(8, 5, 4), st>>>(a);
+  } else if (BN == 16) {
+    auto k = k_umma_int4<16, 16, 5, 2, NA, 4>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(16, 5, 2));
+    k<<<units, 448, smem(16, 5, 2), st>>>(a);
   } else {
-    cudaFuncSetAttribute(k_umma_int4<32, 8, PT, NA, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(32, 8));
-    k_umma_int4<32, 8, PT, NA, 2><<<units, 448, smem(32, 8), st>>>(a);
+    auto k = k_umma_int4<32, 32, 4, 2, NA, 2>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(32, 4, 2));
+    k<<<units, 448, smem(32, 4, 2), st>>>(a);
   }
   return cudaGetLastError();
 }

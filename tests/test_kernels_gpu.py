@@ -265,7 +265,7 @@ def test_moe_bf16_tcgen05_within_tolerance(cuda, name, E, K, d, f, T, split1, sp
 
 
 @pytest.mark.parametrize("name,E,K,d,f", SHAPES)
-@pytest.mark.parametrize("T,split1,split2", [(1, 1, 1), (1, 2, 5), (5, 3, 2)])
+@pytest.mark.parametrize("T,split1,split2", [(1, 1, 1), (1, 2, 5), (5, 3, 2), (12, 2, 3), (20, 1, 2)])
 def test_moe_int4_tcgen05_within_tolerance(cuda, name, E, K, d, f, T, split1, split2):
     """K2 v2 (tcgen05, bf16 (q-8) tiles + per-group fp32 scale epilogue) vs the oracle's
     dequantised INT4 FFN."""
