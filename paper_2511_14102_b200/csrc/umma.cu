@@ -328,12 +328,15 @@ MSPQ_D void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc
 // armed it (diagnostics).
 __device__ long long g_int4_tl[2048];
 __device__ int g_int4_tl_arm;
+__device__ int g_k2_ablate;  // diagnostics: 1 = skip MMAs, 2 = skip TMEM stores, 4 = skip dequant math
 MSPQ_D void tl_mark(bool on, int slot) {
   if (on && slot < 2048) g_int4_tl[slot] = clock64();
 }
 
-// warps: 0 producer, 1 TMEM alloc + MMA, 2..9 dequant (lane quarter warp & 3, k-block half
-// (warp - 2) >> 2 of the group), 10..13 epilogue.
+// warps: 0 producer, 1..NI MMA issuers (warp 1 also allocates TMEM; issuer i takes the groups
+// gi = i mod NI: an N=16 MMA costs its issuing THREAD ~56 cycles, but two issuers on one SM
+// overlap (tools/micro/mma_rate.cu), so the per-group issue cost is split), then 8 dequant warps
+// (lane quarter warp & 3, k-block half of the group), then 4 epilogue warps.
 // A bulk copy costs its issuing thread ~0.3 us however small it is (tools/micro/bulk_rate.cu:
 // 14 / 29 / 48 GB/s per thread at 4 / 8 / 16 KB), so every copy moves TWO 128-column groups:
 // PW weight stages of 16 KB (4 packed tiles) recycle when the dequant warps have read them, PT
@@ -341,13 +344,14 @@ MSPQ_D void tl_mark(bool on, int slot) {
 // tokens, N = 16) a token tile holds 8 rows (1 KB) and the descriptor's 8-row-group stride is 0:
 // the MMA's rows 8..15 alias rows 0..7, whose results the epilogue never stores.  NA TMEM
 // A-slots (64 columns = one group each), NACC TMEM accumulators.
-template <int BN, int BROWS, int PW, int PT, int NA, int NACC>
-__global__ void __launch_bounds__(448, 2) k_umma_int4(UmmaArgs a) {
+template <int BN, int BROWS, int PW, int PT, int NA, int NACC, int NI>
+__global__ void __launch_bounds__(32 * (13 + NI), 2) k_umma_int4(UmmaArgs a) {
+  constexpr int W_DQ = 1 + NI, W_EP = W_DQ + 8;  // first dequant / epilogue warp
   constexpr int TILE_Q = BM * BK / 2;             // 4 KB packed per 128x64 tile
   constexpr int TB = BROWS * 128;                 // token tile bytes per k-block
   constexpr int GS = 2;                           // groups per stage
   constexpr int WST = GS * 2 * TILE_Q, TST = GS * 2 * TB;
-  constexpr uint32_t ACOL = NACC * BN;            // first A-slot column
+  constexpr uint32_t ACOL = NI * NACC * BN;       // first A-slot column (issuer i: acc cols i*NACC*BN..)
   constexpr uint32_t TCOLS = (ACOL + NA * 64) <= 128 ? 128 : ((ACOL + NA * 64) <= 256 ? 256 : 512);
   const int S = a.splits, RT = a.rows / BM;
   const int unit = blockIdx.x;
@@ -366,22 +370,30 @@ __global__ void __launch_bounds__(448, 2) k_umma_int4(UmmaArgs a) {
     return;
   }
   const bool tl = blockIdx.x == 0 && g_int4_tl_arm != 0;
+  const int abl = g_k2_ablate;
+  const bool tla = g_int4_tl_arm != 0 && blockIdx.x < 256;  // per-CTA start/end (globaltimer ns)
+  if (tla && threadIdx.x == 0) {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_int4_tl[1536 + 2 * blockIdx.x] = t;
+  }
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   unsigned char* sT = base;             // PT x TST (SW128 token tiles: 1024-aligned)
   unsigned char* sW = sT + PT * TST;    // PW x WST
   // ONE tcgen05.commit per group (a commit costs ~190 cycles of the issuing thread, 4x an
   // N=16 MMA): done[gi % ND] frees the token stage (producer), the A-slot (dequant) and
-  // publishes the accumulator (epilogue).  ND >= GS*PT, NA, NACC keeps every waiter in one phase.
+  // publishes the accumulator (epilogue).  ND >= GS*PT, NA, NI*NACC keeps every waiter in one
+  // phase.
   constexpr int ND0 = GS * PT > NA ? GS * PT : NA;
-  constexpr int ND = ND0 > NACC ? ND0 : NACC;
+  constexpr int ND = ND0 > NI * NACC ? ND0 : NI * NACC;
   uint64_t* full_w = reinterpret_cast<uint64_t*>(sW + PW * WST);
   uint64_t* empty_w = full_w + PW;
   uint64_t* full_t = empty_w + PW;
   uint64_t* full_a = full_t + PT;
   uint64_t* done = full_a + NA;   // [ND]
-  uint64_t* acce = done + ND;     // [NACC]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + NACC);
+  uint64_t* acce = done + ND;     // [NI][NACC]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + NI * NACC);
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < PW; ++i) {
@@ -391,7 +403,7 @@ __global__ void __launch_bounds__(448, 2) k_umma_int4(UmmaArgs a) {
     for (int i = 0; i < PT; ++i) mbar_init(&full_t[i], 1);
     for (int i = 0; i < NA; ++i) mbar_init(&full_a[i], 256);
     for (int i = 0; i < ND; ++i) mbar_init(&done[i], 1);
-    for (int i = 0; i < NACC; ++i) mbar_init(&acce[i], 128);
+    for (int i = 0; i < NI * NACC; ++i) mbar_init(&acce[i], 128);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -415,7 +427,9 @@ __global__ void __launch_bounds__(448, 2) k_umma_int4(UmmaArgs a) {
       int jw = 0, jt = 0;
       const long long c0 = clock64();
       while (jw < nst || jt < nst) {
+        bool prog = false;
         if (jw < nst && (jw < PW || mbar_test(&empty_w[jw % PW], ((jw / PW) - 1) & 1))) {
+          prog = true;
           tl_mark(tl, 1 + jw);
           const int cnt = min(GS, ngr - jw * GS);
           mbar_expect_tx(&full_w[jw % PW], cnt * 2 * TILE_Q);
@@ -429,54 +443,63 @@ __global__ void __launch_bounds__(448, 2) k_umma_int4(UmmaArgs a) {
             mbar_expect_tx(&full_t[jt % PT], cnt * 2 * TB);
             bulk_g2s(sT + (jt % PT) * TST, bsrc + (int64_t)jt * TST, cnt * 2 * TB, &full_t[jt % PT]);
             ++jt;
+            prog = true;
           }
         }
+        if (!prog) __nanosleep(64);  // polling must not steal issue slots from the dequant warps
         if (clock64() - c0 > 4000000000LL) __trap();
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {  // MMA issuer: A from the TMEM slot, B from the token stage
+  } else if (warp < W_DQ) {
+    if (lane == 0) {  // MMA issuer warp - 1: A from the TMEM slot, B from the token stage
+      const int is = warp - 1;
       constexpr uint32_t idesc = idesc_bf16(BN);
       // SW128 K-major B descriptor; 8-row-group stride 0 in BROWS = 8 mode (rows 8..15 alias 0..7)
       constexpr uint64_t sbo_fix = BROWS == 8 ? ~((uint64_t)0x3FFF << 32) : ~(uint64_t)0;
-      for (int gi = 0; gi < ngr; ++gi) {
-        const int js = gi / GS, st = js % PT, sl = gi % NA, b = gi % NACC;
-        if (gi >= NACC) mbar_wait(&acce[b], ((gi / NACC) - 1) & 1);
-        mbar_wait(&full_t[st], (js / PT) & 1);
-        mbar_wait(&full_a[sl], (gi / NA) & 1);
+      for (int gi = is, u = 0; gi < ngr; gi += NI, ++u) {
+        const int js = gi / GS, st = js % PT, sl = gi % NA, b = u % NACC;
+        if (u >= NACC) mbar_wait_sleep(&acce[is * NACC + b], ((u / NACC) - 1) & 1);
+        mbar_wait_sleep(&full_t[st], (js / PT) & 1);
+        mbar_wait_sleep(&full_a[sl], (gi / NA) & 1);
         tl_mark(tl, 768 + gi);
         tc_fence_after();
         const uint32_t sb = su32(sT + st * TST + (gi % GS) * 2 * TB);
+        if (!(abl & 1))
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
-          umma_ts(tmem + b * BN, tmem + ACOL + sl * 64 + kk * 8,
+          umma_ts(tmem + (is * NACC + b) * BN, tmem + ACOL + sl * 64 + kk * 8,
                   (sw128_desc(sb + (kk >> 2) * TB) & sbo_fix) + 2 * (kk & 3), idesc, kk != 0);
         umma_commit(&done[gi % ND]);
       }
     }
-  } else if (warp < 10) {  // dequant warps: row q*32 + lane, k-block half h of each group
-    const int q = warp & 3, h = (warp - 2) >> 2;
+  } else if (warp < W_EP) {  // dequant warps: row q*32 + lane, k-block half h of each group
+    const int q = warp & 3, h = (warp - W_DQ) >> 2;
     const int r = q * 32 + lane;
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     for (int gi = 0; gi < ngr; ++gi) {
       const int js = gi / GS, st = js % PW, sl = gi % NA;
       mbar_wait_sleep(&full_w[st], (js / PW) & 1);
-      if (threadIdx.x == 64) tl_mark(tl, 256 + gi);
+      if (threadIdx.x == 32 * W_DQ) tl_mark(tl, 256 + gi);
       const uint32_t src = su32(sW + st * WST + ((gi % GS) * 2 + h) * TILE_Q + r * 32);
       const uint4 w0 = lds128(src), w1 = lds128(src + 16);
       const uint32_t ws[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
       uint32_t v[32];
+      if (abl & 4) {
 #pragma unroll
-      for (int wi = 0; wi < 8; ++wi)
+        for (int i = 0; i < 32; ++i) v[i] = ws[i & 7];
+      } else {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) v[wi * 4 + i] = dq2(ws[wi], i);
+        for (int wi = 0; wi < 8; ++wi)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) v[wi * 4 + i] = dq2(ws[wi], i);
+      }
       if (gi % GS == GS - 1 || gi == ngr - 1) mbar_arrive(&empty_w[st]);  // stage consumed: refill it
       if (gi >= NA) mbar_wait_sleep(&done[(gi - NA) % ND], ((gi - NA) / ND) & 1);
       tc_fence_after();
-      tmem_st32(tmem + lane_base + ACOL + sl * 64 + h * 32, v);
+      if (!(abl & 2)) tmem_st32(tmem + lane_base + ACOL + sl * 64 + h * 32, v);
       tc_fence_before();
       mbar_arrive(&full_a[sl]);
-      if (threadIdx.x == 64) tl_mark(tl, 512 + gi);
+      if (threadIdx.x == 32 * W_DQ) tl_mark(tl, 512 + gi);
     }
   } else {  // epilogue warps 10..13: per-group scale, fp32 accumulation in registers
     const int q = warp & 3;
@@ -496,26 +519,31 @@ __global__ void __launch_bounds__(448, 2) k_umma_int4(UmmaArgs a) {
 #pragma unroll
         for (int u = 0; u < SW; ++u) scw[u] = gi + u < ngr ? bf2f(sc[(int64_t)(gi + u) * BM]) : 0.0f;
       }
-      const int b = gi % NACC;
+      const int ab = (gi % NI) * NACC + (gi / NI) % NACC;  // issuer gi % NI, its buffer
       float scale = scw[0];
 #pragma unroll
       for (int u = 1; u < SW; ++u)
         if (gi % SW == u) scale = scw[u];
-      mbar_wait(&done[gi % ND], (gi / ND) & 1);
-      if (threadIdx.x == 320) tl_mark(tl, 1280 + gi);
+      mbar_wait_sleep(&done[gi % ND], (gi / ND) & 1);
+      if (threadIdx.x == 32 * W_EP) tl_mark(tl, 1280 + gi);
       tc_fence_after();
       float v[BN];
-      tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + b * BN, v);
-      if (BN == 32) tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + b * BN + 16, v + 16);
+      tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + ab * BN, v);
+      if (BN == 32) tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + ab * BN + 16, v + 16);
       tc_fence_before();
-      mbar_arrive(&acce[b]);
+      mbar_arrive(&acce[ab]);
 #pragma unroll
       for (int j = 0; j < BN; ++j) acc[j] = fmaf(scale, v[j], acc[j]);
     }
 #pragma unroll
     for (int j = 0; j < BN; ++j)
       if (j < m) outp[(int64_t)(e0 + j) * a.rows + rt * BM + row] = acc[j];
-    if (tl && threadIdx.x == 320) g_int4_tl_arm = 0;
+    if (tla && threadIdx.x == 32 * W_EP) {
+      long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      g_int4_tl[1537 + 2 * blockIdx.x] = t;
+    }
+    if (tl && threadIdx.x == 32 * W_EP) g_int4_tl_arm = 0;  // record one launch only
   }
   tc_fence_before();
   __syncthreads();
@@ -571,36 +599,43 @@ cudaError_t launch_umma_grouped(const UmmaArgs& a, int max_groups, int BN, cudaS
 }
 
 cudaError_t launch_umma_int4(const UmmaArgs& a, int max_groups, int BN, cudaStream_t st) {
-  // 16 KB weight stages (two groups), token stages of two groups, 3 TMEM A-slots and 4 / 2
-  // accumulators in 256 TMEM columns: ~98 KB smem -> 2 CTAs/SM
-  constexpr int NA = 3;
+  // 16 KB weight stages (two groups), token stages of two groups, 3 TMEM A-slots, 2 MMA issuers
+  // with 2 accumulators each (BN = 32: 1 each) in 256 TMEM columns: ~98 KB smem -> 2 CTAs/SM
+  constexpr int NA = 3, NI = 2, THREADS = 32 * (13 + NI);
   const int units = max_groups * (a.rows / BM) * a.splits;
   if (units == 0) return cudaSuccess;
   auto smem = [&](int brows, int pw, int pt) {
     return (size_t)1024 + pt * 4 * brows * 128 + pw * 4 * (BM * BK / 2) + 64 * 8 + 16;
   };
   if (BN == 16 && a.brows == 8) {
-    auto k = k_umma_int4<16, 8, 5, 4, NA, 4>;
+    auto k = k_umma_int4<16, 8, 5, 4, NA, 2, NI>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(8, 5, 4));
-    k<<<units, 448, smem(8, 5, 4), st>>>(a);
+    k<<<units, THREADS, smem(8, 5, 4), st>>>(a);
   } else if (BN == 16) {
-    auto k = k_umma_int4<16, 16, 5, 2, NA, 4>;
+    auto k = k_umma_int4<16, 16, 5, 2, NA, 2, NI>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(16, 5, 2));
-    k<<<units, 448, smem(16, 5, 2), st>>>(a);
+    k<<<units, THREADS, smem(16, 5, 2), st>>>(a);
   } else {
-    auto k = k_umma_int4<32, 32, 4, 2, NA, 2>;
+    auto k = k_umma_int4<32, 32, 4, 2, NA, 1, NI>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(32, 4, 2));
-    k<<<units, 448, smem(32, 4, 2), st>>>(a);
+    k<<<units, THREADS, smem(32, 4, 2), st>>>(a);
   }
   return cudaGetLastError();
 }
 
 // n < 0 arms the recorder for the next K2 launch; n > 0 copies the stamps out
 cudaError_t debug_int4_timeline(long long* dst, int n) {
+  if (n <= -100) {  // -100 - mode: K2 ablation mode (diagnostics only; 0 = normal)
+    const int mode = -100 - n;
+    return cudaMemcpyToSymbol(g_k2_ablate, &mode, sizeof(int));
+  }
   if (n < 0) {
     const int one = 1;
     return cudaMemcpyToSymbol(g_int4_tl_arm, &one, sizeof(int));
   }
+  const int zero = 0;
+  cudaError_t e = cudaMemcpyToSymbol(g_int4_tl_arm, &zero, sizeof(int));
+  if (e != cudaSuccess) return e;
   return cudaMemcpyFromSymbol(dst, g_int4_tl, sizeof(long long) * std::min(n, 2048));
 }
 
