@@ -113,14 +113,15 @@ long long mspq_moe_bf16_tc_ws_bytes(int d, int f, int T, int K, int max_groups, 
   const long long BN = tc_bn(T), N = (long long)T * K;
   auto al = [](long long b) { return (b + 1023) / 1024 * 1024; };
   return al(max_groups * (d / 64) * BN * 128) + al((long long)max_split1 * N * 2 * f * 4) +
-         al(max_groups * (f / 64) * BN * 128);
+         al(max_groups * (f / 64) * BN * 128) + al(max_groups * BN * (d / 64) * 4) +
+         al(max_groups * BN * (f / 64) * 4);
 }
 int mspq_moe_bf16_tc(const int32_t* n_groups, const int32_t* group_expert, const int32_t* group_buf,
                      const int32_t* group_off, const int32_t* entry_tok, const int32_t* entry_group,
                      const void* xn, const void* pool, long long blob_bytes, int d, int f, int T, int K,
                      int max_groups, int split1, int split2, void* ws, float* y, void* stream) {
-  if (d % 128 || f % 128 || T > 32 || split1 < 1 || split2 < 1)
-    return set_error(MSPQ_ERR_SHAPE_MISMATCH, "moe_bf16_tc: d, f % 128, T <= 32, splits >= 1");
+  if (d % 128 || f % 256 || T > 32 || split1 < 1 || split2 < 1)
+    return set_error(MSPQ_ERR_SHAPE_MISMATCH, "moe_bf16_tc: d % 128, f % 256, T <= 32, splits >= 1");
   const int BN = tc_bn(T);
   const long long N = (long long)T * K;
   auto al = [](long long b) { return (b + 1023) / 1024 * 1024; };
@@ -146,8 +147,8 @@ int mspq_moe_int4_tc(const int32_t* n_groups, const int32_t* group_expert, const
                      const int32_t* group_off, const int32_t* entry_tok, const int32_t* entry_group,
                      const void* xn, const void* blobs, long long blob_bytes, int layer, int E, int d, int f, int T,
                      int K, int max_groups, int split1, int split2, void* ws, float* y, void* stream) {
-  if (d % 128 || f % 128 || T > 32 || split1 < 1 || split2 < 1)
-    return set_error(MSPQ_ERR_SHAPE_MISMATCH, "moe_int4_tc: d, f % 128, T <= 32, splits >= 1");
+  if (d % 128 || f % 256 || T > 32 || split1 < 1 || split2 < 1)
+    return set_error(MSPQ_ERR_SHAPE_MISMATCH, "moe_int4_tc: d % 128, f % 256, T <= 32, splits >= 1");
   const int BN = tc_bn(T);
   const int IR = (BN == 16 && T <= 8) ? 8 : BN;  // B image rows (8: aliased 8-row token tiles)
   const long long N = (long long)T * K;
@@ -155,20 +156,22 @@ int mspq_moe_int4_tc(const int32_t* n_groups, const int32_t* group_expert, const
   unsigned char* b1 = (unsigned char*)ws;
   float* p1 = (float*)(b1 + al(max_groups * (d / 64) * BN * 128));
   unsigned char* b2 = (unsigned char*)p1 + al((long long)split1 * N * 2 * f * 4);
+  float* c1 = (float*)(b2 + al(max_groups * (f / 64) * BN * 128));  // [G][IR][d/64]
+  float* c2 = c1 + al(max_groups * BN * (d / 64) * 4) / 4;            // [G][IR][f/64]
   SchedPtrs s{(int32_t*)n_groups, (int32_t*)group_expert, (int32_t*)group_buf, (int32_t*)group_off,
               (int32_t*)entry_tok, nullptr, (int32_t*)entry_group};
   cudaStream_t st = ST(stream);
   const long long q13 = (long long)2 * f * d / 2, s13 = (long long)2 * f * (d / 128) * 2, q2 = (long long)d * f / 2;
-  cudaError_t e = launch_gather_b((const uint16_t*)xn, d, s, max_groups, d, IR, b1, st);
+  cudaError_t e = launch_gather_b((const uint16_t*)xn, d, s, max_groups, d, IR, b1, st, c1);
   if (e != cudaSuccess) return cuda_status(e, "gather_b");
   UmmaArgs u1{(const unsigned char*)blobs, blob_bytes, 0, 2 * f, d, n_groups, group_buf, group_off, b1, p1,
-              N * 2 * f, split1, q13, layer * E, IR};
+              N * 2 * f, split1, q13, layer * E, IR, c1};
   e = launch_umma_int4(u1, max_groups, BN, st);
   if (e != cudaSuccess) return cuda_status(e, "umma_int4 W13");
-  e = launch_finalize_act(p1, split1, N * 2 * f, s, entry_group, (int)N, f, IR, b2, st);
+  e = launch_finalize_act(p1, split1, N * 2 * f, s, entry_group, (int)N, f, IR, b2, st, c2);
   if (e != cudaSuccess) return cuda_status(e, "finalize_act");
   UmmaArgs u2{(const unsigned char*)blobs, blob_bytes, q13 + s13, d, f, n_groups, group_buf, group_off, b2, y,
-              N * d, split2, q13 + s13 + q2, layer * E, IR};
+              N * d, split2, q13 + s13 + q2, layer * E, IR, c2};
   CK(launch_umma_int4(u2, max_groups, BN, st), "umma_int4 W2");
 }
 int mspq_tile_int4(const void* q, const void* s, int rows, int cols, void* tq, void* ts, void* stream) {

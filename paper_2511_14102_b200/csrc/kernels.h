@@ -34,6 +34,7 @@ struct UmmaArgs {
   int64_t s_off;                // INT4: byte offset of the matrix's scales inside a blob
   int expert_base;              // INT4: blob index = expert_base + group_buf[g]
   int brows = 0;                // rows per B image (8 = aliased 8-row tiles, else BN)
+  const float* csum = nullptr;  // INT4: [G][brows][kdim/64] epilogue corrections (see k_gather_b)
 };
 
 struct ExpertArgs {
@@ -81,10 +82,10 @@ cudaError_t debug_int4_timeline(long long* dst, int n);
 cudaError_t launch_tile_int4(const uint32_t* q, const uint16_t* s, int rows, int cols, uint32_t* tq, uint16_t* ts,
                              cudaStream_t st);
 cudaError_t launch_gather_b(const uint16_t* x, int ld, SchedPtrs s, int max_groups, int kdim, int BN,
-                            unsigned char* img, cudaStream_t st);
+                            unsigned char* img, cudaStream_t st, float* csum = nullptr);
 cudaError_t launch_finalize_act(const float* p1, int splits, int64_t split_stride, SchedPtrs s,
                                 const int32_t* entry_group, int n_entries, int f, int BN, unsigned char* img,
-                                cudaStream_t st);
+                                cudaStream_t st, float* csum = nullptr);
 cudaError_t launch_tile_bf16(const uint16_t* src, int rows, int cols, unsigned char* dst, cudaStream_t st);
 cudaError_t launch_fill_bf16(uint64_t seed, uint64_t tensor, float scale, int kind, uint16_t* out,
                              int64_t n, int64_t start, cudaStream_t st);

@@ -84,6 +84,10 @@ MSPQ_D uint64_t sw128_desc(uint32_t saddr) {
 __host__ __device__ constexpr uint32_t idesc_bf16(int n) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 }
+// kind::f16 instruction descriptor with fp16 A/B (format 0), D f32, both K-major
+__host__ __device__ constexpr uint32_t idesc_f16(int n) {
+  return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
 MSPQ_D void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accum) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -109,6 +113,16 @@ MSPQ_D void tmem_ld16(uint32_t taddr, float* v) {
 }
 
 // byte offset of element (row, col) inside one SW128 K-major image with 64 columns per row
+MSPQ_D void tmem_ld8(uint32_t taddr, float* v) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 MSPQ_HD int sw128_off(int row, int col) {
   return (row >> 3) * 1024 + (row & 7) * 128 + ((((col >> 3) ^ (row & 7)) & 7) << 4) + (col & 7) * 2;
 }
@@ -206,39 +220,87 @@ __global__ void __launch_bounds__(192, 1) k_umma_grouped(UmmaArgs a) {
   }
 }
 
-// Gather the tokens of every group into the SW128 B images [G][kdim/64][BN x 64] bf16.
+// K2 B operand (F16): the draft GEMM runs kind::f16 on fp16 operands.  A k-block's columns
+// 0..31 are "class 1" (A = 1024 + q), columns 32..63 "class 16" (A = 1024 + 16 q), so the token
+// image holds b = fp16(x) for class 1 and b = fp16(x / 16) for class 16, and
+//   sum_k (q_k - 8) x_k = D - sum_k c_k b_k,   c = 1032 (class 1) | 1152 (class 16)
+// (class 1: (1024 + q) b - 1032 b = (q - 8) b; class 16: (1024 + 16q) b - 1152 b = (q - 8) 16 b).
+// csum[g][row][kb] = sum over the k-block of c_k b_k in fp32, fixed reduction order.
+MSPQ_D uint16_t f2h_bits(float v) {
+  const __half h = __float2half_rn(v);
+  return *reinterpret_cast<const uint16_t*>(&h);
+}
+MSPQ_D float h2f_bits(uint16_t b) { return __half2float(*reinterpret_cast<const __half*>(&b)); }
+
+// Gather the tokens of every group into the SW128 B images [G][kdim/64][BN x 64]: bf16 (K3), or
+// class-scaled fp16 plus csum (K2, F16).
+template <bool F16>
 __global__ void k_gather_b(const uint16_t* __restrict__ x, int ld, SchedPtrs s, int kdim, int BN,
-                           unsigned char* __restrict__ img) {
+                           unsigned char* __restrict__ img, float* __restrict__ csum) {
   const int kb = blockIdx.x, g = blockIdx.y;
   if (g >= *s.n_groups) return;
   const int e0 = s.group_off[g], m = s.group_off[g + 1] - e0;
   const int kbt = kdim / BK;
   unsigned char* dst = img + ((int64_t)g * kbt + kb) * (BN * 128);
-  for (int i = threadIdx.x; i < BN * 8; i += blockDim.x) {
+  for (int i = threadIdx.x; i < BN * 8; i += blockDim.x) {  // blockDim.x is a multiple of 8
     const int r = i >> 3, c = i & 7;
     uint4 v = make_uint4(0, 0, 0, 0);
     if (r < m) v = *reinterpret_cast<const uint4*>(x + (int64_t)s.entry_tok[e0 + r] * ld + kb * BK + c * 8);
+    if (F16) {
+      const float mul = c < 4 ? 1.0f : 0.0625f, cc = c < 4 ? 1032.0f : 1152.0f;
+      uint32_t w[4] = {v.x, v.y, v.z, v.w};
+      float part = 0.0f;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint16_t lo = f2h_bits(bf2f((uint16_t)(w[j] & 0xFFFFu)) * mul);
+        const uint16_t hi = f2h_bits(bf2f((uint16_t)(w[j] >> 16)) * mul);
+        part = fmaf(cc, h2f_bits(lo), part);
+        part = fmaf(cc, h2f_bits(hi), part);
+        w[j] = (uint32_t)lo | ((uint32_t)hi << 16);
+      }
+      v = make_uint4(w[0], w[1], w[2], w[3]);
+      part += __shfl_xor_sync(0xffffffffu, part, 1);
+      part += __shfl_xor_sync(0xffffffffu, part, 2);
+      part += __shfl_xor_sync(0xffffffffu, part, 4);
+      if (c == 0) csum[((int64_t)g * BN + r) * kbt + kb] = part;
+    }
     *reinterpret_cast<uint4*>(dst + sw128_off(r, c * 8)) = v;
   }
 }
 
 // Stage-1 finalize: sum the K-split partials of the interleaved gate/up rows, act = bf16(silu(g)*u),
-// written straight into the stage-2 B images (entry -> its group's row).
+// written straight into the stage-2 B images (entry -> its group's row); F16: class-scaled fp16
+// of the bf16 act plus csum, as in k_gather_b.
+template <bool F16>
 __global__ void k_finalize_act(const float* __restrict__ p1, int splits, int64_t split_stride, SchedPtrs s,
                                const int32_t* __restrict__ entry_group, int n_entries, int f, int BN,
-                               unsigned char* __restrict__ img) {
+                               unsigned char* __restrict__ img, float* __restrict__ csum) {
+  __shared__ float wpart[8];
   const int e = blockIdx.y;
   if (e >= s.group_off[*s.n_groups]) return;
   const int g = entry_group[e], t = e - s.group_off[g];
   const int kbt = f / BK;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < f; i += gridDim.x * blockDim.x) {
+  for (int i0 = blockIdx.x * blockDim.x; i0 < f; i0 += gridDim.x * blockDim.x) {  // f % 256 == 0
+    const int i = i0 + threadIdx.x;
     float gv = 0.0f, uv = 0.0f;
     for (int sp = 0; sp < splits; ++sp) {
       const float* row = p1 + sp * split_stride + (int64_t)e * 2 * f;
       gv = __fadd_rn(gv, row[2 * i]);
       uv = __fadd_rn(uv, row[2 * i + 1]);
     }
-    const uint16_t act = f2bf(__fmul_rn(silu_det(gv), uv));
+    uint16_t act = f2bf(__fmul_rn(silu_det(gv), uv));
+    if (F16) {
+      const bool c1 = (i % BK) < 32;
+      act = f2h_bits(bf2f(act) * (c1 ? 1.0f : 0.0625f));
+      float part = (c1 ? 1032.0f : 1152.0f) * h2f_bits(act);
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      if ((threadIdx.x & 31) == 0) wpart[threadIdx.x >> 5] = part;
+      __syncthreads();
+      if ((threadIdx.x & 63) == 0)
+        csum[((int64_t)g * BN + t) * kbt + i / BK] = wpart[threadIdx.x >> 5] + wpart[(threadIdx.x >> 5) + 1];
+      __syncthreads();
+    }
     *reinterpret_cast<uint16_t*>(img + ((int64_t)g * kbt + i / BK) * (BN * 128) + sw128_off(t, i % BK)) = act;
   }
 }
@@ -256,21 +318,24 @@ __global__ void k_tile_bf16(const uint16_t* __restrict__ src, int rows, int cols
   }
 }
 
-// ============================================================================ K2 v3 (INT4)
-// The draft's GPTQ-sym INT4 expert GEMM on tcgen05 with the DEQUANTISED WEIGHTS IN TMEM.
+// ============================================================================ K2 v6 (INT4)
+// The draft's GPTQ-sym INT4 expert GEMM on tcgen05 with the EXPANDED WEIGHTS IN TMEM.
 // Per 128-column scale group the producer bulk-copies the two 4 KB packed tiles (weight ring)
-// and the two token tiles (token ring); eight dequant warps expand the packed tiles to the exact
-// bf16 (q - 8) values (one LOP3 + one HSUB2 per two weights via the 128.0 bf16 magic) and
-// tcgen05.st them straight into a TMEM A-slot (lane = weight row, column c = K elements 2c,
-// 2c+1) -- no shared-memory round trip for the 16-bit weights, and the weight stage recycles as
-// soon as it has been read.  The MMA warp runs kind::f16 with A from TMEM and the token tile
-// (B) from smem (an A-from-TMEM N=16 MMA costs ~28 SM cycles against ~39 with A from smem,
-// measured: tools/micro/mma_rate.cu), one accumulator per group; four epilogue warps apply the
-// group's per-row scale in fp32 while the next groups run:
-//   y[row] = sum_g s[row][g] * sum_{k in g} (q[row][k] - 8) * x[k]      (exact GPTQ-sym dequant)
-// Tile-major INT4 layout: packed [rows/128][cols/64][128 rows x 8 words]; word w of a row holds
-// columns 8w..8w+7 with column 8w+2i at bits 4i and 8w+2i+1 at bits 16+4i.  Scales
-// [rows/128][cols/128][128] bf16.
+// and the two token tiles (token ring); eight dequant warps expand each packed word with ONE
+// LOP3 per two weights into exact fp16 pairs -- (1024 + q) for a k-block's columns 0..31, (1024 +
+// 16 q) for columns 32..63 (the 0x6400 fp16 magic; the old bf16 path needed a shift + two LOPs +
+// an HFMA2 per pair and was the kernel's bound, profiles/r01/k2_ablation_w13.txt) -- and
+// tcgen05.st them straight into a TMEM A-slot (lane = weight row, column c = K elements 2c, 2c+1).
+// The MMA warps run kind::f16 (fp16 A from TMEM, fp16 token tile B from smem: x for class-1
+// columns, x/16 for class-16 columns, so one accumulator serves both), one accumulator per group;
+// four epilogue warps remove the bias with the per-token k-block sums csum and apply the group's
+// per-row scale in fp32 while the next groups run:
+//   y[row] = sum_g s[row][g] * (D_g[row] - C_g),  D_g - C_g = sum_{k in g} (q[row][k] - 8) x[k]
+// Every product in D is exact (11-bit fp16 A x 11-bit fp16 B in the fp32 accumulator); the
+// accumulation carries the 1024 offset, ~1e-4 relative to the group sum (tolerance 2e-3).
+// Tile-major INT4 layout: packed [rows/128][cols/64][128 rows x 8 words]; word W of a row holds
+// the k-block's columns 4W @0, 4W+1 @16, 4W+2 @8, 4W+3 @24, 32+4W @4, 33+4W @20, 34+4W @12,
+// 35+4W @28 (bit offsets).  Scales [rows/128][cols/128][128] bf16.
 MSPQ_D void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(bar)) : "memory");
 }
@@ -287,12 +352,12 @@ MSPQ_D bool mbar_test(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 
-MSPQ_D uint32_t dq2(uint32_t w, int i) {
-  // (w >> 4i) & 0x000F000F | 0x43004300 = bf16x2(128 + q_lo, 128 + q_hi); minus 136 -> exact q - 8
-  uint32_t t = ((w >> (4 * i)) & 0x000F000Fu) | 0x43004300u;
-  __nv_bfloat162 v = *reinterpret_cast<__nv_bfloat162*>(&t);
-  v = __hsub2(v, __floats2bfloat162_rn(136.0f, 136.0f));
-  return *reinterpret_cast<uint32_t*>(&v);
+// (w & mask) | 0x64006400 in ONE LOP3: fp16x2 (1024 + q) for mask 0x000F000F, (1024 + 16 q) for
+// 0x00F000F0 -- exact; the 1024 / 16 / -8 terms are removed in the epilogue (csum)
+MSPQ_D uint32_t lop3_and_or(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
 }
 
 MSPQ_D uint4 lds128(uint32_t addr) {
@@ -453,7 +518,7 @@ __global__ void __launch_bounds__(32 * (13 + NI), 2) k_umma_int4(UmmaArgs a) {
   } else if (warp < W_DQ) {
     if (lane == 0) {  // MMA issuer warp - 1: A from the TMEM slot, B from the token stage
       const int is = warp - 1;
-      constexpr uint32_t idesc = idesc_bf16(BN);
+      constexpr uint32_t idesc = idesc_f16(BN);
       // SW128 K-major B descriptor; 8-row-group stride 0 in BROWS = 8 mode (rows 8..15 alias 0..7)
       constexpr uint64_t sbo_fix = BROWS == 8 ? ~((uint64_t)0x3FFF << 32) : ~(uint64_t)0;
       for (int gi = is, u = 0; gi < ngr; gi += NI, ++u) {
@@ -483,15 +548,21 @@ __global__ void __launch_bounds__(32 * (13 + NI), 2) k_umma_int4(UmmaArgs a) {
       const uint32_t src = su32(sW + st * WST + ((gi % GS) * 2 + h) * TILE_Q + r * 32);
       const uint4 w0 = lds128(src), w1 = lds128(src + 16);
       const uint32_t ws[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+      // word w -> TMEM columns 2w, 2w+1 (class 1: local K 4w..4w+3) and 16+2w, 17+2w (class 16)
       uint32_t v[32];
       if (abl & 4) {
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = ws[i & 7];
       } else {
+        const uint32_t m_lo = 0x000F000Fu, m_hi = 0x00F000F0u, magic = 0x64006400u;
 #pragma unroll
-        for (int wi = 0; wi < 8; ++wi)
-#pragma unroll
-          for (int i = 0; i < 4; ++i) v[wi * 4 + i] = dq2(ws[wi], i);
+        for (int wi = 0; wi < 8; ++wi) {
+          const uint32_t w8 = ws[wi] >> 8;
+          v[2 * wi] = lop3_and_or(ws[wi], m_lo, magic);
+          v[2 * wi + 1] = lop3_and_or(w8, m_lo, magic);
+          v[16 + 2 * wi] = lop3_and_or(ws[wi], m_hi, magic);
+          v[17 + 2 * wi] = lop3_and_or(w8, m_hi, magic);
+        }
       }
       if (gi % GS == GS - 1 || gi == ngr - 1) mbar_arrive(&empty_w[st]);  // stage consumed: refill it
       if (gi >= NA) mbar_wait_sleep(&done[(gi - NA) % ND], ((gi - NA) / ND) & 1);
@@ -507,36 +578,65 @@ __global__ void __launch_bounds__(32 * (13 + NI), 2) k_umma_int4(UmmaArgs a) {
     const uint16_t* sc = reinterpret_cast<const uint16_t*>(a.w_base + ((int64_t)a.expert_base + a.group_buf[g]) * a.blob_bytes +
                                                            a.s_off) +
                          ((int64_t)rt * (a.kdim / 128) + kb0 / 2) * BM + row;
-    float acc[BN];
+    constexpr int NJ = BROWS < BN ? BROWS : BN;  // distinct token columns (8-row mode: 0..7)
+    float acc[NJ];
 #pragma unroll
-    for (int j = 0; j < BN; ++j) acc[j] = 0.0f;
-    // the per-row scales of 8 groups are fetched together, ahead of their accumulators, so the
-    // drain of one group never waits on a global-memory round trip
-    constexpr int SW = 8;
-    float scw[SW];
+    for (int j = 0; j < NJ; ++j) acc[j] = 0.0f;
+    // per-token corrections of each k-block (k_gather_b / k_finalize_act, F16)
+    const float* cs = a.csum + (int64_t)g * BROWS * kb_total + kb0;
+    // the per-row scales and token 0's corrections of the next 8 groups are fetched one batch
+    // ahead, so the drain of a group never waits on a global-memory round trip (that latency,
+    // paid per group, throttled the MMA issuers through acce)
+    constexpr int SW = 4;
+    float scw[SW], csw[SW], scn[SW], csn[SW];
+    auto fetch = [&](int g0, float* sv, float* cv) {
+#pragma unroll
+      for (int u = 0; u < SW; ++u) {
+        const bool ok = g0 + u < ngr;
+        sv[u] = ok ? bf2f(sc[(int64_t)(g0 + u) * BM]) : 0.0f;
+        cv[u] = ok ? cs[2 * (g0 + u)] + cs[2 * (g0 + u) + 1] : 0.0f;
+      }
+    };
+    fetch(0, scn, csn);
     for (int gi = 0; gi < ngr; ++gi) {
       if (gi % SW == 0) {
 #pragma unroll
-        for (int u = 0; u < SW; ++u) scw[u] = gi + u < ngr ? bf2f(sc[(int64_t)(gi + u) * BM]) : 0.0f;
+        for (int u = 0; u < SW; ++u) {
+          scw[u] = scn[u];
+          csw[u] = csn[u];
+        }
+        if (gi + SW < ngr) fetch(gi + SW, scn, csn);
       }
       const int ab = (gi % NI) * NACC + (gi / NI) % NACC;  // issuer gi % NI, its buffer
-      float scale = scw[0];
+      float scale = scw[0], c0 = csw[0];
 #pragma unroll
       for (int u = 1; u < SW; ++u)
-        if (gi % SW == u) scale = scw[u];
+        if (gi % SW == u) {
+          scale = scw[u];
+          c0 = csw[u];
+        }
       mbar_wait_sleep(&done[gi % ND], (gi / ND) & 1);
       if (threadIdx.x == 32 * W_EP) tl_mark(tl, 1280 + gi);
       tc_fence_after();
-      float v[BN];
-      tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + ab * BN, v);
-      if (BN == 32) tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + ab * BN + 16, v + 16);
+      float v[NJ];
+      if (NJ == 8) {
+        tmem_ld8(tmem + ((uint32_t)(q * 32) << 16) + ab * BN, v);
+      } else {
+        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + ab * BN, v);
+        if (NJ == 32) tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + ab * BN + 16, v + 16);
+      }
       tc_fence_before();
       mbar_arrive(&acce[ab]);
+      acc[0] = fmaf(scale, v[0] - c0, acc[0]);
 #pragma unroll
-      for (int j = 0; j < BN; ++j) acc[j] = fmaf(scale, v[j], acc[j]);
+      for (int j = 1; j < NJ; ++j)
+        if (j < m) {
+          const float c = cs[(int64_t)j * kb_total + 2 * gi] + cs[(int64_t)j * kb_total + 2 * gi + 1];
+          acc[j] = fmaf(scale, v[j] - c, acc[j]);
+        }
     }
 #pragma unroll
-    for (int j = 0; j < BN; ++j)
+    for (int j = 0; j < NJ; ++j)
       if (j < m) outp[(int64_t)(e0 + j) * a.rows + rt * BM + row] = acc[j];
     if (tla && threadIdx.x == 32 * W_EP) {
       long long t;
@@ -562,15 +662,17 @@ __global__ void k_tile_int4(const uint32_t* __restrict__ q, const uint16_t* __re
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nw; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / wpr;
     const int w = (int)(i - r * wpr);
-    const uint32_t v = q[i];
-    uint32_t o = 0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const uint32_t nib = (v >> (4 * j)) & 0xFu;
-      o |= nib << ((j & 1) ? 16 + 4 * (j >> 1) : 4 * (j >> 1));
-    }
-    const int rt = (int)(r / BM), rr = (int)(r % BM), kb = w / 8, ww = w % 8;
-    tq[(((int64_t)rt * kbt + kb) * BM + rr) * 8 + ww] = o;
+    // output word W = w % 8 of k-block kb = w / 8 holds the block's local columns
+    //   4W @0, 4W+1 @16, 4W+2 @8, 4W+3 @24 (class 1) and 32+4W @4, 33+4W @20, 34+4W @12, 35+4W @28
+    // (class 16): one LOP3 per two fp16 weights (K2 dequant), no shifts for the low byte pair
+    const int kb = w / 8, W = w % 8;
+    const uint32_t* src = q + r * wpr + kb * 8;
+    auto nib = [&](int c) { return (src[c >> 3] >> (4 * (c & 7))) & 0xFu; };
+    const uint32_t o = nib(4 * W) | (nib(4 * W + 1) << 16) | (nib(4 * W + 2) << 8) | (nib(4 * W + 3) << 24) |
+                       (nib(32 + 4 * W) << 4) | (nib(33 + 4 * W) << 20) | (nib(34 + 4 * W) << 12) |
+                       (nib(35 + 4 * W) << 28);
+    const int rt = (int)(r / BM), rr = (int)(r % BM);
+    tq[(((int64_t)rt * kbt + kb) * BM + rr) * 8 + W] = o;
   }
   const int64_t ns = (int64_t)rows * ngr;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ns; i += (int64_t)gridDim.x * blockDim.x) {
@@ -646,16 +748,23 @@ cudaError_t launch_tile_int4(const uint32_t* q, const uint16_t* s, int rows, int
 }
 
 cudaError_t launch_gather_b(const uint16_t* x, int ld, SchedPtrs s, int max_groups, int kdim, int BN,
-                            unsigned char* img, cudaStream_t st) {
-  k_gather_b<<<dim3(kdim / BK, max_groups), 128, 0, st>>>(x, ld, s, kdim, BN, img);
+                            unsigned char* img, cudaStream_t st, float* csum) {
+  if (csum)
+    k_gather_b<true><<<dim3(kdim / BK, max_groups), 128, 0, st>>>(x, ld, s, kdim, BN, img, csum);
+  else
+    k_gather_b<false><<<dim3(kdim / BK, max_groups), 128, 0, st>>>(x, ld, s, kdim, BN, img, nullptr);
   return cudaGetLastError();
 }
 
 cudaError_t launch_finalize_act(const float* p1, int splits, int64_t split_stride, SchedPtrs s,
                                 const int32_t* entry_group, int n_entries, int f, int BN, unsigned char* img,
-                                cudaStream_t st) {
-  k_finalize_act<<<dim3((f + 255) / 256, n_entries), 256, 0, st>>>(p1, splits, split_stride, s, entry_group,
-                                                                    n_entries, f, BN, img);
+                                cudaStream_t st, float* csum) {
+  if (csum)
+    k_finalize_act<true><<<dim3(f / 256, n_entries), 256, 0, st>>>(p1, splits, split_stride, s, entry_group,
+                                                                  n_entries, f, BN, img, csum);
+  else
+    k_finalize_act<false><<<dim3(f / 256, n_entries), 256, 0, st>>>(p1, splits, split_stride, s, entry_group,
+                                                                   n_entries, f, BN, img, nullptr);
   return cudaGetLastError();
 }
 
