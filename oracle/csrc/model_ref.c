@@ -12,6 +12,8 @@
  *   orc_rmsnorm      r = 1/sqrtf(sumsq/d + eps); xn = bf16((h*r)*gamma)
  *   orc_det_exp      range-reduced degree-7 polynomial exp (same ops as the device)
  *   orc_router_topk  logits -> top-k (desc, tie -> lower id) -> softmax over the selection
+ *   orc_gen_bf16     the counter-hash weight generator (oracle/model.py uniform/gen, restated
+ *                    in C only for speed; pinned to the numpy version by test_oracle_cpu)
  */
 #include <math.h>
 #include <stdint.h>
@@ -133,5 +135,21 @@ void orc_act(const float* g, const float* u, int f, uint16_t* a) {
   for (int i = 0; i < f; ++i) {
     float s = g[i] / (1.0f + orc_det_exp(-g[i]));
     a[i] = f2bf(s * u[i]);
+  }
+}
+
+/* w[i] = bf16(val(start + i) * scale), val(idx) = ((mix(key + idx*STEP) >> 40) - 2^23 + 0.5) * 2^-23 */
+static inline uint64_t orc_mix(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+void orc_gen_bf16(uint64_t key, uint64_t start, int64_t n, float scale, uint16_t* out) {
+  for (int64_t i = 0; i < n; ++i) {
+    const uint64_t z = orc_mix(key + (start + (uint64_t)i) * 0xD1B54A32D192ED03ull);
+    const int32_t hi = (int32_t)(z >> 40) - (1 << 23);
+    const float v = ((float)hi + 0.5f) * (1.0f / 8388608.0f);
+    out[i] = f2bf(v * scale);
   }
 }

@@ -51,6 +51,7 @@ def lib():
         L.orc_router_topk.argtypes = [P, P, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, P]
         L.orc_lm_head.argtypes = [P, P, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P]
         L.orc_act.argtypes = [P, P, ctypes.c_int, P]
+        L.orc_gen_bf16.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64, ctypes.c_float, P]
         _lib = L
     return _lib
 
@@ -120,9 +121,16 @@ def t_expert(l, e, m):
     return 0x1000000 + ((l * 1024 + e) * 4 + m)
 
 
-def gen(seed, tensor, rows, cols, scale) -> np.ndarray:
+def gen_np(seed, tensor, rows, cols, scale) -> np.ndarray:
     v = uniform(seed, tensor, rows * cols)
     return f32_to_bf16(v * np.float32(scale)).reshape(rows, cols)
+
+
+def gen(seed, tensor, rows, cols, scale) -> np.ndarray:
+    """bf16 [rows, cols] = gen_np (the pinned numpy definition) via its C restatement."""
+    out = np.empty(rows * cols, dtype=np.uint16)
+    lib().orc_gen_bf16(tensor_key(seed, tensor), 0, rows * cols, ctypes.c_float(np.float32(scale)), _p(out))
+    return out.reshape(rows, cols)
 
 
 def gen_gamma(seed, tensor, d) -> np.ndarray:

@@ -188,3 +188,25 @@ def test_expert_codec_is_lossless_end_to_end(cuda):
             assert ca[key] == cb[key], key
     assert b["h2d_bytes_bf16"] == a["h2d_bytes"]
     assert b["total_new_experts"] > 0 and b["h2d_bytes"] < 0.72 * a["h2d_bytes"]
+
+
+@pytest.mark.parametrize("name,cap,k", [("phi", 4, 3), ("qwen3", 32, 2)])
+def test_generate_full_width_shapes_match_oracle(cuda, name, cap, k):
+    """BASELINE model widths (Phi-3.5-MoE: E=16 top-2 d=4096 ffn=6400 V=32064; Qwen3-30B-A3B:
+    E=128 top-8 d=2048 ffn=768 V=151936) on 2 layers, capped cache, XC host store: every routing
+    trace, draft token, target argmax and committed token equals the CPU oracle's, and the
+    hit/miss log equals the control-plane restatement's."""
+    eng, cfg = _engine(name, L=2)
+    conf = {"policy": "speculative", "cache_capacity": cap, "k": k}
+    eng.configure(conf)
+    prompt = [11, 200, 3001]
+    rep = eng.generate(prompt, 10)
+    model = om.Model(_oracle_desc(cfg))
+    oc = om.speculative_decode(model, prompt[-1], len(prompt) - 1, [c["k"] for c in rep["cycles"]], 10)
+    _check_traces(rep, oc)
+    want = _control_plane_log(rep, conf, cfg.L, cfg.E)
+    for c, w in zip(rep["cycles"], want):
+        got = [(KINDS[ev[0]], ev[2], ev[3], ev[4], ev[5], ev[6]) for ev in c["log"]]
+        assert got == w
+    assert rep["total_new_experts"] > 0
+    eng.close()

@@ -159,3 +159,11 @@ def test_oracle_speculative_decode_is_lossless():
     for ks in ([1], [3], [6, 2, 4]):
         cyc = om.speculative_decode(m, 9, 4, ks, 24)
         assert [t for c in cyc for t in c["committed"]] == greedy
+
+
+def test_c_weight_generator_equals_numpy_definition():
+    """orc_gen_bf16 (speed) == gen_np (the numpy restatement of the counter-hash generator)."""
+    from oracle import model as om
+    for seed, tensor, rows, cols, scale in [(1234, om.t_expert(3, 7, 1), 64, 96, 0.0379),
+                                            (9, om.T_LM, 5, 4096, 1.0), (77, om.t_router(0), 16, 256, 0.25)]:
+        assert np.array_equal(om.gen(seed, tensor, rows, cols, scale), om.gen_np(seed, tensor, rows, cols, scale))
