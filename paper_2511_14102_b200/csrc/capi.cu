@@ -162,6 +162,18 @@ int mspq_moe_int4_tc(const int32_t* n_groups, const int32_t* group_expert, const
               (int32_t*)entry_tok, nullptr, (int32_t*)entry_group};
   cudaStream_t st = ST(stream);
   const long long q13 = (long long)2 * f * d / 2, s13 = (long long)2 * f * (d / 128) * 2, q2 = (long long)d * f / 2;
+  if (T == 1 && IR == 8 && split1 == 1) {
+    // draft shape: both GEMMs build their token tiles from the bf16 rows themselves and W13's
+    // epilogue applies SiLU*up (no gather / finalize kernels, no fp32 W13 plane)
+    uint16_t* act = (uint16_t*)b2;  // [N][f] bf16
+    UmmaArgs u1{(const unsigned char*)blobs, blob_bytes, 0, 2 * f, d, n_groups, group_buf, group_off, nullptr, p1,
+                N * 2 * f, 1, q13, layer * E, IR, nullptr, (const uint16_t*)xn, 0, entry_tok, act};
+    cudaError_t e = launch_umma_int4(u1, max_groups, BN, st);
+    if (e != cudaSuccess) return cuda_status(e, "umma_int4 W13 (fused act)");
+    UmmaArgs u2{(const unsigned char*)blobs, blob_bytes, q13 + s13, d, f, n_groups, group_buf, group_off, nullptr, y,
+                N * d, split2, q13 + s13 + q2, layer * E, IR, nullptr, act, 1, entry_tok, nullptr};
+    CK(launch_umma_int4(u2, max_groups, BN, st), "umma_int4 W2 (self-gather)");
+  }
   cudaError_t e = launch_gather_b((const uint16_t*)xn, d, s, max_groups, d, IR, b1, st, c1);
   if (e != cudaSuccess) return cuda_status(e, "gather_b");
   UmmaArgs u1{(const unsigned char*)blobs, blob_bytes, 0, 2 * f, d, n_groups, group_buf, group_off, b1, p1,

@@ -35,6 +35,10 @@ struct UmmaArgs {
   int expert_base;              // INT4: blob index = expert_base + group_buf[g]
   int brows = 0;                // rows per B image (8 = aliased 8-row tiles, else BN)
   const float* csum = nullptr;  // INT4: [G][brows][kdim/64] epilogue corrections (see k_gather_b)
+  const uint16_t* xsrc = nullptr;  // INT4 self-gather: bf16 token rows [.][kdim] (one token per group)
+  int xsrc_by_entry = 0;           // row of group g = entry_tok[e0] (0) or the entry e0 (1)
+  const int32_t* entry_tok = nullptr;
+  uint16_t* act_out = nullptr;     // INT4 W13, split 1: fused act = bf16(silu(gate) * up) [N][rows/2]
 };
 
 struct ExpertArgs {

@@ -336,6 +336,7 @@ __global__ void k_tile_bf16(const uint16_t* __restrict__ src, int rows, int cols
 // Tile-major INT4 layout: packed [rows/128][cols/64][128 rows x 8 words]; word W of a row holds
 // the k-block's columns 4W @0, 4W+1 @16, 4W+2 @8, 4W+3 @24, 32+4W @4, 33+4W @20, 34+4W @12,
 // 35+4W @28 (bit offsets).  Scales [rows/128][cols/128][128] bf16.
+MSPQ_D void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 MSPQ_D void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(bar)) : "memory");
 }
@@ -482,38 +483,83 @@ __global__ void __launch_bounds__(32 * (13 + NI), 2) k_umma_int4(UmmaArgs a) {
   const uint32_t tmem = *tmem_slot;
   const int ngr = nk / 2;
   const int nst = (ngr + GS - 1) / GS;
+  constexpr int NJ = BROWS < BN ? BROWS : BN;  // distinct token columns (8-row mode: 0..7)
+  float epi_acc[NJ];  // epilogue warps: per-token row results
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) epi_acc[j] = 0.0f;
+#define epi_acc0 epi_acc[0]
 
-  if (warp == 0) {
-    if (lane == 0) {  // producer: the weight ring runs ahead of the token ring
-      const unsigned char* wsrc = a.w_base + ((int64_t)a.expert_base + a.group_buf[g]) * a.blob_bytes + a.w_off +
-                                  ((int64_t)rt * kb_total + kb0) * TILE_Q;
-      const unsigned char* bsrc = a.bimg + ((int64_t)g * kb_total + kb0) * TB;
-      tl_mark(tl, 0);
-      int jw = 0, jt = 0;
-      const long long c0 = clock64();
-      while (jw < nst || jt < nst) {
-        bool prog = false;
-        if (jw < nst && (jw < PW || mbar_test(&empty_w[jw % PW], ((jw / PW) - 1) & 1))) {
-          prog = true;
+  // self-gather (a.xsrc, one token per group): warp 0 builds the fp16 class-scaled token tiles
+  // from the bf16 row itself (no gather kernel, no image in HBM) and keeps each group's
+  // correction sum in smem (csm); otherwise token tiles are bulk-copied from a.bimg
+  const bool selfg = a.xsrc != nullptr;
+  __shared__ float csm[256];
+  if (warp == 0) {  // producer: the weight ring runs ahead of the token ring
+    const unsigned char* wsrc = a.w_base + ((int64_t)a.expert_base + a.group_buf[g]) * a.blob_bytes + a.w_off +
+                                ((int64_t)rt * kb_total + kb0) * TILE_Q;
+    const unsigned char* bsrc = selfg ? nullptr : a.bimg + ((int64_t)g * kb_total + kb0) * TB;
+    const uint16_t* xr = selfg ? a.xsrc + (int64_t)(a.xsrc_by_entry ? e0 : a.entry_tok[e0]) * a.kdim + kb0 * BK
+                               : nullptr;
+    tl_mark(tl && lane == 0, 0);
+    int jw = 0, jt = 0;
+    const long long c0 = clock64();
+    while (jw < nst || jt < nst) {
+      int iw = 0, it = 0;
+      if (lane == 0) {
+        iw = jw < nst && (jw < PW || mbar_test(&empty_w[jw % PW], ((jw / PW) - 1) & 1));
+        const int gl = min(GS * (jt - PT) + GS - 1, ngr - 1);  // last group of stage jt - PT
+        it = jt < nst && jt < jw + iw && (jt < PT || mbar_test(&done[gl % ND], (gl / ND) & 1));
+      }
+      iw = __shfl_sync(0xffffffffu, iw, 0);
+      it = __shfl_sync(0xffffffffu, it, 0);
+      if (iw) {
+        if (lane == 0) {
           tl_mark(tl, 1 + jw);
           const int cnt = min(GS, ngr - jw * GS);
           mbar_expect_tx(&full_w[jw % PW], cnt * 2 * TILE_Q);
           bulk_g2s(sW + (jw % PW) * WST, wsrc + (int64_t)jw * WST, cnt * 2 * TILE_Q, &full_w[jw % PW]);
-          ++jw;
         }
-        if (jt < nst && jt < jw) {
-          const int gl = min(GS * (jt - PT) + GS - 1, ngr - 1);  // last group of stage jt - PT
-          if (jt < PT || mbar_test(&done[gl % ND], (gl / ND) & 1)) {
-            const int cnt = min(GS, ngr - jt * GS);
-            mbar_expect_tx(&full_t[jt % PT], cnt * 2 * TB);
-            bulk_g2s(sT + (jt % PT) * TST, bsrc + (int64_t)jt * TST, cnt * 2 * TB, &full_t[jt % PT]);
-            ++jt;
-            prog = true;
-          }
-        }
-        if (!prog) __nanosleep(64);  // polling must not steal issue slots from the dequant warps
-        if (clock64() - c0 > 4000000000LL) __trap();
+        ++jw;
       }
+      if (it) {
+        const int cnt = min(GS, ngr - jt * GS);
+        unsigned char* tdst = sT + (jt % PT) * TST;
+        if (selfg) {
+          // lane: k-block kbl = lane / 8 of the stage, chunk c = lane % 8 (8 columns); row 0 only
+          // (rows 1..7 of the 8-row tile are never stored by the epilogue)
+          const int kbl = lane >> 3, c = lane & 7;
+          float part = 0.0f;
+          if (kbl < 2 * cnt) {
+            const uint4 v = *reinterpret_cast<const uint4*>(xr + (int64_t)(jt * 4 + kbl) * BK + c * 8);
+            const float mul = c < 4 ? 1.0f : 0.0625f, cc = c < 4 ? 1032.0f : 1152.0f;
+            uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const uint16_t lo = f2h_bits(bf2f((uint16_t)(w[j] & 0xFFFFu)) * mul);
+              const uint16_t hi = f2h_bits(bf2f((uint16_t)(w[j] >> 16)) * mul);
+              part = fmaf(cc, h2f_bits(lo), part);
+              part = fmaf(cc, h2f_bits(hi), part);
+              w[j] = (uint32_t)lo | ((uint32_t)hi << 16);
+            }
+            *reinterpret_cast<uint4*>(tdst + kbl * TB + sw128_off(0, c * 8)) = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+          part += __shfl_xor_sync(0xffffffffu, part, 1);
+          part += __shfl_xor_sync(0xffffffffu, part, 2);
+          part += __shfl_xor_sync(0xffffffffu, part, 4);
+          const float other = __shfl_down_sync(0xffffffffu, part, 8);  // the group's second k-block
+          if (lane == 0) csm[jt * GS] = part + other;
+          if (lane == 16 && cnt > 1) csm[jt * GS + 1] = part + other;
+          fence_proxy_async_smem();  // generic-proxy tile writes -> the MMA's async-proxy reads
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&full_t[jt % PT]);
+        } else if (lane == 0) {
+          mbar_expect_tx(&full_t[jt % PT], cnt * 2 * TB);
+          bulk_g2s(tdst, bsrc + (int64_t)jt * TST, cnt * 2 * TB, &full_t[jt % PT]);
+        }
+        ++jt;
+      }
+      if (!iw && !it) __nanosleep(64);  // polling must not steal issue slots from the dequant warps
+      if (lane == 0 && clock64() - c0 > 4000000000LL) __trap();
     }
   } else if (warp < W_DQ) {
     if (lane == 0) {  // MMA issuer warp - 1: A from the TMEM slot, B from the token stage
@@ -578,15 +624,13 @@ __global__ void __launch_bounds__(32 * (13 + NI), 2) k_umma_int4(UmmaArgs a) {
     const uint16_t* sc = reinterpret_cast<const uint16_t*>(a.w_base + ((int64_t)a.expert_base + a.group_buf[g]) * a.blob_bytes +
                                                            a.s_off) +
                          ((int64_t)rt * (a.kdim / 128) + kb0 / 2) * BM + row;
-    constexpr int NJ = BROWS < BN ? BROWS : BN;  // distinct token columns (8-row mode: 0..7)
-    float acc[NJ];
-#pragma unroll
-    for (int j = 0; j < NJ; ++j) acc[j] = 0.0f;
+    float* acc = epi_acc;
     // per-token corrections of each k-block (k_gather_b / k_finalize_act, F16)
     const float* cs = a.csum + (int64_t)g * BROWS * kb_total + kb0;
-    // the per-row scales and token 0's corrections of the next 8 groups are fetched one batch
+    // the per-row scales and token 0's corrections of the next SW groups are fetched one batch
     // ahead, so the drain of a group never waits on a global-memory round trip (that latency,
-    // paid per group, throttled the MMA issuers through acce)
+    // paid per group, throttled the MMA issuers through acce).  Self-gather: the corrections
+    // live in csm and are applied after the final __syncthreads (sum_g s_g * C_g).
     constexpr int SW = 4;
     float scw[SW], csw[SW], scn[SW], csn[SW];
     auto fetch = [&](int g0, float* sv, float* cv) {
@@ -594,7 +638,7 @@ __global__ void __launch_bounds__(32 * (13 + NI), 2) k_umma_int4(UmmaArgs a) {
       for (int u = 0; u < SW; ++u) {
         const bool ok = g0 + u < ngr;
         sv[u] = ok ? bf2f(sc[(int64_t)(g0 + u) * BM]) : 0.0f;
-        cv[u] = ok ? cs[2 * (g0 + u)] + cs[2 * (g0 + u) + 1] : 0.0f;
+        cv[u] = ok && !selfg ? cs[2 * (g0 + u)] + cs[2 * (g0 + u) + 1] : 0.0f;
       }
     };
     fetch(0, scn, csn);
@@ -619,11 +663,11 @@ __global__ void __launch_bounds__(32 * (13 + NI), 2) k_umma_int4(UmmaArgs a) {
       if (threadIdx.x == 32 * W_EP) tl_mark(tl, 1280 + gi);
       tc_fence_after();
       float v[NJ];
-      if (NJ == 8) {
+      if constexpr (NJ == 8) {
         tmem_ld8(tmem + ((uint32_t)(q * 32) << 16) + ab * BN, v);
       } else {
         tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + ab * BN, v);
-        if (NJ == 32) tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + ab * BN + 16, v + 16);
+        if constexpr (NJ == 32) tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + ab * BN + 16, v + 16);
       }
       tc_fence_before();
       mbar_arrive(&acce[ab]);
@@ -635,9 +679,6 @@ __global__ void __launch_bounds__(32 * (13 + NI), 2) k_umma_int4(UmmaArgs a) {
           acc[j] = fmaf(scale, v[j] - c, acc[j]);
         }
     }
-#pragma unroll
-    for (int j = 0; j < NJ; ++j)
-      if (j < m) outp[(int64_t)(e0 + j) * a.rows + rt * BM + row] = acc[j];
     if (tla && threadIdx.x == 32 * W_EP) {
       long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -647,10 +688,37 @@ __global__ void __launch_bounds__(32 * (13 + NI), 2) k_umma_int4(UmmaArgs a) {
   }
   tc_fence_before();
   __syncthreads();
+  if (warp >= W_EP) {  // output: self-gather corrections, then y planes or the fused SiLU*up
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    if (selfg) {
+      const uint16_t* sc = reinterpret_cast<const uint16_t*>(a.w_base + ((int64_t)a.expert_base + a.group_buf[g]) * a.blob_bytes +
+                                                             a.s_off) +
+                           ((int64_t)rt * (a.kdim / 128) + kb0 / 2) * BM + row;
+      float corr = 0.0f;
+      for (int gi = 0; gi < ngr; ++gi) corr = fmaf(bf2f(sc[(int64_t)gi * BM]), csm[gi], corr);
+      epi_acc0 -= corr;
+    }
+    if (a.act_out) {
+      // interleaved W13 rows: row 2i = gate_i, 2i+1 = up_i; act = bf16(silu(gate) * up), exactly
+      // k_finalize_act's arithmetic on a single split
+      const float up = __shfl_down_sync(0xffffffffu, epi_acc0, 1);
+      if ((lane & 1) == 0 && m > 0)
+        a.act_out[(int64_t)e0 * (a.rows / 2) + (rt * BM + row) / 2] = f2bf(__fmul_rn(silu_det(epi_acc0), up));
+    } else {
+      if (m > 0) outp[(int64_t)e0 * a.rows + rt * BM + row] = epi_acc0;
+#pragma unroll
+      for (int j = 1; j < NJ; ++j)
+        if (j < m) outp[(int64_t)(e0 + j) * a.rows + rt * BM + row] = epi_acc[j];
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
   }
+#undef epi_acc0
 }
 
 // row-major quantised (standard nibble order, scales [rows][cols/128]) -> tile-major INT4 layout
