@@ -399,6 +399,9 @@ MSPQ_D void tl_mark(bool on, int slot) {
   if (on && slot < 2048) g_int4_tl[slot] = clock64();
 }
 
+#ifndef K2_WAIT
+#define K2_WAIT mbar_wait
+#endif
 // warps: 0 producer, 1..NI MMA issuers (warp 1 also allocates TMEM; issuer i takes the groups
 // gi = i mod NI: an N=16 MMA costs its issuing THREAD ~56 cycles, but two issuers on one SM
 // overlap (tools/micro/mma_rate.cu), so the per-group issue cost is split), then 8 dequant warps
@@ -464,12 +467,12 @@ __global__ void __launch_bounds__(32 * (13 + NI), 2) k_umma_int4(UmmaArgs a) {
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < PW; ++i) {
       mbar_init(&full_w[i], 1);
-      mbar_init(&empty_w[i], 256);
+      mbar_init(&empty_w[i], 8);  // one arrival per dequant warp (256 thread arrivals cost ~1k cycles)
     }
     for (int i = 0; i < PT; ++i) mbar_init(&full_t[i], 1);
-    for (int i = 0; i < NA; ++i) mbar_init(&full_a[i], 256);
+    for (int i = 0; i < NA; ++i) mbar_init(&full_a[i], 8);
     for (int i = 0; i < ND; ++i) mbar_init(&done[i], 1);
-    for (int i = 0; i < NI * NACC; ++i) mbar_init(&acce[i], 128);
+    for (int i = 0; i < NI * NACC; ++i) mbar_init(&acce[i], 4);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -569,9 +572,9 @@ __global__ void __launch_bounds__(32 * (13 + NI), 2) k_umma_int4(UmmaArgs a) {
       constexpr uint64_t sbo_fix = BROWS == 8 ? ~((uint64_t)0x3FFF << 32) : ~(uint64_t)0;
       for (int gi = is, u = 0; gi < ngr; gi += NI, ++u) {
         const int js = gi / GS, st = js % PT, sl = gi % NA, b = u % NACC;
-        if (u >= NACC) mbar_wait_sleep(&acce[is * NACC + b], ((u / NACC) - 1) & 1);
-        mbar_wait_sleep(&full_t[st], (js / PT) & 1);
-        mbar_wait_sleep(&full_a[sl], (gi / NA) & 1);
+        if (u >= NACC) K2_WAIT(&acce[is * NACC + b], ((u / NACC) - 1) & 1);
+        K2_WAIT(&full_t[st], (js / PT) & 1);
+        K2_WAIT(&full_a[sl], (gi / NA) & 1);
         tl_mark(tl, 768 + gi);
         tc_fence_after();
         const uint32_t sb = su32(sT + st * TST + (gi % GS) * 2 * TB);
@@ -589,7 +592,7 @@ __global__ void __launch_bounds__(32 * (13 + NI), 2) k_umma_int4(UmmaArgs a) {
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     for (int gi = 0; gi < ngr; ++gi) {
       const int js = gi / GS, st = js % PW, sl = gi % NA;
-      mbar_wait_sleep(&full_w[st], (js / PW) & 1);
+      K2_WAIT(&full_w[st], (js / PW) & 1);
       if (threadIdx.x == 32 * W_DQ) tl_mark(tl, 256 + gi);
       const uint32_t src = su32(sW + st * WST + ((gi % GS) * 2 + h) * TILE_Q + r * 32);
       const uint4 w0 = lds128(src), w1 = lds128(src + 16);
@@ -610,12 +613,14 @@ __global__ void __launch_bounds__(32 * (13 + NI), 2) k_umma_int4(UmmaArgs a) {
           v[17 + 2 * wi] = lop3_and_or(w8, m_hi, magic);
         }
       }
-      if (gi % GS == GS - 1 || gi == ngr - 1) mbar_arrive(&empty_w[st]);  // stage consumed: refill it
-      if (gi >= NA) mbar_wait_sleep(&done[(gi - NA) % ND], ((gi - NA) / ND) & 1);
+      __syncwarp();
+      if (lane == 0 && (gi % GS == GS - 1 || gi == ngr - 1)) mbar_arrive(&empty_w[st]);  // stage consumed
+      if (gi >= NA) K2_WAIT(&done[(gi - NA) % ND], ((gi - NA) / ND) & 1);
       tc_fence_after();
       if (!(abl & 2)) tmem_st32(tmem + lane_base + ACOL + sl * 64 + h * 32, v);
       tc_fence_before();
-      mbar_arrive(&full_a[sl]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full_a[sl]);
       if (threadIdx.x == 32 * W_DQ) tl_mark(tl, 512 + gi);
     }
   } else {  // epilogue warps 10..13: per-group scale, fp32 accumulation in registers
@@ -659,7 +664,7 @@ __global__ void __launch_bounds__(32 * (13 + NI), 2) k_umma_int4(UmmaArgs a) {
           scale = scw[u];
           c0 = csw[u];
         }
-      mbar_wait_sleep(&done[gi % ND], (gi / ND) & 1);
+      K2_WAIT(&done[gi % ND], (gi / ND) & 1);
       if (threadIdx.x == 32 * W_EP) tl_mark(tl, 1280 + gi);
       tc_fence_after();
       float v[NJ];
@@ -670,7 +675,8 @@ __global__ void __launch_bounds__(32 * (13 + NI), 2) k_umma_int4(UmmaArgs a) {
         if constexpr (NJ == 32) tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + ab * BN + 16, v + 16);
       }
       tc_fence_before();
-      mbar_arrive(&acce[ab]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acce[ab]);
       acc[0] = fmaf(scale, v[0] - c0, acc[0]);
 #pragma unroll
       for (int j = 1; j < NJ; ++j)
