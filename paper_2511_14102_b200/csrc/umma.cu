@@ -399,6 +399,12 @@ MSPQ_D void tl_mark(bool on, int slot) {
   if (on && slot < 2048) g_int4_tl[slot] = clock64();
 }
 
+// pure polling wait (mbarrier.test_wait never suspends the thread)
+MSPQ_D void mbar_spin(uint64_t* bar, uint32_t parity) {
+  const long long t0 = clock64();
+  while (!mbar_test(bar, parity))
+    if (clock64() - t0 > 4000000000LL) __trap();
+}
 #ifndef K2_WAIT
 #define K2_WAIT mbar_wait
 #endif
@@ -413,12 +419,11 @@ MSPQ_D void tl_mark(bool on, int slot) {
 // tokens, N = 16) a token tile holds 8 rows (1 KB) and the descriptor's 8-row-group stride is 0:
 // the MMA's rows 8..15 alias rows 0..7, whose results the epilogue never stores.  NA TMEM
 // A-slots (64 columns = one group each), NACC TMEM accumulators.
-template <int BN, int BROWS, int PW, int PT, int NA, int NACC, int NI>
-__global__ void __launch_bounds__(32 * (13 + NI), 2) k_umma_int4(UmmaArgs a) {
-  constexpr int W_DQ = 1 + NI, W_EP = W_DQ + 8;  // first dequant / epilogue warp
+template <int BN, int BROWS, int PW, int PT, int NA, int NACC, int NI, int GS>
+__global__ void __launch_bounds__(32 * (14 + NI), 2) k_umma_int4(UmmaArgs a) {
+  constexpr int W_DQ = 1 + NI, W_EP = W_DQ + 8, W_TK = W_EP + 4;  // first dequant / epilogue warp, token warp
   constexpr int TILE_Q = BM * BK / 2;             // 4 KB packed per 128x64 tile
   constexpr int TB = BROWS * 128;                 // token tile bytes per k-block
-  constexpr int GS = 2;                           // groups per stage
   constexpr int WST = GS * 2 * TILE_Q, TST = GS * 2 * TB;
   constexpr uint32_t ACOL = NI * NACC * BN;       // first A-slot column (issuer i: acc cols i*NACC*BN..)
   constexpr uint32_t TCOLS = (ACOL + NA * 64) <= 128 ? 128 : ((ACOL + NA * 64) <= 256 ? 256 : 512);
@@ -497,45 +502,53 @@ __global__ void __launch_bounds__(32 * (13 + NI), 2) k_umma_int4(UmmaArgs a) {
   // correction sum in smem (csm); otherwise token tiles are bulk-copied from a.bimg
   const bool selfg = a.xsrc != nullptr;
   __shared__ float csm[256];
-  if (warp == 0) {  // producer: the weight ring runs ahead of the token ring
-    const unsigned char* wsrc = a.w_base + ((int64_t)a.expert_base + a.group_buf[g]) * a.blob_bytes + a.w_off +
-                                ((int64_t)rt * kb_total + kb0) * TILE_Q;
+  __shared__ float ksm[2 * GS];
+  if (warp == 0) {  // weight producer: one bulk copy per stage, nothing else on this warp
+    if (lane == 0) {
+      const unsigned char* wsrc = a.w_base + ((int64_t)a.expert_base + a.group_buf[g]) * a.blob_bytes + a.w_off +
+                                  ((int64_t)rt * kb_total + kb0) * TILE_Q;
+      tl_mark(tl, 0);
+      for (int jw = 0; jw < nst; ++jw) {
+        if (jw >= PW) K2_WAIT(&empty_w[jw % PW], ((jw / PW) - 1) & 1);
+        tl_mark(tl, 1 + jw);
+        const int cnt = min(GS, ngr - jw * GS);
+        mbar_expect_tx(&full_w[jw % PW], cnt * 2 * TILE_Q);
+        bulk_g2s(sW + (jw % PW) * WST, wsrc + (int64_t)jw * WST, cnt * 2 * TILE_Q, &full_w[jw % PW]);
+      }
+    }
+  } else if (warp == W_TK) {  // token producer: bulk copies of the B images, or self-gather
     const unsigned char* bsrc = selfg ? nullptr : a.bimg + ((int64_t)g * kb_total + kb0) * TB;
     const uint16_t* xr = selfg ? a.xsrc + (int64_t)(a.xsrc_by_entry ? e0 : a.entry_tok[e0]) * a.kdim + kb0 * BK
                                : nullptr;
-    tl_mark(tl && lane == 0, 0);
-    int jw = 0, jt = 0;
-    const long long c0 = clock64();
-    while (jw < nst || jt < nst) {
-      int iw = 0, it = 0;
-      if (lane == 0) {
-        iw = jw < nst && (jw < PW || mbar_test(&empty_w[jw % PW], ((jw / PW) - 1) & 1));
+    constexpr int XP = (GS * 2 * 8 + 31) / 32;  // 16-byte x chunks per lane per token stage
+    uint4 xq[XP];
+    auto load_x = [&](int js) {  // x chunks of token stage js into registers
+#pragma unroll
+      for (int p2 = 0; p2 < XP; ++p2) {
+        const int task = p2 * 32 + lane, kbl = task >> 3, c = task & 7;
+        xq[p2] = make_uint4(0, 0, 0, 0);
+        if (selfg && js < nst && kbl < 2 * min(GS, ngr - js * GS))
+          xq[p2] = *reinterpret_cast<const uint4*>(xr + (int64_t)(js * GS * 2 + kbl) * BK + c * 8);
+      }
+    };
+    if (selfg) load_x(0);
+    for (int jt = 0; jt < nst; ++jt) {
+      if (jt >= PT) {
         const int gl = min(GS * (jt - PT) + GS - 1, ngr - 1);  // last group of stage jt - PT
-        it = jt < nst && jt < jw + iw && (jt < PT || mbar_test(&done[gl % ND], (gl / ND) & 1));
+        K2_WAIT(&done[gl % ND], (gl / ND) & 1);
       }
-      iw = __shfl_sync(0xffffffffu, iw, 0);
-      it = __shfl_sync(0xffffffffu, it, 0);
-      if (iw) {
-        if (lane == 0) {
-          tl_mark(tl, 1 + jw);
-          const int cnt = min(GS, ngr - jw * GS);
-          mbar_expect_tx(&full_w[jw % PW], cnt * 2 * TILE_Q);
-          bulk_g2s(sW + (jw % PW) * WST, wsrc + (int64_t)jw * WST, cnt * 2 * TILE_Q, &full_w[jw % PW]);
-        }
-        ++jw;
-      }
-      if (it) {
-        const int cnt = min(GS, ngr - jt * GS);
-        unsigned char* tdst = sT + (jt % PT) * TST;
-        if (selfg) {
-          // lane: k-block kbl = lane / 8 of the stage, chunk c = lane % 8 (8 columns); row 0 only
-          // (rows 1..7 of the 8-row tile are never stored by the epilogue)
-          const int kbl = lane >> 3, c = lane & 7;
+      const int cnt = min(GS, ngr - jt * GS);
+      unsigned char* tdst = sT + (jt % PT) * TST;
+      if (selfg) {
+        // task = (k-block kbl of the stage, chunk c of 8 columns); row 0 only (rows 1..7 of the
+        // 8-row tile are never stored by the epilogue); x loaded one stage ahead
+#pragma unroll
+        for (int p2 = 0; p2 < XP; ++p2) {
+          const int task = p2 * 32 + lane, kbl = task >> 3, c = task & 7;
           float part = 0.0f;
           if (kbl < 2 * cnt) {
-            const uint4 v = *reinterpret_cast<const uint4*>(xr + (int64_t)(jt * 4 + kbl) * BK + c * 8);
             const float mul = c < 4 ? 1.0f : 0.0625f, cc = c < 4 ? 1032.0f : 1152.0f;
-            uint32_t w[4] = {v.x, v.y, v.z, v.w};
+            uint32_t w[4] = {xq[p2].x, xq[p2].y, xq[p2].z, xq[p2].w};
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               const uint16_t lo = f2h_bits(bf2f((uint16_t)(w[j] & 0xFFFFu)) * mul);
@@ -549,20 +562,18 @@ __global__ void __launch_bounds__(32 * (13 + NI), 2) k_umma_int4(UmmaArgs a) {
           part += __shfl_xor_sync(0xffffffffu, part, 1);
           part += __shfl_xor_sync(0xffffffffu, part, 2);
           part += __shfl_xor_sync(0xffffffffu, part, 4);
-          const float other = __shfl_down_sync(0xffffffffu, part, 8);  // the group's second k-block
-          if (lane == 0) csm[jt * GS] = part + other;
-          if (lane == 16 && cnt > 1) csm[jt * GS + 1] = part + other;
-          fence_proxy_async_smem();  // generic-proxy tile writes -> the MMA's async-proxy reads
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&full_t[jt % PT]);
-        } else if (lane == 0) {
-          mbar_expect_tx(&full_t[jt % PT], cnt * 2 * TB);
-          bulk_g2s(tdst, bsrc + (int64_t)jt * TST, cnt * 2 * TB, &full_t[jt % PT]);
+          if (c == 0 && kbl < 2 * GS) ksm[kbl] = part;
         }
-        ++jt;
+        __syncwarp();
+        if (lane < cnt) csm[jt * GS + lane] = ksm[2 * lane] + ksm[2 * lane + 1];
+        fence_proxy_async_smem();  // generic-proxy tile writes -> the MMA's async-proxy reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full_t[jt % PT]);
+        load_x(jt + 1);
+      } else if (lane == 0) {
+        mbar_expect_tx(&full_t[jt % PT], cnt * 2 * TB);
+        bulk_g2s(tdst, bsrc + (int64_t)jt * TST, cnt * 2 * TB, &full_t[jt % PT]);
       }
-      if (!iw && !it) __nanosleep(64);  // polling must not steal issue slots from the dequant warps
-      if (lane == 0 && clock64() - c0 > 4000000000LL) __trap();
     }
   } else if (warp < W_DQ) {
     if (lane == 0) {  // MMA issuer warp - 1: A from the TMEM slot, B from the token stage
@@ -588,6 +599,7 @@ __global__ void __launch_bounds__(32 * (13 + NI), 2) k_umma_int4(UmmaArgs a) {
     }
   } else if (warp < W_EP) {  // dequant warps: row q*32 + lane, k-block half h of each group
     const int q = warp & 3, h = (warp - W_DQ) >> 2;
+
     const int r = q * 32 + lane;
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     for (int gi = 0; gi < ngr; ++gi) {
@@ -623,7 +635,7 @@ __global__ void __launch_bounds__(32 * (13 + NI), 2) k_umma_int4(UmmaArgs a) {
       if (lane == 0) mbar_arrive(&full_a[sl]);
       if (threadIdx.x == 32 * W_DQ) tl_mark(tl, 512 + gi);
     }
-  } else {  // epilogue warps 10..13: per-group scale, fp32 accumulation in registers
+  } else if (warp < W_TK) {  // epilogue warps 10..13: per-group scale, fp32 accumulation in registers
     const int q = warp & 3;
     const int row = q * 32 + lane;
     const uint16_t* sc = reinterpret_cast<const uint16_t*>(a.w_base + ((int64_t)a.expert_base + a.group_buf[g]) * a.blob_bytes +
@@ -694,7 +706,7 @@ __global__ void __launch_bounds__(32 * (13 + NI), 2) k_umma_int4(UmmaArgs a) {
   }
   tc_fence_before();
   __syncthreads();
-  if (warp >= W_EP) {  // output: self-gather corrections, then y planes or the fused SiLU*up
+  if (warp >= W_EP && warp < W_TK) {  // output: self-gather corrections, then y planes or fused SiLU*up
     const int q = warp & 3;
     const int row = q * 32 + lane;
     if (selfg) {
@@ -775,26 +787,28 @@ cudaError_t launch_umma_grouped(const UmmaArgs& a, int max_groups, int BN, cudaS
 }
 
 cudaError_t launch_umma_int4(const UmmaArgs& a, int max_groups, int BN, cudaStream_t st) {
-  // 16 KB weight stages (two groups), token stages of two groups, 3 TMEM A-slots, 2 MMA issuers
-  // with 2 accumulators each (BN = 32: 1 each) in 256 TMEM columns: ~98 KB smem -> 2 CTAs/SM
-  constexpr int NA = 3, NI = 2, THREADS = 32 * (13 + NI);
+  // A bulk copy costs its issuing thread ~0.3 us, so the draft variant (8-row tiles) moves THREE
+  // groups (24 KB) per weight copy: 3 x 24 KB in flight, 2 token stages, 3 TMEM A-slots, 2 MMA
+  // issuers x 2 accumulators in 256 TMEM columns, ~86 KB smem -> 2 CTAs/SM.  The wider-token
+  // variants (tests, T > 8) keep two groups per copy.
+  constexpr int NA = 3, NI = 2, THREADS = 32 * (14 + NI);
   const int units = max_groups * (a.rows / BM) * a.splits;
   if (units == 0) return cudaSuccess;
-  auto smem = [&](int brows, int pw, int pt) {
-    return (size_t)1024 + pt * 4 * brows * 128 + pw * 4 * (BM * BK / 2) + 64 * 8 + 16;
+  auto smem = [&](int brows, int pw, int pt, int gs) {
+    return (size_t)1024 + pt * gs * 2 * brows * 128 + pw * gs * 2 * (BM * BK / 2) + 64 * 8 + 16;
   };
   if (BN == 16 && a.brows == 8) {
-    auto k = k_umma_int4<16, 8, 5, 4, NA, 2, NI>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(8, 5, 4));
-    k<<<units, THREADS, smem(8, 5, 4), st>>>(a);
+    auto k = k_umma_int4<16, 8, 3, 2, NA, 2, NI, 3>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(8, 3, 2, 3));
+    k<<<units, THREADS, smem(8, 3, 2, 3), st>>>(a);
   } else if (BN == 16) {
-    auto k = k_umma_int4<16, 16, 5, 2, NA, 2, NI>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(16, 5, 2));
-    k<<<units, THREADS, smem(16, 5, 2), st>>>(a);
+    auto k = k_umma_int4<16, 16, 5, 2, NA, 2, NI, 2>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(16, 5, 2, 2));
+    k<<<units, THREADS, smem(16, 5, 2, 2), st>>>(a);
   } else {
-    auto k = k_umma_int4<32, 32, 4, 2, NA, 1, NI>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(32, 4, 2));
-    k<<<units, THREADS, smem(32, 4, 2), st>>>(a);
+    auto k = k_umma_int4<32, 32, 4, 2, NA, 1, NI, 2>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(32, 4, 2, 2));
+    k<<<units, THREADS, smem(32, 4, 2, 2), st>>>(a);
   }
   return cudaGetLastError();
 }
