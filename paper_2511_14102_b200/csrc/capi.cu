@@ -168,11 +168,11 @@ int mspq_moe_int4_tc(const int32_t* n_groups, const int32_t* group_expert, const
     uint16_t* act = (uint16_t*)b2;  // [N][f] bf16
     UmmaArgs u1{(const unsigned char*)blobs, blob_bytes, 0, 2 * f, d, n_groups, group_buf, group_off, nullptr, p1,
                 N * 2 * f, 1, q13, layer * E, IR, nullptr, (const uint16_t*)xn, 0, entry_tok, act};
-    cudaError_t e = launch_umma_int4(u1, max_groups, BN, st);
+    cudaError_t e = launch_umma_int4p(u1, max_groups, st);
     if (e != cudaSuccess) return cuda_status(e, "umma_int4 W13 (fused act)");
     UmmaArgs u2{(const unsigned char*)blobs, blob_bytes, q13 + s13, d, f, n_groups, group_buf, group_off, nullptr, y,
                 N * d, split2, q13 + s13 + q2, layer * E, IR, nullptr, act, 1, entry_tok, nullptr};
-    CK(launch_umma_int4(u2, max_groups, BN, st), "umma_int4 W2 (self-gather)");
+    CK(launch_umma_int4p(u2, max_groups, st), "umma_int4 W2 (self-gather)");
   }
   cudaError_t e = launch_gather_b((const uint16_t*)xn, d, s, max_groups, d, IR, b1, st, c1);
   if (e != cudaSuccess) return cuda_status(e, "gather_b");

@@ -82,6 +82,7 @@ struct RouteArgs {
 
 cudaError_t launch_umma_grouped(const UmmaArgs& a, int max_groups, int BN, cudaStream_t st);
 cudaError_t launch_umma_int4(const UmmaArgs& a, int max_groups, int BN, cudaStream_t st);
+cudaError_t launch_umma_int4p(const UmmaArgs& a, int max_groups, cudaStream_t st);
 cudaError_t debug_int4_timeline(long long* dst, int n);
 cudaError_t launch_tile_int4(const uint32_t* q, const uint16_t* s, int rows, int cols, uint32_t* tq, uint16_t* ts,
                              cudaStream_t st);

@@ -349,11 +349,11 @@ void make_workspaces(mspq_engine* E) {
 }
 
 // One draft step for a single token, captured once as a CUDA graph.
-// K splits for a draft GEMM: the most that still fit ONE wave of K2 CTAs (2 per SM), so no
-// CTA streams its weights in a second, mostly idle wave
+// K splits for a draft GEMM: the most that still give every SM at most one unit of the
+// persistent K2 (one CTA per SM)
 int split_for(int units_per_split1, int kblocks) {
   const int units = std::max(1, units_per_split1);
-  const int sp = std::max(1, 296 / units);
+  const int sp = std::max(1, 148 / units);  // persistent K2: one CTA per SM
   return std::max(1, std::min({sp, mspq_engine::kMaxSplit, std::max(1, kblocks / 2)}));
 }
 

@@ -739,6 +739,305 @@ __global__ void __launch_bounds__(32 * (14 + NI), 2) k_umma_int4(UmmaArgs a) {
 #undef epi_acc0
 }
 
+// ------------------------------------------------------------------ K2 persistent (draft, T = 1)
+// One CTA per SM (all 512 TMEM columns: 7 A-slots + 2 issuers x 2 accumulators) walks units
+// u = blockIdx.x, + gridDim.x, ... of (group g, 128-row tile rt, K split s).  The per-CTA rate was
+// bounded by the A-slot round trip (dequant -> MMA -> commit -> done -> dequant), ~1 us for 3
+// slots; 7 slots in flight and one CTA per SM keep the weight stream going.  Every role walks the
+// same unit list; a global group counter gi drives all rings and barrier phases, so a unit's
+// pipeline runs straight into the next unit's.  Self-gather only (token rows from a.xsrc): the
+// token warp builds the 8-row fp16 tiles, the epilogue computes the unit's bias corrections from
+// x at the unit's end (4 epilogue warps, named barrier 1) and writes y / the fused SiLU*up.
+template <int PW, int PT, int NA, int NACC, int NI, int GS>
+__global__ void __launch_bounds__(32 * (22 + NI), 1) k_umma_int4p(UmmaArgs a, int n_units) {
+  constexpr int BN = 16, BROWS = 8;
+  // two sets of 8 dequant warps take alternate groups, so one set's TMEM-store round trip
+  // overlaps the other's expansion
+  constexpr int W_DQ = 1 + NI, W_EP = W_DQ + 16, W_TK = W_EP + 4;
+  constexpr int TILE_Q = BM * BK / 2, TB = BROWS * 128;
+  constexpr int WST = GS * 2 * TILE_Q, TST = GS * 2 * TB;
+  constexpr uint32_t ACOL = NI * NACC * BN, TCOLS = 512;
+  static_assert(ACOL + NA * 64 <= 512, "TMEM budget");
+  constexpr int ND0 = GS * PT > NA ? GS * PT : NA;
+  constexpr int ND = ND0 > NI * NACC ? ND0 : NI * NACC;
+  const int S = a.splits, RT = a.rows / BM, kb_total = a.kdim / BK;
+  const int ng_live = *a.n_groups;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int abl = g_k2_ablate;
+  const bool tl = blockIdx.x == 0 && g_int4_tl_arm != 0;
+  const bool tla = g_int4_tl_arm != 0 && blockIdx.x < 256;
+  if (tla && threadIdx.x == 0) {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_int4_tl[1536 + 2 * blockIdx.x] = t;
+  }
+  // unit u -> (g, rt, s, kb0, ngr); identical in every role
+  struct Unit { int g, rt, s, kb0, ngr, e0, m; };
+  auto unit = [&](int u) {
+    Unit x;
+    x.s = u % S;
+    x.rt = (u / S) % RT;
+    x.g = u / (S * RT);
+    int per = (kb_total + S - 1) / S;
+    per = (per + 1) & ~1;
+    x.kb0 = x.s * per;
+    const int nk = max(0, min(kb_total, x.kb0 + per) - x.kb0);
+    x.ngr = x.g < ng_live ? nk / 2 : 0;
+    x.e0 = x.g < ng_live ? a.group_off[x.g] : 0;
+    x.m = x.g < ng_live ? a.group_off[x.g + 1] - x.e0 : 0;
+    return x;
+  };
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  unsigned char* sT = base;           // PT x TST
+  unsigned char* sW = sT + PT * TST;  // PW x WST
+  uint64_t* full_w = reinterpret_cast<uint64_t*>(sW + PW * WST);
+  uint64_t* empty_w = full_w + PW;
+  uint64_t* full_t = empty_w + PW;
+  uint64_t* full_a = full_t + PT;
+  uint64_t* done = full_a + NA;
+  uint64_t* acce = done + ND;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + NI * NACC);
+  __shared__ float csu[256];        // epilogue: per-group corrections of the current unit
+  __shared__ int stage_last[PT];    // token warp: global index of each token stage's last group
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < PW; ++i) {
+      mbar_init(&full_w[i], 1);
+      mbar_init(&empty_w[i], 8 * GS);  // 8 dequant warps per group of the stage
+    }
+    for (int i = 0; i < PT; ++i) mbar_init(&full_t[i], 1);
+    for (int i = 0; i < NA; ++i) mbar_init(&full_a[i], 8);
+    for (int i = 0; i < ND; ++i) mbar_init(&done[i], 1);
+    for (int i = 0; i < NI * NACC; ++i) mbar_init(&acce[i], 4);
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                 "r"(TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {  // weight producer: one bulk copy per stage of GS groups (within a unit)
+    if (lane == 0) {
+      int jw = 0;  // global stage counter
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const Unit x = unit(u);
+        if (x.ngr == 0) continue;
+        const unsigned char* wsrc = a.w_base + ((int64_t)a.expert_base + a.group_buf[x.g]) * a.blob_bytes + a.w_off +
+                                    ((int64_t)x.rt * kb_total + x.kb0) * TILE_Q;
+        const int nst = (x.ngr + GS - 1) / GS;
+        for (int j = 0; j < nst; ++j, ++jw) {
+          if (jw >= PW) K2_WAIT(&empty_w[jw % PW], ((jw / PW) - 1) & 1);
+          tl_mark(tl, 1 + jw);
+          const int cnt = min(GS, x.ngr - j * GS);
+          mbar_expect_tx(&full_w[jw % PW], cnt * 2 * TILE_Q);
+          bulk_g2s(sW + (jw % PW) * WST, wsrc + (int64_t)j * WST, cnt * 2 * TILE_Q, &full_w[jw % PW]);
+        }
+      }
+    }
+  } else if (warp == W_TK) {  // token producer: 8-row fp16 class-scaled tiles from the bf16 row
+    int jt = 0, gdone = 0;  // global token stage / global group index at the stage start
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      const Unit x = unit(u);
+      if (x.ngr == 0) continue;
+      const uint16_t* xr = a.xsrc + (int64_t)(a.xsrc_by_entry ? x.e0 : a.entry_tok[x.e0]) * a.kdim + x.kb0 * BK;
+      const int nst = (x.ngr + GS - 1) / GS;
+      for (int j = 0; j < nst; ++j, ++jt) {
+        const int cnt = min(GS, x.ngr - j * GS);
+        if (jt >= PT) {  // the stage's slot was last read by the groups of global stage jt - PT
+          const int gl = stage_last[(jt - PT) % PT];
+          K2_WAIT(&done[gl % ND], (gl / ND) & 1);
+        }
+        unsigned char* tdst = sT + (jt % PT) * TST;
+#pragma unroll
+        for (int p2 = 0; p2 < (GS * 16 + 31) / 32; ++p2) {
+          const int task = p2 * 32 + lane, kbl = task >> 3, c = task & 7;
+          if (kbl < 2 * cnt) {
+            const uint4 v = *reinterpret_cast<const uint4*>(xr + (int64_t)(j * GS * 2 + kbl) * BK + c * 8);
+            const float mul = c < 4 ? 1.0f : 0.0625f;
+            uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint16_t lo = f2h_bits(bf2f((uint16_t)(w[q] & 0xFFFFu)) * mul);
+              const uint16_t hi = f2h_bits(bf2f((uint16_t)(w[q] >> 16)) * mul);
+              w[q] = (uint32_t)lo | ((uint32_t)hi << 16);
+            }
+            *reinterpret_cast<uint4*>(tdst + kbl * TB + sw128_off(0, c * 8)) = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          stage_last[jt % PT] = gdone + cnt - 1;
+          mbar_arrive(&full_t[jt % PT]);
+        }
+        gdone += cnt;
+      }
+    }
+  } else if (warp < W_DQ) {  // MMA issuers
+    if (lane == 0) {
+      const int is = warp - 1;
+      constexpr uint32_t idesc = idesc_f16(BN);
+      constexpr uint64_t sbo_fix = ~((uint64_t)0x3FFF << 32);  // 8-row tiles: rows 8..15 alias 0..7
+      int gi = 0, js = 0;  // global group, global token stage
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const Unit x = unit(u);
+        for (int gl = 0; gl < x.ngr; ++gl, ++gi) {
+          const int jsg = js + gl / GS;
+          if (gi % NI == is) {
+            const int uu = gi / NI, sl = gi % NA, b = uu % NACC;
+            if (uu >= NACC) K2_WAIT(&acce[is * NACC + b], ((uu / NACC) - 1) & 1);
+            K2_WAIT(&full_t[jsg % PT], (jsg / PT) & 1);
+            K2_WAIT(&full_a[sl], (gi / NA) & 1);
+            tc_fence_after();
+            const uint32_t sb = su32(sT + (jsg % PT) * TST + (gl % GS) * 2 * TB);
+            if (!(abl & 1))
+#pragma unroll
+              for (int kk = 0; kk < 8; ++kk)
+                umma_ts(tmem + (is * NACC + b) * BN, tmem + ACOL + sl * 64 + kk * 8,
+                        (sw128_desc(sb + (kk >> 2) * TB) & sbo_fix) + 2 * (kk & 3), idesc, kk != 0);
+            umma_commit(&done[gi % ND]);
+          }
+        }
+        js += (x.ngr + GS - 1) / GS;
+      }
+    }
+  } else if (warp < W_EP) {  // dequant warps: set ds takes groups gi % 2 == ds; row q*32 + lane, half h
+    const int ds = (warp - W_DQ) >> 3;
+    const int q = warp & 3, h = ((warp - W_DQ) >> 2) & 1;
+    const int r = q * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    int gi = 0, jw = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      const Unit x = unit(u);
+      for (int gl = 0; gl < x.ngr; ++gl, ++gi) {
+        if ((gi & 1) != ds) continue;
+        const int jsw = jw + gl / GS, st = jsw % PW, sl = gi % NA;
+        K2_WAIT(&full_w[st], (jsw / PW) & 1);
+        if (threadIdx.x == 32 * W_DQ) tl_mark(tl, 256 + gi);
+        const uint32_t src = su32(sW + st * WST + ((gl % GS) * 2 + h) * TILE_Q + r * 32);
+        const uint4 w0 = lds128(src), w1 = lds128(src + 16);
+        const uint32_t ws[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+        uint32_t v[32];
+        const uint32_t m_lo = 0x000F000Fu, m_hi = 0x00F000F0u, magic = 0x64006400u;
+#pragma unroll
+        for (int wi = 0; wi < 8; ++wi) {
+          const uint32_t w8 = ws[wi] >> 8;
+          v[2 * wi] = lop3_and_or(ws[wi], m_lo, magic);
+          v[2 * wi + 1] = lop3_and_or(w8, m_lo, magic);
+          v[16 + 2 * wi] = lop3_and_or(ws[wi], m_hi, magic);
+          v[17 + 2 * wi] = lop3_and_or(w8, m_hi, magic);
+        }
+        __syncwarp();
+        if (lane == 0) {  // one arrival per group; the unit's last (short) stage makes up the rest
+          const int cnt = min(GS, x.ngr - (gl / GS) * GS);
+          const uint32_t mult = gl == x.ngr - 1 ? (uint32_t)(GS - cnt + 1) : 1u;
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&empty_w[st])), "r"(mult)
+                       : "memory");
+        }
+        if (gi >= NA) K2_WAIT(&done[(gi - NA) % ND], ((gi - NA) / ND) & 1);
+        tc_fence_after();
+        if (!(abl & 2)) tmem_st32(tmem + lane_base + ACOL + sl * 64 + h * 32, v);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full_a[sl]);
+      }
+      jw += (x.ngr + GS - 1) / GS;
+    }
+  } else if (warp < W_TK) {  // epilogue: per-group scale, per-unit corrections and output
+    const int q = warp & 3, row = q * 32 + lane, et = threadIdx.x - 32 * W_EP;  // et: 0..127
+    int gi = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      const Unit x = unit(u);
+      if (x.g >= ng_live) continue;
+      const uint16_t* sc = reinterpret_cast<const uint16_t*>(a.w_base + ((int64_t)a.expert_base + a.group_buf[x.g]) *
+                                                                            a.blob_bytes + a.s_off) +
+                           ((int64_t)x.rt * (a.kdim / 128) + x.kb0 / 2) * BM + row;
+      // the unit's corrections C_g = sum_k c_k b_k (fp16 b as the token warp builds it), one group
+      // per thread, fixed order; they only need x, so they are ready before the first drain
+      const uint16_t* xr = a.xsrc + (int64_t)(a.xsrc_by_entry ? x.e0 : a.entry_tok[x.e0]) * a.kdim + x.kb0 * BK;
+      {  // thread et: chunk c16 = et % 16 (8 columns) of groups et / 16, + 8, ...; the 16 chunks of a
+         // group are reduced over 16 consecutive lanes in a fixed xor order
+        const int c16 = et & 15, c = c16 & 7;
+        const float mul = c < 4 ? 1.0f : 0.0625f, cc = c < 4 ? 1032.0f : 1152.0f;
+        for (int g0 = 0; g0 < x.ngr; g0 += 8) {
+          const int gg = g0 + (et >> 4);
+          float part = 0.0f;
+          if (gg < x.ngr) {
+            const uint4 v = *reinterpret_cast<const uint4*>(xr + (int64_t)gg * 128 + c16 * 8);
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int q2 = 0; q2 < 4; ++q2) {
+              part = fmaf(cc, h2f_bits(f2h_bits(bf2f((uint16_t)(w[q2] & 0xFFFFu)) * mul)), part);
+              part = fmaf(cc, h2f_bits(f2h_bits(bf2f((uint16_t)(w[q2] >> 16)) * mul)), part);
+            }
+          }
+#pragma unroll
+          for (int o = 1; o < 16; o <<= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+          if (c16 == 0 && gg < x.ngr) csu[gg] = part;
+        }
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      float acc = 0.0f;
+      // the row's scales, SW groups at a time, loaded one batch ahead (a scale load per group on
+      // the drain path held the MMA issuers back through acce)
+      constexpr int SW = 8;
+      float scw[SW], scn[SW];
+#pragma unroll
+      for (int u2 = 0; u2 < SW; ++u2) scn[u2] = u2 < x.ngr ? bf2f(sc[(int64_t)u2 * BM]) : 0.0f;
+      for (int gl = 0; gl < x.ngr; ++gl, ++gi) {
+        const int ab = (gi % NI) * NACC + (gi / NI) % NACC;
+        if (gl % SW == 0) {
+#pragma unroll
+          for (int u2 = 0; u2 < SW; ++u2) {
+            scw[u2] = scn[u2];
+            scn[u2] = gl + SW + u2 < x.ngr ? bf2f(sc[(int64_t)(gl + SW + u2) * BM]) : 0.0f;
+          }
+        }
+        float scale = scw[0];
+#pragma unroll
+        for (int u2 = 1; u2 < SW; ++u2)
+          if (gl % SW == u2) scale = scw[u2];
+        K2_WAIT(&done[gi % ND], (gi / ND) & 1);
+        if (threadIdx.x == 32 * W_EP) tl_mark(tl, 1280 + gi);
+        tc_fence_after();
+        float v[8];
+        tmem_ld8(tmem + ((uint32_t)(q * 32) << 16) + ab * BN, v);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acce[ab]);
+        acc = fmaf(scale, v[0] - csu[gl], acc);
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // csu is rewritten by the next unit
+      if (x.m > 0) {
+        if (a.act_out) {
+          const float up = __shfl_down_sync(0xffffffffu, acc, 1);
+          if ((lane & 1) == 0)
+            a.act_out[(int64_t)x.e0 * (a.rows / 2) + (x.rt * BM + row) / 2] = f2bf(__fmul_rn(silu_det(acc), up));
+        } else {
+          a.out[(int64_t)x.s * a.out_split_stride + (int64_t)x.e0 * a.rows + x.rt * BM + row] = acc;
+        }
+      }
+    }
+    if (tla && threadIdx.x == 32 * W_EP) {
+      long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      g_int4_tl[1537 + 2 * blockIdx.x] = t;
+    }
+    if (tl && threadIdx.x == 32 * W_EP) g_int4_tl_arm = 0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
+  }
+}
+
 // row-major quantised (standard nibble order, scales [rows][cols/128]) -> tile-major INT4 layout
 __global__ void k_tile_int4(const uint32_t* __restrict__ q, const uint16_t* __restrict__ sc, int rows, int cols,
                             uint32_t* __restrict__ tq, uint16_t* __restrict__ ts) {
@@ -810,6 +1109,20 @@ cudaError_t launch_umma_int4(const UmmaArgs& a, int max_groups, int BN, cudaStre
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(32, 4, 2, 2));
     k<<<units, THREADS, smem(32, 4, 2, 2), st>>>(a);
   }
+  return cudaGetLastError();
+}
+
+// Persistent draft-shape K2 (one token per group, 8-row tiles): one CTA per SM.
+cudaError_t launch_umma_int4p(const UmmaArgs& a, int max_groups, cudaStream_t st) {
+  constexpr int PW = 6, PT = 4, NA = 7, NACC = 2, NI = 2, GS = 3, THREADS = 32 * (22 + NI);
+  const int units = max_groups * (a.rows / BM) * a.splits;
+  if (units == 0) return cudaSuccess;
+  static int sms = 0;
+  if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const size_t smem = 1024 + (size_t)PT * GS * 2 * 8 * 128 + (size_t)PW * GS * 2 * (BM * BK / 2) + 64 * 8 + 16;
+  auto k = k_umma_int4p<PW, PT, NA, NACC, NI, GS>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k<<<std::min(units, std::max(sms, 1)), THREADS, smem, st>>>(a, units);
   return cudaGetLastError();
 }
 
