@@ -544,6 +544,17 @@ struct CopyBatch {
   const char* label = "io_new";
 };
 
+// The controller's copy requests are on the critical path of the copy engine (a layer's demand
+// fetches cannot start before the host has read them), so the host polls the event instead of
+// sleeping in cudaEventSynchronize (the blocking-sync wake-up costs tens of microseconds).
+static void spin_wait(cudaEvent_t ev) {
+  for (;;) {
+    const cudaError_t e = cudaEventQuery(ev);
+    if (e == cudaSuccess) return;
+    if (e != cudaErrorNotReady) fail(MSPQ_ERR_CUDA, std::string("cudaEventQuery: ") + cudaGetErrorString(e));
+  }
+}
+
 static int issue_copies(mspq_engine* E, int cycle, CopyBatch& batch, uint64_t& bytes) {
   const int n = E->view.host_stat[S_NREQ];
   if (E->view.host_stat[S_OVERFLOW]) fail(MSPQ_ERR_OVERFLOW, "device controller ran out of buffers / queue");
@@ -573,7 +584,7 @@ static int issue_copies(mspq_engine* E, int cycle, CopyBatch& batch, uint64_t& b
       if (E->stage_rec[sb]) CUDA_OK(cudaStreamWaitEvent(E->sx, E->ev_stage[sb], 0));
       if (reused) CUDA_OK(cudaStreamWaitEvent(E->sdec, E->ev_gemm[E->last_layer[buf]], 0));
       const int nt = E->n_tiles;
-      const int nc = std::max(1, std::min(8, (int)(toff[nt] / (8u << 20))));
+      const int nc = std::max(1, std::min(16, (int)(toff[nt] / (6u << 20))));
       for (int c = 0; c < nc; ++c) {
         const int t0 = (int)((int64_t)nt * c / nc), t1 = (int)((int64_t)nt * (c + 1) / nc);
         const uint32_t b0 = c ? toff[t0] : 0u, b1 = toff[t1];
@@ -581,7 +592,7 @@ static int issue_copies(mspq_engine* E, int cycle, CopyBatch& batch, uint64_t& b
         cudaEvent_t ev = E->pool_event();
         CUDA_OK(cudaEventRecord(ev, E->sx));
         CUDA_OK(cudaStreamWaitEvent(E->sdec, ev, 0));
-        CAPI_OK(mspq_xc_decode(stg, t0, t1, slot, 128, E->sdec));
+        CAPI_OK(mspq_xc_decode(stg, t0, t1, slot, 256, E->sdec));
       }
       CUDA_OK(cudaEventRecord(E->ev_stage[sb], E->sdec));
       E->stage_rec[sb] = 1;
@@ -660,7 +671,7 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
         CUDA_OK(cudaEventRecord(E->ev_g1[i + 1], E->sc));
         launches += E->graph_nodes;
       }
-      CUDA_OK(cudaEventSynchronize(E->ev_row[i]));
+      spin_wait(E->ev_row[i]);
       CopyBatch b;
       issue_copies(E, cycle, b, cyc_bytes);
       if (b.count) batches.push_back(b);
@@ -686,7 +697,7 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
       CUDA_OK(cudaEventRecord(E->ev_w0[l], E->sc));
       CAPI_OK(mspq_build_schedule(tgt, T, K, Ex, E->gbuf, sv.n_groups, sv.group_expert, sv.group_buf, sv.group_off,
                                   sv.entry_tok, sv.entry_of, sv.entry_group, E->sc));
-      CUDA_OK(cudaEventSynchronize(E->ev_w0[l]));
+      spin_wait(E->ev_w0[l]);
       CopyBatch b;
       b.label = "io_new";
       issue_copies(E, cycle, b, cyc_bytes);

@@ -10,7 +10,7 @@ blobs = torch.randint(0, 255, (E * s4,), dtype=torch.uint8, device="cuda")
 ids = torch.tensor([[3, 7]], dtype=torch.int32, device="cuda")
 s = ops.build_schedule(ids, E)
 xn = torch.randint(-3000, 3000, (1, d), dtype=torch.int16, device="cuda")
-sp1, sp2 = int(os.environ.get("SP1", 1)), int(os.environ.get("SP2", 4))
+sp1, sp2 = int(os.environ.get("SP1", 1)), int(os.environ.get("SP2", 2))
 for _ in range(3):
     ops.moe_int4_tc(s, xn, blobs, s4, 0, E, d, f, split1=sp1, split2=sp2)
 torch.cuda.synchronize()
