@@ -210,3 +210,30 @@ def test_generate_full_width_shapes_match_oracle(cuda, name, cap, k):
         assert got == w
     assert rep["total_new_experts"] > 0
     eng.close()
+
+
+def test_shared_host_store_attach_path(cuda, tmp_path):
+    """The multi-rank store (bench.py under torchrun): rank 0 creates and fills a /dev/shm XC store,
+    another engine attaches to it (role 1, no fill) and decodes the same tokens with the same
+    bytes on the link -- the attach path reads the blob sizes from the shared file."""
+    import os
+    import paper_2511_14102_b200 as m
+    cfg = m.ModelConfig.named("tiny")
+    path = "/dev/shm/mspq_test_store_%d" % os.getpid()
+    conf = {"policy": "speculative", "cache_capacity": 3, "k": 3}
+    try:
+        owner = m.Engine(cfg, kmax=8, trace_level=1, host_store_path=path, host_store_role=0)
+        guest = m.Engine(cfg, kmax=8, trace_level=1, host_store_path=path, host_store_role=1)
+        reps = []
+        for eng in (owner, guest):
+            eng.configure(conf)
+            reps.append(eng.generate([3, 9, 27], 20))
+        assert reps[0]["tokens"] == reps[1]["tokens"]
+        assert reps[0]["h2d_bytes"] == reps[1]["h2d_bytes"] > 0
+        assert owner.info()["expert_wire_bytes_mean"] == guest.info()["expert_wire_bytes_mean"]
+        guest.close()
+        owner.close()
+    finally:
+        for p in (path, path + ".ready"):
+            if os.path.exists(p):
+                os.unlink(p)
