@@ -36,6 +36,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "decode tokens/s, Phi-MoE shape, capped expert cache; exposed H2D ms/token"
+CONFIG_NO = {"tiny": 1, "mixtral": 2, "phi": 3, "qwen3": 4}  # BASELINE.json configs[] (1-based)
 
 
 def parse():
@@ -290,7 +291,7 @@ def main():
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": dev_max / a.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (random-init weights from a counter hash, random prompts)",
-        "config": {"workload": f"{a.model}-shaped speculative decode (BASELINE config 3), {a.tokens} tokens/step, "
+        "config": {"workload": f"{a.model}-shaped speculative decode (BASELINE config {CONFIG_NO.get(a.model, '?')}), {a.tokens} tokens/step, "
                                f"per-layer expert cache {cap}/{E}, policy {a.policy}, k={a.k}, INT4 draft, bf16 verify",
                    "shape": {"name": a.model, "L": L, "E": E, "top_k": K, "d": cfgm.d, "ffn": cfgm.f, "vocab": cfgm.V},
                    "cache_capacity_per_layer": cap, "host_store_GB": info["host_store_bytes"] / 1e9,
