@@ -206,18 +206,42 @@ __global__ void __launch_bounds__(256) k_resid_norm_route(RouteArgs a) {
     }
   }
   __syncthreads();
-  if (tid == 0) {
-    int sel[64];
+  // top-k on warp 0: K rounds of a warp argmax over the unused logits (descending, ties -> lower
+  // id: each lane keeps its first maximum in ascending order, the butterfly prefers the lower id
+  // on equal values).  The serial single-thread scan cost ~170 us at E = 128, K = 8.
+  __shared__ int sel[64];
+  __shared__ unsigned int usedm[32];  // E <= 1024
+  if (warp == 0) {
+    usedm[lane] = 0u;
+    __syncwarp();
     for (int j = 0; j < a.K; ++j) {
-      int best = -1;
-      for (int e = 0; e < a.E; ++e) {
-        bool used = false;
-        for (int q = 0; q < j; ++q) used |= (sel[q] == e);
-        if (used) continue;
-        if (best < 0 || lg[e] > lg[best]) best = e;
+      float bv = 0.0f;
+      int bi = -1;
+      for (int e = lane; e < a.E; e += 32) {
+        if ((usedm[e >> 5] >> (e & 31)) & 1u) continue;
+        if (bi < 0 || lg[e] > bv) {
+          bv = lg[e];
+          bi = e;
+        }
       }
-      sel[j] = best;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (oi >= 0 && (bi < 0 || ov > bv || (ov == bv && oi < bi))) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      if (lane == 0) {
+        sel[j] = bi;
+        usedm[bi >> 5] |= 1u << (bi & 31);
+      }
+      __syncwarp();
     }
+  }
+  __syncthreads();
+  if (tid == 0) {
     const float m = lg[sel[0]];
     float ex[64], s = 0.0f;
     for (int j = 0; j < a.K; ++j) {
