@@ -748,9 +748,23 @@ MSPQ_HD size_t stage_bytes_of(int L, int E, int K, int nbuf, int kmax, bool elb)
          2 * al16(n) + al16(n * 4) + al16(n * 8) + al16(L * 4) + (elb ? al16((size_t)kmax * L * K * 4) : 0);
 }
 
+// State copies between global memory and the shared-memory stage: 16-byte vectors, four loads in
+// flight per thread (the element-wise loop was latency-bound: ~50 us each way at L*E = 6144).
+// Both sides are padded to 16 bytes (global arrays to 256), so rounding the byte count up is safe.
 template <class T>
 MSPQ_D void cp(T* dst, const T* src, size_t cnt) {
-  for (size_t i = threadIdx.x; i < cnt; i += blockDim.x) dst[i] = src[i];
+  const size_t n16 = (cnt * sizeof(T) + 15) / 16;
+  uint4* d = reinterpret_cast<uint4*>(dst);
+  const uint4* s = reinterpret_cast<const uint4*>(src);
+  for (size_t i = threadIdx.x; i < n16; i += 4 * (size_t)blockDim.x) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (i + u * blockDim.x < n16) v[u] = s[i + u * blockDim.x];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (i + u * blockDim.x < n16) d[i + u * blockDim.x] = v[u];
+  }
 }
 
 MSPQ_D void stage(const CtlDev& G, CtlDev& S, unsigned char* sm, bool in, bool elb) {
