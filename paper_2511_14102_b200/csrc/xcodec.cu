@@ -267,10 +267,19 @@ __global__ void __launch_bounds__(XC_WARPS * 32, 4) k_xc_decode(const unsigned c
     int wi = 2, bp = 0, cnt = 0;
     uint64_t fifo = 0;
     uint2* d2 = reinterpret_cast<uint2*>(d) + lane;
-    uint32_t smw_next = __ldg(smg);
-    for (int j = 0; j < 64; ++j) {
-      const uint32_t smw = smw_next;
-      if (j + 1 < 64) smw_next = __ldg(smg + 32 * (j + 1));
+    // sign|mantissa words: each step j reads a new 128 B line, so they are fetched 8 steps ahead
+    // (two 8-word register blocks) -- one step ahead left ~64 L2 round trips per tile exposed
+    uint32_t smb0[8], smb1[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) smb0[u] = __ldg(smg + 32 * u);
+#pragma unroll 1
+    for (int jb = 0; jb < 64; jb += 8) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) smb1[u] = jb + 8 < 64 ? __ldg(smg + 32 * (jb + 8 + u)) : 0u;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+      const int j = jb + u;
+      const uint32_t smw = smb0[u];
       while (cnt < 4) {
         const uint32_t win = __funnelshift_l(nxt, cur, bp);
         const uint32_t ent = lut[win >> (32 - XC_LUT_BITS)];
@@ -311,6 +320,9 @@ __global__ void __launch_bounds__(XC_WARPS * 32, 4) k_xc_decode(const unsigned c
         o[q] = ((smb & 0x80u) << 8) | (e << 7) | (smb & 0x7Fu);
       }
       d2[32 * j] = make_uint2(o[0] | (o[1] << 16), o[2] | (o[3] << 16));
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) smb0[u] = smb1[u];
     }
   }
 }
