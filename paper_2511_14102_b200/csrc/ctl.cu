@@ -575,7 +575,16 @@ MSPQ_D void body_replay_cycle(CtlDev C, ReplayTrace tr, int pos, int k_eff, int 
                                    ReplayOut out) {
   const int L = C.L, K = C.K, E = C.E;
   const int64_t rs = (int64_t)L * K;
-  Ctx x{C, {tr.draft + pos * rs, nullptr, tr.gates ? tr.gates + pos * rs : nullptr, k_eff}};
+  // the cycle's ELB rows are read by every Belady next-use scan: keep them in shared memory when
+  // they fit (the serial global-memory scans dominated the replay kernel)
+  __shared__ int elb_sm[4096];
+  const int32_t* elb_src = tr.draft + pos * rs;
+  if ((int64_t)k_eff * rs <= 4096) {
+    for (int i = lane_id(); i < k_eff * rs; i += 32) elb_sm[i] = elb_src[i];
+    __syncwarp();
+    elb_src = elb_sm;
+  }
+  Ctx x{C, {elb_src, nullptr, tr.gates ? tr.gates + pos * rs : nullptr, k_eff}};
   x.emit = false;
   for (int s : {S_NREQ, S_NLOG, S_NPLAN, S_FETCHED, S_DEMAND, S_JIT, S_OVERFLOW}) put(x, s, 0);
   __shared__ unsigned char required[8192];
@@ -584,10 +593,10 @@ MSPQ_D void body_replay_cycle(CtlDev C, ReplayTrace tr, int pos, int k_eff, int 
   const int nwin = (head_pos >= 0 ? 1 : 0) + k_eff;
   auto win_pos = [&](int w) { return head_pos >= 0 ? (w == 0 ? head_pos : pos + w - 1) : pos + w; };
   auto win_row = [&](int w) { return head_pos >= 0 ? w - 1 : w; };
-  if (lane_id() == 0)
-    for (int w = 0; w < nwin; ++w)
-      for (int l = 0; l < L; ++l)
-        for (int j = 0; j < K; ++j) required[l * E + tr.target[(int64_t)win_pos(w) * rs + l * K + j]] = 1;
+  for (int i = lane_id(); i < nwin * L * K; i += 32) {  // idempotent marks: lane-parallel
+    const int w = i / (L * K), r = i - w * (L * K), l = r / K;
+    required[l * E + tr.target[(int64_t)win_pos(w) * rs + r]] = 1;
+  }
   __syncwarp();
 
   // ---- plan_prefetch over the full ELB against the cache as it is now
