@@ -136,6 +136,14 @@ int mspq_moe_bf16_tc(const int32_t* n_groups, const int32_t* group_expert, const
                      const void* xn, const void* pool, long long blob_bytes, int d, int f, int T,
                      int K, int max_groups, int split1, int split2, void* ws, float* y,
                      void* stream);
+/* K3 on a group subset: only the groups g < 256 whose bit is set in gmask8[8] (NULL = all); the
+ * gather of the token images runs when do_gather.  The engine runs the groups whose experts are
+ * resident while the missing ones are still being copied, then the rest (same outputs). */
+int mspq_moe_bf16_tc_part(const int32_t* n_groups, const int32_t* group_expert, const int32_t* group_buf,
+                          const int32_t* group_off, const int32_t* entry_tok, const int32_t* entry_group,
+                          const void* xn, const void* pool, long long blob_bytes, int d, int f, int T,
+                          int K, int max_groups, int split1, int split2, void* ws, float* y,
+                          const uint32_t* gmask8, int do_gather, void* stream);
 /* K2 on tcgen05 (umma.cu k_umma_int4): the INT4 draft FFN over TILE-MAJOR INT4 blobs
  * (mspq_tile_int4), blobs indexed by layer*E + group_buf[g] (= expert id for the draft
  * schedule).  Exact GPTQ-sym dequant: bf16 (q-8) tiles into smem, per-128-column scales in the

@@ -43,6 +43,7 @@ _SIGS = [
     ("mspq_moe_bf16", c_int, [c_void_p] * 9 + [c_ll] + [c_int] * 5 + [c_void_p]),
     ("mspq_moe_bf16_tc_ws_bytes", c_ll, [c_int] * 6),
     ("mspq_moe_bf16_tc", c_int, [c_void_p] * 8 + [c_ll] + [c_int] * 7 + [c_void_p] * 3),
+    ("mspq_moe_bf16_tc_part", c_int, [c_void_p] * 8 + [c_ll] + [c_int] * 7 + [c_void_p] * 3 + [c_int, c_void_p]),
     ("mspq_tile_bf16", c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p]),
     ("mspq_moe_int4_tc", c_int, [c_void_p] * 8 + [c_ll] + [c_int] * 9 + [c_void_p] * 3),
     ("mspq_tile_int4", c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p]),

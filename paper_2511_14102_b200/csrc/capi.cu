@@ -116,12 +116,14 @@ long long mspq_moe_bf16_tc_ws_bytes(int d, int f, int T, int K, int max_groups, 
          al(max_groups * (f / 64) * BN * 128) + al(max_groups * BN * (d / 64) * 4) +
          al(max_groups * BN * (f / 64) * 4);
 }
-int mspq_moe_bf16_tc(const int32_t* n_groups, const int32_t* group_expert, const int32_t* group_buf,
-                     const int32_t* group_off, const int32_t* entry_tok, const int32_t* entry_group,
-                     const void* xn, const void* pool, long long blob_bytes, int d, int f, int T, int K,
-                     int max_groups, int split1, int split2, void* ws, float* y, void* stream) {
+int mspq_moe_bf16_tc_part(const int32_t* n_groups, const int32_t* group_expert, const int32_t* group_buf,
+                          const int32_t* group_off, const int32_t* entry_tok, const int32_t* entry_group,
+                          const void* xn, const void* pool, long long blob_bytes, int d, int f, int T, int K,
+                          int max_groups, int split1, int split2, void* ws, float* y, const uint32_t* gmask8,
+                          int do_gather, void* stream) {
   if (d % 128 || f % 256 || T > 32 || split1 < 1 || split2 < 1)
     return set_error(MSPQ_ERR_SHAPE_MISMATCH, "moe_bf16_tc: d % 128, f % 256, T <= 32, splits >= 1");
+  if (gmask8 && max_groups > 256) return set_error(MSPQ_ERR_SHAPE_MISMATCH, "moe_bf16_tc_part: <= 256 groups");
   const int BN = tc_bn(T);
   const long long N = (long long)T * K;
   auto al = [](long long b) { return (b + 1023) / 1024 * 1024; };
@@ -130,18 +132,35 @@ int mspq_moe_bf16_tc(const int32_t* n_groups, const int32_t* group_expert, const
   unsigned char* b2 = (unsigned char*)p1 + al((long long)split1 * N * 2 * f * 4);
   SchedPtrs s{(int32_t*)n_groups, (int32_t*)group_expert, (int32_t*)group_buf, (int32_t*)group_off,
               (int32_t*)entry_tok, nullptr, (int32_t*)entry_group};
+  GMask gm{};
+  if (gmask8) {
+    for (int i = 0; i < 8; ++i) gm.w[i] = gmask8[i];
+    gm.on = 1;
+  }
   cudaStream_t st = ST(stream);
-  cudaError_t e = launch_gather_b((const uint16_t*)xn, d, s, max_groups, d, BN, b1, st);
-  if (e != cudaSuccess) return cuda_status(e, "gather_b");
+  cudaError_t e = cudaSuccess;
+  if (do_gather) {
+    e = launch_gather_b((const uint16_t*)xn, d, s, max_groups, d, BN, b1, st);
+    if (e != cudaSuccess) return cuda_status(e, "gather_b");
+  }
   UmmaArgs u1{(const unsigned char*)pool, blob_bytes, 0, 2 * f, d, n_groups, group_buf, group_off, b1, p1,
               N * 2 * f, split1};
+  u1.gmask = gm;
   e = launch_umma_grouped(u1, max_groups, BN, st);
   if (e != cudaSuccess) return cuda_status(e, "umma W13");
-  e = launch_finalize_act(p1, split1, N * 2 * f, s, entry_group, (int)N, f, BN, b2, st);
+  e = launch_finalize_act(p1, split1, N * 2 * f, s, entry_group, (int)N, f, BN, b2, st, nullptr, gm);
   if (e != cudaSuccess) return cuda_status(e, "finalize_act");
   UmmaArgs u2{(const unsigned char*)pool, blob_bytes, (long long)2 * f * d * 2, d, f, n_groups, group_buf,
               group_off, b2, y, N * d, split2};
+  u2.gmask = gm;
   CK(launch_umma_grouped(u2, max_groups, BN, st), "umma W2");
+}
+int mspq_moe_bf16_tc(const int32_t* n_groups, const int32_t* group_expert, const int32_t* group_buf,
+                     const int32_t* group_off, const int32_t* entry_tok, const int32_t* entry_group,
+                     const void* xn, const void* pool, long long blob_bytes, int d, int f, int T, int K,
+                     int max_groups, int split1, int split2, void* ws, float* y, void* stream) {
+  return mspq_moe_bf16_tc_part(n_groups, group_expert, group_buf, group_off, entry_tok, entry_group, xn, pool,
+                               blob_bytes, d, f, T, K, max_groups, split1, split2, ws, y, nullptr, 1, stream);
 }
 int mspq_moe_int4_tc(const int32_t* n_groups, const int32_t* group_expert, const int32_t* group_buf,
                      const int32_t* group_off, const int32_t* entry_tok, const int32_t* entry_group,

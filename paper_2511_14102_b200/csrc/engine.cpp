@@ -190,7 +190,8 @@ HostCfg parse_host_cfg(const std::string& text) {
   HostCfg c;
   static const std::set<std::string> known = {"policy", "capacity_mode", "cache_capacity", "entropy_weighted_capacity",
                                               "k", "governor", "phases", "prefetch_budget", "rollback_s", "ema_alpha",
-                                              "initial_accept", "seed", "collect_plans", "profile", "log", "generator"};
+                                              "initial_accept", "seed", "collect_plans", "profile", "log", "generator",
+                                              "verify_overlap"};
   for (auto it = j.begin(); it != j.end(); ++it)
     if (!known.count(it.key())) fail(MSPQ_ERR_INVALID_CONFIG, "unknown key in run config: " + it.key());
   auto num = [&](const json& o, const char* k, double d) {
@@ -240,6 +241,7 @@ HostCfg parse_host_cfg(const std::string& text) {
   c.initial_accept = num(j, "initial_accept", c.initial_accept);
   if (j.contains("collect_plans")) c.collect_plans = j["collect_plans"].get<bool>();
   if (j.contains("log")) c.log = j["log"].get<bool>();
+  if (j.contains("verify_overlap")) c.verify_overlap = j["verify_overlap"].get<bool>();
   if (j.contains("profile")) {
     c.profile = Profile::from_json(j["profile"]);
     c.profile_given = true;

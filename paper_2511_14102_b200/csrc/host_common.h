@@ -55,6 +55,9 @@ struct HostCfg {  // SimConfig (sim.hpp:15-34) from the run-config schema (run_c
   double rollback = 0.0, ema_alpha = 0.1, initial_accept = 0.8;
   bool collect_plans = false;
   bool log = false;  // extension: emit the per-event hit/miss log
+  // extension (live engine): run a verify layer's GEMM for the resident experts while the missing
+  // ones are still on the link (two smaller K3 launches; +4% at cap 14/16, neutral at 4/16)
+  bool verify_overlap = false;
 };
 int parse_policy(const std::string& s);
 const char* policy_name(int p);

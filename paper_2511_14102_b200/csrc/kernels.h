@@ -18,6 +18,16 @@ struct SchedPtrs {
   int32_t* entry_group;   // [N]   group of each entry (nullable)
 };
 
+// Group subset of a grouped GEMM launch (groups < 256): the verify runs the groups whose experts
+// are already resident while the missing ones are still on the link, then the rest.
+struct GMask {
+  uint32_t w[8];
+  int on;
+};
+__host__ __device__ inline bool gmask_has(const GMask& m, int g) {
+  return !m.on || (g < 256 && ((m.w[g >> 5] >> (g & 31)) & 1u));
+}
+
 // tcgen05 grouped GEMM (umma.cu): one matrix (W13 or W2) of every group's expert
 struct UmmaArgs {
   const unsigned char* w_base;  // slot pool of tile-major bf16 expert blobs
@@ -39,6 +49,7 @@ struct UmmaArgs {
   int xsrc_by_entry = 0;           // row of group g = entry_tok[e0] (0) or the entry e0 (1)
   const int32_t* entry_tok = nullptr;
   uint16_t* act_out = nullptr;     // INT4 W13, split 1: fused act = bf16(silu(gate) * up) [N][rows/2]
+  GMask gmask{};                   // K3: only the groups whose bit is set (when gmask.on)
 };
 
 struct ExpertArgs {
@@ -90,7 +101,7 @@ cudaError_t launch_gather_b(const uint16_t* x, int ld, SchedPtrs s, int max_grou
                             unsigned char* img, cudaStream_t st, float* csum = nullptr);
 cudaError_t launch_finalize_act(const float* p1, int splits, int64_t split_stride, SchedPtrs s,
                                 const int32_t* entry_group, int n_entries, int f, int BN, unsigned char* img,
-                                cudaStream_t st, float* csum = nullptr);
+                                cudaStream_t st, float* csum = nullptr, GMask gm = GMask{});
 cudaError_t launch_tile_bf16(const uint16_t* src, int rows, int cols, unsigned char* dst, cudaStream_t st);
 cudaError_t launch_fill_bf16(uint64_t seed, uint64_t tensor, float scale, int kind, uint16_t* out,
                              int64_t n, int64_t start, cudaStream_t st);

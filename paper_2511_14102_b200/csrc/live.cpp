@@ -136,7 +136,8 @@ struct mspq_engine {
   std::vector<cudaEvent_t> ev_ready;
   std::vector<char> ready_rec;
   std::vector<int> last_cycle, last_layer;
-  std::vector<cudaEvent_t> ev_gemm, ev_w0, ev_w1, ev_row, ev_k0, ev_g0, ev_g1;
+  std::vector<cudaEvent_t> ev_gemm, ev_w0, ev_w1, ev_row, ev_k0, ev_g0, ev_g1, ev_ka1;
+  std::vector<char> layer_parts;  // verify layer ran its GEMM in two parts (resident / in flight)
   int graph_nodes = 0;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_pool_next = 0;
@@ -702,28 +703,26 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
       b.label = "io_new";
       issue_copies(E, cycle, b, cyc_bytes);
       if (b.count) batches.push_back(b);
-      // wait for every copy this layer's experts still depend on
+      // the layer's groups (ascending expert = the device schedule's order) split into experts
+      // already resident (part A: their GEMM runs while the copies are still on the link) and
+      // experts whose copy is in flight (part B: after a stream wait on their ready events)
       std::vector<int>& gb = E->layer_bufs;
       gb.clear();
       for (int e = 0; e < Ex; ++e)
         if (E->view.host_sched[1 + e] >= 0) gb.push_back(E->view.host_sched[1 + e]);
       const int ng = (int)gb.size();
-      bool waited = false;
+      uint32_t mA[8] = {0, 0, 0, 0, 0, 0, 0, 0}, mB[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      std::vector<int> pend;
       for (int gi = 0; gi < ng; ++gi) {
         const int buf = gb[gi];
         if (buf < 0 || buf >= E->nbuf) fail(MSPQ_ERR_OVERFLOW, "schedule buffer out of range");
+        bool pending = false;
         if (E->ready_rec[buf]) {
-          if (cudaEventQuery(E->ev_ready[buf]) == cudaErrorNotReady) {
-            CUDA_OK(cudaStreamWaitEvent(E->sc, E->ev_ready[buf], 0));
-            waited = true;
-          } else {
-            E->ready_rec[buf] = 0;
-          }
+          if (cudaEventQuery(E->ev_ready[buf]) == cudaErrorNotReady) pending = true;
+          else E->ready_rec[buf] = 0;
         }
-      }
-      if (waited) {
-        CUDA_OK(cudaEventRecord(E->ev_w1[l], E->sc));
-        stall_ev.push_back({E->ev_w0[l], E->ev_w1[l]});
+        if (pending) pend.push_back(buf);
+        if (gi < 256) (pending ? mB : mA)[gi >> 5] |= 1u << (gi & 31);
       }
       // K splits so each tcgen05 GEMM has >= ~2 CTAs per SM
       auto pick_split = [&](int rows, int kdim) {
@@ -733,9 +732,31 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
       };
       const int sp1 = pick_split(2 * m.f, d), sp2 = pick_split(d, m.f);
       E->yv_splits[l & 1] = sp2;
+      const bool parts = c.verify_overlap && !pend.empty() && (int)pend.size() < ng && ng <= 256;
+      E->layer_parts[l] = parts ? 1 : 0;
+      if (!parts && !pend.empty()) {  // everything waits
+        for (int buf : pend) CUDA_OK(cudaStreamWaitEvent(E->sc, E->ev_ready[buf], 0));
+        CUDA_OK(cudaEventRecord(E->ev_w1[l], E->sc));
+        stall_ev.push_back({E->ev_w0[l], E->ev_w1[l]});
+      }
       CUDA_OK(cudaEventRecord(E->ev_k0[l], E->sc));
-      CAPI_OK(mspq_moe_bf16_tc(sv.n_groups, sv.group_expert, sv.group_buf, sv.group_off, sv.entry_tok, sv.entry_group,
-                               E->xn, E->pool, E->S16, d, m.f, T, K, E->G, sp1, sp2, E->tcws, E->yv[l & 1], E->sc));
+      if (!parts) {
+        CAPI_OK(mspq_moe_bf16_tc(sv.n_groups, sv.group_expert, sv.group_buf, sv.group_off, sv.entry_tok,
+                                 sv.entry_group, E->xn, E->pool, E->S16, d, m.f, T, K, E->G, sp1, sp2, E->tcws,
+                                 E->yv[l & 1], E->sc));
+      } else {
+        CAPI_OK(mspq_moe_bf16_tc_part(sv.n_groups, sv.group_expert, sv.group_buf, sv.group_off, sv.entry_tok,
+                                      sv.entry_group, E->xn, E->pool, E->S16, d, m.f, T, K, E->G, sp1, sp2, E->tcws,
+                                      E->yv[l & 1], mA, 1, E->sc));
+        CUDA_OK(cudaEventRecord(E->ev_ka1[l], E->sc));
+        for (int buf : pend) CUDA_OK(cudaStreamWaitEvent(E->sc, E->ev_ready[buf], 0));
+        CUDA_OK(cudaEventRecord(E->ev_w1[l], E->sc));
+        stall_ev.push_back({E->ev_ka1[l], E->ev_w1[l]});
+        CAPI_OK(mspq_moe_bf16_tc_part(sv.n_groups, sv.group_expert, sv.group_buf, sv.group_off, sv.entry_tok,
+                                      sv.entry_group, E->xn, E->pool, E->S16, d, m.f, T, K, E->G, sp1, sp2, E->tcws,
+                                      E->yv[l & 1], mB, 0, E->sc));
+        launches += 3;
+      }
       CUDA_OK(cudaEventRecord(E->ev_gemm[l], E->sc));
       launches += 7;  // gate_topk, verify_layer, schedule, gather, 2 x tcgen05 GEMM, finalize
       k3_groups += ng;
@@ -790,8 +811,9 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
     const int fetched = E->view.host_stat[S_FETCHED], demand = E->view.host_stat[S_DEMAND];
     const int n_log = E->view.host_stat[S_NLOG];
     for (auto& [a, b] : stall_ev) stall += elapsed_s(a, b);
-    for (int l = 0; l < L; ++l) {
-      const double t = elapsed_s(E->ev_k0[l], E->ev_gemm[l]);
+    for (int l = 0; l < L; ++l) {  // K3 device time, the stream wait between the two parts excluded
+      const double t = E->layer_parts[l] ? elapsed_s(E->ev_k0[l], E->ev_ka1[l]) + elapsed_s(E->ev_w1[l], E->ev_gemm[l])
+                                         : elapsed_s(E->ev_k0[l], E->ev_gemm[l]);
       k3_time += t;
       k3_bytes += (double)layer_groups[l] * E->S16;
     }
@@ -979,7 +1001,8 @@ void destroy(mspq_engine* E) {
   cudaDeviceSynchronize();
   if (E->gexec) cudaGraphExecDestroy(E->gexec);
   if (E->graph) cudaGraphDestroy(E->graph);
-  for (auto v : {&E->ev_ready, &E->ev_gemm, &E->ev_w0, &E->ev_w1, &E->ev_row, &E->ev_pool, &E->ev_k0, &E->ev_g0, &E->ev_g1})
+  for (auto v : {&E->ev_ready, &E->ev_gemm, &E->ev_w0, &E->ev_w1, &E->ev_row, &E->ev_pool, &E->ev_k0, &E->ev_g0, &E->ev_g1,
+                 &E->ev_ka1})
     for (auto ev : *v)
       if (ev) cudaEventDestroy(ev);
   for (auto ev : {E->ev_c0, E->ev_dend, E->ev_end, E->ev_t0})
@@ -1056,7 +1079,9 @@ int mspq_engine_create(const mspq_model_desc* md, const mspq_engine_opts* op, ms
       E->ev_g0.resize(E->Tmax);
       E->ev_g1.resize(E->Tmax);
       E->ev_k0.resize(m.L);
-      for (auto v : {&E->ev_gemm, &E->ev_w0, &E->ev_w1, &E->ev_row, &E->ev_k0, &E->ev_g0, &E->ev_g1})
+      E->ev_ka1.resize(m.L);
+      E->layer_parts.assign(m.L, 0);
+      for (auto v : {&E->ev_gemm, &E->ev_w0, &E->ev_w1, &E->ev_row, &E->ev_k0, &E->ev_g0, &E->ev_g1, &E->ev_ka1})
         for (auto& ev : *v) CUDA_OK(cudaEventCreate(&ev));
       for (auto p : {&E->ev_c0, &E->ev_dend, &E->ev_end, &E->ev_t0}) CUDA_OK(cudaEventCreate(p));
       CUDA_OK(cudaStreamSynchronize(E->sc));

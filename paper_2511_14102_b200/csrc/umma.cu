@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(192, 1) k_umma_grouped(UmmaArgs a) {
   const int S = a.splits, RT = a.rows / BM;
   const int unit = blockIdx.x;
   const int s = unit % S, rt = (unit / S) % RT, g = unit / (S * RT);
-  if (g >= *a.n_groups) return;
+  if (g >= *a.n_groups || !gmask_has(a.gmask, g)) return;
   const int kb_total = a.kdim / BK;
   const int per = (kb_total + S - 1) / S;
   const int kb0 = s * per, nk = max(0, min(kb_total, kb0 + per) - kb0);
@@ -274,11 +274,12 @@ __global__ void k_gather_b(const uint16_t* __restrict__ x, int ld, SchedPtrs s, 
 template <bool F16>
 __global__ void k_finalize_act(const float* __restrict__ p1, int splits, int64_t split_stride, SchedPtrs s,
                                const int32_t* __restrict__ entry_group, int n_entries, int f, int BN,
-                               unsigned char* __restrict__ img, float* __restrict__ csum) {
+                               unsigned char* __restrict__ img, float* __restrict__ csum, GMask gm) {
   __shared__ float wpart[8];
   const int e = blockIdx.y;
   if (e >= s.group_off[*s.n_groups]) return;
   const int g = entry_group[e], t = e - s.group_off[g];
+  if (!gmask_has(gm, g)) return;  // block-uniform
   const int kbt = f / BK;
   for (int i0 = blockIdx.x * blockDim.x; i0 < f; i0 += gridDim.x * blockDim.x) {  // f % 256 == 0
     const int i = i0 + threadIdx.x;
@@ -1159,13 +1160,13 @@ cudaError_t launch_gather_b(const uint16_t* x, int ld, SchedPtrs s, int max_grou
 
 cudaError_t launch_finalize_act(const float* p1, int splits, int64_t split_stride, SchedPtrs s,
                                 const int32_t* entry_group, int n_entries, int f, int BN, unsigned char* img,
-                                cudaStream_t st, float* csum) {
+                                cudaStream_t st, float* csum, GMask gm) {
   if (csum)
     k_finalize_act<true><<<dim3(f / 256, n_entries), 256, 0, st>>>(p1, splits, split_stride, s, entry_group,
-                                                                  n_entries, f, BN, img, csum);
+                                                                  n_entries, f, BN, img, csum, gm);
   else
     k_finalize_act<false><<<dim3(f / 256, n_entries), 256, 0, st>>>(p1, splits, split_stride, s, entry_group,
-                                                                   n_entries, f, BN, img, nullptr);
+                                                                   n_entries, f, BN, img, nullptr, gm);
   return cudaGetLastError();
 }
 

@@ -237,3 +237,21 @@ def test_shared_host_store_attach_path(cuda, tmp_path):
         for p in (path, path + ".ready"):
             if os.path.exists(p):
                 os.unlink(p)
+
+
+def test_verify_overlap_changes_nothing_but_timing(cuda):
+    """verify_overlap runs a layer's GEMM in two parts (resident experts first, in-flight ones
+    after their copies land): tokens, routing and the hit/miss log are unchanged."""
+    import paper_2511_14102_b200 as m
+    cfg = m.ModelConfig.named("tiny")
+    reps = []
+    for ov in (False, True):
+        eng = m.Engine(cfg, kmax=8, trace_level=2)
+        eng.configure({"policy": "speculative", "cache_capacity": 3, "k": 3, "verify_overlap": ov})
+        reps.append(eng.generate([5, 17, 101], 24))
+        eng.close()
+    a, b = reps
+    assert a["tokens"] == b["tokens"]
+    for ca, cb in zip(a["cycles"], b["cycles"]):
+        for key in ["draft_tokens", "target_argmax", "target", "log", "new_experts"]:
+            assert ca[key] == cb[key], key
