@@ -190,10 +190,11 @@ def test_expert_codec_is_lossless_end_to_end(cuda):
     assert b["total_new_experts"] > 0 and b["h2d_bytes"] < 0.72 * a["h2d_bytes"]
 
 
-@pytest.mark.parametrize("name,cap,k", [("phi", 4, 3), ("qwen3", 32, 2)])
+@pytest.mark.parametrize("name,cap,k", [("phi", 4, 3), ("qwen3", 32, 2), ("mixtral", 2, 2)])
 def test_generate_full_width_shapes_match_oracle(cuda, name, cap, k):
     """BASELINE model widths (Phi-3.5-MoE: E=16 top-2 d=4096 ffn=6400 V=32064; Qwen3-30B-A3B:
-    E=128 top-8 d=2048 ffn=768 V=151936) on 2 layers, capped cache, XC host store: every routing
+    E=128 top-8 d=2048 ffn=768 V=151936; Mixtral-8x7B: E=8 top-2 d=4096 ffn=14336 V=32000) on 2
+    layers, capped cache, XC host store: every routing
     trace, draft token, target argmax and committed token equals the CPU oracle's, and the
     hit/miss log equals the control-plane restatement's."""
     eng, cfg = _engine(name, L=2)
