@@ -146,10 +146,13 @@ int mspq_moe_bf16_tc_part(const int32_t* n_groups, const int32_t* group_expert, 
   UmmaArgs u1{(const unsigned char*)pool, blob_bytes, 0, 2 * f, d, n_groups, group_buf, group_off, b1, p1,
               N * 2 * f, split1};
   u1.gmask = gm;
+  if (split1 == 1) u1.act_img = b2;  // SiLU*up in the W13 epilogue, no finalize kernel
   e = launch_umma_grouped(u1, max_groups, BN, st);
   if (e != cudaSuccess) return cuda_status(e, "umma W13");
-  e = launch_finalize_act(p1, split1, N * 2 * f, s, entry_group, (int)N, f, BN, b2, st, nullptr, gm);
-  if (e != cudaSuccess) return cuda_status(e, "finalize_act");
+  if (split1 > 1) {
+    e = launch_finalize_act(p1, split1, N * 2 * f, s, entry_group, (int)N, f, BN, b2, st, nullptr, gm);
+    if (e != cudaSuccess) return cuda_status(e, "finalize_act");
+  }
   UmmaArgs u2{(const unsigned char*)pool, blob_bytes, (long long)2 * f * d * 2, d, f, n_groups, group_buf,
               group_off, b2, y, N * d, split2};
   u2.gmask = gm;

@@ -50,6 +50,7 @@ struct UmmaArgs {
   const int32_t* entry_tok = nullptr;
   uint16_t* act_out = nullptr;     // INT4 W13, split 1: fused act = bf16(silu(gate) * up) [N][rows/2]
   GMask gmask{};                   // K3: only the groups whose bit is set (when gmask.on)
+  unsigned char* act_img = nullptr;  // K3 W13, split 1: fused SiLU*up straight into W2's B images
 };
 
 struct ExpertArgs {

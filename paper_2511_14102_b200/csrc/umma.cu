@@ -208,9 +208,22 @@ __global__ void __launch_bounds__(192, 1) k_umma_grouped(UmmaArgs a) {
     float v[BN];
     tmem_ld16(tmem + ((uint32_t)(q * 32) << 16), v);
     if (BN == 32) tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + 16, v + 16);
+    if (a.act_img) {
+      // W13 with one K split: rows 2i / 2i+1 are gate_i / up_i in adjacent lanes; act =
+      // bf16(silu(gate) * up) goes straight into the W2 B image (k_finalize_act's arithmetic)
+      const int i = row >> 1, kbt2 = (a.rows >> 1) / BK;
+      unsigned char* img = a.act_img + ((int64_t)g * kbt2 + i / BK) * (BN * 128);
 #pragma unroll
-    for (int t = 0; t < BN; ++t)
-      if (t < m) outp[(int64_t)(e0 + t) * a.rows + row] = v[t];
+      for (int t = 0; t < BN; ++t) {
+        const float up = __shfl_down_sync(0xffffffffu, v[t], 1);
+        if (t < m && (lane & 1) == 0)
+          *reinterpret_cast<uint16_t*>(img + sw128_off(t, i % BK)) = f2bf(__fmul_rn(silu_det(v[t]), up));
+      }
+    } else {
+#pragma unroll
+      for (int t = 0; t < BN; ++t)
+        if (t < m) outp[(int64_t)(e0 + t) * a.rows + row] = v[t];
+    }
   }
   tc_fence_before();
   __syncthreads();
