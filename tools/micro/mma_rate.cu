@@ -55,6 +55,42 @@ __global__ void k(long long* out, int iters) {
   __syncthreads();
   if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "r"(128));
 }
+
+// two issuer threads (warp 0 and warp 1, lane 0) in ONE CTA, TS mode, separate accumulators
+__global__ void k2iss(long long* out, int iters) {
+  __shared__ __align__(1024) unsigned char sm[16384];
+  __shared__ uint64_t bar[2];
+  __shared__ uint32_t slot;
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&slot)), "r"(128));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar[1])));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  for (int i = threadIdx.x; i < 16384 / 4; i += blockDim.x) ((uint32_t*)sm)[i] = 0;
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  uint32_t tm = slot;
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0 && w < 2) {
+    const uint64_t db = desc(su32(sm));
+    long long t0 = clock64();
+    for (int i = 0; i < iters; ++i)
+      asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tm + w * 16), "r"(tm + 64 + 8 * (i & 7)), "l"(db + 2 * (i & 3)), "r"(idesc(16)), "r"((uint32_t)(i >= 4)));
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar[w])));
+    uint32_t ok = 0;
+    while (!ok) asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(su32(&bar[w])));
+    out[w] = clock64() - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "r"(128));
+}
 template <int N, int MODE>
 void run(const char* name) {
   long long* d;
@@ -84,6 +120,17 @@ void run_grid(const char* name, int grid) {
   cudaFree(d);
 }
 int main() {
+  {
+    long long* d;
+    cudaMalloc(&d, 16);
+    for (int rep = 0; rep < 2; ++rep) {
+      k2iss<<<1, 64>>>(d, 1024);
+      long long h[2];
+      cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+      printf("TS two issuers in one CTA: %.1f / %.1f cyc per MMA per issuer (%s)\n", h[0] / 1024.0, h[1] / 1024.0,
+             cudaGetErrorString(cudaGetLastError()));
+    }
+  }
   run<16, 0>("SS 1acc");
   run<16, 4>("SS commit8");
   run_grid<16, 0>("SS 1acc", 148);
