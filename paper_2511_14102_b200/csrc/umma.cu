@@ -907,6 +907,7 @@ __global__ void __launch_bounds__(32 * (22 + NI), 1) k_umma_int4p(UmmaArgs a, in
             if (uu >= NACC) K2_WAIT(&acce[is * NACC + b], ((uu / NACC) - 1) & 1);
             K2_WAIT(&full_t[jsg % PT], (jsg / PT) & 1);
             K2_WAIT(&full_a[sl], (gi / NA) & 1);
+            tl_mark(tl, 768 + gi);
             tc_fence_after();
             const uint32_t sb = su32(sT + (jsg % PT) * TST + (gl % GS) * 2 * TB);
             if (!(abl & 1))
@@ -932,7 +933,7 @@ __global__ void __launch_bounds__(32 * (22 + NI), 1) k_umma_int4p(UmmaArgs a, in
         if ((gi & 1) != ds) continue;
         const int jsw = jw + gl / GS, st = jsw % PW, sl = gi % NA;
         K2_WAIT(&full_w[st], (jsw / PW) & 1);
-        if (threadIdx.x == 32 * W_DQ) tl_mark(tl, 256 + gi);
+        if (threadIdx.x == 32 * W_DQ || threadIdx.x == 32 * (W_DQ + 8)) tl_mark(tl, 256 + gi);
         const uint32_t src = su32(sW + st * WST + ((gl % GS) * 2 + h) * TILE_Q + r * 32);
         const uint4 w0 = lds128(src), w1 = lds128(src + 16);
         const uint32_t ws[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
@@ -959,6 +960,7 @@ __global__ void __launch_bounds__(32 * (22 + NI), 1) k_umma_int4p(UmmaArgs a, in
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&full_a[sl]);
+        if (threadIdx.x == 32 * W_DQ || threadIdx.x == 32 * (W_DQ + 8)) tl_mark(tl, 512 + gi);
       }
       jw += (x.ngr + GS - 1) / GS;
     }
