@@ -263,8 +263,14 @@ __global__ void __launch_bounds__(XC_WARPS * 32, 4) k_xc_decode(const unsigned c
     const uint32_t* ws = reinterpret_cast<const uint32_t*>(tb + XC_THDR + XC_VALS) +
                          __ldg(reinterpret_cast<const uint16_t*>(tb + 16) + lane);
     const uint32_t* smg = reinterpret_cast<const uint32_t*>(tb + XC_THDR) + lane;
-    uint32_t cur = __ldg(ws), nxt = __ldg(ws + 1);
-    int wi = 2, bp = 0, cnt = 0;
+    // the lane's bit stream: two live words plus two loaded ahead (each refill's L2 latency used to
+    // stall the next word crossing)
+    // (reads stay inside the tile's stream area: words past its end come back as 0)
+    const uint32_t* wbase = reinterpret_cast<const uint32_t*>(tb + XC_THDR + XC_VALS);
+    const int wend = (int)__ldg(reinterpret_cast<const uint32_t*>(tb) + 1) - (int)(ws - wbase);
+    auto wload = [&](int i) { return i < wend ? __ldg(ws + i) : 0u; };
+    uint32_t cur = wload(0), nxt = wload(1), q2 = wload(2), q3 = wload(3);
+    int wi = 4, bp = 0, cnt = 0;
     uint64_t fifo = 0;
     uint2* d2 = reinterpret_cast<uint2*>(d) + lane;
     // sign|mantissa words: each step j reads a new 128 B line, so they are fetched 8 steps ahead
@@ -307,7 +313,9 @@ __global__ void __launch_bounds__(XC_WARPS * 32, 4) k_xc_decode(const unsigned c
         if (bp >= 32) {
           bp -= 32;
           cur = nxt;
-          nxt = __ldg(ws + wi++);
+          nxt = q2;
+          q2 = q3;
+          q3 = wload(wi++);
         }
       }
       const uint32_t ew = (uint32_t)fifo;
