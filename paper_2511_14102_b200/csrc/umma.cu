@@ -547,9 +547,9 @@ __global__ void __launch_bounds__(32 * (14 + NI), 2) k_umma_int4(UmmaArgs a) {
     };
     if (selfg) load_x(0);
     for (int jt = 0; jt < nst; ++jt) {
-      if (jt >= PT) {
-        const int gl = min(GS * (jt - PT) + GS - 1, ngr - 1);  // last group of stage jt - PT
-        K2_WAIT(&done[gl % ND], (gl / ND) & 1);
+      if (jt >= PT) {  // every group of stage jt - PT (the MMA issuers complete out of order)
+        const int gl = min(GS * (jt - PT) + GS - 1, ngr - 1);
+        for (int gw = GS * (jt - PT); gw <= gl; ++gw) K2_WAIT(&done[gw % ND], (gw / ND) & 1);
       }
       const int cnt = min(GS, ngr - jt * GS);
       unsigned char* tdst = sT + (jt % PT) * TST;
@@ -814,6 +814,7 @@ __global__ void __launch_bounds__(32 * (22 + NI), 1) k_umma_int4p(UmmaArgs a, in
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + NI * NACC);
   __shared__ float csu[256];        // epilogue: per-group corrections of the current unit
   __shared__ int stage_last[PT];    // token warp: global index of each token stage's last group
+  __shared__ int stage_first[PT];   //              ... and first group
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < PW; ++i) {
       mbar_init(&full_w[i], 1);
@@ -862,9 +863,10 @@ __global__ void __launch_bounds__(32 * (22 + NI), 1) k_umma_int4p(UmmaArgs a, in
       const int nst = (x.ngr + GS - 1) / GS;
       for (int j = 0; j < nst; ++j, ++jt) {
         const int cnt = min(GS, x.ngr - j * GS);
-        if (jt >= PT) {  // the stage's slot was last read by the groups of global stage jt - PT
-          const int gl = stage_last[(jt - PT) % PT];
-          K2_WAIT(&done[gl % ND], (gl / ND) & 1);
+        if (jt >= PT) {  // the slot was last read by every group of global stage jt - PT; with
+                         // several MMA issuers their completions are not ordered, so wait on each
+          const int glast = stage_last[(jt - PT) % PT], gfirst = stage_first[(jt - PT) % PT];
+          for (int gw = gfirst; gw <= glast; ++gw) K2_WAIT(&done[gw % ND], (gw / ND) & 1);
         }
         unsigned char* tdst = sT + (jt % PT) * TST;
 #pragma unroll
@@ -886,6 +888,7 @@ __global__ void __launch_bounds__(32 * (22 + NI), 1) k_umma_int4p(UmmaArgs a, in
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
+          stage_first[jt % PT] = gdone;
           stage_last[jt % PT] = gdone + cnt - 1;
           mbar_arrive(&full_t[jt % PT]);
         }
@@ -1130,7 +1133,7 @@ cudaError_t launch_umma_int4(const UmmaArgs& a, int max_groups, int BN, cudaStre
 
 // Persistent draft-shape K2 (one token per group, 8-row tiles): one CTA per SM.
 cudaError_t launch_umma_int4p(const UmmaArgs& a, int max_groups, cudaStream_t st) {
-  constexpr int PW = 6, PT = 4, NA = 7, NACC = 2, NI = 2, GS = 3, THREADS = 32 * (22 + NI);
+  constexpr int PW = 6, PT = 4, NA = 6, NACC = 2, NI = 4, GS = 3, THREADS = 32 * (22 + NI);
   const int units = max_groups * (a.rows / BM) * a.splits;
   if (units == 0) return cudaSuccess;
   static int sms = 0;
