@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--unique", type=int, default=0, help="distinct expert payloads (0 = all)")
     ap.add_argument("--codec", default="xc", choices=["xc", "none"],
                     help="host-store format of the bf16 experts: xc = lossless exponent-coded (default)")
+    ap.add_argument("--verify-overlap", action="store_true",
+                    help="run the verify GEMM of resident experts while a layer's copies are in flight")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--out", default="")
     return ap.parse_args()
@@ -237,6 +239,8 @@ def main():
                    host_store_role=0 if rank == 0 else 1, trace_level=0, expert_codec=a.codec)
     t_create = time.perf_counter() - t_create
     conf = {"policy": a.policy, "cache_capacity": cap}
+    if a.verify_overlap:
+        conf["verify_overlap"] = True
     if a.k == "governor":
         conf.update(k="governor", governor={"k_min": 1, "k_max": 16, "k_slo": 16})
     else:

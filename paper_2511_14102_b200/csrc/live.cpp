@@ -585,9 +585,15 @@ static int issue_copies(mspq_engine* E, int cycle, CopyBatch& batch, uint64_t& b
       if (E->stage_rec[sb]) CUDA_OK(cudaStreamWaitEvent(E->sx, E->ev_stage[sb], 0));
       if (reused) CUDA_OK(cudaStreamWaitEvent(E->sdec, E->ev_gemm[E->last_layer[buf]], 0));
       const int nt = E->n_tiles;
-      const int nc = std::max(1, std::min(16, (int)(toff[nt] / (6u << 20))));
+      // ~24 MB chunks: a pinned H2D chunk pays a fixed start cost (tools/h2d_chunks.py: 54.9 GB/s at
+      // 4 x 25 MB vs 53.6 at 16 x 6 MB), while the exposed tail is one tile per decode warp either way
+      // The last chunk is a small one (1/32 of the tiles), so less decode work is left once the link
+      // goes quiet.
+      const int nm = std::max(1, std::min(8, (int)(toff[nt] / (24u << 20))));
+      const int tail = nm > 1 ? nt / 32 : 0, nc = nm + (tail ? 1 : 0);
       for (int c = 0; c < nc; ++c) {
-        const int t0 = (int)((int64_t)nt * c / nc), t1 = (int)((int64_t)nt * (c + 1) / nc);
+        const int t0 = c < nm ? (int)((int64_t)(nt - tail) * c / nm) : nt - tail;
+        const int t1 = c < nm ? (int)((int64_t)(nt - tail) * (c + 1) / nm) : nt;
         const uint32_t b0 = c ? toff[t0] : 0u, b1 = toff[t1];
         CUDA_OK(cudaMemcpyAsync(stg + b0, hb + b0, b1 - b0, cudaMemcpyHostToDevice, E->sx));
         cudaEvent_t ev = E->pool_event();
@@ -902,6 +908,13 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
       }
       rec["elb"] = elb;
       rec["elb_gates"] = gates;
+      // per verify layer (s from the run start): controller done, GEMM start (after any wait on
+      // in-flight copies), GEMM end
+      json lt = json::array();
+      for (int l = 0; l < L; ++l)
+        lt.push_back({elapsed_s(E->ev_t0, E->ev_w0[l]), elapsed_s(E->ev_t0, E->ev_k0[l]),
+                      elapsed_s(E->ev_t0, E->ev_gemm[l])});
+      rec["layer_times"] = lt;
     }
     if (level >= 2) {
       const int nl = std::min(n_log, E->view.log_cap);
