@@ -841,6 +841,7 @@ MSPQ_D void flush_requests(const CtlDev& G, const CtlDev& S) {
 #define CTL_KERNEL(NAME, BODY, ELB, PARAMS, ARGS)                   \
   template <bool STAGED>                                            \
   __global__ void __launch_bounds__(256) NAME PARAMS {              \
+    pdl_enter(); /* launched with launch_pdl (kernels.h) */         \
     extern __shared__ __align__(16) unsigned char ctl_sm[];         \
     CtlDev S = C;                                                   \
     if constexpr (STAGED) {                                         \
@@ -894,12 +895,12 @@ static size_t prep(K kern, const CtlDev& C, bool elb) {
   if (b > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b);
   return b;
 }
-#define CTL_LAUNCH(KERN, ELB, ...)                                              \
-  do {                                                                          \
-    if (C.stage)                                                                \
-      KERN<true><<<1, 256, prep(KERN<true>, C, ELB), st>>>(__VA_ARGS__);        \
-    else                                                                        \
-      KERN<false><<<1, 32, 0, st>>>(__VA_ARGS__);                               \
+#define CTL_LAUNCH(KERN, ELB, ...)                                                          \
+  do {                                                                                      \
+    cudaError_t e_ = C.stage ? launch_pdl(KERN<true>, dim3(1), dim3(256), prep(KERN<true>, C, ELB), \
+                                          st, __VA_ARGS__)                                  \
+                             : launch_pdl(KERN<false>, dim3(1), dim3(32), 0, st, __VA_ARGS__);     \
+    if (e_ != cudaSuccess) return e_;                                                       \
   } while (0)
 cudaError_t ctl_begin_cycle(const CtlDev& C, int k, cudaStream_t st) {
   CTL_LAUNCH(k_ctl_begin_cycle, true, C, k);

@@ -102,6 +102,7 @@ __global__ void k_embed(const uint16_t* __restrict__ embed, const uint16_t* __re
 
 
 __global__ void __launch_bounds__(256) k_resid_norm_route(RouteArgs a) {
+  pdl_enter();  // launched with launch_pdl (kernels.h)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint16_t* xs = reinterpret_cast<uint16_t*>(smem_raw);                  // d bf16
   float* lg = reinterpret_cast<float*>(smem_raw + a.d * 2);              // E floats
@@ -300,6 +301,7 @@ __global__ void __launch_bounds__(256) k_resid_norm_route(RouteArgs a) {
 // give group and entry offsets.  gbuf (verify) supplies each group's HBM slot-pool buffer.
 __global__ void __launch_bounds__(1024) k_build_schedule(const int32_t* __restrict__ ids, int T, int K, int E,
                                                          const int32_t* __restrict__ gbuf, SchedPtrs s) {
+  pdl_enter();  // launched with launch_pdl (kernels.h)
   __shared__ int sid[4096];
   __shared__ int wsum[2][32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
@@ -750,15 +752,13 @@ cudaError_t launch_route(const RouteArgs& a, int T, cudaStream_t st) {
   size_t smem = (size_t)a.d * 2 + (size_t)a.E * 4;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_resid_norm_route, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_resid_norm_route<<<T, 256, smem, st>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(k_resid_norm_route, dim3(T), dim3(256), smem, st, a);
 }
 
 cudaError_t launch_build_schedule(const int32_t* ids, int T, int K, int E, const int32_t* gbuf,
                                   SchedPtrs s, cudaStream_t st) {
   const int threads = std::max(32, (E + 31) / 32 * 32);
-  k_build_schedule<<<1, threads, 0, st>>>(ids, T, K, E, gbuf, s);
-  return cudaGetLastError();
+  return launch_pdl(k_build_schedule, dim3(1), dim3(threads), 0, st, ids, T, K, E, gbuf, s);
 }
 
 cudaError_t launch_expert(const ExpertArgs& a, bool int4, int max_groups, int max_group_size,

@@ -130,10 +130,7 @@ MSPQ_HD int sw128_off(int row, int col) {
 
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(192, 1) k_umma_grouped(UmmaArgs a) {
-  // Programmatic dependent launch: this grid may be resident before its predecessor finishes
-  // (launch_pdl); nothing is read before the wait, so every input is the predecessor's final state.
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;");
+  pdl_enter();  // launched with launch_pdl (kernels.h)
   const int S = a.splits, RT = a.rows / BM;
   const int unit = blockIdx.x;
   const int s = unit % S, rt = (unit / S) % RT, g = unit / (S * RT);
@@ -255,7 +252,7 @@ MSPQ_D float h2f_bits(uint16_t b) { return __half2float(*reinterpret_cast<const 
 template <bool F16>
 __global__ void k_gather_b(const uint16_t* __restrict__ x, int ld, SchedPtrs s, int kdim, int BN,
                            unsigned char* __restrict__ img, float* __restrict__ csum) {
-  asm volatile("griddepcontrol.launch_dependents;");
+  pdl_enter();
   const int kb = blockIdx.x, g = blockIdx.y;
   if (g >= *s.n_groups) return;
   const int e0 = s.group_off[g], m = s.group_off[g + 1] - e0;
@@ -1094,24 +1091,9 @@ __global__ void k_tile_int4(const uint32_t* __restrict__ q, const uint16_t* __re
 
 }  // namespace
 
-// Launch with programmatic stream serialization: the grid's CTAs are scheduled while the previous
-// kernel on the stream drains (once all its CTAs ran griddepcontrol.launch_dependents) and block in
-// griddepcontrol.wait, so the launch latency between the verify's back-to-back kernels is hidden.
-// MSPQ_NO_PDL=1 launches plainly (A/B timing).
-template <typename Kern>
-static cudaError_t launch_pdl(Kern kern, int grid, int block, size_t smem, cudaStream_t st, const UmmaArgs& a) {
+bool pdl_disabled() {
   static const bool off = getenv("MSPQ_NO_PDL") && atoi(getenv("MSPQ_NO_PDL")) != 0;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(block);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = off ? 0 : 1;
-  return cudaLaunchKernelEx(&cfg, kern, a);
+  return off;
 }
 
 cudaError_t launch_umma_grouped(const UmmaArgs& a, int max_groups, int BN, cudaStream_t st) {
@@ -1121,11 +1103,11 @@ cudaError_t launch_umma_grouped(const UmmaArgs& a, int max_groups, int BN, cudaS
   if (BN == 16) {
     const size_t smem = 1024 + STAGES * (TILE_A + 16 * 128) + (2 * STAGES + 2) * 8 + 16;
     cudaFuncSetAttribute(k_umma_grouped<16, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    return launch_pdl(k_umma_grouped<16, STAGES>, units, 192, smem, st, a);
+    return launch_pdl(k_umma_grouped<16, STAGES>, dim3(units), dim3(192), smem, st, a);
   }
   const size_t smem = 1024 + STAGES * (TILE_A + 32 * 128) + (2 * STAGES + 2) * 8 + 16;
   cudaFuncSetAttribute(k_umma_grouped<32, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  return launch_pdl(k_umma_grouped<32, STAGES>, units, 192, smem, st, a);
+  return launch_pdl(k_umma_grouped<32, STAGES>, dim3(units), dim3(192), smem, st, a);
 }
 
 cudaError_t launch_umma_int4(const UmmaArgs& a, int max_groups, int BN, cudaStream_t st) {
@@ -1194,9 +1176,10 @@ cudaError_t launch_tile_int4(const uint32_t* q, const uint16_t* s, int rows, int
 cudaError_t launch_gather_b(const uint16_t* x, int ld, SchedPtrs s, int max_groups, int kdim, int BN,
                             unsigned char* img, cudaStream_t st, float* csum) {
   if (csum)
-    k_gather_b<true><<<dim3(kdim / BK, max_groups), 128, 0, st>>>(x, ld, s, kdim, BN, img, csum);
+    return launch_pdl(k_gather_b<true>, dim3(kdim / BK, max_groups), dim3(128), 0, st, x, ld, s, kdim, BN, img, csum);
   else
-    k_gather_b<false><<<dim3(kdim / BK, max_groups), 128, 0, st>>>(x, ld, s, kdim, BN, img, nullptr);
+    return launch_pdl(k_gather_b<false>, dim3(kdim / BK, max_groups), dim3(128), 0, st, x, ld, s, kdim, BN, img,
+                      (float*)nullptr);
   return cudaGetLastError();
 }
 
