@@ -136,7 +136,7 @@ struct mspq_engine {
   std::vector<cudaEvent_t> ev_ready;
   std::vector<char> ready_rec;
   std::vector<int> last_cycle, last_layer;
-  std::vector<cudaEvent_t> ev_gemm, ev_w0, ev_w1, ev_row, ev_k0, ev_g0, ev_g1, ev_ka1;
+  std::vector<cudaEvent_t> ev_gemm, ev_w0, ev_w1, ev_row, ev_k0, ev_g0, ev_g1, ev_ka1, ev_rt;
   std::vector<char> layer_parts;  // verify layer ran its GEMM in two parts (resident / in flight)
   int graph_nodes = 0;
   std::vector<cudaEvent_t> ev_pool;
@@ -700,6 +700,7 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
                              E->router + (size_t)l * Ex * d, E->xn, tgt, E->wts_t + (size_t)l * T * K, nullptr, nullptr,
                              nullptr, nullptr, nullptr, l, L, T, d, Ex, K, m.eps, E->sc));
       Sched& sv = E->sv[l & 1];
+      if (level >= 1) CUDA_OK(cudaEventRecord(E->ev_rt[l], E->sc));
       CAPI_OK(mspq_cache_verify_layer(E->cache, l, T, tgt, E->gbuf, E->sc));
       CUDA_OK(cudaEventRecord(E->ev_w0[l], E->sc));
       CAPI_OK(mspq_build_schedule(tgt, T, K, Ex, E->gbuf, sv.n_groups, sv.group_expert, sv.group_buf, sv.group_off,
@@ -909,11 +910,11 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
       rec["elb"] = elb;
       rec["elb_gates"] = gates;
       // per verify layer (s from the run start): controller done, GEMM start (after any wait on
-      // in-flight copies), GEMM end
+      // in-flight copies), GEMM end, K1 (route) done
       json lt = json::array();
       for (int l = 0; l < L; ++l)
         lt.push_back({elapsed_s(E->ev_t0, E->ev_w0[l]), elapsed_s(E->ev_t0, E->ev_k0[l]),
-                      elapsed_s(E->ev_t0, E->ev_gemm[l])});
+                      elapsed_s(E->ev_t0, E->ev_gemm[l]), elapsed_s(E->ev_t0, E->ev_rt[l])});
       rec["layer_times"] = lt;
     }
     if (level >= 2) {
@@ -1015,7 +1016,7 @@ void destroy(mspq_engine* E) {
   if (E->gexec) cudaGraphExecDestroy(E->gexec);
   if (E->graph) cudaGraphDestroy(E->graph);
   for (auto v : {&E->ev_ready, &E->ev_gemm, &E->ev_w0, &E->ev_w1, &E->ev_row, &E->ev_pool, &E->ev_k0, &E->ev_g0, &E->ev_g1,
-                 &E->ev_ka1})
+                 &E->ev_ka1, &E->ev_rt})
     for (auto ev : *v)
       if (ev) cudaEventDestroy(ev);
   for (auto ev : {E->ev_c0, E->ev_dend, E->ev_end, E->ev_t0})
@@ -1093,8 +1094,9 @@ int mspq_engine_create(const mspq_model_desc* md, const mspq_engine_opts* op, ms
       E->ev_g1.resize(E->Tmax);
       E->ev_k0.resize(m.L);
       E->ev_ka1.resize(m.L);
+      E->ev_rt.resize(m.L);
       E->layer_parts.assign(m.L, 0);
-      for (auto v : {&E->ev_gemm, &E->ev_w0, &E->ev_w1, &E->ev_row, &E->ev_k0, &E->ev_g0, &E->ev_g1, &E->ev_ka1})
+      for (auto v : {&E->ev_gemm, &E->ev_w0, &E->ev_w1, &E->ev_row, &E->ev_k0, &E->ev_g0, &E->ev_g1, &E->ev_ka1, &E->ev_rt})
         for (auto& ev : *v) CUDA_OK(cudaEventCreate(&ev));
       for (auto p : {&E->ev_c0, &E->ev_dend, &E->ev_end, &E->ev_t0}) CUDA_OK(cudaEventCreate(p));
       CUDA_OK(cudaStreamSynchronize(E->sc));

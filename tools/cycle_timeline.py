@@ -31,8 +31,9 @@ for c in rep["cycles"][:4]:
           f"copies busy {busy * 1e3:.2f} ms ({busy / span:.3f}), fetched {c['new_experts']}, batches {len(io)}")
     lt = np.array(c["layer_times"]) - t0
     ends = [b for _, b in io]
-    for l, (w0, k0, ge) in enumerate(lt):
+    for l, (w0, k0, ge, rt) in enumerate(lt):
         prev = lt[l - 1][2] if l else dr["start_s"] + dr["duration_s"] - t0
-        print(f"  L{l:2d} ctl-done {w0 * 1e3:8.3f}  (+{(w0 - prev) * 1e6:6.0f} us after prev GEMM)  "
+        print(f"  L{l:2d} ctl-done {w0 * 1e3:8.3f}  (+{(w0 - prev) * 1e6:6.0f} us after prev GEMM: "
+              f"route {(rt - prev) * 1e6:4.0f}, ctl {(w0 - rt) * 1e6:4.0f})  "
               f"gemm start {k0 * 1e3:8.3f}  gemm {(ge - k0) * 1e6:6.0f} us")
     print("  io batches (ms):", [(round((a - t0) * 1e3, 2), round((b - t0) * 1e3, 2)) for a, b in io])
