@@ -271,12 +271,12 @@ MSPQ_D bool policy_step(const Ctx& x, int key, int now, int tag) {
   return hit;
 }
 
+// The host reads the mapped counters only after the launch's event has completed, which makes
+// the kernel's writes visible, so no system-scope fence is needed here (it cost ~2 us per launch).
 MSPQ_D void publish(const Ctx& x) {
   __syncwarp();
-  if (lane_id() == 0 && x.C.hstat) {
-    for (int i = 0; i < S_COUNT; ++i) ((volatile int*)x.C.hstat)[i] = V(x.C.scal)[i];
-    __threadfence_system();
-  }
+  if (x.C.hstat)
+    for (int i = lane_id(); i < S_COUNT; i += 32) ((volatile int*)x.C.hstat)[i] = V(x.C.scal)[i];
   __syncwarp();
 }
 
@@ -494,6 +494,14 @@ MSPQ_D void body_verify_layer(CtlDev C, int l, int nslots, const int32_t* __rest
   Ctx x{C, {C.elb_ids, C.elb_gates, nullptr, k}};
   const int E = C.E, K = C.K, L = C.L;
   __shared__ int gbuf[1024];
+  // the layer's targets come from K1 in global memory; one warp-wide load instead of lane 0's
+  // serial reads
+  __shared__ int tgt_sm[1024];
+  if (nslots * K <= 1024) {
+    for (int i = lane_id(); i < nslots * K; i += 32) tgt_sm[i] = tgt[i];
+    __syncwarp();
+    tgt = tgt_sm;
+  }
   x.gb = gbuf;
   x.step_layer = l;
   put(x, S_NREQ, 0);
@@ -757,23 +765,42 @@ MSPQ_HD size_t stage_bytes_of(int L, int E, int K, int nbuf, int kmax, bool elb)
          2 * al16(n) + al16(n * 4) + al16(n * 8) + al16(L * 4) + (elb ? al16((size_t)kmax * L * K * 4) : 0);
 }
 
-// State copies between global memory and the shared-memory stage: 16-byte vectors, four loads in
-// flight per thread (the element-wise loop was latency-bound: ~50 us each way at L*E = 6144).
-// Both sides are padded to 16 bytes (global arrays to 256), so rounding the byte count up is safe.
-template <class T>
-MSPQ_D void cp(T* dst, const T* src, size_t cnt) {
-  const size_t n16 = (cnt * sizeof(T) + 15) / 16;
-  uint4* d = reinterpret_cast<uint4*>(dst);
-  const uint4* s = reinterpret_cast<const uint4*>(src);
-  for (size_t i = threadIdx.x; i < n16; i += 4 * (size_t)blockDim.x) {
-    uint4 v[4];
+// State copies between global memory and the shared-memory stage use 16-byte vectors. Both sides
+// are padded to 16 bytes (global arrays to 256), so rounding the byte count up is safe.
+// Several arrays in one pass: every thread issues up to 8 independent 16-byte loads before its
+// stores, so the whole stage costs ~2 memory round trips instead of one or more per array (the
+// per-array loop spent ~8 us in and ~6 us out of a ~32 us verify-layer launch).
+struct StageSeg {
+  void* d;
+  const void* s;
+  int n16;
+};
+template <int NS>
+MSPQ_D void cp_multi(const StageSeg (&sg)[NS], int ns) {
+  int total = 0;
+  for (int i = 0; i < ns; ++i) total += sg[i].n16;
+  for (int base = threadIdx.x; base < total; base += 8 * (int)blockDim.x) {
+    uint4 v[8];
+    uint4* dp[8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (i + u * blockDim.x < n16) v[u] = s[i + u * blockDim.x];
+    for (int u = 0; u < 8; ++u) {
+      int idx = base + u * (int)blockDim.x;
+      dp[u] = nullptr;
+      if (idx < total) {
+        int i = 0;
+        while (idx >= sg[i].n16) idx -= sg[i++].n16;
+        v[u] = reinterpret_cast<const uint4*>(sg[i].s)[idx];
+        dp[u] = reinterpret_cast<uint4*>(sg[i].d) + idx;
+      }
+    }
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (i + u * blockDim.x < n16) d[i + u * blockDim.x] = v[u];
+    for (int u = 0; u < 8; ++u)
+      if (dp[u]) *dp[u] = v[u];
   }
+}
+template <class T>
+MSPQ_D StageSeg seg(T* d, const T* s, size_t cnt) {
+  return StageSeg{(void*)d, (const void*)s, (int)((cnt * sizeof(T) + 15) / 16)};
 }
 
 MSPQ_D void stage(const CtlDev& G, CtlDev& S, unsigned char* sm, bool in, bool elb) {
@@ -798,31 +825,22 @@ MSPQ_D void stage(const CtlDev& G, CtlDev& S, unsigned char* sm, bool in, bool e
   S.cap = (int*)take(G.L * 4);
   if (elb) S.elb_ids = (int32_t*)take((size_t)G.kmax * G.L * G.K * 4);
   if (in) {
-    cp(S.res, G.res, n);
-    cp(S.stamp, G.stamp, n);
-    cp(S.clock, G.clock, 1);
-    cp(S.lsize, G.lsize, G.L);
-    cp(S.scal, G.scal, S_COUNT);
-    cp(S.free_stack, G.free_stack, G.nbuf);
-    cp(S.pending, G.pending, G.nbuf);
-    cp(S.snap, G.snap, n);
-    cp(S.sched, G.sched, n);
-    cp(S.cand_first, G.cand_first, n);
-    cp(S.cand_conf, G.cand_conf, n);
-    cp(S.cap, G.cap, G.L);
-    if (elb) cp(S.elb_ids, G.elb_ids, (size_t)G.kmax * G.L * G.K);
+    const StageSeg sg[13] = {seg(S.res, G.res, n),          seg(S.stamp, G.stamp, n),
+                             seg(S.clock, G.clock, 1),      seg(S.lsize, G.lsize, G.L),
+                             seg(S.scal, G.scal, S_COUNT),  seg(S.free_stack, G.free_stack, G.nbuf),
+                             seg(S.pending, G.pending, G.nbuf), seg(S.snap, G.snap, n),
+                             seg(S.sched, G.sched, n),      seg(S.cand_first, G.cand_first, n),
+                             seg(S.cand_conf, G.cand_conf, n), seg(S.cap, G.cap, G.L),
+                             seg(S.elb_ids, G.elb_ids, elb ? (size_t)G.kmax * G.L * G.K : 0)};
+    cp_multi(sg, 13);
   } else {
-    cp(G.res, S.res, n);
-    cp(G.stamp, S.stamp, n);
-    cp(G.clock, S.clock, 1);
-    cp(G.lsize, S.lsize, G.L);
-    cp(G.scal, S.scal, S_COUNT);
-    cp(G.free_stack, S.free_stack, G.nbuf);
-    cp(G.pending, S.pending, G.nbuf);
-    cp(G.snap, S.snap, n);
-    cp(G.sched, S.sched, n);
-    cp(G.cand_first, S.cand_first, n);
-    cp(G.cand_conf, S.cand_conf, n);
+    const StageSeg sg[11] = {seg(G.res, S.res, n),          seg(G.stamp, S.stamp, n),
+                             seg(G.clock, S.clock, 1),      seg(G.lsize, S.lsize, G.L),
+                             seg(G.scal, S.scal, S_COUNT),  seg(G.free_stack, S.free_stack, G.nbuf),
+                             seg(G.pending, S.pending, G.nbuf), seg(G.snap, S.snap, n),
+                             seg(G.sched, S.sched, n),      seg(G.cand_first, S.cand_first, n),
+                             seg(G.cand_conf, S.cand_conf, n)};
+    cp_multi(sg, 11);
   }
 }
 
