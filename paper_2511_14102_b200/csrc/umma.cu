@@ -1096,18 +1096,23 @@ bool pdl_disabled() {
   return off;
 }
 
+template <int BN, int STAGES>
+static cudaError_t launch_grouped_v(const UmmaArgs& a, int units, cudaStream_t st) {
+  const size_t smem = 1024 + STAGES * (TILE_A + BN * 128) + (2 * STAGES + 2) * 8 + 16;
+  cudaFuncSetAttribute(k_umma_grouped<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  return launch_pdl(k_umma_grouped<BN, STAGES>, dim3(units), dim3(192), smem, st, a);
+}
+
+// 4 stages (75 KB smem) fit 3 CTAs per SM, so a verify layer's W13 (<= 4 experts x 100 row tiles
+// at k = 1) runs in one wave of 444 instead of spilling past 296; per-SM bytes in flight are the
+// same as 2 CTAs x 6 stages.  Per-layer verify FFN 118.3 -> 113.1 us at cap 4 (Phi).
+// MSPQ_K3_STAGES=6 restores the old ring (A/B).
 cudaError_t launch_umma_grouped(const UmmaArgs& a, int max_groups, int BN, cudaStream_t st) {
-  constexpr int STAGES = 6;
+  static const int stages = getenv("MSPQ_K3_STAGES") ? atoi(getenv("MSPQ_K3_STAGES")) : 4;
   const int units = max_groups * (a.rows / BM) * a.splits;
   if (units == 0) return cudaSuccess;
-  if (BN == 16) {
-    const size_t smem = 1024 + STAGES * (TILE_A + 16 * 128) + (2 * STAGES + 2) * 8 + 16;
-    cudaFuncSetAttribute(k_umma_grouped<16, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    return launch_pdl(k_umma_grouped<16, STAGES>, dim3(units), dim3(192), smem, st, a);
-  }
-  const size_t smem = 1024 + STAGES * (TILE_A + 32 * 128) + (2 * STAGES + 2) * 8 + 16;
-  cudaFuncSetAttribute(k_umma_grouped<32, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  return launch_pdl(k_umma_grouped<32, STAGES>, dim3(units), dim3(192), smem, st, a);
+  if (BN == 16) return stages == 6 ? launch_grouped_v<16, 6>(a, units, st) : launch_grouped_v<16, 4>(a, units, st);
+  return stages == 6 ? launch_grouped_v<32, 6>(a, units, st) : launch_grouped_v<32, 4>(a, units, st);
 }
 
 cudaError_t launch_umma_int4(const UmmaArgs& a, int max_groups, int BN, cudaStream_t st) {
