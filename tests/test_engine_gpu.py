@@ -256,3 +256,21 @@ def test_verify_overlap_changes_nothing_but_timing(cuda):
     for ca, cb in zip(a["cycles"], b["cycles"]):
         for key in ["draft_tokens", "target_argmax", "target", "log", "new_experts"]:
             assert ca[key] == cb[key], key
+
+
+def test_cycle_record_layer_times_are_ordered(cuda):
+    """The per-layer event times (tools/cycle_timeline.py reads them) follow the verify chain:
+    K1 done <= controller done <= GEMM start < GEMM end <= next layer's K1 done, all inside the
+    cycle's span."""
+    eng, cfg = _engine()
+    eng.configure({"policy": "speculative", "cache_capacity": 3, "k": 3})
+    rep = eng.generate([5, 6, 7], 12)
+    for c in rep["cycles"]:
+        lt = c["layer_times"]
+        assert len(lt) == cfg.L and all(len(v) == 4 for v in lt)
+        t0, t1 = c["start_s"], c["start_s"] + c["span_s"]
+        prev_end = t0
+        for w0, k0, ge, rt in lt:
+            assert prev_end <= rt <= w0 <= k0 < ge <= t1 + 1e-6
+            prev_end = ge
+    eng.close()
