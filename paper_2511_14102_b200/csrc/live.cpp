@@ -99,6 +99,14 @@ struct mspq_engine {
   cudaEvent_t ev_stage[2] = {nullptr, nullptr};
   char stage_rec[2] = {0, 0};
   int stage_next = 0;
+  // opt-in prefetch lane (MSPQ_PF_LANE=1): the planner's prefetches get their own copy stream,
+  // decode stream and staging pair, so a layer's demand copies do not queue behind them
+  bool pf_lane = false;
+  cudaStream_t sx2 = nullptr, sdec2 = nullptr;
+  unsigned char* stage2[2] = {nullptr, nullptr};
+  cudaEvent_t ev_stage2[2] = {nullptr, nullptr};
+  char stage_rec2[2] = {0, 0};
+  int stage_next2 = 0;
   int n_payload = 0;
   bool host_is_shm = false;
   // slot pool
@@ -556,7 +564,13 @@ static void spin_wait(cudaEvent_t ev) {
   }
 }
 
-static int issue_copies(mspq_engine* E, int cycle, CopyBatch& batch, uint64_t& bytes) {
+static int issue_copies(mspq_engine* E, int cycle, CopyBatch& batch, uint64_t& bytes, bool prefetch = false) {
+  const bool l2 = prefetch && E->pf_lane;
+  cudaStream_t sx = l2 ? E->sx2 : E->sx, sdec = l2 ? E->sdec2 : E->sdec;
+  unsigned char** stage = l2 ? E->stage2 : E->stage;
+  cudaEvent_t* ev_stage = l2 ? E->ev_stage2 : E->ev_stage;
+  char* stage_rec = l2 ? E->stage_rec2 : E->stage_rec;
+  int& stage_next = l2 ? E->stage_next2 : E->stage_next;
   const int n = E->view.host_stat[S_NREQ];
   if (E->view.host_stat[S_OVERFLOW]) fail(MSPQ_ERR_OVERFLOW, "device controller ran out of buffers / queue");
   if (n > E->view.req_cap) fail(MSPQ_ERR_OVERFLOW, "copy request queue overflow");
@@ -565,25 +579,28 @@ static int issue_copies(mspq_engine* E, int cycle, CopyBatch& batch, uint64_t& b
     if (buf < 0 || buf >= E->nbuf) fail(MSPQ_ERR_OVERFLOW, "invalid slot buffer");
     if (!batch.a) {
       batch.a = E->pool_event();
-      CUDA_OK(cudaEventRecord(batch.a, E->sx));
+      CUDA_OK(cudaEventRecord(batch.a, sx));
     }
     const bool reused = E->last_cycle[buf] == cycle;  // the slot's last reader is this cycle's GEMM
     unsigned char* slot = E->pool + (size_t)buf * E->S16;
+    // two lanes: a slot may still be under a write issued on the other lane (a prefetch the
+    // controller evicted before its use), so the new writer orders after it
+    if (E->pf_lane && E->ready_rec[buf]) CUDA_OK(cudaStreamWaitEvent(E->codec ? sdec : sx, E->ev_ready[buf], 0));
     if (!E->codec) {
-      if (reused) CUDA_OK(cudaStreamWaitEvent(E->sx, E->ev_gemm[E->last_layer[buf]], 0));
-      CUDA_OK(cudaMemcpyAsync(slot, E->host_blob(E->payload(key)), E->S16, cudaMemcpyHostToDevice, E->sx));
-      CUDA_OK(cudaEventRecord(E->ev_ready[buf], E->sx));
+      if (reused) CUDA_OK(cudaStreamWaitEvent(sx, E->ev_gemm[E->last_layer[buf]], 0));
+      CUDA_OK(cudaMemcpyAsync(slot, E->host_blob(E->payload(key)), E->S16, cudaMemcpyHostToDevice, sx));
+      CUDA_OK(cudaEventRecord(E->ev_ready[buf], sx));
       bytes += (uint64_t)E->S16;
     } else {
       // compressed blob -> staging (copy engine, chunked) -> decode kernel -> slot.  Chunk c's
       // decode starts as soon as its bytes land, so only the last chunk's decode is exposed.
       const unsigned char* hb = E->host_blob(E->payload(key));
       const uint32_t* toff = reinterpret_cast<const uint32_t*>(hb + 64);
-      const int sb = E->stage_next;
-      E->stage_next ^= 1;
-      unsigned char* stg = E->stage[sb];
-      if (E->stage_rec[sb]) CUDA_OK(cudaStreamWaitEvent(E->sx, E->ev_stage[sb], 0));
-      if (reused) CUDA_OK(cudaStreamWaitEvent(E->sdec, E->ev_gemm[E->last_layer[buf]], 0));
+      const int sb = stage_next;
+      stage_next ^= 1;
+      unsigned char* stg = stage[sb];
+      if (stage_rec[sb]) CUDA_OK(cudaStreamWaitEvent(sx, ev_stage[sb], 0));
+      if (reused) CUDA_OK(cudaStreamWaitEvent(sdec, E->ev_gemm[E->last_layer[buf]], 0));
       const int nt = E->n_tiles;
       // ~24 MB chunks: a pinned H2D chunk pays a fixed start cost (tools/h2d_chunks.py: 54.9 GB/s at
       // 4 x 25 MB vs 53.6 at 16 x 6 MB), while the exposed tail is one tile per decode warp either way
@@ -595,15 +612,15 @@ static int issue_copies(mspq_engine* E, int cycle, CopyBatch& batch, uint64_t& b
         const int t0 = c < nm ? (int)((int64_t)(nt - tail) * c / nm) : nt - tail;
         const int t1 = c < nm ? (int)((int64_t)(nt - tail) * (c + 1) / nm) : nt;
         const uint32_t b0 = c ? toff[t0] : 0u, b1 = toff[t1];
-        CUDA_OK(cudaMemcpyAsync(stg + b0, hb + b0, b1 - b0, cudaMemcpyHostToDevice, E->sx));
+        CUDA_OK(cudaMemcpyAsync(stg + b0, hb + b0, b1 - b0, cudaMemcpyHostToDevice, sx));
         cudaEvent_t ev = E->pool_event();
-        CUDA_OK(cudaEventRecord(ev, E->sx));
-        CUDA_OK(cudaStreamWaitEvent(E->sdec, ev, 0));
-        CAPI_OK(mspq_xc_decode(stg, t0, t1, slot, 256, E->sdec));
+        CUDA_OK(cudaEventRecord(ev, sx));
+        CUDA_OK(cudaStreamWaitEvent(sdec, ev, 0));
+        CAPI_OK(mspq_xc_decode(stg, t0, t1, slot, 256, sdec));
       }
-      CUDA_OK(cudaEventRecord(E->ev_stage[sb], E->sdec));
-      E->stage_rec[sb] = 1;
-      CUDA_OK(cudaEventRecord(E->ev_ready[buf], E->sdec));
+      CUDA_OK(cudaEventRecord(ev_stage[sb], sdec));
+      stage_rec[sb] = 1;
+      CUDA_OK(cudaEventRecord(E->ev_ready[buf], sdec));
       bytes += toff[nt];
     }
     E->ready_rec[buf] = 1;
@@ -611,7 +628,7 @@ static int issue_copies(mspq_engine* E, int cycle, CopyBatch& batch, uint64_t& b
   }
   if (batch.a) {
     batch.b = E->pool_event();
-    CUDA_OK(cudaEventRecord(batch.b, E->codec ? E->sdec : E->sx));
+    CUDA_OK(cudaEventRecord(batch.b, E->codec ? sdec : sx));
   }
   return n;
 }
@@ -642,6 +659,7 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
   if (c.use_governor && c.ttft_budget > 0.0) k_slo = std::min(k_slo, k_slo_from_ttft(prof, c.ttft_budget, est(), c.k_min, c.k_max));
   CUDA_OK(cudaEventRecord(E->ev_t0, E->sc));
   CUDA_OK(cudaStreamWaitEvent(E->sx, E->ev_t0, 0));
+  if (E->pf_lane) CUDA_OK(cudaStreamWaitEvent(E->sx2, E->ev_t0, 0));
   std::vector<int> committed;
   json cycles = json::array();
   double stall_total = 0.0, layer_cov_total = 0.0, step_cov_total = 0.0;
@@ -680,7 +698,7 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
       }
       spin_wait(E->ev_row[i]);
       CopyBatch b;
-      issue_copies(E, cycle, b, cyc_bytes);
+      issue_copies(E, cycle, b, cyc_bytes, true);
       if (b.count) batches.push_back(b);
     }
     CUDA_OK(cudaEventRecord(E->ev_dend, E->sc));
@@ -954,6 +972,8 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
   // everything (including trailing prefetches) has landed before we report
   CUDA_OK(cudaStreamSynchronize(E->sx));
   if (E->sdec) CUDA_OK(cudaStreamSynchronize(E->sdec));
+  if (E->sx2) CUDA_OK(cudaStreamSynchronize(E->sx2));
+  if (E->sdec2) CUDA_OK(cudaStreamSynchronize(E->sdec2));
   const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
   json rep;
   const double total_time = cycles.empty() ? 0.0
@@ -1038,7 +1058,11 @@ void destroy(mspq_engine* E) {
   for (int i = 0; i < 2; ++i) {
     if (E->stage[i]) cudaFree(E->stage[i]);
     if (E->ev_stage[i]) cudaEventDestroy(E->ev_stage[i]);
+    if (E->stage2[i]) cudaFree(E->stage2[i]);
+    if (E->ev_stage2[i]) cudaEventDestroy(E->ev_stage2[i]);
   }
+  if (E->sx2) cudaStreamDestroy(E->sx2);
+  if (E->sdec2) cudaStreamDestroy(E->sdec2);
   if (E->sc) cudaStreamDestroy(E->sc);
   if (E->sx) cudaStreamDestroy(E->sx);
   if (E->sdec) cudaStreamDestroy(E->sdec);
@@ -1077,6 +1101,20 @@ int mspq_engine_create(const mspq_model_desc* md, const mspq_engine_opts* op, ms
         for (int i = 0; i < 2; ++i) {
           CUDA_OK(cudaMalloc(&E->stage[i], (size_t)E->Sreg));
           CUDA_OK(cudaEventCreateWithFlags(&E->ev_stage[i], cudaEventDisableTiming));
+        }
+      }
+      {
+        const char* pf = getenv("MSPQ_PF_LANE");
+        E->pf_lane = pf && pf[0] == '1';
+      }
+      if (E->pf_lane) {
+        CUDA_OK(cudaStreamCreateWithPriority(&E->sx2, cudaStreamNonBlocking, lo));
+        if (E->codec) {
+          CUDA_OK(cudaStreamCreateWithPriority(&E->sdec2, cudaStreamNonBlocking, lo));
+          for (int i = 0; i < 2; ++i) {
+            CUDA_OK(cudaMalloc(&E->stage2[i], (size_t)E->Sreg));
+            CUDA_OK(cudaEventCreateWithFlags(&E->ev_stage2[i], cudaEventDisableTiming));
+          }
         }
       }
       E->S4 = mspq_int4_blob_bytes(m.d, m.f);

@@ -240,6 +240,27 @@ def test_shared_host_store_attach_path(cuda, tmp_path):
                 os.unlink(p)
 
 
+@pytest.mark.parametrize("codec", ["none", "xc"])
+def test_prefetch_lane_changes_nothing_but_timing(cuda, codec, monkeypatch):
+    """MSPQ_PF_LANE=1 issues the planner's prefetches on a second copy (+ decode) stream with its
+    own staging pair: tokens, routing, the hit/miss log and the bytes moved are unchanged."""
+    import paper_2511_14102_b200 as m
+    cfg = m.ModelConfig.named("tiny")
+    reps = []
+    for lane in ("0", "1"):
+        monkeypatch.setenv("MSPQ_PF_LANE", lane)
+        eng = m.Engine(cfg, kmax=8, trace_level=2, expert_codec=codec)
+        eng.configure({"policy": "speculative", "cache_capacity": 3, "k": 4})
+        reps.append(eng.generate([5, 17, 101, 9], 32))
+        eng.close()
+    a, b = reps
+    assert a["tokens"] == b["tokens"]
+    assert a["h2d_bytes"] == b["h2d_bytes"] > 0
+    for ca, cb in zip(a["cycles"], b["cycles"]):
+        for key in ["draft_tokens", "target_argmax", "target", "log", "new_experts"]:
+            assert ca[key] == cb[key], key
+
+
 def test_verify_overlap_changes_nothing_but_timing(cuda):
     """verify_overlap runs a layer's GEMM in two parts (resident experts first, in-flight ones
     after their copies land): tokens, routing and the hit/miss log are unchanged."""
