@@ -107,6 +107,12 @@ struct mspq_engine {
   cudaEvent_t ev_stage2[2] = {nullptr, nullptr};
   char stage_rec2[2] = {0, 0};
   int stage_next2 = 0;
+  // opt-in deferred prefetch (MSPQ_PF_DEFER=1, per-layer capacity only): a plan prefetch for layer
+  // j >= 1 is issued on the demand stream right after layer j-1's demand copies, so it covers the
+  // layer boundary (GEMM, K1, controller) when the link would otherwise idle.  FIFO order on the
+  // stream keeps it ahead of any later demand write to the same per-layer slot.
+  bool pf_defer = false;
+  std::vector<std::pair<int, int>> deferred;  // (key, buf), plan order
   int n_payload = 0;
   bool host_is_shm = false;
   // slot pool
@@ -564,19 +570,27 @@ static void spin_wait(cudaEvent_t ev) {
   }
 }
 
-static int issue_copies(mspq_engine* E, int cycle, CopyBatch& batch, uint64_t& bytes, bool prefetch = false) {
+static int issue_copies(mspq_engine* E, int cycle, CopyBatch& batch, uint64_t& bytes, bool prefetch = false,
+                        const std::vector<std::pair<int, int>>* list = nullptr) {
   const bool l2 = prefetch && E->pf_lane;
   cudaStream_t sx = l2 ? E->sx2 : E->sx, sdec = l2 ? E->sdec2 : E->sdec;
   unsigned char** stage = l2 ? E->stage2 : E->stage;
   cudaEvent_t* ev_stage = l2 ? E->ev_stage2 : E->ev_stage;
   char* stage_rec = l2 ? E->stage_rec2 : E->stage_rec;
   int& stage_next = l2 ? E->stage_next2 : E->stage_next;
-  const int n = E->view.host_stat[S_NREQ];
-  if (E->view.host_stat[S_OVERFLOW]) fail(MSPQ_ERR_OVERFLOW, "device controller ran out of buffers / queue");
-  if (n > E->view.req_cap) fail(MSPQ_ERR_OVERFLOW, "copy request queue overflow");
+  const int n = list ? (int)list->size() : E->view.host_stat[S_NREQ];
+  if (!list) {
+    if (E->view.host_stat[S_OVERFLOW]) fail(MSPQ_ERR_OVERFLOW, "device controller ran out of buffers / queue");
+    if (n > E->view.req_cap) fail(MSPQ_ERR_OVERFLOW, "copy request queue overflow");
+  }
   for (int i = 0; i < n; ++i) {
-    const int key = E->view.host_req[i * 3], buf = E->view.host_req[i * 3 + 1];
+    const int key = list ? (*list)[i].first : E->view.host_req[i * 3];
+    const int buf = list ? (*list)[i].second : E->view.host_req[i * 3 + 1];
     if (buf < 0 || buf >= E->nbuf) fail(MSPQ_ERR_OVERFLOW, "invalid slot buffer");
+    if (prefetch && !list && E->pf_defer && key / E->m.E >= 1) {
+      E->deferred.push_back({key, buf});
+      continue;
+    }
     if (!batch.a) {
       batch.a = E->pool_event();
       CUDA_OK(cudaEventRecord(batch.a, sx));
@@ -659,6 +673,11 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
   if (c.use_governor && c.ttft_budget > 0.0) k_slo = std::min(k_slo, k_slo_from_ttft(prof, c.ttft_budget, est(), c.k_min, c.k_max));
   CUDA_OK(cudaEventRecord(E->ev_t0, E->sc));
   CUDA_OK(cudaStreamWaitEvent(E->sx, E->ev_t0, 0));
+  {
+    const char* pd = getenv("MSPQ_PF_DEFER");
+    E->pf_defer = pd && pd[0] == '1' && c.mode == 0;
+  }
+  E->deferred.clear();
   if (E->pf_lane) CUDA_OK(cudaStreamWaitEvent(E->sx2, E->ev_t0, 0));
   std::vector<int> committed;
   json cycles = json::array();
@@ -728,6 +747,23 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
       b.label = "io_new";
       issue_copies(E, cycle, b, cyc_bytes);
       if (b.count) batches.push_back(b);
+      if (!E->deferred.empty()) {
+        // deferred plan prefetches for layer l+1 go right behind layer l's demand copies; when l+1
+        // has none, the earliest remaining layer's are pulled forward so the boundary stays covered
+        int lim = l + 1;
+        bool any = false;
+        for (auto& kb : E->deferred) any |= kb.first / Ex <= lim;
+        if (!any) {
+          lim = L;
+          for (auto& kb : E->deferred) lim = std::min(lim, kb.first / Ex);
+        }
+        std::vector<std::pair<int, int>> now, keep;
+        for (auto& kb : E->deferred) (kb.first / Ex <= lim ? now : keep).push_back(kb);
+        E->deferred.swap(keep);
+        CopyBatch bp;
+        issue_copies(E, cycle, bp, cyc_bytes, true, &now);
+        if (bp.count) batches.push_back(bp);
+      }
       // the layer's groups (ascending expert = the device schedule's order) split into experts
       // already resident (part A: their GEMM runs while the copies are still on the link) and
       // experts whose copy is in flight (part B: after a stream wait on their ready events)
@@ -793,6 +829,7 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
       }
       demand_total += 0;
     }
+    if (!E->deferred.empty()) fail(MSPQ_ERR_OVERFLOW, "deferred prefetch left at the end of the verify pass");
     const int pl = (L - 1) & 1;
     launches += 6;  // embed, final norm, lm head, argmax, accept, begin_cycle
     CAPI_OK(mspq_gate_topk(E->h, E->yv[pl], E->sv[pl].entry_of, E->wts_t + (size_t)(L - 1) * T * K, E->yv_splits[pl],
