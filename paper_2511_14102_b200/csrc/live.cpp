@@ -107,7 +107,7 @@ struct mspq_engine {
   cudaEvent_t ev_stage2[2] = {nullptr, nullptr};
   char stage_rec2[2] = {0, 0};
   int stage_next2 = 0;
-  // opt-in deferred prefetch (MSPQ_PF_DEFER=1, per-layer capacity only): a plan prefetch for layer
+  // deferred prefetch (default on; MSPQ_PF_DEFER=0 turns it off; per-layer capacity only): a plan prefetch for layer
   // j >= 1 is issued on the demand stream right after layer j-1's demand copies, so it covers the
   // layer boundary (GEMM, K1, controller) when the link would otherwise idle.  FIFO order on the
   // stream keeps it ahead of any later demand write to the same per-layer slot.
@@ -675,7 +675,7 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
   CUDA_OK(cudaStreamWaitEvent(E->sx, E->ev_t0, 0));
   {
     const char* pd = getenv("MSPQ_PF_DEFER");
-    E->pf_defer = pd && pd[0] == '1' && c.mode == 0;
+    E->pf_defer = !(pd && pd[0] == '0') && c.mode == 0;  // on by default; MSPQ_PF_DEFER=0 is the A/B switch
   }
   E->deferred.clear();
   if (E->pf_lane) CUDA_OK(cudaStreamWaitEvent(E->sx2, E->ev_t0, 0));
