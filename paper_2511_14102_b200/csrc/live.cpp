@@ -1134,7 +1134,12 @@ int mspq_engine_create(const mspq_model_desc* md, const mspq_engine_opts* op, ms
       E->n_tiles = (int)(E->S16 / 16384);
       E->Sreg = E->codec ? ((mspq_xc_max_blob_bytes(E->n_tiles) + 4095) / 4096) * 4096 : E->S16;
       if (E->codec) {
-        CUDA_OK(cudaStreamCreateWithPriority(&E->sdec, cudaStreamNonBlocking, hi));
+        {
+          // MSPQ_DEC_PRIO=lo: decodes at the compute stream's priority (A/B switch)
+          const char* dp = getenv("MSPQ_DEC_PRIO");
+          const bool dlo = dp && dp[0] == 'l';
+          CUDA_OK(cudaStreamCreateWithPriority(&E->sdec, cudaStreamNonBlocking, dlo ? lo : hi));
+        }
         for (int i = 0; i < 2; ++i) {
           CUDA_OK(cudaMalloc(&E->stage[i], (size_t)E->Sreg));
           CUDA_OK(cudaEventCreateWithFlags(&E->ev_stage[i], cudaEventDisableTiming));
