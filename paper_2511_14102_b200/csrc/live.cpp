@@ -112,6 +112,7 @@ struct mspq_engine {
   // layer boundary (GEMM, K1, controller) when the link would otherwise idle.  FIFO order on the
   // stream keeps it ahead of any later demand write to the same per-layer slot.
   bool pf_defer = false;
+  int dec_ctas = 256;  // decode grid per chunk (MSPQ_DEC_CTAS, A/B switch)
   std::vector<std::pair<int, int>> deferred;  // (key, buf), plan order
   int n_payload = 0;
   bool host_is_shm = false;
@@ -630,7 +631,7 @@ static int issue_copies(mspq_engine* E, int cycle, CopyBatch& batch, uint64_t& b
         cudaEvent_t ev = E->pool_event();
         CUDA_OK(cudaEventRecord(ev, sx));
         CUDA_OK(cudaStreamWaitEvent(sdec, ev, 0));
-        CAPI_OK(mspq_xc_decode(stg, t0, t1, slot, 256, sdec));
+        CAPI_OK(mspq_xc_decode(stg, t0, t1, slot, E->dec_ctas, sdec));
       }
       CUDA_OK(cudaEventRecord(ev_stage[sb], sdec));
       stage_rec[sb] = 1;
@@ -1148,6 +1149,10 @@ int mspq_engine_create(const mspq_model_desc* md, const mspq_engine_opts* op, ms
       {
         const char* pf = getenv("MSPQ_PF_LANE");
         E->pf_lane = pf && pf[0] == '1';
+      }
+      {
+        const char* dc = getenv("MSPQ_DEC_CTAS");
+        if (dc) E->dec_ctas = std::max(1, std::min(1024, atoi(dc)));
       }
       if (E->pf_lane) {
         CUDA_OK(cudaStreamCreateWithPriority(&E->sx2, cudaStreamNonBlocking, lo));
