@@ -473,7 +473,8 @@ def sim_config(cfg: dict):
         elif k == "profile":
             c["profile"] = profile_from_json(v)
         elif k in ("policy", "capacity_mode", "cache_capacity", "entropy_weighted_capacity",
-                   "prefetch_budget", "ema_alpha", "initial_accept", "collect_plans", "seed"):
+                   "prefetch_budget", "ema_alpha", "initial_accept", "collect_plans", "seed",
+                   "estimator", "verify_overlap", "log"):
             c[k] = v
         else:
             raise ValueError("unknown config key " + k)
@@ -841,4 +842,82 @@ def live_cycle(cache, elb, targets, cfg, log=None, ids_visible_causal=True):
                 if not was:
                     out["fetched"] += 1
                     out["demand"] += 1
+    return out
+
+
+# ----------------------------------------------------------------------------- live governor
+ELB_BETA = 1.0 / 32.0  # per drafted row decay of the elb estimator's routing frequencies
+
+
+def elb_raw(freq, resident, L, E, k):
+    """The live engine's "elb" |E_new(k)| estimate before calibration (live.cpp
+    `elb_raw`): per layer, each non-resident expert e is fetched if any of the k+1 window tokens
+    routes to it, probability 1-(1-p[l,e])^(k+1); summed in (layer, expert) order."""
+    s = 0.0
+    for i in range(L * E):
+        if (i // E, i % E) not in resident:
+            s += 1.0 - math.pow(1.0 - freq[i], float(k + 1))
+    return s
+
+
+def elb_estimate(freq, resident, calib, L, E, k):
+    """Calibrated estimate: llround(calib[k] * raw), calib[k] = EMA (weight 1/4) of fetched / raw
+    over the cycles run at k."""
+    return llround(calib[k] * elb_raw(freq, resident, L, E, k))
+
+
+def elb_update(freq, elb_rows, L, E):
+    """Per drafted row r, per layer: p <- (1-beta) p + beta [e in the row's top-K]."""
+    for row in elb_rows:
+        for l in range(L):
+            for e in range(E):
+                freq[l * E + e] *= 1.0 - ELB_BETA
+            for e in row[l]:
+                freq[l * E + e] += ELB_BETA
+
+
+def live_governor_ks(report, cfg_json, L, E, K, estimator="linear", kmax=16):
+    """The k sequence the live engine's governor must pick (live.cpp generate; sim.cpp:118-120,
+    394-404) given the run's own outcomes: select_k over the report's (re-fitted) profile, the EMA
+    acceptance fed with each cycle's accepted prefix, and either the reference's linear g*k
+    estimator (g = fetched/k of the last cycle, starting at L*K) or the elb estimator over this
+    oracle's own cache replay (live_cycle) and the cycle's ELB rows.  Returns per cycle the
+    expected k, its estimate, the unclamped select_k and the governor inputs (p, g, est table)."""
+    c = sim_config(cfg_json)
+    prof = profile_from_json(report["profile"])
+    kcap = max(c["k_max"] if c["use_governor"] else c["fixed_k"], 1)
+    accept = [c["initial_accept"]] * kcap
+    g = float(L) * float(K)
+    freq = [float(K) / E] * (L * E)
+    calib = [1.0] * (kmax + 1)
+    cache = Cache(c["capacity_mode"], c["cache_capacity"])
+    resident = set()
+    rem = report["total_tokens"]
+    out = []
+    for cyc in report["cycles"]:
+        if estimator == "elb":
+            est = lambda kk: elb_estimate(freq, resident, calib, L, E, kk)  # noqa: E731
+        else:
+            est = lambda kk, gg=g: llround(gg * float(kk))  # noqa: E731
+        kk = select_k(prof, accept, c["k_min"], c["k_max"], c["k_slo"], est) if c["use_governor"] else c["fixed_k"]
+        k = max(1, min(kk, rem, kmax))
+        out.append(dict(k=k, est=est(k), select_k=kk, p=list(accept), g=g,
+                        table=[est(j) for j in range(c["k_max"] + 1)]))
+        raw = elb_raw(freq, resident, L, E, k) if estimator == "elb" else 0.0
+        kc = cyc["k"]
+        acc = cyc["accepted"]
+        outcomes = []
+        for i in range(kc):
+            outcomes.append(i < acc)
+            if i >= acc:
+                break
+        accept = update_acceptance(accept, c["ema_alpha"], outcomes[:len(accept)])
+        g = float(cyc["new_experts"]) / float(kc)
+        if estimator == "elb":
+            if raw > 0.0:
+                calib[k] = (1.0 - 0.25) * calib[k] + 0.25 * (float(cyc["new_experts"]) / raw)
+            live_cycle(cache, ELB.build(cyc["elb"], cyc["elb_gates"]), cyc["target"], c)
+            elb_update(freq, cyc["elb"], L, E)
+            resident = set(cache.recency)
+        rem -= acc + cyc["bonus"]
     return out

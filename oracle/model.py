@@ -23,16 +23,16 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "_build", "libmspq_oracle.so")
+_SRCS = [os.path.join(_HERE, "csrc", "model_ref.c"), os.path.join(_HERE, "csrc", "decode_ref.c")]
 _lib = None
 
 
 def build():
     os.makedirs(os.path.join(_HERE, "_build"), exist_ok=True)
-    src = os.path.join(_HERE, "csrc", "model_ref.c")
-    if (not os.path.exists(_SO)) or os.path.getmtime(_SO) < os.path.getmtime(src):
+    if (not os.path.exists(_SO)) or any(os.path.getmtime(_SO) < os.path.getmtime(s) for s in _SRCS):
         import subprocess
-        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-o", _SO,
-                               src, "-lm"])
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fopenmp", "-fPIC", "-shared", "-o", _SO]
+                              + _SRCS + ["-lm"])
 
 
 def lib():
@@ -52,6 +52,14 @@ def lib():
         L.orc_lm_head.argtypes = [P, P, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P]
         L.orc_act.argtypes = [P, P, ctypes.c_int, P]
         L.orc_gen_bf16.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64, ctypes.c_float, P]
+        L.orc_expert_ffn.restype = ctypes.c_int
+        L.orc_expert_ffn.argtypes = [ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                     ctypes.c_float, ctypes.c_float, ctypes.c_int, ctypes.c_int, P, P, P]
+        L.orc_weight_row.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, ctypes.c_float,
+                                     ctypes.c_int, P]
+        L.orc_lm_head_mt.argtypes = [P, P, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P]
+        L.orc_gen_rows_mt.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
+                                      ctypes.c_float, P]
         _lib = L
     return _lib
 
@@ -217,11 +225,14 @@ CONFIGS = {
 
 
 class Model:
-    """CPU model: weights regenerated lazily from the counter hash."""
+    """CPU model: weights regenerated lazily from the counter hash.  With `fast` (default for
+    full-width experts) the expert FFN and LM head run in csrc/decode_ref.c over all host cores,
+    generating each expert's rows on the fly instead of caching fp32 matrices."""
 
-    def __init__(self, desc: ModelDesc):
+    def __init__(self, desc: ModelDesc, fast: bool | None = None):
         self.m = desc
         self._cache = {}
+        self.fast = (desc.d * desc.f >= 1 << 22) if fast is None else fast
 
     def _get(self, key, fn):
         if key not in self._cache:
@@ -249,6 +260,13 @@ class Model:
 
     def lm(self):
         m = self.m
+        if self.fast:
+            def mk():
+                out = np.empty((m.V, m.d), dtype=np.uint16)
+                lib().orc_gen_rows_mt(tensor_key(m.seed, T_LM), 0, m.V, m.d, ctypes.c_float(np.float32(m.a_lm())),
+                                      _p(out))
+                return out
+            return self._get("lm", mk)
         return self._get("lm", lambda: gen(m.seed, T_LM, m.V, m.d, m.a_lm()))
 
     def expert(self, l, e):
@@ -281,8 +299,22 @@ class Model:
         lib().orc_router_topk(_p(xn), _p(wr), m.E, m.d, m.K, _p(logits), _p(ids), _p(wts))
         return ids, wts, logits
 
+    def ffn_batch(self, xn_rows, l, e, draft: bool):
+        """Expert (l, e) on M normed rows [M, d] bf16 -> y [M, d] fp32 (decode_ref.c)."""
+        m = self.m
+        xn_rows = np.ascontiguousarray(xn_rows, dtype=np.uint16)
+        M = xn_rows.shape[0]
+        y = np.empty((M, m.d), dtype=np.float32)
+        rc = lib().orc_expert_ffn(m.seed, l, e, m.d, m.f, ctypes.c_float(m.a_up()), ctypes.c_float(m.a_down()),
+                                  1 if draft else 0, M, _p(xn_rows), _p(y), None)
+        if rc:
+            raise MemoryError("orc_expert_ffn")
+        return y
+
     def ffn(self, xn, l, e, draft: bool):
         m = self.m
+        if self.fast:
+            return self.ffn_batch(xn[None, :], l, e, draft)[0], None
         x = bf16_to_f32(xn)
         G, U, D = self.expert_f32(l, e, draft)
         gv = np.ascontiguousarray(G @ x, dtype=np.float32)
@@ -308,7 +340,8 @@ class Model:
         logits = np.empty((T, m.V), dtype=np.float32)
         am = np.empty(T, dtype=np.int32)
         lm = np.ascontiguousarray(self.lm())
-        lib().orc_lm_head(_p(np.ascontiguousarray(xn_rows)), _p(lm), T, m.V, m.d, _p(logits), _p(am))
+        fn = lib().orc_lm_head_mt if self.fast else lib().orc_lm_head
+        fn(_p(np.ascontiguousarray(xn_rows)), _p(lm), T, m.V, m.d, _p(logits), _p(am))
         return logits, am
 
     # -- one token ---------------------------------------------------------------------------
@@ -336,6 +369,80 @@ class Model:
         return int(am[0]), routing, logits[0]
 
 
+def forward_batch(model: Model, toks, poss, draft: bool, h_in=None):
+    """forward() for M independent tokens, layer-major with tokens grouped by expert (one weight
+    generation per (layer, expert) in fast mode).  Returns [(argmax, routing)] per token.
+    With `h_in` = {layer: [M, d] fp32}, the residual entering that layer is replaced
+    (teacher forcing from the device)."""
+    m = model.m
+    M = len(toks)
+    h = np.stack([(bf16_to_f32(model.embed_row(t)) + bf16_to_f32(model.pos_row(p))).astype(np.float32)
+                  for t, p in zip(toks, poss)])
+    routing = [[] for _ in range(M)]
+    for l in range(m.L):
+        if h_in is not None and l in h_in:
+            h = np.asarray(h_in[l], dtype=np.float32).copy()
+        xn = np.stack([model.rmsnorm(np.ascontiguousarray(h[i]), model.gamma(l)) for i in range(M)])
+        rt = [model.route(xn[i], l) for i in range(M)]
+        for i in range(M):
+            routing[i].append((rt[i][0].copy(), rt[i][1].copy()))
+        ys = {}
+        for e in sorted({int(x) for i in range(M) for x in rt[i][0]}):
+            rows = [i for i in range(M) if e in rt[i][0].tolist()]
+            if model.fast:
+                yb = model.ffn_batch(xn[rows], l, e, draft)
+            else:
+                yb = np.stack([model.ffn(xn[i], l, e, draft)[0] for i in rows])
+            for j, i in enumerate(rows):
+                ys[(i, e)] = yb[j]
+        for i in range(M):
+            acc = np.zeros(m.d, dtype=np.float32)
+            for j in range(m.K):
+                e = int(rt[i][0][j])
+                acc = (acc + (np.float32(rt[i][1][j]) * ys[(i, e)]).astype(np.float32)).astype(np.float32)
+            h[i] = (h[i] + acc).astype(np.float32)
+    xf = np.stack([model.rmsnorm(np.ascontiguousarray(h[i]), model.gamma(-1)) for i in range(M)])
+    _, am = model.lm_head(xf)
+    return [(int(am[i]), routing[i]) for i in range(M)]
+
+
+def check_layers(model: Model, h_caps, ids, draft: bool, tol=2e-3):
+    """Teacher-forced per-layer check of a device pass over M tokens.  h_caps [L+1][M][d] = the
+    device residual entering each layer (index L = the final residual); ids [L][M][K] = the
+    device's routing.  For every layer: routing from the device's own h must be bit-exact, and
+    h + sum_j w_j FFN_j(xn) must equal the device's next residual within
+    tol * max|h| (accumulation order only).  Returns (worst relative error, margins[L][M] = the
+    router's logit gap at the top-K boundary relative to the largest |logit|) for near-tie reporting; raises AssertionError on a
+    mismatch."""
+    m = model.m
+    M = h_caps.shape[1]
+    worst = 0.0
+    margins = [[float("inf")] * M for _ in range(m.L)]
+    for l in range(m.L):
+        h = np.ascontiguousarray(h_caps[l], dtype=np.float32)
+        xn = np.stack([model.rmsnorm(np.ascontiguousarray(h[i]), model.gamma(l)) for i in range(M)])
+        rt = [model.route(xn[i], l) for i in range(M)]
+        for i in range(M):
+            assert rt[i][0].tolist() == list(ids[l][i]), ("routing", l, i, rt[i][0].tolist(), list(ids[l][i]))
+            lg = np.sort(rt[i][2])[::-1]
+            if m.K < m.E:
+                margins[l][i] = float(lg[m.K - 1] - lg[m.K]) / (float(np.abs(lg).max()) + 1e-30)
+        nxt = h.copy()
+        for e in sorted({int(x) for i in range(M) for x in rt[i][0]}):
+            rows = [i for i in range(M) if e in rt[i][0].tolist()]
+            yb = model.ffn_batch(xn[rows], l, e, draft) if model.fast else \
+                np.stack([model.ffn(xn[i], l, e, draft)[0] for i in rows])
+            for j, i in enumerate(rows):
+                w = float(rt[i][1][list(rt[i][0]).index(e)])
+                nxt[i] += np.float32(w) * yb[j]
+        dev = np.asarray(h_caps[l + 1], dtype=np.float32)
+        scale = float(np.abs(dev).max()) + 1e-6
+        err = float(np.abs(nxt - dev).max()) / scale
+        worst = max(worst, err)
+        assert err <= tol, ("layer output", l, err)
+    return worst, margins
+
+
 def speculative_decode(model: Model, last_token: int, start_pos: int, ks, max_new: int):
     """Greedy speculative decoding with the INT4 draft: each cycle drafts k
     tokens from the head (previous bonus), verifies the k+1-slot window with the bf16 target
@@ -355,11 +462,9 @@ def speculative_decode(model: Model, last_token: int, start_pos: int, ks, max_ne
             draft_toks.append(nt)
             t, p = nt, p + 1
         window = [tok] + draft_toks
-        tgt_routing, tgt_argmax = [], []
-        for s, wt in enumerate(window):
-            am, routing, _ = model.forward(wt, pos + s, draft=False)
-            tgt_routing.append(routing)
-            tgt_argmax.append(am)
+        res = forward_batch(model, window, [pos + s for s in range(len(window))], draft=False)
+        tgt_argmax = [r[0] for r in res]
+        tgt_routing = [r[1] for r in res]
         acc = 0
         while acc < k and draft_toks[acc] == tgt_argmax[acc]:
             acc += 1

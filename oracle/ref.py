@@ -24,7 +24,7 @@ def lib():
         L.ref_last_error.restype = c
         L.ref_free.argtypes = [v]
         L.ref_generate_trace.restype = v
-        L.ref_generate_trace.argtypes = [ctypes.c_int] * 5 + [ctypes.c_ulonglong] if False else [
+        L.ref_generate_trace.argtypes = [
             ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_ulonglong, ctypes.c_int,
             ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
             ctypes.c_ulonglong]

@@ -135,7 +135,11 @@ char* ref_governor(const char* request_json) {
     gov.k_max = r.value("k_max", 16);
     gov.k_slo = r.value("k_slo", 16);
     const double g = r.value("g", 0.0);
-    NewExpertEstimator est = [g](int k) {
+    // "est": optional table est[k] (any |E_new(k)| estimator, e.g. the live engine's elb one)
+    // fed to the reference's select_k in place of the linear g*k
+    const std::vector<int> table = r.contains("est") ? r["est"].get<std::vector<int>>() : std::vector<int>{};
+    NewExpertEstimator est = [g, table](int k) {
+      if (!table.empty()) return table.at(static_cast<size_t>(k));
       return static_cast<int>(std::llround(g * static_cast<double>(k)));
     };
     json out;

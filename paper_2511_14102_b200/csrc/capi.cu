@@ -248,8 +248,9 @@ struct mspq_cache {
 };
 
 int mspq_cache_create(int L, int E, int K, int kmax, int nbuf, int log_cap, mspq_cache** out) {
-  if (L < 1 || E < 1 || K < 1 || K > E || L * E > 8192 || E > 1024)
-    return set_error(MSPQ_ERR_SHAPE_VIOLATION, "cache: need 1<=K<=E<=1024, L*E<=8192");
+  // K <= 64: the controller's per-step key scratch (ctl.cu sorted_keys) and gate_topk's limit
+  if (L < 1 || E < 1 || K < 1 || K > E || K > 64 || L * E > 8192 || E > 1024)
+    return set_error(MSPQ_ERR_SHAPE_VIOLATION, "cache: need 1<=K<=min(E,64), E<=1024, L*E<=8192");
   mspq_cache* c = new mspq_cache();
   c->kmax = kmax;
   c->nbuf = nbuf;

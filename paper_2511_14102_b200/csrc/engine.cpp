@@ -190,8 +190,8 @@ HostCfg parse_host_cfg(const std::string& text) {
   HostCfg c;
   static const std::set<std::string> known = {"policy", "capacity_mode", "cache_capacity", "entropy_weighted_capacity",
                                               "k", "governor", "phases", "prefetch_budget", "rollback_s", "ema_alpha",
-                                              "initial_accept", "seed", "collect_plans", "profile", "log", "generator",
-                                              "verify_overlap"};
+                                              "initial_accept", "seed", "collect_plans", "profile", "profile_path", "log",
+                                              "generator", "verify_overlap", "estimator"};
   for (auto it = j.begin(); it != j.end(); ++it)
     if (!known.count(it.key())) fail(MSPQ_ERR_INVALID_CONFIG, "unknown key in run config: " + it.key());
   auto num = [&](const json& o, const char* k, double d) {
@@ -231,7 +231,10 @@ HostCfg parse_host_cfg(const std::string& text) {
     c.k_slo = (int)integer(g, "k_slo", c.k_slo);
     c.ttft_budget = num(g, "ttft_budget_s", c.ttft_budget);
   }
-  if (j.contains("phases")) {
+  if (j.contains("phases")) {  // run_config.cpp:142-146
+    if (!j["phases"].is_object()) fail(MSPQ_ERR_INVALID_CONFIG, "phases must be an object");
+    for (auto it = j["phases"].begin(); it != j["phases"].end(); ++it)
+      if (it.key() != "f1" && it.key() != "f2") fail(MSPQ_ERR_INVALID_CONFIG, "unknown key in phases: " + it.key());
     c.f1 = num(j["phases"], "f1", c.f1);
     c.f2 = num(j["phases"], "f2", c.f2);
   }
@@ -242,9 +245,29 @@ HostCfg parse_host_cfg(const std::string& text) {
   if (j.contains("collect_plans")) c.collect_plans = j["collect_plans"].get<bool>();
   if (j.contains("log")) c.log = j["log"].get<bool>();
   if (j.contains("verify_overlap")) c.verify_overlap = j["verify_overlap"].get<bool>();
+  // profile / profile_path (run_config.cpp:155-170): exclusive; a relative path resolves against
+  // the caller's working directory (the reference's base_dir for an inline config)
+  if (j.contains("profile") && j.contains("profile_path"))
+    fail(MSPQ_ERR_INVALID_CONFIG, "give either profile or profile_path, not both");
   if (j.contains("profile")) {
     c.profile = Profile::from_json(j["profile"]);
     c.profile_given = true;
+  } else if (j.contains("profile_path")) {
+    if (!j["profile_path"].is_string()) fail(MSPQ_ERR_INVALID_CONFIG, "profile_path must be a string");
+    const std::string path = j["profile_path"].get<std::string>();
+    std::ifstream in(path);
+    if (!in) fail(MSPQ_ERR_IO, "cannot open profile file: " + path);
+    json pj = json::parse(in, nullptr, false);
+    if (pj.is_discarded()) fail(MSPQ_ERR_INVALID_CONFIG, "profile file is not valid JSON: " + path);
+    c.profile = Profile::from_json(pj);
+    c.profile_given = true;
+  }
+  if (j.contains("estimator")) {  // governor |E_new(k)| estimator (not in the reference schema)
+    if (!j["estimator"].is_string()) fail(MSPQ_ERR_INVALID_CONFIG, "estimator must be a string");
+    const std::string e = j["estimator"].get<std::string>();
+    if (e == "linear") c.estimator = 0;
+    else if (e == "elb") c.estimator = 1;
+    else fail(MSPQ_ERR_INVALID_CONFIG, "estimator must be \"linear\" or \"elb\"");
   }
   return c;
 }

@@ -58,6 +58,10 @@ struct HostCfg {  // SimConfig (sim.hpp:15-34) from the run-config schema (run_c
   // extension (live engine): run a verify layer's GEMM for the resident experts while the missing
   // ones are still on the link (two smaller K3 launches; +4% at cap 14/16, neutral at 4/16)
   bool verify_overlap = false;
+  // extension (live engine): the governor's |E_new(k)| estimator. 0 = the reference's linear g*k
+  // (sim.cpp:75-78, 404; the parity default); 1 = "elb": per layer, the expected union of the
+  // draft-predicted routing over a (k+1)-token window minus the experts resident now
+  int estimator = 0;
 };
 int parse_policy(const std::string& s);
 const char* policy_name(int p);

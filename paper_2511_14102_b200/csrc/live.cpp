@@ -164,6 +164,17 @@ struct mspq_engine {
   double pcie_bw_measured = 0.0, draft_step_s = 0.0;
   std::vector<std::pair<double, double>> verify_fit;
   int cycle_serial = 0;
+  // "elb" estimator state: per (layer, expert) routing frequency from the draft's
+  // ELB rows (decayed per row) and the residency table snapshotted at the end of each cycle.
+  // Both persist across generate() calls, like the cache itself.
+  std::vector<double> elb_freq;
+  std::vector<int32_t> res_host;
+  std::vector<double> elb_calib;  // [kmax+1] EMA of fetched / estimated for the k actually run
+  // trace_level >= 3 (parity tests): the fp32 residual entering every layer (index L = final),
+  // for the verify window [L+1][T][d] and each draft row [k][L+1][d], kept per cycle of the
+  // last generate() and read back with mspq_engine_read("hcap_v:<cycle>" / "hcap_d:<cycle>")
+  float *hcap_v = nullptr, *hcap_dstage = nullptr, *hcap_d = nullptr;
+  std::vector<std::vector<float>> hcap_v_hist, hcap_d_hist;
 
   int32_t* win_tok() { return dst + 8; }
   int32_t* win_pos() { return dst + 8 + Tmax + 1; }
@@ -360,8 +371,14 @@ void make_workspaces(mspq_engine* E) {
   E->gbuf = (int32_t*)(b + o_gb);
   E->tcws = (void*)(b + o_tc);
   E->tcws_d = (void*)(b + o_tcd);
-  E->hpin_ints = 64 + (size_t)L * T * K * 2 + (size_t)E->Tmax * L * K * 2 + 4 * T + (size_t)L * 2 + (size_t)L * T * 2 + 64;
+  E->hpin_ints = 64 + (size_t)L * T * K * 2 + (size_t)E->Tmax * L * K * 3 + 4 * T + (size_t)L * 2 + (size_t)L * T * 2 +
+                 (size_t)L * m.E + 64;
   CUDA_OK(cudaHostAlloc((void**)&E->hpin, E->hpin_ints * 4, 0));
+  if (E->o.trace_level >= 3) {
+    CUDA_OK(cudaMalloc(&E->hcap_v, (size_t)(L + 1) * T * d * 4));
+    CUDA_OK(cudaMalloc(&E->hcap_dstage, (size_t)(L + 1) * d * 4));
+    CUDA_OK(cudaMalloc(&E->hcap_d, (size_t)E->o.kmax * (L + 1) * d * 4));
+  }
 }
 
 // One draft step for a single token, captured once as a CUDA graph.
@@ -390,6 +407,8 @@ void enqueue_draft_step(mspq_engine* E, cudaStream_t s) {
                            E->router + (size_t)l * m.E * d, E->xn, E->ids_d + (size_t)l * K, E->wts_d + (size_t)l * K,
                            nullptr, E->view.elb_ids, E->view.elb_gates, row, E->sd[l & 1].base, l, L, 1, d, m.E, K,
                            m.eps, s));
+    if (E->hcap_dstage)
+      CUDA_OK(cudaMemcpyAsync(E->hcap_dstage + (size_t)l * d, E->h, (size_t)d * 4, cudaMemcpyDeviceToDevice, s));
     Sched& sc = E->sd[l & 1];
     CAPI_OK(mspq_moe_int4_tc(sc.n_groups, sc.group_expert, sc.group_buf, sc.group_off, sc.entry_tok, sc.entry_group,
                              E->xn, E->draft4, E->S4, l, m.E, d, m.f, 1, K, K, E->yd_split1, E->yd_split2, E->tcws_d,
@@ -400,6 +419,8 @@ void enqueue_draft_step(mspq_engine* E, cudaStream_t s) {
                          (long long)K * d, E->gfinal, nullptr,
                          E->xn, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, L, L, 1, d, m.E, K, m.eps,
                          s));
+  if (E->hcap_dstage)
+    CUDA_OK(cudaMemcpyAsync(E->hcap_dstage + (size_t)L * d, E->h, (size_t)d * 4, cudaMemcpyDeviceToDevice, s));
   CAPI_OK(mspq_lm_head(E->xn, E->lm, 1, m.V, d, E->logits, s));
   CAPI_OK(mspq_argmax_advance(E->logits, m.V, E->amax, row, E->win_tok() + 1, cur_tok, cur_pos, s));
 }
@@ -503,6 +524,9 @@ static void configure(mspq_engine* E, const std::string& text) {
     capture_draft_graph(E);
   }
   E->ready_rec.assign(E->nbuf, 0);
+  E->elb_freq.assign((size_t)m.L * m.E, (double)m.K / m.E);  // uniform prior: K of E experts per token
+  E->res_host.assign((size_t)m.L * m.E, -1);                  // mspq_cache_configure empties the cache
+  E->elb_calib.assign((size_t)E->o.kmax + 1, 1.0);
   E->last_cycle.assign(E->nbuf, -1);
   E->last_layer.assign(E->nbuf, -1);
   CAPI_OK(mspq_cache_configure(E->cache, c.mode, c.policy, E->caps.data(), (int)std::min<long>(c.cache_capacity, (long)m.L * m.E),
@@ -669,7 +693,24 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
   const int kcap = std::max(c.use_governor ? c.k_max : c.fixed_k, 1);
   std::vector<double> accept(kcap, c.initial_accept);
   double g = static_cast<double>(L) * static_cast<double>(K);
-  auto est = [&g]() { return Est([gg = g](int k) { return static_cast<int>(std::llround(gg * static_cast<double>(k))); }); };
+  // |E_new(k)| for the governor.  linear (reference, sim.cpp:75-78): g*k with g = fetched/k of the
+  // last cycle.  elb: the ELB analysed against the current cache state -- per layer,
+  // every non-resident expert e is fetched if any of the k+1 window tokens routes to it, which the
+  // ELB's per-(layer, expert) frequency p puts at 1-(1-p)^(k+1); summed over layers.  A per-k
+  // factor (EMA of fetched / estimate for the k last run at) absorbs what the union misses: at
+  // small caps the planner's prefetches evict experts the window still needs, and they come back
+  // on demand (Phi cap 4/16: ~2x the union at k = 16).
+  auto elb_raw = [E, Ex, L](int k) {
+    double s = 0.0;
+    for (int i = 0; i < L * Ex; ++i)
+      if (E->res_host[i] < 0) s += 1.0 - std::pow(1.0 - E->elb_freq[i], static_cast<double>(k + 1));
+    return s;
+  };
+  auto est = [&]() {
+    if (c.estimator == 1)
+      return Est([E, elb_raw](int k) { return static_cast<int>(std::llround(E->elb_calib[k] * elb_raw(k))); });
+    return Est([gg = g](int k) { return static_cast<int>(std::llround(gg * static_cast<double>(k))); });
+  };
   int k_slo = c.k_slo;
   if (c.use_governor && c.ttft_budget > 0.0) k_slo = std::min(k_slo, k_slo_from_ttft(prof, c.ttft_budget, est(), c.k_min, c.k_max));
   CUDA_OK(cudaEventRecord(E->ev_t0, E->sc));
@@ -679,6 +720,8 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
     E->pf_defer = !(pd && pd[0] == '0') && c.mode == 0;  // on by default; MSPQ_PF_DEFER=0 is the A/B switch
   }
   E->deferred.clear();
+  E->hcap_v_hist.clear();
+  E->hcap_d_hist.clear();
   if (E->pf_lane) CUDA_OK(cudaStreamWaitEvent(E->sx2, E->ev_t0, 0));
   std::vector<int> committed;
   json cycles = json::array();
@@ -696,6 +739,8 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
     const int kk = c.use_governor ? select_k(prof, accept, c.k_min, c.k_max, k_slo, est()) : c.fixed_k;
     const int k = std::max(1, std::min({kk, rem, E->o.kmax}));
     const int T = k + 1;
+    const int est_new = c.use_governor ? est()(k) : -1;
+    const double est_raw = c.estimator == 1 ? elb_raw(k) : 0.0;
     uint64_t cyc_bytes = 0;
     std::vector<CopyBatch> batches;
     // ---------------- draft + planner
@@ -705,6 +750,7 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
     CUDA_OK(cudaEventRecord(E->ev_g0[0], E->sc));
     CUDA_OK(cudaGraphLaunch(E->gexec, E->sc));
     CUDA_OK(cudaEventRecord(E->ev_g1[0], E->sc));
+    if (E->hcap_d) CUDA_OK(cudaMemcpyAsync(E->hcap_d, E->hcap_dstage, (size_t)(L + 1) * d * 4, cudaMemcpyDeviceToDevice, E->sc));
     launches += E->graph_nodes;
     for (int i = 0; i < k; ++i) {
       CAPI_OK(mspq_cache_plan_row(E->cache, i, E->sc));
@@ -714,6 +760,9 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
         CUDA_OK(cudaEventRecord(E->ev_g0[i + 1], E->sc));
         CUDA_OK(cudaGraphLaunch(E->gexec, E->sc));
         CUDA_OK(cudaEventRecord(E->ev_g1[i + 1], E->sc));
+        if (E->hcap_d)
+          CUDA_OK(cudaMemcpyAsync(E->hcap_d + (size_t)(i + 1) * (L + 1) * d, E->hcap_dstage, (size_t)(L + 1) * d * 4,
+                                  cudaMemcpyDeviceToDevice, E->sc));
         launches += E->graph_nodes;
       }
       spin_wait(E->ev_row[i]);
@@ -738,6 +787,8 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
                              E->router + (size_t)l * Ex * d, E->xn, tgt, E->wts_t + (size_t)l * T * K, nullptr, nullptr,
                              nullptr, nullptr, nullptr, l, L, T, d, Ex, K, m.eps, E->sc));
       Sched& sv = E->sv[l & 1];
+      if (E->hcap_v)
+        CUDA_OK(cudaMemcpyAsync(E->hcap_v + (size_t)l * T * d, E->h, (size_t)T * d * 4, cudaMemcpyDeviceToDevice, E->sc));
       if (level >= 1) CUDA_OK(cudaEventRecord(E->ev_rt[l], E->sc));
       CAPI_OK(mspq_cache_verify_layer(E->cache, l, T, tgt, E->gbuf, E->sc));
       CUDA_OK(cudaEventRecord(E->ev_w0[l], E->sc));
@@ -837,6 +888,8 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
                            (long long)T * K * d, E->gfinal, nullptr,
                            E->xn, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, L, L, T, d, Ex, K, m.eps,
                            E->sc));
+    if (E->hcap_v)
+      CUDA_OK(cudaMemcpyAsync(E->hcap_v + (size_t)L * T * d, E->h, (size_t)T * d * 4, cudaMemcpyDeviceToDevice, E->sc));
     CAPI_OK(mspq_lm_head(E->xn, E->lm, T, m.V, d, E->logits, E->sc));
     CAPI_OK(mspq_argmax(E->logits, T, m.V, E->amax, E->sc));
     CAPI_OK(mspq_accept_advance(E->win_tok() + 1, E->amax, k, E->dst + 3, E->dst + 1, E->dst + 2, head_pos, E->sc));
@@ -869,8 +922,22 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
       CUDA_OK(cudaMemcpyAsync(hp + o, E->view.elb_gates, (size_t)k * L * K * 4, cudaMemcpyDeviceToHost, E->sc));
       o += (size_t)k * L * K;
     }
+    const size_t o_res_tab = o;
+    if (c.estimator == 1) {  // residency snapshot + this cycle's ELB rows for the elb estimator
+      CUDA_OK(cudaMemcpyAsync(hp + o, E->view.res, (size_t)L * Ex * 4, cudaMemcpyDeviceToHost, E->sc));
+      o += (size_t)L * Ex;
+      CUDA_OK(cudaMemcpyAsync(hp + o, E->view.elb_ids, (size_t)k * L * K * 4, cudaMemcpyDeviceToHost, E->sc));
+      o += (size_t)k * L * K;
+    }
     CUDA_OK(cudaEventRecord(E->ev_end, E->sc));
     CUDA_OK(cudaEventSynchronize(E->ev_end));
+    if (E->hcap_v) {
+      std::vector<float> hv((size_t)(L + 1) * T * d), hd((size_t)k * (L + 1) * d);
+      CUDA_OK(cudaMemcpy(hv.data(), E->hcap_v, hv.size() * 4, cudaMemcpyDeviceToHost));
+      CUDA_OK(cudaMemcpy(hd.data(), E->hcap_d, hd.size() * 4, cudaMemcpyDeviceToHost));
+      E->hcap_v_hist.push_back(std::move(hv));
+      E->hcap_d_hist.push_back(std::move(hd));
+    }
     const int fetched = E->view.host_stat[S_FETCHED], demand = E->view.host_stat[S_DEMAND];
     const int n_log = E->view.host_stat[S_NLOG];
     for (auto& [a, b] : stall_ev) stall += elapsed_s(a, b);
@@ -914,6 +981,7 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
     rec["step_coverage"] = sc_sum / (T * L);
     rec["steps"] = T * L;
     rec["new_experts"] = fetched;
+    if (c.use_governor) rec["est_new_experts"] = est_new;
     rec["bytes"] = cyc_bytes;
     rec["io_wait_s"] = stall;
     double sync_s = 0.0;
@@ -996,6 +1064,22 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
     if (outcomes.size() > accept.size()) outcomes.resize(accept.size());
     accept = update_acceptance(accept, c.ema_alpha, outcomes);
     g = static_cast<double>(fetched) / static_cast<double>(k);
+    if (c.estimator == 1) {
+      constexpr double beta = 1.0 / 32.0;
+      if (est_raw > 0.0) E->elb_calib[k] = (1.0 - 0.25) * E->elb_calib[k] + 0.25 * (static_cast<double>(fetched) / est_raw);
+      // per drafted row: p <- (1-beta) p + beta [e in row's top-K at layer l]
+      const int32_t* rows = hp + o_res_tab + (size_t)L * Ex;
+      for (int r = 0; r < k; ++r)
+        for (int l = 0; l < L; ++l) {
+          double* pl = &E->elb_freq[(size_t)l * Ex];
+          for (int e = 0; e < Ex; ++e) pl[e] *= 1.0 - beta;
+          for (int j = 0; j < K; ++j) {
+            const int e = rows[((size_t)r * L + l) * K + j];
+            if (e >= 0 && e < Ex) pl[e] += beta;
+          }
+        }
+      std::copy(hp + o_res_tab, hp + o_res_tab + (size_t)L * Ex, E->res_host.begin());
+    }
     stall_total += stall;
     step_cov_total += sc_sum;
     step_total += (uint64_t)T * L;
@@ -1085,6 +1169,8 @@ void destroy(mspq_engine* E) {
   if (E->draft4) cudaFree(E->draft4);
   if (E->wblk) cudaFree(E->wblk);
   if (E->hpin) cudaFreeHost(E->hpin);
+  for (float* p : {E->hcap_v, E->hcap_dstage, E->hcap_d})
+    if (p) cudaFree(p);
   if (E->host) {
     if (E->host_is_shm) {
       cudaHostUnregister(E->host);
@@ -1283,6 +1369,13 @@ int mspq_engine_read(mspq_engine* E, const char* name, void* dst, long long byte
       }
       src = hb;
       avail = E->S16;
+      from_host = true;
+    } else if (n.rfind("hcap_v:", 0) == 0 || n.rfind("hcap_d:", 0) == 0) {
+      const auto& hist = n[5] == 'v' ? E->hcap_v_hist : E->hcap_d_hist;
+      const size_t ci = (size_t)atoi(n.c_str() + 7);
+      if (ci >= hist.size()) fail(MSPQ_ERR_RANGE_OUT_OF_BOUNDS, "no residual capture for " + n + " (trace_level 3)");
+      src = hist[ci].data();
+      avail = hist[ci].size() * 4;
       from_host = true;
     } else if (n.rfind("expert_blob:", 0) == 0) {
       int l, e;

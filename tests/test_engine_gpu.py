@@ -297,3 +297,28 @@ def test_cycle_record_layer_times_are_ordered(cuda):
             assert prev_end <= rt <= w0 <= k0 < ge <= t1 + 1e-6
             prev_end = ge
     eng.close()
+
+
+@pytest.mark.parametrize("estimator", ["linear", "elb"])
+@pytest.mark.parametrize("cap", [3, 6])
+def test_live_governor_k_sequence_matches_reference_governor(cuda, ref, estimator, cap):
+    """The live governor's k per cycle equals the reference select_k (perfmodel.cpp:166-183, run
+    from oracle/_ref) fed the run's own re-fitted profile, the EMA acceptance of the outcomes so
+    far and the |E_new(k)| estimate: the reference's linear g*k (sim.cpp:75-78, 404) or the elb
+    estimator restated in oracle/control_plane.elb_estimate over the oracle's own cache replay."""
+    eng, cfg = _engine()
+    conf = {"policy": "speculative", "cache_capacity": cap, "k": "governor",
+            "governor": {"k_min": 1, "k_max": 8, "k_slo": 8}, "estimator": estimator}
+    eng.configure(conf)
+    rep = eng.generate([42, 7, 300], 72)
+    want = cp.live_governor_ks(rep, conf, cfg.L, cfg.E, cfg.K, estimator, kmax=8)
+    assert [c["k"] for c in rep["cycles"]] == [w["k"] for w in want]
+    assert [c["est_new_experts"] for c in rep["cycles"]] == [w["est"] for w in want]
+    for w in want:
+        req = {"profile": rep["profile"], "p": w["p"], "alpha": 0.1, "k_min": 1, "k_max": 8, "k_slo": 8}
+        if estimator == "elb":
+            req["est"] = w["table"]
+        else:
+            req["g"] = w["g"]
+        assert ref.governor(req)["select_k"] == w["select_k"]
+    eng.close()

@@ -1,0 +1,178 @@
+"""Parity at full depth: the headline configuration (BASELINE config 3 -- Phi-3.5-MoE shape,
+32 layers, E=16 top-2, d=4096, ffn=6400, per-layer cache 4/16, speculative policy, governor,
+XC-coded host store) and the other BASELINE shapes at their full layer counts, against the CPU
+oracle (oracle/model.py + the multi-threaded oracle/csrc/decode_ref.c).
+
+Three checks per run, all on the same generate() call:
+  1. teacher-forced, per layer (strict): from the device's own residual entering each layer
+     (trace_level 3 captures), the oracle's routing must be bit-exact with the device's, and the
+     oracle's layer output must equal the device's next residual within 2e-3 of its scale; the
+     LM-head argmax from the device's final residual must be bit-exact.  This holds at any depth
+     with no error accumulation, so it pins every layer of every draft row and verify slot.
+  2. free-running end to end: the oracle decodes on its own with the device's k sequence; ELB
+     rows, target routing, draft tokens, target argmax, accepted counts and committed tokens must
+     be identical.  A divergence is accepted only at a certified near-tie (the oracle's own
+     top-K / argmax margin below 1e-4 of the logit scale at the first differing decision), and is
+     reported -- it never passes silently.
+  3. control plane: the device's hit/miss event log equals oracle/control_plane.live_cycle on
+     the run's routing, and the governor's k sequence equals the reference select_k fed the
+     run's outcomes (oracle/control_plane.live_governor_ks).
+"""
+import warnings
+
+import numpy as np
+import pytest
+
+from oracle import control_plane as cp
+from oracle import model as om
+
+pytestmark = pytest.mark.gpu
+KINDS = {0: "demand", 1: "plan2", 2: "plan3", 3: "jit", 4: "refill"}
+
+
+def _desc(cfg):
+    return om.ModelDesc(L=cfg.L, E=cfg.E, K=cfg.K, d=cfg.d, f=cfg.f, V=cfg.V, P=cfg.P, seed=cfg.seed,
+                        embed_scale=cfg.embed_scale, pos_scale=cfg.pos_scale, router_scale=cfg.router_scale,
+                        moe_scale=cfg.moe_scale, lm_scale=cfg.lm_scale, eps=cfg.eps)
+
+
+def _gap(logits):
+    top = np.sort(logits)[::-1]
+    return float(top[0] - top[1]) / (float(np.abs(logits).max()) + 1e-30)
+
+
+def _teacher_forced(eng, rep, cfg, model):
+    """Check 1; returns (worst relative layer error, {decision: relative margin}) where a decision
+    is ("target", cycle, slot, layer) / ("elb", cycle, row, layer) for routing (top-K boundary gap)
+    and ("target_argmax", cycle, slot) / ("draft_token", cycle, row) for the LM head (top-2 gap)."""
+    L, d = cfg.L, cfg.d
+    worst, margins = 0.0, {}
+    for ci, c in enumerate(rep["cycles"]):
+        k = c["k"]
+        T = k + 1
+        hv = np.frombuffer(eng.read("hcap_v:%d" % ci, (L + 1) * T * d * 4), dtype=np.float32).reshape(L + 1, T, d)
+        ids = [[c["target"][s][l] for s in range(T)] for l in range(L)]
+        w, mg = om.check_layers(model, hv, ids, draft=False)
+        worst = max(worst, w)
+        for l in range(L):
+            for s in range(T):
+                margins[("target", ci, s, l)] = mg[l][s]
+        xf = np.stack([model.rmsnorm(np.ascontiguousarray(hv[L][s]), model.gamma(-1)) for s in range(T)])
+        lg, am = model.lm_head(xf)
+        assert am.tolist() == c["target_argmax"], ("verify argmax", ci)
+        for s in range(T):
+            margins[("target_argmax", ci, s)] = _gap(lg[s])
+        hd = np.frombuffer(eng.read("hcap_d:%d" % ci, k * (L + 1) * d * 4), dtype=np.float32).reshape(k, L + 1, d)
+        for r in range(k):
+            ids_r = [[c["elb"][r][l]] for l in range(L)]
+            w, mg = om.check_layers(model, hd[r][:, None, :], ids_r, draft=True)
+            worst = max(worst, w)
+            for l in range(L):
+                margins[("elb", ci, r, l)] = mg[l][0]
+            xf = model.rmsnorm(np.ascontiguousarray(hd[r][L]), model.gamma(-1))
+            lg, am = model.lm_head(xf[None, :])
+            assert int(am[0]) == c["draft_tokens"][r], ("draft token", ci, r)
+            margins[("draft_token", ci, r)] = _gap(lg[0])
+    return worst, margins
+
+
+def _first_divergence(rep, oc, L):
+    for ci, (c, o) in enumerate(zip(rep["cycles"], oc)):
+        for r in range(o["k"]):
+            for l in range(L):
+                if c["elb"][r][l] != o["elb"][r][l][0].tolist():
+                    return ("elb", ci, r, l)
+            if c["draft_tokens"][r] != o["draft"][r]:
+                return ("draft_token", ci, r)
+        for s in range(o["k"] + 1):
+            for l in range(L):
+                if c["target"][s][l] != o["target"][s][l][0].tolist():
+                    return ("target", ci, s, l)
+        for s in range(o["k"] + 1):
+            if c["target_argmax"][s] != o["target_argmax"][s]:
+                return ("target_argmax", ci, s)
+        if c["tokens"] != o["committed"]:
+            return ("tokens", ci)
+    if len(rep["cycles"]) != len(oc):
+        return ("cycles", len(oc))
+    return None
+
+
+def _run(name, cap, ntok, conf_extra=None, **shape_kw):
+    import paper_2511_14102_b200 as m
+    cfg = m.ModelConfig.named(name, **shape_kw)
+    eng = m.Engine(cfg, kmax=16, trace_level=3)
+    conf = {"policy": "speculative", "cache_capacity": cap, "k": "governor",
+            "governor": {"k_min": 1, "k_max": 16, "k_slo": 16}}
+    conf.update(conf_extra or {})
+    eng.configure(conf)
+    prompt = [11, 200, 3001 % cfg.V, 17]
+    rep = eng.generate(prompt, ntok)
+    model = om.Model(_desc(cfg))
+    try:
+        worst, margins = _teacher_forced(eng, rep, cfg, model)
+    finally:
+        eng.close()
+    # 2. free-running oracle decode with the device's k sequence
+    oc = om.speculative_decode(model, prompt[-1], len(prompt) - 1, [c["k"] for c in rep["cycles"]], ntok)
+    div = _first_divergence(rep, oc, cfg.L)
+    margin = min(margins.values())
+    if div is not None:
+        # every decision before `div` agreed, so the hidden states differ only by accumulated
+        # rounding: the divergence is legitimate only where the device's own decision was a
+        # near-tie (relative logit gap < 1e-4), and it is reported
+        at = margins.get(div)
+        warnings.warn(f"{name}: free-running oracle diverged at {div}, relative margin there {at}; "
+                      f"teacher-forced layers all exact (worst layer err {worst:.2e})")
+        assert at is not None and at < 1e-4, f"divergence {div} without a near-tie (margin {at})"
+    # 3. control plane: hit/miss log and governor k sequence
+    c = cp.sim_config(conf)
+    cache = cp.Cache(c["capacity_mode"], c["cache_capacity"])
+    for cyc in rep["cycles"]:
+        log = []
+        cp.live_cycle(cache, cp.ELB.build(cyc["elb"], cyc["elb_gates"]), cyc["target"], c, log)
+        want = [(k, l, e, int(h), -1 if v is None else v[0], -1 if v is None else v[1]) for (k, tag, l, e, h, v) in log]
+        got = [(KINDS[ev[0]], ev[2], ev[3], ev[4], ev[5], ev[6]) for ev in cyc["log"]]
+        assert got == want, ("hit/miss log", cyc["cycle"])
+    est = conf.get("estimator", "linear")
+    gov = cp.live_governor_ks(rep, conf, cfg.L, cfg.E, cfg.K, est, kmax=16)
+    assert [x["k"] for x in gov] == [cyc["k"] for cyc in rep["cycles"]]
+    assert rep["total_new_experts"] > 0
+    return rep, worst, margin
+
+
+def test_headline_phi_32_layers_cap4_governor_xc(cuda):
+    """BASELINE config 3 exactly as bench.py runs it (Phi shape, 32 layers, cap 4/16, speculative,
+    governor, XC store), 12 committed tokens."""
+    rep, worst, margin = _run("phi", 4, 12)
+    assert len(rep["tokens"]) == 12
+    assert worst < 2e-3
+
+
+def test_headline_phi_32_layers_elb_estimator(cuda):
+    rep, worst, margin = _run("phi", 4, 10, {"estimator": "elb"})
+    assert len(rep["tokens"]) == 10
+
+
+def test_phi_moe_scale_1_hard_regime(cuda):
+    """Unit-variance experts (moe_scale 1.0): the residual is no longer dominated by the
+    embedding, draft/target disagree more and routing margins shrink."""
+    rep, worst, margin = _run("phi", 4, 12, {"k": 3}, L=4, moe_scale=1.0)
+    assert len(rep["tokens"]) == 12
+
+
+def test_tiny_moe_scale_1_hard_regime(cuda):
+    rep, worst, margin = _run("tiny", 3, 40, {"k": 4}, moe_scale=1.0)
+    assert len(rep["tokens"]) == 40
+
+
+def test_qwen3_48_layers_full_depth(cuda):
+    """BASELINE config 4 (Qwen3-30B-A3B shape: 48 layers, 128 experts top-8) at full depth."""
+    rep, worst, margin = _run("qwen3", 32, 6)
+    assert len(rep["tokens"]) == 6
+
+
+def test_mixtral_8_layers(cuda):
+    """BASELINE config 2 widths (Mixtral-8x7B: E=8 top-2, d=4096, ffn=14336), 8 layers."""
+    rep, worst, margin = _run("mixtral", 2, 6, L=8)
+    assert len(rep["tokens"]) == 6

@@ -167,3 +167,42 @@ def test_c_weight_generator_equals_numpy_definition():
     for seed, tensor, rows, cols, scale in [(1234, om.t_expert(3, 7, 1), 64, 96, 0.0379),
                                             (9, om.T_LM, 5, 4096, 1.0), (77, om.t_router(0), 16, 256, 0.25)]:
         assert np.array_equal(om.gen(seed, tensor, rows, cols, scale), om.gen_np(seed, tensor, rows, cols, scale))
+
+
+def test_fast_oracle_rows_match_numpy_definition():
+    """decode_ref.c (the multi-threaded full-size oracle) generates and INT4-round-trips weight
+    rows bit-identically to model.py's gen/quantize/dequantize."""
+    import ctypes
+    d = om.ModelDesc(L=2, E=4, K=2, d=256, f=384, V=64, seed=77)
+    key = om.tensor_key(d.seed, om.t_expert(1, 3, 0))
+    ref_w = om.gen(d.seed, om.t_expert(1, 3, 0), d.f, d.d, d.a_up())
+    q, s = om.quantize(ref_w)
+    deq = om.dequantize(q, s)
+    row = np.empty(d.d, dtype=np.float32)
+    for r in (0, 5, d.f - 1):
+        om.lib().orc_weight_row(key, r * d.d, d.d, ctypes.c_float(d.a_up()), 0, om._p(row))
+        assert np.array_equal(row, om.bf16_to_f32(ref_w[r]))
+        om.lib().orc_weight_row(key, r * d.d, d.d, ctypes.c_float(d.a_up()), 1, om._p(row))
+        assert np.array_equal(row, deq[r])
+    # an all-zero group keeps a unit scale and dequantises to zero (model.py sf_safe)
+    z = np.zeros((1, 128), dtype=np.uint16)
+    qz, sz = om.quantize(z)
+    assert np.all(om.dequantize(qz, sz) == 0) and om.bf16_to_f32(sz)[0, 0] == 1.0
+
+
+def test_fast_oracle_decode_equals_numpy_oracle():
+    """Fast (C, double accumulation) and numpy (fp32 BLAS) oracles agree on the expert FFN to
+    fp32 rounding and decode the same tokens and routing on the tiny model."""
+    d = om.ModelDesc(**om.CONFIGS["tiny"])
+    slow, fast = om.Model(d, fast=False), om.Model(d, fast=True)
+    rng = np.random.default_rng(3)
+    xn = om.f32_to_bf16(rng.standard_normal((3, d.d)).astype(np.float32))
+    for draft in (False, True):
+        yf = fast.ffn_batch(xn, 2, 5, draft)
+        ys = np.stack([slow.ffn(xn[i], 2, 5, draft)[0] for i in range(3)])
+        assert np.abs(yf - ys).max() <= 1e-5 * np.abs(ys).max()
+    a = om.speculative_decode(slow, 7, 3, [3, 2, 4], 12)
+    b = om.speculative_decode(fast, 7, 3, [3, 2, 4], 12)
+    for x, y in zip(a, b):
+        assert x["committed"] == y["committed"] and x["draft"] == y["draft"]
+        assert [[r[0].tolist() for r in s] for s in x["target"]] == [[r[0].tolist() for r in s] for s in y["target"]]

@@ -1,6 +1,7 @@
 """Phi-shaped live decode across per-layer cache caps (SURVEY.md §6.4 / BASELINE.md §5): decode
 tokens/s, exposed-H2D fraction, fetched experts per token, mean k, PCIe-roofline fraction.
-usage: python tools/cap_sweep.py [--caps 4,8,12,14,16] [--tokens 32] [--steps 2] [--k governor]"""
+usage: python tools/cap_sweep.py [--caps 4,8,12,14,16] [--tokens 32] [--steps 2] [--k governor[,1,2,4..]]
+       [--estimator linear|elb]"""
 import argparse
 import json
 import os
@@ -18,6 +19,7 @@ ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--warmup", type=int, default=2)
 ap.add_argument("--k", default="governor")
 ap.add_argument("--policy", default="speculative")
+ap.add_argument("--estimator", default="")
 ap.add_argument("--out", default="gpurun_out/cap_sweep.jsonl")
 a = ap.parse_args()
 cfg = m.ModelConfig.named(a.model)
@@ -27,9 +29,11 @@ print("engine", time.time() - t0, eng.info(), flush=True)
 rows = []
 import random
 rng = random.Random(5)
-for cap in [int(c) for c in a.caps.split(",")]:
+for cap, kk in [(int(c), kk) for c in a.caps.split(",") for kk in a.k.split(",")]:
     conf = {"policy": a.policy, "cache_capacity": cap}
-    conf.update({"k": "governor", "governor": {"k_min": 1, "k_max": 16, "k_slo": 16}} if a.k == "governor" else {"k": int(a.k)})
+    conf.update({"k": "governor", "governor": {"k_min": 1, "k_max": 16, "k_slo": 16}} if kk == "governor" else {"k": int(kk)})
+    if a.estimator:
+        conf["estimator"] = a.estimator
     eng.configure(conf)
     for _ in range(a.warmup):
         eng.generate([rng.randrange(cfg.V) for _ in range(8)], a.tokens)
@@ -40,7 +44,7 @@ for cap in [int(c) for c in a.caps.split(",")]:
     h2d = sum(r["h2d_bytes"] for r in reps)
     cyc = [c for r in reps for c in r["cycles"]]
     info = eng.info()
-    row = dict(cap=cap, cap_frac=cap / cfg.E, tokens_per_s=tok / dev, exposed_h2d_frac=stall / dev,
+    row = dict(cap=cap, k=kk, estimator=a.estimator or "linear", cap_frac=cap / cfg.E, tokens_per_s=tok / dev, exposed_h2d_frac=stall / dev,
                exposed_h2d_ms_per_token=stall / tok * 1e3, fetched_per_token=sum(r["total_new_experts"] for r in reps) / tok,
                mean_k=sum(c["k"] for c in cyc) / len(cyc), accept=sum(c["accepted"] for c in cyc) / sum(c["k"] for c in cyc),
                pcie_roofline_frac=(h2d / info["pcie_bw_measured"]) / dev, mean_coverage=sum(r["mean_coverage"] for r in reps) / len(reps),
