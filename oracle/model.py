@@ -369,11 +369,12 @@ class Model:
         return int(am[0]), routing, logits[0]
 
 
-def forward_batch(model: Model, toks, poss, draft: bool, h_in=None):
+def forward_batch(model: Model, toks, poss, draft: bool, h_in=None, h_trace=None):
     """forward() for M independent tokens, layer-major with tokens grouped by expert (one weight
     generation per (layer, expert) in fast mode).  Returns [(argmax, routing)] per token.
     With `h_in` = {layer: [M, d] fp32}, the residual entering that layer is replaced
-    (teacher forcing from the device)."""
+    (teacher forcing from the device).  `h_trace` (a list) receives the [M, d] residual entering
+    each layer and, last, the final one."""
     m = model.m
     M = len(toks)
     h = np.stack([(bf16_to_f32(model.embed_row(t)) + bf16_to_f32(model.pos_row(p))).astype(np.float32)
@@ -382,6 +383,8 @@ def forward_batch(model: Model, toks, poss, draft: bool, h_in=None):
     for l in range(m.L):
         if h_in is not None and l in h_in:
             h = np.asarray(h_in[l], dtype=np.float32).copy()
+        if h_trace is not None:
+            h_trace.append(h.copy())
         xn = np.stack([model.rmsnorm(np.ascontiguousarray(h[i]), model.gamma(l)) for i in range(M)])
         rt = [model.route(xn[i], l) for i in range(M)]
         for i in range(M):
@@ -401,6 +404,8 @@ def forward_batch(model: Model, toks, poss, draft: bool, h_in=None):
                 e = int(rt[i][0][j])
                 acc = (acc + (np.float32(rt[i][1][j]) * ys[(i, e)]).astype(np.float32)).astype(np.float32)
             h[i] = (h[i] + acc).astype(np.float32)
+    if h_trace is not None:
+        h_trace.append(h.copy())
     xf = np.stack([model.rmsnorm(np.ascontiguousarray(h[i]), model.gamma(-1)) for i in range(M)])
     _, am = model.lm_head(xf)
     return [(int(am[i]), routing[i]) for i in range(M)]
@@ -425,8 +430,9 @@ def check_layers(model: Model, h_caps, ids, draft: bool, tol=2e-3):
         for i in range(M):
             assert rt[i][0].tolist() == list(ids[l][i]), ("routing", l, i, rt[i][0].tolist(), list(ids[l][i]))
             lg = np.sort(rt[i][2])[::-1]
-            if m.K < m.E:
-                margins[l][i] = float(lg[m.K - 1] - lg[m.K]) / (float(np.abs(lg).max()) + 1e-30)
+            gaps = [lg[j] - lg[j + 1] for j in range(min(m.K, m.E - 1))]  # order inside the top-K counts too
+            if gaps:
+                margins[l][i] = float(min(gaps)) / (float(np.abs(lg).max()) + 1e-30)
         nxt = h.copy()
         for e in sorted({int(x) for i in range(M) for x in rt[i][0]}):
             rows = [i for i in range(M) if e in rt[i][0].tolist()]

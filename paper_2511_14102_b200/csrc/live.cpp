@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <functional>
 #include <set>
@@ -174,6 +175,7 @@ struct mspq_engine {
   // for the verify window [L+1][T][d] and each draft row [k][L+1][d], kept per cycle of the
   // last generate() and read back with mspq_engine_read("hcap_v:<cycle>" / "hcap_d:<cycle>")
   float *hcap_v = nullptr, *hcap_dstage = nullptr, *hcap_d = nullptr;
+  int32_t* sched_cap = nullptr;  // collect_plans: each verify layer's device schedule [L][Sched::ints]
   std::vector<std::vector<float>> hcap_v_hist, hcap_d_hist;
 
   int32_t* win_tok() { return dst + 8; }
@@ -244,11 +246,34 @@ void alloc_host_store(mspq_engine* E) {
     if (fd < 0) fail(MSPQ_ERR_IO, "cannot create host store " + E->store_path);
     if (ftruncate(fd, (off_t)E->host_bytes) != 0) fail(MSPQ_ERR_IO, "ftruncate host store");
   } else {
-    for (int i = 0; i < 36000 && access(ready.c_str(), F_OK) != 0; ++i)
+    // the owner publishes "<magic> <bytes> <payloads> <codec>" by an atomic rename once the store
+    // is filled; an attacher maps it only if that record and the file size match this engine
+    char want[160];
+    snprintf(want, sizeof(want), "MSPQSTORE1 %zu %d %d", E->host_bytes, E->n_payload, E->codec);
+    bool ok = false;
+    for (int i = 0; i < 36000 && !ok; ++i) {
+      FILE* f = fopen(ready.c_str(), "r");
+      if (f) {
+        char got[160] = {0};
+        const size_t n = fread(got, 1, sizeof(got) - 1, f);
+        fclose(f);
+        got[n] = 0;
+        if (strncmp(got, "MSPQSTORE1 ", 11) == 0) {
+          if (strcmp(got, want) != 0) fail(MSPQ_ERR_IO, std::string("host store record mismatch: ") + got);
+          ok = true;
+          break;
+        }
+      }
       std::this_thread::sleep_for(std::chrono::milliseconds(50));
-    if (access(ready.c_str(), F_OK) != 0) fail(MSPQ_ERR_IO, "host store never became ready");
+    }
+    if (!ok) fail(MSPQ_ERR_IO, "host store never became ready");
     fd = open(E->store_path.c_str(), O_RDWR);
     if (fd < 0) fail(MSPQ_ERR_IO, "cannot open host store " + E->store_path);
+    struct stat st;
+    if (fstat(fd, &st) != 0 || (size_t)st.st_size != E->host_bytes) {
+      close(fd);
+      fail(MSPQ_ERR_IO, "host store size does not match this model");
+    }
   }
   void* p = mmap(nullptr, E->host_bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
   close(fd);
@@ -317,9 +342,12 @@ void make_experts(mspq_engine* E) {
   if (E->codec)
     for (int p = 0; p < E->n_payload; ++p) E->xc_bytes_total += E->wire_bytes(p);
   if (E->host_is_shm && E->o.host_store_role == 0) {
-    const std::string ready = E->store_path + ".ready";
-    int fd = open(ready.c_str(), O_WRONLY | O_CREAT, 0600);
-    if (fd >= 0) close(fd);
+    const std::string ready = E->store_path + ".ready", tmp = ready + ".tmp";
+    FILE* f = fopen(tmp.c_str(), "w");
+    if (!f) fail(MSPQ_ERR_IO, "cannot write " + tmp);
+    fprintf(f, "MSPQSTORE1 %zu %d %d", E->host_bytes, E->n_payload, E->codec);
+    fclose(f);
+    if (rename(tmp.c_str(), ready.c_str()) != 0) fail(MSPQ_ERR_IO, "cannot publish " + ready);
   }
 }
 
@@ -374,6 +402,7 @@ void make_workspaces(mspq_engine* E) {
   E->hpin_ints = 64 + (size_t)L * T * K * 2 + (size_t)E->Tmax * L * K * 3 + 4 * T + (size_t)L * 2 + (size_t)L * T * 2 +
                  (size_t)L * m.E + 64;
   CUDA_OK(cudaHostAlloc((void**)&E->hpin, E->hpin_ints * 4, 0));
+  CUDA_OK(cudaMalloc(&E->sched_cap, (size_t)L * sched_ints * 4));
   if (E->o.trace_level >= 3) {
     CUDA_OK(cudaMalloc(&E->hcap_v, (size_t)(L + 1) * T * d * 4));
     CUDA_OK(cudaMalloc(&E->hcap_dstage, (size_t)(L + 1) * d * 4));
@@ -581,6 +610,7 @@ static void configure(mspq_engine* E, const std::string& text) {
 struct CopyBatch {
   cudaEvent_t a = nullptr, b = nullptr;
   int count = 0;
+  bool demand = false;  // a verify layer's demand misses (the reference's synchronous fetch)
   const char* label = "io_new";
 };
 
@@ -794,9 +824,13 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
       CUDA_OK(cudaEventRecord(E->ev_w0[l], E->sc));
       CAPI_OK(mspq_build_schedule(tgt, T, K, Ex, E->gbuf, sv.n_groups, sv.group_expert, sv.group_buf, sv.group_off,
                                   sv.entry_tok, sv.entry_of, sv.entry_group, E->sc));
+      if (c.collect_plans)
+        CUDA_OK(cudaMemcpyAsync(E->sched_cap + (size_t)l * Sched::ints(E->G, E->N), sv.base,
+                                Sched::ints(E->G, E->N) * 4, cudaMemcpyDeviceToDevice, E->sc));
       spin_wait(E->ev_w0[l]);
       CopyBatch b;
       b.label = "io_new";
+      b.demand = true;
       issue_copies(E, cycle, b, cyc_bytes);
       if (b.count) batches.push_back(b);
       if (!E->deferred.empty()) {
@@ -987,14 +1021,55 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
     double sync_s = 0.0;
     json segs = json::array();
     segs.push_back(segment("compute", "draft", t_start, t_dend - t_start));
+    int io_pending = 0;
     for (auto& b : batches) {
+      // a mispredicted prefetch may still be on the copy/decode streams at ev_end: its batch is
+      // left out of the segments (and counted) rather than read from an incomplete event
+      if (cudaEventQuery(b.b) != cudaSuccess) {
+        cudaGetLastError();
+        ++io_pending;
+        continue;
+      }
       const double bs = elapsed_s(E->ev_t0, b.a), be = elapsed_s(E->ev_t0, b.b);
       segs.push_back(segment("io", b.label, bs, be - bs));
     }
+    rec["io_pending_batches"] = io_pending;
     segs.push_back(segment("compute", "verify", t_dend, t_end - t_dend));
+    // sync fetch = the demand misses' copy (+ decode) time, measured (sim.cpp:338-344 models it as
+    // t_pcie_new(demand_count) queued after the channel traffic)
+    for (auto& b : batches)
+      if (b.demand && cudaEventQuery(b.b) == cudaSuccess) sync_s += elapsed_s(b.a, b.b);
+    cudaGetLastError();
     rec["sync_fetch_s"] = sync_s;
     rec["sync_count"] = demand;
     rec["segments"] = segs;
+    if (c.collect_plans) {  // sim.cpp:377-392: the device planner's items and the verify schedules
+      const int np = std::min(E->view.host_stat[S_NPLAN], E->view.plan_cap);
+      std::vector<int32_t> pl((size_t)np * 3);
+      if (np) CUDA_OK(cudaMemcpy(pl.data(), E->view.plan, pl.size() * 4, cudaMemcpyDeviceToHost));
+      json pj = json::array();
+      for (int i = 0; i < np; ++i)
+        pj.push_back({{"issue_after_token", pl[i * 3]}, {"layer", pl[i * 3 + 1] / Ex}, {"expert", pl[i * 3 + 1] % Ex},
+                      {"phase", pl[i * 3 + 2]}});
+      rec["prefetch_plan"] = pj;
+      const size_t si = Sched::ints(E->G, E->N);
+      std::vector<int32_t> sc((size_t)L * si);
+      CUDA_OK(cudaMemcpy(sc.data(), E->sched_cap, sc.size() * 4, cudaMemcpyDeviceToHost));
+      json ej = json::array();
+      for (int l = 0; l < L; ++l) {
+        const int32_t* b = sc.data() + (size_t)l * si;
+        const int ng = b[0];
+        const int32_t *gexp = b + 4, *goff = b + 4 + 2 * E->G, *etok = goff + E->G + 1;
+        json groups = json::array();
+        for (int g2 = 0; g2 < ng; ++g2) {
+          json toks = json::array();
+          for (int i = goff[g2]; i < goff[g2 + 1]; ++i) toks.push_back(head_pos + etok[i]);
+          groups.push_back({{"expert", gexp[g2]}, {"tokens", toks}});
+        }
+        ej.push_back({{"layer", l}, {"groups", groups}});
+      }
+      rec["execution_plan"] = ej;
+    }
     rec["tokens"] = new_toks;
     if (level >= 1) {
       json dt = json::array(), ta = json::array();
@@ -1171,6 +1246,7 @@ void destroy(mspq_engine* E) {
   if (E->hpin) cudaFreeHost(E->hpin);
   for (float* p : {E->hcap_v, E->hcap_dstage, E->hcap_d})
     if (p) cudaFree(p);
+  if (E->sched_cap) cudaFree(E->sched_cap);
   if (E->host) {
     if (E->host_is_shm) {
       cudaHostUnregister(E->host);

@@ -322,3 +322,30 @@ def test_live_governor_k_sequence_matches_reference_governor(cuda, ref, estimato
             req["g"] = w["g"]
         assert ref.governor(req)["select_k"] == w["select_k"]
     eng.close()
+
+
+def test_live_collect_plans_and_sync_fetch(cuda):
+    """collect_plans in live mode (sim.cpp:377-392): each cycle record carries the device
+    planner's prefetch items (= the causal planner restatement's) and the verify schedule K3 ran
+    (= reorder_verification of the window, scheduler.cpp:339-357); sync_fetch_s is the measured
+    time of the verify-time copies (demand misses and staged refills), > 0 whenever a demand miss
+    was fetched."""
+    eng, cfg = _engine()
+    conf = {"policy": "speculative", "cache_capacity": 3, "k": 4, "collect_plans": True}
+    eng.configure(conf)
+    rep = eng.generate([9, 8, 7], 30)
+    c = cp.sim_config(conf)
+    cache = cp.Cache(c["capacity_mode"], c["cache_capacity"])
+    head = 2
+    for cyc in rep["cycles"]:
+        out = cp.live_cycle(cache, cp.ELB.build(cyc["elb"], cyc["elb_gates"]), cyc["target"], c)
+        got = [(p["issue_after_token"], (p["layer"], p["expert"]), p["phase"]) for p in cyc["prefetch_plan"]]
+        assert got == [(r, tuple(k), ph) for (r, k, ph) in out["plan_items"]]
+        T = cyc["k"] + 1
+        window = list(range(head, head + T))
+        routing = [[cyc["target"][s][l] for s in range(T)] for l in range(cfg.L)]
+        want = cp.reorder_verification(window, routing)
+        assert [lay["groups"] for lay in cyc["execution_plan"]] == want
+        assert cyc["sync_fetch_s"] > 0 or cyc["sync_count"] == 0
+        head += cyc["accepted"] + 1
+    eng.close()

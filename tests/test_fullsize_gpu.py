@@ -11,9 +11,14 @@ Three checks per run, all on the same generate() call:
      with no error accumulation, so it pins every layer of every draft row and verify slot.
   2. free-running end to end: the oracle decodes on its own with the device's k sequence; ELB
      rows, target routing, draft tokens, target argmax, accepted counts and committed tokens must
-     be identical.  A divergence is accepted only at a certified near-tie (the oracle's own
-     top-K / argmax margin below 1e-4 of the logit scale at the first differing decision), and is
-     reported -- it never passes silently.
+     be identical.  Over 32 layers the device (fp32 tensor-core accumulation, bf16 activations)
+     and the oracle (double accumulation) drift apart by rounding, so a decision whose logit gap
+     is inside that drift can flip.  A divergence is therefore accepted only when it is certified
+     as such a near-tie: at the first differing decision, the logits the oracle computes from its
+     own residual and from the device's residual differ by more than the device's decision gap
+     (any adjacent pair in the top K+1, or the top-2 of the LM head), while the two residuals agree
+     within check 1's per-layer tolerance times the layers passed.  It is reported as a
+     warning, never passed silently; everything after it is covered by check 1.
   3. control plane: the device's hit/miss event log equals oracle/control_plane.live_cycle on
      the run's routing, and the governor's k sequence equals the reference select_k fed the
      run's outcomes (oracle/control_plane.live_governor_ks).
@@ -46,11 +51,12 @@ def _teacher_forced(eng, rep, cfg, model):
     is ("target", cycle, slot, layer) / ("elb", cycle, row, layer) for routing (top-K boundary gap)
     and ("target_argmax", cycle, slot) / ("draft_token", cycle, row) for the LM head (top-2 gap)."""
     L, d = cfg.L, cfg.d
-    worst, margins = 0.0, {}
+    worst, margins, caps = 0.0, {}, {}
     for ci, c in enumerate(rep["cycles"]):
         k = c["k"]
         T = k + 1
         hv = np.frombuffer(eng.read("hcap_v:%d" % ci, (L + 1) * T * d * 4), dtype=np.float32).reshape(L + 1, T, d)
+        caps[("v", ci)] = hv
         ids = [[c["target"][s][l] for s in range(T)] for l in range(L)]
         w, mg = om.check_layers(model, hv, ids, draft=False)
         worst = max(worst, w)
@@ -63,6 +69,7 @@ def _teacher_forced(eng, rep, cfg, model):
         for s in range(T):
             margins[("target_argmax", ci, s)] = _gap(lg[s])
         hd = np.frombuffer(eng.read("hcap_d:%d" % ci, k * (L + 1) * d * 4), dtype=np.float32).reshape(k, L + 1, d)
+        caps[("d", ci)] = hd
         for r in range(k):
             ids_r = [[c["elb"][r][l]] for l in range(L)]
             w, mg = om.check_layers(model, hd[r][:, None, :], ids_r, draft=True)
@@ -73,7 +80,55 @@ def _teacher_forced(eng, rep, cfg, model):
             lg, am = model.lm_head(xf[None, :])
             assert int(am[0]) == c["draft_tokens"][r], ("draft token", ci, r)
             margins[("draft_token", ci, r)] = _gap(lg[0])
-    return worst, margins
+    return worst, margins, caps
+
+
+def _explain(div, rep, oc, model, caps, prompt):
+    """Certify a free-running divergence as a rounding near-tie (module docstring, check 2).
+    Returns a description; raises AssertionError when the divergence is not explained."""
+    L, K = model.m.L, model.m.K
+    kind, ci = div[0], div[1]
+    o = oc[ci]
+    head = prompt[-1] if ci == 0 else oc[ci - 1]["committed"][-1]
+    pos0 = len(prompt) - 1 + sum(x["accepted"] + 1 for x in oc[:ci])
+    if kind in ("target", "target_argmax"):
+        s = div[2]
+        window = [head] + o["draft"]
+        trace = []
+        om.forward_batch(model, [window[s]], [pos0 + s], draft=False, h_trace=trace)
+        h_dev = caps[("v", ci)][:, s, :]
+    elif kind in ("elb", "draft_token"):
+        r = div[2]
+        tok = head if r == 0 else o["draft"][r - 1]
+        trace = []
+        om.forward_batch(model, [tok], [pos0 + r], draft=True, h_trace=trace)
+        h_dev = caps[("d", ci)][r]
+    else:
+        raise AssertionError(f"divergence {div} is not a routing or argmax decision")
+    if kind in ("target", "elb"):
+        l = div[3]
+        h_o = trace[l][0]
+        hd = np.ascontiguousarray(h_dev[l])
+        lo = model.route(model.rmsnorm(np.ascontiguousarray(h_o), model.gamma(l)), l)[2]
+        ld = model.route(model.rmsnorm(hd, model.gamma(l)), l)[2]
+        srt = np.sort(ld)[::-1]
+        # the trace lists the top-K in logit order: an adjacent swap anywhere in the top K+1 counts
+        gap = float(min(srt[j] - srt[j + 1] for j in range(min(K, len(srt) - 1))))
+    else:
+        h_o = trace[L][0]
+        hd = np.ascontiguousarray(h_dev[L])
+        lo = model.lm_head(model.rmsnorm(np.ascontiguousarray(h_o), model.gamma(-1))[None, :])[0][0]
+        ld = model.lm_head(model.rmsnorm(hd, model.gamma(-1))[None, :])[0][0]
+        srt = np.sort(ld)[::-1]
+        gap = float(srt[0] - srt[1])
+    drift = float(np.abs(lo - ld).max())
+    hrel = float(np.abs(h_o - hd).max()) / (float(np.abs(hd).max()) + 1e-30)
+    msg = (f"divergence {div}: device decision gap {gap:.3e}, logit drift oracle-vs-device residual {drift:.3e}, "
+           f"residual drift {hrel:.2e} (relative)")
+    # the residuals may drift by at most the per-layer tolerance of check 1 for each layer passed
+    depth = div[3] if kind in ("target", "elb") else L
+    assert hrel <= 2e-3 * max(depth, 1) and gap <= drift, msg
+    return msg
 
 
 def _first_divergence(rep, oc, L):
@@ -110,7 +165,7 @@ def _run(name, cap, ntok, conf_extra=None, **shape_kw):
     rep = eng.generate(prompt, ntok)
     model = om.Model(_desc(cfg))
     try:
-        worst, margins = _teacher_forced(eng, rep, cfg, model)
+        worst, margins, caps = _teacher_forced(eng, rep, cfg, model)
     finally:
         eng.close()
     # 2. free-running oracle decode with the device's k sequence
@@ -118,13 +173,9 @@ def _run(name, cap, ntok, conf_extra=None, **shape_kw):
     div = _first_divergence(rep, oc, cfg.L)
     margin = min(margins.values())
     if div is not None:
-        # every decision before `div` agreed, so the hidden states differ only by accumulated
-        # rounding: the divergence is legitimate only where the device's own decision was a
-        # near-tie (relative logit gap < 1e-4), and it is reported
-        at = margins.get(div)
-        warnings.warn(f"{name}: free-running oracle diverged at {div}, relative margin there {at}; "
+        msg = _explain(div, rep, oc, model, caps, prompt)
+        warnings.warn(f"{name}: free-running oracle diverged at a certified rounding near-tie -- {msg}; "
                       f"teacher-forced layers all exact (worst layer err {worst:.2e})")
-        assert at is not None and at < 1e-4, f"divergence {div} without a near-tie (margin {at})"
     # 3. control plane: hit/miss log and governor k sequence
     c = cp.sim_config(conf)
     cache = cp.Cache(c["capacity_mode"], c["cache_capacity"])
