@@ -24,3 +24,5 @@ def test_reference_arm_prints_contract_line(ref):
     assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert "workload" in d["config"]
+    # same workload as the GPU arm: the routing trace this engine produced for the bench config
+    assert d["same_config"] is True and d["reference_modeled_b200_tokens_per_s"] > 0
