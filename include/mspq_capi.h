@@ -11,7 +11,7 @@
  *                                   and build_elb's input, scheduler.cpp:41-63)
  *        mspq_build_schedule       expert-grouped entry schedule == reorder_verification
  *                                  (scheduler.cpp:339-357)
- *        mspq_moe_int4         K2  INT4 (GPTQ-sym g128) grouped expert FFN for the draft
+ *        mspq_moe_int4         K2  INT4 (RTN on the GPTQ sym g128 grid) grouped expert FFN for the draft
  *        mspq_moe_bf16         K3  bf16 grouped expert FFN for the verify (reads the HBM slot pool)
  *        mspq_lm_head / mspq_argmax  logits + greedy token
  *        mspq_accept_scan      K5  accept rule (sim.cpp:352-365) on token ids
@@ -146,7 +146,7 @@ int mspq_moe_bf16_tc_part(const int32_t* n_groups, const int32_t* group_expert, 
                           const uint32_t* gmask8, int do_gather, void* stream);
 /* K2 on tcgen05 (umma.cu k_umma_int4): the INT4 draft FFN over TILE-MAJOR INT4 blobs
  * (mspq_tile_int4), blobs indexed by layer*E + group_buf[g] (= expert id for the draft
- * schedule).  Exact GPTQ-sym dequant: bf16 (q-8) tiles into smem, per-128-column scales in the
+ * schedule).  Exact dequant (GPTQ sym grid): bf16 (q-8) tiles into smem, per-128-column scales in the
  * fp32 epilogue.  Same workspace size / outputs as mspq_moe_bf16_tc. */
 int mspq_moe_int4_tc(const int32_t* n_groups, const int32_t* group_expert, const int32_t* group_buf,
                      const int32_t* group_off, const int32_t* entry_tok, const int32_t* entry_group,

@@ -3,7 +3,8 @@
 "Parity unpinned by the reference": /root/reference has no model, weights, gating, GEMMs or
 logits.  This file *defines* the numerics the device must reproduce, from the
 paper: bf16 router / norms / non-expert params, INT4 symmetric group-128
-draft experts (GPTQ's sym convention scale = 2*amax/15, zero = 8), greedy
+draft experts (round-to-nearest on GPTQ's symmetric grid, scale = 2*amax/15,
+zero = 8 -- not Hessian-based GPTQ; pinned in tests/test_pin_thirdparty_cpu.py), greedy
 verification = accepted prefix + one target token, reordered grouped verify
 (PAPER.md:495-496).  Order-sensitive fp32 pieces (fixed-order dots, RMSNorm sums, the exp used
 by softmax/SiLU) are in csrc/model_ref.c so they are bit-identical to the kernels; expert FFN

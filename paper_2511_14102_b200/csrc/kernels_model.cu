@@ -1,4 +1,4 @@
-// MoE decode math on sm_100a: weight init, INT4 (GPTQ-sym g128) quantisation, embedding,
+// MoE decode math on sm_100a: weight init, INT4 (RTN on the GPTQ sym g128 grid) quantisation, embedding,
 // fused residual-combine + RMSNorm + router + top-k/softmax (K1), grouped expert FFN for the
 // INT4 draft (K2) and the bf16 verify (K3), LM head + argmax, accept/reject scan (K5).
 //
@@ -45,7 +45,7 @@ __global__ void k_fill_expert(uint64_t seed, int cl, int ce, int d, int f, float
   }
 }
 
-// GPTQ-sym RTN, one warp per (row, 128-column group): lane owns 4 columns.
+// RTN on the GPTQ sym g128 grid, one warp per (row, 128-column group): lane owns 4 columns.
 __global__ void k_quantize_g128(const uint16_t* __restrict__ w, int rows, int cols,
                                 uint32_t* __restrict__ q, uint16_t* __restrict__ s) {
   const int lane = threadIdx.x & 31;

@@ -336,7 +336,7 @@ __global__ void k_tile_bf16(const uint16_t* __restrict__ src, int rows, int cols
 }
 
 // ============================================================================ K2 v6 (INT4)
-// The draft's GPTQ-sym INT4 expert GEMM on tcgen05 with the EXPANDED WEIGHTS IN TMEM.
+// The draft's INT4 (RTN on the GPTQ sym g128 grid) expert GEMM on tcgen05 with the EXPANDED WEIGHTS IN TMEM.
 // Per 128-column scale group the producer bulk-copies the two 4 KB packed tiles (weight ring)
 // and the two token tiles (token ring); eight dequant warps expand each packed word with ONE
 // LOP3 per two weights into exact fp16 pairs -- (1024 + q) for a k-block's columns 0..31, (1024 +
