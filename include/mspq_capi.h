@@ -261,6 +261,26 @@ int mspq_engine_info(mspq_engine* eng, char** json);
  * store is coded), "expert_blob:<l>:<e>" (the stored bytes as they cross PCIe)} */
 int mspq_engine_read(mspq_engine* eng, const char* name, void* host_dst, long long bytes);
 
+/* ---------------------------------------------------------------- (3) peer-expert tier
+ * NVLink peer-expert tier (BASELINE.json north_star) with "home"
+ * partitioning: in a group of G engines (one per GPU), engine r keeps the bf16 tile images of
+ * every expert (l, e) with e % G == r permanently in an HBM home region (filled once from the
+ * host store).  A cache miss (demand or prefetch) of an expert homed on an attached peer is
+ * copied HBM -> HBM from the peer's home region (copy engine over NVLink / NVSwitch; a local
+ * home is a device-to-device copy) instead of over PCIe.  Home regions are immutable after the
+ * fill, so peers read them with no coordination.  Cache decisions are unchanged: only the bytes'
+ * source moves (the replaced path: the synchronous fetch sim.cpp:338-344, t_pcie_new
+ * perfmodel.cpp:104-110).  Experts homed on a peer that is not attached keep the PCIe path.
+ *
+ * mspq_engine_home_create: allocate + fill this engine's home region; *ipc_handle (64 bytes,
+ *   cudaIpcMemHandle_t) lets other processes map it.
+ * mspq_engine_peer_attach_ipc: map peer `peer_rank`'s home region from its handle (another
+ *   process; same or another GPU, cudaIpcOpenMemHandle with lazy peer access).
+ * mspq_engine_peer_attach: the same for a peer engine in this process. */
+int mspq_engine_home_create(mspq_engine* eng, int group_size, int rank, void* ipc_handle_out);
+int mspq_engine_peer_attach_ipc(mspq_engine* eng, int peer_rank, const void* ipc_handle);
+int mspq_engine_peer_attach(mspq_engine* eng, int peer_rank, mspq_engine* peer);
+
 #ifdef __cplusplus
 }
 #endif

@@ -140,6 +140,23 @@ class Engine:
         check(lib().mspq_engine_read(self._h, name.encode(), buf, nbytes))
         return bytes(buf)
 
+    # ---- peer-expert tier (include/mspq_capi.h (3)): home partitioning by expert id mod G
+    def home_create(self, group: int, rank: int) -> bytes:
+        """Allocate and fill this engine's HBM home region (experts e with e % group == rank);
+        returns the 64-byte CUDA IPC handle other ranks attach with."""
+        h = (ctypes.c_uint8 * 64)()
+        check(lib().mspq_engine_home_create(self._h, group, rank, h))
+        return bytes(h)
+
+    def peer_attach_ipc(self, peer_rank: int, handle: bytes):
+        """Map another process's home region (its home_create handle)."""
+        buf = (ctypes.c_uint8 * 64).from_buffer_copy(handle)
+        check(lib().mspq_engine_peer_attach_ipc(self._h, peer_rank, buf))
+
+    def peer_attach(self, peer_rank: int, peer: "Engine"):
+        """Attach a peer engine of this process (same or another GPU)."""
+        check(lib().mspq_engine_peer_attach(self._h, peer_rank, peer._h))
+
     def close(self):
         if self._h:
             lib().mspq_engine_destroy(self._h)

@@ -76,6 +76,9 @@ _SIGS = [
     ("mspq_generate", c_int, [c_void_p, c_void_p, c_int, c_int, ctypes.POINTER(c_void_p)]),
     ("mspq_engine_info", c_int, [c_void_p, ctypes.POINTER(c_void_p)]),
     ("mspq_engine_read", c_int, [c_void_p, c_char_p, c_void_p, c_ll]),
+    ("mspq_engine_home_create", c_int, [c_void_p, c_int, c_int, c_void_p]),
+    ("mspq_engine_peer_attach_ipc", c_int, [c_void_p, c_int, c_void_p]),
+    ("mspq_engine_peer_attach", c_int, [c_void_p, c_int, c_void_p]),
 ]
 
 EXPORTS = [s[0] for s in _SIGS]

@@ -176,6 +176,21 @@ struct mspq_engine {
   // last generate() and read back with mspq_engine_read("hcap_v:<cycle>" / "hcap_d:<cycle>")
   float *hcap_v = nullptr, *hcap_dstage = nullptr, *hcap_d = nullptr;
   int32_t* sched_cap = nullptr;  // collect_plans: each verify layer's device schedule [L][Sched::ints]
+  // peer-expert tier (home partitioning, include/mspq_capi.h (3)): expert (l, e) lives in the home
+  // region of engine e % peer_G at slot l * home_per_layer + e / peer_G
+  int peer_G = 0, peer_rank = 0, home_per_layer = 0;
+  unsigned char* home = nullptr;
+  size_t home_bytes = 0;
+  std::vector<unsigned char*> peer_home;  // [G] base of each engine's home region (nullptr = not attached)
+  std::vector<char> peer_ipc;             // [G] mapped with cudaIpcOpenMemHandle (closed on destroy)
+  uint64_t gen_peer_bytes = 0, gen_home_local_bytes = 0;
+  uint64_t n_peer = 0, n_home_local = 0;
+  const unsigned char* home_src(int key) const {
+    if (peer_G <= 0) return nullptr;
+    const int l = key / m.E, e = key % m.E, owner = e % peer_G;
+    const unsigned char* base = peer_home[owner];
+    return base ? base + ((size_t)l * home_per_layer + e / peer_G) * (size_t)S16 : nullptr;
+  }
   std::vector<std::vector<float>> hcap_v_hist, hcap_d_hist;
 
   int32_t* win_tok() { return dst + 8; }
@@ -652,6 +667,26 @@ static int issue_copies(mspq_engine* E, int cycle, CopyBatch& batch, uint64_t& b
     }
     const bool reused = E->last_cycle[buf] == cycle;  // the slot's last reader is this cycle's GEMM
     unsigned char* slot = E->pool + (size_t)buf * E->S16;
+    if (const unsigned char* hs = E->home_src(key)) {
+      // peer-expert tier: HBM -> HBM from the key's home region (a peer's over NVLink, or this
+      // GPU's own), in the decode stream's order so it follows any earlier write into the slot
+      cudaStream_t hst = E->codec ? sdec : sx;
+      if (reused) CUDA_OK(cudaStreamWaitEvent(hst, E->ev_gemm[E->last_layer[buf]], 0));
+      if (E->ready_rec[buf]) CUDA_OK(cudaStreamWaitEvent(hst, E->ev_ready[buf], 0));
+      CUDA_OK(cudaMemcpyAsync(slot, hs, E->S16, cudaMemcpyDeviceToDevice, hst));
+      CUDA_OK(cudaEventRecord(E->ev_ready[buf], hst));
+      const int owner = (key % E->m.E) % E->peer_G;
+      if (owner == E->peer_rank) {
+        E->gen_home_local_bytes += (uint64_t)E->S16;
+        ++E->n_home_local;
+      } else {
+        E->gen_peer_bytes += (uint64_t)E->S16;
+        ++E->n_peer;
+      }
+      E->ready_rec[buf] = 1;
+      ++batch.count;
+      continue;
+    }
     // two lanes: a slot may still be under a write issued on the other lane (a prefetch the
     // controller evicted before its use), so the new writer orders after it
     if (E->pf_lane && E->ready_rec[buf]) CUDA_OK(cudaStreamWaitEvent(E->codec ? sdec : sx, E->ev_ready[buf], 0));
@@ -752,6 +787,8 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
   E->deferred.clear();
   E->hcap_v_hist.clear();
   E->hcap_d_hist.clear();
+  E->gen_peer_bytes = E->gen_home_local_bytes = 0;
+  E->n_peer = E->n_home_local = 0;
   if (E->pf_lane) CUDA_OK(cudaStreamWaitEvent(E->sx2, E->ev_t0, 0));
   std::vector<int> committed;
   json cycles = json::array();
@@ -1188,6 +1225,17 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
   rep["tokens"] = committed;
   rep["h2d_bytes"] = h2d_bytes;
   rep["h2d_bytes_bf16"] = (uint64_t)total_new * (uint64_t)E->S16;
+  if (E->peer_G > 0) {  // peer-expert tier: where the fetched experts' bytes came from
+    json pt;
+    pt["group"] = E->peer_G;
+    pt["rank"] = E->peer_rank;
+    pt["peer_bytes"] = E->gen_peer_bytes;
+    pt["home_local_bytes"] = E->gen_home_local_bytes;
+    pt["peer_fetches"] = E->n_peer;
+    pt["home_local_fetches"] = E->n_home_local;
+    pt["pcie_fetches"] = (uint64_t)total_new - E->n_peer - E->n_home_local;
+    rep["peer_tier"] = pt;
+  }
   rep["expert_codec"] = E->codec ? "xc" : "none";
   rep["wall_s"] = wall;
   rep["profile"] = c.profile.to_json();
@@ -1247,6 +1295,9 @@ void destroy(mspq_engine* E) {
   for (float* p : {E->hcap_v, E->hcap_dstage, E->hcap_d})
     if (p) cudaFree(p);
   if (E->sched_cap) cudaFree(E->sched_cap);
+  for (size_t r = 0; r < E->peer_ipc.size(); ++r)
+    if (E->peer_ipc[r] && E->peer_home[r]) cudaIpcCloseMemHandle(E->peer_home[r]);
+  if (E->home) cudaFree(E->home);
   if (E->host) {
     if (E->host_is_shm) {
       cudaHostUnregister(E->host);
@@ -1398,6 +1449,8 @@ int mspq_engine_info(mspq_engine* E, char** out) {
     j["draft_resident_bytes"] = (uint64_t)m.L * m.E * E->S4;
     j["pcie_bw_measured"] = E->pcie_bw_measured;
     j["draft_step_s"] = E->draft_step_s;
+    j["home_bytes"] = E->home_bytes;
+    j["peer_group"] = E->peer_G;
     if (E->configured) j["profile"] = E->cfg.profile.to_json();
     *out = dupstr(j.dump());
     return MSPQ_OK;
@@ -1464,6 +1517,82 @@ int mspq_engine_read(mspq_engine* E, const char* name, void* dst, long long byte
     if ((size_t)bytes > avail) fail(MSPQ_ERR_RANGE_OUT_OF_BOUNDS, "read beyond tensor");
     if (from_host) memcpy(dst, src, bytes);
     else CUDA_OK(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+    return MSPQ_OK;
+  });
+}
+
+int mspq_engine_home_create(mspq_engine* E, int group, int rank, void* ipc_out) {
+  return guarded([&] {
+    const auto& m = E->m;
+    if (group < 1 || rank < 0 || rank >= group) fail(MSPQ_ERR_INVALID_CONFIG, "peer tier: need 0 <= rank < group");
+    if (E->home) fail(MSPQ_ERR_INVALID_CONFIG, "peer tier: home region already created");
+    CUDA_OK(cudaSetDevice(E->o.device));
+    E->peer_G = group;
+    E->peer_rank = rank;
+    E->home_per_layer = (m.E + group - 1) / group;
+    E->home_bytes = (size_t)m.L * E->home_per_layer * (size_t)E->S16;
+    CUDA_OK(cudaMalloc(&E->home, E->home_bytes));
+    E->peer_home.assign(group, nullptr);
+    E->peer_ipc.assign(group, 0);
+    // fill: every expert homed here, from the host store (XC blobs decoded on the GPU)
+    unsigned char* blob = nullptr;
+    if (E->codec) CUDA_OK(cudaMalloc(&blob, (size_t)E->Sreg));
+    for (int l = 0; l < m.L; ++l)
+      for (int e = rank; e < m.E; e += group) {
+        const int key = l * m.E + e;
+        unsigned char* dst = E->home + ((size_t)l * E->home_per_layer + e / group) * (size_t)E->S16;
+        const unsigned char* hb = E->host_blob(E->payload(key));
+        if (E->codec) {
+          CUDA_OK(cudaMemcpyAsync(blob, hb, E->wire_bytes(E->payload(key)), cudaMemcpyHostToDevice, E->sc));
+          CAPI_OK(mspq_xc_decode(blob, 0, E->n_tiles, dst, 0, E->sc));
+        } else {
+          CUDA_OK(cudaMemcpyAsync(dst, hb, E->S16, cudaMemcpyHostToDevice, E->sc));
+        }
+      }
+    CUDA_OK(cudaStreamSynchronize(E->sc));
+    if (blob) cudaFree(blob);
+    E->peer_home[rank] = E->home;
+    if (ipc_out) {
+      cudaIpcMemHandle_t h;
+      CUDA_OK(cudaIpcGetMemHandle(&h, E->home));
+      memcpy(ipc_out, &h, sizeof(h));
+    }
+    return MSPQ_OK;
+  });
+}
+
+int mspq_engine_peer_attach_ipc(mspq_engine* E, int peer_rank, const void* handle) {
+  return guarded([&] {
+    if (E->peer_G <= 0) fail(MSPQ_ERR_INVALID_CONFIG, "peer tier: create the home region first");
+    if (peer_rank < 0 || peer_rank >= E->peer_G || peer_rank == E->peer_rank)
+      fail(MSPQ_ERR_INVALID_CONFIG, "peer tier: bad peer rank");
+    if (E->peer_home[peer_rank]) fail(MSPQ_ERR_INVALID_CONFIG, "peer tier: peer already attached");
+    CUDA_OK(cudaSetDevice(E->o.device));
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    void* p = nullptr;
+    CUDA_OK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    E->peer_home[peer_rank] = (unsigned char*)p;
+    E->peer_ipc[peer_rank] = 1;
+    return MSPQ_OK;
+  });
+}
+
+int mspq_engine_peer_attach(mspq_engine* E, int peer_rank, mspq_engine* P) {
+  return guarded([&] {
+    if (E->peer_G <= 0 || !P || P->peer_G != E->peer_G || P->peer_rank != peer_rank || !P->home)
+      fail(MSPQ_ERR_INVALID_CONFIG, "peer tier: peer has no home region of this group / rank");
+    if (peer_rank == E->peer_rank) fail(MSPQ_ERR_INVALID_CONFIG, "peer tier: bad peer rank");
+    if (P->o.device != E->o.device) {
+      int ok = 0;
+      CUDA_OK(cudaDeviceCanAccessPeer(&ok, E->o.device, P->o.device));
+      if (!ok) fail(MSPQ_ERR_CUDA, "peer tier: no peer access between the two GPUs");
+      CUDA_OK(cudaSetDevice(E->o.device));
+      const cudaError_t pe = cudaDeviceEnablePeerAccess(P->o.device, 0);
+      if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) CUDA_OK(pe);
+      cudaGetLastError();
+    }
+    E->peer_home[peer_rank] = P->home;
     return MSPQ_OK;
   });
 }
