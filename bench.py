@@ -63,6 +63,9 @@ def parse():
                     help="run the verify GEMM of resident experts while a layer's copies are in flight")
     ap.add_argument("--estimator", default="linear", choices=["linear", "elb"],
                     help="governor |E_new(k)| estimator: the reference's linear g*k or the ELB-based one")
+    ap.add_argument("--peer-tier", action="store_true",
+                    help="NVLink peer-expert tier: every rank keeps the experts e %% N == rank in an HBM home "
+                         "region and serves misses from the owner's home (N=1: the GPU's own home)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="time box of the CPU oracle decode")
     ap.add_argument("--out", default="")
@@ -323,6 +326,17 @@ def main():
     eng = m.Engine(cfgm, kmax=16, device=local, host_store_path=store or None,
                    host_store_role=0 if rank == 0 else 1, trace_level=0, expert_codec=a.codec)
     t_create = time.perf_counter() - t_create
+    t_home = 0.0
+    if a.peer_tier:
+        t_home = time.perf_counter()
+        h = eng.home_create(world, rank)
+        if world > 1:
+            hs = [None] * world
+            torch.distributed.all_gather_object(hs, h)
+            for r in range(world):
+                if r != rank:
+                    eng.peer_attach_ipc(r, hs[r])
+        t_home = time.perf_counter() - t_home
     conf = {"policy": a.policy, "cache_capacity": cap}
     if a.verify_overlap:
         conf["verify_overlap"] = True
@@ -349,6 +363,7 @@ def main():
     if world > 1:
         torch.distributed.barrier()
     info = eng.info()
+    pts = [r["peer_tier"] for r in reps if "peer_tier" in r]
     tok = sum(r["total_tokens"] for r in reps)
     dev_t = sum(r["total_time_s"] for r in reps)
     stall = sum(r["stall_time_s"] for r in reps)
@@ -373,7 +388,11 @@ def main():
     S16 = info["expert_bytes_bf16"]
     # per committed token roofline: PCIe leg (policy's bytes), HBM leg (draft + verify streaming)
     t_pcie = h2d / pcie_bw
-    hbm_bytes = dr_n * (reps[0]["kernels"]["draft_step_bytes"]) + k3_b
+    pb = sum(p["peer_bytes"] for p in pts)
+    lb = sum(p["home_local_bytes"] for p in pts)
+    # HBM leg: draft + verify weight streaming, plus the peer tier's copies (a local home copy
+    # reads and writes this HBM, a peer copy writes it)
+    hbm_bytes = dr_n * (reps[0]["kernels"]["draft_step_bytes"]) + k3_b + 2 * lb + pb
     t_hbm = hbm_bytes / (hbm * 1e9)
     t_roof = max(t_pcie, t_hbm)
     k3_ach = (k3_b / k3_n) / (k3_t / k3_n) / 1e9 if k3_t > 0 else 0.0
@@ -413,6 +432,15 @@ def main():
         "clocks": clk.summary(),
         "engine_create_s": t_create,
     }
+    if pts:
+        line["peer_tier"] = {
+            "group": world, "home_bytes_per_gpu": info["home_bytes"], "home_fill_s": t_home,
+            "peer_fetches": sum(p["peer_fetches"] for p in pts), "home_local_fetches": sum(p["home_local_fetches"] for p in pts),
+            "pcie_fetches": sum(p["pcie_fetches"] for p in pts), "peer_GBps": pb / dev_t / 1e9 if dev_t else None,
+            "home_local_GBps": lb / dev_t / 1e9 if dev_t else None,
+            "note": "misses served HBM->HBM from the owner's home region (expert id mod N); at N=1 every home is "
+                    "this GPU's own, so the copies are local device-to-device, not NVLink"}
+        line["config"]["workload"] += ", peer-expert tier (home partitioning)"
     if not a.no_cpu_baseline and world == 1:
         try:
             v, thr, sample = cpu_oracle_decode(a.model, a.cpu_seconds)

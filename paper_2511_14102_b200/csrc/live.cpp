@@ -162,7 +162,7 @@ struct mspq_engine {
   bool configured = false;
   HostCfg cfg;
   std::vector<int> caps;
-  double pcie_bw_measured = 0.0, draft_step_s = 0.0;
+  double pcie_bw_measured = 0.0, draft_step_s = 0.0, home_bw_measured = 0.0;
   std::vector<std::pair<double, double>> verify_fit;
   int cycle_serial = 0;
   // "elb" estimator state: per (layer, expert) routing frequency from the draft's
@@ -595,13 +595,32 @@ static void configure(mspq_engine* E, const std::string& text) {
     cudaEventDestroy(a);
     cudaEventDestroy(b);
   }
+  if (E->home && E->home_bw_measured == 0.0) {
+    // peer tier: a fetch is an HBM -> HBM copy of the bf16 tile images from a home region
+    // (measured on this GPU's own home; a peer's over NVLink is not measurable on one GPU)
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    const int nb = std::min(E->nbuf, 8);
+    for (int i = 0; i < nb; ++i)
+      CUDA_OK(cudaMemcpyAsync(E->pool + (size_t)i * E->S16, E->home, E->S16, cudaMemcpyDeviceToDevice, E->sx));
+    cudaEventRecord(a, E->sx);
+    for (int i = 0; i < nb; ++i)
+      CUDA_OK(cudaMemcpyAsync(E->pool + (size_t)i * E->S16, E->home, E->S16, cudaMemcpyDeviceToDevice, E->sx));
+    cudaEventRecord(b, E->sx);
+    CUDA_OK(cudaEventSynchronize(b));
+    E->home_bw_measured = (double)nb * E->S16 / elapsed_s(a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
   if (!c.profile_given) {
     Profile p;
-    p.pcie_bandwidth = E->pcie_bw_measured;
+    p.pcie_bandwidth = E->home ? E->home_bw_measured : E->pcie_bw_measured;
     p.pcie_init_latency = 0.0;
     p.pcie_overhead = 10e-6;
-    // bytes one fetch puts on the link: the mean XC blob with the codec
-    p.expert_size_bytes = E->codec ? (uint64_t)(E->xc_bytes_total / E->n_payload) : (uint64_t)E->S16;
+    // bytes one fetch puts on the link: the mean XC blob with the codec (raw tiles from a home)
+    p.expert_size_bytes = E->home ? (uint64_t)E->S16
+                                  : E->codec ? (uint64_t)(E->xc_bytes_total / E->n_payload) : (uint64_t)E->S16;
     p.draft_base = 0.0;
     p.draft_per_token = E->draft_step_s;
     // verify samples from the resident-expert roofline of this model on the measured peaks:
@@ -1450,6 +1469,7 @@ int mspq_engine_info(mspq_engine* E, char** out) {
     j["pcie_bw_measured"] = E->pcie_bw_measured;
     j["draft_step_s"] = E->draft_step_s;
     j["home_bytes"] = E->home_bytes;
+    j["home_bw_measured"] = E->home_bw_measured;
     j["peer_group"] = E->peer_G;
     if (E->configured) j["profile"] = E->cfg.profile.to_json();
     *out = dupstr(j.dump());
