@@ -206,18 +206,18 @@ def cpu_oracle_decode(model_name, seconds, kw=None):
     from oracle import model as om
     import paper_2511_14102_b200 as m
     cfg = m.ModelConfig.named(model_name, **(kw or {}))
-    desc = om.ModelDesc(L=cfg.L, E=cfg.E, K=cfg.K, d=cfg.d, f=cfg.f, V=cfg.V, P=cfg.P, seed=cfg.seed)
+    desc = om.ModelDesc(**cfg.oracle_kwargs())
     model = om.Model(desc, fast=True)
     model.lm()  # weight generation of the LM head is setup, not decode
-    tok, pos, n, cyc = 11, 0, 0, 0
+    prompt = [11, 200, 3001, 17]
+    model.kv = [dict() for _ in range(desc.L)]
+    if desc.H > 0:
+        om.prefill(model, prompt)  # excluded, like the GPU arm's prefill
     t0 = time.perf_counter()
-    while True:
-        out = om.speculative_decode(model, tok, pos, [1], 2)
-        n += sum(len(o["committed"]) for o in out)
-        cyc += len(out)
-        tok, pos = out[-1]["committed"][-1], pos + sum(o["accepted"] + 1 for o in out)
-        if time.perf_counter() - t0 >= seconds:
-            break
+    out = om.speculative_decode(model, prompt[-1], len(prompt) - 1, [1], 10**6, prompt=prompt,
+                                deadline=t0 + seconds, prefilled=True)
+    n = sum(len(o["committed"]) for o in out)
+    cyc = len(out)
     dt = time.perf_counter() - t0
     threads = os.cpu_count() or 1
     return n / dt, threads, (f"oracle greedy speculative decode of the {model_name} model (L={cfg.L}, E={cfg.E}, "

@@ -69,6 +69,11 @@ typedef struct mspq_model_desc {
   unsigned long long seed;
   float embed_scale, pos_scale, a_router, a_up, a_down, a_lm, eps;
   int unique_experts; /* 0 = every (layer, expert) distinct; else payload = key % unique */
+  /* attention (shared by draft and target, bf16): H query heads, Hkv KV heads,
+   * head dim Dh; H = 0 = attention-free layers.  a_qkv / a_o scale Wqkv [(H+2Hkv)Dh][d] and
+   * Wo [d][H Dh]. */
+  int H, Hkv, Dh;
+  float a_qkv, a_o;
 } mspq_model_desc;
 
 typedef struct mspq_engine_opts {
@@ -100,7 +105,8 @@ int mspq_quantize_int4(const void* w_bf16, int rows, int cols, void* q_u32, void
                        void* stream);
 int mspq_embed(const void* embed, const void* pos, const int32_t* tokens,
                const int32_t* positions, int T, int d, float* h, void* stream);
-/* K1.  y/entry_of/prev_wts may be NULL (no combine); y may hold y_splits partial planes
+/* K1.  y/entry_of/prev_wts may be NULL (no combine); entry_of == NULL with y != NULL is the
+ * dense combine h[t] += y[t] (the attention output projection); y may hold y_splits partial planes
  * y_split_stride floats apart (summed in order); router NULL = norm only;
  * elb_ids/elb_gates/elb_row NULL = no ELB write.  sched_block (T == 1 only, nullable): also
  * write the token's expert-grouped schedule, packed [n_groups, pad x3, group_expert[K],
@@ -153,6 +159,21 @@ int mspq_moe_int4_tc(const int32_t* n_groups, const int32_t* group_expert, const
                      const void* xn, const void* blobs, long long blob_bytes, int layer, int E, int d,
                      int f, int T, int K, int max_groups, int split1, int split2, void* ws, float* y,
                      void* stream);
+/* Dense bf16 projection on tcgen05 (K3's grouped GEMM with one group of T tokens):
+ * out[split][T][rows] fp32 partial planes (out_split_stride floats apart) = x[T][kdim] . W^T,
+ * W tile-major SW128 (mspq_tile_bf16).  dsched: device copy of the packed schedule
+ * mspq_dense_sched_fill writes (4 + T ints); ws: mspq_dense_ws_bytes(kdim, T) bytes. */
+long long mspq_dense_ws_bytes(int kdim, int T);
+int mspq_dense_sched_fill(int32_t* host_packed, int T);
+int mspq_dense_bf16_tc(const int32_t* dsched, const void* x, const void* w_tiled, int rows, int kdim, int T,
+                       int split, void* ws, float* out, long long out_split_stride, void* stream);
+/* Shared-KV decode attention over a window of T tokens at positions *pos0 .. *pos0+T-1 (device
+ * pointer): qkv = the QKV projection's split planes [splits][T][(H+2Hkv) Dh]; the window's K/V
+ * rows are written into kc/vc ([P][Hkv][Dh] bf16, this layer) and every token attends causally
+ * to the cache rows before the window plus the window tokens up to itself; out [T][H Dh] bf16.
+ * Draft and target share the cache; rollback = the next window overwrites rows >= its pos0. */
+int mspq_attention(const float* qkv, int splits, long long split_stride, int T, int H, int Hkv, int Dh, int P,
+                   const int32_t* pos0, void* kc, void* vc, void* out, void* stream);
 /* row-major quantised INT4 (q[rows][cols/8] u32, standard nibble order; s[rows][cols/128] bf16)
  * -> tile-major [rows/128][cols/64][128][8] u32 + [rows/128][cols/128][128] bf16 */
 int mspq_tile_int4(const void* q, const void* s, int rows, int cols, void* tq, void* ts, void* stream);
@@ -258,7 +279,11 @@ int mspq_generate(mspq_engine* eng, const int32_t* prompt, int n_prompt, int max
 int mspq_engine_info(mspq_engine* eng, char** json);
 /* copy a device tensor of the engine out (tests): name in {"embed","pos","lm","router:<l>",
  * "gamma:<l>","gamma:final","draft:<l>:<e>","expert:<l>:<e>" (bf16 tile images, decoded if the
- * store is coded), "expert_blob:<l>:<e>" (the stored bytes as they cross PCIe)} */
+ * store is coded), "expert_blob:<l>:<e>" (the stored bytes as they cross PCIe), "kcache:<l>" /
+ * "vcache:<l>" ([P][Hkv][Dh] bf16), "wqkv:<l>" / "wo:<l>" (tile images), "gamma_attn:<l>",
+ * trace_level 3 residual captures of the last generate(): "hcap_v:<cycle>" [L+1][T][d],
+ * "hcap_d:<cycle>" [k][L+1][d] (entering each layer; index L = final) and, with attention,
+ * "hmid_v:<cycle>" [L][T][d] / "hmid_d:<cycle>" [k][L][d] (after the attention residual)} */
 int mspq_engine_read(mspq_engine* eng, const char* name, void* host_dst, long long bytes);
 
 /* ---------------------------------------------------------------- (3) peer-expert tier

@@ -195,8 +195,17 @@ class ModelDesc:
     moe_scale: float = 0.06
     lm_scale: float = 1.0
     eps: float = 1e-6
+    H: int = 0             # attention query heads (0 = attention-free layers)
+    Hkv: int = 0           # KV heads (grouped-query attention)
+    Dh: int = 0            # head dim
 
     # scales passed to the device as fp32 (computed once, identically on both sides)
+    def a_qkv(self):
+        return float(np.float32(math.sqrt(3.0 / self.d)))
+
+    def a_o(self):
+        return float(np.float32(self.moe_scale * math.sqrt(3.0 / max(1, self.H * self.Dh))))
+
     def a_router(self):
         return float(np.float32(self.router_scale * math.sqrt(3.0 / self.d)))
 
@@ -217,12 +226,19 @@ class ModelDesc:
 
 
 CONFIGS = {
-    # BASELINE.json configs (ffn for tiny chosen: 512; Qwen3 moe_intermediate 768)
-    "tiny": dict(L=4, E=8, K=2, d=256, f=512, V=512),
-    "mixtral": dict(L=32, E=8, K=2, d=4096, f=14336, V=32000),
-    "phi": dict(L=32, E=16, K=2, d=4096, f=6400, V=32064),
-    "qwen3": dict(L=48, E=128, K=8, d=2048, f=768, V=151936),
+    # BASELINE.json configs (ffn for tiny chosen: 512; Qwen3 moe_intermediate 768); attention heads
+    # of the named models (Phi-3.5-MoE / Mixtral-8x7B: 32 q, 8 kv, dim 128; Qwen3-30B-A3B: 32 q,
+    # 4 kv, dim 128; tiny chosen: 4 q, 2 kv, dim 64)
+    "tiny": dict(L=4, E=8, K=2, d=256, f=512, V=512, H=4, Hkv=2, Dh=64),
+    "mixtral": dict(L=32, E=8, K=2, d=4096, f=14336, V=32000, H=32, Hkv=8, Dh=128),
+    "phi": dict(L=32, E=16, K=2, d=4096, f=6400, V=32064, H=32, Hkv=8, Dh=128),
+    "qwen3": dict(L=48, E=128, K=8, d=2048, f=768, V=151936, H=32, Hkv=4, Dh=128),
 }
+
+
+def t_attn(l, m):
+    """attention tensors of layer l: 0 = Wqkv [(H+2Hkv)Dh][d], 1 = Wo [d][H Dh], 2 = RMSNorm gamma"""
+    return 0x800000 + l * 16 + m
 
 
 class Model:
@@ -234,6 +250,9 @@ class Model:
         self.m = desc
         self._cache = {}
         self.fast = (desc.d * desc.f >= 1 << 22) if fast is None else fast
+        # the shared KV cache (draft and target write the same rows; rollback = later windows
+        # overwrite): kv[l][pos] = (k [Hkv, Dh], v [Hkv, Dh]) fp32 holding bf16 values
+        self.kv = [dict() for _ in range(desc.L)]
 
     def _get(self, key, fn):
         if key not in self._cache:
@@ -269,6 +288,63 @@ class Model:
                 return out
             return self._get("lm", mk)
         return self._get("lm", lambda: gen(m.seed, T_LM, m.V, m.d, m.a_lm()))
+
+    def _gen_mt(self, tensor, rows, cols, scale):
+        out = np.empty((rows, cols), dtype=np.uint16)
+        lib().orc_gen_rows_mt(tensor_key(self.m.seed, tensor), 0, rows, cols, ctypes.c_float(np.float32(scale)),
+                              _p(out))
+        return out
+
+    def attn_weights(self, l):
+        """(Wqkv fp64 [(H+2Hkv)Dh, d], Wo fp64 [d, H Dh], gamma bf16); cached unless fast."""
+        m = self.m
+        nq, nkv = m.H * m.Dh, m.Hkv * m.Dh
+
+        def mk():
+            wqkv = self._gen_mt(t_attn(l, 0), nq + 2 * nkv, m.d, m.a_qkv())
+            wo = self._gen_mt(t_attn(l, 1), m.d, nq, m.a_o())
+            return (bf16_to_f32(wqkv).astype(np.float64), bf16_to_f32(wo).astype(np.float64),
+                    gen_gamma(m.seed, t_attn(l, 2), m.d))
+        if self.fast:
+            return mk()
+        return self._get(("attn", l), mk)
+
+    def attention(self, h, l, positions, draft_cache=True, ctx=None):
+        """Attention block of layer l for the window rows h [M, d] at consecutive positions:
+        RMSNorm -> QKV (double) -> the window's K/V rounded to bf16 and written to the shared cache
+        -> causal attention over the cache rows before the window (ctx(j) or self.kv) and the
+        window's own rows -> O projection.  Returns the [M, d] fp32 residual update."""
+        m = self.m
+        M = h.shape[0]
+        nq, nkv, G = m.H * m.Dh, m.Hkv * m.Dh, m.H // m.Hkv
+        wqkv, wo, ga = self.attn_weights(l)
+        xa = np.stack([bf16_to_f32(self.rmsnorm(np.ascontiguousarray(h[i]), ga)) for i in range(M)]).astype(np.float64)
+        qkv = (xa @ wqkv.T).astype(np.float32)
+        q = qkv[:, :nq].reshape(M, m.H, m.Dh).astype(np.float64)
+        k_new = bf16_to_f32(f32_to_bf16(qkv[:, nq:nq + nkv])).reshape(M, m.Hkv, m.Dh)
+        v_new = bf16_to_f32(f32_to_bf16(qkv[:, nq + nkv:])).reshape(M, m.Hkv, m.Dh)
+        p0 = positions[0]
+        for i in range(M):
+            self.kv[l][p0 + i] = (k_new[i], v_new[i])
+        if p0 > 0:
+            rows = [ctx(j) if ctx is not None else self.kv[l][j] for j in range(p0)]
+            kc = np.stack([r[0] for r in rows]).astype(np.float64)
+            vc = np.stack([r[1] for r in rows]).astype(np.float64)
+        else:
+            kc = np.zeros((0, m.Hkv, m.Dh))
+            vc = np.zeros((0, m.Hkv, m.Dh))
+        out = np.empty((M, nq), dtype=np.float64)
+        scale = 1.0 / math.sqrt(m.Dh)
+        for i in range(M):
+            keys = np.concatenate([kc, k_new[:i + 1].astype(np.float64)])      # [n, Hkv, Dh]
+            vals = np.concatenate([vc, v_new[:i + 1].astype(np.float64)])
+            for hh in range(m.H):
+                g = hh // G
+                sc = keys[:, g, :] @ q[i, hh] * scale
+                pr = np.exp(sc - sc.max())
+                out[i, hh * m.Dh:(hh + 1) * m.Dh] = (pr @ vals[:, g, :]) / pr.sum()
+        o = bf16_to_f32(f32_to_bf16(out.astype(np.float32))).astype(np.float64)
+        return (o @ wo.T).astype(np.float32)
 
     def expert(self, l, e):
         """bf16 (gate [f,d], up [f,d], down [d,f])."""
@@ -346,36 +422,22 @@ class Model:
         return logits, am
 
     # -- one token ---------------------------------------------------------------------------
-    def forward(self, tok, pos, draft: bool, record=None, h_override=None):
-        """Returns (argmax token, per-layer (ids, wts), final logits).  `h_override[l]`, when
-        given, replaces the residual entering layer l (teacher forcing from the device)."""
-        m = self.m
-        h = (bf16_to_f32(self.embed_row(tok)) + bf16_to_f32(self.pos_row(pos))).astype(np.float32)
-        routing = []
-        for l in range(m.L):
-            if h_override is not None and l in h_override:
-                h = np.asarray(h_override[l], dtype=np.float32).copy()
-            xn = self.rmsnorm(h, self.gamma(l))
-            ids, wts, logits = self.route(xn, l)
-            routing.append((ids.copy(), wts.copy()))
-            acc = np.zeros(m.d, dtype=np.float32)
-            for j in range(m.K):
-                y, _ = self.ffn(xn, l, int(ids[j]), draft)
-                acc = (acc + (np.float32(wts[j]) * y).astype(np.float32)).astype(np.float32)
-            if record is not None:
-                record.append(dict(layer=l, h_in=h.copy(), xn=xn, logits=logits))
-            h = (h + acc).astype(np.float32)
-        xf = self.rmsnorm(h, self.gamma(-1))
-        logits, am = self.lm_head(xf[None, :])
-        return int(am[0]), routing, logits[0]
+    def forward(self, tok, pos, draft: bool):
+        """Returns (argmax token, per-layer (ids, wts), final logits)."""
+        am, routing, logits = forward_batch(self, [tok], [pos], draft, with_logits=True)[0]
+        return am, routing, logits
 
 
-def forward_batch(model: Model, toks, poss, draft: bool, h_in=None, h_trace=None):
-    """forward() for M independent tokens, layer-major with tokens grouped by expert (one weight
-    generation per (layer, expert) in fast mode).  Returns [(argmax, routing)] per token.
-    With `h_in` = {layer: [M, d] fp32}, the residual entering that layer is replaced
-    (teacher forcing from the device).  `h_trace` (a list) receives the [M, d] residual entering
-    each layer and, last, the final one."""
+def forward_batch(model: Model, toks, poss, draft: bool, h_in=None, h_trace=None, with_logits=False,
+                  hmid_trace=None):
+    """Forward pass of a window of M tokens at consecutive positions poss (layer-major, tokens
+    grouped by expert: one weight generation per (layer, expert) in fast mode).  With attention
+    (model.m.H > 0) each layer first runs the shared-KV attention block (Model.attention: the
+    window's K/V rows are written into the model's cache, draft or target alike).
+    Returns [(argmax, routing)] per token (+ logits with `with_logits`).  With `h_in` = {layer:
+    [M, d] fp32}, the residual entering that layer is replaced (teacher forcing from the device).
+    `h_trace` (a list) receives the [M, d] residual entering each layer and, last, the final
+    one; `hmid_trace` the residual after each layer's attention block (what the router sees)."""
     m = model.m
     M = len(toks)
     h = np.stack([(bf16_to_f32(model.embed_row(t)) + bf16_to_f32(model.pos_row(p))).astype(np.float32)
@@ -386,6 +448,10 @@ def forward_batch(model: Model, toks, poss, draft: bool, h_in=None, h_trace=None
             h = np.asarray(h_in[l], dtype=np.float32).copy()
         if h_trace is not None:
             h_trace.append(h.copy())
+        if m.H > 0:
+            h = (h + model.attention(h, l, poss)).astype(np.float32)
+        if hmid_trace is not None:
+            hmid_trace.append(h.copy())
         xn = np.stack([model.rmsnorm(np.ascontiguousarray(h[i]), model.gamma(l)) for i in range(M)])
         rt = [model.route(xn[i], l) for i in range(M)]
         for i in range(M):
@@ -408,24 +474,49 @@ def forward_batch(model: Model, toks, poss, draft: bool, h_in=None, h_trace=None
     if h_trace is not None:
         h_trace.append(h.copy())
     xf = np.stack([model.rmsnorm(np.ascontiguousarray(h[i]), model.gamma(-1)) for i in range(M)])
-    _, am = model.lm_head(xf)
+    lg, am = model.lm_head(xf)
+    if with_logits:
+        return [(int(am[i]), routing[i], lg[i]) for i in range(M)]
     return [(int(am[i]), routing[i]) for i in range(M)]
 
 
-def check_layers(model: Model, h_caps, ids, draft: bool, tol=2e-3):
+def prefill(model: Model, prompt, chunk=17):
+    """The engine's prefill (live.cpp): the target runs the prompt's tokens 0..n-2 (their KV rows)
+    in windows of up to `chunk` = kmax + 1 tokens.  Returns the windows' target routing
+    [[slot][layer] (ids, wts)] per window (for the control-plane replay)."""
+    out = []
+    n = len(prompt) - 1
+    for s0 in range(0, n, chunk):
+        toks = prompt[s0:min(n, s0 + chunk)]
+        res = forward_batch(model, toks, list(range(s0, s0 + len(toks))), draft=False)
+        out.append([r[1] for r in res])
+    return out
+
+
+def check_layers(model: Model, h_caps, ids, draft: bool, tol=2e-3, h_mids=None, positions=None, ctx=None):
     """Teacher-forced per-layer check of a device pass over M tokens.  h_caps [L+1][M][d] = the
     device residual entering each layer (index L = the final residual); ids [L][M][K] = the
     device's routing.  For every layer: routing from the device's own h must be bit-exact, and
     h + sum_j w_j FFN_j(xn) must equal the device's next residual within
     tol * max|h| (accumulation order only).  Returns (worst relative error, margins[L][M] = the
     router's logit gap at the top-K boundary relative to the largest |logit|) for near-tie reporting; raises AssertionError on a
-    mismatch."""
+    mismatch.  With attention, h_mids [L][M][d] = the device residual after each layer's attention
+    block, positions = the window's positions and ctx(l, j) -> (k, v) the device KV rows before
+    the window: the attention block is checked first (h_caps[l] + attn == h_mids[l] within tol),
+    then routing and the MoE from h_mids[l]."""
     m = model.m
     M = h_caps.shape[1]
     worst = 0.0
     margins = [[float("inf")] * M for _ in range(m.L)]
     for l in range(m.L):
         h = np.ascontiguousarray(h_caps[l], dtype=np.float32)
+        if m.H > 0:
+            att = h + model.attention(h, l, positions, ctx=(lambda j, l=l: ctx(l, j)))
+            dev_mid = np.asarray(h_mids[l], dtype=np.float32)
+            err = float(np.abs(att - dev_mid).max()) / (float(np.abs(dev_mid).max()) + 1e-6)
+            worst = max(worst, err)
+            assert err <= tol, ("attention output", l, err)
+            h = np.ascontiguousarray(dev_mid)
         xn = np.stack([model.rmsnorm(np.ascontiguousarray(h[i]), model.gamma(l)) for i in range(M)])
         rt = [model.route(xn[i], l) for i in range(M)]
         for i in range(M):
@@ -450,14 +541,22 @@ def check_layers(model: Model, h_caps, ids, draft: bool, tol=2e-3):
     return worst, margins
 
 
-def speculative_decode(model: Model, last_token: int, start_pos: int, ks, max_new: int):
+def speculative_decode(model: Model, last_token: int, start_pos: int, ks, max_new: int, prompt=None, chunk=17,
+                       deadline=None, prefilled=False):
     """Greedy speculative decoding with the INT4 draft: each cycle drafts k
     tokens from the head (previous bonus), verifies the k+1-slot window with the bf16 target
     (slot i target argmax predicts slot i+1), accepts the longest matching prefix plus the
     target's token at the first mismatch.  Yields per-cycle records; `ks` supplies k per cycle
-    (the governor's choice is a host-timing decision, so the oracle consumes it)."""
+    (the governor's choice is a host-timing decision, so the oracle consumes it).  With attention
+    the prompt is prefilled first (`prompt`, windows of `chunk` tokens).  `deadline`
+    (time.perf_counter() value, bench CPU baseline) stops after the cycle that passes it;
+    `prefilled`: the model's KV cache already holds the prompt (prefill not repeated)."""
     out, tok, pos, committed = [], last_token, start_pos, 0
     ci = 0
+    if model.m.H > 0 and not prefilled:  # attention: fresh shared KV cache, then the prompt's prefill
+        assert prompt is not None and prompt[-1] == last_token and len(prompt) - 1 == start_pos
+        model.kv = [dict() for _ in range(model.m.L)]
+        model.prefill_routing = prefill(model, prompt, chunk)
     while committed < max_new:
         k = min(ks[ci] if ci < len(ks) else ks[-1], max_new - committed)
         k = max(k, 1)
@@ -484,4 +583,8 @@ def speculative_decode(model: Model, last_token: int, start_pos: int, ks, max_ne
         pos += acc + 1
         tok = bonus
         ci += 1
+        if deadline is not None:
+            import time
+            if time.perf_counter() >= deadline:
+                break
     return out

@@ -22,12 +22,13 @@ __version__ = "0.1.0"
 
 POLICIES = ["lru", "lookahead", "sp-sooner", "sp-later", "speculative"]
 
-# BASELINE.json shapes (tiny ffn chosen = 512; Qwen3-30B-A3B moe_intermediate = 768)
+# BASELINE.json shapes (tiny ffn chosen = 512; Qwen3-30B-A3B moe_intermediate = 768) with the
+# named models' attention heads (H query, Hkv KV, head dim Dh; tiny chosen 4/2/64)
 MODEL_SHAPES = {
-    "tiny": dict(L=4, E=8, K=2, d=256, f=512, V=512),
-    "mixtral": dict(L=32, E=8, K=2, d=4096, f=14336, V=32000),
-    "phi": dict(L=32, E=16, K=2, d=4096, f=6400, V=32064),
-    "qwen3": dict(L=48, E=128, K=8, d=2048, f=768, V=151936),
+    "tiny": dict(L=4, E=8, K=2, d=256, f=512, V=512, H=4, Hkv=2, Dh=64),
+    "mixtral": dict(L=32, E=8, K=2, d=4096, f=14336, V=32000, H=32, Hkv=8, Dh=128),
+    "phi": dict(L=32, E=16, K=2, d=4096, f=6400, V=32064, H=32, Hkv=8, Dh=128),
+    "qwen3": dict(L=48, E=128, K=8, d=2048, f=768, V=151936, H=32, Hkv=4, Dh=128),
 }
 
 
@@ -49,6 +50,9 @@ class ModelConfig:
     lm_scale: float = 1.0
     eps: float = 1e-6
     unique_experts: int = 0
+    H: int = 0      # attention query heads (0 = attention-free layers)
+    Hkv: int = 0    # KV heads
+    Dh: int = 0     # head dim
 
     @classmethod
     def named(cls, name, **kw):
@@ -67,7 +71,16 @@ class ModelConfig:
                               f32(math.sqrt(3.0 / self.d)),
                               f32(self.moe_scale * math.sqrt(3.0 / self.f)),
                               f32(self.lm_scale * math.sqrt(3.0 / self.d)), self.eps,
-                              self.unique_experts)
+                              self.unique_experts, self.H, self.Hkv, self.Dh,
+                              f32(math.sqrt(3.0 / self.d)),
+                              f32(self.moe_scale * math.sqrt(3.0 / max(1, self.H * self.Dh))))
+
+    def oracle_kwargs(self) -> dict:
+        """The fields oracle/model.py ModelDesc takes (tests build the CPU oracle from these)."""
+        return dict(L=self.L, E=self.E, K=self.K, d=self.d, f=self.f, V=self.V, P=self.P, seed=self.seed,
+                    embed_scale=self.embed_scale, pos_scale=self.pos_scale, router_scale=self.router_scale,
+                    moe_scale=self.moe_scale, lm_scale=self.lm_scale, eps=self.eps, H=self.H, Hkv=self.Hkv,
+                    Dh=self.Dh)
 
     def expert_bytes_bf16(self):
         return lib().mspq_bf16_blob_bytes(self.d, self.f)

@@ -18,7 +18,8 @@ class ModelDesc(ctypes.Structure):
                 ("V", c_int), ("P", c_int), ("seed", c_ull), ("embed_scale", c_float),
                 ("pos_scale", c_float), ("a_router", c_float), ("a_up", c_float),
                 ("a_down", c_float), ("a_lm", c_float), ("eps", c_float),
-                ("unique_experts", c_int)]
+                ("unique_experts", c_int), ("H", c_int), ("Hkv", c_int), ("Dh", c_int),
+                ("a_qkv", c_float), ("a_o", c_float)]
 
 
 class EngineOpts(ctypes.Structure):
@@ -45,6 +46,10 @@ _SIGS = [
     ("mspq_moe_bf16_tc", c_int, [c_void_p] * 8 + [c_ll] + [c_int] * 7 + [c_void_p] * 3),
     ("mspq_moe_bf16_tc_part", c_int, [c_void_p] * 8 + [c_ll] + [c_int] * 7 + [c_void_p] * 3 + [c_int, c_void_p]),
     ("mspq_tile_bf16", c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p]),
+    ("mspq_dense_ws_bytes", c_ll, [c_int, c_int]),
+    ("mspq_dense_sched_fill", c_int, [c_void_p, c_int]),
+    ("mspq_dense_bf16_tc", c_int, [c_void_p] * 3 + [c_int] * 4 + [c_void_p, c_void_p, c_ll, c_void_p]),
+    ("mspq_attention", c_int, [c_void_p, c_int, c_ll] + [c_int] * 5 + [c_void_p] * 5),
     ("mspq_moe_int4_tc", c_int, [c_void_p] * 8 + [c_ll] + [c_int] * 9 + [c_void_p] * 3),
     ("mspq_tile_int4", c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p]),
     ("mspq_debug_timeline", c_int, [c_void_p, c_int]),

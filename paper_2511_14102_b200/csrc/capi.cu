@@ -165,6 +165,39 @@ int mspq_moe_bf16_tc(const int32_t* n_groups, const int32_t* group_expert, const
   return mspq_moe_bf16_tc_part(n_groups, group_expert, group_buf, group_off, entry_tok, entry_group, xn, pool,
                                blob_bytes, d, f, T, K, max_groups, split1, split2, ws, y, nullptr, 1, stream);
 }
+// dense projection = K3 with one group holding all T tokens; dsched packed per T:
+// [n_groups = 1, group_buf = 0, group_off = {0, T}, entry_tok = 0..T-1]
+long long mspq_dense_ws_bytes(int kdim, int T) { return (long long)(kdim / 64) * tc_bn(T) * 128 + 1024; }
+int mspq_dense_sched_fill(int32_t* host_packed, int T) {
+  host_packed[0] = 1;
+  host_packed[1] = 0;
+  host_packed[2] = 0;
+  host_packed[3] = T;
+  for (int t = 0; t < T; ++t) host_packed[4 + t] = t;
+  return MSPQ_OK;
+}
+int mspq_dense_bf16_tc(const int32_t* dsched, const void* x, const void* w_tiled, int rows, int kdim, int T,
+                       int split, void* ws, float* out, long long out_split_stride, void* stream) {
+  if (rows % 128 || kdim % 64 || T < 1 || T > 32 || split < 1 || split > kdim / 64)
+    return set_error(MSPQ_ERR_SHAPE_MISMATCH, "dense_bf16_tc: rows % 128, kdim % 64, 1 <= T <= 32, 1 <= split <= kdim/64");
+  const int BN = tc_bn(T);
+  int32_t* p = (int32_t*)dsched;
+  SchedPtrs s{p, nullptr, p + 1, p + 2, p + 4, nullptr, nullptr};
+  cudaStream_t st = ST(stream);
+  unsigned char* b1 = (unsigned char*)ws;
+  cudaError_t e = launch_gather_b((const uint16_t*)x, kdim, s, 1, kdim, BN, b1, st);
+  if (e != cudaSuccess) return cuda_status(e, "dense gather");
+  UmmaArgs u{(const unsigned char*)w_tiled, 0, 0, rows, kdim, p, p + 1, p + 2, b1, out, out_split_stride, split};
+  CK(launch_umma_grouped(u, 1, BN, st), "dense umma");
+}
+int mspq_attention(const float* qkv, int splits, long long split_stride, int T, int H, int Hkv, int Dh, int P,
+                   const int32_t* pos0, void* kc, void* vc, void* out, void* stream) {
+  if (H < 1 || Hkv < 1 || H % Hkv || H / Hkv > 8 || Dh % 32 || T < 1 || P < T)
+    return set_error(MSPQ_ERR_SHAPE_MISMATCH, "attention: Hkv | H, H/Hkv <= 8, Dh % 32, 1 <= T <= P");
+  AttnArgs a{qkv, splits, split_stride, T, H, Hkv, Dh, P, pos0, (uint16_t*)kc, (uint16_t*)vc, (uint16_t*)out,
+             1.0f / sqrtf((float)Dh)};
+  CK(launch_attn_window(a, ST(stream)), "attention");
+}
 int mspq_moe_int4_tc(const int32_t* n_groups, const int32_t* group_expert, const int32_t* group_buf,
                      const int32_t* group_off, const int32_t* entry_tok, const int32_t* entry_group,
                      const void* xn, const void* blobs, long long blob_bytes, int layer, int E, int d, int f, int T,

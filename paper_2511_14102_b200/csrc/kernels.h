@@ -121,6 +121,21 @@ struct RouteArgs {
   float eps;
 };
 
+// Shared-KV decode attention over a window of T tokens (attention.cu)
+struct AttnArgs {
+  const float* qkv;        // [splits][T][(H + 2 Hkv) Dh] fp32 partial planes of the QKV projection
+  int splits;
+  int64_t split_stride;
+  int T, H, Hkv, Dh, P;
+  const int32_t* pos0;     // device: position of window token 0
+  uint16_t* kc;            // this layer's K cache [P][Hkv][Dh] bf16
+  uint16_t* vc;            // V cache
+  uint16_t* out;           // [T][H Dh] bf16 attention output
+  float scale;             // 1/sqrt(Dh)
+};
+size_t attn_smem_bytes(int T, int H, int Hkv, int Dh, int P);
+cudaError_t launch_attn_window(const AttnArgs& a, cudaStream_t st);
+
 cudaError_t launch_umma_grouped(const UmmaArgs& a, int max_groups, int BN, cudaStream_t st);
 cudaError_t launch_umma_int4(const UmmaArgs& a, int max_groups, int BN, cudaStream_t st);
 cudaError_t launch_umma_int4p(const UmmaArgs& a, int max_groups, cudaStream_t st);

@@ -123,9 +123,12 @@ __global__ void __launch_bounds__(256) k_resid_norm_route(RouteArgs a) {
     float4 cb[MAXC];
 #pragma unroll
     for (int i = 0; i < MAXC; ++i) cb[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int j = 0; j < a.K; ++j) {
-      const float w = a.prev_wts[t * a.K + j];
-      const float* yb = a.y + (int64_t)a.entry_of[t * a.K + j] * a.d;
+    // MoE combine: h += sum_j w_j y[entry_of(t, j)]; dense combine (entry_of == NULL, the
+    // attention output projection): h += y[t], weight 1 (exact)
+    const int nj = a.entry_of ? a.K : 1;
+    for (int j = 0; j < nj; ++j) {
+      const float w = a.entry_of ? a.prev_wts[t * a.K + j] : 1.0f;
+      const float* yb = a.y + (int64_t)(a.entry_of ? a.entry_of[t * a.K + j] : t) * a.d;
       float4 yv[MAXC];
 #pragma unroll
       for (int i = 0; i < MAXC; ++i)

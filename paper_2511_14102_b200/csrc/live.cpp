@@ -175,6 +175,22 @@ struct mspq_engine {
   // for the verify window [L+1][T][d] and each draft row [k][L+1][d], kept per cycle of the
   // last generate() and read back with mspq_engine_read("hcap_v:<cycle>" / "hcap_d:<cycle>")
   float *hcap_v = nullptr, *hcap_dstage = nullptr, *hcap_d = nullptr;
+  float *hmid_v = nullptr, *hmid_dstage = nullptr, *hmid_d = nullptr;  // after the attention residual
+  std::vector<std::vector<float>> hmid_v_hist, hmid_d_hist;
+  // attention: bf16 weights shared by draft and target, tile-major per layer
+  // [Wqkv (H+2Hkv)Dh x d | Wo d x H Dh]; one KV cache [L][P][Hkv][Dh] shared by both
+  bool attn = false;
+  int Nq = 0, Nkv = 0, Nqkv = 0;
+  unsigned char* wattn = nullptr;
+  size_t wattn_layer = 0;
+  uint16_t* gamma_a = nullptr;
+  uint16_t *kcache = nullptr, *vcache = nullptr;
+  float *qkv = nullptr, *oproj = nullptr;  // split planes [kMaxSplit][Tmax][Nqkv | d]
+  uint16_t* ao = nullptr;                  // [Tmax][Nq] attention output
+  int32_t* dsched = nullptr;               // [Tmax + 1][4 + Tmax] packed dense schedules per T
+  void* dws = nullptr;
+  int32_t* dsched_of(int T) { return dsched + (size_t)T * (4 + Tmax); }
+  size_t kv_layer() const { return (size_t)m.P * m.Hkv * m.Dh; }
   int32_t* sched_cap = nullptr;  // collect_plans: each verify layer's device schedule [L][Sched::ints]
   // peer-expert tier (home partitioning, include/mspq_capi.h (3)): expert (l, e) lives in the home
   // region of engine e % peer_G at slot l * home_per_layer + e / peer_G
@@ -238,6 +254,29 @@ void make_weights(mspq_engine* E) {
   CAPI_OK(mspq_fill_bf16(m.seed, 2, m.pos_scale, 0, E->pos, (long long)n_pos, 0, s));
   CAPI_OK(mspq_fill_bf16(m.seed, 3, m.a_lm, 0, E->lm, (long long)n_lm, 0, s));
   CAPI_OK(mspq_fill_bf16(m.seed, 4, 0.f, 1, E->gfinal, d, 0, s));
+  if (E->attn) {  // tensor ids 0x800000 + 16 l + {0: Wqkv, 1: Wo, 2: attention RMSNorm gamma}
+    const size_t nqkv = (size_t)E->Nqkv * d, no = (size_t)d * E->Nq;
+    E->wattn_layer = (nqkv + no) * 2;
+    CUDA_OK(cudaMalloc(&E->wattn, (size_t)m.L * E->wattn_layer));
+    CUDA_OK(cudaMalloc(&E->gamma_a, (size_t)m.L * d * 2));
+    uint16_t* stg;
+    CUDA_OK(cudaMalloc(&stg, std::max(nqkv, no) * 2));
+    for (int l = 0; l < m.L; ++l) {
+      const uint64_t tb = 0x800000ull + (uint64_t)l * 16;
+      unsigned char* wl = E->wattn + (size_t)l * E->wattn_layer;
+      CAPI_OK(mspq_fill_bf16(m.seed, tb + 0, m.a_qkv, 0, stg, (long long)nqkv, 0, s));
+      CAPI_OK(mspq_tile_bf16(stg, E->Nqkv, d, wl, s));
+      CAPI_OK(mspq_fill_bf16(m.seed, tb + 1, m.a_o, 0, stg, (long long)no, 0, s));
+      CAPI_OK(mspq_tile_bf16(stg, d, E->Nq, wl + nqkv * 2, s));
+      CAPI_OK(mspq_fill_bf16(m.seed, tb + 2, 0.f, 1, E->gamma_a + (size_t)l * d, d, 0, s));
+    }
+    CUDA_OK(cudaStreamSynchronize((cudaStream_t)s));
+    cudaFree(stg);
+    CUDA_OK(cudaMalloc(&E->kcache, (size_t)m.L * E->kv_layer() * 2));
+    CUDA_OK(cudaMalloc(&E->vcache, (size_t)m.L * E->kv_layer() * 2));
+    CUDA_OK(cudaMemset(E->kcache, 0, (size_t)m.L * E->kv_layer() * 2));
+    CUDA_OK(cudaMemset(E->vcache, 0, (size_t)m.L * E->kv_layer() * 2));
+  }
   for (int l = 0; l < m.L; ++l) {
     CAPI_OK(mspq_fill_bf16(m.seed, 0x100ull + (uint64_t)l * 16, 0.f, 1, E->gamma + (size_t)l * d, d, 0, s));
     CAPI_OK(mspq_fill_bf16(m.seed, 0x100ull + (uint64_t)l * 16 + 1, m.a_router, 0, E->router + (size_t)l * m.E * d,
@@ -418,10 +457,26 @@ void make_workspaces(mspq_engine* E) {
                  (size_t)L * m.E + 64;
   CUDA_OK(cudaHostAlloc((void**)&E->hpin, E->hpin_ints * 4, 0));
   CUDA_OK(cudaMalloc(&E->sched_cap, (size_t)L * sched_ints * 4));
+  if (E->attn) {
+    const int KS = mspq_engine::kMaxSplit;
+    CUDA_OK(cudaMalloc(&E->qkv, (size_t)KS * T * E->Nqkv * 4));
+    CUDA_OK(cudaMalloc(&E->oproj, (size_t)KS * T * d * 4));
+    CUDA_OK(cudaMalloc(&E->ao, (size_t)T * E->Nq * 2));
+    CUDA_OK(cudaMalloc(&E->dws, (size_t)mspq_dense_ws_bytes(std::max(d, E->Nq), T)));
+    std::vector<int32_t> ds((size_t)(T + 1) * (4 + T), 0);
+    for (int t = 1; t <= T; ++t) mspq_dense_sched_fill(ds.data() + (size_t)t * (4 + T), t);
+    CUDA_OK(cudaMalloc(&E->dsched, ds.size() * 4));
+    CUDA_OK(cudaMemcpy(E->dsched, ds.data(), ds.size() * 4, cudaMemcpyHostToDevice));
+  }
   if (E->o.trace_level >= 3) {
     CUDA_OK(cudaMalloc(&E->hcap_v, (size_t)(L + 1) * T * d * 4));
     CUDA_OK(cudaMalloc(&E->hcap_dstage, (size_t)(L + 1) * d * 4));
     CUDA_OK(cudaMalloc(&E->hcap_d, (size_t)E->o.kmax * (L + 1) * d * 4));
+    if (E->attn) {
+      CUDA_OK(cudaMalloc(&E->hmid_v, (size_t)L * T * d * 4));
+      CUDA_OK(cudaMalloc(&E->hmid_dstage, (size_t)L * d * 4));
+      CUDA_OK(cudaMalloc(&E->hmid_d, (size_t)E->o.kmax * L * d * 4));
+    }
   }
 }
 
@@ -432,6 +487,35 @@ int split_for(int units_per_split1, int kblocks) {
   const int units = std::max(1, units_per_split1);
   const int sp = std::max(1, 148 / units);  // persistent K2: one CTA per SM
   return std::max(1, std::min({sp, mspq_engine::kMaxSplit, std::max(1, kblocks / 2)}));
+}
+
+// K splits for a dense projection: >= ~2 CTAs per SM of tcgen05 units
+int dense_split(int rows, int kdim) {
+  const int units = std::max(1, rows / 128);
+  return std::max(1, std::min({(296 + units - 1) / units, mspq_engine::kMaxSplit, kdim / 64}));
+}
+
+// Attention block of layer l for the T tokens in E->h (positions *pos0 ..): K1 (the previous
+// layer's MoE combine + attention RMSNorm) -> QKV projection -> shared-KV attention -> O
+// projection into E->oproj (split planes).  The caller's next K1 adds them (dense combine) and
+// routes.  Returns the O projection's split count.  cap_in (nullable): copy of the residual
+// entering the layer (trace_level 3).
+int enqueue_attn(mspq_engine* E, int l, int T, const int32_t* pos0, const float* y, const int32_t* entry_of,
+                 const float* wts, int y_splits, long long y_stride, float* cap_in, cudaStream_t s) {
+  const auto& m = E->m;
+  const int d = m.d;
+  CAPI_OK(mspq_gate_topk(E->h, y, entry_of, wts, y_splits, y_stride, E->gamma_a + (size_t)l * d, nullptr, E->xn,
+                         nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, l, m.L, T, d, m.E, m.K, m.eps,
+                         s));
+  if (cap_in) CUDA_OK(cudaMemcpyAsync(cap_in, E->h, (size_t)T * d * 4, cudaMemcpyDeviceToDevice, s));
+  const unsigned char* wl = E->wattn + (size_t)l * E->wattn_layer;
+  const int spq = dense_split(E->Nqkv, d), spo = dense_split(d, E->Nq);
+  CAPI_OK(mspq_dense_bf16_tc(E->dsched_of(T), E->xn, wl, E->Nqkv, d, T, spq, E->dws, E->qkv, (long long)T * E->Nqkv, s));
+  CAPI_OK(mspq_attention(E->qkv, spq, (long long)T * E->Nqkv, T, m.H, m.Hkv, m.Dh, m.P, pos0,
+                         E->kcache + (size_t)l * E->kv_layer(), E->vcache + (size_t)l * E->kv_layer(), E->ao, s));
+  CAPI_OK(mspq_dense_bf16_tc(E->dsched_of(T), E->ao, wl + (size_t)E->Nqkv * d * 2, d, E->Nq, T, spo, E->dws, E->oproj,
+                             (long long)T * d, s));
+  return spo;
 }
 
 void enqueue_draft_step(mspq_engine* E, cudaStream_t s) {
@@ -445,13 +529,26 @@ void enqueue_draft_step(mspq_engine* E, cudaStream_t s) {
   CAPI_OK(mspq_embed(E->embed, E->pos, cur_tok, cur_pos, 1, d, E->h, s));
   for (int l = 0; l < L; ++l) {
     const int pl = (l - 1) & 1;
-    CAPI_OK(mspq_gate_topk(E->h, l ? E->yd[pl] : nullptr, l ? E->sd[pl].entry_of : nullptr,
-                           l ? E->wts_d + (size_t)(l - 1) * K : nullptr, E->yd_split2, (long long)K * d,
-                           E->gamma + (size_t)l * d,
+    const float* y = l ? E->yd[pl] : nullptr;
+    const int32_t* eo = l ? E->sd[pl].entry_of : nullptr;
+    const float* pw = l ? E->wts_d + (size_t)(l - 1) * K : nullptr;
+    int ysp = E->yd_split2;
+    long long yst = (long long)K * d;
+    if (E->attn) {  // attention first: its K1 takes the MoE combine, the MoE K1 the dense one
+      ysp = enqueue_attn(E, l, 1, cur_pos, y, eo, pw, ysp, yst, E->hcap_dstage ? E->hcap_dstage + (size_t)l * d : nullptr,
+                         s);
+      y = E->oproj;
+      eo = nullptr;
+      pw = nullptr;
+      yst = d;
+    }
+    CAPI_OK(mspq_gate_topk(E->h, y, eo, pw, ysp, yst, E->gamma + (size_t)l * d,
                            E->router + (size_t)l * m.E * d, E->xn, E->ids_d + (size_t)l * K, E->wts_d + (size_t)l * K,
                            nullptr, E->view.elb_ids, E->view.elb_gates, row, E->sd[l & 1].base, l, L, 1, d, m.E, K,
                            m.eps, s));
-    if (E->hcap_dstage)
+    if (E->hmid_dstage)
+      CUDA_OK(cudaMemcpyAsync(E->hmid_dstage + (size_t)l * d, E->h, (size_t)d * 4, cudaMemcpyDeviceToDevice, s));
+    else if (E->hcap_dstage && !E->attn)
       CUDA_OK(cudaMemcpyAsync(E->hcap_dstage + (size_t)l * d, E->h, (size_t)d * 4, cudaMemcpyDeviceToDevice, s));
     Sched& sc = E->sd[l & 1];
     CAPI_OK(mspq_moe_int4_tc(sc.n_groups, sc.group_expert, sc.group_buf, sc.group_off, sc.entry_tok, sc.entry_group,
@@ -806,6 +903,8 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
   E->deferred.clear();
   E->hcap_v_hist.clear();
   E->hcap_d_hist.clear();
+  E->hmid_v_hist.clear();
+  E->hmid_d_hist.clear();
   E->gen_peer_bytes = E->gen_home_local_bytes = 0;
   E->n_peer = E->n_home_local = 0;
   if (E->pf_lane) CUDA_OK(cudaStreamWaitEvent(E->sx2, E->ev_t0, 0));
@@ -815,72 +914,47 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
   uint64_t h2d_bytes = 0, total_new = 0, layer_cov_count = 0, step_total = 0, acc_total = 0;
   const auto wall0 = std::chrono::steady_clock::now();
   int ci = 0;
-  long launches = 0, k3_groups = 0, draft_steps = 0;
+  long k3_groups = 0, draft_steps = 0;
   double k3_time = 0.0, k3_bytes = 0.0, draft_time = 0.0;
+  // verify layers of one window of T tokens (positions head .. head+T-1 in E->win_pos(), tokens
+  // in E->win_tok(), residual embedded in E->h): per layer [attention] -> K1 route -> controller
+  // verify step -> copies -> K3.  Also runs prefill chunks (prefill: no captures / plans).
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> stall_ev;
+  long launches = 0;
   std::vector<int> layer_groups(L, 0);
-  while ((int)committed.size() < max_new) {
-    const int rem = max_new - (int)committed.size();
-    const int cycle = ++E->cycle_serial;
-    E->ev_pool_next = 0;
-    const int kk = c.use_governor ? select_k(prof, accept, c.k_min, c.k_max, k_slo, est()) : c.fixed_k;
-    const int k = std::max(1, std::min({kk, rem, E->o.kmax}));
-    const int T = k + 1;
-    const int est_new = c.use_governor ? est()(k) : -1;
-    const double est_raw = c.estimator == 1 ? elb_raw(k) : 0.0;
-    uint64_t cyc_bytes = 0;
-    std::vector<CopyBatch> batches;
-    // ---------------- draft + planner
-    CUDA_OK(cudaEventRecord(E->ev_c0, E->sc));
-    CUDA_OK(cudaMemsetAsync(E->dst, 0, 4, E->sc));  // row = 0
-    CAPI_OK(mspq_cache_begin_cycle(E->cache, k, E->sc));
-    CUDA_OK(cudaEventRecord(E->ev_g0[0], E->sc));
-    CUDA_OK(cudaGraphLaunch(E->gexec, E->sc));
-    CUDA_OK(cudaEventRecord(E->ev_g1[0], E->sc));
-    if (E->hcap_d) CUDA_OK(cudaMemcpyAsync(E->hcap_d, E->hcap_dstage, (size_t)(L + 1) * d * 4, cudaMemcpyDeviceToDevice, E->sc));
-    launches += E->graph_nodes;
-    for (int i = 0; i < k; ++i) {
-      CAPI_OK(mspq_cache_plan_row(E->cache, i, E->sc));
-      CUDA_OK(cudaEventRecord(E->ev_row[i], E->sc));
-      ++launches;
-      if (i + 1 < k) {
-        CUDA_OK(cudaEventRecord(E->ev_g0[i + 1], E->sc));
-        CUDA_OK(cudaGraphLaunch(E->gexec, E->sc));
-        CUDA_OK(cudaEventRecord(E->ev_g1[i + 1], E->sc));
-        if (E->hcap_d)
-          CUDA_OK(cudaMemcpyAsync(E->hcap_d + (size_t)(i + 1) * (L + 1) * d, E->hcap_dstage, (size_t)(L + 1) * d * 4,
-                                  cudaMemcpyDeviceToDevice, E->sc));
-        launches += E->graph_nodes;
-      }
-      spin_wait(E->ev_row[i]);
-      CopyBatch b;
-      issue_copies(E, cycle, b, cyc_bytes, true);
-      if (b.count) batches.push_back(b);
-    }
-    CUDA_OK(cudaEventRecord(E->ev_dend, E->sc));
-    // ---------------- verify (layer-major)
-    for (int s = 0; s < T; ++s) E->hpin[s] = head_pos + s;
-    CUDA_OK(cudaMemcpyAsync(E->win_pos(), E->hpin, T * 4, cudaMemcpyHostToDevice, E->sc));
-    CAPI_OK(mspq_embed(E->embed, E->pos, E->win_tok(), E->win_pos(), T, d, E->h, E->sc));
-    double stall = 0.0;
-    int demand_total = 0;
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> stall_ev;
+  auto verify_layers = [&](int T, int cycle, bool prefill, std::vector<CopyBatch>& batches, uint64_t& cyc_bytes) {
     for (int l = 0; l < L; ++l) {
       const int pl = (l - 1) & 1;
       int32_t* tgt = E->ids_t + (size_t)l * T * K;
-      CAPI_OK(mspq_gate_topk(E->h, l ? E->yv[pl] : nullptr, l ? E->sv[pl].entry_of : nullptr,
-                             l ? E->wts_t + (size_t)(l - 1) * T * K : nullptr, E->yv_splits[pl],
-                             (long long)T * K * d, E->gamma + (size_t)l * d,
+      const float* y = l ? E->yv[pl] : nullptr;
+      const int32_t* eo = l ? E->sv[pl].entry_of : nullptr;
+      const float* pw = l ? E->wts_t + (size_t)(l - 1) * T * K : nullptr;
+      int ysp = E->yv_splits[pl];
+      long long yst = (long long)T * K * d;
+      const bool cap = E->hcap_v && !prefill;
+      if (E->attn) {
+        ysp = enqueue_attn(E, l, T, E->win_pos(), y, eo, pw, ysp, yst, cap ? E->hcap_v + (size_t)l * T * d : nullptr,
+                           E->sc);
+        y = E->oproj;
+        eo = nullptr;
+        pw = nullptr;
+        yst = (long long)T * d;
+        launches += 4;
+      }
+      CAPI_OK(mspq_gate_topk(E->h, y, eo, pw, ysp, yst, E->gamma + (size_t)l * d,
                              E->router + (size_t)l * Ex * d, E->xn, tgt, E->wts_t + (size_t)l * T * K, nullptr, nullptr,
                              nullptr, nullptr, nullptr, l, L, T, d, Ex, K, m.eps, E->sc));
       Sched& sv = E->sv[l & 1];
-      if (E->hcap_v)
+      if (cap && E->attn)
+        CUDA_OK(cudaMemcpyAsync(E->hmid_v + (size_t)l * T * d, E->h, (size_t)T * d * 4, cudaMemcpyDeviceToDevice, E->sc));
+      else if (cap)
         CUDA_OK(cudaMemcpyAsync(E->hcap_v + (size_t)l * T * d, E->h, (size_t)T * d * 4, cudaMemcpyDeviceToDevice, E->sc));
       if (level >= 1) CUDA_OK(cudaEventRecord(E->ev_rt[l], E->sc));
       CAPI_OK(mspq_cache_verify_layer(E->cache, l, T, tgt, E->gbuf, E->sc));
       CUDA_OK(cudaEventRecord(E->ev_w0[l], E->sc));
       CAPI_OK(mspq_build_schedule(tgt, T, K, Ex, E->gbuf, sv.n_groups, sv.group_expert, sv.group_buf, sv.group_off,
                                   sv.entry_tok, sv.entry_of, sv.entry_group, E->sc));
-      if (c.collect_plans)
+      if (c.collect_plans && !prefill)
         CUDA_OK(cudaMemcpyAsync(E->sched_cap + (size_t)l * Sched::ints(E->G, E->N), sv.base,
                                 Sched::ints(E->G, E->N) * 4, cudaMemcpyDeviceToDevice, E->sc));
       spin_wait(E->ev_w0[l]);
@@ -962,15 +1036,149 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
       }
       CUDA_OK(cudaEventRecord(E->ev_gemm[l], E->sc));
       launches += 7;  // gate_topk, verify_layer, schedule, gather, 2 x tcgen05 GEMM, finalize
-      k3_groups += ng;
       layer_groups[l] = ng;
       for (int gi = 0; gi < ng; ++gi) {
         const int buf = gb[gi];
         E->last_cycle[buf] = cycle;
         E->last_layer[buf] = l;
       }
-      demand_total += 0;
     }
+  };
+  // ---------------- prefill (attention models): the prompt's KV rows 0 .. n_prompt-2 through the
+  // same verify pass (target model, controller demand steps) in windows of up to Tmax tokens with
+  // no draft (k = 0).  Its cache decisions are part of the run (oracle/control_plane replays them
+  // first); its time is reported apart from the decode metric (TTFT vs TPOT).
+  json prefill = json::object();
+  if (E->attn && n_prompt > 1) {
+    const auto pw0 = std::chrono::steady_clock::now();
+    int done = 0, pf_new = 0;
+    uint64_t pf_bytes = 0;
+    json chunks = json::array();
+    while (done < n_prompt - 1) {
+      const int T = std::min(E->Tmax, n_prompt - 1 - done);
+      const int cycle = ++E->cycle_serial;
+      E->ev_pool_next = 0;
+      for (int s2 = 0; s2 < T; ++s2) {
+        E->hpin[s2] = prompt[done + s2];
+        E->hpin[E->Tmax + 1 + s2] = done + s2;
+      }
+      CUDA_OK(cudaMemcpyAsync(E->win_tok(), E->hpin, T * 4, cudaMemcpyHostToDevice, E->sc));
+      CUDA_OK(cudaMemcpyAsync(E->win_pos(), E->hpin + E->Tmax + 1, T * 4, cudaMemcpyHostToDevice, E->sc));
+      CAPI_OK(mspq_cache_begin_cycle(E->cache, 0, E->sc));
+      CAPI_OK(mspq_embed(E->embed, E->pos, E->win_tok(), E->win_pos(), T, d, E->h, E->sc));
+      std::vector<CopyBatch> pb;
+      uint64_t cb = 0;
+      stall_ev.clear();
+      verify_layers(T, cycle, true, pb, cb);
+      if (level >= 1)
+        CUDA_OK(cudaMemcpyAsync(E->hpin, E->ids_t, (size_t)L * T * K * 4, cudaMemcpyDeviceToHost, E->sc));
+      CUDA_OK(cudaEventRecord(E->ev_end, E->sc));
+      CUDA_OK(cudaEventSynchronize(E->ev_end));
+      json ch;
+      ch["start_pos"] = done;
+      ch["T"] = T;
+      ch["new_experts"] = E->view.host_stat[S_FETCHED];
+      ch["bytes"] = cb;
+      pf_new += E->view.host_stat[S_FETCHED];
+      pf_bytes += cb;
+      if (level >= 1) {
+        json tgt = json::array();  // [slot][layer][K]
+        for (int s2 = 0; s2 < T; ++s2) {
+          json sl = json::array();
+          for (int l = 0; l < L; ++l) {
+            json c2 = json::array();
+            for (int j = 0; j < K; ++j) c2.push_back(E->hpin[((size_t)l * T + s2) * K + j]);
+            sl.push_back(c2);
+          }
+          tgt.push_back(sl);
+        }
+        ch["target"] = tgt;
+      }
+      if (level >= 2) {
+        const int nl = std::min(E->view.host_stat[S_NLOG], E->view.log_cap);
+        std::vector<int32_t> lg((size_t)nl * 6);
+        if (nl) CUDA_OK(cudaMemcpy(lg.data(), E->view.log, (size_t)nl * 24, cudaMemcpyDeviceToHost));
+        json lj = json::array();
+        for (int i = 0; i < nl; ++i) {
+          const int32_t* ev = &lg[(size_t)i * 6];
+          lj.push_back({ev[0], ev[1], ev[2] / Ex, ev[2] % Ex, ev[3], ev[4] < 0 ? -1 : ev[4] / Ex,
+                        ev[4] < 0 ? -1 : ev[4] % Ex, ev[5]});
+        }
+        ch["log"] = lj;
+      }
+      chunks.push_back(ch);
+      done += T;
+    }
+    CUDA_OK(cudaStreamSynchronize(E->sx));
+    if (E->sdec) CUDA_OK(cudaStreamSynchronize(E->sdec));
+    if (c.estimator == 1) CUDA_OK(cudaMemcpy(E->res_host.data(), E->view.res, (size_t)L * Ex * 4, cudaMemcpyDeviceToHost));
+    prefill["tokens"] = n_prompt - 1;
+    prefill["new_experts"] = pf_new;
+    prefill["h2d_bytes"] = pf_bytes;
+    prefill["time_s"] = std::chrono::duration<double>(std::chrono::steady_clock::now() - pw0).count();
+    prefill["chunks"] = chunks;
+    // the decode state (head token / position) the prefill windows overwrote
+    E->hpin[0] = 0;
+    E->hpin[1] = prompt[n_prompt - 1];
+    E->hpin[2] = head_pos;
+    CUDA_OK(cudaMemcpyAsync(E->dst, E->hpin, 12, cudaMemcpyHostToDevice, E->sc));
+    CUDA_OK(cudaMemcpyAsync(E->win_tok(), E->hpin + 1, 4, cudaMemcpyHostToDevice, E->sc));
+    CUDA_OK(cudaEventRecord(E->ev_t0, E->sc));  // the decode's clock starts after the prefill
+    CUDA_OK(cudaStreamWaitEvent(E->sx, E->ev_t0, 0));
+    if (E->sdec) CUDA_OK(cudaStreamWaitEvent(E->sdec, E->ev_t0, 0));
+  }
+  const auto wall_dec0 = std::chrono::steady_clock::now();
+  while ((int)committed.size() < max_new) {
+    const int rem = max_new - (int)committed.size();
+    const int cycle = ++E->cycle_serial;
+    E->ev_pool_next = 0;
+    const int kk = c.use_governor ? select_k(prof, accept, c.k_min, c.k_max, k_slo, est()) : c.fixed_k;
+    const int k = std::max(1, std::min({kk, rem, E->o.kmax}));
+    const int T = k + 1;
+    const int est_new = c.use_governor ? est()(k) : -1;
+    const double est_raw = c.estimator == 1 ? elb_raw(k) : 0.0;
+    uint64_t cyc_bytes = 0;
+    std::vector<CopyBatch> batches;
+    // ---------------- draft + planner
+    CUDA_OK(cudaEventRecord(E->ev_c0, E->sc));
+    CUDA_OK(cudaMemsetAsync(E->dst, 0, 4, E->sc));  // row = 0
+    CAPI_OK(mspq_cache_begin_cycle(E->cache, k, E->sc));
+    CUDA_OK(cudaEventRecord(E->ev_g0[0], E->sc));
+    CUDA_OK(cudaGraphLaunch(E->gexec, E->sc));
+    CUDA_OK(cudaEventRecord(E->ev_g1[0], E->sc));
+    if (E->hcap_d) CUDA_OK(cudaMemcpyAsync(E->hcap_d, E->hcap_dstage, (size_t)(L + 1) * d * 4, cudaMemcpyDeviceToDevice, E->sc));
+    if (E->hmid_d) CUDA_OK(cudaMemcpyAsync(E->hmid_d, E->hmid_dstage, (size_t)L * d * 4, cudaMemcpyDeviceToDevice, E->sc));
+    launches += E->graph_nodes;
+    for (int i = 0; i < k; ++i) {
+      CAPI_OK(mspq_cache_plan_row(E->cache, i, E->sc));
+      CUDA_OK(cudaEventRecord(E->ev_row[i], E->sc));
+      ++launches;
+      if (i + 1 < k) {
+        CUDA_OK(cudaEventRecord(E->ev_g0[i + 1], E->sc));
+        CUDA_OK(cudaGraphLaunch(E->gexec, E->sc));
+        CUDA_OK(cudaEventRecord(E->ev_g1[i + 1], E->sc));
+        if (E->hcap_d)
+          CUDA_OK(cudaMemcpyAsync(E->hcap_d + (size_t)(i + 1) * (L + 1) * d, E->hcap_dstage, (size_t)(L + 1) * d * 4,
+                                  cudaMemcpyDeviceToDevice, E->sc));
+        if (E->hmid_d)
+          CUDA_OK(cudaMemcpyAsync(E->hmid_d + (size_t)(i + 1) * L * d, E->hmid_dstage, (size_t)L * d * 4,
+                                  cudaMemcpyDeviceToDevice, E->sc));
+        launches += E->graph_nodes;
+      }
+      spin_wait(E->ev_row[i]);
+      CopyBatch b;
+      issue_copies(E, cycle, b, cyc_bytes, true);
+      if (b.count) batches.push_back(b);
+    }
+    CUDA_OK(cudaEventRecord(E->ev_dend, E->sc));
+    // ---------------- verify (layer-major)
+    for (int s = 0; s < T; ++s) E->hpin[s] = head_pos + s;
+    CUDA_OK(cudaMemcpyAsync(E->win_pos(), E->hpin, T * 4, cudaMemcpyHostToDevice, E->sc));
+    CAPI_OK(mspq_embed(E->embed, E->pos, E->win_tok(), E->win_pos(), T, d, E->h, E->sc));
+    double stall = 0.0;
+    int demand_total = 0;
+    stall_ev.clear();
+    verify_layers(T, cycle, false, batches, cyc_bytes);
     if (!E->deferred.empty()) fail(MSPQ_ERR_OVERFLOW, "deferred prefetch left at the end of the verify pass");
     const int pl = (L - 1) & 1;
     launches += 6;  // embed, final norm, lm head, argmax, accept, begin_cycle
@@ -1027,6 +1235,13 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
       CUDA_OK(cudaMemcpy(hd.data(), E->hcap_d, hd.size() * 4, cudaMemcpyDeviceToHost));
       E->hcap_v_hist.push_back(std::move(hv));
       E->hcap_d_hist.push_back(std::move(hd));
+      if (E->hmid_v) {
+        std::vector<float> mv((size_t)L * T * d), md((size_t)k * L * d);
+        CUDA_OK(cudaMemcpy(mv.data(), E->hmid_v, mv.size() * 4, cudaMemcpyDeviceToHost));
+        CUDA_OK(cudaMemcpy(md.data(), E->hmid_d, md.size() * 4, cudaMemcpyDeviceToHost));
+        E->hmid_v_hist.push_back(std::move(mv));
+        E->hmid_d_hist.push_back(std::move(md));
+      }
     }
     const int fetched = E->view.host_stat[S_FETCHED], demand = E->view.host_stat[S_DEMAND];
     const int n_log = E->view.host_stat[S_NLOG];
@@ -1036,6 +1251,7 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
                                          : elapsed_s(E->ev_k0[l], E->ev_gemm[l]);
       k3_time += t;
       k3_bytes += (double)layer_groups[l] * E->S16;
+      k3_groups += layer_groups[l];
     }
     for (int i = 0; i < k; ++i) draft_time += elapsed_s(E->ev_g0[i], E->ev_g1[i]);
     draft_steps += k;
@@ -1257,6 +1473,8 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
   }
   rep["expert_codec"] = E->codec ? "xc" : "none";
   rep["wall_s"] = wall;
+  rep["decode_wall_s"] = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall_dec0).count();
+  if (!prefill.empty()) rep["prefill"] = prefill;
   rep["profile"] = c.profile.to_json();
   rep["policy"] = policy_name(c.policy);
   // kernel evidence: K3 (bf16 grouped verify FFN, tcgen05) per-launch device time (CUDA events
@@ -1314,6 +1532,9 @@ void destroy(mspq_engine* E) {
   for (float* p : {E->hcap_v, E->hcap_dstage, E->hcap_d})
     if (p) cudaFree(p);
   if (E->sched_cap) cudaFree(E->sched_cap);
+  for (void* p : {(void*)E->wattn, (void*)E->gamma_a, (void*)E->kcache, (void*)E->vcache, (void*)E->qkv, (void*)E->oproj,
+                  (void*)E->ao, (void*)E->dsched, E->dws, (void*)E->hmid_v, (void*)E->hmid_dstage, (void*)E->hmid_d})
+    if (p) cudaFree(p);
   for (size_t r = 0; r < E->peer_ipc.size(); ++r)
     if (E->peer_ipc[r] && E->peer_home[r]) cudaIpcCloseMemHandle(E->peer_home[r]);
   if (E->home) cudaFree(E->home);
@@ -1399,6 +1620,15 @@ int mspq_engine_create(const mspq_model_desc* md, const mspq_engine_opts* op, ms
       E->S4 = mspq_int4_blob_bytes(m.d, m.f);
       E->Tmax = op->kmax + 1;
       E->n_payload = m.unique_experts > 0 ? std::min(m.unique_experts, m.L * m.E) : m.L * m.E;
+      if (m.H > 0) {
+        if (m.Hkv < 1 || m.H % m.Hkv || m.H / m.Hkv > 8 || m.Dh % 64 || (m.H * m.Dh) % 128 ||
+            ((m.H + 2 * m.Hkv) * m.Dh) % 128)
+          fail(MSPQ_ERR_SHAPE_VIOLATION, "attention: need Hkv | H, H/Hkv <= 8, Dh % 64, H*Dh and (H+2Hkv)*Dh % 128");
+        E->attn = true;
+        E->Nq = m.H * m.Dh;
+        E->Nkv = m.Hkv * m.Dh;
+        E->Nqkv = E->Nq + 2 * E->Nkv;
+      }
       make_weights(E);
       alloc_host_store(E);
       make_experts(E);
@@ -1518,6 +1748,29 @@ int mspq_engine_read(mspq_engine* E, const char* name, void* dst, long long byte
       }
       src = hb;
       avail = E->S16;
+      from_host = true;
+    } else if (n.rfind("kcache:", 0) == 0 || n.rfind("vcache:", 0) == 0) {
+      const int l = atoi(n.c_str() + 7);
+      if (!E->attn || l < 0 || l >= m.L) fail(MSPQ_ERR_INVALID_CONFIG, n);
+      src = (n[0] == 'k' ? E->kcache : E->vcache) + (size_t)l * E->kv_layer();
+      avail = E->kv_layer() * 2;
+    } else if (n.rfind("wqkv:", 0) == 0 || n.rfind("wo:", 0) == 0) {
+      const int l = atoi(n.c_str() + (n[1] == 'q' ? 5 : 3));
+      if (!E->attn || l < 0 || l >= m.L) fail(MSPQ_ERR_INVALID_CONFIG, n);
+      const size_t nq = (size_t)E->Nqkv * m.d * 2;
+      src = E->wattn + (size_t)l * E->wattn_layer + (n[1] == 'q' ? 0 : nq);
+      avail = n[1] == 'q' ? nq : (size_t)m.d * E->Nq * 2;
+    } else if (n.rfind("gamma_attn:", 0) == 0) {
+      const int l = atoi(n.c_str() + 11);
+      if (!E->attn || l < 0 || l >= m.L) fail(MSPQ_ERR_INVALID_CONFIG, n);
+      src = E->gamma_a + (size_t)l * m.d;
+      avail = (size_t)m.d * 2;
+    } else if (n.rfind("hmid_v:", 0) == 0 || n.rfind("hmid_d:", 0) == 0) {
+      const auto& hist = n[5] == 'v' ? E->hmid_v_hist : E->hmid_d_hist;
+      const size_t ci = (size_t)atoi(n.c_str() + 7);
+      if (ci >= hist.size()) fail(MSPQ_ERR_RANGE_OUT_OF_BOUNDS, "no residual capture for " + n + " (trace_level 3)");
+      src = hist[ci].data();
+      avail = hist[ci].size() * 4;
       from_host = true;
     } else if (n.rfind("hcap_v:", 0) == 0 || n.rfind("hcap_d:", 0) == 0) {
       const auto& hist = n[5] == 'v' ? E->hcap_v_hist : E->hcap_d_hist;

@@ -26,10 +26,7 @@ def _engine(name="tiny", kmax=8, **kw):
 
 
 def _oracle_desc(cfg):
-    return om.ModelDesc(L=cfg.L, E=cfg.E, K=cfg.K, d=cfg.d, f=cfg.f, V=cfg.V, P=cfg.P, seed=cfg.seed,
-                        embed_scale=cfg.embed_scale, pos_scale=cfg.pos_scale,
-                        router_scale=cfg.router_scale, moe_scale=cfg.moe_scale,
-                        lm_scale=cfg.lm_scale, eps=cfg.eps)
+    return om.ModelDesc(**cfg.oracle_kwargs())
 
 
 def _check_traces(rep, cyc_oracle):
@@ -53,6 +50,11 @@ def _control_plane_log(rep, cfg_json, L, E):
     c = cp.sim_config(cfg_json)
     cache = cp.Cache(c["capacity_mode"], c["cache_capacity"])
     out = []
+    for ch in rep.get("prefill", {}).get("chunks", []):  # prefill windows first (k = 0)
+        log = []
+        cp.live_cycle(cache, cp.ELB.build([], []), ch["target"], c, log)
+        want = [(k, l, e, int(h), -1 if v is None else v[0], -1 if v is None else v[1]) for (k, tag, l, e, h, v) in log]
+        assert [(KINDS[ev[0]], ev[2], ev[3], ev[4], ev[5], ev[6]) for ev in ch["log"]] == want
     for cyc in rep["cycles"]:
         elb = cp.ELB.build(cyc["elb"], cyc["elb_gates"])
         log = []
@@ -71,7 +73,7 @@ def test_generate_tiny_matches_oracle_end_to_end(cuda):
     assert len(rep["tokens"]) == 40
     model = om.Model(_oracle_desc(cfg))
     ks = [c["k"] for c in rep["cycles"]]
-    oc = om.speculative_decode(model, prompt[-1], len(prompt) - 1, ks, 40)
+    oc = om.speculative_decode(model, prompt[-1], len(prompt) - 1, ks, 40, prompt=prompt)
     _check_traces(rep, oc)
     want = _control_plane_log(rep, conf, cfg.L, cfg.E)
     for c, w in zip(rep["cycles"], want):
@@ -113,7 +115,7 @@ def test_generate_governor_and_rerun_determinism(cuda):
         assert 1 <= c["k"] <= 8
     # token stream equals plain greedy target decoding (the oracle's, k=1 cycles commit one draft)
     model = om.Model(_oracle_desc(cfg))
-    oc = om.speculative_decode(model, 42, 0, [c["k"] for c in r1["cycles"]], 32)
+    oc = om.speculative_decode(model, 42, 0, [c["k"] for c in r1["cycles"]], 32, prompt=[42])
     assert r1["tokens"] == [t for o in oc for t in o["committed"]]
     eng.close()
 
@@ -203,7 +205,7 @@ def test_generate_full_width_shapes_match_oracle(cuda, name, cap, k):
     prompt = [11, 200, 3001]
     rep = eng.generate(prompt, 10)
     model = om.Model(_oracle_desc(cfg))
-    oc = om.speculative_decode(model, prompt[-1], len(prompt) - 1, [c["k"] for c in rep["cycles"]], 10)
+    oc = om.speculative_decode(model, prompt[-1], len(prompt) - 1, [c["k"] for c in rep["cycles"]], 10, prompt=prompt)
     _check_traces(rep, oc)
     want = _control_plane_log(rep, conf, cfg.L, cfg.E)
     for c, w in zip(rep["cycles"], want):
@@ -336,6 +338,8 @@ def test_live_collect_plans_and_sync_fetch(cuda):
     rep = eng.generate([9, 8, 7], 30)
     c = cp.sim_config(conf)
     cache = cp.Cache(c["capacity_mode"], c["cache_capacity"])
+    for ch in rep["prefill"]["chunks"]:
+        cp.live_cycle(cache, cp.ELB.build([], []), ch["target"], c)
     head = 2
     for cyc in rep["cycles"]:
         out = cp.live_cycle(cache, cp.ELB.build(cyc["elb"], cyc["elb_gates"]), cyc["target"], c)

@@ -28,17 +28,15 @@ import warnings
 import numpy as np
 import pytest
 
+from helpers import check_control_plane
 from oracle import control_plane as cp
 from oracle import model as om
 
 pytestmark = pytest.mark.gpu
-KINDS = {0: "demand", 1: "plan2", 2: "plan3", 3: "jit", 4: "refill"}
 
 
 def _desc(cfg):
-    return om.ModelDesc(L=cfg.L, E=cfg.E, K=cfg.K, d=cfg.d, f=cfg.f, V=cfg.V, P=cfg.P, seed=cfg.seed,
-                        embed_scale=cfg.embed_scale, pos_scale=cfg.pos_scale, router_scale=cfg.router_scale,
-                        moe_scale=cfg.moe_scale, lm_scale=cfg.lm_scale, eps=cfg.eps)
+    return om.ModelDesc(**cfg.oracle_kwargs())
 
 
 def _gap(logits):
@@ -46,19 +44,41 @@ def _gap(logits):
     return float(top[0] - top[1]) / (float(np.abs(logits).max()) + 1e-30)
 
 
-def _teacher_forced(eng, rep, cfg, model):
-    """Check 1; returns (worst relative layer error, {decision: relative margin}) where a decision
-    is ("target", cycle, slot, layer) / ("elb", cycle, row, layer) for routing (top-K boundary gap)
-    and ("target_argmax", cycle, slot) / ("draft_token", cycle, row) for the LM head (top-2 gap)."""
+def _teacher_forced(eng, rep, cfg, model, prompt):
+    """Check 1; returns (worst relative layer error, {decision: relative margin}, captures) where a
+    decision is ("target", cycle, slot, layer) / ("elb", cycle, row, layer) for routing (adjacent
+    gaps in the top K+1) and ("target_argmax", cycle, slot) / ("draft_token", cycle, row) for the
+    LM head (top-2 gap).  With attention the context of every window is the device's own KV cache
+    (rows before the window are committed, hence final at the end of the run) and each layer's
+    attention block is checked on its own (residual after attention, hmid captures)."""
     L, d = cfg.L, cfg.d
     worst, margins, caps = 0.0, {}, {}
+    ctx = None
+    if cfg.H > 0:
+        rows = cfg.P * cfg.Hkv * cfg.Dh
+        kc = [om.bf16_to_f32(np.frombuffer(eng.read("kcache:%d" % l, rows * 2), dtype=np.uint16)).reshape(
+            cfg.P, cfg.Hkv, cfg.Dh) for l in range(L)]
+        vc = [om.bf16_to_f32(np.frombuffer(eng.read("vcache:%d" % l, rows * 2), dtype=np.uint16)).reshape(
+            cfg.P, cfg.Hkv, cfg.Dh) for l in range(L)]
+        ctx = lambda l, j: (kc[l][j], vc[l][j])  # noqa: E731
+    head = len(prompt) - 1
     for ci, c in enumerate(rep["cycles"]):
         k = c["k"]
         T = k + 1
         hv = np.frombuffer(eng.read("hcap_v:%d" % ci, (L + 1) * T * d * 4), dtype=np.float32).reshape(L + 1, T, d)
+        hd = np.frombuffer(eng.read("hcap_d:%d" % ci, k * (L + 1) * d * 4), dtype=np.float32).reshape(k, L + 1, d)
         caps[("v", ci)] = hv
+        caps[("d", ci)] = hd
+        hmv = hmd = None
+        if cfg.H > 0:
+            hmv = np.frombuffer(eng.read("hmid_v:%d" % ci, L * T * d * 4), dtype=np.float32).reshape(L, T, d)
+            hmd = np.frombuffer(eng.read("hmid_d:%d" % ci, k * L * d * 4), dtype=np.float32).reshape(k, L, d)
+        # the residual the router of layer l reads: after the attention block (= entering l without)
+        caps[("vm", ci)] = hmv if hmv is not None else hv[:L]
+        caps[("dm", ci)] = hmd if hmd is not None else hd[:, :L]
         ids = [[c["target"][s][l] for s in range(T)] for l in range(L)]
-        w, mg = om.check_layers(model, hv, ids, draft=False)
+        w, mg = om.check_layers(model, hv, ids, draft=False, h_mids=hmv, positions=list(range(head, head + T)),
+                                ctx=ctx)
         worst = max(worst, w)
         for l in range(L):
             for s in range(T):
@@ -68,18 +88,20 @@ def _teacher_forced(eng, rep, cfg, model):
         assert am.tolist() == c["target_argmax"], ("verify argmax", ci)
         for s in range(T):
             margins[("target_argmax", ci, s)] = _gap(lg[s])
-        hd = np.frombuffer(eng.read("hcap_d:%d" % ci, k * (L + 1) * d * 4), dtype=np.float32).reshape(k, L + 1, d)
-        caps[("d", ci)] = hd
+        # the k draft rows form one causal window (each row attends to the rows before it)
+        ids_d = [[c["elb"][r][l] for r in range(k)] for l in range(L)]
+        w, mg = om.check_layers(model, np.ascontiguousarray(hd.transpose(1, 0, 2)), ids_d, draft=True,
+                                h_mids=None if hmd is None else np.ascontiguousarray(hmd.transpose(1, 0, 2)),
+                                positions=list(range(head, head + k)), ctx=ctx)
+        worst = max(worst, w)
         for r in range(k):
-            ids_r = [[c["elb"][r][l]] for l in range(L)]
-            w, mg = om.check_layers(model, hd[r][:, None, :], ids_r, draft=True)
-            worst = max(worst, w)
             for l in range(L):
-                margins[("elb", ci, r, l)] = mg[l][0]
+                margins[("elb", ci, r, l)] = mg[l][r]
             xf = model.rmsnorm(np.ascontiguousarray(hd[r][L]), model.gamma(-1))
             lg, am = model.lm_head(xf[None, :])
             assert int(am[0]) == c["draft_tokens"][r], ("draft token", ci, r)
             margins[("draft_token", ci, r)] = _gap(lg[0])
+        head += c["accepted"] + 1
     return worst, margins, caps
 
 
@@ -91,31 +113,36 @@ def _explain(div, rep, oc, model, caps, prompt):
     o = oc[ci]
     head = prompt[-1] if ci == 0 else oc[ci - 1]["committed"][-1]
     pos0 = len(prompt) - 1 + sum(x["accepted"] + 1 for x in oc[:ci])
+    # re-run the oracle on the window prefix up to the decision (its KV rows before pos0 are the
+    # committed ones; the window's own rows are recomputed by this pass)
     if kind in ("target", "target_argmax"):
         s = div[2]
-        window = [head] + o["draft"]
-        trace = []
-        om.forward_batch(model, [window[s]], [pos0 + s], draft=False, h_trace=trace)
-        h_dev = caps[("v", ci)][:, s, :]
+        window = ([head] + o["draft"])[:s + 1]
+        trace, mtrace = [], []
+        om.forward_batch(model, window, list(range(pos0, pos0 + s + 1)), draft=False, h_trace=trace,
+                         hmid_trace=mtrace)
+        trace, mtrace = [t[s] for t in trace], [t[s] for t in mtrace]
+        h_dev, hm_dev = caps[("v", ci)][:, s, :], caps[("vm", ci)][:, s, :]
     elif kind in ("elb", "draft_token"):
         r = div[2]
-        tok = head if r == 0 else o["draft"][r - 1]
-        trace = []
-        om.forward_batch(model, [tok], [pos0 + r], draft=True, h_trace=trace)
-        h_dev = caps[("d", ci)][r]
+        toks = ([head] + o["draft"])[:r + 1]
+        trace, mtrace = [], []
+        om.forward_batch(model, toks, list(range(pos0, pos0 + r + 1)), draft=True, h_trace=trace, hmid_trace=mtrace)
+        trace, mtrace = [t[r] for t in trace], [t[r] for t in mtrace]
+        h_dev, hm_dev = caps[("d", ci)][r], caps[("dm", ci)][r]
     else:
         raise AssertionError(f"divergence {div} is not a routing or argmax decision")
     if kind in ("target", "elb"):
         l = div[3]
-        h_o = trace[l][0]
-        hd = np.ascontiguousarray(h_dev[l])
+        h_o = mtrace[l]  # the router's input: the residual after the attention block
+        hd = np.ascontiguousarray(hm_dev[l])
         lo = model.route(model.rmsnorm(np.ascontiguousarray(h_o), model.gamma(l)), l)[2]
         ld = model.route(model.rmsnorm(hd, model.gamma(l)), l)[2]
         srt = np.sort(ld)[::-1]
         # the trace lists the top-K in logit order: an adjacent swap anywhere in the top K+1 counts
         gap = float(min(srt[j] - srt[j + 1] for j in range(min(K, len(srt) - 1))))
     else:
-        h_o = trace[L][0]
+        h_o = trace[L]
         hd = np.ascontiguousarray(h_dev[L])
         lo = model.lm_head(model.rmsnorm(np.ascontiguousarray(h_o), model.gamma(-1))[None, :])[0][0]
         ld = model.lm_head(model.rmsnorm(hd, model.gamma(-1))[None, :])[0][0]
@@ -165,26 +192,20 @@ def _run(name, cap, ntok, conf_extra=None, **shape_kw):
     rep = eng.generate(prompt, ntok)
     model = om.Model(_desc(cfg))
     try:
-        worst, margins, caps = _teacher_forced(eng, rep, cfg, model)
+        worst, margins, caps = _teacher_forced(eng, rep, cfg, model, prompt)
     finally:
         eng.close()
     # 2. free-running oracle decode with the device's k sequence
-    oc = om.speculative_decode(model, prompt[-1], len(prompt) - 1, [c["k"] for c in rep["cycles"]], ntok)
+    oc = om.speculative_decode(model, prompt[-1], len(prompt) - 1, [c["k"] for c in rep["cycles"]], ntok,
+                               prompt=prompt)
     div = _first_divergence(rep, oc, cfg.L)
     margin = min(margins.values())
     if div is not None:
         msg = _explain(div, rep, oc, model, caps, prompt)
         warnings.warn(f"{name}: free-running oracle diverged at a certified rounding near-tie -- {msg}; "
                       f"teacher-forced layers all exact (worst layer err {worst:.2e})")
-    # 3. control plane: hit/miss log and governor k sequence
-    c = cp.sim_config(conf)
-    cache = cp.Cache(c["capacity_mode"], c["cache_capacity"])
-    for cyc in rep["cycles"]:
-        log = []
-        cp.live_cycle(cache, cp.ELB.build(cyc["elb"], cyc["elb_gates"]), cyc["target"], c, log)
-        want = [(k, l, e, int(h), -1 if v is None else v[0], -1 if v is None else v[1]) for (k, tag, l, e, h, v) in log]
-        got = [(KINDS[ev[0]], ev[2], ev[3], ev[4], ev[5], ev[6]) for ev in cyc["log"]]
-        assert got == want, ("hit/miss log", cyc["cycle"])
+    # 3. control plane: hit/miss log (prefill windows, then decode cycles) and governor k sequence
+    check_control_plane(rep, conf)
     est = conf.get("estimator", "linear")
     gov = cp.live_governor_ks(rep, conf, cfg.L, cfg.E, cfg.K, est, kmax=16)
     assert [x["k"] for x in gov] == [cyc["k"] for cyc in rep["cycles"]]

@@ -152,12 +152,14 @@ def test_model_oracle_properties():
 def test_oracle_speculative_decode_is_lossless():
     """Greedy speculative decoding commits exactly the target's greedy sequence."""
     m = om.Model(om.ModelDesc(**om.CONFIGS["tiny"]))
+    prompt = [1, 2, 3, 4, 9]
+    om.prefill(m, prompt)  # shared-KV attention: the prompt's rows 0..3
     greedy, tok = [], 9
     for p in range(4, 4 + 24):
         tok, _, _ = m.forward(tok, p, draft=False)
         greedy.append(tok)
     for ks in ([1], [3], [6, 2, 4]):
-        cyc = om.speculative_decode(m, 9, 4, ks, 24)
+        cyc = om.speculative_decode(m, 9, 4, ks, 24, prompt=prompt)
         assert [t for c in cyc for t in c["committed"]] == greedy
 
 
@@ -201,8 +203,8 @@ def test_fast_oracle_decode_equals_numpy_oracle():
         yf = fast.ffn_batch(xn, 2, 5, draft)
         ys = np.stack([slow.ffn(xn[i], 2, 5, draft)[0] for i in range(3)])
         assert np.abs(yf - ys).max() <= 1e-5 * np.abs(ys).max()
-    a = om.speculative_decode(slow, 7, 3, [3, 2, 4], 12)
-    b = om.speculative_decode(fast, 7, 3, [3, 2, 4], 12)
+    a = om.speculative_decode(slow, 7, 3, [3, 2, 4], 12, prompt=[5, 6, 8, 7])
+    b = om.speculative_decode(fast, 7, 3, [3, 2, 4], 12, prompt=[5, 6, 8, 7])
     for x, y in zip(a, b):
         assert x["committed"] == y["committed"] and x["draft"] == y["draft"]
         assert [[r[0].tolist() for r in s] for s in x["target"]] == [[r[0].tolist() for r in s] for s in y["target"]]
