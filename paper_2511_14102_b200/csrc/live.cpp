@@ -1117,6 +1117,12 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
     prefill["h2d_bytes"] = pf_bytes;
     prefill["time_s"] = std::chrono::duration<double>(std::chrono::steady_clock::now() - pw0).count();
     prefill["chunks"] = chunks;
+    if (E->peer_G > 0) {  // the decode's peer-tier counters start after the prefill
+      prefill["peer_fetches"] = E->n_peer;
+      prefill["home_local_fetches"] = E->n_home_local;
+      E->gen_peer_bytes = E->gen_home_local_bytes = 0;
+      E->n_peer = E->n_home_local = 0;
+    }
     // the decode state (head token / position) the prefill windows overwrote
     E->hpin[0] = 0;
     E->hpin[1] = prompt[n_prompt - 1];
