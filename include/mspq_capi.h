@@ -116,6 +116,13 @@ int mspq_gate_topk(float* h, const float* y, const int32_t* entry_of, const floa
                    float* logits, int32_t* elb_ids, float* elb_gates, const int32_t* elb_row,
                    int32_t* sched_block, int layer, int L, int T, int d, int E, int K, float eps,
                    void* stream);
+/* K1 that also writes xn as the SW128 B image of a dense tcgen05 GEMM (mspq_dense_bf16_tc with
+ * x = NULL reads it from its workspace): bimg = that workspace, T <= 32 */
+int mspq_gate_topk_img(float* h, const float* y, const int32_t* entry_of, const float* prev_wts,
+                       int y_splits, long long y_split_stride, const void* gamma, const void* router, void* xn,
+                       int32_t* ids, float* wts, float* logits, int32_t* elb_ids, float* elb_gates,
+                       const int32_t* elb_row, int32_t* sched_block, int layer, int L, int T, int d, int E, int K,
+                       float eps, void* bimg, void* stream);
 /* schedule arrays: n_groups[1], group_expert[G], group_buf[G], group_off[G+1], entry_tok[T*K],
  * entry_of[T*K]; gbuf[E] (nullable) gives group_buf per expert (else group_buf = expert id) */
 int mspq_build_schedule(const int32_t* ids, int T, int K, int E, const int32_t* gbuf, int32_t* n_groups,
@@ -162,7 +169,8 @@ int mspq_moe_int4_tc(const int32_t* n_groups, const int32_t* group_expert, const
 /* Dense bf16 projection on tcgen05 (K3's grouped GEMM with one group of T tokens):
  * out[split][T][rows] fp32 partial planes (out_split_stride floats apart) = x[T][kdim] . W^T,
  * W tile-major SW128 (mspq_tile_bf16).  dsched: device copy of the packed schedule
- * mspq_dense_sched_fill writes (4 + T ints); ws: mspq_dense_ws_bytes(kdim, T) bytes. */
+ * mspq_dense_sched_fill writes (4 + T ints); ws: mspq_dense_ws_bytes(kdim, T) bytes.  x = NULL:
+ * ws already holds the B image (written by mspq_gate_topk_img or mspq_attention). */
 long long mspq_dense_ws_bytes(int kdim, int T);
 int mspq_dense_sched_fill(int32_t* host_packed, int T);
 int mspq_dense_bf16_tc(const int32_t* dsched, const void* x, const void* w_tiled, int rows, int kdim, int T,
@@ -170,10 +178,11 @@ int mspq_dense_bf16_tc(const int32_t* dsched, const void* x, const void* w_tiled
 /* Shared-KV decode attention over a window of T tokens at positions *pos0 .. *pos0+T-1 (device
  * pointer): qkv = the QKV projection's split planes [splits][T][(H+2Hkv) Dh]; the window's K/V
  * rows are written into kc/vc ([P][Hkv][Dh] bf16, this layer) and every token attends causally
- * to the cache rows before the window plus the window tokens up to itself; out [T][H Dh] bf16.
+ * to the cache rows before the window plus the window tokens up to itself; out [T][H Dh] bf16
+ * (nullable) and/or oimg = the O projection's B image (a dense GEMM workspace, x = NULL).
  * Draft and target share the cache; rollback = the next window overwrites rows >= its pos0. */
 int mspq_attention(const float* qkv, int splits, long long split_stride, int T, int H, int Hkv, int Dh, int P,
-                   const int32_t* pos0, void* kc, void* vc, void* out, void* stream);
+                   const int32_t* pos0, void* kc, void* vc, void* out, void* oimg, void* stream);
 /* row-major quantised INT4 (q[rows][cols/8] u32, standard nibble order; s[rows][cols/128] bf16)
  * -> tile-major [rows/128][cols/64][128][8] u32 + [rows/128][cols/128][128] bf16 */
 int mspq_tile_int4(const void* q, const void* s, int rows, int cols, void* tq, void* ts, void* stream);

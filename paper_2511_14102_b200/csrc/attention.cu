@@ -28,6 +28,10 @@ MSPQ_D float warp_max(float v) {
   return v;
 }
 
+// lane l owns head dims [VEC*l, VEC*l + VEC) (Dh = 32 VEC): q in registers, one vector load per
+// key row; keys are split over the 8 warps both for the scores and for the value sum, whose
+// per-warp partials are added in warp order (deterministic)
+template <int VEC>
 __global__ void __launch_bounds__(AT_THREADS) k_attn_window(AttnArgs a) {
   pdl_enter();  // launched with launch_pdl (kernels.h)
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -35,19 +39,13 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_window(AttnArgs a) {
   const int G = a.H / a.Hkv, Dh = a.Dh;
   const int Nq = a.H * Dh, Nkv = a.Hkv * Dh, Nqkv = Nq + 2 * Nkv;
   const int p0 = *a.pos0, pt = p0 + t, n = pt + 1;
-  float* qs = reinterpret_cast<float*>(smem_raw);        // [G][Dh] fp32
-  uint16_t* wk = reinterpret_cast<uint16_t*>(qs + G * Dh);  // [T][Dh] in-window keys, bf16
-  uint16_t* wv = wk + a.T * Dh;                              // [T][Dh] in-window values
-  float* sc = reinterpret_cast<float*>(wv + a.T * Dh);      // [G][P] scores -> probabilities
+  uint16_t* wk = reinterpret_cast<uint16_t*>(smem_raw);     // [T][Dh] in-window keys, bf16
+  uint16_t* wv = wk + a.T * Dh;                             // [T][Dh] in-window values
+  float* sc = reinterpret_cast<float*>(wv + a.T * Dh);     // [G][P] scores -> probabilities
+  float* red = sc + (size_t)G * a.P;                        // [AT_WARPS][G][Dh] value partials
   __shared__ float hsum[AT_MAXG];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // (1) q of the G heads (their columns are contiguous), in-window k/v of tokens 0..t
-  for (int i = tid; i < G * Dh; i += AT_THREADS) {
-    const float* src = a.qkv + (int64_t)t * Nqkv + g * G * Dh + i;
-    float v = 0.0f;
-    for (int s = 0; s < a.splits; ++s) v = __fadd_rn(v, src[s * a.split_stride]);
-    qs[i] = v;
-  }
+  // (1) in-window k/v of tokens 0..t (split planes summed in order, rounded to bf16 like the cache)
   for (int i = tid; i < (t + 1) * Dh; i += AT_THREADS) {
     const int tt = i / Dh, dd = i - tt * Dh;
     const float* src = a.qkv + (int64_t)tt * Nqkv + Nq + g * Dh + dd;
@@ -59,28 +57,50 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_window(AttnArgs a) {
     wk[i] = f2bf(kv);
     wv[i] = f2bf(vv);
   }
+  // q of the G heads, lane slice, fp32 in registers
+  float q[AT_MAXG][VEC];
+#pragma unroll
+  for (int i = 0; i < AT_MAXG; ++i)
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      float x = 0.0f;
+      if (i < G) {
+        const float* src = a.qkv + (int64_t)t * Nqkv + (g * G + i) * Dh + lane * VEC + v;
+        for (int s = 0; s < a.splits; ++s) x = __fadd_rn(x, src[s * a.split_stride]);
+      }
+      q[i][v] = x;
+    }
   __syncthreads();
   for (int dd = tid; dd < Dh; dd += AT_THREADS) {  // this token's row of the shared cache
     a.kc[((int64_t)pt * a.Hkv + g) * Dh + dd] = wk[t * Dh + dd];
     a.vc[((int64_t)pt * a.Hkv + g) * Dh + dd] = wv[t * Dh + dd];
   }
-  // (2) scores, one warp per key position
-  for (int j = warp; j < n; j += AT_WARPS) {
-    const uint16_t* kr = j < p0 ? a.kc + ((int64_t)j * a.Hkv + g) * Dh : wk + (j - p0) * Dh;
-    float part[AT_MAXG];
-#pragma unroll
-    for (int i = 0; i < AT_MAXG; ++i) part[i] = 0.0f;
-    for (int dd = lane; dd < Dh; dd += 32) {
-      const float kk = bf2f(kr[dd]);
-#pragma unroll
-      for (int i = 0; i < AT_MAXG; ++i)
-        if (i < G) part[i] = fmaf(qs[i * Dh + dd], kk, part[i]);
+  auto row_vec = [&](const uint16_t* cache, const uint16_t* win, int j, float* o) {
+    const uint16_t* r = (j < p0 ? cache + ((int64_t)j * a.Hkv + g) * Dh : win + (j - p0) * Dh) + lane * VEC;
+    if (VEC == 4) {
+      const uint2 u = *reinterpret_cast<const uint2*>(r);
+      o[0] = __uint_as_float(u.x << 16);
+      o[1] = __uint_as_float(u.x & 0xffff0000u);
+      o[2] = __uint_as_float(u.y << 16);
+      o[3] = __uint_as_float(u.y & 0xffff0000u);
+    } else {
+      const uint32_t u = *reinterpret_cast<const uint32_t*>(r);
+      o[0] = __uint_as_float(u << 16);
+      o[1] = __uint_as_float(u & 0xffff0000u);
     }
+  };
+  // (2) scores: warps stride over the key positions
+  for (int j = warp; j < n; j += AT_WARPS) {
+    float kk[VEC];
+    row_vec(a.kc, wk, j, kk);
 #pragma unroll
     for (int i = 0; i < AT_MAXG; ++i)
       if (i < G) {
-        const float z = warp_butterfly_sum(part[i]);
-        if (lane == 0) sc[i * a.P + j] = __fmul_rn(z, a.scale);
+        float part = 0.0f;
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) part = fmaf(q[i][v], kk[v], part);
+        part = warp_butterfly_sum(part);
+        if (lane == 0) sc[i * a.P + j] = __fmul_rn(part, a.scale);
       }
   }
   __syncthreads();
@@ -100,16 +120,38 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_window(AttnArgs a) {
     if (lane == 0) hsum[warp] = s;
   }
   __syncthreads();
-  // (4) o = sum_j p_j v_j / sum_j p_j
+  // (4) value sums: warp w takes keys j = w, w + 8, ...; partials added in warp order
+  float acc[AT_MAXG][VEC];
+#pragma unroll
+  for (int i = 0; i < AT_MAXG; ++i)
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) acc[i][v] = 0.0f;
+  for (int j = warp; j < n; j += AT_WARPS) {
+    float vv[VEC];
+    row_vec(a.vc, wv, j, vv);
+#pragma unroll
+    for (int i = 0; i < AT_MAXG; ++i)
+      if (i < G) {
+        const float pj = sc[i * a.P + j];
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) acc[i][v] = fmaf(pj, vv[v], acc[i][v]);
+      }
+  }
+#pragma unroll
+  for (int i = 0; i < AT_MAXG; ++i)
+    if (i < G)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) red[((size_t)warp * G + i) * Dh + lane * VEC + v] = acc[i][v];
+  __syncthreads();
   for (int o = tid; o < G * Dh; o += AT_THREADS) {
-    const int i = o / Dh, dd = o - i * Dh;
-    const float* pr = sc + i * a.P;
-    float acc = 0.0f;
-    for (int j = 0; j < n; ++j) {
-      const uint16_t* vr = j < p0 ? a.vc + ((int64_t)j * a.Hkv + g) * Dh : wv + (j - p0) * Dh;
-      acc = fmaf(pr[j], bf2f(vr[dd]), acc);
-    }
-    a.out[(int64_t)t * Nq + g * G * Dh + o] = f2bf(__fdiv_rn(acc, hsum[i]));
+    const int i = o / Dh;
+    float x = 0.0f;
+#pragma unroll
+    for (int w = 0; w < AT_WARPS; ++w) x = __fadd_rn(x, red[(size_t)w * G * Dh + o]);
+    const uint16_t ob = f2bf(__fdiv_rn(x, hsum[i]));
+    const int col = g * G * Dh + o;
+    if (a.out) a.out[(int64_t)t * Nq + col] = ob;
+    if (a.oimg) *reinterpret_cast<uint16_t*>(a.oimg + (int64_t)(col >> 6) * (a.o_bn * 128) + sw128_off(t, col & 63)) = ob;
   }
 }
 
@@ -117,14 +159,22 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_window(AttnArgs a) {
 
 size_t attn_smem_bytes(int T, int H, int Hkv, int Dh, int P) {
   const int G = H / Hkv;
-  return (size_t)G * Dh * 4 + (size_t)2 * T * Dh * 2 + (size_t)G * P * 4;
+  return (size_t)2 * T * Dh * 2 + (size_t)G * P * 4 + (size_t)AT_WARPS * G * Dh * 4;
 }
 
 cudaError_t launch_attn_window(const AttnArgs& a, cudaStream_t st) {
   const size_t smem = attn_smem_bytes(a.T, a.H, a.Hkv, a.Dh, a.P);
-  cudaError_t e = cudaFuncSetAttribute(k_attn_window, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  return launch_pdl(k_attn_window, dim3(a.T, a.Hkv), dim3(AT_THREADS), smem, st, a);
+  if (a.Dh == 128) {
+    cudaError_t e = cudaFuncSetAttribute(k_attn_window<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    return launch_pdl(k_attn_window<4>, dim3(a.T, a.Hkv), dim3(AT_THREADS), smem, st, a);
+  }
+  if (a.Dh == 64) {
+    cudaError_t e = cudaFuncSetAttribute(k_attn_window<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    return launch_pdl(k_attn_window<2>, dim3(a.T, a.Hkv), dim3(AT_THREADS), smem, st, a);
+  }
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace mspq

@@ -9,6 +9,8 @@
 #include "kernels.h"
 #include "status.h"
 
+static int tc_bn(int T) { return T <= 16 ? 16 : 32; }
+
 using namespace mspq;
 
 namespace mspq {
@@ -67,17 +69,26 @@ int mspq_embed(const void* embed, const void* pos, const int32_t* tokens, const 
   CK(launch_embed((const uint16_t*)embed, (const uint16_t*)pos, tokens, positions, T, d, h, ST(stream)),
      "embed");
 }
+int mspq_gate_topk_img(float* h, const float* y, const int32_t* entry_of, const float* prev_wts,
+                       int y_splits, long long y_split_stride, const void* gamma, const void* router, void* xn,
+                       int32_t* ids, float* wts, float* logits, int32_t* elb_ids, float* elb_gates,
+                       const int32_t* elb_row, int32_t* sched_block, int layer, int L, int T, int d, int E, int K,
+                       float eps, void* bimg, void* stream) {
+  if (d % 256 || K > 64 || E > 1024 || K > E || (bimg && T > 32))
+    return set_error(MSPQ_ERR_SHAPE_MISMATCH, "gate_topk: need d%256==0, K<=min(E,64), E<=1024 (image: T<=32)");
+  RouteArgs a{h, y, entry_of, prev_wts, (const uint16_t*)gamma, (const uint16_t*)router,
+              (uint16_t*)xn, ids, wts, logits, y_splits < 1 ? 1 : y_splits, y_split_stride,
+              elb_ids, elb_gates, elb_row, T == 1 ? sched_block : nullptr, layer, L, d, E, K, eps,
+              (unsigned char*)bimg, tc_bn(T)};
+  CK(launch_route(a, T, ST(stream)), "gate_topk");
+}
 int mspq_gate_topk(float* h, const float* y, const int32_t* entry_of, const float* prev_wts,
                    int y_splits, long long y_split_stride, const void* gamma, const void* router, void* xn, int32_t* ids, float* wts,
                    float* logits, int32_t* elb_ids, float* elb_gates, const int32_t* elb_row,
                    int32_t* sched_block, int layer, int L, int T, int d, int E, int K, float eps,
                    void* stream) {
-  if (d % 256 || K > 64 || E > 1024 || K > E)
-    return set_error(MSPQ_ERR_SHAPE_MISMATCH, "gate_topk: need d%256==0, K<=min(E,64), E<=1024");
-  RouteArgs a{h, y, entry_of, prev_wts, (const uint16_t*)gamma, (const uint16_t*)router,
-              (uint16_t*)xn, ids, wts, logits, y_splits < 1 ? 1 : y_splits, y_split_stride,
-              elb_ids, elb_gates, elb_row, T == 1 ? sched_block : nullptr, layer, L, d, E, K, eps};
-  CK(launch_route(a, T, ST(stream)), "gate_topk");
+  return mspq_gate_topk_img(h, y, entry_of, prev_wts, y_splits, y_split_stride, gamma, router, xn, ids, wts, logits,
+                            elb_ids, elb_gates, elb_row, sched_block, layer, L, T, d, E, K, eps, nullptr, stream);
 }
 int mspq_build_schedule(const int32_t* ids, int T, int K, int E, const int32_t* gbuf, int32_t* n_groups,
                         int32_t* group_expert, int32_t* group_buf, int32_t* group_off,
@@ -108,7 +119,6 @@ int mspq_moe_bf16(const int32_t* n_groups, const int32_t* group_expert, const in
                0, E, d, f};
   CK(launch_expert(a, false, max_groups, max_group_size, ST(stream)), "moe_bf16");
 }
-static int tc_bn(int T) { return T <= 16 ? 16 : 32; }
 long long mspq_moe_bf16_tc_ws_bytes(int d, int f, int T, int K, int max_groups, int max_split1) {
   const long long BN = tc_bn(T), N = (long long)T * K;
   auto al = [](long long b) { return (b + 1023) / 1024 * 1024; };
@@ -185,17 +195,19 @@ int mspq_dense_bf16_tc(const int32_t* dsched, const void* x, const void* w_tiled
   SchedPtrs s{p, nullptr, p + 1, p + 2, p + 4, nullptr, nullptr};
   cudaStream_t st = ST(stream);
   unsigned char* b1 = (unsigned char*)ws;
-  cudaError_t e = launch_gather_b((const uint16_t*)x, kdim, s, 1, kdim, BN, b1, st);
-  if (e != cudaSuccess) return cuda_status(e, "dense gather");
+  if (x) {  // x == NULL: the producer already wrote the B image into ws (K1 / attention epilogue)
+    cudaError_t e = launch_gather_b((const uint16_t*)x, kdim, s, 1, kdim, BN, b1, st);
+    if (e != cudaSuccess) return cuda_status(e, "dense gather");
+  }
   UmmaArgs u{(const unsigned char*)w_tiled, 0, 0, rows, kdim, p, p + 1, p + 2, b1, out, out_split_stride, split};
   CK(launch_umma_grouped(u, 1, BN, st), "dense umma");
 }
 int mspq_attention(const float* qkv, int splits, long long split_stride, int T, int H, int Hkv, int Dh, int P,
-                   const int32_t* pos0, void* kc, void* vc, void* out, void* stream) {
-  if (H < 1 || Hkv < 1 || H % Hkv || H / Hkv > 8 || Dh % 32 || T < 1 || P < T)
-    return set_error(MSPQ_ERR_SHAPE_MISMATCH, "attention: Hkv | H, H/Hkv <= 8, Dh % 32, 1 <= T <= P");
+                   const int32_t* pos0, void* kc, void* vc, void* out, void* oimg, void* stream) {
+  if (H < 1 || Hkv < 1 || H % Hkv || H / Hkv > 8 || (Dh != 64 && Dh != 128) || T < 1 || P < T)
+    return set_error(MSPQ_ERR_SHAPE_MISMATCH, "attention: Hkv | H, H/Hkv <= 8, Dh in {64, 128}, 1 <= T <= P");
   AttnArgs a{qkv, splits, split_stride, T, H, Hkv, Dh, P, pos0, (uint16_t*)kc, (uint16_t*)vc, (uint16_t*)out,
-             1.0f / sqrtf((float)Dh)};
+             1.0f / sqrtf((float)Dh), (unsigned char*)oimg, tc_bn(T)};
   CK(launch_attn_window(a, ST(stream)), "attention");
 }
 int mspq_moe_int4_tc(const int32_t* n_groups, const int32_t* group_expert, const int32_t* group_buf,

@@ -84,6 +84,11 @@ MSPQ_D float det_exp(float x) {
 MSPQ_D float silu_det(float g) { return __fdiv_rn(g, __fadd_rn(1.0f, det_exp(-g))); }
 
 // ------------------------------------------------------------------ warp helpers
+// byte offset of bf16 element (row, col) inside one UMMA K-major SWIZZLE_128B image of 64 columns
+MSPQ_HD int sw128_off(int row, int col) {
+  return (row >> 3) * 1024 + (row & 7) * 128 + ((((col >> 3) ^ (row & 7)) & 7) << 4) + (col & 7) * 2;
+}
+
 MSPQ_D float warp_butterfly_sum(float v) {
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));

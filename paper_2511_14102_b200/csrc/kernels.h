@@ -119,6 +119,8 @@ struct RouteArgs {
   int32_t* sched;            // T == 1: packed draft schedule (nullable), see mspq_gate_topk
   int layer, L, d, E, K;
   float eps;
+  unsigned char* bimg = nullptr;  // also write xn as the SW128 B image of a dense GEMM (nullable)
+  int bimg_bn = 16;               // rows per B image k-block
 };
 
 // Shared-KV decode attention over a window of T tokens (attention.cu)
@@ -130,8 +132,10 @@ struct AttnArgs {
   const int32_t* pos0;     // device: position of window token 0
   uint16_t* kc;            // this layer's K cache [P][Hkv][Dh] bf16
   uint16_t* vc;            // V cache
-  uint16_t* out;           // [T][H Dh] bf16 attention output
+  uint16_t* out;           // [T][H Dh] bf16 attention output (nullable)
   float scale;             // 1/sqrt(Dh)
+  unsigned char* oimg = nullptr;  // the output as the O projection's SW128 B image (nullable)
+  int o_bn = 16;
 };
 size_t attn_smem_bytes(int T, int H, int Hkv, int Dh, int P);
 cudaError_t launch_attn_window(const AttnArgs& a, cudaStream_t st);

@@ -192,6 +192,10 @@ __global__ void __launch_bounds__(256) k_resid_norm_route(RouteArgs a) {
       const uint2 packed = make_uint2((uint32_t)b[0] | ((uint32_t)b[1] << 16), (uint32_t)b[2] | ((uint32_t)b[3] << 16));
       reinterpret_cast<uint2*>(xs)[c] = packed;
       reinterpret_cast<uint2*>(a.xn + (int64_t)t * a.d)[c] = packed;
+      if (a.bimg) {  // columns 4c..4c+3 sit in one 16-byte swizzle chunk of k-block 4c/64
+        const int col = 4 * c;
+        *reinterpret_cast<uint2*>(a.bimg + (int64_t)(col >> 6) * (a.bimg_bn * 128) + sw128_off(t, col & 63)) = packed;
+      }
     }
   }
   if (!a.router) return;

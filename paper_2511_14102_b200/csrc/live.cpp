@@ -504,17 +504,20 @@ int enqueue_attn(mspq_engine* E, int l, int T, const int32_t* pos0, const float*
                  const float* wts, int y_splits, long long y_stride, float* cap_in, cudaStream_t s) {
   const auto& m = E->m;
   const int d = m.d;
-  CAPI_OK(mspq_gate_topk(E->h, y, entry_of, wts, y_splits, y_stride, E->gamma_a + (size_t)l * d, nullptr, E->xn,
-                         nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, l, m.L, T, d, m.E, m.K, m.eps,
-                         s));
+  // the normed rows go straight into the QKV GEMM's B image and the attention output into the O
+  // GEMM's (one workspace, used in stream order): no gather kernels
+  CAPI_OK(mspq_gate_topk_img(E->h, y, entry_of, wts, y_splits, y_stride, E->gamma_a + (size_t)l * d, nullptr, E->xn,
+                             nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, l, m.L, T, d, m.E, m.K,
+                             m.eps, E->dws, s));
   if (cap_in) CUDA_OK(cudaMemcpyAsync(cap_in, E->h, (size_t)T * d * 4, cudaMemcpyDeviceToDevice, s));
   const unsigned char* wl = E->wattn + (size_t)l * E->wattn_layer;
   const int spq = dense_split(E->Nqkv, d), spo = dense_split(d, E->Nq);
-  CAPI_OK(mspq_dense_bf16_tc(E->dsched_of(T), E->xn, wl, E->Nqkv, d, T, spq, E->dws, E->qkv, (long long)T * E->Nqkv, s));
+  CAPI_OK(mspq_dense_bf16_tc(E->dsched_of(T), nullptr, wl, E->Nqkv, d, T, spq, E->dws, E->qkv, (long long)T * E->Nqkv, s));
   CAPI_OK(mspq_attention(E->qkv, spq, (long long)T * E->Nqkv, T, m.H, m.Hkv, m.Dh, m.P, pos0,
-                         E->kcache + (size_t)l * E->kv_layer(), E->vcache + (size_t)l * E->kv_layer(), E->ao, s));
-  CAPI_OK(mspq_dense_bf16_tc(E->dsched_of(T), E->ao, wl + (size_t)E->Nqkv * d * 2, d, E->Nq, T, spo, E->dws, E->oproj,
-                             (long long)T * d, s));
+                         E->kcache + (size_t)l * E->kv_layer(), E->vcache + (size_t)l * E->kv_layer(), nullptr, E->dws,
+                         s));
+  CAPI_OK(mspq_dense_bf16_tc(E->dsched_of(T), nullptr, wl + (size_t)E->Nqkv * d * 2, d, E->Nq, T, spo, E->dws,
+                             E->oproj, (long long)T * d, s));
   return spo;
 }
 
@@ -1627,9 +1630,9 @@ int mspq_engine_create(const mspq_model_desc* md, const mspq_engine_opts* op, ms
       E->Tmax = op->kmax + 1;
       E->n_payload = m.unique_experts > 0 ? std::min(m.unique_experts, m.L * m.E) : m.L * m.E;
       if (m.H > 0) {
-        if (m.Hkv < 1 || m.H % m.Hkv || m.H / m.Hkv > 8 || m.Dh % 64 || (m.H * m.Dh) % 128 ||
+        if (m.Hkv < 1 || m.H % m.Hkv || m.H / m.Hkv > 8 || (m.Dh != 64 && m.Dh != 128) || (m.H * m.Dh) % 128 ||
             ((m.H + 2 * m.Hkv) * m.Dh) % 128)
-          fail(MSPQ_ERR_SHAPE_VIOLATION, "attention: need Hkv | H, H/Hkv <= 8, Dh % 64, H*Dh and (H+2Hkv)*Dh % 128");
+          fail(MSPQ_ERR_SHAPE_VIOLATION, "attention: need Hkv | H, H/Hkv <= 8, Dh in {64, 128}, H*Dh and (H+2Hkv)*Dh % 128");
         E->attn = true;
         E->Nq = m.H * m.Dh;
         E->Nkv = m.Hkv * m.Dh;

@@ -124,9 +124,6 @@ MSPQ_D void tmem_ld8(uint32_t taddr, float* v) {
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-MSPQ_HD int sw128_off(int row, int col) {
-  return (row >> 3) * 1024 + (row & 7) * 128 + ((((col >> 3) ^ (row & 7)) & 7) << 4) + (col & 7) * 2;
-}
 
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(192, 1) k_umma_grouped(UmmaArgs a) {

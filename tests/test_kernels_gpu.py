@@ -300,3 +300,75 @@ def test_moe_int4_tcgen05_within_tolerance(cuda, name, E, K, d, f, T, split1, sp
             got = y[eo[t, j]]
             tol = 2e-3 * np.abs(want).max() + 1e-5
             assert np.abs(got - want).max() <= tol, (t, j, np.abs(got - want).max(), tol)
+
+
+def _ptr(t):
+    import ctypes
+    return ctypes.c_void_p(t.data_ptr())
+
+
+@pytest.mark.parametrize("H,Hkv,Dh,T,p0", [(4, 2, 64, 5, 37), (32, 8, 128, 17, 300), (32, 4, 128, 1, 1000)])
+def test_attention_window_vs_fp64_reference(cuda, H, Hkv, Dh, T, p0):
+    """mspq_attention (shared-KV decode attention, attention.cu) against a float64 reference on
+    the same inputs: the window's K/V rows land in the cache as bf16 of the split-plane sums, and
+    each token's output matches softmax(q K^T / sqrt(Dh)) V over the causal context within 2e-3 of
+    its scale (fp32 accumulation + bf16 output)."""
+    from paper_2511_14102_b200._lib import check, lib
+    rng = np.random.default_rng(H + T + p0)
+    P, S = 2048, 3
+    Nq, Nkv = H * Dh, Hkv * Dh
+    qkv = (rng.standard_normal((S, T, Nq + 2 * Nkv)) * 0.5).astype(np.float32)
+    kc0 = om.f32_to_bf16(rng.standard_normal((P, Hkv, Dh)).astype(np.float32))
+    vc0 = om.f32_to_bf16(rng.standard_normal((P, Hkv, Dh)).astype(np.float32))
+    d_qkv = torch.from_numpy(qkv).cuda()
+    d_kc, d_vc = to_dev(kc0), to_dev(vc0)
+    d_out = torch.zeros(T * Nq, dtype=torch.int16, device="cuda")
+    d_pos = torch.tensor([p0], dtype=torch.int32, device="cuda")
+    check(lib().mspq_attention(_ptr(d_qkv), S, T * (Nq + 2 * Nkv), T, H, Hkv, Dh, P, _ptr(d_pos), _ptr(d_kc),
+                               _ptr(d_vc), _ptr(d_out), None, None))
+    torch.cuda.synchronize()
+    tot = qkv.sum(axis=0, dtype=np.float32) if S == 1 else qkv[0] + qkv[1] + qkv[2]
+    knew = om.f32_to_bf16(tot[:, Nq:Nq + Nkv]).reshape(T, Hkv, Dh)
+    vnew = om.f32_to_bf16(tot[:, Nq + Nkv:]).reshape(T, Hkv, Dh)
+    kc = i16_to_u16(d_kc).reshape(P, Hkv, Dh)
+    vc = i16_to_u16(d_vc).reshape(P, Hkv, Dh)
+    assert np.array_equal(kc[p0:p0 + T], knew) and np.array_equal(vc[p0:p0 + T], vnew)
+    assert np.array_equal(kc[:p0], kc0[:p0])
+    K64 = om.bf16_to_f32(np.concatenate([kc0[:p0], knew])).astype(np.float64)
+    V64 = om.bf16_to_f32(np.concatenate([vc0[:p0], vnew])).astype(np.float64)
+    out = om.bf16_to_f32(i16_to_u16(d_out)).reshape(T, H, Dh)
+    G = H // Hkv
+    for t in range(T):
+        for h in range(H):
+            q = tot[t, h * Dh:(h + 1) * Dh].astype(np.float64)
+            s = K64[:p0 + t + 1, h // G] @ q / np.sqrt(Dh)
+            p = np.exp(s - s.max())
+            want = (p @ V64[:p0 + t + 1, h // G]) / p.sum()
+            assert np.abs(out[t, h] - want).max() <= 2e-3 * (np.abs(want).max() + 1e-3), (t, h)
+
+
+def test_dense_projection_vs_fp64_reference(cuda):
+    """mspq_dense_bf16_tc (the attention projections: K3's tcgen05 GEMM with one group) on
+    tile-major bf16 weights, with the B image built by the gather or by K1 (x = NULL)."""
+    from paper_2511_14102_b200 import ops
+    from paper_2511_14102_b200._lib import check, lib
+    import ctypes
+    rng = np.random.default_rng(4)
+    rows, kdim, T, split = 768, 512, 7, 3
+    w = om.f32_to_bf16((rng.standard_normal((rows, kdim)) * 0.05).astype(np.float32))
+    x = om.f32_to_bf16(rng.standard_normal((T, kdim)).astype(np.float32))
+    d_w = to_dev(w)
+    d_wt = torch.empty(rows * kdim, dtype=torch.int16, device="cuda")
+    check(lib().mspq_tile_bf16(_ptr(d_w), rows, kdim, _ptr(d_wt), None))
+    ds = (ctypes.c_int32 * (4 + T))()
+    lib().mspq_dense_sched_fill(ds, T)
+    d_ds = torch.tensor(list(ds), dtype=torch.int32, device="cuda")
+    ws = torch.zeros(lib().mspq_dense_ws_bytes(kdim, T), dtype=torch.uint8, device="cuda")
+    out = torch.zeros(split * T * rows, dtype=torch.float32, device="cuda")
+    check(lib().mspq_dense_bf16_tc(_ptr(d_ds), _ptr(to_dev(x)), _ptr(d_wt), rows, kdim, T, split, _ptr(ws), _ptr(out),
+                                   T * rows, None))
+    torch.cuda.synchronize()
+    got = out.cpu().numpy().reshape(split, T, rows).sum(axis=0)
+    want = om.bf16_to_f32(x).astype(np.float64) @ om.bf16_to_f32(w).astype(np.float64).T
+    assert np.abs(got - want).max() <= 1e-4 * np.abs(want).max()
+    del ops
