@@ -171,6 +171,10 @@ struct mspq_engine {
   std::vector<double> elb_freq;
   std::vector<int32_t> res_host;
   std::vector<double> elb_calib;  // [kmax+1] EMA of fetched / estimated for the k actually run
+  // the governor's learned state (EMA acceptance p_i, g) persists across generate() calls of one
+  // configuration, as in serving; configure() resets it
+  std::vector<double> gov_accept;
+  double gov_g = -1.0;
   // trace_level >= 3 (parity tests): the fp32 residual entering every layer (index L = final),
   // for the verify window [L+1][T][d] and each draft row [k][L+1][d], kept per cycle of the
   // last generate() and read back with mspq_engine_read("hcap_v:<cycle>" / "hcap_d:<cycle>")
@@ -671,6 +675,8 @@ static void configure(mspq_engine* E, const std::string& text) {
   E->elb_freq.assign((size_t)m.L * m.E, (double)m.K / m.E);  // uniform prior: K of E experts per token
   E->res_host.assign((size_t)m.L * m.E, -1);                  // mspq_cache_configure empties the cache
   E->elb_calib.assign((size_t)E->o.kmax + 1, 1.0);
+  E->gov_accept.clear();
+  E->gov_g = -1.0;
   E->last_cycle.assign(E->nbuf, -1);
   E->last_layer.assign(E->nbuf, -1);
   CAPI_OK(mspq_cache_configure(E->cache, c.mode, c.policy, E->caps.data(), (int)std::min<long>(c.cache_capacity, (long)m.L * m.E),
@@ -726,12 +732,13 @@ static void configure(mspq_engine* E, const std::string& text) {
     // verify samples from the resident-expert roofline of this model on the measured peaks:
     // per layer E[union(w)] bf16 experts + router, plus the LM head, at the draft's achieved
     // bytes/s (the same kernels' streaming rate).
-    const double draft_bytes = (double)m.L * m.K * E->S4 + (double)m.V * m.d * 2 + (double)m.L * m.E * m.d * 2;
+    const double dense = (double)m.V * m.d * 2 + (double)m.L * m.E * m.d * 2 + (double)m.L * E->wattn_layer;
+    const double draft_bytes = (double)m.L * m.K * E->S4 + dense;
     const double bw = draft_bytes / std::max(E->draft_step_s, 1e-6);
     p.verify_samples.clear();
     for (double w : {1.0, 5.0, 9.0, 17.0}) {
       const double uni = (double)m.E * (1.0 - std::pow(1.0 - (double)m.K / m.E, w));
-      const double bytes = (double)m.L * uni * E->S16 + (double)m.V * m.d * 2 + (double)m.L * m.E * m.d * 2;
+      const double bytes = (double)m.L * uni * E->S16 + dense;
       p.verify_samples.push_back({w, bytes / bw});
     }
     c.profile = p;
@@ -875,8 +882,10 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
   CUDA_OK(cudaMemcpyAsync(E->dst, E->hpin, 12, cudaMemcpyHostToDevice, E->sc));
   CUDA_OK(cudaMemcpyAsync(E->win_tok(), E->hpin + 1, 4, cudaMemcpyHostToDevice, E->sc));
   const int kcap = std::max(c.use_governor ? c.k_max : c.fixed_k, 1);
-  std::vector<double> accept(kcap, c.initial_accept);
-  double g = static_cast<double>(L) * static_cast<double>(K);
+  if (E->gov_accept.empty()) E->gov_accept.assign(kcap, c.initial_accept);
+  if (E->gov_g < 0.0) E->gov_g = static_cast<double>(L) * static_cast<double>(K);
+  std::vector<double>& accept = E->gov_accept;
+  double& g = E->gov_g;
   // |E_new(k)| for the governor.  linear (reference, sim.cpp:75-78): g*k with g = fetched/k of the
   // last cycle.  elb: the ELB analysed against the current cache state -- per layer,
   // every non-resident expert e is fetched if any of the k+1 window tokens routes to it, which the
@@ -1497,7 +1506,8 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
   ks["k3_groups"] = k3_groups;
   ks["draft_steps"] = draft_steps;
   ks["draft_time_s"] = draft_time;
-  ks["draft_step_bytes"] = (double)m.L * m.K * E->S4 + (double)m.V * m.d * 2 + (double)m.L * m.E * m.d * 2;
+  ks["draft_step_bytes"] = (double)m.L * m.K * E->S4 + (double)m.V * m.d * 2 + (double)m.L * m.E * m.d * 2 +
+                           (double)m.L * E->wattn_layer;
   rep["kernels"] = ks;
   return rep.dump();
 }

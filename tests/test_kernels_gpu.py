@@ -311,8 +311,8 @@ def _ptr(t):
 def test_attention_window_vs_fp64_reference(cuda, H, Hkv, Dh, T, p0):
     """mspq_attention (shared-KV decode attention, attention.cu) against a float64 reference on
     the same inputs: the window's K/V rows land in the cache as bf16 of the split-plane sums, and
-    each token's output matches softmax(q K^T / sqrt(Dh)) V over the causal context within 2e-3 of
-    its scale (fp32 accumulation + bf16 output)."""
+    each token's output matches softmax(q K^T / sqrt(Dh)) V over the causal context within 4e-3 of
+    its scale (bf16 output rounding, up to 2^-9 relative, + fp32 accumulation)."""
     from paper_2511_14102_b200._lib import check, lib
     rng = np.random.default_rng(H + T + p0)
     P, S = 2048, 3
@@ -344,7 +344,8 @@ def test_attention_window_vs_fp64_reference(cuda, H, Hkv, Dh, T, p0):
             s = K64[:p0 + t + 1, h // G] @ q / np.sqrt(Dh)
             p = np.exp(s - s.max())
             want = (p @ V64[:p0 + t + 1, h // G]) / p.sum()
-            assert np.abs(out[t, h] - want).max() <= 2e-3 * (np.abs(want).max() + 1e-3), (t, h)
+            # bf16 output: half an ulp is 2^-9 of the value; + fp32 accumulation and __expf
+            assert np.abs(out[t, h] - want).max() <= 4e-3 * (np.abs(want).max() + 1e-3), (t, h)
 
 
 def test_dense_projection_vs_fp64_reference(cuda):
