@@ -179,10 +179,13 @@ int mspq_dense_bf16_tc(const int32_t* dsched, const void* x, const void* w_tiled
  * pointer): qkv = the QKV projection's split planes [splits][T][(H+2Hkv) Dh]; the window's K/V
  * rows are written into kc/vc ([P][Hkv][Dh] bf16, this layer) and every token attends causally
  * to the cache rows before the window plus the window tokens up to itself; out [T][H Dh] bf16
- * (nullable) and/or oimg = the O projection's B image (a dense GEMM workspace, x = NULL).
+ * (nullable) and/or oimg = the O projection's B image (a dense GEMM workspace, x = NULL).  Split-K
+ * over the context (16 key chunks per token and KV head, merged in order); ws =
+ * mspq_attention_ws_bytes(T, H, Hkv, Dh) bytes; P <= 4096.
  * Draft and target share the cache; rollback = the next window overwrites rows >= its pos0. */
+long long mspq_attention_ws_bytes(int T, int H, int Hkv, int Dh);
 int mspq_attention(const float* qkv, int splits, long long split_stride, int T, int H, int Hkv, int Dh, int P,
-                   const int32_t* pos0, void* kc, void* vc, void* out, void* oimg, void* stream);
+                   const int32_t* pos0, void* kc, void* vc, void* out, void* oimg, void* ws, void* stream);
 /* row-major quantised INT4 (q[rows][cols/8] u32, standard nibble order; s[rows][cols/128] bf16)
  * -> tile-major [rows/128][cols/64][128][8] u32 + [rows/128][cols/128][128] bf16 */
 int mspq_tile_int4(const void* q, const void* s, int rows, int cols, void* tq, void* ts, void* stream);

@@ -7,7 +7,7 @@
 // k_umma_grouped with one group of T tokens) -> k_attn_window -> O projection (dense tcgen05
 // GEMM) -> K1 (dense combine h += o, MoE RMSNorm, router).
 //
-// k_attn_window: one CTA per (window token t, KV head g).  The window's own keys/values come
+// k_attn_partial + k_attn_combine: split-K over the context per (window token t, KV head g).  The window's own keys/values come
 // straight from the QKV GEMM's fp32 split planes (summed in split order, rounded to bf16 -- the
 // same bf16 values the cache stores), so tokens of one window never wait on each other's cache
 // writes; positions before the window are read from the cache.  The CTA writes its token's K/V
@@ -21,6 +21,7 @@ namespace mspq {
 namespace {
 
 constexpr int AT_THREADS = 256, AT_WARPS = AT_THREADS / 32, AT_MAXG = 8;
+constexpr int AT_SPLITS = 16, AT_MAXPOS = 4096, AT_MAXCHUNK = AT_MAXPOS / AT_SPLITS;
 
 MSPQ_D float warp_max(float v) {
 #pragma unroll
@@ -28,36 +29,44 @@ MSPQ_D float warp_max(float v) {
   return v;
 }
 
-// lane l owns head dims [VEC*l, VEC*l + VEC) (Dh = 32 VEC): q in registers, one vector load per
-// key row; keys are split over the 8 warps both for the scores and for the value sum, whose
-// per-warp partials are added in warp order (deterministic)
+// Split-K (flash-decoding) over the context: CTA (t, g, s) takes key positions
+// [s*chunk, (s+1)*chunk) of token t's causal range (chunk = ceil(n / AT_SPLITS)), so a T = 1 draft
+// step still spreads over Hkv x AT_SPLITS CTAs.  Lane l owns head dims [VEC*l, VEC*l + VEC)
+// (Dh = 32 VEC): q in registers, one vector load per key row; warps stride over the chunk's keys.
+// Each CTA leaves (max, sum of exp, unnormalised V sum) per head; k_attn_combine merges the
+// AT_SPLITS partials in split order (deterministic) and writes bf16.
+MSPQ_D int attn_chunk(int n) { return (n + AT_SPLITS - 1) / AT_SPLITS; }
+
 template <int VEC>
-__global__ void __launch_bounds__(AT_THREADS) k_attn_window(AttnArgs a) {
+__global__ void __launch_bounds__(AT_THREADS) k_attn_partial(AttnArgs a) {
   pdl_enter();  // launched with launch_pdl (kernels.h)
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int t = blockIdx.x, g = blockIdx.y;
+  const int t = blockIdx.x, g = blockIdx.y, sp = blockIdx.z;
   const int G = a.H / a.Hkv, Dh = a.Dh;
   const int Nq = a.H * Dh, Nkv = a.Hkv * Dh, Nqkv = Nq + 2 * Nkv;
   const int p0 = *a.pos0, pt = p0 + t, n = pt + 1;
+  const int chunk = attn_chunk(n), j0 = sp * chunk, j1 = min(n, j0 + chunk);
   uint16_t* wk = reinterpret_cast<uint16_t*>(smem_raw);     // [T][Dh] in-window keys, bf16
   uint16_t* wv = wk + a.T * Dh;                             // [T][Dh] in-window values
-  float* sc = reinterpret_cast<float*>(wv + a.T * Dh);     // [G][P] scores -> probabilities
-  float* red = sc + (size_t)G * a.P;                        // [AT_WARPS][G][Dh] value partials
-  __shared__ float hsum[AT_MAXG];
+  float* sc = reinterpret_cast<float*>(wv + a.T * Dh);     // [G][chunk] scores -> exp
+  float* red = sc + (size_t)G * AT_MAXCHUNK;                // [AT_WARPS][G][Dh] value partials
+  __shared__ float hmax[AT_MAXG], hsum[AT_MAXG];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float* part = a.part + (((size_t)t * a.Hkv + g) * AT_SPLITS + sp) * (size_t)G * (Dh + 2);
   // (1) in-window k/v of tokens 0..t (split planes summed in order, rounded to bf16 like the cache)
-  for (int i = tid; i < (t + 1) * Dh; i += AT_THREADS) {
-    const int tt = i / Dh, dd = i - tt * Dh;
-    const float* src = a.qkv + (int64_t)tt * Nqkv + Nq + g * Dh + dd;
-    float kv = 0.0f, vv = 0.0f;
-    for (int s = 0; s < a.splits; ++s) {
-      kv = __fadd_rn(kv, src[s * a.split_stride]);
-      vv = __fadd_rn(vv, src[s * a.split_stride + Nkv]);
+  const bool need_win = j1 > p0 || sp == 0;
+  if (need_win)
+    for (int i = tid; i < (t + 1) * Dh; i += AT_THREADS) {
+      const int tt = i / Dh, dd = i - tt * Dh;
+      const float* src = a.qkv + (int64_t)tt * Nqkv + Nq + g * Dh + dd;
+      float kv = 0.0f, vv = 0.0f;
+      for (int s = 0; s < a.splits; ++s) {
+        kv = __fadd_rn(kv, src[s * a.split_stride]);
+        vv = __fadd_rn(vv, src[s * a.split_stride + Nkv]);
+      }
+      wk[i] = f2bf(kv);
+      wv[i] = f2bf(vv);
     }
-    wk[i] = f2bf(kv);
-    wv[i] = f2bf(vv);
-  }
-  // q of the G heads, lane slice, fp32 in registers
   float q[AT_MAXG][VEC];
 #pragma unroll
   for (int i = 0; i < AT_MAXG; ++i)
@@ -71,10 +80,11 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_window(AttnArgs a) {
       q[i][v] = x;
     }
   __syncthreads();
-  for (int dd = tid; dd < Dh; dd += AT_THREADS) {  // this token's row of the shared cache
-    a.kc[((int64_t)pt * a.Hkv + g) * Dh + dd] = wk[t * Dh + dd];
-    a.vc[((int64_t)pt * a.Hkv + g) * Dh + dd] = wv[t * Dh + dd];
-  }
+  if (sp == 0)
+    for (int dd = tid; dd < Dh; dd += AT_THREADS) {  // this token's row of the shared cache
+      a.kc[((int64_t)pt * a.Hkv + g) * Dh + dd] = wk[t * Dh + dd];
+      a.vc[((int64_t)pt * a.Hkv + g) * Dh + dd] = wv[t * Dh + dd];
+    }
   auto row_vec = [&](const uint16_t* cache, const uint16_t* win, int j, float* o) {
     const uint16_t* r = (j < p0 ? cache + ((int64_t)j * a.Hkv + g) * Dh : win + (j - p0) * Dh) + lane * VEC;
     if (VEC == 4) {
@@ -89,50 +99,53 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_window(AttnArgs a) {
       o[1] = __uint_as_float(u & 0xffff0000u);
     }
   };
-  // (2) scores: warps stride over the key positions
-  for (int j = warp; j < n; j += AT_WARPS) {
+  // (2) scores of this chunk
+  for (int j = j0 + warp; j < j1; j += AT_WARPS) {
     float kk[VEC];
     row_vec(a.kc, wk, j, kk);
 #pragma unroll
     for (int i = 0; i < AT_MAXG; ++i)
       if (i < G) {
-        float part = 0.0f;
+        float pp = 0.0f;
 #pragma unroll
-        for (int v = 0; v < VEC; ++v) part = fmaf(q[i][v], kk[v], part);
-        part = warp_butterfly_sum(part);
-        if (lane == 0) sc[i * a.P + j] = __fmul_rn(part, a.scale);
+        for (int v = 0; v < VEC; ++v) pp = fmaf(q[i][v], kk[v], pp);
+        pp = warp_butterfly_sum(pp);
+        if (lane == 0) sc[i * AT_MAXCHUNK + (j - j0)] = __fmul_rn(pp, a.scale);
       }
   }
   __syncthreads();
-  // (3) softmax numerators per head (warp i owns head i)
+  // (3) chunk max and exp sums per head (warp i owns head i)
   if (warp < G) {
-    float* sr = sc + warp * a.P;
+    float* sr = sc + warp * AT_MAXCHUNK;
     float m = -INFINITY;
-    for (int j = lane; j < n; j += 32) m = fmaxf(m, sr[j]);
+    for (int j = lane; j < j1 - j0; j += 32) m = fmaxf(m, sr[j]);
     m = warp_max(m);
     float s = 0.0f;
-    for (int j = lane; j < n; j += 32) {
+    for (int j = lane; j < j1 - j0; j += 32) {
       const float e = __expf(__fsub_rn(sr[j], m));
       sr[j] = e;
       s = __fadd_rn(s, e);
     }
     s = warp_butterfly_sum(s);
-    if (lane == 0) hsum[warp] = s;
+    if (lane == 0) {
+      hmax[warp] = m;
+      hsum[warp] = s;
+    }
   }
   __syncthreads();
-  // (4) value sums: warp w takes keys j = w, w + 8, ...; partials added in warp order
+  // (4) unnormalised value sums, per-warp partials added in warp order
   float acc[AT_MAXG][VEC];
 #pragma unroll
   for (int i = 0; i < AT_MAXG; ++i)
 #pragma unroll
     for (int v = 0; v < VEC; ++v) acc[i][v] = 0.0f;
-  for (int j = warp; j < n; j += AT_WARPS) {
+  for (int j = j0 + warp; j < j1; j += AT_WARPS) {
     float vv[VEC];
     row_vec(a.vc, wv, j, vv);
 #pragma unroll
     for (int i = 0; i < AT_MAXG; ++i)
       if (i < G) {
-        const float pj = sc[i * a.P + j];
+        const float pj = sc[i * AT_MAXCHUNK + (j - j0)];
 #pragma unroll
         for (int v = 0; v < VEC; ++v) acc[i][v] = fmaf(pj, vv[v], acc[i][v]);
       }
@@ -144,11 +157,37 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_window(AttnArgs a) {
       for (int v = 0; v < VEC; ++v) red[((size_t)warp * G + i) * Dh + lane * VEC + v] = acc[i][v];
   __syncthreads();
   for (int o = tid; o < G * Dh; o += AT_THREADS) {
-    const int i = o / Dh;
     float x = 0.0f;
 #pragma unroll
     for (int w = 0; w < AT_WARPS; ++w) x = __fadd_rn(x, red[(size_t)w * G * Dh + o]);
-    const uint16_t ob = f2bf(__fdiv_rn(x, hsum[i]));
+    part[2 * G + o] = x;
+  }
+  if (tid < G) {
+    part[tid] = j1 > j0 ? hmax[tid] : -INFINITY;
+    part[G + tid] = j1 > j0 ? hsum[tid] : 0.0f;
+  }
+}
+
+// merge the AT_SPLITS partials of (t, g) in split order: o = sum_s e^(m_s - M) acc_s / sum_s e^(m_s - M) l_s
+__global__ void __launch_bounds__(AT_THREADS) k_attn_combine(AttnArgs a) {
+  pdl_enter();
+  const int t = blockIdx.x, g = blockIdx.y;
+  const int G = a.H / a.Hkv, Dh = a.Dh, Nq = a.H * Dh;
+  const float* part = a.part + ((size_t)t * a.Hkv + g) * AT_SPLITS * (size_t)G * (Dh + 2);
+  const size_t ps = (size_t)G * (Dh + 2);
+  for (int o = threadIdx.x; o < G * Dh; o += AT_THREADS) {
+    const int i = o / Dh;
+    float M = -INFINITY;
+    for (int s = 0; s < AT_SPLITS; ++s) M = fmaxf(M, part[s * ps + i]);
+    float den = 0.0f, num = 0.0f;
+    for (int s = 0; s < AT_SPLITS; ++s) {
+      const float ms = part[s * ps + i];
+      if (ms == -INFINITY) continue;
+      const float w = __expf(__fsub_rn(ms, M));
+      den = fmaf(w, part[s * ps + G + i], den);
+      num = fmaf(w, part[s * ps + 2 * G + o], num);
+    }
+    const uint16_t ob = f2bf(__fdiv_rn(num, den));
     const int col = g * G * Dh + o;
     if (a.out) a.out[(int64_t)t * Nq + col] = ob;
     if (a.oimg) *reinterpret_cast<uint16_t*>(a.oimg + (int64_t)(col >> 6) * (a.o_bn * 128) + sw128_off(t, col & 63)) = ob;
@@ -159,22 +198,29 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_window(AttnArgs a) {
 
 size_t attn_smem_bytes(int T, int H, int Hkv, int Dh, int P) {
   const int G = H / Hkv;
-  return (size_t)2 * T * Dh * 2 + (size_t)G * P * 4 + (size_t)AT_WARPS * G * Dh * 4;
+  (void)P;
+  return (size_t)2 * T * Dh * 2 + (size_t)G * AT_MAXCHUNK * 4 + (size_t)AT_WARPS * G * Dh * 4;
+}
+size_t attn_part_floats(int T, int H, int Hkv, int Dh) {
+  return (size_t)T * Hkv * AT_SPLITS * (size_t)(H / Hkv) * (Dh + 2);
 }
 
 cudaError_t launch_attn_window(const AttnArgs& a, cudaStream_t st) {
+  if (a.P > AT_MAXPOS) return cudaErrorInvalidValue;
   const size_t smem = attn_smem_bytes(a.T, a.H, a.Hkv, a.Dh, a.P);
+  const dim3 grid(a.T, a.Hkv, AT_SPLITS);
+  cudaError_t e;
   if (a.Dh == 128) {
-    cudaError_t e = cudaFuncSetAttribute(k_attn_window<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    return launch_pdl(k_attn_window<4>, dim3(a.T, a.Hkv), dim3(AT_THREADS), smem, st, a);
+    e = cudaFuncSetAttribute(k_attn_partial<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) e = launch_pdl(k_attn_partial<4>, grid, dim3(AT_THREADS), smem, st, a);
+  } else if (a.Dh == 64) {
+    e = cudaFuncSetAttribute(k_attn_partial<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) e = launch_pdl(k_attn_partial<2>, grid, dim3(AT_THREADS), smem, st, a);
+  } else {
+    return cudaErrorInvalidValue;
   }
-  if (a.Dh == 64) {
-    cudaError_t e = cudaFuncSetAttribute(k_attn_window<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    return launch_pdl(k_attn_window<2>, dim3(a.T, a.Hkv), dim3(AT_THREADS), smem, st, a);
-  }
-  return cudaErrorInvalidValue;
+  if (e != cudaSuccess) return e;
+  return launch_pdl(k_attn_combine, dim3(a.T, a.Hkv), dim3(AT_THREADS), 0, st, a);
 }
 
 }  // namespace mspq

@@ -202,12 +202,16 @@ int mspq_dense_bf16_tc(const int32_t* dsched, const void* x, const void* w_tiled
   UmmaArgs u{(const unsigned char*)w_tiled, 0, 0, rows, kdim, p, p + 1, p + 2, b1, out, out_split_stride, split};
   CK(launch_umma_grouped(u, 1, BN, st), "dense umma");
 }
+long long mspq_attention_ws_bytes(int T, int H, int Hkv, int Dh) {
+  return (long long)attn_part_floats(T, H, Hkv, Dh) * 4;
+}
 int mspq_attention(const float* qkv, int splits, long long split_stride, int T, int H, int Hkv, int Dh, int P,
-                   const int32_t* pos0, void* kc, void* vc, void* out, void* oimg, void* stream) {
-  if (H < 1 || Hkv < 1 || H % Hkv || H / Hkv > 8 || (Dh != 64 && Dh != 128) || T < 1 || P < T)
-    return set_error(MSPQ_ERR_SHAPE_MISMATCH, "attention: Hkv | H, H/Hkv <= 8, Dh in {64, 128}, 1 <= T <= P");
+                   const int32_t* pos0, void* kc, void* vc, void* out, void* oimg, void* ws, void* stream) {
+  if (H < 1 || Hkv < 1 || H % Hkv || H / Hkv > 8 || (Dh != 64 && Dh != 128) || T < 1 || P < T || P > 4096 || !ws)
+    return set_error(MSPQ_ERR_SHAPE_MISMATCH,
+                     "attention: Hkv | H, H/Hkv <= 8, Dh in {64, 128}, 1 <= T <= P <= 4096, workspace");
   AttnArgs a{qkv, splits, split_stride, T, H, Hkv, Dh, P, pos0, (uint16_t*)kc, (uint16_t*)vc, (uint16_t*)out,
-             1.0f / sqrtf((float)Dh), (unsigned char*)oimg, tc_bn(T)};
+             1.0f / sqrtf((float)Dh), (unsigned char*)oimg, tc_bn(T), (float*)ws};
   CK(launch_attn_window(a, ST(stream)), "attention");
 }
 int mspq_moe_int4_tc(const int32_t* n_groups, const int32_t* group_expert, const int32_t* group_buf,

@@ -136,8 +136,10 @@ struct AttnArgs {
   float scale;             // 1/sqrt(Dh)
   unsigned char* oimg = nullptr;  // the output as the O projection's SW128 B image (nullable)
   int o_bn = 16;
+  float* part = nullptr;          // split-K partials, attn_part_floats(T, H, Hkv, Dh) floats
 };
 size_t attn_smem_bytes(int T, int H, int Hkv, int Dh, int P);
+size_t attn_part_floats(int T, int H, int Hkv, int Dh);
 cudaError_t launch_attn_window(const AttnArgs& a, cudaStream_t st);
 
 cudaError_t launch_umma_grouped(const UmmaArgs& a, int max_groups, int BN, cudaStream_t st);

@@ -193,6 +193,7 @@ struct mspq_engine {
   uint16_t* ao = nullptr;                  // [Tmax][Nq] attention output
   int32_t* dsched = nullptr;               // [Tmax + 1][4 + Tmax] packed dense schedules per T
   void* dws = nullptr;
+  float* attn_part = nullptr;  // split-K attention partials
   int32_t* dsched_of(int T) { return dsched + (size_t)T * (4 + Tmax); }
   size_t kv_layer() const { return (size_t)m.P * m.Hkv * m.Dh; }
   int32_t* sched_cap = nullptr;  // collect_plans: each verify layer's device schedule [L][Sched::ints]
@@ -467,6 +468,7 @@ void make_workspaces(mspq_engine* E) {
     CUDA_OK(cudaMalloc(&E->oproj, (size_t)KS * T * d * 4));
     CUDA_OK(cudaMalloc(&E->ao, (size_t)T * E->Nq * 2));
     CUDA_OK(cudaMalloc(&E->dws, (size_t)mspq_dense_ws_bytes(std::max(d, E->Nq), T)));
+    CUDA_OK(cudaMalloc(&E->attn_part, (size_t)mspq_attention_ws_bytes(T, m.H, m.Hkv, m.Dh)));
     std::vector<int32_t> ds((size_t)(T + 1) * (4 + T), 0);
     for (int t = 1; t <= T; ++t) mspq_dense_sched_fill(ds.data() + (size_t)t * (4 + T), t);
     CUDA_OK(cudaMalloc(&E->dsched, ds.size() * 4));
@@ -519,7 +521,7 @@ int enqueue_attn(mspq_engine* E, int l, int T, const int32_t* pos0, const float*
   CAPI_OK(mspq_dense_bf16_tc(E->dsched_of(T), nullptr, wl, E->Nqkv, d, T, spq, E->dws, E->qkv, (long long)T * E->Nqkv, s));
   CAPI_OK(mspq_attention(E->qkv, spq, (long long)T * E->Nqkv, T, m.H, m.Hkv, m.Dh, m.P, pos0,
                          E->kcache + (size_t)l * E->kv_layer(), E->vcache + (size_t)l * E->kv_layer(), nullptr, E->dws,
-                         s));
+                         E->attn_part, s));
   CAPI_OK(mspq_dense_bf16_tc(E->dsched_of(T), nullptr, wl + (size_t)E->Nqkv * d * 2, d, E->Nq, T, spo, E->dws,
                              E->oproj, (long long)T * d, s));
   return spo;
@@ -1552,7 +1554,7 @@ void destroy(mspq_engine* E) {
     if (p) cudaFree(p);
   if (E->sched_cap) cudaFree(E->sched_cap);
   for (void* p : {(void*)E->wattn, (void*)E->gamma_a, (void*)E->kcache, (void*)E->vcache, (void*)E->qkv, (void*)E->oproj,
-                  (void*)E->ao, (void*)E->dsched, E->dws, (void*)E->hmid_v, (void*)E->hmid_dstage, (void*)E->hmid_d})
+                  (void*)E->ao, (void*)E->dsched, E->dws, (void*)E->attn_part, (void*)E->hmid_v, (void*)E->hmid_dstage, (void*)E->hmid_d})
     if (p) cudaFree(p);
   for (size_t r = 0; r < E->peer_ipc.size(); ++r)
     if (E->peer_ipc[r] && E->peer_home[r]) cudaIpcCloseMemHandle(E->peer_home[r]);

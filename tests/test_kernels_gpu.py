@@ -324,8 +324,9 @@ def test_attention_window_vs_fp64_reference(cuda, H, Hkv, Dh, T, p0):
     d_kc, d_vc = to_dev(kc0), to_dev(vc0)
     d_out = torch.zeros(T * Nq, dtype=torch.int16, device="cuda")
     d_pos = torch.tensor([p0], dtype=torch.int32, device="cuda")
+    ws = torch.zeros(lib().mspq_attention_ws_bytes(T, H, Hkv, Dh), dtype=torch.uint8, device="cuda")
     check(lib().mspq_attention(_ptr(d_qkv), S, T * (Nq + 2 * Nkv), T, H, Hkv, Dh, P, _ptr(d_pos), _ptr(d_kc),
-                               _ptr(d_vc), _ptr(d_out), None, None))
+                               _ptr(d_vc), _ptr(d_out), None, _ptr(ws), None))
     torch.cuda.synchronize()
     tot = qkv.sum(axis=0, dtype=np.float32) if S == 1 else qkv[0] + qkv[1] + qkv[2]
     knew = om.f32_to_bf16(tot[:, Nq:Nq + Nkv]).reshape(T, Hkv, Dh)

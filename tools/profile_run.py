@@ -15,6 +15,7 @@ ap.add_argument("--tokens", type=int, default=4)
 ap.add_argument("--unique", type=int, default=16)
 ap.add_argument("--cap", type=int, default=4)
 ap.add_argument("--k", default="4")
+ap.add_argument("--prompt-len", type=int, default=3, help="prompt tokens (attention context)")
 a = ap.parse_args()
 cfg = m.ModelConfig.named(a.model, unique_experts=a.unique)
 eng = m.Engine(cfg, kmax=16, trace_level=0)
@@ -23,7 +24,8 @@ eng.configure(conf)
 eng.generate([1, 2, 3], 8)
 torch.cuda.synchronize()
 torch.cuda.profiler.start()
-r = eng.generate([5, 6, 7], a.tokens)
+prompt = [(5 + 7 * i) % cfg.V for i in range(a.prompt_len)]
+r = eng.generate(prompt, a.tokens)
 torch.cuda.synchronize()
 torch.cuda.profiler.stop()
 print("tokens", r["tokens"], "cycles", len(r["cycles"]), "k3", r["kernels"])
