@@ -274,6 +274,12 @@ int mspq_cache_replay_cycle(mspq_cache* c, const int32_t* target, const int32_t*
  * with "log": true in config_json also the per-event hit/miss log. */
 int mspq_replay(int device, const char* trace_jsonl, const char* config_json,
                 char** report_json);
+/* compare_policies / sweep_k (sim.cpp:539-574, sim.hpp:88-109) over mspq_replay:
+ * rows [{"policy","capacity","coverage","tpot"}] / [{"k","tpot","mean_accepted","coverage","ttft"}] */
+int mspq_compare_policies(int device, const char* trace_jsonl, const char* config_json,
+                          const char* policies_json, const char* capacities_json, char** rows_json);
+int mspq_sweep_k(int device, const char* trace_jsonl, const char* config_json, const char* ks_json,
+                 char** rows_json);
 /* Amortization-Roofline governor (perfmodel.cpp:85-217) on a JSON request:
  * {"profile":{...},"p":[...],"alpha":a,"k_min","k_max","k_slo","g","ttft_budget","outcomes"}
  * -> {"select_k","k_slo_ttft","t_cycle":[k=0..],"k_accept":[..],"t_verify":[..],"updated_p"} */

@@ -39,6 +39,12 @@ def lib():
         L.ref_select_victim.argtypes = [c, ctypes.c_int, c, ctypes.c_int, ctypes.c_int]
         L.ref_governor.restype = v
         L.ref_governor.argtypes = [c]
+        L.ref_trace_analysis.restype = v
+        L.ref_trace_analysis.argtypes = [c]
+        L.ref_compare_policies.restype = v
+        L.ref_compare_policies.argtypes = [c, c, c, c]
+        L.ref_sweep_k.restype = v
+        L.ref_sweep_k.argtypes = [c, c, c]
         _lib = L
     return _lib
 
@@ -88,3 +94,19 @@ def select_victim(trace_jsonl: str, k: int, resident, now: int, layer_filter: in
 
 def governor(request: dict) -> dict:
     return json.loads(_take(lib().ref_governor(json.dumps(request).encode())))
+
+
+def trace_analysis(trace_jsonl: str) -> dict:
+    """classify_fidelity (both granularities) + layer_entropy per layer (trace.cpp:401-462)."""
+    return json.loads(_take(lib().ref_trace_analysis(trace_jsonl.encode())))
+
+
+def compare_policies(trace_jsonl: str, config: dict, policies, capacities) -> list:
+    return json.loads(_take(lib().ref_compare_policies(trace_jsonl.encode(), json.dumps(config).encode(),
+                                                       json.dumps(list(policies)).encode(),
+                                                       json.dumps(list(capacities)).encode())))
+
+
+def sweep_k(trace_jsonl: str, config: dict, ks) -> list:
+    return json.loads(_take(lib().ref_sweep_k(trace_jsonl.encode(), json.dumps(config).encode(),
+                                              json.dumps(list(ks)).encode())))

@@ -170,4 +170,57 @@ char* ref_governor(const char* request_json) {
   });
 }
 
+// compare_policies / sweep_k (sim.cpp:539-574) with the rows as JSON
+char* ref_compare_policies(const char* trace_jsonl, const char* config_json, const char* policies_json,
+                           const char* capacities_json) {
+  return guarded([&] {
+    std::istringstream in(trace_jsonl);
+    const Trace trace = parse_trace(in);
+    const RunConfig cfg = parse_run_config(json::parse(config_json));
+    std::vector<Policy> pols;
+    for (const auto& p : json::parse(policies_json)) pols.push_back(parse_policy(p.get<std::string>()));
+    const std::vector<std::size_t> caps = json::parse(capacities_json).get<std::vector<std::size_t>>();
+    json rows = json::array();
+    for (const auto& r : compare_policies(trace, cfg.sim, pols, caps))
+      rows.push_back({{"policy", to_string(r.policy)}, {"capacity", r.capacity}, {"coverage", r.coverage},
+                      {"tpot", r.tpot}});
+    return rows.dump();
+  });
+}
+
+char* ref_sweep_k(const char* trace_jsonl, const char* config_json, const char* ks_json) {
+  return guarded([&] {
+    std::istringstream in(trace_jsonl);
+    const Trace trace = parse_trace(in);
+    const RunConfig cfg = parse_run_config(json::parse(config_json));
+    const std::vector<int> ks = json::parse(ks_json).get<std::vector<int>>();
+    json rows = json::array();
+    for (const auto& r : sweep_k(trace, cfg.sim, ks))
+      rows.push_back({{"k", r.k}, {"tpot", r.tpot}, {"mean_accepted", r.mean_accepted}, {"coverage", r.coverage},
+                      {"ttft", r.first_cycle_latency}});
+    return rows.dump();
+  });
+}
+
+// classify_fidelity (both granularities) + layer_entropy of every layer (trace.cpp:401-462)
+char* ref_trace_analysis(const char* trace_jsonl) {
+  return guarded([&] {
+    std::istringstream in(trace_jsonl);
+    const Trace tr = parse_trace(in);
+    json out;
+    for (auto [name, gran] : {std::pair<const char*, FidelityGranularity>{"token_layer", FidelityGranularity::TokenLayer},
+                              {"token", FidelityGranularity::Token}}) {
+      const FidelityStats f = classify_fidelity(tr, gran);
+      out["fidelity"][name] = {{"hard_rate", f.hard_rate}, {"soft_rate", f.soft_rate},
+                               {"mismatch_rate", f.mismatch_rate}, {"hard_count", f.hard_count},
+                               {"soft_count", f.soft_count}, {"mismatch_count", f.mismatch_count},
+                               {"total", f.total}};
+    }
+    json ent = json::array();
+    for (int l = 0; l < tr.shape.num_moe_layers; ++l) ent.push_back(layer_entropy(tr, l));
+    out["layer_entropy"] = ent;
+    return out.dump();
+  });
+}
+
 }  // extern "C"

@@ -107,6 +107,24 @@ def run_simulation(trace_jsonl: str, config: dict, device: int = 0) -> dict:
 replay = run_simulation
 
 
+def compare_policies(trace_jsonl: str, config: dict, policies, capacities, device: int = 0) -> list:
+    """compare_policies (sim.cpp:539-552) on the device control plane: one run_simulation per
+    (policy, capacity); rows {"policy", "capacity", "coverage", "tpot"} (PolicyRow, sim.hpp:88-93)."""
+    out = ctypes.c_void_p()
+    check(lib().mspq_compare_policies(device, trace_jsonl.encode(), _cfg_json(config), json.dumps(list(policies)).encode(),
+                                      json.dumps([int(c) for c in capacities]).encode(), ctypes.byref(out)))
+    return json.loads(take_string(out))
+
+
+def sweep_k(trace_jsonl: str, config: dict, ks, device: int = 0) -> list:
+    """sweep_k (sim.cpp:563-574): fixed-k runs; rows {"k", "tpot", "mean_accepted", "coverage",
+    "ttft"} (SweepRow, sim.hpp:101-107)."""
+    out = ctypes.c_void_p()
+    check(lib().mspq_sweep_k(device, trace_jsonl.encode(), _cfg_json(config), json.dumps([int(k) for k in ks]).encode(),
+                             ctypes.byref(out)))
+    return json.loads(take_string(out))
+
+
 def governor(request: dict) -> dict:
     """Amortization-Roofline governor evaluation (perfmodel.cpp:85-217) in the product."""
     out = ctypes.c_void_p()

@@ -77,6 +77,8 @@ _SIGS = [
     ("mspq_cache_replay_cycle", c_int, [c_void_p] * 4 + [c_int] * 3 + [c_void_p] * 7),
     ("mspq_replay", c_int, [c_int, c_char_p, c_char_p, ctypes.POINTER(c_void_p)]),
     ("mspq_governor", c_int, [c_char_p, ctypes.POINTER(c_void_p)]),
+    ("mspq_compare_policies", c_int, [c_int, c_char_p, c_char_p, c_char_p, c_char_p, ctypes.POINTER(c_void_p)]),
+    ("mspq_sweep_k", c_int, [c_int, c_char_p, c_char_p, c_char_p, ctypes.POINTER(c_void_p)]),
     ("mspq_engine_create", c_int, [ctypes.POINTER(ModelDesc), ctypes.POINTER(EngineOpts), ctypes.POINTER(c_void_p)]),
     ("mspq_engine_destroy", c_int, [c_void_p]),
     ("mspq_engine_configure", c_int, [c_void_p, c_char_p]),

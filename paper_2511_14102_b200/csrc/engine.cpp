@@ -702,6 +702,52 @@ extern "C" int mspq_replay(int device, const char* trace_jsonl, const char* conf
   });
 }
 
+// compare_policies / sweep_k (sim.cpp:539-574) on the device control plane: run_simulation of
+// the trace once per (policy, capacity) / per fixed k, rows as in PolicyRow / SweepRow
+// (sim.hpp:88-109).  policies_json: ["lru", ...]; capacities_json / ks_json: integer arrays.
+extern "C" int mspq_compare_policies(int device, const char* trace_jsonl, const char* config_json,
+                                     const char* policies_json, const char* capacities_json, char** rows_json) {
+  using namespace mspq_host;
+  return guarded([&] {
+    json base = json::parse(config_json, nullptr, false);
+    json pols = json::parse(policies_json, nullptr, false), caps = json::parse(capacities_json, nullptr, false);
+    if (base.is_discarded() || !pols.is_array() || !caps.is_array())
+      fail(MSPQ_ERR_INVALID_CONFIG, "compare_policies: config object, policy and capacity arrays");
+    json rows = json::array();
+    for (const auto& pol : pols)
+      for (const auto& cap : caps) {
+        json cfg = base;
+        cfg["policy"] = pol;
+        cfg["cache_capacity"] = cap;
+        const json rep = json::parse(replay(device, trace_jsonl, cfg.dump()));
+        rows.push_back({{"policy", pol}, {"capacity", cap}, {"coverage", rep["mean_step_coverage"]},
+                        {"tpot", rep["tpot_s"]}});
+      }
+    *rows_json = dup(rows.dump());
+    return MSPQ_OK;
+  });
+}
+
+extern "C" int mspq_sweep_k(int device, const char* trace_jsonl, const char* config_json, const char* ks_json,
+                            char** rows_json) {
+  using namespace mspq_host;
+  return guarded([&] {
+    json base = json::parse(config_json, nullptr, false);
+    json ks = json::parse(ks_json, nullptr, false);
+    if (base.is_discarded() || !ks.is_array()) fail(MSPQ_ERR_INVALID_CONFIG, "sweep_k: config object, k array");
+    json rows = json::array();
+    for (const auto& k : ks) {
+      json cfg = base;
+      cfg["k"] = k;  // fixed k: the governor is off (SimConfig use_governor = false)
+      const json rep = json::parse(replay(device, trace_jsonl, cfg.dump()));
+      rows.push_back({{"k", k}, {"tpot", rep["tpot_s"]}, {"mean_accepted", rep["mean_accepted"]},
+                      {"coverage", rep["mean_step_coverage"]}, {"ttft", rep["ttft_s"]}});
+    }
+    *rows_json = dup(rows.dump());
+    return MSPQ_OK;
+  });
+}
+
 // Governor evaluation for parity tests: same request/response schema as oracle/ref_shim.cpp's
 // ref_governor (select_k, k_slo_from_ttft, t_cycle/k_accept/t_verify tables, EMA update).
 extern "C" int mspq_governor(const char* request_json, char** out_json) {

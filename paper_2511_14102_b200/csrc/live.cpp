@@ -163,6 +163,8 @@ struct mspq_engine {
   HostCfg cfg;
   std::vector<int> caps;
   double pcie_bw_measured = 0.0, draft_step_s = 0.0, home_bw_measured = 0.0;
+  std::pair<double, double> pcie_fixed{0.0, -1.0};             // (init latency, per-copy overhead) s
+  std::vector<std::pair<double, double>> verify_measured;       // (window, s) timed verify passes
   std::vector<std::pair<double, double>> verify_fit;
   int cycle_serial = 0;
   // "elb" estimator state: per (layer, expert) routing frequency from the draft's
@@ -620,6 +622,118 @@ void capture_draft_graph(mspq_engine* E) {
   E->graph_nodes = (int)nn;
 }
 
+// PCIe fixed costs (perfmodel.hpp:15-30 T_pcie,init and T_pcie,overhead), measured on the copy
+// stream: init = one 4 KB pinned H2D copy from idle (the first byte's latency); overhead = the
+// per-copy constant of t(n) = overhead + n / B fitted on 8 MB and 32 MB copies
+std::pair<double, double> measure_pcie_fixed(mspq_engine* E) {
+  const size_t n1 = 8u << 20, n2 = 32u << 20;
+  void* dbuf;
+  CUDA_OK(cudaMalloc(&dbuf, n2));
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  auto timed = [&](size_t n, int reps) {
+    CUDA_OK(cudaMemcpyAsync(dbuf, E->host, n, cudaMemcpyHostToDevice, E->sx));  // warm
+    CUDA_OK(cudaStreamSynchronize(E->sx));
+    double best = 1e30;
+    for (int r = 0; r < reps; ++r) {
+      cudaEventRecord(a, E->sx);
+      CUDA_OK(cudaMemcpyAsync(dbuf, E->host, n, cudaMemcpyHostToDevice, E->sx));
+      cudaEventRecord(b, E->sx);
+      CUDA_OK(cudaEventSynchronize(b));
+      best = std::min(best, elapsed_s(a, b));
+    }
+    return best;
+  };
+  const double t0 = timed(4096, 8), t1 = timed(n1, 4), t2 = timed(n2, 4);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(dbuf);
+  const double over = std::max(0.0, (t1 * (double)n2 - t2 * (double)n1) / (double)(n2 - n1));
+  return {t0, over};
+}
+
+// Verify samples (perfmodel.hpp:26 t_verify(window)), MEASURED: for window w in {1, 5, 9, 17} (<= Tmax),
+// one full target pass over w tokens with u = round(E (1 - (1 - K/E)^w)) distinct experts per layer
+// resident (the expected union) -- embed, per layer [attention] + K1 + schedule + K3 grouped GEMM
+// (+ the final norm and LM head), exactly the kernels a verify runs, on the compute stream, no
+// copies.  The experts are the first u slot-pool buffers (timing does not depend on their values).
+std::vector<std::pair<double, double>> measure_verify(mspq_engine* E) {
+  const auto& m = E->m;
+  const int L = m.L, K = m.K, Ex = m.E, d = m.d;
+  std::vector<std::pair<double, double>> out;
+  std::vector<int32_t> gb(Ex), ids;
+  for (int e = 0; e < Ex; ++e) gb[e] = e < E->nbuf ? e : E->nbuf - 1;
+  int32_t* dgb;
+  int32_t* dids;
+  CUDA_OK(cudaMalloc(&dgb, Ex * 4));
+  CUDA_OK(cudaMalloc(&dids, (size_t)E->Tmax * K * 4));
+  CUDA_OK(cudaMemcpy(dgb, gb.data(), Ex * 4, cudaMemcpyHostToDevice));
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  for (int w : {1, 5, 9, 17}) {
+    if (w > E->Tmax) break;
+    const int u = std::max(K, std::min(Ex, (int)std::lround((double)Ex * (1.0 - std::pow(1.0 - (double)K / Ex, w)))));
+    ids.assign((size_t)w * K, 0);
+    for (int t = 0; t < w; ++t)
+      for (int j = 0; j < K; ++j) ids[(size_t)t * K + j] = (t * K + j) % u;  // distinct within a token (K <= u)
+    for (int s2 = 0; s2 < w; ++s2) {
+      E->hpin[s2] = s2 % m.V;
+      E->hpin[E->Tmax + 1 + s2] = s2;
+    }
+    CUDA_OK(cudaMemcpyAsync(dids, ids.data(), ids.size() * 4, cudaMemcpyHostToDevice, E->sc));
+    CUDA_OK(cudaMemcpyAsync(E->win_tok(), E->hpin, w * 4, cudaMemcpyHostToDevice, E->sc));
+    CUDA_OK(cudaMemcpyAsync(E->win_pos(), E->hpin + E->Tmax + 1, w * 4, cudaMemcpyHostToDevice, E->sc));
+    double best = 1e30;
+    for (int rep = 0; rep < 3; ++rep) {
+      CUDA_OK(cudaEventRecord(a, E->sc));
+      CAPI_OK(mspq_embed(E->embed, E->pos, E->win_tok(), E->win_pos(), w, d, E->h, E->sc));
+      int ysp = 1;
+      for (int l = 0; l < L; ++l) {
+        const float* y = l ? E->yv[(l - 1) & 1] : nullptr;
+        const int32_t* eo = l ? E->sv[(l - 1) & 1].entry_of : nullptr;
+        const float* pw = l ? E->wts_t : nullptr;
+        long long yst = (long long)w * K * d;
+        if (E->attn) {
+          ysp = enqueue_attn(E, l, w, E->win_pos(), y, eo, pw, ysp, yst, nullptr, E->sc);
+          y = E->oproj;
+          eo = nullptr;
+          pw = nullptr;
+          yst = (long long)w * d;
+        }
+        CAPI_OK(mspq_gate_topk(E->h, y, eo, pw, ysp, yst, E->gamma + (size_t)l * d, E->router + (size_t)l * Ex * d,
+                               E->xn, E->ids_t, E->wts_t, nullptr, nullptr, nullptr, nullptr, nullptr, l, L, w, d, Ex,
+                               K, m.eps, E->sc));
+        Sched& sv = E->sv[l & 1];
+        CAPI_OK(mspq_build_schedule(dids, w, K, Ex, dgb, sv.n_groups, sv.group_expert, sv.group_buf, sv.group_off,
+                                    sv.entry_tok, sv.entry_of, sv.entry_group, E->sc));
+        const int units = std::max(1, u * (2 * m.f / 128));
+        const int sp1 = std::max(1, std::min({(296 + units - 1) / units, mspq_engine::kMaxSplit, d / 64}));
+        const int units2 = std::max(1, u * (d / 128));
+        const int sp2 = std::max(1, std::min({(296 + units2 - 1) / units2, mspq_engine::kMaxSplit, m.f / 64}));
+        CAPI_OK(mspq_moe_bf16_tc(sv.n_groups, sv.group_expert, sv.group_buf, sv.group_off, sv.entry_tok,
+                                 sv.entry_group, E->xn, E->pool, E->S16, d, m.f, w, K, E->G, sp1, sp2, E->tcws,
+                                 E->yv[l & 1], E->sc));
+        ysp = sp2;
+      }
+      CAPI_OK(mspq_gate_topk(E->h, E->yv[(L - 1) & 1], E->sv[(L - 1) & 1].entry_of, E->wts_t, ysp,
+                             (long long)w * K * d, E->gfinal, nullptr, E->xn, nullptr, nullptr, nullptr, nullptr,
+                             nullptr, nullptr, nullptr, L, L, w, d, Ex, K, m.eps, E->sc));
+      CAPI_OK(mspq_lm_head(E->xn, E->lm, w, m.V, d, E->logits, E->sc));
+      CUDA_OK(cudaEventRecord(b, E->sc));
+      CUDA_OK(cudaEventSynchronize(b));
+      best = std::min(best, elapsed_s(a, b));
+    }
+    out.push_back({(double)w, best});
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(dgb);
+  cudaFree(dids);
+  return out;
+}
+
 double measure_pcie(mspq_engine* E) {
   const size_t bytes = std::min<size_t>(E->S16, 64u << 20);
   void* dbuf;
@@ -721,27 +835,24 @@ static void configure(mspq_engine* E, const std::string& text) {
     cudaEventDestroy(a);
     cudaEventDestroy(b);
   }
+  if (E->pcie_fixed.second < 0.0) E->pcie_fixed = measure_pcie_fixed(E);
+  if (E->verify_measured.empty()) E->verify_measured = measure_verify(E);
   if (!c.profile_given) {
     Profile p;
     p.pcie_bandwidth = E->home ? E->home_bw_measured : E->pcie_bw_measured;
-    p.pcie_init_latency = 0.0;
-    p.pcie_overhead = 10e-6;
+    p.pcie_init_latency = E->home ? 0.0 : E->pcie_fixed.first;
+    p.pcie_overhead = E->home ? 0.0 : E->pcie_fixed.second;
     // bytes one fetch puts on the link: the mean XC blob with the codec (raw tiles from a home)
     p.expert_size_bytes = E->home ? (uint64_t)E->S16
                                   : E->codec ? (uint64_t)(E->xc_bytes_total / E->n_payload) : (uint64_t)E->S16;
     p.draft_base = 0.0;
     p.draft_per_token = E->draft_step_s;
-    // verify samples from the resident-expert roofline of this model on the measured peaks:
-    // per layer E[union(w)] bf16 experts + router, plus the LM head, at the draft's achieved
-    // bytes/s (the same kernels' streaming rate).
-    const double dense = (double)m.V * m.d * 2 + (double)m.L * m.E * m.d * 2 + (double)m.L * E->wattn_layer;
-    const double draft_bytes = (double)m.L * m.K * E->S4 + dense;
-    const double bw = draft_bytes / std::max(E->draft_step_s, 1e-6);
-    p.verify_samples.clear();
-    for (double w : {1.0, 5.0, 9.0, 17.0}) {
-      const double uni = (double)m.E * (1.0 - std::pow(1.0 - (double)m.K / m.E, w));
-      const double bytes = (double)m.L * uni * E->S16 + dense;
-      p.verify_samples.push_back({w, bytes / bw});
+    // verify samples: timed target passes with the expected per-layer expert union resident
+    p.verify_samples = E->verify_measured;
+    if (p.verify_samples.size() < 2) {  // kmax < 4: extend linearly from the measured point(s)
+      const double w0 = p.verify_samples.empty() ? 1.0 : p.verify_samples.back().first;
+      const double t0 = p.verify_samples.empty() ? E->draft_step_s : p.verify_samples.back().second;
+      p.verify_samples.push_back({w0 + 4.0, t0 * 1.5});
     }
     c.profile = p;
   }
@@ -928,6 +1039,9 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
   uint64_t h2d_bytes = 0, total_new = 0, layer_cov_count = 0, step_total = 0, acc_total = 0;
   const auto wall0 = std::chrono::steady_clock::now();
   int ci = 0;
+  // trace_level >= 1: the committed positions of the reference trace this run exports
+  // (to_reference_trace): target routing + the draft's routing of the same token
+  std::vector<std::vector<int>> an_target, an_draft;  // [pos][L*K]
   long k3_groups = 0, draft_steps = 0;
   double k3_time = 0.0, k3_bytes = 0.0, draft_time = 0.0;
   // verify layers of one window of T tokens (positions head .. head+T-1 in E->win_pos(), tokens
@@ -1399,6 +1513,19 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
         gates.push_back(gl);
       }
       rec["elb"] = elb;
+      {  // positions this cycle commits to the exported trace: slot 0 (cycle > 0), slots 1..accepted
+        const int acc_c = consumed - bonus;
+        for (int s2 = (ci > 0 ? 0 : 1); s2 <= acc_c; ++s2) {
+          std::vector<int> tg((size_t)L * K), dr((size_t)L * K);
+          for (int l = 0; l < L; ++l)
+            for (int j = 0; j < K; ++j) {
+              tg[(size_t)l * K + j] = hp[o_tr + ((size_t)l * T + s2) * K + j];
+              dr[(size_t)l * K + j] = s2 < k ? hp[o_e + ((size_t)s2 * L + l) * K + j] : tg[(size_t)l * K + j];
+            }
+          an_target.push_back(std::move(tg));
+          an_draft.push_back(std::move(dr));
+        }
+      }
       rec["elb_gates"] = gates;
       // per verify layer (s from the run start): controller done, GEMM start (after any wait on
       // in-flight copies), GEMM end, K1 (route) done
@@ -1492,6 +1619,62 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
     rep["peer_tier"] = pt;
   }
   rep["expert_codec"] = E->codec ? "xc" : "none";
+  if (!an_target.empty()) {
+    // draft -> target routing fidelity and per-layer routing entropy of the run
+    // (classify_fidelity / layer_entropy, trace.cpp:401-462, on the exported trace's positions)
+    auto cell = [&](size_t p, int l) {
+      std::vector<int> a(an_target[p].begin() + (size_t)l * K, an_target[p].begin() + (size_t)(l + 1) * K);
+      std::vector<int> b(an_draft[p].begin() + (size_t)l * K, an_draft[p].begin() + (size_t)(l + 1) * K);
+      if (a == b) return 0;
+      std::sort(a.begin(), a.end());
+      std::sort(b.begin(), b.end());
+      return a == b ? 1 : 2;
+    };
+    auto stats = [&](bool per_token) {
+      uint64_t cnt[3] = {0, 0, 0};
+      for (size_t p = 0; p < an_target.size(); ++p) {
+        if (!per_token) {
+          for (int l = 0; l < L; ++l) ++cnt[cell(p, l)];
+        } else {
+          int worst = 0;
+          for (int l = 0; l < L && worst < 2; ++l) worst = std::max(worst, cell(p, l));
+          ++cnt[worst];
+        }
+      }
+      const double n = static_cast<double>(cnt[0] + cnt[1] + cnt[2]);
+      json f;
+      f["hard_rate"] = static_cast<double>(cnt[0]) / n;
+      f["soft_rate"] = static_cast<double>(cnt[1]) / n;
+      f["mismatch_rate"] = 1.0 - static_cast<double>(cnt[0]) / n - static_cast<double>(cnt[1]) / n;
+      f["hard_count"] = cnt[0];
+      f["soft_count"] = cnt[1];
+      f["mismatch_count"] = cnt[2];
+      f["total"] = cnt[0] + cnt[1] + cnt[2];
+      return f;
+    };
+    json fid;
+    fid["token_layer"] = stats(false);
+    fid["token"] = stats(true);
+    rep["fidelity"] = fid;
+    json ent = json::array();
+    for (int l = 0; l < L; ++l) {
+      std::vector<uint64_t> cnt(Ex, 0);
+      uint64_t tot = 0;
+      for (auto& tg : an_target)
+        for (int j = 0; j < K; ++j) {
+          ++cnt[tg[(size_t)l * K + j]];
+          ++tot;
+        }
+      double h = 0.0;
+      for (uint64_t c2 : cnt) {
+        if (c2 == 0) continue;
+        const double pr = static_cast<double>(c2) / static_cast<double>(tot);
+        h -= pr * std::log2(pr);
+      }
+      ent.push_back(h);
+    }
+    rep["layer_entropy"] = ent;
+  }
   rep["wall_s"] = wall;
   rep["decode_wall_s"] = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall_dec0).count();
   if (!prefill.empty()) rep["prefill"] = prefill;
@@ -1719,6 +1902,11 @@ int mspq_engine_info(mspq_engine* E, char** out) {
     j["draft_resident_bytes"] = (uint64_t)m.L * m.E * E->S4;
     j["pcie_bw_measured"] = E->pcie_bw_measured;
     j["draft_step_s"] = E->draft_step_s;
+    j["pcie_init_latency_measured"] = E->pcie_fixed.first;
+    j["pcie_overhead_measured"] = E->pcie_fixed.second;
+    json vs = json::array();
+    for (auto& [w, t] : E->verify_measured) vs.push_back({w, t});
+    j["verify_samples_measured"] = vs;
     j["home_bytes"] = E->home_bytes;
     j["home_bw_measured"] = E->home_bw_measured;
     j["peer_group"] = E->peer_G;

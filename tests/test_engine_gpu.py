@@ -353,3 +353,48 @@ def test_live_collect_plans_and_sync_fetch(cuda):
         assert cyc["sync_fetch_s"] > 0 or cyc["sync_count"] == 0
         head += cyc["accepted"] + 1
     eng.close()
+
+
+def test_live_fidelity_and_entropy_equal_reference_on_exported_trace(cuda, ref):
+    """The live report's draft->target routing fidelity (both granularities) and per-layer
+    routing entropy equal the reference's classify_fidelity / layer_entropy (trace.cpp:401-462,
+    run from oracle/_ref) on the reference trace the same run exports (to_reference_trace)."""
+    import paper_2511_14102_b200 as m
+    eng, cfg = _engine()
+    eng.configure({"policy": "speculative", "cache_capacity": 3, "k": 4})
+    rep = eng.generate([3, 1, 4, 1, 5], 48)
+    eng.close()
+    want = ref.trace_analysis(m.to_reference_trace(rep, cfg))
+    assert rep["fidelity"] == want["fidelity"]
+    assert rep["layer_entropy"] == want["layer_entropy"]
+    assert 0.0 < rep["fidelity"]["token_layer"]["hard_rate"] <= 1.0
+
+
+def test_device_compare_policies_and_sweep_k_equal_reference(cuda, ref):
+    """compare_policies / sweep_k (sim.cpp:539-574) over the device control plane equal the
+    reference's rows on the same trace."""
+    import paper_2511_14102_b200 as m
+    tr = ref.generate_trace(4, 12, 2, 120, seed=3)
+    base = {"policy": "speculative", "cache_capacity": 4, "k": 4}
+    pols, caps = ["lru", "lookahead", "speculative"], [3, 6]
+    assert m.compare_policies(tr, base, pols, caps) == ref.compare_policies(tr, base, pols, caps)
+    assert m.sweep_k(tr, base, [1, 2, 5, 8]) == ref.sweep_k(tr, base, [1, 2, 5, 8])
+
+
+def test_hardware_profile_refit_is_measured(cuda):
+    """The B200 re-fit of HardwareProfile (perfmodel.hpp:15-30): PCIe bandwidth, init latency and
+    per-copy overhead from timed copies, draft time from the captured draft graph, and verify
+    samples from timed target passes at windows 1/5/9 with the expected expert union resident."""
+    eng, cfg = _engine()
+    eng.configure({"policy": "speculative", "cache_capacity": 3, "k": "governor",
+                   "governor": {"k_min": 1, "k_max": 8, "k_slo": 8}})
+    info = eng.info()
+    prof = info["profile"]
+    vs = info["verify_samples_measured"]
+    assert [w for w, _ in vs] == [1.0, 5.0, 9.0]  # kmax 8: windows up to 9
+    assert all(t > 0 for _, t in vs) and vs[-1][1] >= vs[0][1]
+    assert prof["verify_samples"] == vs
+    assert prof["pcie_init_latency_s"] == info["pcie_init_latency_measured"] > 0
+    assert prof["pcie_overhead_s"] == info["pcie_overhead_measured"] >= 0
+    assert prof["draft_per_token_s"] == info["draft_step_s"] > 0
+    eng.close()
