@@ -624,9 +624,10 @@ void capture_draft_graph(mspq_engine* E) {
 
 // PCIe fixed costs (perfmodel.hpp:15-30 T_pcie,init and T_pcie,overhead), measured on the copy
 // stream: init = one 4 KB pinned H2D copy from idle (the first byte's latency); overhead = the
-// per-copy constant of t(n) = overhead + n / B fitted on 8 MB and 32 MB copies
+// per-copy constant of t(n) = overhead + n / B fitted on two copy sizes (32 MB and 8 MB, or the
+// store's size and a quarter of it for small models)
 std::pair<double, double> measure_pcie_fixed(mspq_engine* E) {
-  const size_t n1 = 8u << 20, n2 = 32u << 20;
+  const size_t n2 = std::min<size_t>(32u << 20, E->host_bytes & ~(size_t)4095), n1 = n2 / 4;
   void* dbuf;
   CUDA_OK(cudaMalloc(&dbuf, n2));
   cudaEvent_t a, b;
