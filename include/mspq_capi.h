@@ -186,6 +186,17 @@ int mspq_dense_bf16_tc(const int32_t* dsched, const void* x, const void* w_tiled
 long long mspq_attention_ws_bytes(int T, int H, int Hkv, int Dh);
 int mspq_attention(const float* qkv, int splits, long long split_stride, int T, int H, int Hkv, int Dh, int P,
                    const int32_t* pos0, void* kc, void* vc, void* out, void* oimg, void* ws, void* stream);
+/* K2 for the draft's single token: INT4 expert GEMV on warp MMA (gemv_int4.cu).  blobs = L*E
+ * draft blobs in FRAGMENT-MAJOR order (mspq_fragtile_int4 for q, scales row-major: W13q | W13s |
+ * W2q | W2s with the mspq_int4_blob_bytes offsets); groups = the K experts of the token in the
+ * draft schedule (n_groups / group_expert, group g = entry g); act [K][f] bf16 scratch (SiLU(gate)
+ * * up of W13, fused); y [K][d] fp32 (one plane). */
+int mspq_moe_int4_gemv(const int32_t* n_groups, const int32_t* group_expert, const void* xn, const void* blobs,
+                       long long blob_bytes, int layer, int E, int d, int f, int K, void* act, float* y,
+                       void* stream);
+/* row-major quantised INT4 q[rows][cols/8] (standard nibble order) -> fragment-major words
+ * [rows/16][cols/64][32 lanes][4] for mspq_moe_int4_gemv (layout in gemv_int4.cu) */
+int mspq_fragtile_int4(const void* q, int rows, int cols, void* fq, void* stream);
 /* row-major quantised INT4 (q[rows][cols/8] u32, standard nibble order; s[rows][cols/128] bf16)
  * -> tile-major [rows/128][cols/64][128][8] u32 + [rows/128][cols/128][128] bf16 */
 int mspq_tile_int4(const void* q, const void* s, int rows, int cols, void* tq, void* ts, void* stream);

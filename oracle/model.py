@@ -480,9 +480,9 @@ def forward_batch(model: Model, toks, poss, draft: bool, h_in=None, h_trace=None
     return [(int(am[i]), routing[i]) for i in range(M)]
 
 
-def prefill(model: Model, prompt, chunk=17):
+def prefill(model: Model, prompt, chunk=32):
     """The engine's prefill (live.cpp): the target runs the prompt's tokens 0..n-2 (their KV rows)
-    in windows of up to `chunk` = kmax + 1 tokens.  Returns the windows' target routing
+    in windows of up to `chunk` tokens (32, the engine's prefill window).  Returns the windows' target routing
     [[slot][layer] (ids, wts)] per window (for the control-plane replay)."""
     out = []
     n = len(prompt) - 1
@@ -541,7 +541,7 @@ def check_layers(model: Model, h_caps, ids, draft: bool, tol=2e-3, h_mids=None, 
     return worst, margins
 
 
-def speculative_decode(model: Model, last_token: int, start_pos: int, ks, max_new: int, prompt=None, chunk=17,
+def speculative_decode(model: Model, last_token: int, start_pos: int, ks, max_new: int, prompt=None, chunk=32,
                        deadline=None, prefilled=False):
     """Greedy speculative decoding with the INT4 draft: each cycle drafts k
     tokens from the head (previous bonus), verifies the k+1-slot window with the bf16 target

@@ -15,7 +15,7 @@ JSON_DIR = "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_front
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I" + CSRC,
           "-I" + os.path.join(ROOT, "include"), "-I" + JSON_DIR]
-SOURCES = ["kernels_model.cu", "umma.cu", "attention.cu", "ctl.cu", "xcodec.cu", "capi.cu", "engine.cpp", "live.cpp"]
+SOURCES = ["kernels_model.cu", "umma.cu", "attention.cu", "gemv_int4.cu", "ctl.cu", "xcodec.cu", "capi.cu", "engine.cpp", "live.cpp"]
 
 
 def _needs(src, obj, deps):

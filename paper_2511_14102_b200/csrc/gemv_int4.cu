@@ -1,0 +1,198 @@
+// K2 for the draft step (T = 1): INT4 expert GEMV on warp-level MMA (mma.sync m16n8k16, f16 in,
+// f32 accumulate) with the weights in FRAGMENT-MAJOR order, so one 16-byte load per lane is four
+// ready-made A fragments after one LOP3 per two weights.
+//
+// Why not tcgen05 here: a single token is an N = 1 GEMM; the UMMA path (k_umma_int4p) pads it to
+// N = 16 and moves every 8 KB weight group through smem -> TMEM A-slot -> MMA -> commit hand-offs,
+// which capped it at ~1.4 TB/s (~0.2 of HBM, profiles/r01).  Here the weight bytes go straight
+// from global memory into registers; the warp MMA does the dot products (its throughput is ~5x
+// what one token needs) and the kernel is bound by the bytes in flight.
+//
+// Layout (mspq_fragtile_int4): W [R][C] -> q[R/16][C/64][32 lanes][4 words].  Word v of lane l
+// covers k16-block kb = 4 * chunk + v, rows r0 = 16 rt + l/4, r1 = r0 + 8, columns c = 16 kb +
+// 2 (l%4) + {0, 1} ("class 1") and c + 8 + {0, 1} ("class 16"):
+//   bits  0 / 16: W[r0][c], W[r0][c+1]      bits  8 / 24: W[r1][c], W[r1][c+1]
+//   bits  4 / 20: W[r0][c+8], W[r0][c+9]    bits 12 / 28: W[r1][c+8], W[r1][c+9]
+// so (w & 0x000F000F) | 0x64006400 is the fp16 pair (1024 + q) for (a0, a1) and
+// (w & 0x00F000F0) | 0x64006400 the pair (1024 + 16 q) for (a4, a5); w >> 8 gives rows r1.  The
+// B fragment holds x for class-1 columns and x / 16 for class-16 ones, so D = sum_k (q_k - 8) x_k
+// + C, C = sum_k c_k b_k (c = 1032 | 1152), the same exact-product scheme as the tcgen05 K2
+// (DESIGN.md §5); the per-128-column bf16 scale is applied in fp32 per group.  Scales stay
+// row-major [R][C/128].
+#include "common.cuh"
+#include "kernels.h"
+
+namespace mspq {
+namespace {
+
+constexpr int GV_WARPS = 8, GV_THREADS = 32 * GV_WARPS, GV_TILES = 2;  // 2 row tiles = 32 rows per CTA
+
+MSPQ_D void mma16816(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+MSPQ_D uint32_t lop_magic(uint32_t w, uint32_t mask) {
+  uint32_t o;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(o) : "r"(w), "r"(mask), "r"(0x64006400u));  // (w & mask) | magic
+  return o;
+}
+MSPQ_D uint4 ldg_stream(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+// grid (R / 32, groups): CTA = 32 rows of one group's expert matrix, 8 warps split the 128-column
+// scale groups (warp w takes groups w, w + 8, ...), partial rows reduced in warp order.
+__global__ void __launch_bounds__(GV_THREADS) k_int4_gemv(GemvArgs a) {
+  pdl_enter();  // launched with launch_pdl (kernels.h)
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int g = blockIdx.y;
+  if (g >= *a.n_groups) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kdim = a.kdim, ngr = kdim / 128, nchunk = kdim / 64;
+  uint16_t* xh = reinterpret_cast<uint16_t*>(smem_raw);            // [kdim] class-scaled fp16
+  float* cg = reinterpret_cast<float*>(smem_raw + kdim * 2);        // [ngr] corrections
+  float* red = cg + ngr;                                            // [GV_WARPS][32] row partials
+  const uint16_t* x = a.x + (a.x_per_group ? (int64_t)g * kdim : 0);
+  for (int k = tid; k < kdim; k += GV_THREADS) {
+    const float v = bf2f(x[k]) * ((k & 15) >= 8 ? 0.0625f : 1.0f);
+    const __half h = __float2half_rn(v);
+    xh[k] = *reinterpret_cast<const uint16_t*>(&h);
+  }
+  __syncthreads();
+  for (int gq = tid; gq < ngr; gq += GV_THREADS) {  // C_g = sum_k c_k b_k, fixed order
+    float c = 0.0f;
+    for (int k = 128 * gq; k < 128 * gq + 128; ++k) {
+      const float b = __half2float(*reinterpret_cast<const __half*>(&xh[k]));
+      c = fmaf((k & 15) >= 8 ? 1152.0f : 1032.0f, b, c);
+    }
+    cg[gq] = c;
+  }
+  __syncthreads();
+  const int expert = a.group_expert[g];
+  const unsigned char* blob = a.blobs + ((int64_t)a.layer * a.E + expert) * a.blob_bytes;
+  const uint4* q = reinterpret_cast<const uint4*>(blob + a.q_off);
+  const uint16_t* sc = reinterpret_cast<const uint16_t*>(blob + a.s_off);
+  const int rt0 = blockIdx.x * GV_TILES;
+  const int gi = lane >> 2, ti = lane & 3;
+  float acc[GV_TILES][2];
+#pragma unroll
+  for (int i = 0; i < GV_TILES; ++i) acc[i][0] = acc[i][1] = 0.0f;
+  // register double buffer: the next scale group's 2 tiles x 2 chunks are in flight while the
+  // current one is multiplied
+  uint4 cur[GV_TILES][2], nxt[GV_TILES][2];
+  auto load = [&](int gq, uint4 (&dst)[GV_TILES][2]) {
+#pragma unroll
+    for (int i = 0; i < GV_TILES; ++i)
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+        dst[i][c] = ldg_stream(q + (((int64_t)(rt0 + i) * nchunk + 2 * gq + c) * 32 + lane));
+  };
+  int gq = warp;
+  if (gq < ngr) load(gq, cur);
+  for (; gq < ngr; gq += GV_WARPS) {
+    const bool more = gq + GV_WARPS < ngr;
+    if (more) load(gq + GV_WARPS, nxt);
+    float d[GV_TILES][4];
+#pragma unroll
+    for (int i = 0; i < GV_TILES; ++i) d[i][0] = d[i][1] = d[i][2] = d[i][3] = 0.0f;
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int kb = 8 * gq + 4 * c + v;  // k16 block
+        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&xh[16 * kb + 2 * ti]);
+        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(&xh[16 * kb + 8 + 2 * ti]);
+#pragma unroll
+        for (int i = 0; i < GV_TILES; ++i) {
+          const uint32_t w = v == 0 ? cur[i][c].x : v == 1 ? cur[i][c].y : v == 2 ? cur[i][c].z : cur[i][c].w;
+          const uint32_t w8 = w >> 8;
+          uint32_t af[4];
+          af[0] = lop_magic(w, 0x000F000Fu);   // (r0, c..c+1)     1024 + q
+          af[1] = lop_magic(w8, 0x000F000Fu);  // (r1, c..c+1)
+          af[2] = lop_magic(w, 0x00F000F0u);   // (r0, c+8..c+9)   1024 + 16 q
+          af[3] = lop_magic(w8, 0x00F000F0u);  // (r1, c+8..c+9)
+          mma16816(d[i], af, b0, b1);
+        }
+      }
+    const float cgq = cg[gq];
+#pragma unroll
+    for (int i = 0; i < GV_TILES; ++i) {
+      const int r0 = 16 * (rt0 + i) + gi;
+      const float s0 = bf2f(sc[(int64_t)r0 * ngr + gq]), s1 = bf2f(sc[(int64_t)(r0 + 8) * ngr + gq]);
+      acc[i][0] = fmaf(s0, __fsub_rn(d[i][0], cgq), acc[i][0]);  // every B column is x: column 2 ti == column 0
+      acc[i][1] = fmaf(s1, __fsub_rn(d[i][2], cgq), acc[i][1]);
+    }
+    if (more) {
+#pragma unroll
+      for (int i = 0; i < GV_TILES; ++i) {
+        cur[i][0] = nxt[i][0];
+        cur[i][1] = nxt[i][1];
+      }
+    }
+  }
+  if (ti == 0) {
+#pragma unroll
+    for (int i = 0; i < GV_TILES; ++i) {
+      red[warp * 32 + 16 * i + gi] = acc[i][0];
+      red[warp * 32 + 16 * i + gi + 8] = acc[i][1];
+    }
+  }
+  __syncthreads();
+  if (tid < 32) {
+    float v = 0.0f;
+#pragma unroll
+    for (int w = 0; w < GV_WARPS; ++w) v = __fadd_rn(v, red[w * 32 + tid]);
+    const int row = 32 * blockIdx.x + tid;
+    if (a.act) {
+      // W13 rows 2i / 2i+1 = gate_i / up_i (adjacent lanes): act = bf16(silu(gate) * up)
+      const float up = __shfl_down_sync(0xffffffffu, v, 1);
+      if ((tid & 1) == 0) a.act[(int64_t)g * (a.rows / 2) + row / 2] = f2bf(__fmul_rn(silu_det(v), up));
+    } else {
+      a.y[(int64_t)g * a.rows + row] = v;
+    }
+  }
+}
+
+// row-major quantised INT4 (standard nibble order) -> fragment-major words (header comment)
+__global__ void k_fragtile_int4(const uint32_t* __restrict__ q, int rows, int cols, uint32_t* __restrict__ fq) {
+  const int wpr = cols / 8, nchunk = cols / 64;
+  const int64_t n = (int64_t)rows * wpr;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int v = (int)(i & 3), lane = (int)((i >> 2) & 31);
+    const int64_t rest = i >> 7;
+    const int chunk = (int)(rest % nchunk);
+    const int64_t rt = rest / nchunk;
+    const int r0 = (int)(16 * rt + (lane >> 2)), r1 = r0 + 8;
+    const int c = 16 * (4 * chunk + v) + 2 * (lane & 3);
+    auto nib = [&](int r, int col) { return (q[(int64_t)r * wpr + (col >> 3)] >> (4 * (col & 7))) & 0xFu; };
+    fq[i] = nib(r0, c) | (nib(r0, c + 1) << 16) | (nib(r1, c) << 8) | (nib(r1, c + 1) << 24) | (nib(r0, c + 8) << 4) |
+            (nib(r0, c + 9) << 20) | (nib(r1, c + 8) << 12) | (nib(r1, c + 9) << 28);
+  }
+}
+
+}  // namespace
+
+size_t gemv_smem_bytes(int kdim) { return (size_t)kdim * 2 + (size_t)(kdim / 128) * 4 + GV_WARPS * 32 * 4 + 16; }
+
+cudaError_t launch_int4_gemv(const GemvArgs& a, int max_groups, cudaStream_t st) {
+  const size_t smem = gemv_smem_bytes(a.kdim);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_int4_gemv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  return launch_pdl(k_int4_gemv, dim3(a.rows / 32, max_groups), dim3(GV_THREADS), smem, st, a);
+}
+
+cudaError_t launch_fragtile_int4(const uint32_t* q, int rows, int cols, uint32_t* fq, cudaStream_t st) {
+  k_fragtile_int4<<<148 * 4, 256, 0, st>>>(q, rows, cols, fq);
+  return cudaGetLastError();
+}
+
+}  // namespace mspq

@@ -142,6 +142,23 @@ size_t attn_smem_bytes(int T, int H, int Hkv, int Dh, int P);
 size_t attn_part_floats(int T, int H, int Hkv, int Dh);
 cudaError_t launch_attn_window(const AttnArgs& a, cudaStream_t st);
 
+// K2 for one token: INT4 expert GEMV on warp MMA over fragment-major weights (gemv_int4.cu)
+struct GemvArgs {
+  const unsigned char* blobs;  // all L*E draft blobs (fragment-major q, row-major scales)
+  int64_t blob_bytes;
+  int64_t q_off, s_off;        // the matrix's q words and scales inside a blob
+  int rows, kdim;
+  int layer, E;
+  const int32_t* n_groups;     // the draft schedule: group g = expert group_expert[g] = entry g
+  const int32_t* group_expert;
+  const uint16_t* x;           // bf16 input rows
+  int x_per_group;             // 0: one row for every group (W13), 1: row g (W2 on the act rows)
+  float* y;                    // W2: [groups][rows] fp32
+  uint16_t* act;               // W13: [groups][rows/2] bf16 SiLU(gate) * up
+};
+cudaError_t launch_int4_gemv(const GemvArgs& a, int max_groups, cudaStream_t st);
+cudaError_t launch_fragtile_int4(const uint32_t* q, int rows, int cols, uint32_t* fq, cudaStream_t st);
+
 cudaError_t launch_umma_grouped(const UmmaArgs& a, int max_groups, int BN, cudaStream_t st);
 cudaError_t launch_umma_int4(const UmmaArgs& a, int max_groups, int BN, cudaStream_t st);
 cudaError_t launch_umma_int4p(const UmmaArgs& a, int max_groups, cudaStream_t st);

@@ -138,6 +138,7 @@ struct mspq_engine {
   void* tcws_d = nullptr;
   static constexpr int kMaxSplit = 8;
   uint16_t* act = nullptr;
+  uint16_t* act_d = nullptr;  // draft GEMV: [K][f] SiLU(gate) * up
   float* logits = nullptr;
   int32_t* amax = nullptr;
   int32_t* gbuf = nullptr;  // [E] first-request buffer per expert of the current verify layer
@@ -373,9 +374,13 @@ void make_experts(mspq_engine* E) {
     CAPI_OK(mspq_quantize_int4(st, 2 * m.f, m.d, rq, rq + q13, E->sc));
     CAPI_OK(mspq_quantize_int4(st + (size_t)2 * m.f * m.d * 2, m.d, m.f, rq + q13 + s13, rq + q13 + s13 + q2, E->sc));
     for (int key = p; key < LE; key += E->n_payload) {
+      // draft blob for the T = 1 GEMV (gemv_int4.cu): fragment-major q words, row-major scales
       unsigned char* b4 = E->draft4 + (size_t)key * S4;
-      CAPI_OK(mspq_tile_int4(rq, rq + q13, 2 * m.f, m.d, b4, b4 + q13, E->sc));
-      CAPI_OK(mspq_tile_int4(rq + q13 + s13, rq + q13 + s13 + q2, m.d, m.f, b4 + q13 + s13, b4 + q13 + s13 + q2, E->sc));
+      CAPI_OK(mspq_fragtile_int4(rq, 2 * m.f, m.d, b4, E->sc));
+      CUDA_OK(cudaMemcpyAsync(b4 + q13, rq + q13, (size_t)s13, cudaMemcpyDeviceToDevice, E->sc));
+      CAPI_OK(mspq_fragtile_int4(rq + q13 + s13, m.d, m.f, b4 + q13 + s13, E->sc));
+      CUDA_OK(cudaMemcpyAsync(b4 + q13 + s13 + q2, rq + q13 + s13 + q2, (size_t)(S4 - q13 - s13 - q2),
+                              cudaMemcpyDeviceToDevice, E->sc));
     }
     if (fill_host) {
       // host store keeps the tile-major SW128 images K3 streams with one bulk copy per tile
@@ -464,6 +469,7 @@ void make_workspaces(mspq_engine* E) {
                  (size_t)L * m.E + 64;
   CUDA_OK(cudaHostAlloc((void**)&E->hpin, E->hpin_ints * 4, 0));
   CUDA_OK(cudaMalloc(&E->sched_cap, (size_t)L * sched_ints * 4));
+  CUDA_OK(cudaMalloc(&E->act_d, (size_t)K * f * 2));
   if (E->attn) {
     const int KS = mspq_engine::kMaxSplit;
     CUDA_OK(cudaMalloc(&E->qkv, (size_t)KS * T * E->Nqkv * 4));
@@ -532,8 +538,8 @@ int enqueue_attn(mspq_engine* E, int l, int T, const int32_t* pos0, const float*
 void enqueue_draft_step(mspq_engine* E, cudaStream_t s) {
   const auto& m = E->m;
   const int K = m.K, L = m.L, d = m.d;
-  E->yd_split1 = split_for(K * (2 * m.f / 128), d / 64);
-  E->yd_split2 = split_for(K * (d / 128), m.f / 64);
+  E->yd_split1 = 1;  // the draft GEMV writes one plane per expert (no K splits)
+  E->yd_split2 = 1;
   int32_t* row = E->dst + 0;
   int32_t* cur_tok = E->dst + 1;
   int32_t* cur_pos = E->dst + 2;
@@ -562,9 +568,8 @@ void enqueue_draft_step(mspq_engine* E, cudaStream_t s) {
     else if (E->hcap_dstage && !E->attn)
       CUDA_OK(cudaMemcpyAsync(E->hcap_dstage + (size_t)l * d, E->h, (size_t)d * 4, cudaMemcpyDeviceToDevice, s));
     Sched& sc = E->sd[l & 1];
-    CAPI_OK(mspq_moe_int4_tc(sc.n_groups, sc.group_expert, sc.group_buf, sc.group_off, sc.entry_tok, sc.entry_group,
-                             E->xn, E->draft4, E->S4, l, m.E, d, m.f, 1, K, K, E->yd_split1, E->yd_split2, E->tcws_d,
-                             E->yd[l & 1], s));
+    CAPI_OK(mspq_moe_int4_gemv(sc.n_groups, sc.group_expert, E->xn, E->draft4, E->S4, l, m.E, d, m.f, K, E->act_d,
+                               E->yd[l & 1], s));
   }
   const int pl = (L - 1) & 1;
   CAPI_OK(mspq_gate_topk(E->h, E->yd[pl], E->sd[pl].entry_of, E->wts_d + (size_t)(L - 1) * K, E->yd_split2,
@@ -654,7 +659,7 @@ std::pair<double, double> measure_pcie_fixed(mspq_engine* E) {
   return {t0, over};
 }
 
-// Verify samples (perfmodel.hpp:26 t_verify(window)), MEASURED: for window w in {1, 5, 9, 17} (<= Tmax),
+// Verify samples (perfmodel.hpp:26 t_verify(window)), MEASURED: for window w in {1, 5, 9, 17} (<= kmax+1),
 // one full target pass over w tokens with u = round(E (1 - (1 - K/E)^w)) distinct experts per layer
 // resident (the expected union) -- embed, per layer [attention] + K1 + schedule + K3 grouped GEMM
 // (+ the final norm and LM head), exactly the kernels a verify runs, on the compute stream, no
@@ -674,7 +679,7 @@ std::vector<std::pair<double, double>> measure_verify(mspq_engine* E) {
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   for (int w : {1, 5, 9, 17}) {
-    if (w > E->Tmax) break;
+    if (w > E->o.kmax + 1) break;  // decode windows are k + 1 <= kmax + 1
     const int u = std::max(K, std::min(Ex, (int)std::lround((double)Ex * (1.0 - std::pow(1.0 - (double)K / Ex, w)))));
     ids.assign((size_t)w * K, 0);
     for (int t = 0; t < w; ++t)
@@ -776,7 +781,7 @@ static void configure(mspq_engine* E, const std::string& text) {
     E->cache = nullptr;
     CUDA_OK(cudaMalloc(&E->pool, (size_t)nbuf * E->S16));
     E->nbuf = nbuf;
-    CAPI_OK(mspq_cache_create(m.L, m.E, m.K, E->o.kmax, nbuf, E->o.log_cap, &E->cache));
+    CAPI_OK(mspq_cache_create(m.L, m.E, m.K, E->Tmax - 1, nbuf, E->o.log_cap, &E->cache));
     CAPI_OK(mspq_cache_view_get(E->cache, &E->view));
     for (auto ev : E->ev_ready) cudaEventDestroy(ev);
     E->ev_ready.assign(nbuf, nullptr);
@@ -1737,6 +1742,7 @@ void destroy(mspq_engine* E) {
   for (float* p : {E->hcap_v, E->hcap_dstage, E->hcap_d})
     if (p) cudaFree(p);
   if (E->sched_cap) cudaFree(E->sched_cap);
+  if (E->act_d) cudaFree(E->act_d);
   for (void* p : {(void*)E->wattn, (void*)E->gamma_a, (void*)E->kcache, (void*)E->vcache, (void*)E->qkv, (void*)E->oproj,
                   (void*)E->ao, (void*)E->dsched, E->dws, (void*)E->attn_part, (void*)E->hmid_v, (void*)E->hmid_dstage, (void*)E->hmid_d})
     if (p) cudaFree(p);
@@ -1823,7 +1829,9 @@ int mspq_engine_create(const mspq_model_desc* md, const mspq_engine_opts* op, ms
         }
       }
       E->S4 = mspq_int4_blob_bytes(m.d, m.f);
-      E->Tmax = op->kmax + 1;
+      // window capacity: the decode's k+1 slots, and 32-token prefill windows with attention (the
+      // widest K3 / K1 / attention launch; fewer prefill windows = fewer expert re-fetches)
+      E->Tmax = std::max(op->kmax + 1, m.H > 0 ? 32 : 0);
       E->n_payload = m.unique_experts > 0 ? std::min(m.unique_experts, m.L * m.E) : m.L * m.E;
       if (m.H > 0) {
         if (m.Hkv < 1 || m.H % m.Hkv || m.H / m.Hkv > 8 || (m.Dh != 64 && m.Dh != 128) || (m.H * m.Dh) % 128 ||

@@ -374,3 +374,47 @@ def test_dense_projection_vs_fp64_reference(cuda):
     want = om.bf16_to_f32(x).astype(np.float64) @ om.bf16_to_f32(w).astype(np.float64).T
     assert np.abs(got - want).max() <= 1e-4 * np.abs(want).max()
     del ops
+
+
+@pytest.mark.parametrize("name,E,K,d,f", SHAPES)
+def test_moe_int4_gemv_draft_within_tolerance(cuda, name, E, K, d, f):
+    """The draft's K2 for one token (mspq_moe_int4_gemv: warp-MMA GEMV over fragment-major INT4,
+    gemv_int4.cu) vs the oracle's dequantised INT4 FFN, every expert of the token; the fused
+    SiLU*up act rows match the oracle's bf16 activation to one bf16 ulp."""
+    from paper_2511_14102_b200 import ops
+    from paper_2511_14102_b200._lib import check, lib
+    desc = om.ModelDesc(L=2, E=E, K=K, d=d, f=f, V=512, seed=29)
+    mdl = om.Model(desc)
+    layer = 1
+    rng = np.random.default_rng(E + d)
+    ids = np.sort(rng.choice(E, K, replace=False)).astype(np.int32)
+    xn = om.f32_to_bf16(rng.standard_normal(d).astype(np.float32))
+    s4 = ops.int4_blob_bytes(d, f)
+    q13b, s13b, q2b = 2 * f * d // 2, 2 * f * (d // 128) * 2, d * f // 2
+    blobs = torch.zeros(2 * E * s4, dtype=torch.uint8, device="cuda")
+    for e in ids.tolist():
+        b = ops.fill_expert(desc.seed, layer, e, d, f, desc.a_up(), desc.a_down())
+        q13, s13 = ops.quantize_int4(b[:2 * f * d], 2 * f, d)
+        q2, s2 = ops.quantize_int4(b[2 * f * d:], d, f)
+        f13, f2 = torch.empty_like(q13), torch.empty_like(q2)
+        check(lib().mspq_fragtile_int4(_ptr(q13), 2 * f, d, _ptr(f13), None))
+        check(lib().mspq_fragtile_int4(_ptr(q2), d, f, _ptr(f2), None))
+        o = (layer * E + e) * s4
+        blobs[o:o + s4] = torch.cat([f13.view(torch.uint8), s13.view(torch.uint8), f2.view(torch.uint8),
+                                     s2.view(torch.uint8)])
+        assert q13b + s13b + q2b + s2.numel() * 2 == s4
+    n_groups = torch.tensor([K], dtype=torch.int32, device="cuda")
+    gexp = torch.from_numpy(ids).cuda()
+    act = torch.zeros(K * f, dtype=torch.int16, device="cuda")
+    y = torch.zeros(K * d, dtype=torch.float32, device="cuda")
+    check(lib().mspq_moe_int4_gemv(_ptr(n_groups), _ptr(gexp), _ptr(to_dev(xn)), _ptr(blobs), s4, layer, E, d, f, K,
+                                   _ptr(act), _ptr(y), None))
+    torch.cuda.synchronize()
+    y = y.cpu().numpy().reshape(K, d)
+    act = om.bf16_to_f32(i16_to_u16(act).reshape(K, f))
+    for g, e in enumerate(ids.tolist()):
+        want, a_want = mdl.ffn(xn, layer, e, draft=True)
+        tol = 2e-3 * np.abs(want).max() + 1e-5
+        assert np.abs(y[g] - want).max() <= tol, (g, np.abs(y[g] - want).max(), tol)
+        aw = om.bf16_to_f32(a_want)
+        assert np.all(np.abs(act[g] - aw) <= 2 ** -7 * np.abs(aw) + 1e-6), g
