@@ -53,20 +53,20 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_partial(AttnArgs a) {
   __shared__ float hmax[AT_MAXG], hsum[AT_MAXG];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   float* part = a.part + (((size_t)t * a.Hkv + g) * AT_SPLITS + sp) * (size_t)G * (Dh + 2);
-  // (1) in-window k/v of tokens 0..t (split planes summed in order, rounded to bf16 like the cache)
-  const bool need_win = j1 > p0 || sp == 0;
-  if (need_win)
-    for (int i = tid; i < (t + 1) * Dh; i += AT_THREADS) {
-      const int tt = i / Dh, dd = i - tt * Dh;
-      const float* src = a.qkv + (int64_t)tt * Nqkv + Nq + g * Dh + dd;
-      float kv = 0.0f, vv = 0.0f;
-      for (int s = 0; s < a.splits; ++s) {
-        kv = __fadd_rn(kv, src[s * a.split_stride]);
-        vv = __fadd_rn(vv, src[s * a.split_stride + Nkv]);
-      }
-      wk[i] = f2bf(kv);
-      wv[i] = f2bf(vv);
+  // (1) the window rows inside this chunk (split planes summed in order, rounded to bf16 like the
+  // cache): window tokens tt with p0 + tt in [j0, j1); most chunks hold none
+  const int w0 = max(j0, p0) - p0, w1 = j1 - p0;
+  for (int i = tid; i < (w1 - w0) * Dh; i += AT_THREADS) {
+    const int tt = w0 + i / Dh, dd = i % Dh;
+    const float* src = a.qkv + (int64_t)tt * Nqkv + Nq + g * Dh + dd;
+    float kv = 0.0f, vv = 0.0f;
+    for (int s = 0; s < a.splits; ++s) {
+      kv = __fadd_rn(kv, src[s * a.split_stride]);
+      vv = __fadd_rn(vv, src[s * a.split_stride + Nkv]);
     }
+    wk[tt * Dh + dd] = f2bf(kv);
+    wv[tt * Dh + dd] = f2bf(vv);
+  }
   float q[AT_MAXG][VEC];
 #pragma unroll
   for (int i = 0; i < AT_MAXG; ++i)
@@ -80,8 +80,8 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_partial(AttnArgs a) {
       q[i][v] = x;
     }
   __syncthreads();
-  if (sp == 0)
-    for (int dd = tid; dd < Dh; dd += AT_THREADS) {  // this token's row of the shared cache
+  if (j0 <= pt && pt < j1)  // the chunk holding the token's own position writes its cache row
+    for (int dd = tid; dd < Dh; dd += AT_THREADS) {
       a.kc[((int64_t)pt * a.Hkv + g) * Dh + dd] = wk[t * Dh + dd];
       a.vc[((int64_t)pt * a.Hkv + g) * Dh + dd] = wv[t * Dh + dd];
     }
