@@ -894,10 +894,6 @@ def live_governor_ks(report, cfg_json, L, E, K, estimator="linear", kmax=16):
     resident = set()
     rem = report["total_tokens"]
     out = []
-    if estimator == "elb":  # the prefill windows (attention models) fill the cache first
-        for ch in report.get("prefill", {}).get("chunks", []):
-            live_cycle(cache, ELB.build([], []), ch["target"], c)
-        resident = set(cache.recency)
     for cyc in report["cycles"]:
         if estimator == "elb":
             est = lambda kk: elb_estimate(freq, resident, calib, L, E, kk)  # noqa: E731

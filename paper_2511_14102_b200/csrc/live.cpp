@@ -197,6 +197,14 @@ struct mspq_engine {
   int32_t* dsched = nullptr;               // [Tmax + 1][4 + Tmax] packed dense schedules per T
   void* dws = nullptr;
   float* attn_part = nullptr;  // split-K attention partials
+  // prefill (§2.2 of DESIGN.md): every expert of a layer streamed into one of two layer buffers
+  unsigned char* pf_buf[2] = {nullptr, nullptr};
+  cudaEvent_t pf_ready[2] = {nullptr, nullptr}, pf_done[2] = {nullptr, nullptr};
+  float* pf_h = nullptr;                 // [n][d] residual of every prompt token
+  float* pf_y[2] = {nullptr, nullptr};   // [chunk][kMaxSplit][32 K][d] MoE planes by layer parity
+  int32_t* pf_gbuf = nullptr;            // [E] identity expert -> layer-buffer slot
+  int32_t* pf_eo = nullptr;              // [chunk][32 K] each chunk's entry_of, kept for the next layer
+  int pf_n = 0;                          // prompt capacity of pf_h / pf_y
   int32_t* dsched_of(int T) { return dsched + (size_t)T * (4 + Tmax); }
   size_t kv_layer() const { return (size_t)m.P * m.Hkv * m.Dh; }
   int32_t* sched_cap = nullptr;  // collect_plans: each verify layer's device schedule [L][Sched::ints]
@@ -885,6 +893,37 @@ static void spin_wait(cudaEvent_t ev) {
   }
 }
 
+// one expert's bf16 tile images into dst: raw H2D on the copy stream, or the XC blob in chunks
+// through a staging buffer and decoded as each chunk lands (the same pipeline as issue_copies)
+static uint64_t copy_expert(mspq_engine* E, int key, unsigned char* dst) {
+  const unsigned char* hb = E->host_blob(E->payload(key));
+  if (!E->codec) {
+    CUDA_OK(cudaMemcpyAsync(dst, hb, E->S16, cudaMemcpyHostToDevice, E->sx));
+    return (uint64_t)E->S16;
+  }
+  const uint32_t* toff = reinterpret_cast<const uint32_t*>(hb + 64);
+  const int sb = E->stage_next;
+  E->stage_next ^= 1;
+  unsigned char* stg = E->stage[sb];
+  if (E->stage_rec[sb]) CUDA_OK(cudaStreamWaitEvent(E->sx, E->ev_stage[sb], 0));
+  const int nt = E->n_tiles;
+  const int nm = std::max(1, std::min(8, (int)(toff[nt] / (24u << 20))));
+  const int tail = nm > 1 ? nt / 32 : 0, nc = nm + (tail ? 1 : 0);
+  for (int c = 0; c < nc; ++c) {
+    const int t0 = c < nm ? (int)((int64_t)(nt - tail) * c / nm) : nt - tail;
+    const int t1 = c < nm ? (int)((int64_t)(nt - tail) * (c + 1) / nm) : nt;
+    const uint32_t b0 = c ? toff[t0] : 0u, b1 = toff[t1];
+    CUDA_OK(cudaMemcpyAsync(stg + b0, hb + b0, b1 - b0, cudaMemcpyHostToDevice, E->sx));
+    cudaEvent_t ev = E->pool_event();
+    CUDA_OK(cudaEventRecord(ev, E->sx));
+    CUDA_OK(cudaStreamWaitEvent(E->sdec, ev, 0));
+    CAPI_OK(mspq_xc_decode(stg, t0, t1, dst, E->dec_ctas, E->sdec));
+  }
+  CUDA_OK(cudaEventRecord(E->ev_stage[sb], E->sdec));
+  E->stage_rec[sb] = 1;
+  return toff[nt];
+}
+
 static int issue_copies(mspq_engine* E, int cycle, CopyBatch& batch, uint64_t& bytes, bool prefetch = false,
                         const std::vector<std::pair<int, int>>* list = nullptr) {
   const bool l2 = prefetch && E->pf_lane;
@@ -1178,91 +1217,113 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
       }
     }
   };
-  // ---------------- prefill (attention models): the prompt's KV rows 0 .. n_prompt-2 through the
-  // same verify pass (target model, controller demand steps) in windows of up to Tmax tokens with
-  // no draft (k = 0).  Its cache decisions are part of the run (oracle/control_plane replays them
-  // first); its time is reported apart from the decode metric (TTFT vs TPOT).
+  // ---------------- prefill (attention models): the prompt's tokens 0 .. n_prompt-2 through the
+  // target, layer-major over the whole prompt in chunks of up to 32 tokens, so their KV rows exist
+  // before the first cycle.  A prompt routes to (nearly) every expert of every layer, so the
+  // prefill streams each layer's E experts from the host store into one of two layer buffers,
+  // two layers ahead of the compute, outside the capped cache (whose state the prefill leaves
+  // alone) -- each expert crosses the link once instead of once per window slot.  Its time is
+  // reported apart from the decode metric (TTFT vs TPOT).
   json prefill = json::object();
   if (E->attn && n_prompt > 1) {
     const auto pw0 = std::chrono::steady_clock::now();
-    int done = 0, pf_new = 0;
-    uint64_t pf_bytes = 0;
-    json chunks = json::array();
-    while (done < n_prompt - 1) {
-      const int T = std::min(E->Tmax, n_prompt - 1 - done);
-      const int cycle = ++E->cycle_serial;
-      E->ev_pool_next = 0;
-      for (int s2 = 0; s2 < T; ++s2) {
-        E->hpin[s2] = prompt[done + s2];
-        E->hpin[E->Tmax + 1 + s2] = done + s2;
+    const int n = n_prompt - 1, CH = 32, nch = (n + CH - 1) / CH;
+    if (nch > L) fail(MSPQ_ERR_RANGE_OUT_OF_BOUNDS, "prompt longer than 32 x layers tokens");
+    const size_t plane = (size_t)mspq_engine::kMaxSplit * CH * K * d;  // floats per chunk planes
+    if (!E->pf_buf[0]) {
+      for (int i = 0; i < 2; ++i) {
+        CUDA_OK(cudaMalloc(&E->pf_buf[i], (size_t)Ex * E->S16));
+        CUDA_OK(cudaEventCreateWithFlags(&E->pf_ready[i], cudaEventDisableTiming));
+        CUDA_OK(cudaEventCreateWithFlags(&E->pf_done[i], cudaEventDisableTiming));
       }
-      CUDA_OK(cudaMemcpyAsync(E->win_tok(), E->hpin, T * 4, cudaMemcpyHostToDevice, E->sc));
-      CUDA_OK(cudaMemcpyAsync(E->win_pos(), E->hpin + E->Tmax + 1, T * 4, cudaMemcpyHostToDevice, E->sc));
-      CAPI_OK(mspq_cache_begin_cycle(E->cache, 0, E->sc));
-      CAPI_OK(mspq_embed(E->embed, E->pos, E->win_tok(), E->win_pos(), T, d, E->h, E->sc));
-      std::vector<CopyBatch> pb;
-      uint64_t cb = 0;
-      stall_ev.clear();
-      verify_layers(T, cycle, true, pb, cb);
-      if (level >= 1)
-        CUDA_OK(cudaMemcpyAsync(E->hpin, E->ids_t, (size_t)L * T * K * 4, cudaMemcpyDeviceToHost, E->sc));
-      CUDA_OK(cudaEventRecord(E->ev_end, E->sc));
-      CUDA_OK(cudaEventSynchronize(E->ev_end));
-      json ch;
-      ch["start_pos"] = done;
-      ch["T"] = T;
-      ch["new_experts"] = E->view.host_stat[S_FETCHED];
-      ch["bytes"] = cb;
-      pf_new += E->view.host_stat[S_FETCHED];
-      pf_bytes += cb;
-      if (level >= 1) {
-        json tgt = json::array();  // [slot][layer][K]
-        for (int s2 = 0; s2 < T; ++s2) {
-          json sl = json::array();
-          for (int l = 0; l < L; ++l) {
-            json c2 = json::array();
-            for (int j = 0; j < K; ++j) c2.push_back(E->hpin[((size_t)l * T + s2) * K + j]);
-            sl.push_back(c2);
-          }
-          tgt.push_back(sl);
-        }
-        ch["target"] = tgt;
-      }
-      if (level >= 2) {
-        const int nl = std::min(E->view.host_stat[S_NLOG], E->view.log_cap);
-        std::vector<int32_t> lg((size_t)nl * 6);
-        if (nl) CUDA_OK(cudaMemcpy(lg.data(), E->view.log, (size_t)nl * 24, cudaMemcpyDeviceToHost));
-        json lj = json::array();
-        for (int i = 0; i < nl; ++i) {
-          const int32_t* ev = &lg[(size_t)i * 6];
-          lj.push_back({ev[0], ev[1], ev[2] / Ex, ev[2] % Ex, ev[3], ev[4] < 0 ? -1 : ev[4] / Ex,
-                        ev[4] < 0 ? -1 : ev[4] % Ex, ev[5]});
-        }
-        ch["log"] = lj;
-      }
-      chunks.push_back(ch);
-      done += T;
+      std::vector<int32_t> idn(Ex);
+      for (int e = 0; e < Ex; ++e) idn[e] = e;
+      CUDA_OK(cudaMalloc(&E->pf_gbuf, Ex * 4));
+      CUDA_OK(cudaMemcpy(E->pf_gbuf, idn.data(), Ex * 4, cudaMemcpyHostToDevice));
     }
+    if (n > E->pf_n) {
+      for (float* p : {E->pf_h, E->pf_y[0], E->pf_y[1]})
+        if (p) cudaFree(p);
+      CUDA_OK(cudaMalloc(&E->pf_h, (size_t)n * d * 4));
+      CUDA_OK(cudaMalloc(&E->pf_y[0], (size_t)nch * plane * 4));
+      CUDA_OK(cudaMalloc(&E->pf_y[1], (size_t)nch * plane * 4));
+      if (E->pf_eo) cudaFree(E->pf_eo);
+      CUDA_OK(cudaMalloc(&E->pf_eo, (size_t)nch * CH * K * 4 * 2));
+      E->pf_n = n;
+    }
+    std::vector<int32_t> pos_all(n), tok_all(prompt, prompt + n);
+    for (int i = 0; i < n; ++i) pos_all[i] = i;
+    int32_t *d_tok = nullptr, *d_pos = nullptr;
+    CUDA_OK(cudaMalloc(&d_tok, (size_t)n * 4));
+    CUDA_OK(cudaMalloc(&d_pos, (size_t)n * 4));
+    CUDA_OK(cudaMemcpyAsync(d_tok, tok_all.data(), (size_t)n * 4, cudaMemcpyHostToDevice, E->sc));
+    CUDA_OK(cudaMemcpyAsync(d_pos, pos_all.data(), (size_t)n * 4, cudaMemcpyHostToDevice, E->sc));
+    CAPI_OK(mspq_embed(E->embed, E->pos, d_tok, d_pos, n, d, E->pf_h, E->sc));
+    uint64_t pf_bytes = 0;
+    E->ev_pool_next = 0;
+    auto stream_layer = [&](int l) {  // layer l's experts into buffer l & 1, after layer l-2's GEMMs
+      const int bi = l & 1;
+      if (l >= 2) CUDA_OK(cudaStreamWaitEvent(E->sx, E->pf_done[bi], 0));
+      for (int e = 0; e < Ex; ++e) pf_bytes += copy_expert(E, l * Ex + e, E->pf_buf[bi] + (size_t)e * E->S16);
+      CUDA_OK(cudaEventRecord(E->pf_ready[bi], E->codec ? E->sdec : E->sx));
+    };
+    stream_layer(0);
+    if (L > 1) stream_layer(1);
+    std::vector<int> ysp_ch(nch, 1);
+    for (int l = 0; l < L; ++l) {
+      if (E->ev_pool_next > E->ev_pool.size() / 2 + 256) E->ev_pool_next = 0;  // events of finished layers
+      bool waited = false;
+      for (int c = 0; c < nch; ++c) {
+        const int t0 = c * CH, T = std::min(CH, n - t0);
+        float* hc = E->pf_h + (size_t)t0 * d;
+        float* yprev = E->pf_y[(l - 1) & 1] + (size_t)c * plane;
+        float* ycur = E->pf_y[l & 1] + (size_t)c * plane;
+        Sched& sv = E->sv[c & 1];
+        // attention block of chunk c (the residual lives in pf_h; E->h is the window workspace)
+        CUDA_OK(cudaMemcpyAsync(E->h, hc, (size_t)T * d * 4, cudaMemcpyDeviceToDevice, E->sc));
+        int32_t* eo_prev = E->pf_eo + ((size_t)((l - 1) & 1) * nch + c) * CH * K;
+        int32_t* eo_cur = E->pf_eo + ((size_t)(l & 1) * nch + c) * CH * K;
+        const int ysp = enqueue_attn(E, l, T, d_pos + t0, l ? yprev : nullptr, l ? eo_prev : nullptr,
+                                     l ? E->wts_t + (size_t)c * CH * K : nullptr, ysp_ch[c], (long long)T * K * d,
+                                     nullptr, E->sc);
+        int32_t* ids = E->ids_t;  // [T][K] of this chunk
+        CAPI_OK(mspq_gate_topk(E->h, E->oproj, nullptr, nullptr, ysp, (long long)T * d, E->gamma + (size_t)l * d,
+                               E->router + (size_t)l * Ex * d, E->xn, ids, E->wts_t + (size_t)c * CH * K, nullptr,
+                               nullptr, nullptr, nullptr, nullptr, l, L, T, d, Ex, K, m.eps, E->sc));
+        CAPI_OK(mspq_build_schedule(ids, T, K, Ex, E->pf_gbuf, sv.n_groups, sv.group_expert, sv.group_buf,
+                                    sv.group_off, sv.entry_tok, sv.entry_of, sv.entry_group, E->sc));
+        if (!waited) {  // the layer's experts have landed
+          CUDA_OK(cudaStreamWaitEvent(E->sc, E->pf_ready[l & 1], 0));
+          waited = true;
+        }
+        const int G = std::min(Ex, T * K);
+        const int units = std::max(1, G * (2 * m.f / 128));
+        const int sp1 = std::max(1, std::min({(296 + units - 1) / units, mspq_engine::kMaxSplit, d / 64}));
+        const int units2 = std::max(1, G * (d / 128));
+        const int sp2 = std::max(1, std::min({(296 + units2 - 1) / units2, mspq_engine::kMaxSplit, m.f / 64}));
+        CAPI_OK(mspq_moe_bf16_tc(sv.n_groups, sv.group_expert, sv.group_buf, sv.group_off, sv.entry_tok,
+                                 sv.entry_group, E->xn, E->pf_buf[l & 1], E->S16, d, m.f, T, K, E->G, sp1, sp2,
+                                 E->tcws, ycur, E->sc));
+        CUDA_OK(cudaMemcpyAsync(hc, E->h, (size_t)T * d * 4, cudaMemcpyDeviceToDevice, E->sc));
+        ysp_ch[c] = sp2;
+        // the chunk's entry_of must survive until layer l+1's combine of this chunk (the Sched
+        // double buffer holds two chunks); its routing weights stay at wts_t + c * 32 K
+        CUDA_OK(cudaMemcpyAsync(eo_cur, sv.entry_of, (size_t)T * K * 4, cudaMemcpyDeviceToDevice, E->sc));
+      }
+      CUDA_OK(cudaEventRecord(E->pf_done[l & 1], E->sc));
+      if (l + 2 < L) stream_layer(l + 2);
+    }
+    CUDA_OK(cudaStreamSynchronize(E->sc));
     CUDA_OK(cudaStreamSynchronize(E->sx));
     if (E->sdec) CUDA_OK(cudaStreamSynchronize(E->sdec));
-    if (c.estimator == 1) CUDA_OK(cudaMemcpy(E->res_host.data(), E->view.res, (size_t)L * Ex * 4, cudaMemcpyDeviceToHost));
-    prefill["tokens"] = n_prompt - 1;
-    prefill["new_experts"] = pf_new;
+    cudaFree(d_tok);
+    cudaFree(d_pos);
+    prefill["tokens"] = n;
+    prefill["windows"] = nch;
+    prefill["expert_copies"] = (uint64_t)L * Ex;
     prefill["h2d_bytes"] = pf_bytes;
     prefill["time_s"] = std::chrono::duration<double>(std::chrono::steady_clock::now() - pw0).count();
-    prefill["chunks"] = chunks;
-    if (E->peer_G > 0) {  // the decode's peer-tier counters start after the prefill
-      prefill["peer_fetches"] = E->n_peer;
-      prefill["home_local_fetches"] = E->n_home_local;
-      E->gen_peer_bytes = E->gen_home_local_bytes = 0;
-      E->n_peer = E->n_home_local = 0;
-    }
-    // the decode state (head token / position) the prefill windows overwrote
-    E->hpin[0] = 0;
-    E->hpin[1] = prompt[n_prompt - 1];
-    E->hpin[2] = head_pos;
-    CUDA_OK(cudaMemcpyAsync(E->dst, E->hpin, 12, cudaMemcpyHostToDevice, E->sc));
-    CUDA_OK(cudaMemcpyAsync(E->win_tok(), E->hpin + 1, 4, cudaMemcpyHostToDevice, E->sc));
+    // the decode state (head token / position) the prefill's embed left alone, and the decode's clock
     CUDA_OK(cudaEventRecord(E->ev_t0, E->sc));  // the decode's clock starts after the prefill
     CUDA_OK(cudaStreamWaitEvent(E->sx, E->ev_t0, 0));
     if (E->sdec) CUDA_OK(cudaStreamWaitEvent(E->sdec, E->ev_t0, 0));
@@ -1743,6 +1804,15 @@ void destroy(mspq_engine* E) {
     if (p) cudaFree(p);
   if (E->sched_cap) cudaFree(E->sched_cap);
   if (E->act_d) cudaFree(E->act_d);
+  for (int i = 0; i < 2; ++i) {
+    if (E->pf_buf[i]) cudaFree(E->pf_buf[i]);
+    if (E->pf_y[i]) cudaFree(E->pf_y[i]);
+    if (E->pf_ready[i]) cudaEventDestroy(E->pf_ready[i]);
+    if (E->pf_done[i]) cudaEventDestroy(E->pf_done[i]);
+  }
+  if (E->pf_h) cudaFree(E->pf_h);
+  if (E->pf_gbuf) cudaFree(E->pf_gbuf);
+  if (E->pf_eo) cudaFree(E->pf_eo);
   for (void* p : {(void*)E->wattn, (void*)E->gamma_a, (void*)E->kcache, (void*)E->vcache, (void*)E->qkv, (void*)E->oproj,
                   (void*)E->ao, (void*)E->dsched, E->dws, (void*)E->attn_part, (void*)E->hmid_v, (void*)E->hmid_dstage, (void*)E->hmid_d})
     if (p) cudaFree(p);
