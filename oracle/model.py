@@ -376,22 +376,25 @@ class Model:
         lib().orc_router_topk(_p(xn), _p(wr), m.E, m.d, m.K, _p(logits), _p(ids), _p(wts))
         return ids, wts, logits
 
-    def ffn_batch(self, xn_rows, l, e, draft: bool):
-        """Expert (l, e) on M normed rows [M, d] bf16 -> y [M, d] fp32 (decode_ref.c)."""
+    def ffn_batch(self, xn_rows, l, e, draft: bool, with_act=False):
+        """Expert (l, e) on M normed rows [M, d] bf16 -> y [M, d] fp32 (decode_ref.c) (+ the bf16
+        SiLU(gate) * up rows [M, f] with `with_act`)."""
         m = self.m
         xn_rows = np.ascontiguousarray(xn_rows, dtype=np.uint16)
         M = xn_rows.shape[0]
         y = np.empty((M, m.d), dtype=np.float32)
+        act = np.empty((M, m.f), dtype=np.uint16) if with_act else None
         rc = lib().orc_expert_ffn(m.seed, l, e, m.d, m.f, ctypes.c_float(m.a_up()), ctypes.c_float(m.a_down()),
-                                  1 if draft else 0, M, _p(xn_rows), _p(y), None)
+                                  1 if draft else 0, M, _p(xn_rows), _p(y), _p(act) if with_act else None)
         if rc:
             raise MemoryError("orc_expert_ffn")
-        return y
+        return (y, act) if with_act else y
 
     def ffn(self, xn, l, e, draft: bool):
         m = self.m
         if self.fast:
-            return self.ffn_batch(xn[None, :], l, e, draft)[0], None
+            y, a = self.ffn_batch(xn[None, :], l, e, draft, with_act=True)
+            return y[0], a[0]
         x = bf16_to_f32(xn)
         G, U, D = self.expert_f32(l, e, draft)
         gv = np.ascontiguousarray(G @ x, dtype=np.float32)

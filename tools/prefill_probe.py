@@ -25,7 +25,7 @@ for rep_i in range(2):
     r = eng.generate(prompt, 8)
     wall = time.perf_counter() - t0
     pf = r["prefill"]
-    print(json.dumps({"wall_s": wall, "prefill_s": pf["time_s"], "prefill_new_experts": pf["new_experts"],
-                      "prefill_h2d_GB": pf["h2d_bytes"] / 1e9, "windows": [(c["T"], c["new_experts"]) for c in pf["chunks"]],
+    print(json.dumps({"wall_s": wall, "prefill_s": pf["time_s"], "prefill_expert_copies": pf["expert_copies"],
+                      "prefill_h2d_GB": pf["h2d_bytes"] / 1e9, "windows": pf["windows"],
                       "decode_s": r["total_time_s"], "decode_tokens": r["total_tokens"]}))
 eng.close()
