@@ -896,6 +896,11 @@ static void spin_wait(cudaEvent_t ev) {
 // one expert's bf16 tile images into dst: raw H2D on the copy stream, or the XC blob in chunks
 // through a staging buffer and decoded as each chunk lands (the same pipeline as issue_copies)
 static uint64_t copy_expert(mspq_engine* E, int key, unsigned char* dst) {
+  if (const unsigned char* hs = E->home_src(key)) {  // peer tier: HBM -> HBM from the key's home
+    cudaStream_t hst = E->codec ? E->sdec : E->sx;
+    CUDA_OK(cudaMemcpyAsync(dst, hs, E->S16, cudaMemcpyDeviceToDevice, hst));
+    return 0;  // no PCIe bytes
+  }
   const unsigned char* hb = E->host_blob(E->payload(key));
   if (!E->codec) {
     CUDA_OK(cudaMemcpyAsync(dst, hb, E->S16, cudaMemcpyHostToDevice, E->sx));
