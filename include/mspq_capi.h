@@ -190,9 +190,10 @@ int mspq_attention(const float* qkv, int splits, long long split_stride, int T, 
  * draft blobs in FRAGMENT-MAJOR order (mspq_fragtile_int4 for q, scales row-major: W13q | W13s |
  * W2q | W2s with the mspq_int4_blob_bytes offsets); groups = the K experts of the token in the
  * draft schedule (n_groups / group_expert, group g = entry g); act [K][f] bf16 scratch (SiLU(gate)
- * * up of W13, fused); y [K][d] fp32 (one plane). */
+ * * up of W13, fused); y [split2][K][d] fp32 planes (W2 split over its K dimension; the
+ * consumer sums them in order). */
 int mspq_moe_int4_gemv(const int32_t* n_groups, const int32_t* group_expert, const void* xn, const void* blobs,
-                       long long blob_bytes, int layer, int E, int d, int f, int K, void* act, float* y,
+                       long long blob_bytes, int layer, int E, int d, int f, int K, int split2, void* act, float* y,
                        void* stream);
 /* row-major quantised INT4 q[rows][cols/8] (standard nibble order) -> fragment-major words
  * [rows/16][cols/64][32 lanes][4] for mspq_moe_int4_gemv (layout in gemv_int4.cu) */

@@ -219,19 +219,19 @@ int mspq_fragtile_int4(const void* q, int rows, int cols, void* fq, void* stream
   CK(launch_fragtile_int4((const uint32_t*)q, rows, cols, (uint32_t*)fq, ST(stream)), "fragtile_int4");
 }
 int mspq_moe_int4_gemv(const int32_t* n_groups, const int32_t* group_expert, const void* xn, const void* blobs,
-                       long long blob_bytes, int layer, int E, int d, int f, int K, void* act, float* y,
+                       long long blob_bytes, int layer, int E, int d, int f, int K, int split2, void* act, float* y,
                        void* stream) {
-  if (d % 128 || f % 128 || (2 * f) % 32 || d % 32 || K < 1)
-    return set_error(MSPQ_ERR_SHAPE_MISMATCH, "moe_int4_gemv: d, f multiples of 128");
+  if (d % 128 || f % 128 || (2 * f) % 32 || d % 32 || K < 1 || split2 < 1 || split2 > f / 128)
+    return set_error(MSPQ_ERR_SHAPE_MISMATCH, "moe_int4_gemv: d, f multiples of 128, 1 <= split2 <= f/128");
   const long long q13 = (long long)2 * f * d / 2, s13 = (long long)2 * f * (d / 128) * 2, q2 = (long long)d * f / 2;
   cudaStream_t st = ST(stream);
   GemvArgs g1{(const unsigned char*)blobs, blob_bytes, 0, q13, 2 * f, d, layer, E, n_groups, group_expert,
               (const uint16_t*)xn, 0, nullptr, (uint16_t*)act};
-  cudaError_t e = launch_int4_gemv(g1, K, st);
+  cudaError_t e = launch_int4_gemv(g1, K, 1, st);
   if (e != cudaSuccess) return cuda_status(e, "int4 gemv W13");
   GemvArgs g2{(const unsigned char*)blobs, blob_bytes, q13 + s13, q13 + s13 + q2, d, f, layer, E, n_groups,
               group_expert, (const uint16_t*)act, 1, y, nullptr};
-  CK(launch_int4_gemv(g2, K, st), "int4 gemv W2");
+  CK(launch_int4_gemv(g2, K, split2, st), "int4 gemv W2");
 }
 int mspq_moe_int4_tc(const int32_t* n_groups, const int32_t* group_expert, const int32_t* group_buf,
                      const int32_t* group_off, const int32_t* entry_tok, const int32_t* entry_group,

@@ -47,43 +47,28 @@ MSPQ_D uint4 ldg_stream(const void* p) {
   return v;
 }
 
-// grid (R / 32, groups): CTA = 32 rows of one group's expert matrix, 8 warps split the 128-column
-// scale groups (warp w takes groups w, w + 8, ...), partial rows reduced in warp order.
+// grid (R / 32, groups, ksplit): CTA = 32 rows of one group's expert matrix over the scale groups
+// of its K split; the 8 warps take groups w, w + 8, ... of the split, partial rows reduced in warp
+// order.  The first weight loads are issued before the x prologue (they do not depend on it), and
+// each group's bias C_g = sum_k c_k b_k is reduced from the B fragments the lanes already hold
+// (quad shuffles, fixed order) instead of a serial prologue.  K splits (W2) write separate planes
+// [split][groups][rows] that the next K1 combine sums in order.
 __global__ void __launch_bounds__(GV_THREADS) k_int4_gemv(GemvArgs a) {
   pdl_enter();  // launched with launch_pdl (kernels.h)
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int g = blockIdx.y;
+  const int g = blockIdx.y, sp = blockIdx.z, S = gridDim.z;
   if (g >= *a.n_groups) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kdim = a.kdim, ngr = kdim / 128, nchunk = kdim / 64;
+  const int gq0 = sp * ngr / S, gq1 = (sp + 1) * ngr / S;
   uint16_t* xh = reinterpret_cast<uint16_t*>(smem_raw);            // [kdim] class-scaled fp16
-  float* cg = reinterpret_cast<float*>(smem_raw + kdim * 2);        // [ngr] corrections
-  float* red = cg + ngr;                                            // [GV_WARPS][32] row partials
-  const uint16_t* x = a.x + (a.x_per_group ? (int64_t)g * kdim : 0);
-  for (int k = tid; k < kdim; k += GV_THREADS) {
-    const float v = bf2f(x[k]) * ((k & 15) >= 8 ? 0.0625f : 1.0f);
-    const __half h = __float2half_rn(v);
-    xh[k] = *reinterpret_cast<const uint16_t*>(&h);
-  }
-  __syncthreads();
-  for (int gq = tid; gq < ngr; gq += GV_THREADS) {  // C_g = sum_k c_k b_k, fixed order
-    float c = 0.0f;
-    for (int k = 128 * gq; k < 128 * gq + 128; ++k) {
-      const float b = __half2float(*reinterpret_cast<const __half*>(&xh[k]));
-      c = fmaf((k & 15) >= 8 ? 1152.0f : 1032.0f, b, c);
-    }
-    cg[gq] = c;
-  }
-  __syncthreads();
+  float* red = reinterpret_cast<float*>(smem_raw + kdim * 2);       // [GV_WARPS][32] row partials
   const int expert = a.group_expert[g];
   const unsigned char* blob = a.blobs + ((int64_t)a.layer * a.E + expert) * a.blob_bytes;
   const uint4* q = reinterpret_cast<const uint4*>(blob + a.q_off);
   const uint16_t* sc = reinterpret_cast<const uint16_t*>(blob + a.s_off);
   const int rt0 = blockIdx.x * GV_TILES;
   const int gi = lane >> 2, ti = lane & 3;
-  float acc[GV_TILES][2];
-#pragma unroll
-  for (int i = 0; i < GV_TILES; ++i) acc[i][0] = acc[i][1] = 0.0f;
   // register double buffer: the next scale group's 2 tiles x 2 chunks are in flight while the
   // current one is multiplied
   uint4 cur[GV_TILES][2], nxt[GV_TILES][2];
@@ -94,14 +79,26 @@ __global__ void __launch_bounds__(GV_THREADS) k_int4_gemv(GemvArgs a) {
       for (int c = 0; c < 2; ++c)
         dst[i][c] = ldg_stream(q + (((int64_t)(rt0 + i) * nchunk + 2 * gq + c) * 32 + lane));
   };
-  int gq = warp;
-  if (gq < ngr) load(gq, cur);
-  for (; gq < ngr; gq += GV_WARPS) {
-    const bool more = gq + GV_WARPS < ngr;
+  int gq = gq0 + warp;
+  if (gq < gq1) load(gq, cur);
+  const uint16_t* x = a.x + (a.x_per_group ? (int64_t)g * kdim : 0);
+  for (int k = 2 * tid; k < kdim; k += 2 * GV_THREADS) {
+    const uint32_t u = *reinterpret_cast<const uint32_t*>(x + k);
+    const float m = (k & 15) >= 8 ? 0.0625f : 1.0f;
+    const __half2 h2 = __floats2half2_rn(__uint_as_float(u << 16) * m, __uint_as_float(u & 0xffff0000u) * m);
+    *reinterpret_cast<__half2*>(&xh[k]) = h2;
+  }
+  __syncthreads();
+  float acc[GV_TILES][2];
+#pragma unroll
+  for (int i = 0; i < GV_TILES; ++i) acc[i][0] = acc[i][1] = 0.0f;
+  for (; gq < gq1; gq += GV_WARPS) {
+    const bool more = gq + GV_WARPS < gq1;
     if (more) load(gq + GV_WARPS, nxt);
     float d[GV_TILES][4];
 #pragma unroll
     for (int i = 0; i < GV_TILES; ++i) d[i][0] = d[i][1] = d[i][2] = d[i][3] = 0.0f;
+    float c1 = 0.0f, c16 = 0.0f;  // this lane's share of C_g: sum b over class-1 / class-16 columns
 #pragma unroll
     for (int c = 0; c < 2; ++c)
 #pragma unroll
@@ -109,6 +106,10 @@ __global__ void __launch_bounds__(GV_THREADS) k_int4_gemv(GemvArgs a) {
         const int kb = 8 * gq + 4 * c + v;  // k16 block
         const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&xh[16 * kb + 2 * ti]);
         const uint32_t b1 = *reinterpret_cast<const uint32_t*>(&xh[16 * kb + 8 + 2 * ti]);
+        const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&b0));
+        const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&b1));
+        c1 = __fadd_rn(__fadd_rn(c1, f0.x), f0.y);
+        c16 = __fadd_rn(__fadd_rn(c16, f1.x), f1.y);
 #pragma unroll
         for (int i = 0; i < GV_TILES; ++i) {
           const uint32_t w = v == 0 ? cur[i][c].x : v == 1 ? cur[i][c].y : v == 2 ? cur[i][c].z : cur[i][c].w;
@@ -121,13 +122,16 @@ __global__ void __launch_bounds__(GV_THREADS) k_int4_gemv(GemvArgs a) {
           mma16816(d[i], af, b0, b1);
         }
       }
-    const float cgq = cg[gq];
+    // C_g over the quad's four column slices (lanes ti = 0..3 of a row group), fixed order
+    float cl = fmaf(1152.0f, c16, __fmul_rn(1032.0f, c1));
+    cl = __fadd_rn(cl, __shfl_xor_sync(0xffffffffu, cl, 1));
+    cl = __fadd_rn(cl, __shfl_xor_sync(0xffffffffu, cl, 2));
 #pragma unroll
     for (int i = 0; i < GV_TILES; ++i) {
       const int r0 = 16 * (rt0 + i) + gi;
       const float s0 = bf2f(sc[(int64_t)r0 * ngr + gq]), s1 = bf2f(sc[(int64_t)(r0 + 8) * ngr + gq]);
-      acc[i][0] = fmaf(s0, __fsub_rn(d[i][0], cgq), acc[i][0]);  // every B column is x: column 2 ti == column 0
-      acc[i][1] = fmaf(s1, __fsub_rn(d[i][2], cgq), acc[i][1]);
+      acc[i][0] = fmaf(s0, __fsub_rn(d[i][0], cl), acc[i][0]);  // every B column is x: column 2 ti == column 0
+      acc[i][1] = fmaf(s1, __fsub_rn(d[i][2], cl), acc[i][1]);
     }
     if (more) {
 #pragma unroll
@@ -155,7 +159,7 @@ __global__ void __launch_bounds__(GV_THREADS) k_int4_gemv(GemvArgs a) {
       const float up = __shfl_down_sync(0xffffffffu, v, 1);
       if ((tid & 1) == 0) a.act[(int64_t)g * (a.rows / 2) + row / 2] = f2bf(__fmul_rn(silu_det(v), up));
     } else {
-      a.y[(int64_t)g * a.rows + row] = v;
+      a.y[((int64_t)sp * gridDim.y + g) * a.rows + row] = v;
     }
   }
 }
@@ -179,15 +183,15 @@ __global__ void k_fragtile_int4(const uint32_t* __restrict__ q, int rows, int co
 
 }  // namespace
 
-size_t gemv_smem_bytes(int kdim) { return (size_t)kdim * 2 + (size_t)(kdim / 128) * 4 + GV_WARPS * 32 * 4 + 16; }
+size_t gemv_smem_bytes(int kdim) { return (size_t)kdim * 2 + GV_WARPS * 32 * 4 + 16; }
 
-cudaError_t launch_int4_gemv(const GemvArgs& a, int max_groups, cudaStream_t st) {
+cudaError_t launch_int4_gemv(const GemvArgs& a, int max_groups, int ksplit, cudaStream_t st) {
   const size_t smem = gemv_smem_bytes(a.kdim);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_int4_gemv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  return launch_pdl(k_int4_gemv, dim3(a.rows / 32, max_groups), dim3(GV_THREADS), smem, st, a);
+  return launch_pdl(k_int4_gemv, dim3(a.rows / 32, max_groups, ksplit), dim3(GV_THREADS), smem, st, a);
 }
 
 cudaError_t launch_fragtile_int4(const uint32_t* q, int rows, int cols, uint32_t* fq, cudaStream_t st) {

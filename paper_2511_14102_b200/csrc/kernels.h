@@ -153,10 +153,10 @@ struct GemvArgs {
   const int32_t* group_expert;
   const uint16_t* x;           // bf16 input rows
   int x_per_group;             // 0: one row for every group (W13), 1: row g (W2 on the act rows)
-  float* y;                    // W2: [groups][rows] fp32
+  float* y;                    // W2: [ksplit][groups][rows] fp32 planes
   uint16_t* act;               // W13: [groups][rows/2] bf16 SiLU(gate) * up
 };
-cudaError_t launch_int4_gemv(const GemvArgs& a, int max_groups, cudaStream_t st);
+cudaError_t launch_int4_gemv(const GemvArgs& a, int max_groups, int ksplit, cudaStream_t st);
 cudaError_t launch_fragtile_int4(const uint32_t* q, int rows, int cols, uint32_t* fq, cudaStream_t st);
 
 cudaError_t launch_umma_grouped(const UmmaArgs& a, int max_groups, int BN, cudaStream_t st);

@@ -546,8 +546,10 @@ int enqueue_attn(mspq_engine* E, int l, int T, const int32_t* pos0, const float*
 void enqueue_draft_step(mspq_engine* E, cudaStream_t s) {
   const auto& m = E->m;
   const int K = m.K, L = m.L, d = m.d;
-  E->yd_split1 = 1;  // the draft GEMV writes one plane per expert (no K splits)
-  E->yd_split2 = 1;
+  // the draft GEMV: W13 in one pass (SiLU*up fused), W2 over K splits so a layer launches >= ~3
+  // CTAs per SM (d/32 row blocks x K experts x split2)
+  E->yd_split1 = 1;
+  E->yd_split2 = std::max(1, std::min(m.f / 128, (3 * 148 + (d / 32) * K - 1) / ((d / 32) * K)));
   int32_t* row = E->dst + 0;
   int32_t* cur_tok = E->dst + 1;
   int32_t* cur_pos = E->dst + 2;
@@ -576,8 +578,8 @@ void enqueue_draft_step(mspq_engine* E, cudaStream_t s) {
     else if (E->hcap_dstage && !E->attn)
       CUDA_OK(cudaMemcpyAsync(E->hcap_dstage + (size_t)l * d, E->h, (size_t)d * 4, cudaMemcpyDeviceToDevice, s));
     Sched& sc = E->sd[l & 1];
-    CAPI_OK(mspq_moe_int4_gemv(sc.n_groups, sc.group_expert, E->xn, E->draft4, E->S4, l, m.E, d, m.f, K, E->act_d,
-                               E->yd[l & 1], s));
+    CAPI_OK(mspq_moe_int4_gemv(sc.n_groups, sc.group_expert, E->xn, E->draft4, E->S4, l, m.E, d, m.f, K,
+                               E->yd_split2, E->act_d, E->yd[l & 1], s));
   }
   const int pl = (L - 1) & 1;
   CAPI_OK(mspq_gate_topk(E->h, E->yd[pl], E->sd[pl].entry_of, E->wts_d + (size_t)(L - 1) * K, E->yd_split2,

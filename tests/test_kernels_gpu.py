@@ -406,11 +406,12 @@ def test_moe_int4_gemv_draft_within_tolerance(cuda, name, E, K, d, f):
     n_groups = torch.tensor([K], dtype=torch.int32, device="cuda")
     gexp = torch.from_numpy(ids).cuda()
     act = torch.zeros(K * f, dtype=torch.int16, device="cuda")
-    y = torch.zeros(K * d, dtype=torch.float32, device="cuda")
+    split2 = 3
+    y = torch.zeros(split2 * K * d, dtype=torch.float32, device="cuda")
     check(lib().mspq_moe_int4_gemv(_ptr(n_groups), _ptr(gexp), _ptr(to_dev(xn)), _ptr(blobs), s4, layer, E, d, f, K,
-                                   _ptr(act), _ptr(y), None))
+                                   split2, _ptr(act), _ptr(y), None))
     torch.cuda.synchronize()
-    y = y.cpu().numpy().reshape(K, d)
+    y = y.cpu().numpy().reshape(split2, K, d).sum(axis=0)
     act = om.bf16_to_f32(i16_to_u16(act).reshape(K, f))
     for g, e in enumerate(ids.tolist()):
         want, a_want = mdl.ffn(xn, layer, e, draft=True)
