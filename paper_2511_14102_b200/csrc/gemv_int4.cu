@@ -69,18 +69,24 @@ __global__ void __launch_bounds__(GV_THREADS) k_int4_gemv(GemvArgs a) {
   const uint16_t* sc = reinterpret_cast<const uint16_t*>(blob + a.s_off);
   const int rt0 = blockIdx.x * GV_TILES;
   const int gi = lane >> 2, ti = lane & 3;
-  // register double buffer: the next scale group's 2 tiles x 2 chunks are in flight while the
-  // current one is multiplied
-  uint4 cur[GV_TILES][2], nxt[GV_TILES][2];
-  auto load = [&](int gq, uint4 (&dst)[GV_TILES][2]) {
+  // memory-level parallelism: a warp issues the loads of NB scale groups (NB x 2 KB) at once,
+  // then multiplies them; the first batch is issued before the x prologue
+  constexpr int NB = 4;
+  uint4 buf[NB][GV_TILES][2];
+  auto load_batch = [&](int gfirst) {
 #pragma unroll
-    for (int i = 0; i < GV_TILES; ++i)
+    for (int b = 0; b < NB; ++b) {
+      const int gb = gfirst + b * GV_WARPS;
+      if (gb < gq1)
 #pragma unroll
-      for (int c = 0; c < 2; ++c)
-        dst[i][c] = ldg_stream(q + (((int64_t)(rt0 + i) * nchunk + 2 * gq + c) * 32 + lane));
+        for (int i = 0; i < GV_TILES; ++i)
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+            buf[b][i][c] = ldg_stream(q + (((int64_t)(rt0 + i) * nchunk + 2 * gb + c) * 32 + lane));
+    }
   };
   int gq = gq0 + warp;
-  if (gq < gq1) load(gq, cur);
+  load_batch(gq);
   const uint16_t* x = a.x + (a.x_per_group ? (int64_t)g * kdim : 0);
   for (int k = 2 * tid; k < kdim; k += 2 * GV_THREADS) {
     const uint32_t u = *reinterpret_cast<const uint32_t*>(x + k);
@@ -92,54 +98,52 @@ __global__ void __launch_bounds__(GV_THREADS) k_int4_gemv(GemvArgs a) {
   float acc[GV_TILES][2];
 #pragma unroll
   for (int i = 0; i < GV_TILES; ++i) acc[i][0] = acc[i][1] = 0.0f;
-  for (; gq < gq1; gq += GV_WARPS) {
-    const bool more = gq + GV_WARPS < gq1;
-    if (more) load(gq + GV_WARPS, nxt);
-    float d[GV_TILES][4];
+  for (; gq < gq1; gq += NB * GV_WARPS) {
 #pragma unroll
-    for (int i = 0; i < GV_TILES; ++i) d[i][0] = d[i][1] = d[i][2] = d[i][3] = 0.0f;
-    float c1 = 0.0f, c16 = 0.0f;  // this lane's share of C_g: sum b over class-1 / class-16 columns
+    for (int b = 0; b < NB; ++b) {
+      const int gb = gq + b * GV_WARPS;
+      if (gb >= gq1) break;
+      float d[GV_TILES][4];
 #pragma unroll
-    for (int c = 0; c < 2; ++c)
+      for (int i = 0; i < GV_TILES; ++i) d[i][0] = d[i][1] = d[i][2] = d[i][3] = 0.0f;
+      float c1 = 0.0f, c16 = 0.0f;  // this lane's share of C_g: sum b over class-1 / class-16 columns
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const int kb = 8 * gq + 4 * c + v;  // k16 block
-        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&xh[16 * kb + 2 * ti]);
-        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(&xh[16 * kb + 8 + 2 * ti]);
-        const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&b0));
-        const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&b1));
-        c1 = __fadd_rn(__fadd_rn(c1, f0.x), f0.y);
-        c16 = __fadd_rn(__fadd_rn(c16, f1.x), f1.y);
+      for (int c = 0; c < 2; ++c)
 #pragma unroll
-        for (int i = 0; i < GV_TILES; ++i) {
-          const uint32_t w = v == 0 ? cur[i][c].x : v == 1 ? cur[i][c].y : v == 2 ? cur[i][c].z : cur[i][c].w;
-          const uint32_t w8 = w >> 8;
-          uint32_t af[4];
-          af[0] = lop_magic(w, 0x000F000Fu);   // (r0, c..c+1)     1024 + q
-          af[1] = lop_magic(w8, 0x000F000Fu);  // (r1, c..c+1)
-          af[2] = lop_magic(w, 0x00F000F0u);   // (r0, c+8..c+9)   1024 + 16 q
-          af[3] = lop_magic(w8, 0x00F000F0u);  // (r1, c+8..c+9)
-          mma16816(d[i], af, b0, b1);
+        for (int v = 0; v < 4; ++v) {
+          const int kb = 8 * gb + 4 * c + v;  // k16 block
+          const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&xh[16 * kb + 2 * ti]);
+          const uint32_t b1 = *reinterpret_cast<const uint32_t*>(&xh[16 * kb + 8 + 2 * ti]);
+          const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&b0));
+          const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&b1));
+          c1 = __fadd_rn(__fadd_rn(c1, f0.x), f0.y);
+          c16 = __fadd_rn(__fadd_rn(c16, f1.x), f1.y);
+#pragma unroll
+          for (int i = 0; i < GV_TILES; ++i) {
+            const uint4 wv = buf[b][i][c];
+            const uint32_t w = v == 0 ? wv.x : v == 1 ? wv.y : v == 2 ? wv.z : wv.w;
+            const uint32_t w8 = w >> 8;
+            uint32_t af[4];
+            af[0] = lop_magic(w, 0x000F000Fu);   // (r0, c..c+1)     1024 + q
+            af[1] = lop_magic(w8, 0x000F000Fu);  // (r1, c..c+1)
+            af[2] = lop_magic(w, 0x00F000F0u);   // (r0, c+8..c+9)   1024 + 16 q
+            af[3] = lop_magic(w8, 0x00F000F0u);  // (r1, c+8..c+9)
+            mma16816(d[i], af, b0, b1);
+          }
         }
-      }
-    // C_g over the quad's four column slices (lanes ti = 0..3 of a row group), fixed order
-    float cl = fmaf(1152.0f, c16, __fmul_rn(1032.0f, c1));
-    cl = __fadd_rn(cl, __shfl_xor_sync(0xffffffffu, cl, 1));
-    cl = __fadd_rn(cl, __shfl_xor_sync(0xffffffffu, cl, 2));
-#pragma unroll
-    for (int i = 0; i < GV_TILES; ++i) {
-      const int r0 = 16 * (rt0 + i) + gi;
-      const float s0 = bf2f(sc[(int64_t)r0 * ngr + gq]), s1 = bf2f(sc[(int64_t)(r0 + 8) * ngr + gq]);
-      acc[i][0] = fmaf(s0, __fsub_rn(d[i][0], cl), acc[i][0]);  // every B column is x: column 2 ti == column 0
-      acc[i][1] = fmaf(s1, __fsub_rn(d[i][2], cl), acc[i][1]);
-    }
-    if (more) {
+      // C_g over the quad's four column slices (lanes ti = 0..3 of a row group), fixed order
+      float cl = fmaf(1152.0f, c16, __fmul_rn(1032.0f, c1));
+      cl = __fadd_rn(cl, __shfl_xor_sync(0xffffffffu, cl, 1));
+      cl = __fadd_rn(cl, __shfl_xor_sync(0xffffffffu, cl, 2));
 #pragma unroll
       for (int i = 0; i < GV_TILES; ++i) {
-        cur[i][0] = nxt[i][0];
-        cur[i][1] = nxt[i][1];
+        const int r0 = 16 * (rt0 + i) + gi;
+        const float s0 = bf2f(sc[(int64_t)r0 * ngr + gb]), s1 = bf2f(sc[(int64_t)(r0 + 8) * ngr + gb]);
+        acc[i][0] = fmaf(s0, __fsub_rn(d[i][0], cl), acc[i][0]);  // every B column is x: column 2 ti == column 0
+        acc[i][1] = fmaf(s1, __fsub_rn(d[i][2], cl), acc[i][1]);
       }
     }
+    if (gq + NB * GV_WARPS < gq1) load_batch(gq + NB * GV_WARPS);
   }
   if (ti == 0) {
 #pragma unroll
