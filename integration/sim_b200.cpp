@@ -12,7 +12,7 @@
 namespace moespeq {
 
 namespace {
-CycleRecord cycle_from_json(const nlohmann::json& c) {
+CycleRecord cycle_from_json(const nlohmann::ordered_json& c) {
   CycleRecord r;
   r.cycle_index = c["cycle"];
   r.k_used = c["k"];
@@ -31,8 +31,8 @@ CycleRecord cycle_from_json(const nlohmann::json& c) {
   for (const auto& s : c["segments"])
     r.segments.push_back({s["label"].get<std::string>(), s["start_s"].get<double>(), s["duration_s"].get<double>(),
                           s["lane"].get<std::string>() == "io" ? 1 : 0});
-  if (c.contains("prefetch_plan")) r.prefetch_plan = nlohmann::ordered_json::parse(c["prefetch_plan"].dump());
-  if (c.contains("execution_plan")) r.execution_plan = nlohmann::ordered_json::parse(c["execution_plan"].dump());
+  if (c.contains("prefetch_plan")) r.prefetch_plan = c["prefetch_plan"];
+  if (c.contains("execution_plan")) r.execution_plan = c["execution_plan"];
   return r;
 }
 }  // namespace
@@ -42,7 +42,7 @@ SimReport run_simulation_b200(const Trace& trace, const nlohmann::json& run_conf
   const std::string t = write_trace(trace), c = run_config.dump();
   if (const int s = mspq_replay(device, t.c_str(), c.c_str(), &out); s != 0)
     throw Error(s >= 1 && s <= 18 ? static_cast<ErrorCode>(s - 1) : ErrorCode::InvalidConfig, mspq_last_error());
-  const nlohmann::json j = nlohmann::json::parse(out);
+  const nlohmann::ordered_json j = nlohmann::ordered_json::parse(out);  // keeps the plans' key order
   mspq_free(out);
   SimReport r;
   r.total_tokens = j["total_tokens"];

@@ -1270,7 +1270,10 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
     E->ev_pool_next = 0;
     auto stream_layer = [&](int l) {  // layer l's experts into buffer l & 1, after layer l-2's GEMMs
       const int bi = l & 1;
-      if (l >= 2) CUDA_OK(cudaStreamWaitEvent(E->sx, E->pf_done[bi], 0));
+      if (l >= 2) {  // every stream that writes the buffer (copy; decode / home copies) waits for its readers
+        CUDA_OK(cudaStreamWaitEvent(E->sx, E->pf_done[bi], 0));
+        if (E->sdec) CUDA_OK(cudaStreamWaitEvent(E->sdec, E->pf_done[bi], 0));
+      }
       for (int e = 0; e < Ex; ++e) pf_bytes += copy_expert(E, l * Ex + e, E->pf_buf[bi] + (size_t)e * E->S16);
       CUDA_OK(cudaEventRecord(E->pf_ready[bi], E->codec ? E->sdec : E->sx));
     };
