@@ -198,6 +198,8 @@ int mspq_moe_int4_gemv(const int32_t* n_groups, const int32_t* group_expert, con
 /* row-major quantised INT4 q[rows][cols/8] (standard nibble order) -> fragment-major words
  * [rows/16][cols/64][32 lanes][4] for mspq_moe_int4_gemv (layout in gemv_int4.cu) */
 int mspq_fragtile_int4(const void* q, int rows, int cols, void* fq, void* stream);
+/* diagnostics: tile/batch variant of the draft GEMV (tools/gemv_bench.py A/B; 0 = the default) */
+int mspq_debug_gemv_variant(int v);
 /* row-major quantised INT4 (q[rows][cols/8] u32, standard nibble order; s[rows][cols/128] bf16)
  * -> tile-major [rows/128][cols/64][128][8] u32 + [rows/128][cols/128][128] bf16 */
 int mspq_tile_int4(const void* q, const void* s, int rows, int cols, void* tq, void* ts, void* stream);

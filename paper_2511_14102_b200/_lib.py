@@ -52,6 +52,7 @@ _SIGS = [
     ("mspq_attention_ws_bytes", c_ll, [c_int] * 4),
     ("mspq_attention", c_int, [c_void_p, c_int, c_ll] + [c_int] * 5 + [c_void_p] * 7),
     ("mspq_gate_topk_img", c_int, [c_void_p] * 4 + [c_int, c_ll] + [c_void_p] * 10 + [c_int] * 6 + [c_float, c_void_p, c_void_p]),
+    ("mspq_debug_gemv_variant", c_int, [c_int]),
     ("mspq_fragtile_int4", c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p]),
     ("mspq_moe_int4_gemv", c_int, [c_void_p] * 4 + [c_ll] + [c_int] * 6 + [c_void_p] * 3),
     ("mspq_moe_int4_tc", c_int, [c_void_p] * 8 + [c_ll] + [c_int] * 9 + [c_void_p] * 3),

@@ -214,6 +214,10 @@ int mspq_attention(const float* qkv, int splits, long long split_stride, int T, 
              1.0f / sqrtf((float)Dh), (unsigned char*)oimg, tc_bn(T), (float*)ws};
   CK(launch_attn_window(a, ST(stream)), "attention");
 }
+int mspq_debug_gemv_variant(int v) {
+  gemv_set_variant(v);
+  return MSPQ_OK;
+}
 int mspq_fragtile_int4(const void* q, int rows, int cols, void* fq, void* stream) {
   if (rows % 32 || cols % 128) return set_error(MSPQ_ERR_SHAPE_MISMATCH, "fragtile_int4: rows % 32, cols % 128");
   CK(launch_fragtile_int4((const uint32_t*)q, rows, cols, (uint32_t*)fq, ST(stream)), "fragtile_int4");

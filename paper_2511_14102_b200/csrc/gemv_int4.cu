@@ -25,7 +25,7 @@
 namespace mspq {
 namespace {
 
-constexpr int GV_WARPS = 8, GV_THREADS = 32 * GV_WARPS, GV_TILES = 2;  // 2 row tiles = 32 rows per CTA
+constexpr int GV_WARPS = 8, GV_THREADS = 32 * GV_WARPS;
 
 MSPQ_D void mma16816(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
   asm volatile(
@@ -39,11 +39,17 @@ MSPQ_D uint32_t lop_magic(uint32_t w, uint32_t mask) {
   asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(o) : "r"(w), "r"(mask), "r"(0x64006400u));  // (w & mask) | magic
   return o;
 }
+template <bool H256>
 MSPQ_D uint4 ldg_stream(const void* p) {
   uint4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p));
+  if (H256)
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+  else
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
   return v;
 }
 
@@ -53,7 +59,9 @@ MSPQ_D uint4 ldg_stream(const void* p) {
 // each group's bias C_g = sum_k c_k b_k is reduced from the B fragments the lanes already hold
 // (quad shuffles, fixed order) instead of a serial prologue.  K splits (W2) write separate planes
 // [split][groups][rows] that the next K1 combine sums in order.
+template <int GV_TILES, int NB, bool H256>
 __global__ void __launch_bounds__(GV_THREADS) k_int4_gemv(GemvArgs a) {
+  constexpr int ROWS = 16 * GV_TILES;
   pdl_enter();  // launched with launch_pdl (kernels.h)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int g = blockIdx.y, sp = blockIdx.z, S = gridDim.z;
@@ -62,7 +70,7 @@ __global__ void __launch_bounds__(GV_THREADS) k_int4_gemv(GemvArgs a) {
   const int kdim = a.kdim, ngr = kdim / 128, nchunk = kdim / 64;
   const int gq0 = sp * ngr / S, gq1 = (sp + 1) * ngr / S;
   uint16_t* xh = reinterpret_cast<uint16_t*>(smem_raw);            // [kdim] class-scaled fp16
-  float* red = reinterpret_cast<float*>(smem_raw + kdim * 2);       // [GV_WARPS][32] row partials
+  float* red = reinterpret_cast<float*>(smem_raw + kdim * 2);       // [GV_WARPS][ROWS] row partials
   const int expert = a.group_expert[g];
   const unsigned char* blob = a.blobs + ((int64_t)a.layer * a.E + expert) * a.blob_bytes;
   const uint4* q = reinterpret_cast<const uint4*>(blob + a.q_off);
@@ -71,7 +79,6 @@ __global__ void __launch_bounds__(GV_THREADS) k_int4_gemv(GemvArgs a) {
   const int gi = lane >> 2, ti = lane & 3;
   // memory-level parallelism: a warp issues the loads of NB scale groups (NB x 2 KB) at once,
   // then multiplies them; the first batch is issued before the x prologue
-  constexpr int NB = 4;
   uint4 buf[NB][GV_TILES][2];
   auto load_batch = [&](int gfirst) {
 #pragma unroll
@@ -82,7 +89,7 @@ __global__ void __launch_bounds__(GV_THREADS) k_int4_gemv(GemvArgs a) {
         for (int i = 0; i < GV_TILES; ++i)
 #pragma unroll
           for (int c = 0; c < 2; ++c)
-            buf[b][i][c] = ldg_stream(q + (((int64_t)(rt0 + i) * nchunk + 2 * gb + c) * 32 + lane));
+            buf[b][i][c] = ldg_stream<H256>(q + (((int64_t)(rt0 + i) * nchunk + 2 * gb + c) * 32 + lane));
     }
   };
   int gq = gq0 + warp;
@@ -148,21 +155,22 @@ __global__ void __launch_bounds__(GV_THREADS) k_int4_gemv(GemvArgs a) {
   if (ti == 0) {
 #pragma unroll
     for (int i = 0; i < GV_TILES; ++i) {
-      red[warp * 32 + 16 * i + gi] = acc[i][0];
-      red[warp * 32 + 16 * i + gi + 8] = acc[i][1];
+      red[warp * ROWS + 16 * i + gi] = acc[i][0];
+      red[warp * ROWS + 16 * i + gi + 8] = acc[i][1];
     }
   }
   __syncthreads();
-  if (tid < 32) {
+  if (tid < ((ROWS + 31) & ~31)) {  // whole warps (the shuffle below needs every lane)
     float v = 0.0f;
+    if (tid < ROWS)
 #pragma unroll
-    for (int w = 0; w < GV_WARPS; ++w) v = __fadd_rn(v, red[w * 32 + tid]);
-    const int row = 32 * blockIdx.x + tid;
+      for (int w = 0; w < GV_WARPS; ++w) v = __fadd_rn(v, red[w * ROWS + tid]);
+    const int row = ROWS * blockIdx.x + tid;
     if (a.act) {
-      // W13 rows 2i / 2i+1 = gate_i / up_i (adjacent lanes): act = bf16(silu(gate) * up)
+      // W13 rows 2i / 2i+1 = gate_i / up_i (adjacent lanes of one warp): act = bf16(silu(gate) * up)
       const float up = __shfl_down_sync(0xffffffffu, v, 1);
-      if ((tid & 1) == 0) a.act[(int64_t)g * (a.rows / 2) + row / 2] = f2bf(__fmul_rn(silu_det(v), up));
-    } else {
+      if ((tid & 1) == 0 && tid < ROWS) a.act[(int64_t)g * (a.rows / 2) + row / 2] = f2bf(__fmul_rn(silu_det(v), up));
+    } else if (tid < ROWS) {
       a.y[((int64_t)sp * gridDim.y + g) * a.rows + row] = v;
     }
   }
@@ -187,15 +195,30 @@ __global__ void k_fragtile_int4(const uint32_t* __restrict__ q, int rows, int co
 
 }  // namespace
 
-size_t gemv_smem_bytes(int kdim) { return (size_t)kdim * 2 + GV_WARPS * 32 * 4 + 16; }
+static int g_gemv_variant = 0;  // tools/gemv_bench.py A/B only (mspq_debug_gemv_variant)
+void gemv_set_variant(int v) { g_gemv_variant = v; }
 
-cudaError_t launch_int4_gemv(const GemvArgs& a, int max_groups, int ksplit, cudaStream_t st) {
-  const size_t smem = gemv_smem_bytes(a.kdim);
+template <int TILES, int NB, bool H256>
+static cudaError_t launch_gemv_v(const GemvArgs& a, int max_groups, int ksplit, cudaStream_t st) {
+  const size_t smem = (size_t)a.kdim * 2 + GV_WARPS * 16 * TILES * 4 + 16;
+  if (a.rows % (16 * TILES)) return cudaErrorInvalidValue;
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_int4_gemv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_int4_gemv<TILES, NB, H256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
     if (e != cudaSuccess) return e;
   }
-  return launch_pdl(k_int4_gemv, dim3(a.rows / 32, max_groups, ksplit), dim3(GV_THREADS), smem, st, a);
+  return launch_pdl(k_int4_gemv<TILES, NB, H256>, dim3(a.rows / (16 * TILES), max_groups, ksplit), dim3(GV_THREADS),
+                    smem, st, a);
+}
+
+cudaError_t launch_int4_gemv(const GemvArgs& a, int max_groups, int ksplit, cudaStream_t st) {
+  switch (g_gemv_variant) {
+    case 1: return launch_gemv_v<2, 4, true>(a, max_groups, ksplit, st);
+    case 2: return launch_gemv_v<4, 2, false>(a, max_groups, ksplit, st);
+    case 3: return launch_gemv_v<1, 4, false>(a, max_groups, ksplit, st);
+    case 4: return launch_gemv_v<2, 2, false>(a, max_groups, ksplit, st);
+    default: return launch_gemv_v<2, 4, false>(a, max_groups, ksplit, st);
+  }
 }
 
 cudaError_t launch_fragtile_int4(const uint32_t* q, int rows, int cols, uint32_t* fq, cudaStream_t st) {

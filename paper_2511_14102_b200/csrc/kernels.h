@@ -158,6 +158,7 @@ struct GemvArgs {
 };
 cudaError_t launch_int4_gemv(const GemvArgs& a, int max_groups, int ksplit, cudaStream_t st);
 cudaError_t launch_fragtile_int4(const uint32_t* q, int rows, int cols, uint32_t* fq, cudaStream_t st);
+void gemv_set_variant(int v);
 
 cudaError_t launch_umma_grouped(const UmmaArgs& a, int max_groups, int BN, cudaStream_t st);
 cudaError_t launch_umma_int4(const UmmaArgs& a, int max_groups, int BN, cudaStream_t st);

@@ -17,6 +17,7 @@ ap.add_argument("--model", default="phi")
 ap.add_argument("--split2", type=int, default=2)
 ap.add_argument("--iters", type=int, default=200)
 ap.add_argument("--tc", action="store_true", help="time the tcgen05 K2 (k_umma_int4p, tile-major blobs) instead")
+ap.add_argument("--variant", type=int, default=0, help="GEMV tile/batch variant (mspq_debug_gemv_variant)")
 a = ap.parse_args()
 cfg = m.ModelConfig.named(a.model)
 d, f, E, K = cfg.d, cfg.f, cfg.E, cfg.K
@@ -51,6 +52,7 @@ def run(i):
         check(lib().mspq_moe_int4_gemv(P(ng), P(pr), P(x), P(blobs), s4, 0, E, d, f, K, a.split2, P(act), P(y), None))
 
 
+check(lib().mspq_debug_gemv_variant(a.variant))
 for i in range(20):
     run(i)
 torch.cuda.synchronize()
@@ -61,5 +63,5 @@ for i in range(a.iters):
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / a.iters
-print(f"{'tcgen05 K2' if a.tc else 'GEMV'} {a.model}: {ms * 1e3:.1f} us per layer (W13 + W2 of {K} experts, {K * s4 / 1e6:.1f} MB) = "
+print(f"{'tcgen05 K2' if a.tc else 'GEMV v%d' % a.variant} {a.model}: {ms * 1e3:.1f} us per layer (W13 + W2 of {K} experts, {K * s4 / 1e6:.1f} MB) = "
       f"{K * s4 / (ms * 1e-3) / 1e12:.2f} TB/s")
