@@ -282,6 +282,17 @@ int mspq_cache_replay_cycle(mspq_cache* c, const int32_t* target, const int32_t*
                             int32_t* out_cov, int32_t* out_step, int32_t* out_flush_keys,
                             void* stream);
 
+/* the whole trace in ONE launch: the Amortization-Roofline governor runs on the device between
+ * cycles (same double arithmetic as mspq_governor), cycle ci writes its ReplayOut block to
+ * slices + ci * stride at offsets {batches, jit_rows, cov, step} (counts at 0) and k_eff[ci].
+ * acc[n] = the trace's acc flags; gov_ints = {use_governor, fixed_k, k_min, k_max, k_slo, kcap};
+ * gov_reals = {ema_alpha, initial_accept, pcie_bw, pcie_init, pcie_overhead, expert_bytes,
+ * draft_base, draft_per_token}; vs_xy = nvs verify samples (window, seconds). */
+int mspq_cache_replay_all(mspq_cache* c, const int32_t* target, const int32_t* draft, const double* gates,
+                          const unsigned char* acc, int n, const int32_t* gov_ints, const double* gov_reals,
+                          int nvs, const double* vs_xy, int32_t* slices, int stride, const int32_t* offsets,
+                          int32_t* k_eff, int32_t* n_cycles, int32_t* flush_keys, void* stream);
+
 /* ---------------------------------------------------------------- (2) engine */
 /* run_simulation on the device control plane: trace = reference JSONL (trace.hpp:76-80),
  * config = reference run-config JSON (run_config.hpp:30-50).  *report_json: SimReport JSON;

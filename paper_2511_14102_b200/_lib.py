@@ -78,6 +78,8 @@ _SIGS = [
     ("mspq_cache_plan_row", c_int, [c_void_p, c_int, c_void_p]),
     ("mspq_cache_verify_layer", c_int, [c_void_p, c_int, c_int] + [c_void_p] * 3),
     ("mspq_cache_replay_cycle", c_int, [c_void_p] * 4 + [c_int] * 3 + [c_void_p] * 7),
+    ("mspq_cache_replay_all", c_int, [c_void_p] * 5 + [c_int, c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_int]
+     + [c_void_p] * 5),
     ("mspq_replay", c_int, [c_int, c_char_p, c_char_p, ctypes.POINTER(c_void_p)]),
     ("mspq_governor", c_int, [c_char_p, ctypes.POINTER(c_void_p)]),
     ("mspq_compare_policies", c_int, [c_int, c_char_p, c_char_p, c_char_p, c_char_p, ctypes.POINTER(c_void_p)]),

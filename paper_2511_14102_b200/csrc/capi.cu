@@ -463,4 +463,36 @@ int mspq_cache_replay_cycle(mspq_cache* c, const int32_t* target, const int32_t*
   CK(ctl_replay_cycle(c->C, tr, pos, k_eff, head_pos, o, ST(stream)), "cache_replay_cycle");
 }
 
+// whole-trace replay (one launch, governor on the device); see include/mspq_capi.h
+int mspq_cache_replay_all(mspq_cache* c, const int32_t* target, const int32_t* draft, const double* gates,
+                          const unsigned char* acc, int n, const int32_t* gov_ints, const double* gov_reals,
+                          int nvs, const double* vs_xy, int32_t* slices, int stride, const int32_t* offsets,
+                          int32_t* k_eff, int32_t* n_cycles, int32_t* flush_keys, void* stream) {
+  if (nvs < 2 || nvs > 16) return set_error(MSPQ_ERR_INSUFFICIENT_SAMPLES, "replay_all: 2..16 verify samples");
+  GovDev g{};
+  g.use_gov = gov_ints[0];
+  g.fixed_k = gov_ints[1];
+  g.k_min = gov_ints[2];
+  g.k_max = gov_ints[3];
+  g.k_slo = gov_ints[4];
+  g.kcap = gov_ints[5];
+  if (g.kcap > 64 || g.kcap > c->kmax) return set_error(MSPQ_ERR_K_OUT_OF_RANGE, "replay_all: k above kmax");
+  g.alpha = gov_reals[0];
+  g.initial_accept = gov_reals[1];
+  g.pcie_bw = gov_reals[2];
+  g.init_lat = gov_reals[3];
+  g.overhead = gov_reals[4];
+  g.expert_bytes = gov_reals[5];
+  g.draft_base = gov_reals[6];
+  g.draft_tok = gov_reals[7];
+  g.nvs = nvs;
+  for (int i = 0; i < nvs; ++i) {
+    g.vs_x[i] = vs_xy[2 * i];
+    g.vs_y[i] = vs_xy[2 * i + 1];
+  }
+  ReplayTrace tr{target, draft, gates};
+  ReplayAllOut o{slices, stride, offsets[0], offsets[1], offsets[2], offsets[3], k_eff, n_cycles, flush_keys};
+  CK(ctl_replay_all(c->C, tr, acc, n, g, o, ST(stream)), "cache_replay_all");
+}
+
 }  // extern "C"

@@ -854,6 +854,84 @@ MSPQ_D void flush_requests(const CtlDev& G, const CtlDev& S) {
   (void)src;
 }
 
+// ------------------------------------------------------------------ whole-trace replay
+// The governor in IEEE double with explicit round-to-nearest ops (no FMA contraction), the same
+// operation sequence as engine.cpp / perfmodel.cpp, so select_k picks the host's k bit for bit.
+MSPQ_D double gv_k_accept(const double* p, int k) {  // perfmodel.cpp:85-97
+  double sum = 0.0, prefix = 1.0;
+  for (int i = 0; i < k; ++i) {
+    prefix = __dmul_rn(prefix, p[i]);
+    sum = __dadd_rn(sum, prefix);
+  }
+  return sum;
+}
+MSPQ_D double gv_t_verify(const GovDev& g, double window) {  // perfmodel.cpp:112-123
+  int hi = 1;
+  while (hi + 1 < g.nvs && g.vs_x[hi] < window) ++hi;
+  const double x0 = g.vs_x[hi - 1], y0 = g.vs_y[hi - 1], x1 = g.vs_x[hi], y1 = g.vs_y[hi];
+  const double t = __ddiv_rn(__dsub_rn(window, x0), __dsub_rn(x1, x0));
+  return __dadd_rn(y0, __dmul_rn(t, __dsub_rn(y1, y0)));
+}
+MSPQ_D double gv_t_cycle(const GovDev& g, int k, int n) {  // perfmodel.cpp:99-128
+  const double td = __dadd_rn(g.draft_base, __dmul_rn((double)k, g.draft_tok));
+  const double tp = n == 0 ? 0.0 : __dadd_rn(g.overhead, __ddiv_rn(__dmul_rn((double)n, g.expert_bytes), g.pcie_bw));
+  return __dadd_rn(__dadd_rn(fmax(td, g.init_lat), tp), gv_t_verify(g, (double)(k + 1)));
+}
+MSPQ_D int gv_select_k(const GovDev& g, const double* p, double gg) {  // perfmodel.cpp:166-183
+  const int hi = min(g.k_max, g.k_slo);
+  int best_k = g.k_min;
+  double best = -1.0;
+  for (int k = g.k_min; k <= hi; ++k) {
+    const int est = (int)llround(__dmul_rn(gg, (double)k));
+    const double v = __ddiv_rn(gv_k_accept(p, k), gv_t_cycle(g, k, est));
+    if (v > best) {
+      best = v;
+      best_k = k;
+    }
+  }
+  return best_k;
+}
+
+MSPQ_D void body_replay_all(CtlDev C, ReplayTrace tr, const unsigned char* acc, int n, GovDev gv, ReplayAllOut o) {
+  __shared__ double p[64];
+  __shared__ int k_sh;
+  const int lane = lane_id();
+  for (int i = lane; i < gv.kcap; i += 32) p[i] = gv.initial_accept;
+  double gg = (double)C.L * (double)C.K;
+  int pos = 0, head_pos = -1, ci = 0;
+  __syncwarp();
+  while (pos < n) {
+    const int rem = n - pos;
+    if (lane == 0) k_sh = gv.use_gov ? gv_select_k(gv, p, gg) : gv.fixed_k;
+    __syncwarp();
+    const int k_eff = min(k_sh, rem);
+    int* sl = o.slices + (size_t)ci * o.stride;
+    ReplayOut oc{sl, sl + o.o_batch, sl + o.o_jit, sl + o.o_cov, sl + o.o_step, o.flush_keys};
+    body_replay_cycle(C, tr, pos, k_eff, head_pos, oc);
+    __syncwarp();
+    const int fetched = ((volatile int*)sl)[R_FETCHED];
+    int accepted = 0;
+    while (accepted < k_eff && acc[pos + accepted]) ++accepted;
+    const int consumed = min(accepted + 1, rem);
+    const int bonus = consumed - min(accepted, consumed);
+    if (lane == 0) {
+      o.k_eff[ci] = k_eff;
+      // EMA over the outcomes up to and including the first rejection (perfmodel.cpp:206-217)
+      for (int i = 0; i < k_eff && i < gv.kcap; ++i) {
+        const bool ok = acc[pos + i] != 0;
+        p[i] = __dadd_rn(__dmul_rn(__dsub_rn(1.0, gv.alpha), p[i]), __dmul_rn(gv.alpha, ok ? 1.0 : 0.0));
+        if (!ok) break;
+      }
+    }
+    gg = __ddiv_rn((double)fetched, (double)k_eff);
+    head_pos = bonus > 0 ? pos + accepted : -1;
+    pos += consumed;
+    ++ci;
+    __syncwarp();
+  }
+  if (lane == 0) *o.n_cycles = ci;
+}
+
 // STAGED is a template parameter so the state pointers' address space (shared vs global) is
 // known at compile time inside the control logic.
 #define CTL_KERNEL(NAME, BODY, ELB, PARAMS, ARGS)                   \
@@ -878,6 +956,10 @@ CTL_KERNEL(k_ctl_verify_layer, body_verify_layer, true,
            (CtlDev C, int l, int nslots, const int32_t* tgt, int32_t* gbuf), (S, l, nslots, tgt, gbuf))
 CTL_KERNEL(k_ctl_replay_cycle, body_replay_cycle, false,
            (CtlDev C, ReplayTrace tr, int pos, int k_eff, int head_pos, ReplayOut o), (S, tr, pos, k_eff, head_pos, o))
+
+CTL_KERNEL(k_ctl_replay_all, body_replay_all, false,
+           (CtlDev C, ReplayTrace tr, const unsigned char* acc, int n, GovDev gv, ReplayAllOut o),
+           (S, tr, acc, n, gv, o))
 
 size_t ctl_stage_bytes(const CtlDev& C, bool elb) {
   const size_t b = stage_bytes_of(C.L, C.E, C.K, C.nbuf, C.kmax, elb);
@@ -936,6 +1018,12 @@ cudaError_t ctl_verify_layer(const CtlDev& C, int l, int nslots, const int32_t* 
 cudaError_t ctl_replay_cycle(const CtlDev& C, const ReplayTrace& tr, int pos, int k_eff,
                              int head_pos, const ReplayOut& o, cudaStream_t st) {
   CTL_LAUNCH(k_ctl_replay_cycle, false, C, tr, pos, k_eff, head_pos, o);
+  return cudaGetLastError();
+}
+
+cudaError_t ctl_replay_all(const CtlDev& C, const ReplayTrace& tr, const unsigned char* acc, int n,
+                           const GovDev& gv, const ReplayAllOut& o, cudaStream_t st) {
+  CTL_LAUNCH(k_ctl_replay_all, false, C, tr, acc, n, gv, o);
   return cudaGetLastError();
 }
 

@@ -66,6 +66,28 @@ struct ReplayOut {
   int* flush_keys;  // [L*E]
 };
 
+// Whole-trace replay in one launch (k_ctl_replay_all): the Amortization-Roofline governor runs on
+// the device between cycles (perfmodel.cpp:85-217 in IEEE double, no contraction, bit-identical to
+// the host's), so no per-cycle host round trip.  Per-cycle outputs go to slices of `stride` ints
+// laid out like one ReplayOut (counts | batches | jit_rows | cov | step) at slot ci.
+struct GovDev {
+  int use_gov, fixed_k, k_min, k_max, k_slo, kcap;
+  double alpha, initial_accept;
+  double pcie_bw, init_lat, overhead, expert_bytes, draft_base, draft_tok;
+  int nvs;
+  double vs_x[16], vs_y[16];
+};
+struct ReplayAllOut {
+  int* slices;     // [max_cycles][stride]
+  int stride;      // ints per cycle slice
+  int o_batch, o_jit, o_cov, o_step;  // offsets inside a slice
+  int* k_eff;      // [max_cycles]
+  int* n_cycles;   // [1]
+  int* flush_keys; // [L*E] scratch
+};
+cudaError_t ctl_replay_all(const CtlDev& C, const ReplayTrace& tr, const unsigned char* acc, int n,
+                           const GovDev& gv, const ReplayAllOut& o, cudaStream_t st);
+
 size_t ctl_stage_bytes(const CtlDev& C, bool elb);
 cudaError_t ctl_reset(const CtlDev& C, int nbuf, cudaStream_t st);
 cudaError_t ctl_begin_cycle(const CtlDev& C, int k, cudaStream_t st);

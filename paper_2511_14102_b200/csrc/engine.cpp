@@ -484,6 +484,49 @@ std::string replay(int device, const std::string& trace_text, const std::string&
   int k_slo = c.k_slo;
   if (c.use_governor && c.ttft_budget > 0.0) k_slo = std::min(k_slo, k_slo_from_ttft(prof, c.ttft_budget, est(), c.k_min, c.k_max));
 
+  // Without per-event logs or plans the whole trace runs in ONE device launch with the governor on
+  // the device (mspq_cache_replay_all); the host then walks the per-cycle slices with the timing
+  // model below and re-derives every k to check the device's choice.  With logs/plans (tests) each
+  // cycle is one launch.
+  const bool all_mode = !c.log && !c.collect_plans && (int)prof.verify_samples.size() <= 16;
+  std::vector<int32_t> k_dev;
+  int32_t* h_all = nullptr;
+  if (all_mode) {
+    std::vector<unsigned char> acc8(t.acc.begin(), t.acc.end());
+    unsigned char* d_acc;
+    int32_t *d_slices, *d_k, *d_nc;
+    CUDA_OK(cudaMalloc(&d_acc, (size_t)n));
+    guard.d.push_back(d_acc);
+    CUDA_OK(cudaMalloc(&d_slices, (size_t)n * o_end * 4));
+    guard.d.push_back(d_slices);
+    CUDA_OK(cudaMalloc(&d_k, (size_t)n * 4));
+    guard.d.push_back(d_k);
+    CUDA_OK(cudaMalloc(&d_nc, 4));
+    guard.d.push_back(d_nc);
+    CUDA_OK(cudaMemcpyAsync(d_acc, acc8.data(), (size_t)n, cudaMemcpyHostToDevice, st));
+    const int32_t gi[6] = {c.use_governor ? 1 : 0, c.fixed_k, c.k_min, c.k_max, k_slo, kcap};
+    const double gr[8] = {c.ema_alpha, c.initial_accept, prof.pcie_bandwidth, prof.pcie_init_latency,
+                          prof.pcie_overhead, static_cast<double>(prof.expert_size_bytes), prof.draft_base,
+                          prof.draft_per_token};
+    std::vector<double> vs;
+    for (auto& [w, tv] : prof.verify_samples) {
+      vs.push_back(w);
+      vs.push_back(tv);
+    }
+    const int32_t offs[4] = {(int32_t)o_batch, (int32_t)o_jit, (int32_t)o_cov, (int32_t)o_step};
+    CAPI_OK(mspq_cache_replay_all(cache, d_tgt, d_dr, d_g, d_acc, n, gi, gr, (int)prof.verify_samples.size(),
+                                  vs.data(), d_slices, (int)o_end, offs, d_k, d_nc, d_flush, st));
+    int32_t nc = 0;
+    CUDA_OK(cudaMemcpyAsync(&nc, d_nc, 4, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaStreamSynchronize(st));
+    if (nc < 1 || nc > n) fail(MSPQ_ERR_INTERNAL, "replay_all: cycle count");
+    k_dev.resize(nc);
+    CUDA_OK(cudaHostAlloc((void**)&h_all, (size_t)nc * o_end * 4, 0));
+    guard.h.push_back(h_all);
+    CUDA_OK(cudaMemcpy(h_all, d_slices, (size_t)nc * o_end * 4, cudaMemcpyDeviceToHost));
+    CUDA_OK(cudaMemcpy(k_dev.data(), d_k, (size_t)nc * 4, cudaMemcpyDeviceToHost));
+  }
+
   double now = 0.0, step_cov_total = 0.0, layer_cov_total = 0.0, stall = 0.0;
   uint64_t step_total = 0, layer_cov_count = 0, acc_total = 0, total_new = 0;
   int pos = 0, ci = 0, head_pos = -1;
@@ -501,10 +544,16 @@ std::string replay(int device, const std::string& trace_text, const std::string&
     json segs = json::array();
     const double draft_dur = t_draft(prof, k_eff), draft_end = t0 + draft_dur;
     segs.push_back(segment("compute", "draft", t0, draft_dur));
-    CAPI_OK(mspq_cache_replay_cycle(cache, d_tgt, d_dr, d_g, pos, k_eff, head_pos, d_out + o_counts,
-                                    d_out + o_batch, d_out + o_jit, d_out + o_cov, d_out + o_step, d_flush, st));
-    CUDA_OK(cudaMemcpyAsync(h_out, d_out, o_end * 4, cudaMemcpyDeviceToHost, st));
-    CUDA_OK(cudaStreamSynchronize(st));
+    if (all_mode) {
+      if (ci >= (int)k_dev.size() || k_dev[ci] != k_eff)
+        fail(MSPQ_ERR_INTERNAL, "replay_all: device governor chose a different k than the host");
+      h_out = h_all + (size_t)ci * o_end;
+    } else {
+      CAPI_OK(mspq_cache_replay_cycle(cache, d_tgt, d_dr, d_g, pos, k_eff, head_pos, d_out + o_counts,
+                                      d_out + o_batch, d_out + o_jit, d_out + o_cov, d_out + o_step, d_flush, st));
+      CUDA_OK(cudaMemcpyAsync(h_out, d_out, o_end * 4, cudaMemcpyDeviceToHost, st));
+      CUDA_OK(cudaStreamSynchronize(st));
+    }
     const int32_t* cnt = h_out + o_counts;
     if (cnt[5]) fail(MSPQ_ERR_OVERFLOW, "device controller overflow");
     const int fetched = cnt[1], demand = cnt[2], nplan = cnt[3], nbatch = cnt[0];

@@ -84,3 +84,27 @@ def test_replay_event_log_matches_python_oracle(cuda, ref):
                 for (k, tag, l, e, h, v) in log]
         gotn = [(kinds[ev[0]], ev[2], ev[3], ev[4], ev[5], ev[6]) for ev in dev]
         assert gotn == want, trial
+
+
+def test_replay_one_launch_path_against_reference(cuda, ref):
+    """Without logs / plans the whole trace replays in ONE launch with the governor on the device
+    (mspq_cache_replay_all): every report stays bit-exact with the reference run_simulation,
+    governor-chosen k included (the host re-derives each k and fails on a mismatch)."""
+    import paper_2511_14102_b200 as m
+    rng = random.Random(77)
+    pol = ["lru", "lookahead", "sp-sooner", "sp-later", "speculative"]
+    for trial in range(60):
+        L, N = rng.randint(1, 8), rng.randint(2, 32)
+        K = rng.randint(1, min(4, N - 1))
+        soft = 0.468 if K >= 2 else 0.0
+        tr = ref.generate_trace(L, N, K, rng.randint(1, 300), 0.441, soft, 1 - 0.441 - soft, rng.random(),
+                                rng.choice([0.0, 1.0, 2.0]), rng.randint(0, 10**9), expert_bytes=rng.choice([25_000_000, 157_286_400]))
+        cfg = {"policy": pol[trial % 5], "capacity_mode": rng.choice(["per_layer", "global"]),
+               "cache_capacity": K + rng.randint(0, N), "prefetch_budget": rng.randint(0, 4),
+               "k": rng.randint(1, 12)}
+        if rng.random() < 0.7:
+            cfg["k"] = "governor"
+            cfg["governor"] = {"k_min": 1, "k_max": rng.choice([8, 16]), "k_slo": 16}
+        want = ref.run_simulation(tr, cfg)
+        got = m.run_simulation(tr, cfg)
+        assert diff(got, want) is None, (trial, cfg, diff(got, want))
