@@ -212,12 +212,15 @@ static cudaError_t launch_gemv_v(const GemvArgs& a, int max_groups, int ksplit, 
 }
 
 cudaError_t launch_int4_gemv(const GemvArgs& a, int max_groups, int ksplit, cudaStream_t st) {
+  // default: 64 rows per CTA, 2 scale groups (8 KB per warp) per load batch -- best of the A/B at
+  // the three BASELINE shapes (profiles/r02/gemv_variants.txt: Phi 2.81, Qwen3 1.67, Mixtral 3.81
+  // TB/s in-stream; 32 rows x 4 groups: 2.74 / 1.30 / 3.50; tcgen05 K2: 1.49 / 0.86 / 1.88)
   switch (g_gemv_variant) {
     case 1: return launch_gemv_v<2, 4, true>(a, max_groups, ksplit, st);
-    case 2: return launch_gemv_v<4, 2, false>(a, max_groups, ksplit, st);
     case 3: return launch_gemv_v<1, 4, false>(a, max_groups, ksplit, st);
     case 4: return launch_gemv_v<2, 2, false>(a, max_groups, ksplit, st);
-    default: return launch_gemv_v<2, 4, false>(a, max_groups, ksplit, st);
+    case 5: return launch_gemv_v<2, 4, false>(a, max_groups, ksplit, st);
+    default: return launch_gemv_v<4, 2, false>(a, max_groups, ksplit, st);
   }
 }
 

@@ -547,9 +547,9 @@ void enqueue_draft_step(mspq_engine* E, cudaStream_t s) {
   const auto& m = E->m;
   const int K = m.K, L = m.L, d = m.d;
   // the draft GEMV: W13 in one pass (SiLU*up fused), W2 over K splits so a layer launches >= ~3
-  // CTAs per SM (d/32 row blocks x K experts x split2)
+  // CTAs per SM (d/64 row blocks x K experts x split2)
   E->yd_split1 = 1;
-  E->yd_split2 = std::max(1, std::min(m.f / 128, (3 * 148 + (d / 32) * K - 1) / ((d / 32) * K)));
+  E->yd_split2 = std::max(1, std::min(m.f / 128, (3 * 148 + (d / 64) * K - 1) / ((d / 64) * K)));
   int32_t* row = E->dst + 0;
   int32_t* cur_tok = E->dst + 1;
   int32_t* cur_pos = E->dst + 2;
