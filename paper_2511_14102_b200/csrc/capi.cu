@@ -225,7 +225,7 @@ int mspq_fragtile_int4(const void* q, int rows, int cols, void* fq, void* stream
 int mspq_moe_int4_gemv(const int32_t* n_groups, const int32_t* group_expert, const void* xn, const void* blobs,
                        long long blob_bytes, int layer, int E, int d, int f, int K, int split2, void* act, float* y,
                        void* stream) {
-  if (d % 128 || f % 128 || (2 * f) % 32 || d % 32 || K < 1 || split2 < 1 || split2 > f / 128)
+  if (d % 128 || f % 128 || K < 1 || split2 < 1 || split2 > f / 128)
     return set_error(MSPQ_ERR_SHAPE_MISMATCH, "moe_int4_gemv: d, f multiples of 128, 1 <= split2 <= f/128");
   const long long q13 = (long long)2 * f * d / 2, s13 = (long long)2 * f * (d / 128) * 2, q2 = (long long)d * f / 2;
   cudaStream_t st = ST(stream);
