@@ -11,7 +11,24 @@ CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libmspq.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-JSON_DIR = "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann"
+def _json_dir():
+    """Directory holding nlohmann/json.hpp (header-only, MIT): $MSPQ_JSON_DIR, else the first of the
+    usual install places, else the copy inside the venv's cudnn_frontend package."""
+    cands = [os.environ.get("MSPQ_JSON_DIR", ""), "/usr/include/nlohmann", "/usr/local/include/nlohmann"]
+    try:
+        import site
+        for sp in site.getsitepackages():
+            cands.append(os.path.join(sp, "include", "cudnn_frontend", "thirdparty", "nlohmann"))
+    except Exception:  # noqa: BLE001
+        pass
+    cands.append("/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann")
+    for c in cands:
+        if c and os.path.exists(os.path.join(c, "json.hpp")):
+            return c
+    raise RuntimeError("nlohmann/json.hpp not found: set MSPQ_JSON_DIR")
+
+
+JSON_DIR = _json_dir()
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I" + CSRC,
           "-I" + os.path.join(ROOT, "include"), "-I" + JSON_DIR]
@@ -51,8 +68,7 @@ def build(verbose=False, force=False):
         list(ex.map(run, jobs))
     objs = [os.path.join(OBJ, s + ".o") for s in SOURCES]
     if force or jobs or not os.path.exists(LIB):
-        run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcuda"] if False else
-            [NVCC] + ARCH + ["-shared", "-o", LIB] + objs)
+        run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs)
     return LIB
 
 
