@@ -11,8 +11,8 @@
  *                                   and build_elb's input, scheduler.cpp:41-63)
  *        mspq_build_schedule       expert-grouped entry schedule == reorder_verification
  *                                  (scheduler.cpp:339-357)
- *        mspq_moe_int4         K2  INT4 (RTN on the GPTQ sym g128 grid) grouped expert FFN for the draft
- *        mspq_moe_bf16         K3  bf16 grouped expert FFN for the verify (reads the HBM slot pool)
+ *        mspq_moe_int4_gemv    K2  INT4 (RTN on the GPTQ sym g128 grid) expert FFN of the draft token
+ *        mspq_moe_bf16_tc      K3  bf16 grouped expert FFN for the verify (reads the HBM slot pool)
  *        mspq_lm_head / mspq_argmax  logits + greedy token
  *        mspq_accept_scan      K5  accept rule (sim.cpp:352-365) on token ids
  *      plus weight generation / quantisation helpers used by tests.
@@ -128,17 +128,6 @@ int mspq_gate_topk_img(float* h, const float* y, const int32_t* entry_of, const 
 int mspq_build_schedule(const int32_t* ids, int T, int K, int E, const int32_t* gbuf, int32_t* n_groups,
                         int32_t* group_expert, int32_t* group_buf, int32_t* group_off,
                         int32_t* entry_tok, int32_t* entry_of, int32_t* entry_group, void* stream);
-/* K2: blobs = all L*E INT4 expert blobs, blob_bytes apart, indexed by layer*E + expert.
- * max_group_size = most entries any group can have (= window tokens T; 1 selects the M=1 path) */
-int mspq_moe_int4(const int32_t* n_groups, const int32_t* group_expert, const int32_t* group_buf,
-                  const int32_t* group_off, const int32_t* entry_tok, const void* xn, void* act,
-                  float* y, const void* blobs, long long blob_bytes, int layer, int E, int d,
-                  int f, int max_groups, int max_group_size, void* stream);
-/* K3: pool = HBM slot pool, group_buf[g] = buffer index of group g's expert */
-int mspq_moe_bf16(const int32_t* n_groups, const int32_t* group_expert, const int32_t* group_buf,
-                  const int32_t* group_off, const int32_t* entry_tok, const void* xn, void* act,
-                  float* y, const void* pool, long long blob_bytes, int E, int d, int f,
-                  int max_groups, int max_group_size, void* stream);
 /* K3 on tcgen05 (umma.cu): the same grouped FFN over TILE-MAJOR bf16 experts (each 128x64
  * block a contiguous SW128 K-major image, see mspq_tile_bf16).  Runs gather -> W13 GEMM ->
  * SiLU*up -> W2 GEMM.  split1/split2 = K splits of the two GEMMs; y = [split2][T*K][d] fp32

@@ -40,8 +40,6 @@ _SIGS = [
     ("mspq_embed", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p]),
     ("mspq_gate_topk", c_int, [c_void_p] * 4 + [c_int, c_ll] + [c_void_p] * 10 + [c_int] * 6 + [c_float, c_void_p]),
     ("mspq_build_schedule", c_int, [c_void_p, c_int, c_int, c_int] + [c_void_p] * 9),
-    ("mspq_moe_int4", c_int, [c_void_p] * 9 + [c_ll] + [c_int] * 6 + [c_void_p]),
-    ("mspq_moe_bf16", c_int, [c_void_p] * 9 + [c_ll] + [c_int] * 5 + [c_void_p]),
     ("mspq_moe_bf16_tc_ws_bytes", c_ll, [c_int] * 6),
     ("mspq_moe_bf16_tc", c_int, [c_void_p] * 8 + [c_ll] + [c_int] * 7 + [c_void_p] * 3),
     ("mspq_moe_bf16_tc_part", c_int, [c_void_p] * 8 + [c_ll] + [c_int] * 7 + [c_void_p] * 3 + [c_int, c_void_p]),

@@ -97,28 +97,6 @@ int mspq_build_schedule(const int32_t* ids, int T, int K, int E, const int32_t* 
   SchedPtrs s{n_groups, group_expert, group_buf, group_off, entry_tok, entry_of, entry_group};
   CK(launch_build_schedule(ids, T, K, E, gbuf, s, ST(stream)), "build_schedule");
 }
-int mspq_moe_int4(const int32_t* n_groups, const int32_t* group_expert, const int32_t* group_buf,
-                  const int32_t* group_off, const int32_t* entry_tok, const void* xn, void* act,
-                  float* y, const void* blobs, long long blob_bytes, int layer, int E, int d, int f,
-                  int max_groups, int max_group_size, void* stream) {
-  if (d % 256 || f % 256) return set_error(MSPQ_ERR_SHAPE_MISMATCH, "moe_int4: d, f % 256");
-  SchedPtrs s{(int32_t*)n_groups, (int32_t*)group_expert, (int32_t*)group_buf, (int32_t*)group_off,
-              (int32_t*)entry_tok, nullptr, nullptr};
-  ExpertArgs a{s, (const uint16_t*)xn, (uint16_t*)act, y, (const unsigned char*)blobs, blob_bytes,
-               layer, E, d, f};
-  CK(launch_expert(a, true, max_groups, max_group_size, ST(stream)), "moe_int4");
-}
-int mspq_moe_bf16(const int32_t* n_groups, const int32_t* group_expert, const int32_t* group_buf,
-                  const int32_t* group_off, const int32_t* entry_tok, const void* xn, void* act,
-                  float* y, const void* pool, long long blob_bytes, int E, int d, int f,
-                  int max_groups, int max_group_size, void* stream) {
-  if (d % 256 || f % 256) return set_error(MSPQ_ERR_SHAPE_MISMATCH, "moe_bf16: d, f % 256");
-  SchedPtrs s{(int32_t*)n_groups, (int32_t*)group_expert, (int32_t*)group_buf, (int32_t*)group_off,
-              (int32_t*)entry_tok, nullptr, nullptr};
-  ExpertArgs a{s, (const uint16_t*)xn, (uint16_t*)act, y, (const unsigned char*)pool, blob_bytes,
-               0, E, d, f};
-  CK(launch_expert(a, false, max_groups, max_group_size, ST(stream)), "moe_bf16");
-}
 long long mspq_moe_bf16_tc_ws_bytes(int d, int f, int T, int K, int max_groups, int max_split1) {
   const long long BN = tc_bn(T), N = (long long)T * K;
   auto al = [](long long b) { return (b + 1023) / 1024 * 1024; };

@@ -82,15 +82,6 @@ struct UmmaArgs {
   unsigned char* act_img = nullptr;  // K3 W13, split 1: fused SiLU*up straight into W2's B images
 };
 
-struct ExpertArgs {
-  SchedPtrs s;
-  const uint16_t* xn;           // [T][d] bf16 normed input
-  uint16_t* act;                // [N][f] bf16
-  float* y;                     // [N][d] fp32
-  const unsigned char* w_base;  // int4: all L*E draft blobs; bf16: slot pool
-  int64_t blob_bytes;
-  int layer, E, d, f;
-};
 
 // Draft-loop state living on the device so a draft step is a replayable CUDA graph.
 struct DraftState {
@@ -183,8 +174,6 @@ cudaError_t launch_embed(const uint16_t* embed, const uint16_t* pos, const int32
 cudaError_t launch_route(const RouteArgs& a, int T, cudaStream_t st);
 cudaError_t launch_build_schedule(const int32_t* ids, int T, int K, int E, const int32_t* gbuf,
                                   SchedPtrs s, cudaStream_t st);
-cudaError_t launch_expert(const ExpertArgs& a, bool int4, int max_groups, int max_group_size,
-                          cudaStream_t st);
 cudaError_t launch_lm_head(const uint16_t* xn, const uint16_t* lm, int T, int V, int d,
                            float* logits, cudaStream_t st);
 cudaError_t launch_argmax(const float* logits, int T, int V, int32_t* out, DraftState ds,

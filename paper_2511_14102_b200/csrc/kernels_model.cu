@@ -1,6 +1,7 @@
 // MoE decode math on sm_100a: weight init, INT4 (RTN on the GPTQ sym g128 grid) quantisation, embedding,
-// fused residual-combine + RMSNorm + router + top-k/softmax (K1), grouped expert FFN for the
-// INT4 draft (K2) and the bf16 verify (K3), LM head + argmax, accept/reject scan (K5).
+// fused residual-combine + RMSNorm + router + top-k/softmax (K1), the expert-grouped schedule,
+// LM head + argmax, accept/reject scan (K5).  The expert FFNs are on tensor cores: umma.cu (K3,
+// tcgen05) and gemv_int4.cu (the draft's K2).
 //
 // Layouts:
 //   bf16 expert blob  : W13[2f][d] rows interleaved (2i = gate_i, 2i+1 = up_i) ++ W2[d][f]
@@ -363,248 +364,6 @@ __global__ void __launch_bounds__(1024) k_build_schedule(const int32_t* __restri
   }
 }
 
-// ============================================================================ K2 / K3
-// Grouped expert GEMV on CUDA cores (v0).  One CTA = 8 warps; warp owns RPW output rows of one
-// group's expert for all of that group's entries (<= MT).  MODE 0: up/gate (interleaved rows,
-// SiLU*up epilogue -> bf16 act [entry][f]); MODE 1: down (-> fp32 y [entry][d]).
-template <int MODE, bool INT4, int RPW, int MT>
-__device__ __forceinline__ void grouped_rows_body(const ExpertArgs& a, int g, int m, int e0,
-                                                  const unsigned char* blob, int row0) {
-  const int lane = threadIdx.x & 31;
-  const int cols = MODE == 0 ? a.d : a.f;
-  constexpr int PR = MODE == 0 ? 2 * RPW : RPW;  // physical rows per warp
-  // weight pointers
-  const unsigned char* wq;
-  const uint16_t* ws;
-  const uint16_t* wb;
-  if (INT4) {
-    const int64_t q13 = (int64_t)2 * a.f * a.d / 2, s13 = (int64_t)2 * a.f * (a.d / 128) * 2;
-    const int64_t q2 = (int64_t)a.d * a.f / 2;
-    wq = blob + (MODE == 0 ? 0 : q13 + s13);
-    ws = reinterpret_cast<const uint16_t*>(blob + (MODE == 0 ? q13 : q13 + s13 + q2));
-    wb = nullptr;
-  } else {
-    wb = reinterpret_cast<const uint16_t*>(blob) + (MODE == 0 ? 0 : (int64_t)2 * a.f * a.d);
-    wq = nullptr;
-    ws = nullptr;
-  }
-  const int prow0 = MODE == 0 ? 2 * row0 : row0;
-  float acc[PR][MT];
-#pragma unroll
-  for (int r = 0; r < PR; ++r)
-#pragma unroll
-    for (int t = 0; t < MT; ++t) acc[r][t] = 0.0f;
-
-  if (!INT4) {
-    const int nch = cols >> 3;
-#pragma unroll 2
-    for (int c = lane; c < nch; c += 32) {
-      float wf[PR][8];
-#pragma unroll
-      for (int r = 0; r < PR; ++r) {
-        uint4 wv = ldg_nc_v4(wb + (int64_t)(prow0 + r) * cols + 8 * c);
-        bf16x8_to_f32(wv, wf[r]);
-      }
-#pragma unroll
-      for (int t = 0; t < MT; ++t) {
-        if (t < m) {
-          const uint16_t* xp = MODE == 0 ? a.xn + (int64_t)a.s.entry_tok[e0 + t] * a.d
-                                         : a.act + (int64_t)(e0 + t) * a.f;
-          uint4 xv = *reinterpret_cast<const uint4*>(xp + 8 * c);
-          float xf[8];
-          bf16x8_to_f32(xv, xf);
-#pragma unroll
-          for (int r = 0; r < PR; ++r)
-#pragma unroll
-            for (int e = 0; e < 8; ++e) acc[r][t] = fmaf(wf[r][e], xf[e], acc[r][t]);
-        }
-      }
-    }
-  } else {
-    const int nch = cols >> 5;  // 32 columns per 16-byte word group
-    const int ngr = cols >> 7;
-#pragma unroll 2
-    for (int c = lane; c < nch; c += 32) {
-      uint4 wv[PR];
-      float sc[PR];
-#pragma unroll
-      for (int r = 0; r < PR; ++r) {
-        wv[r] = ldg_nc_v4(wq + ((int64_t)(prow0 + r) * cols + 32 * c) / 2);
-        sc[r] = bf2f(ws[(int64_t)(prow0 + r) * ngr + (c >> 2)]);
-      }
-#pragma unroll
-      for (int t = 0; t < MT; ++t) {
-        if (t < m) {
-          const uint16_t* xp = MODE == 0 ? a.xn + (int64_t)a.s.entry_tok[e0 + t] * a.d
-                                         : a.act + (int64_t)(e0 + t) * a.f;
-          float xf[32];
-#pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            uint4 xv = *reinterpret_cast<const uint4*>(xp + 32 * c + 8 * v);
-            bf16x8_to_f32(xv, xf + 8 * v);
-          }
-#pragma unroll
-          for (int r = 0; r < PR; ++r) {
-            float p = 0.0f;
-            const uint32_t wr[4] = {wv[r].x, wv[r].y, wv[r].z, wv[r].w};
-#pragma unroll
-            for (int v = 0; v < 4; ++v)
-#pragma unroll
-              for (int n = 0; n < 8; ++n) {
-                const float qf = __uint_as_float(0x4B000000u | ((wr[v] >> (4 * n)) & 0xFu)) - 8388616.0f;
-                p = fmaf(qf, xf[8 * v + n], p);
-              }
-            acc[r][t] = fmaf(p, sc[r], acc[r][t]);
-          }
-        }
-      }
-    }
-  }
-  // reduce & epilogue
-#pragma unroll
-  for (int r = 0; r < PR; ++r)
-#pragma unroll
-    for (int t = 0; t < MT; ++t) acc[r][t] = warp_butterfly_sum(acc[r][t]);
-  if (lane == 0) {
-#pragma unroll
-    for (int t = 0; t < MT; ++t) {
-      if (t < m) {
-        if (MODE == 0) {
-#pragma unroll
-          for (int r = 0; r < RPW; ++r) {
-            const float gv = acc[2 * r][t], uv = acc[2 * r + 1][t];
-            a.act[(int64_t)(e0 + t) * a.f + row0 + r] = f2bf(__fmul_rn(silu_det(gv), uv));
-          }
-        } else {
-#pragma unroll
-          for (int r = 0; r < RPW; ++r) a.y[(int64_t)(e0 + t) * a.d + row0 + r] = acc[r][t];
-        }
-      }
-    }
-  }
-}
-
-// K2 fast path for one-entry groups (the draft decodes one token): x staged once in smem as fp32,
-// warp owns RPW output rows, lane owns 32-column chunks (one 16-byte word group of nibbles per
-// row), two chunks in flight per lane.  Per element: nibble->float (LOP3 + FADD via the 2^23
-// magic) and one FFMA; the group-128 scale is applied once per 32-column partial.
-template <int MODE, int RPW>
-__global__ void __launch_bounds__(256) k_int4_m1(ExpertArgs a) {
-  extern __shared__ __align__(16) float xs[];
-  const int g = blockIdx.y;
-  if (g >= *a.s.n_groups) return;
-  const int e0 = a.s.group_off[g];
-  const int cols = MODE == 0 ? a.d : a.f;
-  const uint16_t* xp = MODE == 0 ? a.xn + (int64_t)a.s.entry_tok[e0] * a.d : a.act + (int64_t)e0 * a.f;
-  for (int i = threadIdx.x; i < cols / 8; i += 256) {  // 16-byte loads, 8 bf16 -> 8 fp32
-    float f8[8];
-    bf16x8_to_f32(reinterpret_cast<const uint4*>(xp)[i], f8);
-    reinterpret_cast<float4*>(xs)[2 * i] = make_float4(f8[0], f8[1], f8[2], f8[3]);
-    reinterpret_cast<float4*>(xs)[2 * i + 1] = make_float4(f8[4], f8[5], f8[6], f8[7]);
-  }
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nrows = MODE == 0 ? a.f : a.d;
-  const unsigned char* blob = a.w_base + ((int64_t)a.layer * a.E + a.s.group_expert[g]) * a.blob_bytes;
-  const int64_t q13 = (int64_t)2 * a.f * a.d / 2, s13 = (int64_t)2 * a.f * (a.d / 128) * 2;
-  const int64_t q2 = (int64_t)a.d * a.f / 2;
-  const unsigned char* wq = blob + (MODE == 0 ? 0 : q13 + s13);
-  const uint16_t* ws = reinterpret_cast<const uint16_t*>(blob + (MODE == 0 ? q13 : q13 + s13 + q2));
-  constexpr int PR = MODE == 0 ? 2 * RPW : RPW;
-  const int nch = cols >> 5, ngr = cols >> 7;
-  // persistent over row blocks: the x staging above is paid once per CTA
-  for (int row0 = (blockIdx.x * 8 + warp) * RPW; row0 < nrows; row0 += gridDim.x * 8 * RPW) {
-  const int prow0 = MODE == 0 ? 2 * row0 : row0;
-  float acc[PR];
-#pragma unroll
-  for (int r = 0; r < PR; ++r) acc[r] = 0.0f;
-#pragma unroll 2
-  for (int c = lane; c < nch; c += 32) {
-    uint4 wv[PR];
-    float sc[PR];
-#pragma unroll
-    for (int r = 0; r < PR; ++r) {
-      wv[r] = ldg_nc_v4(wq + ((int64_t)(prow0 + r) * cols + 32 * c) / 2);
-      sc[r] = bf2f(ws[(int64_t)(prow0 + r) * ngr + (c >> 2)]);
-    }
-    float xf[32];
-#pragma unroll
-    for (int v = 0; v < 8; ++v) {
-      const float4 t = reinterpret_cast<const float4*>(xs + 32 * c)[v];
-      xf[4 * v] = t.x;
-      xf[4 * v + 1] = t.y;
-      xf[4 * v + 2] = t.z;
-      xf[4 * v + 3] = t.w;
-    }
-#pragma unroll
-    for (int r = 0; r < PR; ++r) {
-      const uint32_t wr[4] = {wv[r].x, wv[r].y, wv[r].z, wv[r].w};
-      float p = 0.0f;
-#pragma unroll
-      for (int v = 0; v < 4; ++v)
-#pragma unroll
-        for (int n = 0; n < 8; ++n) {
-          const float qf = __uint_as_float(0x4B000000u | ((wr[v] >> (4 * n)) & 0xFu)) - 8388616.0f;
-          p = fmaf(qf, xf[8 * v + n], p);
-        }
-      acc[r] = fmaf(p, sc[r], acc[r]);
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < PR; ++r) acc[r] = warp_butterfly_sum(acc[r]);
-  if (lane == 0) {
-    if (MODE == 0) {
-#pragma unroll
-      for (int r = 0; r < RPW; ++r)
-        a.act[(int64_t)e0 * a.f + row0 + r] = f2bf(__fmul_rn(silu_det(acc[2 * r]), acc[2 * r + 1]));
-    } else {
-#pragma unroll
-      for (int r = 0; r < RPW; ++r) a.y[(int64_t)e0 * a.d + row0 + r] = acc[r];
-    }
-  }
-  }
-}
-
-template <int MODE, bool INT4, int RPW>
-__global__ void __launch_bounds__(256) k_grouped_rows(ExpertArgs a) {
-  const int g = blockIdx.y;
-  if (g >= *a.s.n_groups) return;
-  const int e0 = a.s.group_off[g];
-  const int m = a.s.group_off[g + 1] - e0;
-  const int warp = threadIdx.x >> 5;
-  const int row0 = (blockIdx.x * 8 + warp) * RPW;
-  const int nrows = MODE == 0 ? a.f : a.d;
-  if (row0 >= nrows) return;
-  const unsigned char* blob;
-  if (INT4)
-    blob = a.w_base + ((int64_t)a.layer * a.E + a.s.group_expert[g]) * a.blob_bytes;
-  else
-    blob = a.w_base + (int64_t)a.s.group_buf[g] * a.blob_bytes;
-  if (INT4) {
-    for (int base = 0; base < m; base += 4) {
-      const int mm = min(4, m - base);
-      if (mm == 1)
-        grouped_rows_body<MODE, INT4, RPW, 1>(a, g, 1, e0 + base, blob, row0);
-      else
-        grouped_rows_body<MODE, INT4, RPW, 4>(a, g, mm, e0 + base, blob, row0);
-    }
-    return;
-  }
-  for (int base = 0; base < m; base += 16) {
-    const int mm = min(16, m - base);
-    if (mm == 1)
-      grouped_rows_body<MODE, INT4, RPW, 1>(a, g, 1, e0 + base, blob, row0);
-    else if (mm <= 2)
-      grouped_rows_body<MODE, INT4, RPW, 2>(a, g, mm, e0 + base, blob, row0);
-    else if (mm <= 4)
-      grouped_rows_body<MODE, INT4, RPW, 4>(a, g, mm, e0 + base, blob, row0);
-    else if (mm <= 8)
-      grouped_rows_body<MODE, INT4, RPW, 8>(a, g, mm, e0 + base, blob, row0);
-    else
-      grouped_rows_body<MODE, INT4, RPW, 16>(a, g, mm, e0 + base, blob, row0);
-  }
-}
-
 // ============================================================================ LM head
 // logits[t][v] by the same fixed-order warp dot as the router; one warp owns RPW vocab rows
 // for all T tokens.
@@ -766,43 +525,6 @@ cudaError_t launch_build_schedule(const int32_t* ids, int T, int K, int E, const
                                   SchedPtrs s, cudaStream_t st) {
   const int threads = std::max(32, (E + 31) / 32 * 32);
   return launch_pdl(k_build_schedule, dim3(1), dim3(threads), 0, st, ids, T, K, E, gbuf, s);
-}
-
-cudaError_t launch_expert(const ExpertArgs& a, bool int4, int max_groups, int max_group_size,
-                          cudaStream_t st) {
-  if (int4 && max_group_size == 1) {
-    constexpr int R0 = 2, R1 = 4;
-    const size_t sm0 = (size_t)a.d * 4, sm1 = (size_t)a.f * 4;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_int4_m1<0, R0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      cudaFuncSetAttribute(k_int4_m1<1, R1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      attr = true;
-    }
-    // ~4 CTAs per SM in total across the groups, each looping over row blocks
-    const int per_group = std::max(1, (148 * 4) / std::max(1, max_groups));
-    const int nb0 = std::min((a.f + 8 * R0 - 1) / (8 * R0), per_group);
-    const int nb1 = std::min((a.d + 8 * R1 - 1) / (8 * R1), per_group);
-    k_int4_m1<0, R0><<<dim3(nb0, max_groups), 256, sm0, st>>>(a);
-    k_int4_m1<1, R1><<<dim3(nb1, max_groups), 256, sm1, st>>>(a);
-    return cudaGetLastError();
-  }
-  constexpr int RPW0 = 2, RPW1 = 4;
-  {
-    dim3 grid((a.f + 8 * RPW0 - 1) / (8 * RPW0), max_groups);
-    if (int4)
-      k_grouped_rows<0, true, RPW0><<<grid, 256, 0, st>>>(a);
-    else
-      k_grouped_rows<0, false, RPW0><<<grid, 256, 0, st>>>(a);
-  }
-  {
-    dim3 grid((a.d + 8 * RPW1 - 1) / (8 * RPW1), max_groups);
-    if (int4)
-      k_grouped_rows<1, true, RPW1><<<grid, 256, 0, st>>>(a);
-    else
-      k_grouped_rows<1, false, RPW1><<<grid, 256, 0, st>>>(a);
-  }
-  return cudaGetLastError();
 }
 
 cudaError_t launch_lm_head(const uint16_t* xn, const uint16_t* lm, int T, int V, int d,

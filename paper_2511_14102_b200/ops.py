@@ -87,26 +87,6 @@ def build_schedule(ids, E):
     return s
 
 
-def moe_int4(s: Schedule, xn, blobs, blob_bytes, layer, E, d, f, max_group_size=None):
-    N = s.T * s.K
-    act = torch.empty(N, f, dtype=torch.int16, device=xn.device)
-    y = torch.empty(N, d, dtype=torch.float32, device=xn.device)
-    check(lib().mspq_moe_int4(_p(s.n_groups), _p(s.group_expert), _p(s.group_buf), _p(s.group_off),
-                              _p(s.entry_tok), _p(xn), _p(act), _p(y), _p(blobs), blob_bytes, layer,
-                              E, d, f, s.G, max_group_size or s.T, _s()))
-    return act, y
-
-
-def moe_bf16(s: Schedule, xn, pool, blob_bytes, E, d, f):
-    N = s.T * s.K
-    act = torch.empty(N, f, dtype=torch.int16, device=xn.device)
-    y = torch.empty(N, d, dtype=torch.float32, device=xn.device)
-    check(lib().mspq_moe_bf16(_p(s.n_groups), _p(s.group_expert), _p(s.group_buf), _p(s.group_off),
-                              _p(s.entry_tok), _p(xn), _p(act), _p(y), _p(pool), blob_bytes, E, d,
-                              f, s.G, s.T, _s()))
-    return act, y
-
-
 def tile_bf16(src_i16, rows, cols):
     dst = torch.empty(rows * cols, dtype=torch.int16, device=src_i16.device)
     check(lib().mspq_tile_bf16(_p(src_i16), rows, cols, _p(dst), _s()))

@@ -126,50 +126,6 @@ def test_argmax_tie_breaks_to_lower_id(cuda):
     assert ops.argmax(x).tolist() == [17, 4098]
 
 
-@pytest.mark.parametrize("name,E,K,d,f", SHAPES)
-@pytest.mark.parametrize("T", [1, 5])
-def test_moe_int4_and_bf16_within_tolerance(cuda, name, E, K, d, f, T):
-    """K2/K3 vs float64 oracle: |y - y_ref| <= 2e-3 * max|y_ref| + 1e-5 (fp32 accumulation,
-    bf16 activation rounding may flip by one bf16 ulp)."""
-    from paper_2511_14102_b200 import ops
-    L = 1
-    desc = om.ModelDesc(L=L, E=E, K=K, d=d, f=f, V=512, seed=13)
-    mdl = om.Model(desc)
-    T = min(T, 2) if name == "mixtral" else T
-    rng = np.random.default_rng(2)
-    ids = np.stack([rng.choice(E, K, replace=False) for _ in range(T)]).astype(np.int32)
-    used = sorted(set(ids.ravel().tolist()))
-    xn = om.f32_to_bf16(rng.standard_normal((T, d)).astype(np.float32))
-    s = ops.build_schedule(torch.from_numpy(ids).cuda(), E)
-    sb = ops.bf16_blob_bytes(d, f)
-    s4 = ops.int4_blob_bytes(d, f)
-    # bf16 pool: buffer index = expert id; int4 blobs for layer 0, all experts (only used filled)
-    pool = torch.zeros(E * sb // 2, dtype=torch.int16, device="cuda")
-    blobs = torch.zeros(E * s4, dtype=torch.uint8, device="cuda")
-    for e in used:
-        b = ops.fill_expert(desc.seed, 0, e, d, f, desc.a_up(), desc.a_down())
-        pool[e * sb // 2:(e + 1) * sb // 2] = b
-        q13, s13 = ops.quantize_int4(b[:2 * f * d], 2 * f, d)
-        q2, s2 = ops.quantize_int4(b[2 * f * d:], d, f)
-        parts = [q13.view(torch.uint8), s13.view(torch.uint8), q2.view(torch.uint8), s2.view(torch.uint8)]
-        blobs[e * s4:(e + 1) * s4] = torch.cat(parts)
-    ng = int(s.n_groups.item())
-    assert ng == len(used)
-    eo = s.entry_of.cpu().numpy().reshape(T, K)
-    for int4 in (False, True):
-        if int4:
-            _, y = ops.moe_int4(s, to_dev(xn), blobs, s4, 0, E, d, f)
-        else:
-            _, y = ops.moe_bf16(s, to_dev(xn), pool, sb, E, d, f)
-        y = y.cpu().numpy()
-        for t in range(T):
-            for j in range(K):
-                want, _ = mdl.ffn(xn[t], 0, int(ids[t, j]), draft=int4)
-                got = y[eo[t, j]]
-                tol = 2e-3 * np.abs(want).max() + 1e-5
-                assert np.abs(got - want).max() <= tol, (int4, t, j, np.abs(got - want).max(), tol)
-
-
 def test_schedule_is_reorder_verification(cuda):
     from paper_2511_14102_b200 import ops
     from oracle import control_plane as cp
