@@ -474,7 +474,7 @@ def sim_config(cfg: dict):
             c["profile"] = profile_from_json(v)
         elif k in ("policy", "capacity_mode", "cache_capacity", "entropy_weighted_capacity",
                    "prefetch_budget", "ema_alpha", "initial_accept", "collect_plans", "seed",
-                   "estimator", "verify_overlap", "log"):
+                   "estimator", "verify_overlap", "log", "prefetch_defer"):
             c[k] = v
         else:
             raise ValueError("unknown config key " + k)

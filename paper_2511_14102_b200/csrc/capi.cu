@@ -377,7 +377,7 @@ int mspq_cache_create(int L, int E, int K, int kmax, int nbuf, int log_cap, mspq
   C.plan = (int*)(b + o_plan);
   C.cov = (int*)(b + o_cov);
   C.step = (int*)(b + o_step);
-  C.stage = ctl_stage_bytes(C, true) > 0 && !getenv("MSPQ_CTL_NO_STAGING") ? 1 : 0;
+  C.stage = ctl_stage_bytes(C, true) > 0 ? 1 : 0;  // mspq_cache_set_staging(0) turns it off (tests)
   *out = c;
   return MSPQ_OK;
 }

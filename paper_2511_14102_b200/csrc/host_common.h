@@ -62,6 +62,9 @@ struct HostCfg {  // SimConfig (sim.hpp:15-34) from the run-config schema (run_c
   // (sim.cpp:75-78, 404; the parity default); 1 = "elb": per layer, the expected union of the
   // draft-predicted routing over a (k+1)-token window minus the experts resident now
   int estimator = 0;
+  // extension (live engine): issue a layer's plan prefetches behind the previous layer's demand
+  // copies (per-layer capacity mode) instead of in plan order at draft time
+  bool prefetch_defer = true;
 };
 int parse_policy(const std::string& s);
 const char* policy_name(int p);

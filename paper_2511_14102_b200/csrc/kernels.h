@@ -11,15 +11,13 @@ namespace mspq {
 // Programmatic dependent launch (PDL) for back-to-back kernels on one stream.  A kernel launched
 // with launch_pdl() may be resident before its predecessor finishes, so it must start with
 // pdl_enter(): griddepcontrol.wait (the predecessor's writes are complete and visible; nothing may be
-// read before it) then launch_dependents (lets the next PDL kernel get scheduled).  MSPQ_NO_PDL=1
-// launches plainly, for A/B timing.
+// read before it) then launch_dependents (lets the next PDL kernel get scheduled).
 #ifdef __CUDACC__
 __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
 }
 #endif
-bool pdl_disabled();
 template <typename... P, typename... A>
 inline cudaError_t launch_pdl(void (*kern)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                               A&&... args) {
@@ -32,7 +30,7 @@ inline cudaError_t launch_pdl(void (*kern)(P...), dim3 grid, dim3 block, size_t 
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = pdl_disabled() ? 0 : 1;
+  cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...);
 }
 

@@ -100,20 +100,12 @@ struct mspq_engine {
   cudaEvent_t ev_stage[2] = {nullptr, nullptr};
   char stage_rec[2] = {0, 0};
   int stage_next = 0;
-  // opt-in prefetch lane (MSPQ_PF_LANE=1): the planner's prefetches get their own copy stream,
-  // decode stream and staging pair, so a layer's demand copies do not queue behind them
-  bool pf_lane = false;
-  cudaStream_t sx2 = nullptr, sdec2 = nullptr;
-  unsigned char* stage2[2] = {nullptr, nullptr};
-  cudaEvent_t ev_stage2[2] = {nullptr, nullptr};
-  char stage_rec2[2] = {0, 0};
-  int stage_next2 = 0;
-  // deferred prefetch (default on; MSPQ_PF_DEFER=0 turns it off; per-layer capacity only): a plan prefetch for layer
-  // j >= 1 is issued on the demand stream right after layer j-1's demand copies, so it covers the
-  // layer boundary (GEMM, K1, controller) when the link would otherwise idle.  FIFO order on the
-  // stream keeps it ahead of any later demand write to the same per-layer slot.
+  // deferred prefetch (run-config "prefetch_defer", default on; per-layer capacity only): a plan
+  // prefetch for layer j >= 1 is issued on the demand stream right after layer j-1's demand
+  // copies, so it covers the layer boundary (GEMM, K1, controller) when the link would otherwise
+  // idle.  FIFO order on the stream keeps it ahead of any later demand write to the same slot.
   bool pf_defer = false;
-  int dec_ctas = 256;  // decode grid per chunk (MSPQ_DEC_CTAS, A/B switch)
+  static constexpr int dec_ctas = 256;  // decode grid per chunk (128 measured the same, profiles/r01)
   std::vector<std::pair<int, int>> deferred;  // (key, buf), plan order
   int n_payload = 0;
   bool host_is_shm = false;
@@ -933,12 +925,11 @@ static uint64_t copy_expert(mspq_engine* E, int key, unsigned char* dst) {
 
 static int issue_copies(mspq_engine* E, int cycle, CopyBatch& batch, uint64_t& bytes, bool prefetch = false,
                         const std::vector<std::pair<int, int>>* list = nullptr) {
-  const bool l2 = prefetch && E->pf_lane;
-  cudaStream_t sx = l2 ? E->sx2 : E->sx, sdec = l2 ? E->sdec2 : E->sdec;
-  unsigned char** stage = l2 ? E->stage2 : E->stage;
-  cudaEvent_t* ev_stage = l2 ? E->ev_stage2 : E->ev_stage;
-  char* stage_rec = l2 ? E->stage_rec2 : E->stage_rec;
-  int& stage_next = l2 ? E->stage_next2 : E->stage_next;
+  cudaStream_t sx = E->sx, sdec = E->sdec;
+  unsigned char** stage = E->stage;
+  cudaEvent_t* ev_stage = E->ev_stage;
+  char* stage_rec = E->stage_rec;
+  int& stage_next = E->stage_next;
   const int n = list ? (int)list->size() : E->view.host_stat[S_NREQ];
   if (!list) {
     if (E->view.host_stat[S_OVERFLOW]) fail(MSPQ_ERR_OVERFLOW, "device controller ran out of buffers / queue");
@@ -980,7 +971,6 @@ static int issue_copies(mspq_engine* E, int cycle, CopyBatch& batch, uint64_t& b
     }
     // two lanes: a slot may still be under a write issued on the other lane (a prefetch the
     // controller evicted before its use), so the new writer orders after it
-    if (E->pf_lane && E->ready_rec[buf]) CUDA_OK(cudaStreamWaitEvent(E->codec ? sdec : sx, E->ev_ready[buf], 0));
     if (!E->codec) {
       if (reused) CUDA_OK(cudaStreamWaitEvent(sx, E->ev_gemm[E->last_layer[buf]], 0));
       CUDA_OK(cudaMemcpyAsync(slot, E->host_blob(E->payload(key)), E->S16, cudaMemcpyHostToDevice, sx));
@@ -1073,10 +1063,7 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
   if (c.use_governor && c.ttft_budget > 0.0) k_slo = std::min(k_slo, k_slo_from_ttft(prof, c.ttft_budget, est(), c.k_min, c.k_max));
   CUDA_OK(cudaEventRecord(E->ev_t0, E->sc));
   CUDA_OK(cudaStreamWaitEvent(E->sx, E->ev_t0, 0));
-  {
-    const char* pd = getenv("MSPQ_PF_DEFER");
-    E->pf_defer = !(pd && pd[0] == '0') && c.mode == 0;  // on by default; MSPQ_PF_DEFER=0 is the A/B switch
-  }
+  E->pf_defer = c.prefetch_defer && c.mode == 0;  // run-config "prefetch_defer" (default on)
   E->deferred.clear();
   E->hcap_v_hist.clear();
   E->hcap_d_hist.clear();
@@ -1084,7 +1071,6 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
   E->hmid_d_hist.clear();
   E->gen_peer_bytes = E->gen_home_local_bytes = 0;
   E->n_peer = E->n_home_local = 0;
-  if (E->pf_lane) CUDA_OK(cudaStreamWaitEvent(E->sx2, E->ev_t0, 0));
   std::vector<int> committed;
   json cycles = json::array();
   double stall_total = 0.0, layer_cov_total = 0.0, step_cov_total = 0.0;
@@ -1665,8 +1651,6 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
   // everything (including trailing prefetches) has landed before we report
   CUDA_OK(cudaStreamSynchronize(E->sx));
   if (E->sdec) CUDA_OK(cudaStreamSynchronize(E->sdec));
-  if (E->sx2) CUDA_OK(cudaStreamSynchronize(E->sx2));
-  if (E->sdec2) CUDA_OK(cudaStreamSynchronize(E->sdec2));
   const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
   json rep;
   const double total_time = cycles.empty() ? 0.0
@@ -1840,11 +1824,7 @@ void destroy(mspq_engine* E) {
   for (int i = 0; i < 2; ++i) {
     if (E->stage[i]) cudaFree(E->stage[i]);
     if (E->ev_stage[i]) cudaEventDestroy(E->ev_stage[i]);
-    if (E->stage2[i]) cudaFree(E->stage2[i]);
-    if (E->ev_stage2[i]) cudaEventDestroy(E->ev_stage2[i]);
   }
-  if (E->sx2) cudaStreamDestroy(E->sx2);
-  if (E->sdec2) cudaStreamDestroy(E->sdec2);
   if (E->sc) cudaStreamDestroy(E->sc);
   if (E->sx) cudaStreamDestroy(E->sx);
   if (E->sdec) cudaStreamDestroy(E->sdec);
@@ -1879,33 +1859,10 @@ int mspq_engine_create(const mspq_model_desc* md, const mspq_engine_opts* op, ms
       E->n_tiles = (int)(E->S16 / 16384);
       E->Sreg = E->codec ? ((mspq_xc_max_blob_bytes(E->n_tiles) + 4095) / 4096) * 4096 : E->S16;
       if (E->codec) {
-        {
-          // MSPQ_DEC_PRIO=lo: decodes at the compute stream's priority (A/B switch)
-          const char* dp = getenv("MSPQ_DEC_PRIO");
-          const bool dlo = dp && dp[0] == 'l';
-          CUDA_OK(cudaStreamCreateWithPriority(&E->sdec, cudaStreamNonBlocking, dlo ? lo : hi));
-        }
+        CUDA_OK(cudaStreamCreateWithPriority(&E->sdec, cudaStreamNonBlocking, hi));
         for (int i = 0; i < 2; ++i) {
           CUDA_OK(cudaMalloc(&E->stage[i], (size_t)E->Sreg));
           CUDA_OK(cudaEventCreateWithFlags(&E->ev_stage[i], cudaEventDisableTiming));
-        }
-      }
-      {
-        const char* pf = getenv("MSPQ_PF_LANE");
-        E->pf_lane = pf && pf[0] == '1';
-      }
-      {
-        const char* dc = getenv("MSPQ_DEC_CTAS");
-        if (dc) E->dec_ctas = std::max(1, std::min(1024, atoi(dc)));
-      }
-      if (E->pf_lane) {
-        CUDA_OK(cudaStreamCreateWithPriority(&E->sx2, cudaStreamNonBlocking, lo));
-        if (E->codec) {
-          CUDA_OK(cudaStreamCreateWithPriority(&E->sdec2, cudaStreamNonBlocking, lo));
-          for (int i = 0; i < 2; ++i) {
-            CUDA_OK(cudaMalloc(&E->stage2[i], (size_t)E->Sreg));
-            CUDA_OK(cudaEventCreateWithFlags(&E->ev_stage2[i], cudaEventDisableTiming));
-          }
         }
       }
       E->S4 = mspq_int4_blob_bytes(m.d, m.f);

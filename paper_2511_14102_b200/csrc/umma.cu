@@ -1088,10 +1088,6 @@ __global__ void k_tile_int4(const uint32_t* __restrict__ q, const uint16_t* __re
 
 }  // namespace
 
-bool pdl_disabled() {
-  static const bool off = getenv("MSPQ_NO_PDL") && atoi(getenv("MSPQ_NO_PDL")) != 0;
-  return off;
-}
 
 template <int BN, int STAGES>
 static cudaError_t launch_grouped_v(const UmmaArgs& a, int units, cudaStream_t st) {
@@ -1103,13 +1099,11 @@ static cudaError_t launch_grouped_v(const UmmaArgs& a, int units, cudaStream_t s
 // 4 stages (75 KB smem) fit 3 CTAs per SM, so a verify layer's W13 (<= 4 experts x 100 row tiles
 // at k = 1) runs in one wave of 444 instead of spilling past 296; per-SM bytes in flight are the
 // same as 2 CTAs x 6 stages.  Per-layer verify FFN 118.3 -> 113.1 us at cap 4 (Phi).
-// MSPQ_K3_STAGES=6 restores the old ring (A/B).
 cudaError_t launch_umma_grouped(const UmmaArgs& a, int max_groups, int BN, cudaStream_t st) {
-  static const int stages = getenv("MSPQ_K3_STAGES") ? atoi(getenv("MSPQ_K3_STAGES")) : 4;
   const int units = max_groups * (a.rows / BM) * a.splits;
   if (units == 0) return cudaSuccess;
-  if (BN == 16) return stages == 6 ? launch_grouped_v<16, 6>(a, units, st) : launch_grouped_v<16, 4>(a, units, st);
-  return stages == 6 ? launch_grouped_v<32, 6>(a, units, st) : launch_grouped_v<32, 4>(a, units, st);
+  if (BN == 16) return launch_grouped_v<16, 4>(a, units, st);
+  return launch_grouped_v<32, 4>(a, units, st);
 }
 
 cudaError_t launch_umma_int4(const UmmaArgs& a, int max_groups, int BN, cudaStream_t st) {

@@ -237,19 +237,17 @@ def test_shared_host_store_attach_path(cuda, tmp_path):
                 os.unlink(p)
 
 
-@pytest.mark.parametrize("switch", ["MSPQ_PF_LANE", "MSPQ_PF_DEFER"])
 @pytest.mark.parametrize("codec", ["none", "xc"])
-def test_prefetch_issue_order_changes_nothing_but_timing(cuda, codec, switch, monkeypatch):
-    """MSPQ_PF_LANE=1 issues the planner's prefetches on a second copy (+ decode) stream with its
-    own staging pair; MSPQ_PF_DEFER=1 issues each layer's prefetches behind the previous layer's
-    demand copies. Tokens, routing, the hit/miss log and the bytes moved are unchanged."""
+def test_prefetch_issue_order_changes_nothing_but_timing(cuda, codec):
+    """"prefetch_defer" (default on) issues each layer's plan prefetches behind the previous
+    layer's demand copies instead of in plan order at draft time: tokens, routing, the hit/miss
+    log and the bytes moved are unchanged."""
     import paper_2511_14102_b200 as m
     cfg = m.ModelConfig.named("tiny")
     reps = []
-    for lane in ("0", "1"):
-        monkeypatch.setenv(switch, lane)
+    for defer in (False, True):
         eng = m.Engine(cfg, kmax=8, trace_level=2, expert_codec=codec)
-        eng.configure({"policy": "speculative", "cache_capacity": 3, "k": 4})
+        eng.configure({"policy": "speculative", "cache_capacity": 3, "k": 4, "prefetch_defer": defer})
         reps.append(eng.generate([5, 17, 101, 9], 32))
         eng.close()
     a, b = reps

@@ -9,7 +9,7 @@ cfg = dict(case["config"]); cfg["log"] = True
 ref = case["report"]
 for rep in range(3):
     got = m.run_simulation(case["trace"], cfg)
-    print("rep", rep, "total", got["total_time_s"], "ref", ref["total_time_s"], "staging", os.environ.get("MSPQ_CTL_NO_STAGING"))
+    print("rep", rep, "total", got["total_time_s"], "ref", ref["total_time_s"])
 log = []
 orc = cp.simulate(case["trace"], json.dumps(case["config"]), log=log)
 print("oracle total", orc["total_time_s"])
