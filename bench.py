@@ -290,6 +290,56 @@ def run_reference_arm(a):
     print(json.dumps(line))
 
 
+def numa_node_of(local):
+    """NUMA node and CPU list of GPU `local` (sysfs via its PCI bus id); (-1, None) if unknown."""
+    try:
+        import torch
+        pr = torch.cuda.get_device_properties(local)
+        bus = "%04x:%02x:%02x.0" % (getattr(pr, "pci_domain_id", 0), pr.pci_bus_id, pr.pci_device_id)
+        base = "/sys/bus/pci/devices/" + bus
+        node = int(open(base + "/numa_node").read().strip())
+        cpus = open(base + "/local_cpulist").read().strip()
+        return node, cpus
+    except Exception:  # noqa: BLE001
+        return -1, None
+
+
+def parse_cpulist(text):
+    out = set()
+    for part in text.split(","):
+        if "-" in part:
+            lo, hi = part.split("-")
+            out.update(range(int(lo), int(hi) + 1))
+        elif part:
+            out.add(int(part))
+    return out
+
+
+def xc_ratio_gaussian(d, f, seed=7):
+    """Lossless XC codec ratio of one expert with N(0, sigma^2) weights (SURVEY.md §8(d)'s
+    distribution; the bench model itself is uniform-init): bf16 tile images of a d x f expert
+    (W13 [2f][d] + W2 [d][f], sigma = 1/sqrt(d)) encoded with mspq_xc_encode."""
+    import ctypes
+    import torch
+    from paper_2511_14102_b200._lib import check, lib
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    w13 = (torch.randn(2 * f, d, device="cuda", generator=g) / d ** 0.5).to(torch.bfloat16)
+    w2 = (torch.randn(d, f, device="cuda", generator=g) / d ** 0.5).to(torch.bfloat16)
+    n = 3 * d * f
+    img = torch.empty(n, dtype=torch.int16, device="cuda")
+    P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    check(lib().mspq_tile_bf16(P(w13), 2 * f, d, P(img), None))
+    check(lib().mspq_tile_bf16(P(w2), d, f, ctypes.c_void_p(img.data_ptr() + 2 * f * d * 2), None))
+    n_tiles = n * 2 // 16384
+    scratch = torch.empty(lib().mspq_xc_scratch_bytes(n_tiles), dtype=torch.uint8, device="cuda")
+    cap = lib().mspq_xc_max_blob_bytes(n_tiles)
+    out = torch.empty(cap, dtype=torch.uint8, device="cuda")
+    nb = ctypes.c_longlong(0)
+    check(lib().mspq_xc_encode(P(img), n_tiles, P(scratch), P(out), cap, ctypes.byref(nb), None))
+    torch.cuda.synchronize()
+    return nb.value / (n * 2)
+
+
 def spawn_ranks(a):
     """--gpus N without torchrun: relaunch this script under torch.distributed.run, one rank per
     GPU on this node (127.0.0.1 rendezvous), and return its exit code."""
@@ -318,16 +368,29 @@ def main():
     cfgm = m.ModelConfig.named(a.model, unique_experts=a.unique)
     E, K, L = cfgm.E, cfgm.K, cfgm.L
     cap = a.cap or max(K, E // 4)
+    # NUMA placement: run this rank on its GPU's node and give every node one copy of the pinned
+    # store (a PCIe read then stays on the GPU's own socket); this box has one node
+    node, cpus = numa_node_of(local)
+    if cpus:
+        try:
+            os.sched_setaffinity(0, parse_cpulist(cpus))
+        except OSError:
+            pass
     store = ""
     if world > 1:
-        # one shared pinned store per run: rank 0 picks a fresh name (no stale file can be attached)
-        # and the others attach once its ready record is published (live.cpp alloc_host_store)
+        # one shared pinned store per NUMA node and run: rank 0 picks a fresh name (no stale file can be
+        # attached), the lowest rank of each node creates its node's copy, the others attach once its
+        # ready record is published (live.cpp alloc_host_store)
         name = ["/dev/shm/mspq_store_%s_%d_%d" % (a.model, os.getpid(), time.time_ns() % 10**9)]
         torch.distributed.broadcast_object_list(name, src=0)
-        store = name[0]
+        nodes = [None] * world
+        torch.distributed.all_gather_object(nodes, node)
+        store = "%s_n%d" % (name[0], max(node, 0))
+        store_owner = min(r for r in range(world) if nodes[r] == node)
     t_create = time.perf_counter()
     eng = m.Engine(cfgm, kmax=16, device=local, host_store_path=store or None,
-                   host_store_role=0 if rank == 0 else 1, trace_level=0, expert_codec=a.codec)
+                   host_store_role=0 if (not store or rank == store_owner) else 1, trace_level=0,
+                   expert_codec=a.codec)
     t_create = time.perf_counter() - t_create
     t_home = 0.0
     if a.peer_tier:
@@ -389,6 +452,12 @@ def main():
     dev_max, wall_max, tok_all = aggregate(dev_t, wall, tok, world)
     if rank != 0:
         eng.close()
+        if store and rank == store_owner:  # this rank created its node's store copy
+            for p in (store, store + ".ready"):
+                try:
+                    os.unlink(p)
+                except OSError:
+                    pass
         return
     hbm, tf, pk_kind = peaks()
     pcie_bw = info["pcie_bw_measured"]
@@ -444,7 +513,13 @@ def main():
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "engine_create_s": t_create,
+        "numa_node": node,
     }
+    try:
+        line["xc_ratio"] = {"bench_model_uniform_init": info["expert_wire_bytes_mean"] / info["expert_bytes_bf16"],
+                            "gaussian_weights": xc_ratio_gaussian(cfgm.d, cfgm.f)}
+    except Exception as e:  # noqa: BLE001
+        line["xc_ratio"] = {"error": str(e)}
     if pts:
         line["peer_tier"] = {
             "group": world, "home_bytes_per_gpu": info["home_bytes"], "home_fill_s": t_home,
@@ -468,7 +543,7 @@ def main():
         except Exception as e:  # noqa: BLE001
             line["cpu_reference_sim"] = {"value": None, "sample": f"unavailable: {e}"}
     eng.close()
-    if store:
+    if store and rank == store_owner:
         for p in (store, store + ".ready"):
             try:
                 os.unlink(p)

@@ -114,3 +114,55 @@ def test_peer_tier_two_processes_over_cuda_ipc(cuda):
         _same_decisions(out[r], want)
         pt = out[r]["peer_tier"]
         assert out[r]["h2d_bytes"] == 0 and pt["peer_fetches"] > 0 and pt["home_local_fetches"] > 0
+
+
+def _store_rank_main(rank, world, port, path, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2511_14102_b200 as m
+        cfg = m.ModelConfig.named("tiny")
+        eng = m.Engine(cfg, kmax=8, trace_level=2, host_store_path=path, host_store_role=0 if rank == 0 else 1)
+        eng.configure(CONF)
+        rep = eng.generate(PROMPT, 32)
+        dist.barrier()  # the owner keeps the store mapped until every rank is done
+        q.put((rank, {k: rep[k] for k in ("tokens", "total_new_experts", "cycles", "h2d_bytes")}))
+        eng.close()
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_shared_host_store_two_processes(cuda):
+    """bench.py's multi-rank layout on one box: rank 0 creates and fills the /dev/shm pinned store,
+    rank 1 attaches to it from another process (record + size check), and both decode the same
+    tokens with the same cache decisions and the same bytes on the link."""
+    import socket
+
+    import torch.multiprocessing as mp
+    base = _engine()
+    want = base.generate(PROMPT, 32)
+    base.close()
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    path = "/dev/shm/mspq_test_store2_%d" % os.getpid()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_store_rank_main, args=(r, 2, port, path, q)) for r in range(2)]
+    try:
+        for p in ps:
+            p.start()
+        out = dict(q.get(timeout=600) for _ in ps)
+        for p in ps:
+            p.join(timeout=120)
+    finally:
+        for f in (path, path + ".ready"):
+            if os.path.exists(f):
+                os.unlink(f)
+    for r in range(2):
+        assert isinstance(out[r], dict), out[r]
+        _same_decisions(out[r], want)
+        assert out[r]["h2d_bytes"] == want["h2d_bytes"] > 0
