@@ -69,6 +69,8 @@ def parse():
     ap.add_argument("--streams", type=int, default=0,
                     help="independent request streams over all ranks (BASELINE config 5: 8); stream s is served "
                          "by rank s %% N, a rank's streams one after another on its engine; 0 = one per rank")
+    ap.add_argument("--same-device", action="store_true",
+                    help="test mode: every rank uses cuda:0 (exercises the multi-rank path on a one-GPU box)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="time box of the CPU oracle decode")
     ap.add_argument("--out", default="")
@@ -359,6 +361,8 @@ def main():
     if a.impl == "reference":
         return run_reference_arm(a)
     rank, world, local = dist_env()
+    if a.same_device:
+        local = 0
     import torch
     torch.cuda.set_device(local)
     if world > 1:
