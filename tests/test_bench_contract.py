@@ -26,3 +26,12 @@ def test_reference_arm_prints_contract_line(ref):
     assert "workload" in d["config"]
     # same workload as the GPU arm: the routing trace this engine produced for the bench config
     assert d["same_config"] is True and d["reference_modeled_b200_tokens_per_s"] > 0
+
+
+def test_numa_cpulist_parsing():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    bm = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bm)
+    assert bm.parse_cpulist("0-3,8,10-11") == {0, 1, 2, 3, 8, 10, 11}
+    assert bm.parse_cpulist("5") == {5}
