@@ -1849,9 +1849,11 @@ int mspq_engine_create(const mspq_model_desc* md, const mspq_engine_opts* op, ms
       E->store_path = op->host_store_path ? op->host_store_path : "";
       E->o.host_store_path = nullptr;
       CUDA_OK(cudaSetDevice(op->device));
-      CUDA_OK(cudaStreamCreateWithFlags(&E->sc, cudaStreamNonBlocking));
       int lo, hi;
       cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      // compute at the highest priority: the verify GEMMs' CTAs go ahead of the XC decodes of
+      // prefetched experts that run beside them (the decodes have slack: the link is slower)
+      CUDA_OK(cudaStreamCreateWithPriority(&E->sc, cudaStreamNonBlocking, hi));
       CUDA_OK(cudaStreamCreateWithPriority(&E->sx, cudaStreamNonBlocking, hi));
       E->S16 = mspq_bf16_blob_bytes(m.d, m.f);
       E->codec = op->expert_codec;
@@ -1859,7 +1861,7 @@ int mspq_engine_create(const mspq_model_desc* md, const mspq_engine_opts* op, ms
       E->n_tiles = (int)(E->S16 / 16384);
       E->Sreg = E->codec ? ((mspq_xc_max_blob_bytes(E->n_tiles) + 4095) / 4096) * 4096 : E->S16;
       if (E->codec) {
-        CUDA_OK(cudaStreamCreateWithPriority(&E->sdec, cudaStreamNonBlocking, hi));
+        CUDA_OK(cudaStreamCreateWithPriority(&E->sdec, cudaStreamNonBlocking, lo));
         for (int i = 0; i < 2; ++i) {
           CUDA_OK(cudaMalloc(&E->stage[i], (size_t)E->Sreg));
           CUDA_OK(cudaEventCreateWithFlags(&E->ev_stage[i], cudaEventDisableTiming));
