@@ -176,150 +176,6 @@ __global__ void __launch_bounds__(GV_THREADS) k_int4_gemv(GemvArgs a) {
   }
 }
 
-// Persistent variant: grid = SMs x resident CTAs; CTA c takes units c, c + grid, ... where a unit is
-// (group, row block of ROWS rows, K split).  Fine units (32 rows) keep the last wave short (Phi W13:
-// 800 units on 296 CTAs instead of 1.35 waves of whole CTAs), the staged x is reused across units
-// of the same group, and the next unit's first weight batch is issued before this unit's epilogue.
-template <int GV_TILES, int NB>
-__global__ void __launch_bounds__(GV_THREADS) k_int4_gemv_p(GemvArgs a, int ksplit) {
-  constexpr int ROWS = 16 * GV_TILES;
-  pdl_enter();  // launched with launch_pdl (kernels.h)
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int kdim = a.kdim, ngr = kdim / 128, nchunk = kdim / 64;
-  const int rb_per = a.rows / ROWS, units_per_g = rb_per * ksplit, total = *a.n_groups * units_per_g;
-  uint16_t* xh = reinterpret_cast<uint16_t*>(smem_raw);            // [kdim] class-scaled fp16
-  float* red = reinterpret_cast<float*>(smem_raw + kdim * 2);       // [GV_WARPS][ROWS] row partials
-  const int gi = lane >> 2, ti = lane & 3;
-  uint4 buf[NB][GV_TILES][2];
-  int staged = -1;  // group whose x sits in xh (W13: every group shares x)
-  auto unit_geom = [&](int u, int& g, int& rb, int& gq0, int& gq1, const uint4*& q, const uint16_t*& sc) {
-    g = u / units_per_g;
-    const int r = u - g * units_per_g, sp = r / rb_per;
-    rb = r - sp * rb_per;
-    gq0 = sp * ngr / ksplit;
-    gq1 = (sp + 1) * ngr / ksplit;
-    const unsigned char* blob = a.blobs + ((int64_t)a.layer * a.E + a.group_expert[g]) * a.blob_bytes;
-    q = reinterpret_cast<const uint4*>(blob + a.q_off);
-    sc = reinterpret_cast<const uint16_t*>(blob + a.s_off);
-  };
-  auto load_batch = [&](const uint4* q, int rt0, int gfirst, int gq1) {
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      const int gb = gfirst + b * GV_WARPS;
-      if (gb < gq1)
-#pragma unroll
-        for (int i = 0; i < GV_TILES; ++i)
-#pragma unroll
-          for (int c = 0; c < 2; ++c)
-            buf[b][i][c] = ldg_stream<false>(q + (((int64_t)(rt0 + i) * nchunk + 2 * gb + c) * 32 + lane));
-    }
-  };
-  int unit = blockIdx.x;
-  if (unit >= total) return;
-  int g, rb, gq0, gq1;
-  const uint4* q;
-  const uint16_t* sc;
-  unit_geom(unit, g, rb, gq0, gq1, q, sc);
-  load_batch(q, rb * GV_TILES, gq0 + warp, gq1);
-  while (true) {
-    const int want_x = a.x_per_group ? g : 0;
-    if (staged != want_x) {
-      __syncthreads();  // every warp is done with the previous x
-      const uint16_t* x = a.x + (int64_t)want_x * kdim;
-      for (int k = 2 * tid; k < kdim; k += 2 * GV_THREADS) {
-        const uint32_t u = *reinterpret_cast<const uint32_t*>(x + k);
-        const float m = (k & 15) >= 8 ? 0.0625f : 1.0f;
-        const __half2 h2 = __floats2half2_rn(__uint_as_float(u << 16) * m, __uint_as_float(u & 0xffff0000u) * m);
-        *reinterpret_cast<__half2*>(&xh[k]) = h2;
-      }
-      __syncthreads();
-      staged = want_x;
-    }
-    const int rt0 = rb * GV_TILES;
-    float acc[GV_TILES][2];
-#pragma unroll
-    for (int i = 0; i < GV_TILES; ++i) acc[i][0] = acc[i][1] = 0.0f;
-    for (int gq = gq0 + warp; gq < gq1; gq += NB * GV_WARPS) {
-#pragma unroll
-      for (int b = 0; b < NB; ++b) {
-        const int gb = gq + b * GV_WARPS;
-        if (gb >= gq1) break;
-        float d[GV_TILES][4];
-#pragma unroll
-        for (int i = 0; i < GV_TILES; ++i) d[i][0] = d[i][1] = d[i][2] = d[i][3] = 0.0f;
-        float c1 = 0.0f, c16 = 0.0f;
-#pragma unroll
-        for (int c = 0; c < 2; ++c)
-#pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            const int kb = 8 * gb + 4 * c + v;
-            const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&xh[16 * kb + 2 * ti]);
-            const uint32_t b1 = *reinterpret_cast<const uint32_t*>(&xh[16 * kb + 8 + 2 * ti]);
-            const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&b0));
-            const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&b1));
-            c1 = __fadd_rn(__fadd_rn(c1, f0.x), f0.y);
-            c16 = __fadd_rn(__fadd_rn(c16, f1.x), f1.y);
-#pragma unroll
-            for (int i = 0; i < GV_TILES; ++i) {
-              const uint4 wv = buf[b][i][c];
-              const uint32_t w = v == 0 ? wv.x : v == 1 ? wv.y : v == 2 ? wv.z : wv.w;
-              const uint32_t w8 = w >> 8;
-              uint32_t af[4];
-              af[0] = lop_magic(w, 0x000F000Fu);
-              af[1] = lop_magic(w8, 0x000F000Fu);
-              af[2] = lop_magic(w, 0x00F000F0u);
-              af[3] = lop_magic(w8, 0x00F000F0u);
-              mma16816(d[i], af, b0, b1);
-            }
-          }
-        float cl = fmaf(1152.0f, c16, __fmul_rn(1032.0f, c1));
-        cl = __fadd_rn(cl, __shfl_xor_sync(0xffffffffu, cl, 1));
-        cl = __fadd_rn(cl, __shfl_xor_sync(0xffffffffu, cl, 2));
-#pragma unroll
-        for (int i = 0; i < GV_TILES; ++i) {
-          const int r0 = 16 * (rt0 + i) + gi;
-          const float s0 = bf2f(sc[(int64_t)r0 * ngr + gb]), s1 = bf2f(sc[(int64_t)(r0 + 8) * ngr + gb]);
-          acc[i][0] = fmaf(s0, __fsub_rn(d[i][0], cl), acc[i][0]);
-          acc[i][1] = fmaf(s1, __fsub_rn(d[i][2], cl), acc[i][1]);
-        }
-      }
-      if (gq + NB * GV_WARPS < gq1) load_batch(q, rt0, gq + NB * GV_WARPS, gq1);
-    }
-    // the next unit's first batch goes out before this unit's epilogue
-    const int cur_g = g, cur_rb = rb, cur_sp_plane = (unit % units_per_g) / rb_per;
-    const int next = unit + gridDim.x;
-    if (next < total) {
-      unit_geom(next, g, rb, gq0, gq1, q, sc);
-      load_batch(q, rb * GV_TILES, gq0 + warp, gq1);
-    }
-    if (ti == 0) {
-#pragma unroll
-      for (int i = 0; i < GV_TILES; ++i) {
-        red[warp * ROWS + 16 * i + gi] = acc[i][0];
-        red[warp * ROWS + 16 * i + gi + 8] = acc[i][1];
-      }
-    }
-    __syncthreads();
-    if (tid < ((ROWS + 31) & ~31)) {
-      float v = 0.0f;
-      if (tid < ROWS)
-#pragma unroll
-        for (int w = 0; w < GV_WARPS; ++w) v = __fadd_rn(v, red[w * ROWS + tid]);
-      const int row = ROWS * cur_rb + tid;
-      if (a.act) {
-        const float up = __shfl_down_sync(0xffffffffu, v, 1);
-        if ((tid & 1) == 0 && tid < ROWS) a.act[(int64_t)cur_g * (a.rows / 2) + row / 2] = f2bf(__fmul_rn(silu_det(v), up));
-      } else if (tid < ROWS) {
-        a.y[((int64_t)cur_sp_plane * *a.n_groups + cur_g) * a.rows + row] = v;
-      }
-    }
-    __syncthreads();  // red is reused by the next unit
-    if (next >= total) break;
-    unit = next;
-  }
-}
-
 // row-major quantised INT4 (standard nibble order) -> fragment-major words (header comment)
 __global__ void k_fragtile_int4(const uint32_t* __restrict__ q, int rows, int cols, uint32_t* __restrict__ fq) {
   const int wpr = cols / 8, nchunk = cols / 64;
@@ -359,33 +215,12 @@ cudaError_t launch_int4_gemv(const GemvArgs& a, int max_groups, int ksplit, cuda
   // default: 64 rows per CTA, 2 scale groups (8 KB per warp) per load batch -- best of the A/B at
   // the three BASELINE shapes (profiles/r02/gemv_variants.txt: Phi 2.81, Qwen3 1.67, Mixtral 3.81
   // TB/s in-stream; 32 rows x 4 groups: 2.74 / 1.30 / 3.50; tcgen05 K2: 1.49 / 0.86 / 1.88)
-  if (g_gemv_variant == 0 || g_gemv_variant == 7) {  // persistent (default): 32-row / 16-row units
-    static int grid_cache[2] = {0, 0};
-    const int vi = g_gemv_variant == 0 ? 0 : 1;
-    const size_t smem = (size_t)a.kdim * 2 + GV_WARPS * 64 * 4 + 16;
-    auto kern = vi == 0 ? k_int4_gemv_p<2, 4> : k_int4_gemv_p<1, 4>;
-    if (smem > 48 * 1024) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-    }
-    if (!grid_cache[vi]) {
-      int dev = 0, sms = 148, per = 1;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, GV_THREADS, smem);
-      grid_cache[vi] = sms * std::max(1, per);
-    }
-    const int rows_per = vi == 0 ? 32 : 16;
-    if (a.rows % rows_per) return cudaErrorInvalidValue;
-    const int units = max_groups * (a.rows / rows_per) * ksplit;
-    return launch_pdl(kern, dim3(std::min(grid_cache[vi], units)), dim3(GV_THREADS), smem, st, a, ksplit);
-  }
   switch (g_gemv_variant) {
     case 1: return launch_gemv_v<2, 4, true>(a, max_groups, ksplit, st);
     case 3: return launch_gemv_v<1, 4, false>(a, max_groups, ksplit, st);
     case 4: return launch_gemv_v<2, 2, false>(a, max_groups, ksplit, st);
     case 5: return launch_gemv_v<2, 4, false>(a, max_groups, ksplit, st);
-    default: return launch_gemv_v<4, 2, false>(a, max_groups, ksplit, st);  // 6: the non-persistent default
+    default: return launch_gemv_v<4, 2, false>(a, max_groups, ksplit, st);
   }
 }
 
