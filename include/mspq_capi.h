@@ -87,6 +87,7 @@ typedef struct mspq_engine_opts {
   int trace_level;              /* 0 = counts only, 1 = per-cycle tokens/routing, 2 = + event log */
   int expert_codec;             /* host-store format of the bf16 experts: 0 = raw tile images,
                                    1 = XC lossless blobs (mspq_xc_encode), decoded on the GPU */
+  int max_streams;              /* request streams mspq_generate_batch can run together (<= 1 = one) */
 } mspq_engine_opts;
 
 typedef struct mspq_engine mspq_engine;
@@ -189,6 +190,11 @@ int mspq_moe_int4_gemv(const int32_t* n_groups, const int32_t* group_expert, con
 int mspq_fragtile_int4(const void* q, int rows, int cols, void* fq, void* stream);
 /* diagnostics: tile/batch variant of the draft GEMV (tools/gemv_bench.py A/B; 0 = the default) */
 int mspq_debug_gemv_variant(int v);
+/* the same over a batch of several request streams' windows: meta[T][3] = per token (batch row of
+ * its window's first token, stream index, position); stream s's cache = kc + s * kv_stream_stride */
+int mspq_attention_batched(const float* qkv, int splits, long long split_stride, int T, int H, int Hkv, int Dh, int P,
+                           const int32_t* meta, long long kv_stream_stride, void* kc, void* vc, void* out, void* oimg,
+                           void* ws, void* stream);
 /* row-major quantised INT4 (q[rows][cols/8] u32, standard nibble order; s[rows][cols/128] bf16)
  * -> tile-major [rows/128][cols/64][128][8] u32 + [rows/128][cols/128][128] bf16 */
 int mspq_tile_int4(const void* q, const void* s, int rows, int cols, void* tq, void* ts, void* stream);
@@ -308,6 +314,14 @@ int mspq_engine_configure(mspq_engine* eng, const char* config_json);
  * first window head).  *report_json: SimReport JSON + measured fields + per-cycle traces. */
 int mspq_generate(mspq_engine* eng, const int32_t* prompt, int n_prompt, int max_new,
                   char** report_json);
+/* several independent request streams decoded together: each stream has its own prompt, KV cache
+ * and draft; every cycle the streams' verify windows go through ONE layer-major verify pass (one
+ * grouped GEMM per layer over all streams' tokens, so they share the expert weight reads) over one
+ * shared expert cache.  prompts: n_streams prompts back to back, lens[n_streams]; all streams share
+ * k (k+1 slots each, n_streams (k+1) <= 32).  Cache policy must be "lru" (the ELB-driven policies
+ * are defined for one stream's lookahead).  *report_json: per-stream tokens + per-cycle records. */
+int mspq_generate_batch(mspq_engine* eng, const int32_t* prompts, const int32_t* lens, int n_streams,
+                        int max_new, char** report_json);
 int mspq_engine_info(mspq_engine* eng, char** json);
 /* copy a device tensor of the engine out (tests): name in {"embed","pos","lm","router:<l>",
  * "gamma:<l>","gamma:final","draft:<l>:<e>","expert:<l>:<e>" (bf16 tile images, decoded if the

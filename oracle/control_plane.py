@@ -774,7 +774,11 @@ def live_cycle(cache, elb, targets, cfg, log=None, ids_visible_causal=True):
     k = elb.filled
     policy = cfg["policy"]
     out = dict(fetched=0, demand=0, plan_items=[], coverage_hits=[], coverage_size=[],
-               step_hits=[], step_size=[], jit=0)
+               step_hits=[], step_size=[], jit=0, refetch=0)
+    # refetch: an insertion in verify layer l of a key the layer already requested (evicted after
+    # its first request): the engine serves it from the first-request buffer, still parked
+    # (live.cpp issue_copies, refetch_from_hbm; ctl.cu erase)
+    demanded = [None]
 
     def victim_layer(key):
         return key[0] if cache.mode == "per_layer" else -1
@@ -793,6 +797,8 @@ def live_cycle(cache, elb, targets, cfg, log=None, ids_visible_causal=True):
             cache.erase(ev)
         cache.insert(key)
         out["fetched"] += 1
+        if demanded[0] is not None and key in demanded[0]:
+            out["refetch"] += 1
         if log is not None:
             log.append((kind, tag, key[0], key[1], False, ev))
         return True
@@ -806,6 +812,7 @@ def live_cycle(cache, elb, targets, cfg, log=None, ids_visible_causal=True):
                 ins(key, True, 0, i + 1 if ids_visible_causal else None, "plan%d" % phase, row)
     nslots = len(targets)
     for l in range(L):
+        demanded[0] = set()
         req_l = sorted({(l, e) for s in range(nslots) for e in targets[s][l]})
         out["coverage_hits"].append(sum(1 for key in req_l if cache.contains(key)))
         out["coverage_size"].append(len(req_l))
@@ -842,6 +849,9 @@ def live_cycle(cache, elb, targets, cfg, log=None, ids_visible_causal=True):
                 if not was:
                     out["fetched"] += 1
                     out["demand"] += 1
+                    if key in demanded[0]:
+                        out["refetch"] += 1
+                demanded[0].add(key)
     return out
 
 
@@ -904,6 +914,7 @@ def live_governor_ks(report, cfg_json, L, E, K, estimator="linear", kmax=16):
         out.append(dict(k=k, est=est(k), select_k=kk, p=list(accept), g=g,
                         table=[est(j) for j in range(c["k_max"] + 1)]))
         raw = elb_raw(freq, resident, L, E, k) if estimator == "elb" else 0.0
+        refetch_on = cfg_json.get("refetch_from_hbm", True)
         kc = cyc["k"]
         acc = cyc["accepted"]
         outcomes = []
@@ -914,9 +925,11 @@ def live_governor_ks(report, cfg_json, L, E, K, estimator="linear", kmax=16):
         accept = update_acceptance(accept, c["ema_alpha"], outcomes[:len(accept)])
         g = float(cyc["new_experts"]) / float(kc)
         if estimator == "elb":
+            lc = live_cycle(cache, ELB.build(cyc["elb"], cyc["elb_gates"]), cyc["target"], c)
+            # calibrated on the fetches that crossed the link (in-layer refetches come from HBM)
+            moved = float(cyc["new_experts"]) - (float(lc["refetch"]) if refetch_on else 0.0)
             if raw > 0.0:
-                calib[k] = (1.0 - 0.25) * calib[k] + 0.25 * (float(cyc["new_experts"]) / raw)
-            live_cycle(cache, ELB.build(cyc["elb"], cyc["elb_gates"]), cyc["target"], c)
+                calib[k] = (1.0 - 0.25) * calib[k] + 0.25 * (moved / raw)
             elb_update(freq, cyc["elb"], L, E)
             resident = set(cache.recency)
         rem -= acc + cyc["bonus"]

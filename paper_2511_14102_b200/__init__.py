@@ -139,14 +139,14 @@ class Engine:
     def __init__(self, model: ModelConfig, kmax: int = 16, device: int = 0,
                  host_store_path: str | None = None, host_store_role: int = 0,
                  slot_extra: int = 0, trace_level: int = 1, log_cap: int = 0,
-                 expert_codec: str = "xc"):
+                 expert_codec: str = "xc", max_streams: int = 1):
         self.model = model
         self._desc = model.desc()
         self._path = (host_store_path or "").encode()
         if expert_codec not in ("none", "xc"):
             raise ValueError("expert_codec must be 'none' or 'xc'")
         self._opts = _lib.EngineOpts(device, kmax, self._path, host_store_role, slot_extra,
-                                     log_cap, trace_level, 1 if expert_codec == "xc" else 0)
+                                     log_cap, trace_level, 1 if expert_codec == "xc" else 0, max_streams)
         self._h = ctypes.c_void_p()
         check(lib().mspq_engine_create(ctypes.byref(self._desc), ctypes.byref(self._opts),
                                        ctypes.byref(self._h)))
@@ -159,6 +159,17 @@ class Engine:
         arr = (ctypes.c_int32 * len(prompt))(*prompt)
         out = ctypes.c_void_p()
         check(lib().mspq_generate(self._h, arr, len(prompt), max_new_tokens, ctypes.byref(out)))
+        return json.loads(take_string(out))
+
+    def generate_batch(self, prompts, max_new_tokens: int) -> dict:
+        """Several independent request streams decoded together (mspq_generate_batch): one
+        layer-major verify pass per cycle over every stream's window, sharing the expert weight
+        reads; each stream's tokens equal its own greedy decode."""
+        flat = [t for p in prompts for t in p]
+        arr = (ctypes.c_int32 * len(flat))(*flat)
+        lens = (ctypes.c_int32 * len(prompts))(*[len(p) for p in prompts])
+        out = ctypes.c_void_p()
+        check(lib().mspq_generate_batch(self._h, arr, lens, len(prompts), max_new_tokens, ctypes.byref(out)))
         return json.loads(take_string(out))
 
     def info(self) -> dict:

@@ -25,7 +25,7 @@ class ModelDesc(ctypes.Structure):
 class EngineOpts(ctypes.Structure):
     _fields_ = [("device", c_int), ("kmax", c_int), ("host_store_path", c_char_p),
                 ("host_store_role", c_int), ("slot_extra", c_int), ("log_cap", c_int),
-                ("trace_level", c_int), ("expert_codec", c_int)]
+                ("trace_level", c_int), ("expert_codec", c_int), ("max_streams", c_int)]
 
 
 # (name, restype, argtypes)
@@ -48,6 +48,7 @@ _SIGS = [
     ("mspq_dense_sched_fill", c_int, [c_void_p, c_int]),
     ("mspq_dense_bf16_tc", c_int, [c_void_p] * 3 + [c_int] * 4 + [c_void_p, c_void_p, c_ll, c_void_p]),
     ("mspq_attention_ws_bytes", c_ll, [c_int] * 4),
+    ("mspq_attention_batched", c_int, [c_void_p, c_int, c_ll] + [c_int] * 5 + [c_void_p, c_ll] + [c_void_p] * 5),
     ("mspq_attention", c_int, [c_void_p, c_int, c_ll] + [c_int] * 5 + [c_void_p] * 7),
     ("mspq_gate_topk_img", c_int, [c_void_p] * 4 + [c_int, c_ll] + [c_void_p] * 10 + [c_int] * 6 + [c_float, c_void_p, c_void_p]),
     ("mspq_debug_gemv_variant", c_int, [c_int]),
@@ -86,6 +87,7 @@ _SIGS = [
     ("mspq_engine_destroy", c_int, [c_void_p]),
     ("mspq_engine_configure", c_int, [c_void_p, c_char_p]),
     ("mspq_generate", c_int, [c_void_p, c_void_p, c_int, c_int, ctypes.POINTER(c_void_p)]),
+    ("mspq_generate_batch", c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, ctypes.POINTER(c_void_p)]),
     ("mspq_engine_info", c_int, [c_void_p, ctypes.POINTER(c_void_p)]),
     ("mspq_engine_read", c_int, [c_void_p, c_char_p, c_void_p, c_ll]),
     ("mspq_engine_home_create", c_int, [c_void_p, c_int, c_int, c_void_p]),

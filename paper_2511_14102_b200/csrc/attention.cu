@@ -44,7 +44,19 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_partial(AttnArgs a) {
   const int t = blockIdx.x, g = blockIdx.y, sp = blockIdx.z;
   const int G = a.H / a.Hkv, Dh = a.Dh;
   const int Nq = a.H * Dh, Nkv = a.Hkv * Dh, Nqkv = Nq + 2 * Nkv;
-  const int p0 = *a.pos0, pt = p0 + t, n = pt + 1;
+  // token t of the batch: its window starts at batch row wb, it belongs to request stream s_id
+  // (own KV cache) and sits at position pt; one stream: wb = 0, s_id = 0, pt = *pos0 + t
+  int wb = 0, s_id = 0, pt;
+  if (a.meta) {
+    wb = a.meta[3 * t];
+    s_id = a.meta[3 * t + 1];
+    pt = a.meta[3 * t + 2];
+  } else {
+    pt = *a.pos0 + t;
+  }
+  const int tl = t - wb, p0 = pt - tl, n = pt + 1;
+  uint16_t* const kc = a.kc + (int64_t)s_id * a.kv_stream_stride;
+  uint16_t* const vc = a.vc + (int64_t)s_id * a.kv_stream_stride;
   const int chunk = attn_chunk(n), j0 = sp * chunk, j1 = min(n, j0 + chunk);
   uint16_t* wk = reinterpret_cast<uint16_t*>(smem_raw);     // [T][Dh] in-window keys, bf16
   uint16_t* wv = wk + a.T * Dh;                             // [T][Dh] in-window values
@@ -58,7 +70,7 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_partial(AttnArgs a) {
   const int w0 = max(j0, p0) - p0, w1 = j1 - p0;
   for (int i = tid; i < (w1 - w0) * Dh; i += AT_THREADS) {
     const int tt = w0 + i / Dh, dd = i % Dh;
-    const float* src = a.qkv + (int64_t)tt * Nqkv + Nq + g * Dh + dd;
+    const float* src = a.qkv + (int64_t)(wb + tt) * Nqkv + Nq + g * Dh + dd;
     float kv = 0.0f, vv = 0.0f;
     for (int s = 0; s < a.splits; ++s) {
       kv = __fadd_rn(kv, src[s * a.split_stride]);
@@ -82,8 +94,8 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_partial(AttnArgs a) {
   __syncthreads();
   if (j0 <= pt && pt < j1)  // the chunk holding the token's own position writes its cache row
     for (int dd = tid; dd < Dh; dd += AT_THREADS) {
-      a.kc[((int64_t)pt * a.Hkv + g) * Dh + dd] = wk[t * Dh + dd];
-      a.vc[((int64_t)pt * a.Hkv + g) * Dh + dd] = wv[t * Dh + dd];
+      kc[((int64_t)pt * a.Hkv + g) * Dh + dd] = wk[tl * Dh + dd];
+      vc[((int64_t)pt * a.Hkv + g) * Dh + dd] = wv[tl * Dh + dd];
     }
   auto row_vec = [&](const uint16_t* cache, const uint16_t* win, int j, float* o) {
     const uint16_t* r = (j < p0 ? cache + ((int64_t)j * a.Hkv + g) * Dh : win + (j - p0) * Dh) + lane * VEC;
@@ -102,7 +114,7 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_partial(AttnArgs a) {
   // (2) scores of this chunk
   for (int j = j0 + warp; j < j1; j += AT_WARPS) {
     float kk[VEC];
-    row_vec(a.kc, wk, j, kk);
+    row_vec(kc, wk, j, kk);
 #pragma unroll
     for (int i = 0; i < AT_MAXG; ++i)
       if (i < G) {
@@ -141,7 +153,7 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_partial(AttnArgs a) {
     for (int v = 0; v < VEC; ++v) acc[i][v] = 0.0f;
   for (int j = j0 + warp; j < j1; j += AT_WARPS) {
     float vv[VEC];
-    row_vec(a.vc, wv, j, vv);
+    row_vec(vc, wv, j, vv);
 #pragma unroll
     for (int i = 0; i < AT_MAXG; ++i)
       if (i < G) {

@@ -191,7 +191,8 @@ HostCfg parse_host_cfg(const std::string& text) {
   static const std::set<std::string> known = {"policy", "capacity_mode", "cache_capacity", "entropy_weighted_capacity",
                                               "k", "governor", "phases", "prefetch_budget", "rollback_s", "ema_alpha",
                                               "initial_accept", "seed", "collect_plans", "profile", "profile_path", "log",
-                                              "generator", "verify_overlap", "estimator", "prefetch_defer"};
+                                              "generator", "verify_overlap", "estimator", "prefetch_defer",
+                                              "refetch_from_hbm"};
   for (auto it = j.begin(); it != j.end(); ++it)
     if (!known.count(it.key())) fail(MSPQ_ERR_INVALID_CONFIG, "unknown key in run config: " + it.key());
   auto num = [&](const json& o, const char* k, double d) {
@@ -246,6 +247,7 @@ HostCfg parse_host_cfg(const std::string& text) {
   if (j.contains("log")) c.log = j["log"].get<bool>();
   if (j.contains("verify_overlap")) c.verify_overlap = j["verify_overlap"].get<bool>();
   if (j.contains("prefetch_defer")) c.prefetch_defer = j["prefetch_defer"].get<bool>();
+  if (j.contains("refetch_from_hbm")) c.refetch_from_hbm = j["refetch_from_hbm"].get<bool>();
   // profile / profile_path (run_config.cpp:155-170): exclusive; a relative path resolves against
   // the caller's working directory (the reference's base_dir for an inline config)
   if (j.contains("profile") && j.contains("profile_path"))

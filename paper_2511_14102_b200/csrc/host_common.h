@@ -65,6 +65,9 @@ struct HostCfg {  // SimConfig (sim.hpp:15-34) from the run-config schema (run_c
   // extension (live engine): issue a layer's plan prefetches behind the previous layer's demand
   // copies (per-layer capacity mode) instead of in plan order at draft time
   bool prefetch_defer = true;
+  // a fetch of an expert whose first-request buffer of the same verify layer still holds it (evicted
+  // and requested again inside one layer) is served HBM -> HBM from that buffer instead of the link
+  bool refetch_from_hbm = true;
 };
 int parse_policy(const std::string& s);
 const char* policy_name(int p);

@@ -126,6 +126,8 @@ struct AttnArgs {
   unsigned char* oimg = nullptr;  // the output as the O projection's SW128 B image (nullable)
   int o_bn = 16;
   float* part = nullptr;          // split-K partials, attn_part_floats(T, H, Hkv, Dh) floats
+  const int32_t* meta = nullptr;  // batched streams: per token (window base row, stream, position)
+  int64_t kv_stream_stride = 0;   // elements between two streams' caches (same layer)
 };
 size_t attn_smem_bytes(int T, int H, int Hkv, int Dh, int P);
 size_t attn_part_floats(int T, int H, int Hkv, int Dh);

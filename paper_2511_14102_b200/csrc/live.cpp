@@ -189,6 +189,25 @@ struct mspq_engine {
   int32_t* dsched = nullptr;               // [Tmax + 1][4 + Tmax] packed dense schedules per T
   void* dws = nullptr;
   float* attn_part = nullptr;  // split-K attention partials
+  // several request streams (mspq_generate_batch): stream s has its own device decode state, KV
+  // cache (kv_base + s * L * kv_layer) and captured draft graph; E->dst / E->kcache / E->vcache /
+  // E->gexec point at the current one (stream 0 outside a batch)
+  int S = 1;
+  std::vector<int32_t*> dst_s;
+  uint16_t *kv_base_k = nullptr, *kv_base_v = nullptr;
+  std::vector<cudaGraph_t> graph_s;
+  std::vector<cudaGraphExec_t> gexec_s;
+  int32_t* bmeta = nullptr;  // [Tmax][3] batch window metadata (window base row, stream, position)
+  int32_t* btok = nullptr;   // [Tmax] batch tokens
+  int32_t* bpos = nullptr;   // [Tmax] batch positions
+  void use_stream(int st) {
+    dst = dst_s[st];
+    if (kv_base_k) {
+      kcache = kv_base_k + (size_t)st * m.L * kv_layer();
+      vcache = kv_base_v + (size_t)st * m.L * kv_layer();
+    }
+    gexec = gexec_s.empty() ? gexec : gexec_s[st];
+  }
   // prefill (§2.2 of DESIGN.md): every expert of a layer streamed into one of two layer buffers
   unsigned char* pf_buf[2] = {nullptr, nullptr};
   cudaEvent_t pf_ready[2] = {nullptr, nullptr}, pf_done[2] = {nullptr, nullptr};
@@ -209,6 +228,8 @@ struct mspq_engine {
   std::vector<char> peer_ipc;             // [G] mapped with cudaIpcOpenMemHandle (closed on destroy)
   uint64_t gen_peer_bytes = 0, gen_home_local_bytes = 0;
   uint64_t n_peer = 0, n_home_local = 0;
+  uint64_t n_refetch = 0;  // fetches served from the key's first-request buffer of the layer
+  std::vector<int> fill_at;
   const unsigned char* home_src(int key) const {
     if (peer_G <= 0) return nullptr;
     const int l = key / m.E, e = key % m.E, owner = e % peer_G;
@@ -280,10 +301,13 @@ void make_weights(mspq_engine* E) {
     }
     CUDA_OK(cudaStreamSynchronize((cudaStream_t)s));
     cudaFree(stg);
-    CUDA_OK(cudaMalloc(&E->kcache, (size_t)m.L * E->kv_layer() * 2));
-    CUDA_OK(cudaMalloc(&E->vcache, (size_t)m.L * E->kv_layer() * 2));
-    CUDA_OK(cudaMemset(E->kcache, 0, (size_t)m.L * E->kv_layer() * 2));
-    CUDA_OK(cudaMemset(E->vcache, 0, (size_t)m.L * E->kv_layer() * 2));
+    const size_t kvb = (size_t)E->S * m.L * E->kv_layer() * 2;  // one cache per request stream
+    CUDA_OK(cudaMalloc(&E->kcache, kvb));
+    CUDA_OK(cudaMalloc(&E->vcache, kvb));
+    CUDA_OK(cudaMemset(E->kcache, 0, kvb));
+    CUDA_OK(cudaMemset(E->vcache, 0, kvb));
+    E->kv_base_k = E->kcache;
+    E->kv_base_v = E->vcache;
   }
   for (int l = 0; l < m.L; ++l) {
     CAPI_OK(mspq_fill_bf16(m.seed, 0x100ull + (uint64_t)l * 16, 0.f, 1, E->gamma + (size_t)l * d, d, 0, s));
@@ -462,6 +486,15 @@ void make_workspaces(mspq_engine* E) {
   E->logits = (float*)(b + o_lg);
   E->amax = (int32_t*)(b + o_am);
   E->dst = (int32_t*)(b + o_dst);
+  E->dst_s.assign(E->S, nullptr);
+  E->dst_s[0] = E->dst;
+  for (int st = 1; st < E->S; ++st) {
+    CUDA_OK(cudaMalloc(&E->dst_s[st], (size_t)(8 + 2 * (T + 1)) * 4));
+    CUDA_OK(cudaMemset(E->dst_s[st], 0, (size_t)(8 + 2 * (T + 1)) * 4));
+  }
+  CUDA_OK(cudaMalloc(&E->bmeta, (size_t)T * 3 * 4));
+  CUDA_OK(cudaMalloc(&E->btok, (size_t)T * 4));
+  CUDA_OK(cudaMalloc(&E->bpos, (size_t)T * 4));
   E->gbuf = (int32_t*)(b + o_gb);
   E->tcws = (void*)(b + o_tc);
   E->tcws_d = (void*)(b + o_tcd);
@@ -515,7 +548,8 @@ int dense_split(int rows, int kdim) {
 // routes.  Returns the O projection's split count.  cap_in (nullable): copy of the residual
 // entering the layer (trace_level 3).
 int enqueue_attn(mspq_engine* E, int l, int T, const int32_t* pos0, const float* y, const int32_t* entry_of,
-                 const float* wts, int y_splits, long long y_stride, float* cap_in, cudaStream_t s) {
+                 const float* wts, int y_splits, long long y_stride, float* cap_in, cudaStream_t s,
+                 const int32_t* meta = nullptr) {
   const auto& m = E->m;
   const int d = m.d;
   // the normed rows go straight into the QKV GEMM's B image and the attention output into the O
@@ -527,9 +561,14 @@ int enqueue_attn(mspq_engine* E, int l, int T, const int32_t* pos0, const float*
   const unsigned char* wl = E->wattn + (size_t)l * E->wattn_layer;
   const int spq = dense_split(E->Nqkv, d), spo = dense_split(d, E->Nq);
   CAPI_OK(mspq_dense_bf16_tc(E->dsched_of(T), nullptr, wl, E->Nqkv, d, T, spq, E->dws, E->qkv, (long long)T * E->Nqkv, s));
-  CAPI_OK(mspq_attention(E->qkv, spq, (long long)T * E->Nqkv, T, m.H, m.Hkv, m.Dh, m.P, pos0,
-                         E->kcache + (size_t)l * E->kv_layer(), E->vcache + (size_t)l * E->kv_layer(), nullptr, E->dws,
-                         E->attn_part, s));
+  if (meta)  // batched request streams: per-token window / stream / position, one KV cache per stream
+    CAPI_OK(mspq_attention_batched(E->qkv, spq, (long long)T * E->Nqkv, T, m.H, m.Hkv, m.Dh, m.P, meta,
+                                   (long long)m.L * (long long)E->kv_layer(), E->kv_base_k + (size_t)l * E->kv_layer(),
+                                   E->kv_base_v + (size_t)l * E->kv_layer(), nullptr, E->dws, E->attn_part, s));
+  else
+    CAPI_OK(mspq_attention(E->qkv, spq, (long long)T * E->Nqkv, T, m.H, m.Hkv, m.Dh, m.P, pos0,
+                           E->kcache + (size_t)l * E->kv_layer(), E->vcache + (size_t)l * E->kv_layer(), nullptr,
+                           E->dws, E->attn_part, s));
   CAPI_OK(mspq_dense_bf16_tc(E->dsched_of(T), nullptr, wl + (size_t)E->Nqkv * d * 2, d, E->Nq, T, spo, E->dws,
                              E->oproj, (long long)T * d, s));
   return spo;
@@ -788,12 +827,22 @@ static void configure(mspq_engine* E, const std::string& text) {
     for (auto ev : E->ev_ready) cudaEventDestroy(ev);
     E->ev_ready.assign(nbuf, nullptr);
     for (auto& ev : E->ev_ready) CUDA_OK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    if (E->gexec) {
-      cudaGraphExecDestroy(E->gexec);
-      cudaGraphDestroy(E->graph);
-      E->gexec = nullptr;
+    for (size_t st = 0; st < E->gexec_s.size(); ++st) {
+      cudaGraphExecDestroy(E->gexec_s[st]);
+      cudaGraphDestroy(E->graph_s[st]);
     }
-    capture_draft_graph(E);
+    E->gexec_s.clear();
+    E->graph_s.clear();
+    E->gexec = nullptr;
+    for (int st = 0; st < E->S; ++st) {  // one draft graph per request stream (its state, its KV cache)
+      E->gexec_s.push_back(nullptr);
+      E->use_stream(st);
+      E->gexec = nullptr;
+      capture_draft_graph(E);
+      E->gexec_s[st] = E->gexec;
+      E->graph_s.push_back(E->graph);
+    }
+    E->use_stream(0);
   }
   E->ready_rec.assign(E->nbuf, 0);
   E->elb_freq.assign((size_t)m.L * m.E, (double)m.K / m.E);  // uniform prior: K of E experts per token
@@ -924,7 +973,7 @@ static uint64_t copy_expert(mspq_engine* E, int key, unsigned char* dst) {
 }
 
 static int issue_copies(mspq_engine* E, int cycle, CopyBatch& batch, uint64_t& bytes, bool prefetch = false,
-                        const std::vector<std::pair<int, int>>* list = nullptr) {
+                        const std::vector<std::pair<int, int>>* list = nullptr, int layer = -1) {
   cudaStream_t sx = E->sx, sdec = E->sdec;
   unsigned char** stage = E->stage;
   cudaEvent_t* ev_stage = E->ev_stage;
@@ -935,6 +984,22 @@ static int issue_copies(mspq_engine* E, int cycle, CopyBatch& batch, uint64_t& b
     if (E->view.host_stat[S_OVERFLOW]) fail(MSPQ_ERR_OVERFLOW, "device controller ran out of buffers / queue");
     if (n > E->view.req_cap) fail(MSPQ_ERR_OVERFLOW, "copy request queue overflow");
   }
+  // refetch_from_hbm: per request, the index in this list of the request that fills the key's
+  // first-request buffer (-1 = filled before this list); a refetch may copy from it only after it
+  std::vector<int>& fill_at = E->fill_at;
+  if (layer >= 0 && E->cfg.refetch_from_hbm) {
+    fill_at.assign(n, -1);
+    for (int i = 0; i < n; ++i) {
+      const int key = E->view.host_req[i * 3];
+      if (key / E->m.E == layer && E->view.host_req[i * 3 + 1] == E->view.host_sched[1 + key % E->m.E])
+        fill_at[i] = i;
+    }
+  }
+  auto filled_before = [&](int i, int key, int b0) {
+    for (int j = 0; j < n; ++j)
+      if (fill_at[j] >= 0 && E->view.host_req[j * 3] == key && E->view.host_req[j * 3 + 1] == b0) return j < i;
+    return true;
+  };
   for (int i = 0; i < n; ++i) {
     const int key = list ? (*list)[i].first : E->view.host_req[i * 3];
     const int buf = list ? (*list)[i].second : E->view.host_req[i * 3 + 1];
@@ -949,6 +1014,24 @@ static int issue_copies(mspq_engine* E, int cycle, CopyBatch& batch, uint64_t& b
     }
     const bool reused = E->last_cycle[buf] == cycle;  // the slot's last reader is this cycle's GEMM
     unsigned char* slot = E->pool + (size_t)buf * E->S16;
+    if (layer >= 0 && key / E->m.E == layer && E->cfg.refetch_from_hbm) {
+      // evicted and requested again inside this verify layer: the key's first-request buffer
+      // (host_sched, published by the controller with this request list) is parked until the
+      // layer's GEMM has read it (ctl.cu erase), so it still holds the expert -- copy it HBM -> HBM
+      // on the writer lane, in order after the write that filled it.  Same decision, no link bytes.
+      const int b0 = E->view.host_sched[1 + key % E->m.E];
+      if (b0 >= 0 && b0 < E->nbuf && b0 != buf && !list && filled_before(i, key, b0)) {
+        cudaStream_t w = E->codec ? sdec : sx;
+        if (reused) CUDA_OK(cudaStreamWaitEvent(w, E->ev_gemm[E->last_layer[buf]], 0));
+        if (E->ready_rec[b0]) CUDA_OK(cudaStreamWaitEvent(w, E->ev_ready[b0], 0));
+        CUDA_OK(cudaMemcpyAsync(slot, E->pool + (size_t)b0 * E->S16, E->S16, cudaMemcpyDeviceToDevice, w));
+        CUDA_OK(cudaEventRecord(E->ev_ready[buf], w));
+        E->ready_rec[buf] = 1;
+        ++E->n_refetch;
+        ++batch.count;
+        continue;
+      }
+    }
     if (const unsigned char* hs = E->home_src(key)) {
       // peer-expert tier: HBM -> HBM from the key's home region (a peer's over NVLink, or this
       // GPU's own), in the decode stream's order so it follows any earlier write into the slot
@@ -1018,6 +1101,119 @@ static int issue_copies(mspq_engine* E, int cycle, CopyBatch& batch, uint64_t& b
   return n;
 }
 
+// Prefill of one prompt's tokens 0 .. n_prompt-2 (attention models): the target,
+// layer-major over the whole prompt in chunks of up to 32 tokens, so their KV rows exist before the
+// first cycle.  A prompt routes to (nearly) every expert of every layer, so each layer's E experts
+// are streamed from the host store (or the peer tier's homes) into one of two layer buffers, two
+// layers ahead of the compute, outside the capped cache (whose state the prefill leaves alone).
+// Writes the KV rows of the engine's current stream (E->kcache / E->vcache).
+static json run_prefill(mspq_engine* E, const int32_t* prompt, int n_prompt) {
+  const auto& m = E->m;
+  const int L = m.L, K = m.K, Ex = m.E, d = m.d;
+  json prefill = json::object();
+  const auto pw0 = std::chrono::steady_clock::now();
+  const int n = n_prompt - 1, CH = 32, nch = (n + CH - 1) / CH;
+  if (nch > L) fail(MSPQ_ERR_RANGE_OUT_OF_BOUNDS, "prompt longer than 32 x layers tokens");
+  const size_t plane = (size_t)mspq_engine::kMaxSplit * CH * K * d;  // floats per chunk planes
+  if (!E->pf_buf[0]) {
+    for (int i = 0; i < 2; ++i) {
+      CUDA_OK(cudaMalloc(&E->pf_buf[i], (size_t)Ex * E->S16));
+      CUDA_OK(cudaEventCreateWithFlags(&E->pf_ready[i], cudaEventDisableTiming));
+      CUDA_OK(cudaEventCreateWithFlags(&E->pf_done[i], cudaEventDisableTiming));
+    }
+    std::vector<int32_t> idn(Ex);
+    for (int e = 0; e < Ex; ++e) idn[e] = e;
+    CUDA_OK(cudaMalloc(&E->pf_gbuf, Ex * 4));
+    CUDA_OK(cudaMemcpy(E->pf_gbuf, idn.data(), Ex * 4, cudaMemcpyHostToDevice));
+  }
+  if (n > E->pf_n) {
+    for (float* p : {E->pf_h, E->pf_y[0], E->pf_y[1]})
+      if (p) cudaFree(p);
+    CUDA_OK(cudaMalloc(&E->pf_h, (size_t)n * d * 4));
+    CUDA_OK(cudaMalloc(&E->pf_y[0], (size_t)nch * plane * 4));
+    CUDA_OK(cudaMalloc(&E->pf_y[1], (size_t)nch * plane * 4));
+    if (E->pf_eo) cudaFree(E->pf_eo);
+    CUDA_OK(cudaMalloc(&E->pf_eo, (size_t)nch * CH * K * 4 * 2));
+    E->pf_n = n;
+  }
+  std::vector<int32_t> pos_all(n), tok_all(prompt, prompt + n);
+  for (int i = 0; i < n; ++i) pos_all[i] = i;
+  int32_t *d_tok = nullptr, *d_pos = nullptr;
+  CUDA_OK(cudaMalloc(&d_tok, (size_t)n * 4));
+  CUDA_OK(cudaMalloc(&d_pos, (size_t)n * 4));
+  CUDA_OK(cudaMemcpyAsync(d_tok, tok_all.data(), (size_t)n * 4, cudaMemcpyHostToDevice, E->sc));
+  CUDA_OK(cudaMemcpyAsync(d_pos, pos_all.data(), (size_t)n * 4, cudaMemcpyHostToDevice, E->sc));
+  CAPI_OK(mspq_embed(E->embed, E->pos, d_tok, d_pos, n, d, E->pf_h, E->sc));
+  uint64_t pf_bytes = 0;
+  E->ev_pool_next = 0;
+  auto stream_layer = [&](int l) {  // layer l's experts into buffer l & 1, after layer l-2's GEMMs
+    const int bi = l & 1;
+    if (l >= 2) {  // every stream that writes the buffer (copy; decode / home copies) waits for its readers
+      CUDA_OK(cudaStreamWaitEvent(E->sx, E->pf_done[bi], 0));
+      if (E->sdec) CUDA_OK(cudaStreamWaitEvent(E->sdec, E->pf_done[bi], 0));
+    }
+    for (int e = 0; e < Ex; ++e) pf_bytes += copy_expert(E, l * Ex + e, E->pf_buf[bi] + (size_t)e * E->S16);
+    CUDA_OK(cudaEventRecord(E->pf_ready[bi], E->codec ? E->sdec : E->sx));
+  };
+  stream_layer(0);
+  if (L > 1) stream_layer(1);
+  std::vector<int> ysp_ch(nch, 1);
+  for (int l = 0; l < L; ++l) {
+    if (E->ev_pool_next > E->ev_pool.size() / 2 + 256) E->ev_pool_next = 0;  // events of finished layers
+    bool waited = false;
+    for (int c = 0; c < nch; ++c) {
+      const int t0 = c * CH, T = std::min(CH, n - t0);
+      float* hc = E->pf_h + (size_t)t0 * d;
+      float* yprev = E->pf_y[(l - 1) & 1] + (size_t)c * plane;
+      float* ycur = E->pf_y[l & 1] + (size_t)c * plane;
+      Sched& sv = E->sv[c & 1];
+      // attention block of chunk c (the residual lives in pf_h; E->h is the window workspace)
+      CUDA_OK(cudaMemcpyAsync(E->h, hc, (size_t)T * d * 4, cudaMemcpyDeviceToDevice, E->sc));
+      int32_t* eo_prev = E->pf_eo + ((size_t)((l - 1) & 1) * nch + c) * CH * K;
+      int32_t* eo_cur = E->pf_eo + ((size_t)(l & 1) * nch + c) * CH * K;
+      const int ysp = enqueue_attn(E, l, T, d_pos + t0, l ? yprev : nullptr, l ? eo_prev : nullptr,
+                                   l ? E->wts_t + (size_t)c * CH * K : nullptr, ysp_ch[c], (long long)T * K * d,
+                                   nullptr, E->sc);
+      int32_t* ids = E->ids_t;  // [T][K] of this chunk
+      CAPI_OK(mspq_gate_topk(E->h, E->oproj, nullptr, nullptr, ysp, (long long)T * d, E->gamma + (size_t)l * d,
+                             E->router + (size_t)l * Ex * d, E->xn, ids, E->wts_t + (size_t)c * CH * K, nullptr,
+                             nullptr, nullptr, nullptr, nullptr, l, L, T, d, Ex, K, m.eps, E->sc));
+      CAPI_OK(mspq_build_schedule(ids, T, K, Ex, E->pf_gbuf, sv.n_groups, sv.group_expert, sv.group_buf,
+                                  sv.group_off, sv.entry_tok, sv.entry_of, sv.entry_group, E->sc));
+      if (!waited) {  // the layer's experts have landed
+        CUDA_OK(cudaStreamWaitEvent(E->sc, E->pf_ready[l & 1], 0));
+        waited = true;
+      }
+      const int G = std::min(Ex, T * K);
+      const int units = std::max(1, G * (2 * m.f / 128));
+      const int sp1 = std::max(1, std::min({(296 + units - 1) / units, mspq_engine::kMaxSplit, d / 64}));
+      const int units2 = std::max(1, G * (d / 128));
+      const int sp2 = std::max(1, std::min({(296 + units2 - 1) / units2, mspq_engine::kMaxSplit, m.f / 64}));
+      CAPI_OK(mspq_moe_bf16_tc(sv.n_groups, sv.group_expert, sv.group_buf, sv.group_off, sv.entry_tok,
+                               sv.entry_group, E->xn, E->pf_buf[l & 1], E->S16, d, m.f, T, K, E->G, sp1, sp2,
+                               E->tcws, ycur, E->sc));
+      CUDA_OK(cudaMemcpyAsync(hc, E->h, (size_t)T * d * 4, cudaMemcpyDeviceToDevice, E->sc));
+      ysp_ch[c] = sp2;
+      // the chunk's entry_of must survive until layer l+1's combine of this chunk (the Sched
+      // double buffer holds two chunks); its routing weights stay at wts_t + c * 32 K
+      CUDA_OK(cudaMemcpyAsync(eo_cur, sv.entry_of, (size_t)T * K * 4, cudaMemcpyDeviceToDevice, E->sc));
+    }
+    CUDA_OK(cudaEventRecord(E->pf_done[l & 1], E->sc));
+    if (l + 2 < L) stream_layer(l + 2);
+  }
+  CUDA_OK(cudaStreamSynchronize(E->sc));
+  CUDA_OK(cudaStreamSynchronize(E->sx));
+  if (E->sdec) CUDA_OK(cudaStreamSynchronize(E->sdec));
+  cudaFree(d_tok);
+  cudaFree(d_pos);
+  prefill["tokens"] = n;
+  prefill["windows"] = nch;
+  prefill["expert_copies"] = (uint64_t)L * Ex;
+  prefill["h2d_bytes"] = pf_bytes;
+  prefill["time_s"] = std::chrono::duration<double>(std::chrono::steady_clock::now() - pw0).count();
+  return prefill;
+}
+
 static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt, int max_new) {
   if (!E->configured) fail(MSPQ_ERR_INVALID_CONFIG, "engine not configured");
   if (n_prompt < 1) fail(MSPQ_ERR_EMPTY_RANGE, "empty prompt");
@@ -1071,6 +1267,7 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
   E->hmid_d_hist.clear();
   E->gen_peer_bytes = E->gen_home_local_bytes = 0;
   E->n_peer = E->n_home_local = 0;
+  E->n_refetch = 0;
   std::vector<int> committed;
   json cycles = json::array();
   double stall_total = 0.0, layer_cov_total = 0.0, step_cov_total = 0.0;
@@ -1127,7 +1324,7 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
       CopyBatch b;
       b.label = "io_new";
       b.demand = true;
-      issue_copies(E, cycle, b, cyc_bytes);
+      issue_copies(E, cycle, b, cyc_bytes, false, nullptr, l);
       if (b.count) batches.push_back(b);
       if (!E->deferred.empty()) {
         // deferred plan prefetches for layer l+1 go right behind layer l's demand copies; when l+1
@@ -1219,106 +1416,7 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
   // reported apart from the decode metric (TTFT vs TPOT).
   json prefill = json::object();
   if (E->attn && n_prompt > 1) {
-    const auto pw0 = std::chrono::steady_clock::now();
-    const int n = n_prompt - 1, CH = 32, nch = (n + CH - 1) / CH;
-    if (nch > L) fail(MSPQ_ERR_RANGE_OUT_OF_BOUNDS, "prompt longer than 32 x layers tokens");
-    const size_t plane = (size_t)mspq_engine::kMaxSplit * CH * K * d;  // floats per chunk planes
-    if (!E->pf_buf[0]) {
-      for (int i = 0; i < 2; ++i) {
-        CUDA_OK(cudaMalloc(&E->pf_buf[i], (size_t)Ex * E->S16));
-        CUDA_OK(cudaEventCreateWithFlags(&E->pf_ready[i], cudaEventDisableTiming));
-        CUDA_OK(cudaEventCreateWithFlags(&E->pf_done[i], cudaEventDisableTiming));
-      }
-      std::vector<int32_t> idn(Ex);
-      for (int e = 0; e < Ex; ++e) idn[e] = e;
-      CUDA_OK(cudaMalloc(&E->pf_gbuf, Ex * 4));
-      CUDA_OK(cudaMemcpy(E->pf_gbuf, idn.data(), Ex * 4, cudaMemcpyHostToDevice));
-    }
-    if (n > E->pf_n) {
-      for (float* p : {E->pf_h, E->pf_y[0], E->pf_y[1]})
-        if (p) cudaFree(p);
-      CUDA_OK(cudaMalloc(&E->pf_h, (size_t)n * d * 4));
-      CUDA_OK(cudaMalloc(&E->pf_y[0], (size_t)nch * plane * 4));
-      CUDA_OK(cudaMalloc(&E->pf_y[1], (size_t)nch * plane * 4));
-      if (E->pf_eo) cudaFree(E->pf_eo);
-      CUDA_OK(cudaMalloc(&E->pf_eo, (size_t)nch * CH * K * 4 * 2));
-      E->pf_n = n;
-    }
-    std::vector<int32_t> pos_all(n), tok_all(prompt, prompt + n);
-    for (int i = 0; i < n; ++i) pos_all[i] = i;
-    int32_t *d_tok = nullptr, *d_pos = nullptr;
-    CUDA_OK(cudaMalloc(&d_tok, (size_t)n * 4));
-    CUDA_OK(cudaMalloc(&d_pos, (size_t)n * 4));
-    CUDA_OK(cudaMemcpyAsync(d_tok, tok_all.data(), (size_t)n * 4, cudaMemcpyHostToDevice, E->sc));
-    CUDA_OK(cudaMemcpyAsync(d_pos, pos_all.data(), (size_t)n * 4, cudaMemcpyHostToDevice, E->sc));
-    CAPI_OK(mspq_embed(E->embed, E->pos, d_tok, d_pos, n, d, E->pf_h, E->sc));
-    uint64_t pf_bytes = 0;
-    E->ev_pool_next = 0;
-    auto stream_layer = [&](int l) {  // layer l's experts into buffer l & 1, after layer l-2's GEMMs
-      const int bi = l & 1;
-      if (l >= 2) {  // every stream that writes the buffer (copy; decode / home copies) waits for its readers
-        CUDA_OK(cudaStreamWaitEvent(E->sx, E->pf_done[bi], 0));
-        if (E->sdec) CUDA_OK(cudaStreamWaitEvent(E->sdec, E->pf_done[bi], 0));
-      }
-      for (int e = 0; e < Ex; ++e) pf_bytes += copy_expert(E, l * Ex + e, E->pf_buf[bi] + (size_t)e * E->S16);
-      CUDA_OK(cudaEventRecord(E->pf_ready[bi], E->codec ? E->sdec : E->sx));
-    };
-    stream_layer(0);
-    if (L > 1) stream_layer(1);
-    std::vector<int> ysp_ch(nch, 1);
-    for (int l = 0; l < L; ++l) {
-      if (E->ev_pool_next > E->ev_pool.size() / 2 + 256) E->ev_pool_next = 0;  // events of finished layers
-      bool waited = false;
-      for (int c = 0; c < nch; ++c) {
-        const int t0 = c * CH, T = std::min(CH, n - t0);
-        float* hc = E->pf_h + (size_t)t0 * d;
-        float* yprev = E->pf_y[(l - 1) & 1] + (size_t)c * plane;
-        float* ycur = E->pf_y[l & 1] + (size_t)c * plane;
-        Sched& sv = E->sv[c & 1];
-        // attention block of chunk c (the residual lives in pf_h; E->h is the window workspace)
-        CUDA_OK(cudaMemcpyAsync(E->h, hc, (size_t)T * d * 4, cudaMemcpyDeviceToDevice, E->sc));
-        int32_t* eo_prev = E->pf_eo + ((size_t)((l - 1) & 1) * nch + c) * CH * K;
-        int32_t* eo_cur = E->pf_eo + ((size_t)(l & 1) * nch + c) * CH * K;
-        const int ysp = enqueue_attn(E, l, T, d_pos + t0, l ? yprev : nullptr, l ? eo_prev : nullptr,
-                                     l ? E->wts_t + (size_t)c * CH * K : nullptr, ysp_ch[c], (long long)T * K * d,
-                                     nullptr, E->sc);
-        int32_t* ids = E->ids_t;  // [T][K] of this chunk
-        CAPI_OK(mspq_gate_topk(E->h, E->oproj, nullptr, nullptr, ysp, (long long)T * d, E->gamma + (size_t)l * d,
-                               E->router + (size_t)l * Ex * d, E->xn, ids, E->wts_t + (size_t)c * CH * K, nullptr,
-                               nullptr, nullptr, nullptr, nullptr, l, L, T, d, Ex, K, m.eps, E->sc));
-        CAPI_OK(mspq_build_schedule(ids, T, K, Ex, E->pf_gbuf, sv.n_groups, sv.group_expert, sv.group_buf,
-                                    sv.group_off, sv.entry_tok, sv.entry_of, sv.entry_group, E->sc));
-        if (!waited) {  // the layer's experts have landed
-          CUDA_OK(cudaStreamWaitEvent(E->sc, E->pf_ready[l & 1], 0));
-          waited = true;
-        }
-        const int G = std::min(Ex, T * K);
-        const int units = std::max(1, G * (2 * m.f / 128));
-        const int sp1 = std::max(1, std::min({(296 + units - 1) / units, mspq_engine::kMaxSplit, d / 64}));
-        const int units2 = std::max(1, G * (d / 128));
-        const int sp2 = std::max(1, std::min({(296 + units2 - 1) / units2, mspq_engine::kMaxSplit, m.f / 64}));
-        CAPI_OK(mspq_moe_bf16_tc(sv.n_groups, sv.group_expert, sv.group_buf, sv.group_off, sv.entry_tok,
-                                 sv.entry_group, E->xn, E->pf_buf[l & 1], E->S16, d, m.f, T, K, E->G, sp1, sp2,
-                                 E->tcws, ycur, E->sc));
-        CUDA_OK(cudaMemcpyAsync(hc, E->h, (size_t)T * d * 4, cudaMemcpyDeviceToDevice, E->sc));
-        ysp_ch[c] = sp2;
-        // the chunk's entry_of must survive until layer l+1's combine of this chunk (the Sched
-        // double buffer holds two chunks); its routing weights stay at wts_t + c * 32 K
-        CUDA_OK(cudaMemcpyAsync(eo_cur, sv.entry_of, (size_t)T * K * 4, cudaMemcpyDeviceToDevice, E->sc));
-      }
-      CUDA_OK(cudaEventRecord(E->pf_done[l & 1], E->sc));
-      if (l + 2 < L) stream_layer(l + 2);
-    }
-    CUDA_OK(cudaStreamSynchronize(E->sc));
-    CUDA_OK(cudaStreamSynchronize(E->sx));
-    if (E->sdec) CUDA_OK(cudaStreamSynchronize(E->sdec));
-    cudaFree(d_tok);
-    cudaFree(d_pos);
-    prefill["tokens"] = n;
-    prefill["windows"] = nch;
-    prefill["expert_copies"] = (uint64_t)L * Ex;
-    prefill["h2d_bytes"] = pf_bytes;
-    prefill["time_s"] = std::chrono::duration<double>(std::chrono::steady_clock::now() - pw0).count();
+    prefill = run_prefill(E, prompt, n_prompt);
     // the decode state (head token / position) the prefill's embed left alone, and the decode's clock
     CUDA_OK(cudaEventRecord(E->ev_t0, E->sc));  // the decode's clock starts after the prefill
     CUDA_OK(cudaStreamWaitEvent(E->sx, E->ev_t0, 0));
@@ -1333,6 +1431,7 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
     const int k = std::max(1, std::min({kk, rem, E->o.kmax}));
     const int T = k + 1;
     const int est_new = c.use_governor ? est()(k) : -1;
+    const uint64_t refetch0 = E->n_refetch;
     const double est_raw = c.estimator == 1 ? elb_raw(k) : 0.0;
     uint64_t cyc_bytes = 0;
     std::vector<CopyBatch> batches;
@@ -1484,6 +1583,7 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
     rec["step_coverage"] = sc_sum / (T * L);
     rec["steps"] = T * L;
     rec["new_experts"] = fetched;
+    rec["refetch_hbm"] = E->n_refetch - refetch0;
     if (c.use_governor) rec["est_new_experts"] = est_new;
     rec["bytes"] = cyc_bytes;
     rec["io_wait_s"] = stall;
@@ -1623,7 +1723,10 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
     g = static_cast<double>(fetched) / static_cast<double>(k);
     if (c.estimator == 1) {
       constexpr double beta = 1.0 / 32.0;
-      if (est_raw > 0.0) E->elb_calib[k] = (1.0 - 0.25) * E->elb_calib[k] + 0.25 * (static_cast<double>(fetched) / est_raw);
+      // calibrated against the fetches that crossed the link: an in-layer refetch served from HBM
+      // (refetch_from_hbm) is exactly what the union model leaves out
+      const double moved = static_cast<double>(fetched) - static_cast<double>(E->n_refetch - refetch0);
+      if (est_raw > 0.0) E->elb_calib[k] = (1.0 - 0.25) * E->elb_calib[k] + 0.25 * (moved / est_raw);
       // per drafted row: p <- (1-beta) p + beta [e in row's top-K at layer l]
       const int32_t* rows = hp + o_res_tab + (size_t)L * Ex;
       for (int r = 0; r < k; ++r)
@@ -1668,6 +1771,7 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
   rep["tokens"] = committed;
   rep["h2d_bytes"] = h2d_bytes;
   rep["h2d_bytes_bf16"] = (uint64_t)total_new * (uint64_t)E->S16;
+  rep["refetch_hbm"] = E->n_refetch;
   if (E->peer_G > 0) {  // peer-expert tier: where the fetched experts' bytes came from
     json pt;
     pt["group"] = E->peer_G;
@@ -1676,7 +1780,7 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
     pt["home_local_bytes"] = E->gen_home_local_bytes;
     pt["peer_fetches"] = E->n_peer;
     pt["home_local_fetches"] = E->n_home_local;
-    pt["pcie_fetches"] = (uint64_t)total_new - E->n_peer - E->n_home_local;
+    pt["pcie_fetches"] = (uint64_t)total_new - E->n_peer - E->n_home_local - E->n_refetch;
     rep["peer_tier"] = pt;
   }
   rep["expert_codec"] = E->codec ? "xc" : "none";
@@ -1758,6 +1862,283 @@ static std::string generate(mspq_engine* E, const int32_t* prompt, int n_prompt,
   return rep.dump();
 }
 
+// ============================================================================ generate_batch
+// Several request streams decoded together (include/mspq_capi.h mspq_generate_batch).  Each cycle:
+// every active stream drafts k tokens with its own captured draft graph (its state, its KV cache);
+// their verify windows are concatenated into ONE batch of n (k+1) tokens that goes through a single
+// layer-major verify pass -- K1 over the batch, attention with per-token (window, stream, position)
+// metadata, one controller step over all slots, one grouped GEMM per layer, so the streams share
+// the expert weight reads and the fetches -- then each stream's accept runs on its slice.
+static std::string generate_batch(mspq_engine* E, const int32_t* prompts, const int32_t* lens, int n_streams,
+                                  int max_new) {
+  if (!E->configured) fail(MSPQ_ERR_INVALID_CONFIG, "engine not configured");
+  const auto& m = E->m;
+  const HostCfg& c = E->cfg;
+  if (n_streams < 1 || n_streams > E->S) fail(MSPQ_ERR_INVALID_CONFIG, "more streams than the engine's max_streams");
+  if (c.policy != 0) fail(MSPQ_ERR_INVALID_CONFIG, "generate_batch needs the lru policy");
+  const int L = m.L, K = m.K, Ex = m.E, d = m.d, n = n_streams;
+  std::vector<const int32_t*> pr(n);
+  std::vector<int> plen(n), head(n);
+  for (int i = 0, off = 0; i < n; off += lens[i], ++i) {
+    pr[i] = prompts + off;
+    plen[i] = lens[i];
+    if (plen[i] < 1) fail(MSPQ_ERR_EMPTY_RANGE, "empty prompt");
+    if (plen[i] - 1 + max_new + E->Tmax >= m.P) fail(MSPQ_ERR_RANGE_OUT_OF_BOUNDS, "positions exceed the positional table");
+    for (int j = 0; j < plen[i]; ++j)
+      if (pr[i][j] < 0 || pr[i][j] >= m.V) fail(MSPQ_ERR_RANGE_OUT_OF_BOUNDS, "prompt token out of vocab");
+    head[i] = plen[i] - 1;
+  }
+  const int level = E->o.trace_level;
+  const auto wall0 = std::chrono::steady_clock::now();
+  E->n_refetch = 0;
+  json prefills = json::array();
+  for (int i = 0; i < n; ++i) {  // prefill + device decode state of every stream
+    E->use_stream(i);
+    if (E->attn && plen[i] > 1) prefills.push_back(run_prefill(E, pr[i], plen[i]));
+    E->hpin[0] = 0;
+    E->hpin[1] = pr[i][plen[i] - 1];
+    E->hpin[2] = head[i];
+    CUDA_OK(cudaMemcpyAsync(E->dst, E->hpin, 12, cudaMemcpyHostToDevice, E->sc));
+    CUDA_OK(cudaMemcpyAsync(E->win_tok(), E->hpin + 1, 4, cudaMemcpyHostToDevice, E->sc));
+    CUDA_OK(cudaStreamSynchronize(E->sc));
+  }
+  E->use_stream(0);
+  CUDA_OK(cudaEventRecord(E->ev_t0, E->sc));
+  CUDA_OK(cudaStreamWaitEvent(E->sx, E->ev_t0, 0));
+  if (E->sdec) CUDA_OK(cudaStreamWaitEvent(E->sdec, E->ev_t0, 0));
+  std::vector<std::vector<int>> committed(n);
+  json cycles = json::array();
+  uint64_t h2d = 0, total_new = 0;
+  double stall_total = 0.0;
+  std::vector<double> accept(std::max(c.use_governor ? c.k_max : c.fixed_k, 1), c.initial_accept);
+  double g = static_cast<double>(L) * static_cast<double>(K);
+  auto est = [&]() { return Est([gg = g](int k) { return static_cast<int>(std::llround(gg * static_cast<double>(k))); }); };
+  std::vector<int32_t> hbuf;
+  int ci = 0;
+  while (true) {
+    std::vector<int> act;
+    for (int i = 0; i < n; ++i)
+      if ((int)committed[i].size() < max_new) act.push_back(i);
+    if (act.empty()) break;
+    const int na = (int)act.size();
+    int rem = max_new;
+    for (int i : act) rem = std::min(rem, max_new - (int)committed[i].size());
+    const int kk = c.use_governor ? select_k(c.profile, accept, c.k_min, c.k_max, c.k_slo, est()) : c.fixed_k;
+    const int k = std::max(1, std::min({kk, rem, E->o.kmax, E->Tmax / na - 1}));
+    if (k < 1 || na * (k + 1) > E->Tmax) fail(MSPQ_ERR_K_OUT_OF_RANGE, "batch window exceeds 32 slots");
+    const int Tw = k + 1, T = na * Tw;
+    const int cycle = ++E->cycle_serial;
+    E->ev_pool_next = 0;
+    uint64_t cyc_bytes = 0;
+    CUDA_OK(cudaEventRecord(E->ev_c0, E->sc));
+    CAPI_OK(mspq_cache_begin_cycle(E->cache, k, E->sc));
+    // ---- drafts (each stream's own graph; lru: no planner)
+    for (int j = 0; j < na; ++j) {
+      E->use_stream(act[j]);
+      CUDA_OK(cudaMemsetAsync(E->dst, 0, 4, E->sc));  // row = 0
+      for (int i = 0; i < k; ++i) CUDA_OK(cudaGraphLaunch(E->gexec, E->sc));
+    }
+    CUDA_OK(cudaEventRecord(E->ev_dend, E->sc));
+    // ---- the batch: windows back to back, per-token metadata
+    hbuf.assign((size_t)T * 3 + T, 0);
+    for (int j = 0; j < na; ++j)
+      for (int sl = 0; sl < Tw; ++sl) {
+        const int t = j * Tw + sl;
+        hbuf[(size_t)t * 3] = j * Tw;
+        hbuf[(size_t)t * 3 + 1] = act[j];
+        hbuf[(size_t)t * 3 + 2] = head[act[j]] + sl;
+        hbuf[(size_t)T * 3 + t] = head[act[j]] + sl;
+      }
+    std::memcpy(E->hpin, hbuf.data(), hbuf.size() * 4);  // the previous cycle's reads are synchronised
+    CUDA_OK(cudaMemcpyAsync(E->bmeta, E->hpin, (size_t)T * 12, cudaMemcpyHostToDevice, E->sc));
+    CUDA_OK(cudaMemcpyAsync(E->bpos, E->hpin + (size_t)T * 3, (size_t)T * 4, cudaMemcpyHostToDevice, E->sc));
+    for (int j = 0; j < na; ++j)
+      CUDA_OK(cudaMemcpyAsync(E->btok + j * Tw, E->dst_s[act[j]] + 8, (size_t)Tw * 4, cudaMemcpyDeviceToDevice, E->sc));
+    E->use_stream(0);
+    CAPI_OK(mspq_embed(E->embed, E->pos, E->btok, E->bpos, T, d, E->h, E->sc));
+    // ---- one layer-major verify pass over the whole batch
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> stall_ev;
+    int ysp_prev = 1;
+    for (int l = 0; l < L; ++l) {
+      const int pl = (l - 1) & 1;
+      int32_t* tgt = E->ids_t + (size_t)l * T * K;
+      const float* y = l ? E->yv[pl] : nullptr;
+      const int32_t* eo = l ? E->sv[pl].entry_of : nullptr;
+      const float* pw = l ? E->wts_t + (size_t)(l - 1) * T * K : nullptr;
+      int ysp = ysp_prev;
+      long long yst = (long long)T * K * d;
+      if (E->attn) {
+        ysp = enqueue_attn(E, l, T, nullptr, y, eo, pw, ysp, yst, nullptr, E->sc, E->bmeta);
+        y = E->oproj;
+        eo = nullptr;
+        pw = nullptr;
+        yst = (long long)T * d;
+      }
+      CAPI_OK(mspq_gate_topk(E->h, y, eo, pw, ysp, yst, E->gamma + (size_t)l * d, E->router + (size_t)l * Ex * d,
+                             E->xn, tgt, E->wts_t + (size_t)l * T * K, nullptr, nullptr, nullptr, nullptr, nullptr, l,
+                             L, T, d, Ex, K, m.eps, E->sc));
+      Sched& sv = E->sv[l & 1];
+      CAPI_OK(mspq_cache_verify_layer(E->cache, l, T, tgt, E->gbuf, E->sc));
+      CUDA_OK(cudaEventRecord(E->ev_w0[l], E->sc));
+      CAPI_OK(mspq_build_schedule(tgt, T, K, Ex, E->gbuf, sv.n_groups, sv.group_expert, sv.group_buf, sv.group_off,
+                                  sv.entry_tok, sv.entry_of, sv.entry_group, E->sc));
+      spin_wait(E->ev_w0[l]);
+      CopyBatch b;
+      b.demand = true;
+      issue_copies(E, cycle, b, cyc_bytes, false, nullptr, l);
+      std::vector<int> gb;
+      for (int e = 0; e < Ex; ++e)
+        if (E->view.host_sched[1 + e] >= 0) gb.push_back(E->view.host_sched[1 + e]);
+      bool waited = false;
+      for (int buf : gb) {
+        if (buf < 0 || buf >= E->nbuf) fail(MSPQ_ERR_OVERFLOW, "schedule buffer out of range");
+        if (E->ready_rec[buf]) {
+          if (cudaEventQuery(E->ev_ready[buf]) == cudaErrorNotReady) {
+            CUDA_OK(cudaStreamWaitEvent(E->sc, E->ev_ready[buf], 0));
+            waited = true;
+          } else {
+            E->ready_rec[buf] = 0;
+          }
+        }
+      }
+      if (waited) {
+        CUDA_OK(cudaEventRecord(E->ev_w1[l], E->sc));
+        stall_ev.push_back({E->ev_w0[l], E->ev_w1[l]});
+      }
+      const int ng = std::max(1, (int)gb.size());
+      auto pick_split = [&](int rows, int kdim) {
+        const int units = std::max(1, ng * (rows / 128));
+        return std::max(1, std::min({(296 + units - 1) / units, mspq_engine::kMaxSplit, kdim / 64}));
+      };
+      const int sp1 = pick_split(2 * m.f, d), sp2 = pick_split(d, m.f);
+      CAPI_OK(mspq_moe_bf16_tc(sv.n_groups, sv.group_expert, sv.group_buf, sv.group_off, sv.entry_tok, sv.entry_group,
+                               E->xn, E->pool, E->S16, d, m.f, T, K, E->G, sp1, sp2, E->tcws, E->yv[l & 1], E->sc));
+      CUDA_OK(cudaEventRecord(E->ev_gemm[l], E->sc));
+      for (int buf : gb) {
+        E->last_cycle[buf] = cycle;
+        E->last_layer[buf] = l;
+      }
+      ysp_prev = sp2;
+    }
+    const int pl = (L - 1) & 1;
+    CAPI_OK(mspq_gate_topk(E->h, E->yv[pl], E->sv[pl].entry_of, E->wts_t + (size_t)(L - 1) * T * K, ysp_prev,
+                           (long long)T * K * d, E->gfinal, nullptr, E->xn, nullptr, nullptr, nullptr, nullptr, nullptr,
+                           nullptr, nullptr, L, L, T, d, Ex, K, m.eps, E->sc));
+    CAPI_OK(mspq_lm_head(E->xn, E->lm, T, m.V, d, E->logits, E->sc));
+    CAPI_OK(mspq_argmax(E->logits, T, m.V, E->amax, E->sc));
+    for (int j = 0; j < na; ++j) {  // accept per stream on its slice; next head = its bonus
+      int32_t* ds = E->dst_s[act[j]];
+      CAPI_OK(mspq_accept_advance(ds + 8 + 1, E->amax + j * Tw, k, ds + 3, ds + 1, ds + 2, head[act[j]], E->sc));
+      CUDA_OK(cudaMemcpyAsync(ds + 8, ds + 1, 4, cudaMemcpyDeviceToDevice, E->sc));
+    }
+    // results back: per stream (accepted, bonus, drafts), target argmax, routing (level >= 1)
+    int32_t* hp = E->hpin;
+    for (int j = 0; j < na; ++j) {
+      CUDA_OK(cudaMemcpyAsync(hp + j * (2 + k), E->dst_s[act[j]] + 3, 8, cudaMemcpyDeviceToHost, E->sc));
+      CUDA_OK(cudaMemcpyAsync(hp + j * (2 + k) + 2, E->dst_s[act[j]] + 8 + 1, (size_t)k * 4, cudaMemcpyDeviceToHost, E->sc));
+    }
+    const size_t o_tr = (size_t)na * (2 + k);
+    if (level >= 1)
+      CUDA_OK(cudaMemcpyAsync(hp + o_tr, E->ids_t, (size_t)L * T * K * 4, cudaMemcpyDeviceToHost, E->sc));
+    CUDA_OK(cudaEventRecord(E->ev_end, E->sc));
+    CUDA_OK(cudaEventSynchronize(E->ev_end));
+    const int fetched = E->view.host_stat[S_FETCHED];
+    double stall = 0.0;
+    for (auto& [a, b2] : stall_ev) stall += elapsed_s(a, b2);
+    json rec;
+    rec["cycle"] = ci;
+    rec["k"] = k;
+    rec["streams"] = act;
+    rec["new_experts"] = fetched;
+    rec["bytes"] = cyc_bytes;
+    rec["io_wait_s"] = stall;
+    rec["start_s"] = elapsed_s(E->ev_t0, E->ev_c0);
+    rec["span_s"] = elapsed_s(E->ev_c0, E->ev_end);
+    json toks = json::array(), accs = json::array();
+    int acc_sum = 0;
+    for (int j = 0; j < na; ++j) {
+      const int sidx = act[j];
+      const int accepted = hp[j * (2 + k)], bonus_tok = hp[j * (2 + k) + 1];
+      std::vector<int> nt;
+      for (int i = 0; i < accepted; ++i) nt.push_back(hp[j * (2 + k) + 2 + i]);
+      nt.push_back(bonus_tok);
+      const int remi = max_new - (int)committed[sidx].size();
+      if ((int)nt.size() > remi) nt.resize(remi);
+      for (int t2 : nt) committed[sidx].push_back(t2);
+      head[sidx] += accepted + 1;
+      toks.push_back(nt);
+      accs.push_back(accepted);
+      acc_sum += accepted;
+      // governor EMA over every stream's outcomes
+      std::vector<bool> outcomes;
+      for (int i = 0; i < k; ++i) {
+        outcomes.push_back(i < accepted);
+        if (i >= accepted) break;
+      }
+      if (outcomes.size() > accept.size()) outcomes.resize(accept.size());
+      accept = update_acceptance(accept, c.ema_alpha, outcomes);
+    }
+    rec["tokens"] = toks;
+    rec["accepted"] = accs;
+    if (level >= 1) {
+      json tgt = json::array();  // [slot][layer][K] over the batch
+      for (int t = 0; t < T; ++t) {
+        json sl = json::array();
+        for (int l = 0; l < L; ++l) {
+          json c2 = json::array();
+          for (int j2 = 0; j2 < K; ++j2) c2.push_back(hp[o_tr + ((size_t)l * T + t) * K + j2]);
+          sl.push_back(c2);
+        }
+        tgt.push_back(sl);
+      }
+      rec["target"] = tgt;
+    }
+    if (level >= 2) {
+      const int nl = std::min(E->view.host_stat[S_NLOG], E->view.log_cap);
+      std::vector<int32_t> lg((size_t)nl * 6);
+      if (nl) CUDA_OK(cudaMemcpy(lg.data(), E->view.log, (size_t)nl * 24, cudaMemcpyDeviceToHost));
+      json lj = json::array();
+      for (int i = 0; i < nl; ++i) {
+        const int32_t* ev = &lg[(size_t)i * 6];
+        lj.push_back({ev[0], ev[1], ev[2] / Ex, ev[2] % Ex, ev[3], ev[4] < 0 ? -1 : ev[4] / Ex,
+                      ev[4] < 0 ? -1 : ev[4] % Ex, ev[5]});
+      }
+      rec["log"] = lj;
+    }
+    cycles.push_back(rec);
+    g = static_cast<double>(fetched) / static_cast<double>(k * na);
+    total_new += fetched;
+    h2d += cyc_bytes;
+    stall_total += stall;
+    ++ci;
+  }
+  CUDA_OK(cudaStreamSynchronize(E->sx));
+  if (E->sdec) CUDA_OK(cudaStreamSynchronize(E->sdec));
+  E->use_stream(0);
+  json rep;
+  size_t tot = 0;
+  json st = json::array();
+  for (int i = 0; i < n; ++i) {
+    st.push_back(committed[i]);
+    tot += committed[i].size();
+  }
+  const double total_time = cycles.empty() ? 0.0
+                                           : cycles.back()["start_s"].get<double>() + cycles.back()["span_s"].get<double>();
+  rep["streams"] = n;
+  rep["tokens"] = st;
+  rep["total_tokens"] = tot;
+  rep["total_time_s"] = total_time;
+  rep["stall_time_s"] = stall_total;
+  rep["total_new_experts"] = total_new;
+  rep["h2d_bytes"] = h2d;
+  rep["h2d_bytes_bf16"] = total_new * (uint64_t)E->S16;
+  rep["refetch_hbm"] = E->n_refetch;
+  rep["cycles"] = cycles;
+  rep["prefill"] = prefills;
+  rep["wall_s"] = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+  return rep.dump();
+}
+
 // ============================================================================ C-ABI
 namespace {
 template <class F>
@@ -1780,8 +2161,16 @@ char* dupstr(const std::string& s) {
 void destroy(mspq_engine* E) {
   if (!E) return;
   cudaDeviceSynchronize();
-  if (E->gexec) cudaGraphExecDestroy(E->gexec);
-  if (E->graph) cudaGraphDestroy(E->graph);
+  for (size_t st = 0; st < E->gexec_s.size(); ++st) {
+    if (E->gexec_s[st]) cudaGraphExecDestroy(E->gexec_s[st]);
+    if (E->graph_s[st]) cudaGraphDestroy(E->graph_s[st]);
+  }
+  for (size_t st = 1; st < E->dst_s.size(); ++st)
+    if (E->dst_s[st]) cudaFree(E->dst_s[st]);
+  for (void* p : {(void*)E->bmeta, (void*)E->btok, (void*)E->bpos})
+    if (p) cudaFree(p);
+  E->kcache = E->kv_base_k;  // the allocations (stream 0)
+  E->vcache = E->kv_base_v;
   for (auto v : {&E->ev_ready, &E->ev_gemm, &E->ev_w0, &E->ev_w1, &E->ev_row, &E->ev_pool, &E->ev_k0, &E->ev_g0, &E->ev_g1,
                  &E->ev_ka1, &E->ev_rt})
     for (auto ev : *v)
@@ -1870,7 +2259,8 @@ int mspq_engine_create(const mspq_model_desc* md, const mspq_engine_opts* op, ms
       E->S4 = mspq_int4_blob_bytes(m.d, m.f);
       // window capacity: the decode's k+1 slots, and 32-token prefill windows with attention (the
       // widest K3 / K1 / attention launch; fewer prefill windows = fewer expert re-fetches)
-      E->Tmax = std::max(op->kmax + 1, m.H > 0 ? 32 : 0);
+      E->S = std::max(1, std::min(op->max_streams, 32));
+      E->Tmax = std::max(op->kmax + 1, (m.H > 0 || E->S > 1) ? 32 : 0);
       E->n_payload = m.unique_experts > 0 ? std::min(m.unique_experts, m.L * m.E) : m.L * m.E;
       if (m.H > 0) {
         if (m.Hkv < 1 || m.H % m.Hkv || m.H / m.Hkv > 8 || (m.Dh != 64 && m.Dh != 128) || (m.H * m.Dh) % 128 ||
@@ -1925,6 +2315,14 @@ int mspq_engine_configure(mspq_engine* E, const char* cfg) {
 int mspq_generate(mspq_engine* E, const int32_t* prompt, int n, int max_new, char** report) {
   return guarded([&] {
     *report = dupstr(generate(E, prompt, n, max_new));
+    return MSPQ_OK;
+  });
+}
+
+int mspq_generate_batch(mspq_engine* E, const int32_t* prompts, const int32_t* lens, int n_streams, int max_new,
+                        char** report) {
+  return guarded([&] {
+    *report = dupstr(generate_batch(E, prompts, lens, n_streams, max_new));
     return MSPQ_OK;
   });
 }

@@ -54,6 +54,8 @@ def check_control_plane(rep, conf):
     cache = cp.Cache(c["capacity_mode"], c["cache_capacity"])
     for cyc in rep["cycles"]:
         log = []
-        cp.live_cycle(cache, cp.ELB.build(cyc["elb"], cyc["elb_gates"]), cyc["target"], c, log)
+        out = cp.live_cycle(cache, cp.ELB.build(cyc["elb"], cyc["elb_gates"]), cyc["target"], c, log)
         assert device_events(cyc["log"]) == _events(log), ("hit/miss log", cyc["cycle"])
+        want = out["refetch"] if conf.get("refetch_from_hbm", True) else 0
+        assert cyc["refetch_hbm"] == want, ("in-layer refetches", cyc["cycle"])
     return cache

@@ -12,6 +12,7 @@ Near-ties are not masked: a mismatch fails the test."""
 import numpy as np
 import pytest
 
+from helpers import check_control_plane
 from oracle import control_plane as cp
 from oracle import model as om
 
@@ -85,6 +86,7 @@ def test_live_hit_miss_sequence_all_policies(cuda, policy, mode):
             "k": 5, "prefetch_budget": 1}
     eng.configure(conf)
     rep = eng.generate([1, 2, 3], 30)
+    check_control_plane(rep, conf)  # + each cycle's in-layer refetch count (served from HBM)
     want = _control_plane_log(rep, conf, cfg.L, cfg.E)
     tot_fetched = 0
     for c, w in zip(rep["cycles"], want):
@@ -183,7 +185,9 @@ def test_expert_codec_is_lossless_end_to_end(cuda):
     for ca, cb in zip(a["cycles"], b["cycles"]):
         for key in ["k", "draft_tokens", "target_argmax", "target", "elb", "log", "new_experts"]:
             assert ca[key] == cb[key], key
-    assert b["h2d_bytes_bf16"] == a["h2d_bytes"]
+    # the raw store moves every fetch's bf16 bytes except the in-layer refetches (served from HBM)
+    assert b["h2d_bytes_bf16"] - a["refetch_hbm"] * cfg.expert_bytes_bf16() == a["h2d_bytes"]
+    assert a["refetch_hbm"] == b["refetch_hbm"]
     assert b["total_new_experts"] > 0 and b["h2d_bytes"] < 0.72 * a["h2d_bytes"]
 
 
@@ -389,3 +393,30 @@ def test_hardware_profile_refit_is_measured(cuda):
     assert prof["pcie_overhead_s"] == info["pcie_overhead_measured"] >= 0
     assert prof["draft_per_token_s"] == info["draft_step_s"] > 0
     eng.close()
+
+
+@pytest.mark.parametrize("codec", ["xc", "none"])
+@pytest.mark.parametrize("policy", ["lru", "speculative"])
+def test_refetch_from_hbm_moves_bytes_not_decisions(cuda, codec, policy):
+    """An expert evicted and requested again inside one verify layer is copied HBM -> HBM from its
+    first-request buffer (parked until the layer's GEMM) instead of crossing the link again: the
+    tokens, routing and hit/miss log are the run without it, the link carries fewer bytes."""
+    import paper_2511_14102_b200 as m
+    cfg = m.ModelConfig.named("tiny")
+    conf = {"policy": policy, "cache_capacity": 2, "k": 8, "prefetch_budget": 1}
+    reps = {}
+    for on in (False, True):
+        eng = m.Engine(cfg, kmax=8, trace_level=2, expert_codec=codec)
+        eng.configure(dict(conf, refetch_from_hbm=on))
+        reps[on] = eng.generate([3, 1, 4, 1, 5], 40)
+        eng.close()
+    a, b = reps[False], reps[True]
+    assert a["tokens"] == b["tokens"] and a["total_new_experts"] == b["total_new_experts"]
+    for ca, cb in zip(a["cycles"], b["cycles"]):
+        for key in ["k", "draft_tokens", "target_argmax", "target", "log", "new_experts"]:
+            assert ca[key] == cb[key], key
+    assert a["refetch_hbm"] == 0 and b["refetch_hbm"] > 0
+    assert b["h2d_bytes"] < a["h2d_bytes"]
+    if codec == "none":
+        S = cfg.expert_bytes_bf16()
+        assert a["h2d_bytes"] - b["h2d_bytes"] == b["refetch_hbm"] * S

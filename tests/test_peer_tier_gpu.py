@@ -47,7 +47,7 @@ def test_peer_tier_in_process_moves_bytes_not_decisions(cuda, codec):
     pt = got["peer_tier"]
     assert got["h2d_bytes"] == 0 and pt["pcie_fetches"] == 0
     assert pt["peer_fetches"] > 0 and pt["home_local_fetches"] > 0
-    assert pt["peer_fetches"] + pt["home_local_fetches"] == got["total_new_experts"]
+    assert pt["peer_fetches"] + pt["home_local_fetches"] + got["refetch_hbm"] == got["total_new_experts"]
     S = e0.model.expert_bytes_bf16()
     assert pt["peer_bytes"] == pt["peer_fetches"] * S and pt["home_local_bytes"] == pt["home_local_fetches"] * S
     e0.close()
