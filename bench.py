@@ -69,6 +69,9 @@ def parse():
     ap.add_argument("--streams", type=int, default=0,
                     help="independent request streams over all ranks (BASELINE config 5: 8); stream s is served "
                          "by rank s %% N, a rank's streams one after another on its engine; 0 = one per rank")
+    ap.add_argument("--batch", action="store_true",
+                    help="decode a rank's streams together (Engine.generate_batch: one verify pass per cycle over "
+                         "every stream's window, shared expert reads and fetches); needs --policy lru")
     ap.add_argument("--same-device", action="store_true",
                     help="test mode: every rank uses cuda:0 (exercises the multi-rank path on a one-GPU box)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -356,6 +359,8 @@ def spawn_ranks(a):
 
 def main():
     a = parse()
+    if a.batch and a.policy != "lru":  # generate_batch runs the lru controller (no draft-driven planner)
+        a.policy = "lru"
     if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(spawn_ranks(a))
     if a.impl == "reference":
@@ -392,9 +397,11 @@ def main():
         store = "%s_n%d" % (name[0], max(node, 0))
         store_owner = min(r for r in range(world) if nodes[r] == node)
     t_create = time.perf_counter()
+    n_streams = a.streams or world
+    mine = [st for st in range(n_streams) if st % world == rank]
     eng = m.Engine(cfgm, kmax=16, device=local, host_store_path=store or None,
                    host_store_role=0 if (not store or rank == store_owner) else 1, trace_level=0,
-                   expert_codec=a.codec)
+                   expert_codec=a.codec, max_streams=len(mine) if a.batch else 1)
     t_create = time.perf_counter() - t_create
     t_home = 0.0
     if a.peer_tier:
@@ -417,12 +424,15 @@ def main():
     else:
         conf["k"] = int(a.k)
     eng.configure(conf)
-    n_streams = a.streams or world
-    mine = [st for st in range(n_streams) if st % world == rank]
     ps = {st: prompts(a.warmup + a.steps, cfgm.V, seed=1000 + st) for st in mine}
+
+    def step(i):  # one step = every stream of this rank decodes --tokens new tokens
+        if a.batch:
+            return [eng.generate_batch([ps[st][i] for st in mine], a.tokens)]
+        return [eng.generate(ps[st][i], a.tokens) for st in mine]
+
     for i in range(a.warmup):
-        for st in mine:
-            eng.generate(ps[st][i], a.tokens)
+        step(i)
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -430,8 +440,7 @@ def main():
     with ClockSampler(local) as clk:
         w0 = time.perf_counter()
         for i in range(a.steps):
-            for st in mine:
-                reps.append(eng.generate(ps[st][a.warmup + i], a.tokens))
+            reps.extend(step(a.warmup + i))
         torch.cuda.synchronize()
         wall = time.perf_counter() - w0
     if world > 1:
@@ -452,7 +461,10 @@ def main():
     launches = sum(r["kernels"]["kernel_launches"] for r in reps)
     ks = [c for r in reps for c in r.get("cycles", [])]
     mean_k = statistics.mean([c["k"] for c in ks]) if ks else None
-    acc = sum(c["accepted"] for c in ks) / max(1, sum(c["k"] for c in ks))
+    if a.batch:  # a batch cycle drafts k tokens for each of its streams
+        acc = sum(sum(c["accepted"]) for c in ks) / max(1, sum(c["k"] * len(c["streams"]) for c in ks))
+    else:
+        acc = sum(c["accepted"] for c in ks) / max(1, sum(c["k"] for c in ks))
     dev_max, wall_max, tok_all = aggregate(dev_t, wall, tok, world)
     if rank != 0:
         eng.close()
@@ -487,6 +499,8 @@ def main():
                    "shape": {"name": a.model, "L": L, "E": E, "top_k": K, "d": cfgm.d, "ffn": cfgm.f, "vocab": cfgm.V},
                    "cache_capacity_per_layer": cap, "host_store_GB": info["host_store_bytes"] / 1e9,
                    "streams": n_streams, "streams_per_gpu": len(mine),
+                   "stream_batching": "one verify pass per cycle over the rank's streams" if a.batch
+                   else "a rank's streams one after another",
                    "expert_codec": a.codec,
                    "l2": "inputs larger than L2: each verify layer streams >= 157 MB of experts; no flush needed"},
         "exposed_h2d_ms_per_token": stall / max(tok, 1) * 1e3,
@@ -499,7 +513,9 @@ def main():
                 "note": "wall clock of Engine.generate() (host prompt in, host tokens out) including each "
                         "request's prefill of its 128-token prompt; decode_only excludes the prefill",
                 "decode_only": tok / max(1e-9, sum(r.get("decode_wall_s", r["wall_s"]) for r in reps)),
-                "prefill_s_per_step": sum(r.get("prefill", {}).get("time_s", 0.0) for r in reps) / a.steps,
+                "prefill_s_per_step": sum(p.get("time_s", 0.0) for r in reps
+                                          for p in (r.get("prefill") if isinstance(r.get("prefill"), list)
+                                                    else [r.get("prefill", {})])) / a.steps,
                 "expert_h2d_bytes_per_step": h2d / a.steps},
         "roofline": {"bound": "hbm",
                      "kernel": "K3 bf16 grouped verify FFN on tcgen05 (gather + k_umma_grouped W13 + SiLU + W2), per layer",

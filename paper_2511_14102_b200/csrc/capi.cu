@@ -134,6 +134,7 @@ int mspq_moe_bf16_tc_part(const int32_t* n_groups, const int32_t* group_expert, 
   UmmaArgs u1{(const unsigned char*)pool, blob_bytes, 0, 2 * f, d, n_groups, group_buf, group_off, b1, p1,
               N * 2 * f, split1};
   u1.gmask = gm;
+  u1.early_a = do_gather;  // the gather sits between the schedule's writer and W13 (UmmaArgs::early_a)
   if (split1 == 1) u1.act_img = b2;  // SiLU*up in the W13 epilogue, no finalize kernel
   e = launch_umma_grouped(u1, max_groups, BN, st);
   if (e != cudaSuccess) return cuda_status(e, "umma W13");
@@ -144,6 +145,7 @@ int mspq_moe_bf16_tc_part(const int32_t* n_groups, const int32_t* group_expert, 
   UmmaArgs u2{(const unsigned char*)pool, blob_bytes, (long long)2 * f * d * 2, d, f, n_groups, group_buf,
               group_off, b2, y, N * d, split2};
   u2.gmask = gm;
+  u2.early_a = 1;  // W13 (whose own wait ordered it after the schedule) precedes W2
   CK(launch_umma_grouped(u2, max_groups, BN, st), "umma W2");
 }
 int mspq_moe_bf16_tc(const int32_t* n_groups, const int32_t* group_expert, const int32_t* group_buf,
@@ -178,6 +180,7 @@ int mspq_dense_bf16_tc(const int32_t* dsched, const void* x, const void* w_tiled
     if (e != cudaSuccess) return cuda_status(e, "dense gather");
   }
   UmmaArgs u{(const unsigned char*)w_tiled, 0, 0, rows, kdim, p, p + 1, p + 2, b1, out, out_split_stride, split};
+  u.early_a = 1;  // weights and dsched are static: the A stream starts under the predecessor's tail
   CK(launch_umma_grouped(u, 1, BN, st), "dense umma");
 }
 long long mspq_attention_ws_bytes(int T, int H, int Hkv, int Dh) {

@@ -62,7 +62,12 @@ MSPQ_D uint4 ldg_stream(const void* p) {
 template <int GV_TILES, int NB, bool H256>
 __global__ void __launch_bounds__(GV_THREADS) k_int4_gemv(GemvArgs a) {
   constexpr int ROWS = 16 * GV_TILES;
-  pdl_enter();  // launched with launch_pdl (kernels.h)
+  // launched with launch_pdl (kernels.h).  W13 (x = the K1 output, schedule written by K1) waits
+  // first.  W2's predecessor is W13, whose own wait ordered it after the K1 that wrote the schedule,
+  // so W2 may read the schedule and issue its first weight loads (static data) before its wait --
+  // they overlap W13's last wave -- and waits only before it reads W13's act rows.
+  const bool early = a.x_per_group != 0;
+  if (!early) pdl_enter();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int g = blockIdx.y, sp = blockIdx.z, S = gridDim.z;
   if (g >= *a.n_groups) return;
@@ -94,6 +99,7 @@ __global__ void __launch_bounds__(GV_THREADS) k_int4_gemv(GemvArgs a) {
   };
   int gq = gq0 + warp;
   load_batch(gq);
+  if (early) pdl_enter();
   const uint16_t* x = a.x + (a.x_per_group ? (int64_t)g * kdim : 0);
   for (int k = 2 * tid; k < kdim; k += 2 * GV_THREADS) {
     const uint32_t u = *reinterpret_cast<const uint32_t*>(x + k);

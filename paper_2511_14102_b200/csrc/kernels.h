@@ -78,6 +78,10 @@ struct UmmaArgs {
   uint16_t* act_out = nullptr;     // INT4 W13, split 1: fused act = bf16(silu(gate) * up) [N][rows/2]
   GMask gmask{};                   // K3: only the groups whose bit is set (when gmask.on)
   unsigned char* act_img = nullptr;  // K3 W13, split 1: fused SiLU*up straight into W2's B images
+  // K3: the schedule and the A (weight) bytes were complete before the PREDECESSOR kernel's
+  // griddepcontrol.wait returned, so the producer may read the schedule and stream its first A
+  // tiles before its own wait (overlapping the predecessor's tail); only B waits
+  int early_a = 0;
 };
 
 

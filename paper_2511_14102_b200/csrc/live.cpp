@@ -1903,6 +1903,7 @@ static std::string generate_batch(mspq_engine* E, const int32_t* prompts, const 
     CUDA_OK(cudaStreamSynchronize(E->sc));
   }
   E->use_stream(0);
+  const auto wall_dec0 = std::chrono::steady_clock::now();
   CUDA_OK(cudaEventRecord(E->ev_t0, E->sc));
   CUDA_OK(cudaStreamWaitEvent(E->sx, E->ev_t0, 0));
   if (E->sdec) CUDA_OK(cudaStreamWaitEvent(E->sdec, E->ev_t0, 0));
@@ -1914,6 +1915,9 @@ static std::string generate_batch(mspq_engine* E, const int32_t* prompts, const 
   double g = static_cast<double>(L) * static_cast<double>(K);
   auto est = [&]() { return Est([gg = g](int k) { return static_cast<int>(std::llround(gg * static_cast<double>(k))); }); };
   std::vector<int32_t> hbuf;
+  std::vector<int> layer_groups(L, 0);
+  long launches = 0, k3_groups = 0, draft_steps = 0;
+  double k3_time = 0.0, k3_bytes = 0.0, draft_time = 0.0;
   int ci = 0;
   while (true) {
     std::vector<int> act;
@@ -2011,9 +2015,12 @@ static std::string generate_batch(mspq_engine* E, const int32_t* prompts, const 
         return std::max(1, std::min({(296 + units - 1) / units, mspq_engine::kMaxSplit, kdim / 64}));
       };
       const int sp1 = pick_split(2 * m.f, d), sp2 = pick_split(d, m.f);
+      CUDA_OK(cudaEventRecord(E->ev_k0[l], E->sc));
       CAPI_OK(mspq_moe_bf16_tc(sv.n_groups, sv.group_expert, sv.group_buf, sv.group_off, sv.entry_tok, sv.entry_group,
                                E->xn, E->pool, E->S16, d, m.f, T, K, E->G, sp1, sp2, E->tcws, E->yv[l & 1], E->sc));
       CUDA_OK(cudaEventRecord(E->ev_gemm[l], E->sc));
+      launches += (E->attn ? 4 : 0) + 7;
+      layer_groups[l] = (int)gb.size();
       for (int buf : gb) {
         E->last_cycle[buf] = cycle;
         E->last_layer[buf] = l;
@@ -2045,6 +2052,14 @@ static std::string generate_batch(mspq_engine* E, const int32_t* prompts, const 
     const int fetched = E->view.host_stat[S_FETCHED];
     double stall = 0.0;
     for (auto& [a, b2] : stall_ev) stall += elapsed_s(a, b2);
+    for (int l = 0; l < L; ++l) {  // K3 device time per layer (as generate())
+      k3_time += elapsed_s(E->ev_k0[l], E->ev_gemm[l]);
+      k3_bytes += (double)layer_groups[l] * E->S16;
+      k3_groups += layer_groups[l];
+    }
+    draft_time += elapsed_s(E->ev_c0, E->ev_dend);
+    draft_steps += (long)na * k;
+    launches += (long)na * k * E->graph_nodes + 2 + 3 + 2 * na;  // drafts, begin/embed, final norm/lm/argmax, accepts
     json rec;
     rec["cycle"] = ci;
     rec["k"] = k;
@@ -2135,7 +2150,20 @@ static std::string generate_batch(mspq_engine* E, const int32_t* prompts, const 
   rep["refetch_hbm"] = E->n_refetch;
   rep["cycles"] = cycles;
   rep["prefill"] = prefills;
-  rep["wall_s"] = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+  json ks;  // same kernel evidence as generate(); the draft span covers every stream's k graph replays
+  ks["kernel_launches"] = launches;
+  ks["k3_launches"] = (long)L * (long)cycles.size();
+  ks["k3_time_s"] = k3_time;
+  ks["k3_weight_bytes"] = k3_bytes;
+  ks["k3_groups"] = k3_groups;
+  ks["draft_steps"] = draft_steps;
+  ks["draft_time_s"] = draft_time;
+  ks["draft_step_bytes"] = (double)m.L * m.K * E->S4 + (double)m.V * m.d * 2 + (double)m.L * m.E * m.d * 2 +
+                           (double)m.L * E->wattn_layer;
+  rep["kernels"] = ks;
+  const auto wall1 = std::chrono::steady_clock::now();
+  rep["wall_s"] = std::chrono::duration<double>(wall1 - wall0).count();
+  rep["decode_wall_s"] = std::chrono::duration<double>(wall1 - wall_dec0).count();
   return rep.dump();
 }
 

@@ -127,7 +127,9 @@ MSPQ_D void tmem_ld8(uint32_t taddr, float* v) {
 
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(192, 1) k_umma_grouped(UmmaArgs a) {
-  pdl_enter();  // launched with launch_pdl (kernels.h)
+  // launched with launch_pdl (kernels.h); with a.early_a only the producer's B loads and the
+  // global writes wait for the predecessor (UmmaArgs::early_a)
+  if (!a.early_a) pdl_enter();
   const int S = a.splits, RT = a.rows / BM;
   const int unit = blockIdx.x;
   const int s = unit % S, rt = (unit / S) % RT, g = unit / (S * RT);
@@ -139,6 +141,7 @@ __global__ void __launch_bounds__(192, 1) k_umma_grouped(UmmaArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* outp = a.out + (int64_t)s * a.out_split_stride;
   if (nk == 0) {  // empty split: contribute zeros
+    if (a.early_a) pdl_enter();
     for (int i = threadIdx.x; i < m * BM; i += blockDim.x)
       outp[(int64_t)(e0 + i / BM) * a.rows + rt * BM + (i % BM)] = 0.0f;
     return;
@@ -170,12 +173,24 @@ __global__ void __launch_bounds__(192, 1) k_umma_grouped(UmmaArgs a) {
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  // with early_a every thread but the producer waits here (nothing to do before B lands anyway)
+  if (a.early_a && threadIdx.x != 0) pdl_enter();
   if (warp == 0) {
     if (lane == 0) {  // producer
       const unsigned char* wsrc = a.w_base + (int64_t)a.group_buf[g] * a.blob_bytes + a.w_off +
                                   ((int64_t)rt * kb_total + kb0) * TILE_A;
       const unsigned char* bsrc = a.bimg + ((int64_t)g * kb_total + kb0) * (BN * 128);
-      for (int i = 0; i < nk; ++i) {
+      int i0 = 0;
+      if (a.early_a) {  // the ring's first A tiles before the wait, their B tiles after it
+        i0 = min(nk, STAGES);
+        for (int i = 0; i < i0; ++i) {
+          mbar_expect_tx(&full[i], TILE_A + BN * 128);
+          bulk_g2s(sA + i * TILE_A, wsrc + (int64_t)i * TILE_A, TILE_A, &full[i]);
+        }
+        pdl_enter();
+        for (int i = 0; i < i0; ++i) bulk_g2s(sB + i * BN * 128, bsrc + (int64_t)i * BN * 128, BN * 128, &full[i]);
+      }
+      for (int i = i0; i < nk; ++i) {
         const int st = i % STAGES, r = i / STAGES;
         if (r > 0) mbar_wait(&empty[st], (r - 1) & 1);
         mbar_expect_tx(&full[st], TILE_A + BN * 128);

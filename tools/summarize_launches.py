@@ -10,6 +10,7 @@ def load(path):
     hdr, data = rows[hi], rows[hi + 1:]
     ki, mi, vi, ui = (hdr.index(x) for x in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit"))
     ii = hdr.index("ID")
+    gi = hdr.index("Grid Size") if (BY_GRID and "Grid Size" in hdr) else None
     per = collections.defaultdict(dict)
     names = {}
     for r in data:
@@ -21,7 +22,7 @@ def load(path):
                  "byte": 1, "Kbyte": 1e3, "KB": 1e3, "MB": 1e6, "GB": 1e9,
                  "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
         per[r[ii]][r[mi]] = v * scale
-        names[r[ii]] = r[ki]
+        names[r[ii]] = r[ki].split("(")[0][:70] + (" grid" + r[gi] if gi is not None else "")
     return per, names
 
 
@@ -29,7 +30,7 @@ def main(path):
     per, names = load(path)
     agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
     for i, m in per.items():
-        n = names[i].split("(")[0][:70]
+        n = names[i]
         a = agg[n]
         a[0] += 1
         a[1] += m.get("gpu__time_duration.sum", 0.0)
@@ -40,5 +41,7 @@ def main(path):
         print(f"{t:10.1f} {100 * t / tot:5.1f}% {c:6d} {t / c:9.2f} {b / c / 1e6:9.2f} {b / max(t, 1e-9) / 1e3:8.0f}  {n}")
 
 
+BY_GRID = "--grid" in sys.argv  # key on (kernel, grid size): separates prefill from decode launches
+
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main([x for x in sys.argv[1:] if not x.startswith("--")][0])
