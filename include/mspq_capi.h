@@ -170,8 +170,9 @@ int mspq_dense_bf16_tc(const int32_t* dsched, const void* x, const void* w_tiled
  * rows are written into kc/vc ([P][Hkv][Dh] bf16, this layer) and every token attends causally
  * to the cache rows before the window plus the window tokens up to itself; out [T][H Dh] bf16
  * (nullable) and/or oimg = the O projection's B image (a dense GEMM workspace, x = NULL).  Split-K
- * over the context (16 key chunks per token and KV head, merged in order); ws =
- * mspq_attention_ws_bytes(T, H, Hkv, Dh) bytes; P <= 4096.
+ * over the context (16 key chunks per token and KV head, merged in order by the last chunk's CTA);
+ * ws = mspq_attention_ws_bytes(T, H, Hkv, Dh) bytes, ZERO-FILLED before the first call (its merge
+ * counters return to zero after every call); P <= 4096, T * Hkv <= 2048.
  * Draft and target share the cache; rollback = the next window overwrites rows >= its pos0. */
 long long mspq_attention_ws_bytes(int T, int H, int Hkv, int Dh);
 int mspq_attention(const float* qkv, int splits, long long split_stride, int T, int H, int Hkv, int Dh, int P,

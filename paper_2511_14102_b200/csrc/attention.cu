@@ -37,6 +37,35 @@ MSPQ_D float warp_max(float v) {
 // AT_SPLITS partials in split order (deterministic) and writes bf16.
 MSPQ_D int attn_chunk(int n) { return (n + AT_SPLITS - 1) / AT_SPLITS; }
 
+// merge the AT_SPLITS partials of (t, g) in split order: o = sum_s e^(m_s - M) acc_s / sum_s e^(m_s - M) l_s
+// (run by the last of the (t, g) CTAs to finish; the partials are read from L2)
+MSPQ_D void attn_merge(const AttnArgs& a, int t, int g) {
+  const int G = a.H / a.Hkv, Dh = a.Dh, Nq = a.H * Dh;
+  const float* part = a.part + ((size_t)t * a.Hkv + g) * AT_SPLITS * (size_t)G * (Dh + 2);
+  const size_t ps = (size_t)G * (Dh + 2);
+  for (int o = threadIdx.x; o < G * Dh; o += AT_THREADS) {
+    const int i = o / Dh;
+    float ms[AT_SPLITS];
+#pragma unroll
+    for (int s = 0; s < AT_SPLITS; ++s) ms[s] = __ldcg(part + s * ps + i);
+    float M = -INFINITY;
+#pragma unroll
+    for (int s = 0; s < AT_SPLITS; ++s) M = fmaxf(M, ms[s]);
+    float den = 0.0f, num = 0.0f;
+#pragma unroll
+    for (int s = 0; s < AT_SPLITS; ++s) {
+      if (ms[s] == -INFINITY) continue;
+      const float w = __expf(__fsub_rn(ms[s], M));
+      den = fmaf(w, __ldcg(part + s * ps + G + i), den);
+      num = fmaf(w, __ldcg(part + s * ps + 2 * G + o), num);
+    }
+    const uint16_t ob = f2bf(__fdiv_rn(num, den));
+    const int col = g * G * Dh + o;
+    if (a.out) a.out[(int64_t)t * Nq + col] = ob;
+    if (a.oimg) *reinterpret_cast<uint16_t*>(a.oimg + (int64_t)(col >> 6) * (a.o_bn * 128) + sw128_off(t, col & 63)) = ob;
+  }
+}
+
 template <int VEC>
 __global__ void __launch_bounds__(AT_THREADS) k_attn_partial(AttnArgs a) {
   pdl_enter();  // launched with launch_pdl (kernels.h)
@@ -178,32 +207,18 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_partial(AttnArgs a) {
     part[tid] = j1 > j0 ? hmax[tid] : -INFINITY;
     part[G + tid] = j1 > j0 ? hsum[tid] : 0.0f;
   }
-}
-
-// merge the AT_SPLITS partials of (t, g) in split order: o = sum_s e^(m_s - M) acc_s / sum_s e^(m_s - M) l_s
-__global__ void __launch_bounds__(AT_THREADS) k_attn_combine(AttnArgs a) {
-  pdl_enter();
-  const int t = blockIdx.x, g = blockIdx.y;
-  const int G = a.H / a.Hkv, Dh = a.Dh, Nq = a.H * Dh;
-  const float* part = a.part + ((size_t)t * a.Hkv + g) * AT_SPLITS * (size_t)G * (Dh + 2);
-  const size_t ps = (size_t)G * (Dh + 2);
-  for (int o = threadIdx.x; o < G * Dh; o += AT_THREADS) {
-    const int i = o / Dh;
-    float M = -INFINITY;
-    for (int s = 0; s < AT_SPLITS; ++s) M = fmaxf(M, part[s * ps + i]);
-    float den = 0.0f, num = 0.0f;
-    for (int s = 0; s < AT_SPLITS; ++s) {
-      const float ms = part[s * ps + i];
-      if (ms == -INFINITY) continue;
-      const float w = __expf(__fsub_rn(ms, M));
-      den = fmaf(w, part[s * ps + G + i], den);
-      num = fmaf(w, part[s * ps + 2 * G + o], num);
-    }
-    const uint16_t ob = f2bf(__fdiv_rn(num, den));
-    const int col = g * G * Dh + o;
-    if (a.out) a.out[(int64_t)t * Nq + col] = ob;
-    if (a.oimg) *reinterpret_cast<uint16_t*>(a.oimg + (int64_t)(col >> 6) * (a.o_bn * 128) + sw128_off(t, col & 63)) = ob;
-  }
+  // the last of the AT_SPLITS CTAs of (t, g) merges (threadfence-reduction pattern); it resets
+  // the counter, so the workspace stays zeroed between launches
+  __shared__ int last;
+  __threadfence();
+  __syncthreads();
+  int* cnt = a.cnt + t * a.Hkv + g;
+  if (tid == 0) last = atomicAdd(cnt, 1) == AT_SPLITS - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  attn_merge(a, t, g);
+  if (tid == 0) *cnt = 0;
 }
 
 }  // namespace
@@ -213,12 +228,15 @@ size_t attn_smem_bytes(int T, int H, int Hkv, int Dh, int P) {
   (void)P;
   return (size_t)2 * T * Dh * 2 + (size_t)G * AT_MAXCHUNK * 4 + (size_t)AT_WARPS * G * Dh * 4;
 }
-size_t attn_part_floats(int T, int H, int Hkv, int Dh) {
-  return (size_t)T * Hkv * AT_SPLITS * (size_t)(H / Hkv) * (Dh + 2);
+size_t attn_part_floats(int T, int H, int Hkv, int Dh) {  // merge counters + partials, in 4-byte words
+  return (size_t)AT_CNT + (size_t)T * Hkv * AT_SPLITS * (size_t)(H / Hkv) * (Dh + 2);
 }
 
-cudaError_t launch_attn_window(const AttnArgs& a, cudaStream_t st) {
-  if (a.P > AT_MAXPOS) return cudaErrorInvalidValue;
+cudaError_t launch_attn_window(const AttnArgs& a0, cudaStream_t st) {
+  if (a0.P > AT_MAXPOS || a0.T * a0.Hkv > AT_CNT) return cudaErrorInvalidValue;
+  AttnArgs a = a0;
+  a.cnt = reinterpret_cast<int*>(a0.part);
+  a.part = a0.part + AT_CNT;
   const size_t smem = attn_smem_bytes(a.T, a.H, a.Hkv, a.Dh, a.P);
   const dim3 grid(a.T, a.Hkv, AT_SPLITS);
   cudaError_t e;
@@ -231,8 +249,7 @@ cudaError_t launch_attn_window(const AttnArgs& a, cudaStream_t st) {
   } else {
     return cudaErrorInvalidValue;
   }
-  if (e != cudaSuccess) return e;
-  return launch_pdl(k_attn_combine, dim3(a.T, a.Hkv), dim3(AT_THREADS), 0, st, a);
+  return e;
 }
 
 }  // namespace mspq

@@ -189,17 +189,20 @@ long long mspq_attention_ws_bytes(int T, int H, int Hkv, int Dh) {
 int mspq_attention_batched(const float* qkv, int splits, long long split_stride, int T, int H, int Hkv, int Dh, int P,
                            const int32_t* meta, long long kv_stream_stride, void* kc, void* vc, void* out, void* oimg,
                            void* ws, void* stream) {
-  if (H < 1 || Hkv < 1 || H % Hkv || H / Hkv > 8 || (Dh != 64 && Dh != 128) || T < 1 || P > 4096 || !ws || !meta)
-    return set_error(MSPQ_ERR_SHAPE_MISMATCH, "attention_batched: Hkv | H, H/Hkv <= 8, Dh in {64, 128}, P <= 4096");
+  if (H < 1 || Hkv < 1 || H % Hkv || H / Hkv > 8 || (Dh != 64 && Dh != 128) || T < 1 || P > 4096 || !ws || !meta ||
+      T * Hkv > AT_CNT)
+    return set_error(MSPQ_ERR_SHAPE_MISMATCH,
+                     "attention_batched: Hkv | H, H/Hkv <= 8, Dh in {64, 128}, P <= 4096, T * Hkv <= 2048");
   AttnArgs a{qkv, splits, split_stride, T, H, Hkv, Dh, P, nullptr, (uint16_t*)kc, (uint16_t*)vc, (uint16_t*)out,
              1.0f / sqrtf((float)Dh), (unsigned char*)oimg, tc_bn(T), (float*)ws, meta, kv_stream_stride};
   CK(launch_attn_window(a, ST(stream)), "attention_batched");
 }
 int mspq_attention(const float* qkv, int splits, long long split_stride, int T, int H, int Hkv, int Dh, int P,
                    const int32_t* pos0, void* kc, void* vc, void* out, void* oimg, void* ws, void* stream) {
-  if (H < 1 || Hkv < 1 || H % Hkv || H / Hkv > 8 || (Dh != 64 && Dh != 128) || T < 1 || P < T || P > 4096 || !ws)
+  if (H < 1 || Hkv < 1 || H % Hkv || H / Hkv > 8 || (Dh != 64 && Dh != 128) || T < 1 || P < T || P > 4096 || !ws ||
+      T * Hkv > AT_CNT)
     return set_error(MSPQ_ERR_SHAPE_MISMATCH,
-                     "attention: Hkv | H, H/Hkv <= 8, Dh in {64, 128}, 1 <= T <= P <= 4096, workspace");
+                     "attention: Hkv | H, H/Hkv <= 8, Dh in {64, 128}, 1 <= T <= P <= 4096, T * Hkv <= 2048, workspace");
   AttnArgs a{qkv, splits, split_stride, T, H, Hkv, Dh, P, pos0, (uint16_t*)kc, (uint16_t*)vc, (uint16_t*)out,
              1.0f / sqrtf((float)Dh), (unsigned char*)oimg, tc_bn(T), (float*)ws};
   CK(launch_attn_window(a, ST(stream)), "attention");

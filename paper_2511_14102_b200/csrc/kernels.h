@@ -114,6 +114,8 @@ struct RouteArgs {
   float eps;
   unsigned char* bimg = nullptr;  // also write xn as the SW128 B image of a dense GEMM (nullable)
   int bimg_bn = 16;               // rows per B image k-block
+  int stage = 0;                  // set by launch_route: h and every y plane of the token land in smem
+                                  // by one round of bulk copies instead of one round trip per plane
 };
 
 // Shared-KV decode attention over a window of T tokens (attention.cu)
@@ -129,10 +131,14 @@ struct AttnArgs {
   float scale;             // 1/sqrt(Dh)
   unsigned char* oimg = nullptr;  // the output as the O projection's SW128 B image (nullable)
   int o_bn = 16;
-  float* part = nullptr;          // split-K partials, attn_part_floats(T, H, Hkv, Dh) floats
+  // workspace (attn_part_floats(T, H, Hkv, Dh) words, zeroed once): [AT_CNT merge counters][split-K
+  // partials]; the launcher points part / cnt into it
+  float* part = nullptr;
   const int32_t* meta = nullptr;  // batched streams: per token (window base row, stream, position)
   int64_t kv_stream_stride = 0;   // elements between two streams' caches (same layer)
+  int* cnt = nullptr;             // [T][Hkv] arrivals of the split CTAs (the last one merges, resets to 0)
 };
+constexpr int AT_CNT = 2048;  // merge counters at the head of the attention workspace: T * Hkv <= AT_CNT
 size_t attn_smem_bytes(int T, int H, int Hkv, int Dh, int P);
 size_t attn_part_floats(int T, int H, int Hkv, int Dh);
 cudaError_t launch_attn_window(const AttnArgs& a, cudaStream_t st);

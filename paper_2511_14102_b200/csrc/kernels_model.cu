@@ -103,15 +103,44 @@ __global__ void k_embed(const uint16_t* __restrict__ embed, const uint16_t* __re
 
 
 __global__ void __launch_bounds__(256) k_resid_norm_route(RouteArgs a) {
-  pdl_enter();  // launched with launch_pdl (kernels.h)
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint16_t* xs = reinterpret_cast<uint16_t*>(smem_raw);                  // d bf16
-  float* lg = reinterpret_cast<float*>(smem_raw + a.d * 2);              // E floats
+  const int nj = a.y ? (a.entry_of ? a.K : 1) : 0;
+  // smem: [stage rows: h, then y(j, sp) for j < nj, sp < y_splits][d] fp32 | xs d bf16 | lg E fp32
+  const int64_t n_stage = a.stage ? (int64_t)(1 + nj * a.y_splits) * a.d : 0;
+  float* ys = reinterpret_cast<float*>(smem_raw);
+  uint16_t* xs = reinterpret_cast<uint16_t*>(smem_raw + n_stage * 4);    // d bf16
+  float* lg = reinterpret_cast<float*>(smem_raw + n_stage * 4 + a.d * 2);  // E floats
   __shared__ float part[8];
   __shared__ float rscale;
+  __shared__ __align__(8) uint64_t stage_bar;
   const int t = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // the router rows and gamma are static: start pulling them into L2 under the predecessor's tail
+  if (t == 0 && tid == 0) {
+    if (a.router)
+      for (int64_t o = 0, nb = (int64_t)a.E * a.d * 2; o < nb; o += 65536)
+        bulk_prefetch_l2(reinterpret_cast<const unsigned char*>(a.router) + o, (uint32_t)(nb - o < 65536 ? nb - o : 65536));
+    bulk_prefetch_l2(a.gamma, (uint32_t)a.d * 2);
+  }
+  pdl_enter();  // launched with launch_pdl (kernels.h)
   float* h = a.h + (int64_t)t * a.d;
   const int nch = a.d >> 2;
+  if (a.stage) {  // one round of bulk copies: h row + every (entry, split) plane row of this token
+    if (tid == 0) {
+      mbar_init(&stage_bar, 1);
+      fence_barrier_init();
+      const uint32_t rb = (uint32_t)a.d * 4;
+      mbar_expect_tx(&stage_bar, (uint32_t)n_stage * 4);
+      bulk_g2s(ys, h, rb, &stage_bar);
+      for (int j = 0; j < nj; ++j) {
+        const float* yb = a.y + (int64_t)(a.entry_of ? a.entry_of[t * a.K + j] : t) * a.d;
+        for (int sp = 0; sp < a.y_splits; ++sp)
+          bulk_g2s(ys + (int64_t)(1 + j * a.y_splits + sp) * a.d, yb + sp * a.y_split_stride, rb, &stage_bar);
+      }
+    }
+    __syncthreads();
+    mbar_wait(&stage_bar, 0);
+  }
+  const float* hsrc = a.stage ? ys : h;
   // Latency-bound single CTA per token: every thread owns <= 8 float4 chunks (c = tid + 256 i,
   // d <= 8192); all loads of a phase are issued before use.  Summation orders are unchanged
   // (k-slot order for the combine, chunk order for the sum of squares).
@@ -119,7 +148,7 @@ __global__ void __launch_bounds__(256) k_resid_norm_route(RouteArgs a) {
   float4 hv[MAXC];
 #pragma unroll
   for (int i = 0; i < MAXC; ++i)
-    if (tid + 256 * i < nch) hv[i] = reinterpret_cast<float4*>(h)[tid + 256 * i];
+    if (tid + 256 * i < nch) hv[i] = reinterpret_cast<const float4*>(hsrc)[tid + 256 * i];
   if (a.y) {
     float4 cb[MAXC];
 #pragma unroll
@@ -129,7 +158,9 @@ __global__ void __launch_bounds__(256) k_resid_norm_route(RouteArgs a) {
     const int nj = a.entry_of ? a.K : 1;
     for (int j = 0; j < nj; ++j) {
       const float w = a.entry_of ? a.prev_wts[t * a.K + j] : 1.0f;
-      const float* yb = a.y + (int64_t)(a.entry_of ? a.entry_of[t * a.K + j] : t) * a.d;
+      const float* yb = a.stage ? ys + (int64_t)(1 + j * a.y_splits) * a.d
+                                : a.y + (int64_t)(a.entry_of ? a.entry_of[t * a.K + j] : t) * a.d;
+      const int64_t pst = a.stage ? a.d : a.y_split_stride;
       float4 yv[MAXC];
 #pragma unroll
       for (int i = 0; i < MAXC; ++i)
@@ -138,7 +169,7 @@ __global__ void __launch_bounds__(256) k_resid_norm_route(RouteArgs a) {
 #pragma unroll
         for (int i = 0; i < MAXC; ++i)
           if (tid + 256 * i < nch) {
-            const float4 p = reinterpret_cast<const float4*>(yb + sp * a.y_split_stride)[tid + 256 * i];
+            const float4 p = reinterpret_cast<const float4*>(yb + sp * pst)[tid + 256 * i];
             yv[i] = make_float4(__fadd_rn(yv[i].x, p.x), __fadd_rn(yv[i].y, p.y), __fadd_rn(yv[i].z, p.z),
                                 __fadd_rn(yv[i].w, p.w));
           }
@@ -514,10 +545,18 @@ cudaError_t launch_embed(const uint16_t* embed, const uint16_t* pos, const int32
   return cudaGetLastError();
 }
 
-cudaError_t launch_route(const RouteArgs& a, int T, cudaStream_t st) {
+cudaError_t launch_route(const RouteArgs& a0, int T, cudaStream_t st) {
+  RouteArgs a = a0;
   size_t smem = (size_t)a.d * 2 + (size_t)a.E * 4;
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_resid_norm_route, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int nj = a.y ? (a.entry_of ? a.K : 1) : 0;
+  const size_t stage_bytes = (size_t)(1 + nj * a.y_splits) * a.d * 4;
+  // stage when there is something to combine and it fits next to xs / lg (16-byte aligned rows)
+  a.stage = (nj > 0 && stage_bytes + smem <= 200 * 1024 && a.d % 4 == 0 && a.y_split_stride % 4 == 0) ? 1 : 0;
+  if (a.stage) smem += stage_bytes;
+  if (smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(k_resid_norm_route, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
   return launch_pdl(k_resid_norm_route, dim3(T), dim3(256), smem, st, a);
 }
 

@@ -510,6 +510,7 @@ void make_workspaces(mspq_engine* E) {
     CUDA_OK(cudaMalloc(&E->ao, (size_t)T * E->Nq * 2));
     CUDA_OK(cudaMalloc(&E->dws, (size_t)mspq_dense_ws_bytes(std::max(d, E->Nq), T)));
     CUDA_OK(cudaMalloc(&E->attn_part, (size_t)mspq_attention_ws_bytes(T, m.H, m.Hkv, m.Dh)));
+    CUDA_OK(cudaMemset(E->attn_part, 0, (size_t)mspq_attention_ws_bytes(T, m.H, m.Hkv, m.Dh)));  // merge counters
     std::vector<int32_t> ds((size_t)(T + 1) * (4 + T), 0);
     for (int t = 1; t <= T; ++t) mspq_dense_sched_fill(ds.data() + (size_t)t * (4 + T), t);
     CUDA_OK(cudaMalloc(&E->dsched, ds.size() * 4));

@@ -21,25 +21,6 @@ namespace {
 
 constexpr int BM = 128, BK = 64, TILE_A = BM * BK * 2;
 
-MSPQ_D uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-MSPQ_D void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(bar)), "r"(count) : "memory");
-}
-MSPQ_D void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
-}
-MSPQ_D bool mbar_try(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(su32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
 // try_wait with a suspend-time hint: the waiting warp sleeps until the phase completes (or
 // ~1 ms passes) instead of spinning and stealing issue slots from the working warps
 MSPQ_D bool mbar_try_sleep(uint64_t* bar, uint32_t parity) {
@@ -59,20 +40,6 @@ MSPQ_D void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_sleep(bar, parity))
     if (clock64() - t0 > 4000000000LL) __trap();
 }
-// bounded wait: a lost arrival traps (error) instead of hanging the GPU
-MSPQ_D void mbar_wait(uint64_t* bar, uint32_t parity) {
-  if (mbar_try(bar, parity)) return;
-  const long long t0 = clock64();
-  while (!mbar_try(bar, parity))
-    if (clock64() - t0 > 4000000000LL) __trap();
-}
-MSPQ_D void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   su32(dst)),
-               "l"(src), "r"(bytes), "r"(su32(bar))
-               : "memory");
-}
-MSPQ_D void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 MSPQ_D void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 MSPQ_D void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
