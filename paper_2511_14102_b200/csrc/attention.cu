@@ -22,6 +22,7 @@ namespace {
 
 constexpr int AT_THREADS = 256, AT_WARPS = AT_THREADS / 32, AT_MAXG = 8;
 constexpr int AT_SPLITS = 16, AT_MAXPOS = 4096, AT_MAXCHUNK = AT_MAXPOS / AT_SPLITS;
+constexpr int AT_MAXSPLIT = 8;  // QKV projection K-split planes (the engine's kMaxSplit)
 
 MSPQ_D float warp_max(float v) {
 #pragma unroll
@@ -67,7 +68,7 @@ MSPQ_D void attn_merge(const AttnArgs& a, int t, int g) {
 }
 
 template <int VEC>
-__global__ void __launch_bounds__(AT_THREADS) k_attn_partial(AttnArgs a) {
+__global__ void __launch_bounds__(AT_THREADS, 2) k_attn_partial(AttnArgs a) {
   pdl_enter();  // launched with launch_pdl (kernels.h)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int t = blockIdx.x, g = blockIdx.y, sp = blockIdx.z;
@@ -100,26 +101,59 @@ __global__ void __launch_bounds__(AT_THREADS) k_attn_partial(AttnArgs a) {
   for (int i = tid; i < (w1 - w0) * Dh; i += AT_THREADS) {
     const int tt = w0 + i / Dh, dd = i % Dh;
     const float* src = a.qkv + (int64_t)(wb + tt) * Nqkv + Nq + g * Dh + dd;
-    float kv = 0.0f, vv = 0.0f;
-    for (int s = 0; s < a.splits; ++s) {
-      kv = __fadd_rn(kv, src[s * a.split_stride]);
-      vv = __fadd_rn(vv, src[s * a.split_stride + Nkv]);
+    // every split's K and V value in flight at once, then summed in split order
+    float kr[AT_MAXSPLIT], vr[AT_MAXSPLIT];
+#pragma unroll
+    for (int s = 0; s < AT_MAXSPLIT; ++s) {
+      kr[s] = s < a.splits ? src[s * a.split_stride] : 0.0f;
+      vr[s] = s < a.splits ? src[s * a.split_stride + Nkv] : 0.0f;
     }
+    float kv = 0.0f, vv = 0.0f;
+#pragma unroll
+    for (int s = 0; s < AT_MAXSPLIT; ++s)
+      if (s < a.splits) {
+        kv = __fadd_rn(kv, kr[s]);
+        vv = __fadd_rn(vv, vr[s]);
+      }
     wk[tt * Dh + dd] = f2bf(kv);
     wv[tt * Dh + dd] = f2bf(vv);
   }
+  // q: the lane's VEC dims of the G heads, split planes summed in order; two splits' vector loads
+  // (2 G of them) in flight per step
   float q[AT_MAXG][VEC];
 #pragma unroll
   for (int i = 0; i < AT_MAXG; ++i)
 #pragma unroll
-    for (int v = 0; v < VEC; ++v) {
-      float x = 0.0f;
-      if (i < G) {
-        const float* src = a.qkv + (int64_t)t * Nqkv + (g * G + i) * Dh + lane * VEC + v;
-        for (int s = 0; s < a.splits; ++s) x = __fadd_rn(x, src[s * a.split_stride]);
+    for (int v = 0; v < VEC; ++v) q[i][v] = 0.0f;
+  const float* qsrc = a.qkv + (int64_t)t * Nqkv + (g * G) * Dh + lane * VEC;
+  for (int s0 = 0; s0 < a.splits; s0 += 2) {
+    float qr[2][AT_MAXG][VEC];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int i = 0; i < AT_MAXG; ++i) {
+        const bool ok = i < G && s0 + u < a.splits;
+        const float* src = qsrc + (int64_t)(s0 + u) * a.split_stride + i * Dh;
+        if (VEC == 4) {
+          const float4 f = ok ? *reinterpret_cast<const float4*>(src) : make_float4(0.f, 0.f, 0.f, 0.f);
+          qr[u][i][0] = f.x;
+          qr[u][i][1] = f.y;
+          qr[u][i][2 % VEC] = f.z;
+          qr[u][i][3 % VEC] = f.w;
+        } else {
+          const float2 f = ok ? *reinterpret_cast<const float2*>(src) : make_float2(0.f, 0.f);
+          qr[u][i][0] = f.x;
+          qr[u][i][1] = f.y;
+        }
       }
-      q[i][v] = x;
-    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+      if (s0 + u < a.splits)
+#pragma unroll
+        for (int i = 0; i < AT_MAXG; ++i)
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) q[i][v] = __fadd_rn(q[i][v], qr[u][i][v]);
+  }
   __syncthreads();
   if (j0 <= pt && pt < j1)  // the chunk holding the token's own position writes its cache row
     for (int dd = tid; dd < Dh; dd += AT_THREADS) {
@@ -233,7 +267,8 @@ size_t attn_part_floats(int T, int H, int Hkv, int Dh) {  // merge counters + pa
 }
 
 cudaError_t launch_attn_window(const AttnArgs& a0, cudaStream_t st) {
-  if (a0.P > AT_MAXPOS || a0.T * a0.Hkv > AT_CNT) return cudaErrorInvalidValue;
+  if (a0.P > AT_MAXPOS || a0.T * a0.Hkv > AT_CNT || a0.splits < 1 || a0.splits > AT_MAXSPLIT)
+    return cudaErrorInvalidValue;
   AttnArgs a = a0;
   a.cnt = reinterpret_cast<int*>(a0.part);
   a.part = a0.part + AT_CNT;

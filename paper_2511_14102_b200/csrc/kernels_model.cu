@@ -412,28 +412,35 @@ __global__ void __launch_bounds__(256) k_lm_head(const uint16_t* __restrict__ xn
     for (int r = 0; r < RPW; ++r)
 #pragma unroll
       for (int t = 0; t < 4; ++t) acc[r][t] = 0.0f;
-    for (int c = lane; c < nch; c += 32) {
-      float wf[RPW][8];
+    // LU column chunks' weight loads in flight per warp before any is used (the chunk order of
+    // the accumulation is unchanged)
+    constexpr int LU = 4;
+    for (int c0 = lane; c0 < nch; c0 += 32 * LU) {
+      uint4 wr[LU][RPW];
 #pragma unroll
-      for (int r = 0; r < RPW; ++r) {
-        if (v0 + r < V) {
-          uint4 wv = ldg_nc_v4(lm + (int64_t)(v0 + r) * d + 8 * c);
-          bf16x8_to_f32(wv, wf[r]);
-        } else {
+      for (int u = 0; u < LU; ++u)
 #pragma unroll
-          for (int e = 0; e < 8; ++e) wf[r][e] = 0.0f;
-        }
-      }
+        for (int r = 0; r < RPW; ++r)
+          wr[u][r] = (c0 + 32 * u < nch && v0 + r < V) ? ldg_nc_v4(lm + (int64_t)(v0 + r) * d + 8 * (c0 + 32 * u))
+                                                       : make_uint4(0, 0, 0, 0);
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        if (t0 + t < T) {
-          uint4 xv = *reinterpret_cast<const uint4*>(xn + (int64_t)(t0 + t) * d + 8 * c);
-          float xf[8];
-          bf16x8_to_f32(xv, xf);
+      for (int u = 0; u < LU; ++u) {
+        const int c = c0 + 32 * u;
+        if (c >= nch) break;
+        float wf[RPW][8];
 #pragma unroll
-          for (int r = 0; r < RPW; ++r)
+        for (int r = 0; r < RPW; ++r) bf16x8_to_f32(wr[u][r], wf[r]);
 #pragma unroll
-            for (int e = 0; e < 8; ++e) acc[r][t] = fmaf(xf[e], wf[r][e], acc[r][t]);
+        for (int t = 0; t < 4; ++t) {
+          if (t0 + t < T) {
+            uint4 xv = *reinterpret_cast<const uint4*>(xn + (int64_t)(t0 + t) * d + 8 * c);
+            float xf[8];
+            bf16x8_to_f32(xv, xf);
+#pragma unroll
+            for (int r = 0; r < RPW; ++r)
+#pragma unroll
+              for (int e = 0; e < 8; ++e) acc[r][t] = fmaf(xf[e], wf[r][e], acc[r][t]);
+          }
         }
       }
     }

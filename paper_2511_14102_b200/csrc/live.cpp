@@ -105,7 +105,9 @@ struct mspq_engine {
   // copies, so it covers the layer boundary (GEMM, K1, controller) when the link would otherwise
   // idle.  FIFO order on the stream keeps it ahead of any later demand write to the same slot.
   bool pf_defer = false;
-  static constexpr int dec_ctas = 256;  // decode grid per chunk (128 measured the same, profiles/r01)
+  // decode grid per chunk: <= one CTA per SM, so a decode never holds a whole SM register file
+  // and the verify GEMM (higher stream priority) co-resides on every SM (256: K3 0.66 of HBM at cap 4)
+  static constexpr int dec_ctas = 128;
   std::vector<std::pair<int, int>> deferred;  // (key, buf), plan order
   int n_payload = 0;
   bool host_is_shm = false;
