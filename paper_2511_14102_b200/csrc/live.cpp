@@ -540,9 +540,23 @@ int split_for(int units_per_split1, int kblocks) {
 }
 
 // K splits for a dense projection: >= ~2 CTAs per SM of tcgen05 units
+// K split of a dense projection: the fewest k-blocks on the busiest SM, counting at least 2 CTAs
+// per SM (one CTA's 3-stage ring alone does not cover the HBM latency); ties -> fewer planes.
+// Phi QKV (48 row tiles x 64 k-blocks): 6 splits = 288 CTAs, <= 2 per SM (7 put 3 on 40 SMs).
 int dense_split(int rows, int kdim) {
-  const int units = std::max(1, rows / 128);
-  return std::max(1, std::min({(296 + units - 1) / units, mspq_engine::kMaxSplit, kdim / 64}));
+  const int rt = std::max(1, rows / 128), kb = std::max(1, kdim / 64);
+  int best = 1;
+  long best_cost = -1;
+  for (int sp = 1; sp <= std::min(mspq_engine::kMaxSplit, kb); ++sp) {
+    const int per = (kb + sp - 1) / sp, eff = (kb + per - 1) / per;  // non-empty splits
+    const long per_sm = std::max(2L, ((long)rt * eff + 147) / 148);
+    const long cost = per_sm * per;
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best = eff;
+    }
+  }
+  return best;
 }
 
 // Attention block of layer l for the T tokens in E->h (positions *pos0 ..): K1 (the previous

@@ -1078,14 +1078,16 @@ static cudaError_t launch_grouped_v(const UmmaArgs& a, int units, cudaStream_t s
   return launch_pdl(k_umma_grouped<BN, STAGES>, dim3(units), dim3(192), smem, st, a);
 }
 
-// 4 stages (75 KB smem) fit 3 CTAs per SM, so a verify layer's W13 (<= 4 experts x 100 row tiles
-// at k = 1) runs in one wave of 444 instead of spilling past 296; per-SM bytes in flight are the
-// same as 2 CTAs x 6 stages.  Per-layer verify FFN 118.3 -> 113.1 us at cap 4 (Phi).
+// 3 stages (57 KB smem at BN = 16, 63 KB at BN = 32) fit 3 CTAs per SM with room left for an XC
+// decode CTA (25 KB) on the same SM, so a verify layer's W13 (<= 4 experts x 100 row tiles at
+// k = 1) stays one wave of 444 while the codec runs beside it (with 4 stages a resident decode CTA
+// cut the SM to 2 GEMM CTAs: K3 0.66 of HBM in the cap-4 bench); 3 x 3 x 16 KB in flight per SM
+// is still ~2x what the HBM latency needs.
 cudaError_t launch_umma_grouped(const UmmaArgs& a, int max_groups, int BN, cudaStream_t st) {
   const int units = max_groups * (a.rows / BM) * a.splits;
   if (units == 0) return cudaSuccess;
-  if (BN == 16) return launch_grouped_v<16, 4>(a, units, st);
-  return launch_grouped_v<32, 4>(a, units, st);
+  if (BN == 16) return launch_grouped_v<16, 3>(a, units, st);
+  return launch_grouped_v<32, 3>(a, units, st);
 }
 
 cudaError_t launch_umma_int4(const UmmaArgs& a, int max_groups, int BN, cudaStream_t st) {
