@@ -231,6 +231,9 @@ MSPQ_D void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) 
                : "memory");
 }
 MSPQ_D void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+MSPQ_D void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(bar)) : "memory");
+}
 // fire-and-forget L2 prefetch of [src, src + bytes) (bytes a multiple of 16)
 MSPQ_D void bulk_prefetch_l2(const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");

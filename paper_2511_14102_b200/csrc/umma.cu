@@ -333,9 +333,6 @@ __global__ void k_tile_bf16(const uint16_t* __restrict__ src, int rows, int cols
 // the k-block's columns 4W @0, 4W+1 @16, 4W+2 @8, 4W+3 @24, 32+4W @4, 33+4W @20, 34+4W @12,
 // 35+4W @28 (bit offsets).  Scales [rows/128][cols/128][128] bf16.
 MSPQ_D void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-MSPQ_D void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(bar)) : "memory");
-}
 // non-blocking probe of a phase
 MSPQ_D bool mbar_test(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
