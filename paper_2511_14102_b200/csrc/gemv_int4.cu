@@ -182,186 +182,6 @@ __global__ void __launch_bounds__(GV_THREADS) k_int4_gemv(GemvArgs a) {
   }
 }
 
-// Persistent ring variant (default): one CTA per SM walks the same (row block, group, K split)
-// units as k_int4_gemv, but a producer warp streams the weights into a shared-memory ring with
-// 1-D bulk copies (cp.async.bulk; a row tile's scale groups are contiguous in the fragment-major
-// layout, so a stage = 8 scale groups x TILES row tiles = TILES copies of 8 KB) and runs up to
-// RS stages ahead, across unit boundaries.  The 8 compute warps take stage group w each -- the
-// same groups, in the same order, with the same arithmetic as k_int4_gemv -- so the results are
-// bit-identical; what changes is that the weight bytes of the next units are in flight while a
-// unit computes, and there is no per-unit launch / ramp / wave tail.
-constexpr int GR_TILES = 4, GR_STAGES = 4, GR_STAGE_BYTES = GR_TILES * 8 * 2 * 512;  // 32 KB
-constexpr int GR_THREADS = 32 * (GV_WARPS + 1);
-struct GrUnit {
-  int g, sp, rt0, gq0, gq1;
-};
-MSPQ_D GrUnit gr_unit(const GemvArgs& a, int u, int RB, int S) {
-  const int ngr = a.kdim / 128;
-  GrUnit r;
-  const int rb = u % RB, rest = u / RB;
-  r.sp = rest % S;
-  r.g = rest / S;
-  r.rt0 = rb * GR_TILES;
-  r.gq0 = r.sp * ngr / S;
-  r.gq1 = (r.sp + 1) * ngr / S;
-  return r;
-}
-
-__global__ void __launch_bounds__(GR_THREADS, 1) k_int4_gemv_ring(GemvArgs a, int S, int G) {
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  constexpr int ROWS = 16 * GR_TILES;
-  unsigned char* ring = smem_raw;                                          // [RS][32 KB]
-  uint16_t* xh = reinterpret_cast<uint16_t*>(smem_raw + GR_STAGES * GR_STAGE_BYTES);  // [kdim]
-  float* red = reinterpret_cast<float*>(xh + a.kdim);                    // [8][ROWS]
-  uint64_t* full = reinterpret_cast<uint64_t*>(red + GV_WARPS * ROWS);   // [RS]
-  uint64_t* empty = full + GR_STAGES;                                    // [RS]
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int RB = a.rows / ROWS, nchunk = a.kdim / 64, ngr = a.kdim / 128;
-  const int n_units = G * S * RB;  // G = max groups
-  const bool early = a.x_per_group != 0;   // W2: see k_int4_gemv
-  if (tid == 0) {
-    for (int i = 0; i < GR_STAGES; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], GV_WARPS);
-    }
-    fence_barrier_init();
-  }
-  __syncthreads();
-  if (warp == GV_WARPS) {  // producer warp
-    if (!early) pdl_enter();
-    if (lane == 0) {
-      const int ng = *a.n_groups;
-      int it = 0;
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-        const GrUnit w = gr_unit(a, u, RB, S);
-        if (w.g >= ng) continue;
-        const unsigned char* q = a.blobs + ((int64_t)a.layer * a.E + a.group_expert[w.g]) * a.blob_bytes + a.q_off;
-        for (int gs = w.gq0; gs < w.gq1; gs += GV_WARPS, ++it) {
-          const int slot = it % GR_STAGES, r = it / GR_STAGES;
-          if (r > 0) mbar_wait(&empty[slot], (r - 1) & 1);
-          const int nst = min(GV_WARPS, w.gq1 - gs);
-          const uint32_t tb = (uint32_t)nst * 2 * 512;  // one tile's chunks of this stage
-          mbar_expect_tx(&full[slot], tb * GR_TILES);
-          for (int i = 0; i < GR_TILES; ++i)
-            bulk_g2s(ring + slot * GR_STAGE_BYTES + i * (GR_STAGE_BYTES / GR_TILES),
-                     q + ((int64_t)(w.rt0 + i) * nchunk + 2 * gs) * 512, tb, &full[slot]);
-        }
-      }
-    }
-    return;
-  }
-  // compute warps
-  pdl_enter();
-  const int ng = *a.n_groups;
-  const int gi = lane >> 2, ti = lane & 3;
-  int it = 0, xg = -1;
-  for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-    const GrUnit w = gr_unit(a, u, RB, S);
-    if (w.g >= ng) continue;
-    const int xrow = a.x_per_group ? w.g : 0;
-    if (xrow != xg) {  // (re)build the class-scaled fp16 x for this unit's group
-      asm volatile("bar.sync 1, %0;" ::"r"(GV_WARPS * 32));  // every warp is done with the old x
-      const uint16_t* x = a.x + (int64_t)xrow * a.kdim;
-      for (int k = 2 * tid; k < a.kdim; k += 2 * GV_WARPS * 32) {
-        const uint32_t uu = *reinterpret_cast<const uint32_t*>(x + k);
-        const float m = (k & 15) >= 8 ? 0.0625f : 1.0f;
-        const __half2 h2 = __floats2half2_rn(__uint_as_float(uu << 16) * m, __uint_as_float(uu & 0xffff0000u) * m);
-        *reinterpret_cast<__half2*>(&xh[k]) = h2;
-      }
-      asm volatile("bar.sync 1, %0;" ::"r"(GV_WARPS * 32));
-      xg = xrow;
-    }
-    const uint16_t* sc = reinterpret_cast<const uint16_t*>(
-        a.blobs + ((int64_t)a.layer * a.E + a.group_expert[w.g]) * a.blob_bytes + a.s_off);
-    float acc[GR_TILES][2];
-#pragma unroll
-    for (int i = 0; i < GR_TILES; ++i) acc[i][0] = acc[i][1] = 0.0f;
-    for (int gs = w.gq0; gs < w.gq1; gs += GV_WARPS, ++it) {
-      const int slot = it % GR_STAGES, r = it / GR_STAGES;
-      const int gb = gs + warp;
-      const bool mine = gb < w.gq1;
-      float s0v[GR_TILES], s1v[GR_TILES];
-      if (mine)  // scale loads ahead of the stage wait
-#pragma unroll
-        for (int i = 0; i < GR_TILES; ++i) {
-          const int r0 = 16 * (w.rt0 + i) + gi;
-          s0v[i] = bf2f(sc[(int64_t)r0 * ngr + gb]);
-          s1v[i] = bf2f(sc[(int64_t)(r0 + 8) * ngr + gb]);
-        }
-      mbar_wait(&full[slot], r & 1);
-      if (mine) {
-        const unsigned char* st = ring + slot * GR_STAGE_BYTES;
-        uint4 buf[GR_TILES][2];
-#pragma unroll
-        for (int i = 0; i < GR_TILES; ++i)
-#pragma unroll
-          for (int c = 0; c < 2; ++c)
-            buf[i][c] = *reinterpret_cast<const uint4*>(st + i * (GR_STAGE_BYTES / GR_TILES) + ((2 * warp + c) * 32 + lane) * 16);
-        float d[GR_TILES][4];
-#pragma unroll
-        for (int i = 0; i < GR_TILES; ++i) d[i][0] = d[i][1] = d[i][2] = d[i][3] = 0.0f;
-        float c1 = 0.0f, c16 = 0.0f;
-#pragma unroll
-        for (int c = 0; c < 2; ++c)
-#pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            const int kb = 8 * gb + 4 * c + v;
-            const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&xh[16 * kb + 2 * ti]);
-            const uint32_t b1 = *reinterpret_cast<const uint32_t*>(&xh[16 * kb + 8 + 2 * ti]);
-            const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&b0));
-            const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&b1));
-            c1 = __fadd_rn(__fadd_rn(c1, f0.x), f0.y);
-            c16 = __fadd_rn(__fadd_rn(c16, f1.x), f1.y);
-#pragma unroll
-            for (int i = 0; i < GR_TILES; ++i) {
-              const uint4 wv = buf[i][c];
-              const uint32_t ww = v == 0 ? wv.x : v == 1 ? wv.y : v == 2 ? wv.z : wv.w;
-              const uint32_t w8 = ww >> 8;
-              uint32_t af[4];
-              af[0] = lop_magic(ww, 0x000F000Fu);
-              af[1] = lop_magic(w8, 0x000F000Fu);
-              af[2] = lop_magic(ww, 0x00F000F0u);
-              af[3] = lop_magic(w8, 0x00F000F0u);
-              mma16816(d[i], af, b0, b1);
-            }
-          }
-        float cl = fmaf(1152.0f, c16, __fmul_rn(1032.0f, c1));
-        cl = __fadd_rn(cl, __shfl_xor_sync(0xffffffffu, cl, 1));
-        cl = __fadd_rn(cl, __shfl_xor_sync(0xffffffffu, cl, 2));
-#pragma unroll
-        for (int i = 0; i < GR_TILES; ++i) {
-          acc[i][0] = fmaf(s0v[i], __fsub_rn(d[i][0], cl), acc[i][0]);
-          acc[i][1] = fmaf(s1v[i], __fsub_rn(d[i][2], cl), acc[i][1]);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);
-    }
-    // unit epilogue: warp partials reduced in warp order (k_int4_gemv's)
-    if (ti == 0) {
-#pragma unroll
-      for (int i = 0; i < GR_TILES; ++i) {
-        red[warp * ROWS + 16 * i + gi] = acc[i][0];
-        red[warp * ROWS + 16 * i + gi + 8] = acc[i][1];
-      }
-    }
-    asm volatile("bar.sync 1, %0;" ::"r"(GV_WARPS * 32));
-    if (tid < ROWS) {
-      float v = 0.0f;
-#pragma unroll
-      for (int ww = 0; ww < GV_WARPS; ++ww) v = __fadd_rn(v, red[ww * ROWS + tid]);
-      const int row = ROWS * (w.rt0 / GR_TILES) + tid;
-      if (a.act) {
-        const float up = __shfl_down_sync(0xffffffffu, v, 1);
-        if ((tid & 1) == 0) a.act[(int64_t)w.g * (a.rows / 2) + row / 2] = f2bf(__fmul_rn(silu_det(v), up));
-      } else {
-        a.y[((int64_t)w.sp * G + w.g) * a.rows + row] = v;
-      }
-    }
-    asm volatile("bar.sync 1, %0;" ::"r"(GV_WARPS * 32));  // red is reused by the next unit
-  }
-}
-
 // row-major quantised INT4 (standard nibble order) -> fragment-major words (header comment)
 __global__ void k_fragtile_int4(const uint32_t* __restrict__ q, int rows, int cols, uint32_t* __restrict__ fq) {
   const int wpr = cols / 8, nchunk = cols / 64;
@@ -402,27 +222,11 @@ cudaError_t launch_int4_gemv(const GemvArgs& a, int max_groups, int ksplit, cuda
   // the three BASELINE shapes (profiles/r02/gemv_variants.txt: Phi 2.81, Qwen3 1.67, Mixtral 3.81
   // TB/s in-stream; 32 rows x 4 groups: 2.74 / 1.30 / 3.50; tcgen05 K2: 1.49 / 0.86 / 1.88)
   switch (g_gemv_variant) {
-    case 0: {
-      if (a.rows % (16 * GR_TILES) || a.kdim % 128) return cudaErrorInvalidValue;
-      const size_t smem = (size_t)GR_STAGES * GR_STAGE_BYTES + (size_t)a.kdim * 2 + GV_WARPS * 16 * GR_TILES * 4 +
-                          2 * GR_STAGES * 8;
-      cudaError_t e = cudaFuncSetAttribute(k_int4_gemv_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      static int n_sm = 0;
-      if (!n_sm) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-      }
-      const int units = max_groups * ksplit * (a.rows / (16 * GR_TILES));
-      return launch_pdl(k_int4_gemv_ring, dim3(std::min(units, n_sm)), dim3(GR_THREADS), smem, st, a, ksplit,
-                        max_groups);
-    }
     case 1: return launch_gemv_v<2, 4, true>(a, max_groups, ksplit, st);
     case 3: return launch_gemv_v<1, 4, false>(a, max_groups, ksplit, st);
     case 4: return launch_gemv_v<2, 2, false>(a, max_groups, ksplit, st);
     case 5: return launch_gemv_v<2, 4, false>(a, max_groups, ksplit, st);
-    default: return launch_gemv_v<4, 2, false>(a, max_groups, ksplit, st);  // 2: the per-unit-CTA kernel
+    default: return launch_gemv_v<4, 2, false>(a, max_groups, ksplit, st);
   }
 }
 

@@ -1072,6 +1072,8 @@ template <int BN, int STAGES>
 static cudaError_t launch_grouped_v(const UmmaArgs& a, int units, cudaStream_t st) {
   const size_t smem = 1024 + STAGES * (TILE_A + BN * 128) + (2 * STAGES + 2) * 8 + 16;
   cudaFuncSetAttribute(k_umma_grouped<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_umma_grouped<BN, STAGES>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       cudaSharedmemCarveoutMaxShared);
   return launch_pdl(k_umma_grouped<BN, STAGES>, dim3(units), dim3(192), smem, st, a);
 }
 

@@ -455,6 +455,13 @@ int mspq_xc_decode(const void* blob, int tile0, int tile1, void* dst, int n_ctas
   if (tile1 == tile0) return MSPQ_OK;
   const int need = (tile1 - tile0 + XC_WARPS - 1) / XC_WARPS;
   const int grid = std::max(1, std::min(n_ctas > 0 ? n_ctas : 32, need));
+  // decodes run beside the verify GEMM (K3, ~57 KB smem per CTA): ask for the max-shared carveout
+  // so an SM holding a decode CTA is not configured with too little shared memory to co-host K3
+  static bool carve = false;
+  if (!carve) {
+    cudaFuncSetAttribute(k_xc_decode, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    carve = true;
+  }
   k_xc_decode<<<grid, XC_WARPS * 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>((const unsigned char*)blob, tile0,
                                                                                   tile1, (uint16_t*)dst);
   return cuda_status(cudaGetLastError(), "xc_decode");
