@@ -276,10 +276,10 @@ cudaError_t launch_attn_window(const AttnArgs& a0, cudaStream_t st) {
   const dim3 grid(a.T, a.Hkv, AT_SPLITS);
   cudaError_t e;
   if (a.Dh == 128) {
-    e = cudaFuncSetAttribute(k_attn_partial<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = cudaFuncSetAttribute(k_attn_partial<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
     if (e == cudaSuccess) e = launch_pdl(k_attn_partial<4>, grid, dim3(AT_THREADS), smem, st, a);
   } else if (a.Dh == 64) {
-    e = cudaFuncSetAttribute(k_attn_partial<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = cudaFuncSetAttribute(k_attn_partial<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
     if (e == cudaSuccess) e = launch_pdl(k_attn_partial<2>, grid, dim3(AT_THREADS), smem, st, a);
   } else {
     return cudaErrorInvalidValue;

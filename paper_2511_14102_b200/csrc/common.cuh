@@ -11,6 +11,10 @@
 
 #define MSPQ_HD __host__ __device__ __forceinline__
 #define MSPQ_D __device__ __forceinline__
+// Dynamic shared-memory limit for kernels whose size varies per launch (K1 staging <= ~205 KB,
+// attention): set as a constant, so a captured graph node and a later direct launch of another size
+// never race on the function attribute; static smem + this stays under sm_100's 227 KB opt-in.
+constexpr int kMaxDynSmem = 210 * 1024;
 
 namespace mspq {
 

@@ -992,7 +992,10 @@ cudaError_t ctl_reset(const CtlDev& C, int nbuf, cudaStream_t st) {
 template <class K>
 static size_t prep(K kern, const CtlDev& C, bool elb) {
   const size_t b = ctl_stage_bytes(C, elb);
-  if (b > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b);
+  // one constant limit (the largest stage ctl_stage_bytes admits): replays of different configs run
+  // concurrently from several host threads (replay_many), and a per-launch size could be lowered by
+  // another thread between its set and this launch
+  if (b > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 211 * 1024);
   return b;
 }
 #define CTL_LAUNCH(KERN, ELB, ...)                                                          \

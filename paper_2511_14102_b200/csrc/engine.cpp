@@ -19,6 +19,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <exception>
 #include <fstream>
 #include <functional>
 #include <limits>
@@ -754,9 +755,41 @@ extern "C" int mspq_replay(int device, const char* trace_jsonl, const char* conf
   });
 }
 
+namespace mspq_host {
+// Independent replays of one trace run CONCURRENTLY: each config gets its own host thread, device
+// cache controller and stream, so the device executes the configs' launches side by side (the
+// reference's compare_policies / sweep_k loop over run_simulation serially, sim.cpp:539-574).
+// Rows come back in config order; the first failing config's error is rethrown.
+std::vector<json> replay_many(int device, const char* trace_jsonl, const std::vector<json>& cfgs) {
+  const size_t n = cfgs.size();
+  std::vector<std::string> out(n);
+  std::vector<std::exception_ptr> err(n);
+  const size_t width = std::max<size_t>(1, std::min<size_t>(n, 32));
+  for (size_t b = 0; b < n; b += width) {
+    std::vector<std::thread> th;
+    for (size_t i = b; i < std::min(n, b + width); ++i)
+      th.emplace_back([&, i] {
+        try {
+          out[i] = replay(device, trace_jsonl, cfgs[i].dump());
+        } catch (...) {
+          err[i] = std::current_exception();
+        }
+      });
+    for (auto& t : th) t.join();
+  }
+  std::vector<json> reps;
+  for (size_t i = 0; i < n; ++i) {
+    if (err[i]) std::rethrow_exception(err[i]);
+    reps.push_back(json::parse(out[i]));
+  }
+  return reps;
+}
+}  // namespace mspq_host
+
 // compare_policies / sweep_k (sim.cpp:539-574) on the device control plane: run_simulation of
 // the trace once per (policy, capacity) / per fixed k, rows as in PolicyRow / SweepRow
-// (sim.hpp:88-109).  policies_json: ["lru", ...]; capacities_json / ks_json: integer arrays.
+// (sim.hpp:88-109), the configs replayed concurrently (replay_many).  policies_json: ["lru", ...];
+// capacities_json / ks_json: integer arrays.
 extern "C" int mspq_compare_policies(int device, const char* trace_jsonl, const char* config_json,
                                      const char* policies_json, const char* capacities_json, char** rows_json) {
   using namespace mspq_host;
@@ -766,15 +799,18 @@ extern "C" int mspq_compare_policies(int device, const char* trace_jsonl, const 
     if (base.is_discarded() || !pols.is_array() || !caps.is_array())
       fail(MSPQ_ERR_INVALID_CONFIG, "compare_policies: config object, policy and capacity arrays");
     json rows = json::array();
+    std::vector<json> cfgs;
     for (const auto& pol : pols)
       for (const auto& cap : caps) {
         json cfg = base;
         cfg["policy"] = pol;
         cfg["cache_capacity"] = cap;
-        const json rep = json::parse(replay(device, trace_jsonl, cfg.dump()));
-        rows.push_back({{"policy", pol}, {"capacity", cap}, {"coverage", rep["mean_step_coverage"]},
-                        {"tpot", rep["tpot_s"]}});
+        cfgs.push_back(cfg);
       }
+    const std::vector<json> reps = replay_many(device, trace_jsonl, cfgs);
+    for (size_t i = 0; i < cfgs.size(); ++i)
+      rows.push_back({{"policy", cfgs[i]["policy"]}, {"capacity", cfgs[i]["cache_capacity"]},
+                      {"coverage", reps[i]["mean_step_coverage"]}, {"tpot", reps[i]["tpot_s"]}});
     *rows_json = dup(rows.dump());
     return MSPQ_OK;
   });
@@ -788,13 +824,16 @@ extern "C" int mspq_sweep_k(int device, const char* trace_jsonl, const char* con
     json ks = json::parse(ks_json, nullptr, false);
     if (base.is_discarded() || !ks.is_array()) fail(MSPQ_ERR_INVALID_CONFIG, "sweep_k: config object, k array");
     json rows = json::array();
+    std::vector<json> cfgs;
     for (const auto& k : ks) {
       json cfg = base;
       cfg["k"] = k;  // fixed k: the governor is off (SimConfig use_governor = false)
-      const json rep = json::parse(replay(device, trace_jsonl, cfg.dump()));
-      rows.push_back({{"k", k}, {"tpot", rep["tpot_s"]}, {"mean_accepted", rep["mean_accepted"]},
-                      {"coverage", rep["mean_step_coverage"]}, {"ttft", rep["ttft_s"]}});
+      cfgs.push_back(cfg);
     }
+    const std::vector<json> reps = replay_many(device, trace_jsonl, cfgs);
+    for (size_t i = 0; i < cfgs.size(); ++i)
+      rows.push_back({{"k", cfgs[i]["k"]}, {"tpot", reps[i]["tpot_s"]}, {"mean_accepted", reps[i]["mean_accepted"]},
+                      {"coverage", reps[i]["mean_step_coverage"]}, {"ttft", reps[i]["ttft_s"]}});
     *rows_json = dup(rows.dump());
     return MSPQ_OK;
   });

@@ -561,7 +561,10 @@ cudaError_t launch_route(const RouteArgs& a0, int T, cudaStream_t st) {
   a.stage = (nj > 0 && stage_bytes + smem <= 200 * 1024 && a.d % 4 == 0 && a.y_split_stride % 4 == 0) ? 1 : 0;
   if (a.stage) smem += stage_bytes;
   if (smem > 48 * 1024) {
-    const cudaError_t e = cudaFuncSetAttribute(k_resid_norm_route, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // one constant limit, not the per-launch size: captured draft-graph nodes (staging 144 KB at
+    // Phi) replay after verify launches of a different size
+    const cudaError_t e = cudaFuncSetAttribute(k_resid_norm_route, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               kMaxDynSmem);
     if (e != cudaSuccess) return e;
   }
   return launch_pdl(k_resid_norm_route, dim3(T), dim3(256), smem, st, a);

@@ -37,6 +37,25 @@ for name, (L, E, K), cap in [("tiny", (4, 8, 2), 4), ("mixtral", (32, 8, 2), 2),
                    speedup=t_ref / t_dev, identical=json.dumps(got, sort_keys=True) == json.dumps(want, sort_keys=True))
         rows.append(row)
         print(json.dumps(row), flush=True)
+# compare_policies (sim.cpp:539-574): the reference loops run_simulation over (policy, capacity)
+# serially; the device replays the configs concurrently (replay_many).  Rows must match exactly.
+POLS = ["lru", "lookahead", "sp-sooner", "sp-later", "speculative"]
+for name, (L, E, K), caps in [("phi", (32, 16, 2), [4, 8, 12]), ("qwen3", (48, 128, 8), [16, 32, 64])]:
+    sh = m.MODEL_SHAPES[name]
+    tr = ref.generate_trace(L, E, K, a.tokens, seed=1, expert_bytes=3 * sh["d"] * sh["f"] * 2)
+    cfg = {"k": "governor", "governor": {"k_min": 1, "k_max": 16, "k_slo": 16}}
+    t0 = time.perf_counter()
+    want = ref.compare_policies(tr, cfg, POLS, caps)  # the reference's own compare_policies (oracle/_ref)
+    t_ref = time.perf_counter() - t0
+    m.compare_policies(tr, cfg, POLS, caps)  # warm
+    t0 = time.perf_counter()
+    got = m.compare_policies(tr, cfg, POLS, caps)
+    t_dev = time.perf_counter() - t0
+    row = dict(model=name, api="compare_policies", configs=len(POLS) * len(caps), tokens=a.tokens,
+               ref_cpu_s=t_ref, device_s=t_dev, speedup=t_ref / t_dev,
+               identical=json.dumps(got, sort_keys=True) == json.dumps(want, sort_keys=True))
+    rows.append(row)
+    print(json.dumps(row), flush=True)
 os.makedirs(os.path.dirname(a.out), exist_ok=True)
 with open(a.out, "w") as f:
     for r in rows:
