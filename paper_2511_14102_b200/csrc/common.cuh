@@ -162,6 +162,28 @@ MSPQ_D void warp_dot2_bf16(const uint16_t* __restrict__ x, const uint16_t* __res
   float a0 = 0.0f, a1 = 0.0f;
   const int nchunks = n >> 3;
   int c = lane;
+  // 8 chunks of each row in flight per step (16 weight loads per lane); x comes from shared memory
+  for (; c + 224 < nchunks; c += 256) {
+    uint4 v0[8], v1[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      v0[u] = ldg_nc_v4(w0 + 8 * (c + 32 * u));
+      v1[u] = ldg_nc_v4(w1 + 8 * (c + 32 * u));
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint4 xv = *reinterpret_cast<const uint4*>(x + 8 * (c + 32 * u));
+      float xf[8], f0[8], f1[8];
+      bf16x8_to_f32(xv, xf);
+      bf16x8_to_f32(v0[u], f0);
+      bf16x8_to_f32(v1[u], f1);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        a0 = fmaf(xf[e], f0[e], a0);
+        a1 = fmaf(xf[e], f1[e], a1);
+      }
+    }
+  }
   for (; c + 96 < nchunks; c += 128) {
     uint4 v0[4], v1[4], xv[4];
 #pragma unroll

@@ -128,16 +128,22 @@ __global__ void __launch_bounds__(256) k_resid_norm_route(RouteArgs a) {
     if (tid == 0) {
       mbar_init(&stage_bar, 1);
       fence_barrier_init();
-      const uint32_t rb = (uint32_t)a.d * 4;
       mbar_expect_tx(&stage_bar, (uint32_t)n_stage * 4);
-      bulk_g2s(ys, h, rb, &stage_bar);
-      for (int j = 0; j < nj; ++j) {
-        const float* yb = a.y + (int64_t)(a.entry_of ? a.entry_of[t * a.K + j] : t) * a.d;
-        for (int sp = 0; sp < a.y_splits; ++sp)
-          bulk_g2s(ys + (int64_t)(1 + j * a.y_splits + sp) * a.d, yb + sp * a.y_split_stride, rb, &stage_bar);
-      }
     }
     __syncthreads();
+    // copy c (0 = h, 1 + j * splits + sp = plane sp of entry j) is issued by lane c / 8 of warp
+    // c % 8: the issues proceed in parallel on 8 warps instead of one thread's serial sequence
+    const int ncp = 1 + nj * a.y_splits, cp = (tid & 31) * 8 + (tid >> 5);
+    if (cp < ncp) {
+      const uint32_t rb = (uint32_t)a.d * 4;
+      if (cp == 0) {
+        bulk_g2s(ys, h, rb, &stage_bar);
+      } else {
+        const int j = (cp - 1) / a.y_splits, sp = (cp - 1) % a.y_splits;
+        const float* yb = a.y + (int64_t)(a.entry_of ? a.entry_of[t * a.K + j] : t) * a.d;
+        bulk_g2s(ys + (int64_t)cp * a.d, yb + sp * a.y_split_stride, rb, &stage_bar);
+      }
+    }
     mbar_wait(&stage_bar, 0);
   }
   const float* hsrc = a.stage ? ys : h;
