@@ -23,6 +23,7 @@ namespace {
 constexpr int AT_THREADS = 256, AT_WARPS = AT_THREADS / 32, AT_MAXG = 8;
 constexpr int AT_SPLITS = 16, AT_MAXPOS = 4096, AT_MAXCHUNK = AT_MAXPOS / AT_SPLITS;
 constexpr int AT_MAXSPLIT = 8;  // QKV projection K-split planes (the engine's kMaxSplit)
+constexpr int AT_PRE = 2;       // keys per warp whose K and V rows are loaded before the score loop (<= 2)
 
 MSPQ_D float warp_max(float v) {
 #pragma unroll
@@ -67,7 +68,7 @@ MSPQ_D void attn_merge(const AttnArgs& a, int t, int g) {
   }
 }
 
-template <int VEC>
+template <int VEC, int MG>  // MG: register arrays sized for G = H / Hkv <= MG (4 or AT_MAXG)
 __global__ void __launch_bounds__(AT_THREADS, 2) k_attn_partial(AttnArgs a) {
   pdl_enter();  // launched with launch_pdl (kernels.h)
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -120,18 +121,18 @@ __global__ void __launch_bounds__(AT_THREADS, 2) k_attn_partial(AttnArgs a) {
   }
   // q: the lane's VEC dims of the G heads, split planes summed in order; two splits' vector loads
   // (2 G of them) in flight per step
-  float q[AT_MAXG][VEC];
+  float q[MG][VEC];
 #pragma unroll
-  for (int i = 0; i < AT_MAXG; ++i)
+  for (int i = 0; i < MG; ++i)
 #pragma unroll
     for (int v = 0; v < VEC; ++v) q[i][v] = 0.0f;
   const float* qsrc = a.qkv + (int64_t)t * Nqkv + (g * G) * Dh + lane * VEC;
   for (int s0 = 0; s0 < a.splits; s0 += 2) {
-    float qr[2][AT_MAXG][VEC];
+    float qr[2][MG][VEC];
 #pragma unroll
     for (int u = 0; u < 2; ++u)
 #pragma unroll
-      for (int i = 0; i < AT_MAXG; ++i) {
+      for (int i = 0; i < MG; ++i) {
         const bool ok = i < G && s0 + u < a.splits;
         const float* src = qsrc + (int64_t)(s0 + u) * a.split_stride + i * Dh;
         if (VEC == 4) {
@@ -150,7 +151,7 @@ __global__ void __launch_bounds__(AT_THREADS, 2) k_attn_partial(AttnArgs a) {
     for (int u = 0; u < 2; ++u)
       if (s0 + u < a.splits)
 #pragma unroll
-        for (int i = 0; i < AT_MAXG; ++i)
+        for (int i = 0; i < MG; ++i)
 #pragma unroll
           for (int v = 0; v < VEC; ++v) q[i][v] = __fadd_rn(q[i][v], qr[u][i][v]);
   }
@@ -174,12 +175,28 @@ __global__ void __launch_bounds__(AT_THREADS, 2) k_attn_partial(AttnArgs a) {
       o[1] = __uint_as_float(u & 0xffff0000u);
     }
   };
-  // (2) scores of this chunk
-  for (int j = j0 + warp; j < j1; j += AT_WARPS) {
-    float kk[VEC];
-    row_vec(kc, wk, j, kk);
+  // the warp's first AT_PRE keys: K AND V rows loaded together up front (one memory round trip
+  // instead of one per key and per operand; short decode contexts have <= 2 keys per warp)
+  float kpre[AT_PRE][VEC], vpre[AT_PRE][VEC];
 #pragma unroll
-    for (int i = 0; i < AT_MAXG; ++i)
+  for (int p = 0; p < AT_PRE; ++p) {
+    const int j = j0 + warp + p * AT_WARPS;
+    if (j < j1) {
+      row_vec(kc, wk, j, kpre[p]);
+      row_vec(vc, wv, j, vpre[p]);
+    }
+  }
+  // (2) scores of this chunk
+  for (int j = j0 + warp, p = 0; j < j1; j += AT_WARPS, ++p) {
+    float kk[VEC];
+    if (p < AT_PRE) {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) kk[v] = p == 0 ? kpre[0][v] : kpre[AT_PRE - 1][v];  // static indices
+    } else {
+      row_vec(kc, wk, j, kk);
+    }
+#pragma unroll
+    for (int i = 0; i < MG; ++i)
       if (i < G) {
         float pp = 0.0f;
 #pragma unroll
@@ -209,16 +226,21 @@ __global__ void __launch_bounds__(AT_THREADS, 2) k_attn_partial(AttnArgs a) {
   }
   __syncthreads();
   // (4) unnormalised value sums, per-warp partials added in warp order
-  float acc[AT_MAXG][VEC];
+  float acc[MG][VEC];
 #pragma unroll
-  for (int i = 0; i < AT_MAXG; ++i)
+  for (int i = 0; i < MG; ++i)
 #pragma unroll
     for (int v = 0; v < VEC; ++v) acc[i][v] = 0.0f;
-  for (int j = j0 + warp; j < j1; j += AT_WARPS) {
+  for (int j = j0 + warp, p = 0; j < j1; j += AT_WARPS, ++p) {
     float vv[VEC];
-    row_vec(vc, wv, j, vv);
+    if (p < AT_PRE) {
 #pragma unroll
-    for (int i = 0; i < AT_MAXG; ++i)
+      for (int v = 0; v < VEC; ++v) vv[v] = p == 0 ? vpre[0][v] : vpre[AT_PRE - 1][v];
+    } else {
+      row_vec(vc, wv, j, vv);
+    }
+#pragma unroll
+    for (int i = 0; i < MG; ++i)
       if (i < G) {
         const float pj = sc[i * AT_MAXCHUNK + (j - j0)];
 #pragma unroll
@@ -226,7 +248,7 @@ __global__ void __launch_bounds__(AT_THREADS, 2) k_attn_partial(AttnArgs a) {
       }
   }
 #pragma unroll
-  for (int i = 0; i < AT_MAXG; ++i)
+  for (int i = 0; i < MG; ++i)
     if (i < G)
 #pragma unroll
       for (int v = 0; v < VEC; ++v) red[((size_t)warp * G + i) * Dh + lane * VEC + v] = acc[i][v];
@@ -275,15 +297,17 @@ cudaError_t launch_attn_window(const AttnArgs& a0, cudaStream_t st) {
   const size_t smem = attn_smem_bytes(a.T, a.H, a.Hkv, a.Dh, a.P);
   const dim3 grid(a.T, a.Hkv, AT_SPLITS);
   cudaError_t e;
-  if (a.Dh == 128) {
-    e = cudaFuncSetAttribute(k_attn_partial<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
-    if (e == cudaSuccess) e = launch_pdl(k_attn_partial<4>, grid, dim3(AT_THREADS), smem, st, a);
-  } else if (a.Dh == 64) {
-    e = cudaFuncSetAttribute(k_attn_partial<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
-    if (e == cudaSuccess) e = launch_pdl(k_attn_partial<2>, grid, dim3(AT_THREADS), smem, st, a);
-  } else {
+  auto go = [&](auto kern) {
+    cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+    return e2 == cudaSuccess ? launch_pdl(kern, grid, dim3(AT_THREADS), smem, st, a) : e2;
+  };
+  const bool g4 = a.H / a.Hkv <= 4;
+  if (a.Dh == 128)
+    e = g4 ? go(k_attn_partial<4, 4>) : go(k_attn_partial<4, AT_MAXG>);
+  else if (a.Dh == 64)
+    e = g4 ? go(k_attn_partial<2, 4>) : go(k_attn_partial<2, AT_MAXG>);
+  else
     return cudaErrorInvalidValue;
-  }
   return e;
 }
 
