@@ -228,9 +228,6 @@ int mspq_xc_encode(const void* tiles, long long n_tiles, void* scratch, void* ou
                    long long* out_bytes, void* stream);
 /* decode tiles [tile0, tile1) of a device blob into dst (tile t -> dst + 16 KB * t); n_ctas <= 0
  * picks the default grid (32 CTAs of 8 warps) */
-/* HBM -> HBM copy of one expert's bytes on SMs (peer-expert tier: this GPU's home region or a
- * peer's NVLink/IPC-mapped one); bytes and both pointers 16-byte aligned. */
-int mspq_copy_expert(void* dst, const void* src, long long bytes, void* stream);
 int mspq_xc_decode(const void* blob, int tile0, int tile1, void* dst, int n_ctas, void* stream);
 long long mspq_int4_blob_bytes(int d, int f);
 long long mspq_bf16_blob_bytes(int d, int f);

@@ -215,11 +215,6 @@ int mspq_fragtile_int4(const void* q, int rows, int cols, void* fq, void* stream
   if (rows % 32 || cols % 128) return set_error(MSPQ_ERR_SHAPE_MISMATCH, "fragtile_int4: rows % 32, cols % 128");
   CK(launch_fragtile_int4((const uint32_t*)q, rows, cols, (uint32_t*)fq, ST(stream)), "fragtile_int4");
 }
-int mspq_copy_expert(void* dst, const void* src, long long bytes, void* stream) {
-  if (bytes < 0 || bytes % 16 || ((uintptr_t)dst | (uintptr_t)src) % 16)
-    return set_error(MSPQ_ERR_SHAPE_MISMATCH, "copy_expert: 16-byte aligned pointers and size");
-  CK(launch_copy_expert((unsigned char*)dst, (const unsigned char*)src, bytes, ST(stream)), "copy_expert");
-}
 int mspq_moe_int4_gemv(const int32_t* n_groups, const int32_t* group_expert, const void* xn, const void* blobs,
                        long long blob_bytes, int layer, int E, int d, int f, int K, int split2, void* act, float* y,
                        void* stream) {

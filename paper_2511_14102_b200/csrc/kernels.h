@@ -173,8 +173,6 @@ cudaError_t launch_finalize_act(const float* p1, int splits, int64_t split_strid
                                 const int32_t* entry_group, int n_entries, int f, int BN, unsigned char* img,
                                 cudaStream_t st, float* csum = nullptr, GMask gm = GMask{});
 cudaError_t launch_tile_bf16(const uint16_t* src, int rows, int cols, unsigned char* dst, cudaStream_t st);
-// HBM -> HBM expert copy on SMs (peer tier: a local home or a peer's NVLink-mapped home); bytes % 16 == 0
-cudaError_t launch_copy_expert(unsigned char* dst, const unsigned char* src, int64_t bytes, cudaStream_t st);
 cudaError_t launch_fill_bf16(uint64_t seed, uint64_t tensor, float scale, int kind, uint16_t* out,
                              int64_t n, int64_t start, cudaStream_t st);
 cudaError_t launch_fill_expert(uint64_t seed, int cl, int ce, int d, int f, float a_up,

@@ -552,29 +552,6 @@ cudaError_t launch_quantize(const uint16_t* w, int rows, int cols, uint32_t* q, 
   return cudaGetLastError();
 }
 
-// Peer-tier expert copy: 16-byte vectors, 4 in flight per thread, grid-stride over the expert.  On
-// the low-priority decode stream its CTAs fill SMs the compute stream leaves idle; the
-// copy-engine D2D path held the G = 1 tier's stall at ~0.20 of the decode time.
-__global__ void __launch_bounds__(512) k_copy_expert(uint4* __restrict__ dst, const uint4* __restrict__ src, int64_t n) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  for (; i + 3 * stride < n; i += 4 * stride) {
-    const uint4 a = __ldcs(src + i), b = __ldcs(src + i + stride), c = __ldcs(src + i + 2 * stride),
-                d = __ldcs(src + i + 3 * stride);
-    __stcs(dst + i, a);
-    __stcs(dst + i + stride, b);
-    __stcs(dst + i + 2 * stride, c);
-    __stcs(dst + i + 3 * stride, d);
-  }
-  for (; i < n; i += stride) __stcs(dst + i, __ldcs(src + i));
-}
-cudaError_t launch_copy_expert(unsigned char* dst, const unsigned char* src, int64_t bytes, cudaStream_t st) {
-  if (bytes % 16 || ((uintptr_t)dst | (uintptr_t)src) % 16) return cudaErrorInvalidValue;
-  k_copy_expert<<<148 * 2, 512, 0, st>>>(reinterpret_cast<uint4*>(dst), reinterpret_cast<const uint4*>(src),
-                                         bytes / 16);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_embed(const uint16_t* embed, const uint16_t* pos, const int32_t* tokens,
                          const int32_t* positions, int T, int d, float* h, cudaStream_t st) {
   k_embed<<<T, 256, 0, st>>>(embed, pos, tokens, positions, d, h);

@@ -1055,7 +1055,7 @@ static int issue_copies(mspq_engine* E, int cycle, CopyBatch& batch, uint64_t& b
       cudaStream_t hst = E->codec ? sdec : sx;
       if (reused) CUDA_OK(cudaStreamWaitEvent(hst, E->ev_gemm[E->last_layer[buf]], 0));
       if (E->ready_rec[buf]) CUDA_OK(cudaStreamWaitEvent(hst, E->ev_ready[buf], 0));
-      CAPI_OK(mspq_copy_expert(slot, hs, (long long)E->S16, hst));
+      CUDA_OK(cudaMemcpyAsync(slot, hs, E->S16, cudaMemcpyDeviceToDevice, hst));
       CUDA_OK(cudaEventRecord(E->ev_ready[buf], hst));
       const int owner = (key % E->m.E) % E->peer_G;
       if (owner == E->peer_rank) {
